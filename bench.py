@@ -1,0 +1,338 @@
+"""Stage-I stabilization throughput on B200 (BASELINE.json metric:
+"stabilized frames/s at 1080p (1/2/4/8 B200); kernel % of HBM roofline").
+
+One step = stabilizing the whole configs[2] sequence (1920x1080 RGB as
+BT.601 Y/Cb/Cr 4:4:4, 1000 frames, similarity, 1000 corners, RANSAC 500 @ 3
+px, smoothing radius 30).  `value` is device-resident throughput (inputs in
+HBM before the timed region; 6.2 GB of input per step, far larger than L2);
+`e2e` is the same step through the C-ABI host-buffer entry point
+(stabgpu_stabilize_sequence) with pinned-host input and output copied inside
+the timed region.  N > 1 (torchrun): contiguous re-detect-aligned frame
+shards per rank, one all-gather of ~100 B/frame motion records, every rank
+composes its own frames.
+
+--impl reference times the reference's own CPU implementation (the
+unmodified reference sources compiled into oracle/_ref, driven segment-
+parallel on all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "stabilized frames/s at 1080p (1/2/4/8 B200); kernel % of HBM roofline"
+UNIT = "frames/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def render(cfg, first, count, pinned=False, threads=0):
+    import torch
+
+    from paper_1701_03572_b200.synth import Video
+
+    spec = cfg.video
+    v = Video(spec, threads=threads)
+    planes = 3 if spec.color else 1
+    shape = (count, spec.height, spec.width)
+    bufs = [torch.empty(shape, dtype=torch.uint8, pin_memory=pinned) for _ in range(planes)]
+    step = 50
+    for f0 in range(0, count, step):
+        n = min(step, count - f0)
+        v.render(first + f0, n, out=[b[f0:f0 + n] for b in bufs])
+    return bufs
+
+
+# --------------------------------------------------------------- reference ---
+def cpu_reference(cfg, frames_y, frames_cb, frames_cr, threads):
+    """The reference CPU path on `threads` host threads over the given frames;
+    returns frames/s."""
+    import ctypes as C
+
+    sys.path.insert(0, ROOT)
+    from tests import _oracle
+
+    ref = _oracle.reference()
+    y = np.ascontiguousarray(frames_y)
+    cb = None if frames_cb is None else np.ascontiguousarray(frames_cb)
+    cr = None if frames_cr is None else np.ascontiguousarray(frames_cr)
+    t0 = time.perf_counter()
+    ref.stabilize_sequence(y, cfg.stab, cb, cr, compose=True, threads=threads)
+    dt = time.perf_counter() - t0
+    del C
+    return len(y) / dt, dt
+
+
+def run_reference_arm(args, cfg):
+    import torch.distributed as dist  # noqa: F401
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n_total = cfg.video.frames
+    sample = int(min(n_total, max(2 * threads * cfg.stab.flow.redetect_interval, 60)))
+    sample = min(sample, 400)
+    planes = render(cfg, 0, sample, pinned=False)
+    arrs = [p.numpy() for p in planes] + [None] * (3 - len(planes))
+    for _ in range(args.warmup):
+        cpu_reference(cfg, arrs[0][: min(sample, 2 * cfg.stab.flow.redetect_interval + 1)], *[
+            None if a is None else a[: min(sample, 2 * cfg.stab.flow.redetect_interval + 1)]
+            for a in arrs[1:]], threads)
+    times = []
+    for _ in range(args.steps):
+        fps, dt = cpu_reference(cfg, arrs[0], arrs[1], arrs[2], threads)
+        times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    value = sample / (ms / 1000.0)
+    desc = f"first {sample} of {n_total} frames of {args.config}, reference stage functions on {threads} threads"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
+            "config": workload(args, cfg), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload(args, cfg):
+    v = cfg.video
+    s = cfg.stab
+    return {"workload": f"BASELINE {args.config}: {cfg.name}", "width": v.width, "height": v.height,
+            "frames": v.frames, "planes": 3 if v.color else 1, "max_corners": s.detect.max_corners,
+            "min_distance": s.detect.min_distance, "levels": s.flow.max_levels,
+            "lk_window": 2 * s.flow.window_radius + 1, "ransac_iters": s.ransac.iterations,
+            "smooth_radius": s.smooth_radius, "model": "similarity" if s.selector.mode == 2 else
+            ("rigid" if s.selector.mode == 1 else "hybrid"),
+            "parallelism": f"frame-shards x{args.gpus}" if args.gpus > 1 else "1 GPU",
+            "l2": "inputs per step (6.2 GB at 1080p RGB) >> 126 MB L2; no flush needed",
+            "seed": hex(v.seed)}
+
+
+# --------------------------------------------------------------------- ours ---
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_03572_b200 import _lib, pipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = cfg.video.frames
+    spec = cfg.video
+    planes = 3 if spec.color else 1
+    shards = pipeline.shard_ranges(n, cfg.stab.flow.redetect_interval, world)
+    sh = shards[rank]
+    lo, hi = sh.frames_needed if world > 1 else (0, n)
+    count = hi - lo
+    t0 = time.time()
+    host = render(cfg, lo, count, pinned=True)
+    gen_s = time.time() - t0
+    dev = [h.cuda() for h in host]
+    outs = [torch.empty_like(d) for d in dev]
+    host_out = [torch.empty_like(h, pin_memory=True) for h in host]
+    ctx = _lib.context(local)
+    ctx.enable_timing(True)
+    stream = torch.cuda.current_stream(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    def step_device():
+        if world == 1:
+            pipeline.stabilize_sequence_device(dev[0], cfg.stab, *(dev[1:] if planes == 3 else (None, None)),
+                                               out_y=outs[0], out_cb=outs[1] if planes == 3 else None,
+                                               out_cr=outs[2] if planes == 3 else None, records=False)
+        else:
+            pipeline.stabilize_sharded(n, dev[0], lo, cfg.stab, rank, world,
+                                       *(dev[1:] if planes == 3 else (None, None)), device=local)
+
+    cfg_c = cfg.stab.c()
+    rec = np.zeros(n, pipeline.RECORD_DT)
+
+    def step_e2e():
+        if world == 1:
+            pipeline.stabilize_sequence_host_buffers(
+                ctx, host[0], host[1] if planes == 3 else None, host[2] if planes == 3 else None,
+                n, spec.width, spec.height, spec.width if planes == 3 else 0,
+                spec.height if planes == 3 else 0, cfg_c, host_out[0],
+                host_out[1] if planes == 3 else None, host_out[2] if planes == 3 else None, rec)
+        else:
+            d = [h.cuda(non_blocking=True) for h in host]
+            oy, ob, orr, _ = pipeline.stabilize_sharded(n, d[0], lo, cfg.stab, rank, world,
+                                                        *(d[1:] if planes == 3 else (None, None)),
+                                                        device=local)
+            a, b = sh.own_begin - lo, sh.own_end - lo
+            if oy is not None:
+                host_out[0][a:b].copy_(oy, non_blocking=True)
+                if planes == 3:
+                    host_out[1][a:b].copy_(ob, non_blocking=True)
+                    host_out[2][a:b].copy_(orr, non_blocking=True)
+            torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        launches0 = ctx.stats().launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        comp = []
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+            s = ctx.stats()
+            comp.append((s.ms_pyramid, s.ms_detect, s.ms_track, s.ms_fit, s.ms_plan, s.ms_compose))
+        ev1.record(stream)
+        barrier()
+        ms = ev0.elapsed_time(ev1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        launches = (ctx.stats().launches - launches0) // max(steps, 1)
+        return ms, launches, comp
+
+    with ClockSampler(local) as clk:
+        ms_dev, launches, comp = timed(step_device, args.steps, args.warmup)
+    ms_e2e, _, _ = timed(step_e2e, max(1, min(args.steps, 3)), 1)
+    value = n / (ms_dev / 1000.0)
+    e2e = n / (ms_e2e / 1000.0)
+    fb = spec.width * spec.height * planes
+
+    line = None
+    if rank == 0:
+        hbm, peak_src = peaks()
+        c = np.array(comp).mean(axis=0) if comp and world == 1 else np.zeros(6)
+        # dominant HBM-bound kernel family: K8 compose (luma warp+crop and chroma),
+        # algorithmic bytes = one read + one write of every plane of every frame
+        alg = 2.0 * fb * (sh.own_end - sh.own_begin if world > 1 else n)
+        comp_ms = float(c[5]) if c[5] > 0 else None
+        achieved = alg / (comp_ms / 1000.0) / 1e9 if comp_ms else None
+        stages = dict(zip(["pyramid", "detect", "track", "fit", "plan", "compose"],
+                          [round(float(x), 3) for x in c]))
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE generator, host C)",
+                "config": workload(args, cfg),
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": fb * n,
+                        "d2h_bytes_per_step": fb * n + n * pipeline.RECORD_BYTES,
+                        "ms_per_step": ms_e2e},
+                "roofline": {"bound": "hbm", "kernel": "K8 compose (luma_kernel + chroma_kernel)",
+                             "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                             "peak_source": peak_src,
+                             "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms},
+                "stage_ms": stages,
+                "gpu_launches": int(launches),
+                "clocks": clk.summary(),
+                "input_gen_s": round(gen_s, 1)}
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            sample = min(n, max(6 * threads, 40))
+            hs = [h[:sample].numpy() for h in host] + [None] * (3 - planes)
+            fps, dt = cpu_reference(cfg, hs[0], hs[1], hs[2], threads)
+            line["cpu_baseline"] = {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": f"first {sample} frames of {args.config} "
+                                              f"({dt:.1f} s, reference stage functions, segment-parallel)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_1701_03572_b200.synth import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.config == "c5":
+        raise SystemExit("c5 (multi-stream) is a parity config; bench runs c1-c4")
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

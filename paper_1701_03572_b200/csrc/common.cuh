@@ -1,0 +1,70 @@
+// common.cuh — shared device helpers for the sm_100a stabilization kernels.
+//
+// Floating-point rule for every kernel: where the reference C++
+// (/root/reference/proj/src) evaluates an expression, the device code uses
+// the explicitly rounded intrinsics (__dadd_rn, __dmul_rn, ...) in the SAME
+// order, so ptxas can never fuse a multiply-add the x86-64 reference did not
+// fuse.  Only reductions whose order differs by construction (warp/block
+// trees) are allowed to differ, and the tests bound that difference.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stabgpu.h"
+
+namespace stabgpu {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// clamp_u8(std::lround(v)), image_ops.cpp:19-21 — lround rounds half away
+// from zero, which __double2int_rn (half to even) does not.
+__device__ __forceinline__ uint8_t round_u8(double v) {
+    const long long r = llround(v);
+    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+}
+
+// sample_bilinear, image_ops.cpp:98-113 (0 outside [0,w-1]x[0,h-1]).
+__device__ __forceinline__ double sample_bilinear(const uint8_t* __restrict__ f, int w, int h,
+                                                  double px, double py) {
+    const double xmax = (double)w - 1.0, ymax = (double)h - 1.0;
+    if (!(px >= 0.0 && py >= 0.0 && px <= xmax && py <= ymax)) return 0.0;
+    const int x0 = (int)px, y0 = (int)py;
+    const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+    const double fx = dsub(px, (double)x0), fy = dsub(py, (double)y0);
+    const double a = f[(size_t)y0 * w + x0], b = f[(size_t)y0 * w + x1];
+    const double c = f[(size_t)y1 * w + x0], d = f[(size_t)y1 * w + x1];
+    const double top = dadd(a, dmul(fx, dsub(b, a)));
+    const double bot = dadd(c, dmul(fx, dsub(d, c)));
+    return dadd(top, dmul(fy, dsub(bot, top)));
+}
+
+// Positive doubles order like their bit patterns.
+__device__ __forceinline__ unsigned long long dbits(double v) {
+    return (unsigned long long)__double_as_longlong(v);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Butterfly sum of doubles: IEEE addition is commutative, so every lane ends
+// with the same bits and control flow that depends on the sum stays uniform.
+__device__ __forceinline__ double warp_dsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+}  // namespace stabgpu
+
+#define STABGPU_HOST_DEVICE __host__ __device__

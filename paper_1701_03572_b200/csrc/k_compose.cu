@@ -1,0 +1,224 @@
+// k_compose.cu — K8: fused inverse-similarity warp + crop/resize, batched
+// over frames, plus the single-pass chroma path.
+//
+// Reference: sample_bilinear (image_ops.cpp:98-113), warp_similarity
+// (115-134), crop_resize (136-159), compose_plane (165-202),
+// compose_stabilized (206-219).
+//
+// Luma keeps the reference's two roundings: every output pixel is a bilinear
+// sample of the WARPED-AND-ROUNDED frame, so each CTA first re-creates the
+// warped uint8 pixels its 64x16 output tile reads (a <=66x18 tile in shared
+// memory, 4 source taps each) and then resamples them.  The warped frame
+// never touches HBM: one read of the source, one write of the output.
+// Warped coordinates use the reference's row start exactly and advance by
+// x*c instead of x sequential additions of c (image_ops.cpp:124-131); the two
+// differ by a few ulps, which can move a value across a .5 rounding tie, so
+// luma parity is +-1 (tests count such pixels).  crop_resize and the chroma
+// path evaluate per pixel in the reference itself and are bit-exact.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace stabgpu {
+
+namespace {
+
+constexpr int OTW = 64, OTH = 16;  // output tile
+constexpr int WTW = OTW + 8, WTH = OTH + 4;
+
+struct CropGeom {
+    int mx, my;
+    double step_x, step_y;
+};
+
+__host__ __device__ inline CropGeom crop_geom(int w, int h, double crop) {
+    CropGeom g;
+    g.mx = (int)llround(crop * w);
+    g.my = (int)llround(crop * h);
+    const int cw = w - 2 * g.mx, ch = h - 2 * g.my;
+    g.step_x = w > 1 ? (double)(cw - 1) / (w - 1) : 0.0;
+    g.step_y = h > 1 ? (double)(ch - 1) / (h - 1) : 0.0;
+    return g;
+}
+
+// warp_similarity value of output pixel (u, v) (image_ops.cpp:123-131)
+__device__ __forceinline__ uint8_t warped(const uint8_t* __restrict__ src, int w, int h,
+                                          const FramePlan& p, int u, int v) {
+    const double rx = dadd(dmul(p.c, dsub(0.0, p.tx)), dmul(p.sn, dsub((double)v, p.ty)));
+    const double ry = dadd(dmul(-p.sn, dsub(0.0, p.tx)), dmul(p.c, dsub((double)v, p.ty)));
+    const double sx = dadd(rx, dmul((double)u, p.c));
+    const double sy = dsub(ry, dmul((double)u, p.sn));
+    return round_u8(sample_bilinear(src, w, h, sx, sy));
+}
+
+__global__ void __launch_bounds__(256) luma_kernel(PlaneBatch in, const FramePlan* __restrict__ plan,
+                                                   CropGeom g, uint8_t* __restrict__ out) {
+    __shared__ uint8_t wt[WTH][WTW];
+    const int w = in.w, h = in.h;
+    const int f = blockIdx.z;
+    const FramePlan p = plan[f];
+    const uint8_t* src = in.base + (size_t)f * in.stride;
+    uint8_t* dst = out + (size_t)f * in.stride;
+    const int X0 = blockIdx.x * OTW, Y0 = blockIdx.y * OTH;
+    const int tx = (threadIdx.x & 15) * 4, ty = threadIdx.x >> 4;
+    const bool identity = g.mx == 0 && g.my == 0;
+    const int y = Y0 + ty;
+    uint8_t o[4] = {0, 0, 0, 0};
+    if (identity) {  // crop_resize returns the warped frame (image_ops.cpp:143-145)
+        if (y < h)
+            for (int k = 0; k < 4; ++k)
+                if (X0 + tx + k < w) o[k] = warped(src, w, h, p, X0 + tx + k, y);
+    } else {
+        // warped pixels the tile samples: columns [u0, u1], rows [v0, v1]
+        const int xl = min(X0 + OTW - 1, w - 1), yl = min(Y0 + OTH - 1, h - 1);
+        const int u0 = (int)dadd((double)g.mx, dmul((double)X0, g.step_x));
+        const int v0 = (int)dadd((double)g.my, dmul((double)Y0, g.step_y));
+        const int u1 = min((int)dadd((double)g.mx, dmul((double)xl, g.step_x)) + 1, w - 1);
+        const int v1 = min((int)dadd((double)g.my, dmul((double)yl, g.step_y)) + 1, h - 1);
+        const int nu = u1 - u0 + 1, nv = v1 - v0 + 1;
+        for (int i = threadIdx.x; i < nu * nv; i += blockDim.x) {
+            const int r = i / nu, c = i - r * nu;
+            wt[r][c] = warped(src, w, h, p, u0 + c, v0 + r);
+        }
+        __syncthreads();
+        if (y < h) {
+            const double sy = dadd((double)g.my, dmul((double)y, g.step_y));
+            const int y0 = (int)sy, y1 = min(y0 + 1, h - 1);
+            const double fy = dsub(sy, (double)y0);
+            for (int k = 0; k < 4; ++k) {
+                const int x = X0 + tx + k;
+                if (x >= w) break;
+                // sample_bilinear on the warped tile (image_ops.cpp:98-113)
+                const double sx = dadd((double)g.mx, dmul((double)x, g.step_x));
+                if (!(sx >= 0.0 && sy >= 0.0 && sx <= (double)w - 1.0 && sy <= (double)h - 1.0)) {
+                    o[k] = 0;
+                    continue;
+                }
+                const int x0 = (int)sx, x1 = min(x0 + 1, w - 1);
+                const double fx = dsub(sx, (double)x0);
+                const double a = wt[y0 - v0][x0 - u0], b = wt[y0 - v0][x1 - u0];
+                const double c = wt[y1 - v0][x0 - u0], d = wt[y1 - v0][x1 - u0];
+                const double top = dadd(a, dmul(fx, dsub(b, a)));
+                const double bot = dadd(c, dmul(fx, dsub(d, c)));
+                o[k] = round_u8(dadd(top, dmul(fy, dsub(bot, top))));
+            }
+        }
+    }
+    if (y >= h) return;
+    const int x = X0 + tx;
+    uint8_t* row = dst + (size_t)y * w;
+    if (x + 3 < w && (w & 3) == 0) {
+        __stcs(reinterpret_cast<unsigned*>(row + x),
+               (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
+    } else {
+        for (int k = 0; k < 4; ++k)
+            if (x + k < w) row[x + k] = o[k];
+    }
+}
+
+// compose_plane (image_ops.cpp:165-202): crop in luma space, inverse warp,
+// sample the chroma plane, fill 128.  Both planes in one launch (grid.y).
+__global__ void __launch_bounds__(256) chroma_kernel(PlaneBatch cb, PlaneBatch cr,
+                                                     const FramePlan* __restrict__ plan, int lw,
+                                                     int lh, CropGeom g, uint8_t* __restrict__ ocb,
+                                                     uint8_t* __restrict__ ocr) {
+    const int cw = cb.w, ch = cb.h;
+    const int f = blockIdx.z;
+    const PlaneBatch& pb = blockIdx.y & 1 ? cr : cb;
+    uint8_t* out = (blockIdx.y & 1 ? ocr : ocb) + (size_t)f * pb.stride;
+    const uint8_t* src = pb.base + (size_t)f * pb.stride;
+    const FramePlan p = plan[f];
+    const double fx = (double)lw / cw, fy = (double)lh / ch;
+    const long long npx = (long long)cw * ch;
+    const long long stride = (long long)gridDim.x * blockDim.x * 4;
+    for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < npx; i0 += stride) {
+        uint8_t o[4];
+        for (int k = 0; k < 4; ++k) {
+            const long long i = i0 + k;
+            if (i >= npx) break;
+            const int y = (int)(i / cw), x = (int)(i - (long long)y * cw);
+            double lx = dsub(dmul(dadd((double)x, 0.5), fx), 0.5);
+            double ly = dsub(dmul(dadd((double)y, 0.5), fy), 0.5);
+            if (g.mx != 0 || g.my != 0) {
+                lx = dadd((double)g.mx, dmul(lx, g.step_x));
+                ly = dadd((double)g.my, dmul(ly, g.step_y));
+            }
+            const double dx = dsub(lx, p.tx), dy = dsub(ly, p.ty);
+            const double qx = dadd(dmul(p.c, dx), dmul(p.sn, dy));
+            const double qy = dadd(dmul(-p.sn, dx), dmul(p.c, dy));
+            const double px = dsub(ddiv(dadd(qx, 0.5), fx), 0.5);
+            const double py = dsub(ddiv(dadd(qy, 0.5), fy), 0.5);
+            double v = 128.0;
+            if (px >= 0.0 && py >= 0.0 && px <= (double)cw - 1.0 && py <= (double)ch - 1.0)
+                v = sample_bilinear(src, cw, ch, px, py);
+            o[k] = round_u8(v);
+        }
+        if (i0 + 3 < npx && (npx & 3) == 0) {
+            __stcs(reinterpret_cast<unsigned*>(out + i0),
+                   (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
+        } else {
+            for (int k = 0; k < 4 && i0 + k < npx; ++k) out[i0 + k] = o[k];
+        }
+    }
+}
+
+__global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropGeom g,
+                            uint8_t* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w) return;
+    if (g.mx == 0 && g.my == 0) {
+        out[(size_t)y * w + x] = src[(size_t)y * w + x];
+        return;
+    }
+    const double sy = dadd((double)g.my, dmul((double)y, g.step_y));
+    const double sx = dadd((double)g.mx, dmul((double)x, g.step_x));
+    out[(size_t)y * w + x] = round_u8(sample_bilinear(src, w, h, sx, sy));
+}
+
+__global__ void warp_kernel(const uint8_t* __restrict__ src, int w, int h,
+                            const FramePlan* __restrict__ plan, uint8_t* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w) return;
+    out[(size_t)y * w + x] = warped(src, w, h, *plan, x, y);
+}
+
+}  // namespace
+
+void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                    double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
+                    cudaStream_t st) {
+    if (frames <= 0) return;
+    const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
+    for (int f0 = 0; f0 < frames; f0 += 65535) {
+        const int nf = min(65535, frames - f0);
+        PlaneBatch yb = y;
+        yb.base += (size_t)f0 * y.stride;
+        dim3 grid((y.w + OTW - 1) / OTW, (y.h + OTH - 1) / OTH, nf);
+        luma_kernel<<<grid, 256, 0, st>>>(yb, plan + f0, g, out_y + (size_t)f0 * y.stride);
+        if (cb.base && cr.base && out_cb && out_cr) {
+            PlaneBatch b1 = cb, b2 = cr;
+            b1.base += (size_t)f0 * cb.stride;
+            b2.base += (size_t)f0 * cr.stride;
+            const long long npx = (long long)cb.w * cb.h;
+            const long long nb = (npx / 4 + 255) / 256;
+            const int bx = (int)(nb < 1024 ? nb : 1024);
+            dim3 g2(max(bx, 1), 2, nf);
+            chroma_kernel<<<g2, 256, 0, st>>>(b1, b2, plan + f0, y.w, y.h, g,
+                                              out_cb + (size_t)f0 * cb.stride,
+                                              out_cr + (size_t)f0 * cr.stride);
+        }
+    }
+}
+
+void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
+                      cudaStream_t st) {
+    dim3 grid((w + 127) / 128, h);
+    warp_kernel<<<grid, 128, 0, st>>>(src, w, h, plan, out);
+}
+
+void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,
+                      cudaStream_t st) {
+    dim3 grid((w + 127) / 128, h);
+    crop_kernel<<<grid, 128, 0, st>>>(src, w, h, crop_geom(w, h, crop_ratio), out);
+}
+
+}  // namespace stabgpu

@@ -1,0 +1,629 @@
+// k_detect.cu — K2/K3/K4: Shi-Tomasi corners, batched over detection frames.
+//
+// Reference: gradients (image_ops.cpp:79-96), min_eig + response_in_rect
+// (features.cpp:41-74) and detect_corners (features.cpp:89-141).
+//
+// Exactness argument.  A central difference of uint8 pixels is
+// k/2 with |k| <= 255, so every product dx*dx, dx*dy, dy*dy in the reference
+// is an exact multiple of 1/4 and the block sums are exact in any order.  The
+// kernels therefore sum integer products and scale by 0.25 (exact), then
+// evaluate min_eig with correctly rounded fp64 ops in the reference order:
+// the response bits are identical to the reference, so the candidate set,
+// the sort order and the greedy selection are identical too.
+//
+// K2 (resp_max_kernel): response over the ROI, block max, atomicMax of the
+//     bit pattern (responses are >= 0, so bit order == value order).
+// K3 (cand_kernel): recomputes the response (cheaper than writing an 8 B/px
+//     map), keeps r >= quality*max && r > 0, warp-ballot compaction.
+// K4 (select_kernel): one 1024-thread CTA per detection frame.  Candidates
+//     are bucketed by a monotone 13-bit-truncated float key (histogram +
+//     scatter in shared memory), then consumed in score order in chunks of
+//     <= 4096: each chunk is first tested against the accepted-corner grid
+//     (cell >= min_distance, so only the 3x3 neighbourhood can conflict),
+//     the survivors are bitonic-sorted by (score desc, y*w+x asc) — the
+//     reference comparator, features.cpp:119-123 — and one warp runs the
+//     greedy scan 32 candidates at a time with ballots, which reproduces the
+//     sequential rank-order rule exactly, including the early stop at
+//     max_corners.  A bucket holding more than 4096 candidates (large ties)
+//     is merge-sorted in global memory first.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace stabgpu {
+
+namespace {
+
+constexpr int RTW = 32, RTH = 16;  // response tile
+
+__device__ __forceinline__ double min_eig_q(int sxx4, int sxy4, int syy4) {
+    // features.cpp:41-45 on the exact quarter-integer sums
+    const double sxx = (double)sxx4 * 0.25, sxy = (double)sxy4 * 0.25, syy = (double)syy4 * 0.25;
+    const double half_trace = dmul(0.5, dadd(sxx, syy));
+    const double half_diff = dmul(0.5, dsub(sxx, syy));
+    return dsub(half_trace, dsqrt(dadd(dmul(half_diff, half_diff), dmul(sxy, sxy))));
+}
+
+// Shared tile computation: integer structure-tensor sums for a RTW x RTH tile
+// at (X0, Y0).  Products outside the frame are zero, which is exactly the
+// reference's truncated window (features.cpp:55-60).
+template <int H>
+struct RespTile {
+    static constexpr int PW = RTW + 2 * H, PH = RTH + 2 * H;
+    static constexpr int IW = PW + 2, IH = PH + 2;
+    uint8_t img[IH][IW];
+    int pxx[PH][PW], pxy[PH][PW], pyy[PH][PW];
+
+    __device__ void load(const uint8_t* __restrict__ f, int w, int h, int X0, int Y0) {
+        for (int i = threadIdx.x; i < IH * IW; i += blockDim.x) {
+            const int r = i / IW, c = i % IW;
+            const int y = clampi(Y0 - H - 1 + r, 0, h - 1), x = clampi(X0 - H - 1 + c, 0, w - 1);
+            img[r][c] = __ldg(f + (size_t)y * w + x);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < PH * PW; i += blockDim.x) {
+            const int r = i / PW, c = i % PW;
+            const int x = X0 - H + c, y = Y0 - H + r;
+            int gx = 0, gy = 0;
+            if (x >= 0 && x < w && y >= 0 && y < h) {
+                gx = (int)img[r + 1][c + 2] - (int)img[r + 1][c];
+                gy = (int)img[r + 2][c + 1] - (int)img[r][c + 1];
+            }
+            pxx[r][c] = gx * gx;
+            pxy[r][c] = gx * gy;
+            pyy[r][c] = gy * gy;
+        }
+        __syncthreads();
+    }
+
+    __device__ double response(int tx, int ty) const {
+        int sxx = 0, sxy = 0, syy = 0;
+#pragma unroll
+        for (int dy = 0; dy <= 2 * H; ++dy)
+#pragma unroll
+            for (int dx = 0; dx <= 2 * H; ++dx) {
+                sxx += pxx[ty + dy][tx + dx];
+                sxy += pxy[ty + dy][tx + dx];
+                syy += pyy[ty + dy][tx + dx];
+            }
+        return min_eig_q(sxx, sxy, syy);
+    }
+};
+
+template <int H>
+__global__ void __launch_bounds__(256) resp_max_kernel(PlaneBatch fr, stabgpu_roi roi,
+                                                       unsigned long long* __restrict__ maxbits) {
+    __shared__ RespTile<H> t;
+    __shared__ unsigned long long wmax[8];
+    const uint8_t* f = fr.base + (size_t)blockIdx.z * fr.stride;
+    const int X0 = roi.x0 + blockIdx.x * RTW, Y0 = roi.y0 + blockIdx.y * RTH;
+    t.load(f, fr.w, fr.h, X0, Y0);
+    unsigned long long m = 0;
+    for (int i = threadIdx.x; i < RTW * RTH; i += blockDim.x) {
+        const int tx = i % RTW, ty = i / RTW;
+        if (X0 + tx < roi.x1 && Y0 + ty < roi.y1) {
+            const double r = t.response(tx, ty);
+            if (r > 0.0) m = max(m, dbits(r));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; ++i) m = max(m, wmax[i]);
+        if (m) atomicMax(&maxbits[blockIdx.z], m);
+    }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) cand_kernel(PlaneBatch fr, stabgpu_roi roi, double quality,
+                                                   const unsigned long long* __restrict__ maxbits,
+                                                   unsigned int* __restrict__ count,
+                                                   unsigned long long* __restrict__ cand_key,
+                                                   unsigned int* __restrict__ cand_idx, size_t cap) {
+    const unsigned long long mb = maxbits[blockIdx.z];
+    if (mb == 0) return;  // max_response <= 0: no corners (features.cpp:103-105)
+    __shared__ RespTile<H> t;
+    const uint8_t* f = fr.base + (size_t)blockIdx.z * fr.stride;
+    const int X0 = roi.x0 + blockIdx.x * RTW, Y0 = roi.y0 + blockIdx.y * RTH;
+    t.load(f, fr.w, fr.h, X0, Y0);
+    const double thr = dmul(quality, __longlong_as_double((long long)mb));
+    const int lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < RTW * RTH; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const int tx = i % RTW, ty = i / RTW;
+        double r = 0.0;
+        bool keep = false;
+        if (X0 + tx < roi.x1 && Y0 + ty < roi.y1) {
+            r = t.response(tx, ty);
+            keep = r >= thr && r > 0.0;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, keep);
+        if (!ball) continue;
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&count[blockIdx.z], (unsigned)__popc(ball));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+            const size_t pos = (size_t)blockIdx.z * cap + base + __popc(ball & ((1u << lane) - 1));
+            cand_key[pos] = dbits(r);
+            cand_idx[pos] = (unsigned)((Y0 + ty) * fr.w + X0 + tx);
+        }
+    }
+}
+
+// Generic block size (any odd >= 3): direct evaluation from global memory.
+__global__ void resp_generic_kernel(PlaneBatch fr, stabgpu_roi roi, int half, int mode,
+                                    double quality, unsigned long long* __restrict__ maxbits,
+                                    unsigned int* __restrict__ count,
+                                    unsigned long long* __restrict__ cand_key,
+                                    unsigned int* __restrict__ cand_idx, size_t cap,
+                                    double* __restrict__ resp_out) {
+    const uint8_t* f = fr.base + (size_t)blockIdx.z * fr.stride;
+    const int w = fr.w, h = fr.h;
+    const int x = roi.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = roi.y0 + blockIdx.y;
+    bool valid = x < roi.x1 && y < roi.y1;
+    double r = 0.0;
+    if (valid) {
+        long long sxx = 0, sxy = 0, syy = 0;
+        for (int wy = max(y - half, 0); wy <= min(y + half, h - 1); ++wy)
+            for (int wx = max(x - half, 0); wx <= min(x + half, w - 1); ++wx) {
+                const int gx = (int)f[(size_t)wy * w + min(wx + 1, w - 1)] - (int)f[(size_t)wy * w + max(wx - 1, 0)];
+                const int gy = (int)f[(size_t)min(wy + 1, h - 1) * w + wx] - (int)f[(size_t)max(wy - 1, 0) * w + wx];
+                sxx += gx * gx;
+                sxy += gx * gy;
+                syy += gy * gy;
+            }
+        const double dxx = (double)sxx * 0.25, dxy = (double)sxy * 0.25, dyy = (double)syy * 0.25;
+        const double ht = dmul(0.5, dadd(dxx, dyy)), hd = dmul(0.5, dsub(dxx, dyy));
+        r = dsub(ht, dsqrt(dadd(dmul(hd, hd), dmul(dxy, dxy))));
+    }
+    if (mode == 0) {  // max
+        if (valid && r > 0.0) atomicMax(&maxbits[blockIdx.z], dbits(r));
+    } else if (mode == 1) {  // candidates
+        const unsigned long long mb = maxbits[blockIdx.z];
+        if (mb == 0 || !valid) return;
+        const double thr = dmul(quality, __longlong_as_double((long long)mb));
+        if (r >= thr && r > 0.0) {
+            const unsigned pos = atomicAdd(&count[blockIdx.z], 1u);
+            cand_key[(size_t)blockIdx.z * cap + pos] = dbits(r);
+            cand_idx[(size_t)blockIdx.z * cap + pos] = (unsigned)(y * w + x);
+        }
+    } else if (valid) {  // full response map (min_eig_response)
+        resp_out[(size_t)y * w + x] = r;
+    }
+}
+
+// ---------------------------------------------------------------- K4 ----
+
+constexpr int SEL_THREADS = 1024;
+constexpr int CAP = 4096;       // chunk capacity (candidates sorted per pass)
+constexpr int MAX_CELLS = 8192; // accepted-corner grid cells
+constexpr int SMEM_CORNERS = 8192;
+
+__device__ __forceinline__ unsigned bucket_of(unsigned long long key, unsigned maxf_bits) {
+    const float sf = __double2float_rn(__longlong_as_double((long long)key));
+    const unsigned d = maxf_bits - __float_as_uint(sf);
+    return min(d >> kBucketShift, (unsigned)(kBuckets - 1));
+}
+
+// (score desc, idx asc): a precedes b
+__device__ __forceinline__ bool before(unsigned long long ka, unsigned ia, unsigned long long kb,
+                                       unsigned ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
+
+// Block-wide exclusive scan of one value per thread (1024 threads).
+__device__ unsigned block_excl_scan(unsigned v, unsigned* warp_tot, unsigned* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned t = warp_tot[lane];
+        unsigned s = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_tot[lane] = s - t;
+        if (lane == 31) *total = s;
+    }
+    __syncthreads();
+    const unsigned r = warp_tot[wid] + x - v;
+    __syncthreads();
+    return r;
+}
+
+struct SelShared {
+    unsigned bstart[kBuckets + 1];
+    unsigned warp_tot[32];
+    unsigned total;
+    int naccepted;
+    int done;
+    int gw, gh, cell;
+    int b0, b1, big;
+};
+
+// bitonic sort of n (power of two) keys in shared memory, (score desc, idx asc)
+__device__ void bitonic_sort(unsigned long long* key, unsigned* idx, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const bool up = (i & k) == 0;  // ascending in "before" order
+                    const unsigned long long ka = key[i], kb = key[p];
+                    const unsigned ia = idx[i], ib = idx[p];
+                    const bool sw = up ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+                    if (sw) {
+                        key[i] = kb;
+                        key[p] = ka;
+                        idx[i] = ib;
+                        idx[p] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Does (x, y) lie closer than min_dist to an accepted corner?
+__device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy,
+                                          const int* anext, int gw, int gh, int cell, int rx0,
+                                          int ry0, double md2) {
+    const int cx = (x - rx0) / cell, cy = (y - ry0) / cell;
+    for (int gy = max(cy - 1, 0); gy <= min(cy + 1, gh - 1); ++gy)
+        for (int gx = max(cx - 1, 0); gx <= min(cx + 1, gw - 1); ++gx)
+            for (int a = heads[gy * gw + gx]; a >= 0; a = anext[a]) {
+                const short2 p = axy[a];
+                const long long dx = x - p.x, dy = y - p.y;
+                if ((double)(dx * dx + dy * dy) < md2) return true;
+            }
+    return false;
+}
+
+// In-place stable-free merge sort of [0, m) by (score desc, idx asc) in
+// global memory, ping-ponging with tmp (keys are unique, so rank-merging is
+// exact).  Used only for buckets larger than CAP.
+__device__ void global_merge_sort(unsigned long long* key, unsigned* idx, unsigned long long* tkey,
+                                  unsigned* tidx, unsigned m) {
+    unsigned long long *sk = key, *dk = tkey;
+    unsigned *si = idx, *di = tidx;
+    for (unsigned width = 1; width < m; width <<= 1) {
+        for (unsigned i = threadIdx.x; i < m; i += blockDim.x) {
+            const unsigned run = i / (2 * width) * (2 * width);
+            const unsigned a0 = run, a1 = min(run + width, m), b0 = a1, b1 = min(run + 2 * width, m);
+            const bool inA = i < a1;
+            const unsigned long long k = sk[i];
+            const unsigned id = si[i];
+            // rank of (k,id) in the other run
+            unsigned lo = inA ? b0 : a0, hi = inA ? b1 : a1;
+            while (lo < hi) {
+                const unsigned mid = (lo + hi) >> 1;
+                if (before(sk[mid], si[mid], k, id)) lo = mid + 1;
+                else hi = mid;
+            }
+            const unsigned pos = inA ? run + (i - a0) + (lo - b0) : run + (i - b0) + (lo - a0);
+            dk[pos] = k;
+            di[pos] = id;
+        }
+        __syncthreads();
+        unsigned long long* t1 = sk;
+        sk = dk;
+        dk = t1;
+        unsigned* t2 = si;
+        si = di;
+        di = t2;
+    }
+    if (sk != key) {
+        for (unsigned i = threadIdx.x; i < m; i += blockDim.x) {
+            key[i] = sk[i];
+            idx[i] = si[i];
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SEL_THREADS, 1)
+    select_kernel(stabgpu_detect_cfg cfg, stabgpu_roi roi, int w, DetectScratch s,
+                  double2* __restrict__ out_xy, double* __restrict__ out_score,
+                  int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SelShared& S = *reinterpret_cast<SelShared*>(smem);
+    unsigned char* p = smem + ((sizeof(SelShared) + 15) & ~size_t(15));
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(p);
+    p += sizeof(unsigned long long) * CAP;
+    unsigned* cidx = reinterpret_cast<unsigned*>(p);
+    p += sizeof(unsigned) * CAP;
+    unsigned* cursor = reinterpret_cast<unsigned*>(ckey);  // aliases the chunk during scatter
+    int* heads = reinterpret_cast<int*>(p);
+    p += sizeof(int) * MAX_CELLS;
+    const int maxc = cfg.max_corners;
+    const int d = blockIdx.x;
+    short2* axy;
+    int* anext;
+    if (maxc <= SMEM_CORNERS) {
+        axy = reinterpret_cast<short2*>(p);
+        p += sizeof(short2) * maxc;
+        anext = reinterpret_cast<int*>(p);
+    } else {
+        axy = g_axy + (size_t)d * maxc;
+        anext = g_anext + (size_t)d * maxc;
+    }
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned n = s.count[d];
+    const unsigned long long mb = s.maxbits[d];
+    if (n == 0 || mb == 0) {
+        if (tid == 0) out_n[d] = 0;
+        return;
+    }
+    const unsigned maxf = __float_as_uint(__double2float_rn(__longlong_as_double((long long)mb)));
+    const unsigned long long* ck = s.cand_key + (size_t)d * s.cap;
+    const unsigned* ci = s.cand_idx + (size_t)d * s.cap;
+    unsigned long long* sk = s.sort_key + (size_t)d * s.cap;
+    unsigned* si = s.sort_idx + (size_t)d * s.cap;
+
+    // ---- histogram + exclusive scan + scatter into bucket order
+    for (int b = tid; b < kBuckets; b += SEL_THREADS) cursor[b] = 0;
+    __syncthreads();
+    for (unsigned i = tid; i < n; i += SEL_THREADS) atomicAdd(&cursor[bucket_of(ck[i], maxf)], 1u);
+    __syncthreads();
+    {
+        constexpr int PER = kBuckets / SEL_THREADS;  // 8
+        unsigned v[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            v[k] = cursor[tid * PER + k];
+            sum += v[k];
+        }
+        unsigned off = block_excl_scan(sum, S.warp_tot, &S.total);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            S.bstart[tid * PER + k] = off;
+            cursor[tid * PER + k] = off;
+            off += v[k];
+        }
+        if (tid == 0) S.bstart[kBuckets] = n;
+    }
+    __syncthreads();
+    for (unsigned i = tid; i < n; i += SEL_THREADS) {
+        const unsigned long long k = ck[i];
+        const unsigned pos = atomicAdd(&cursor[bucket_of(k, maxf)], 1u);
+        sk[pos] = k;
+        si[pos] = ci[i];
+    }
+    // ---- accepted-corner grid: cell >= min_distance and <= MAX_CELLS cells
+    if (tid == 0) {
+        const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
+        int cell = max(1, (int)ceil(cfg.min_distance));
+        while ((long long)((rw + cell - 1) / cell) * ((rh + cell - 1) / cell) > MAX_CELLS) ++cell;
+        S.cell = cell;
+        S.gw = (rw + cell - 1) / cell;
+        S.gh = (rh + cell - 1) / cell;
+        S.naccepted = 0;
+        S.done = 0;
+        S.b0 = 0;
+    }
+    __syncthreads();
+    for (int c = tid; c < S.gw * S.gh; c += SEL_THREADS) heads[c] = -1;
+    __threadfence_block();
+    __syncthreads();
+    const double md2 = dmul(cfg.min_distance, cfg.min_distance);
+    const int gw = S.gw, gh = S.gh, cell = S.cell;
+
+    while (true) {
+        // ---- next chunk of whole buckets [b0, b1) with <= CAP candidates
+        if (tid == 0) {
+            int b0 = S.b0;
+            while (b0 < kBuckets && S.bstart[b0 + 1] == S.bstart[b0]) ++b0;
+            S.b0 = b0;
+            if (b0 >= kBuckets) {
+                S.done = 1;
+            } else {
+                const unsigned limit = S.bstart[b0] + CAP;
+                int lo = b0 + 1, hi = kBuckets;  // largest b1 with bstart[b1] <= limit
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (S.bstart[mid] <= limit) lo = mid;
+                    else hi = mid - 1;
+                }
+                S.big = S.bstart[b0 + 1] - S.bstart[b0] > (unsigned)CAP;
+                S.b1 = S.big ? b0 + 1 : lo;
+            }
+        }
+        __syncthreads();
+        if (S.done) break;
+        const unsigned lo = S.bstart[S.b0], hi = S.bstart[S.b1];
+        const bool big = S.big;
+        if (big) {  // rare: tie-heavy bucket -> sort it in global memory
+            global_merge_sort(sk + lo, si + lo, const_cast<unsigned long long*>(ck) + lo,
+                              const_cast<unsigned*>(ci) + lo, hi - lo);
+        }
+        for (unsigned c0 = lo; c0 < hi; c0 += CAP) {
+            const unsigned m = min((unsigned)CAP, hi - c0);
+            // load + grid prefilter + compaction (survivors keep relative order
+            // only within a sorted big bucket; otherwise they are sorted below)
+            constexpr int PER = CAP / SEL_THREADS;
+            unsigned long long kk[PER];
+            unsigned ii[PER];
+            unsigned alive = 0;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const unsigned j = tid * PER + q;
+                kk[q] = 0;
+                ii[q] = 0;
+                if (j < m) {
+                    kk[q] = sk[c0 + j];
+                    ii[q] = si[c0 + j];
+                    const int x = (int)(ii[q] % (unsigned)w), y = (int)(ii[q] / (unsigned)w);
+                    if (!conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2))
+                        alive |= 1u << q;
+                }
+            }
+            const unsigned off = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
+            const unsigned ns = S.total;
+            {
+                unsigned o = off;
+#pragma unroll
+                for (int q = 0; q < PER; ++q)
+                    if (alive & (1u << q)) {
+                        ckey[o] = kk[q];
+                        cidx[o] = ii[q];
+                        ++o;
+                    }
+            }
+            __syncthreads();
+            if (ns == 0) continue;
+            if (!big) {
+                int np = 1;
+                while (np < (int)ns) np <<= 1;
+                for (int j = ns + tid; j < np; j += SEL_THREADS) {
+                    ckey[j] = 0;
+                    cidx[j] = 0xffffffffu;
+                }
+                __syncthreads();
+                bitonic_sort(ckey, cidx, np);
+            }
+            // ---- exact greedy over the sorted survivors, 32 at a time
+            if (tid < 32) {
+                int nacc = S.naccepted;
+                for (unsigned w0 = 0; w0 < ns && nacc < maxc; w0 += 32) {
+                    const unsigned j = w0 + lane;
+                    int x = 0, y = 0;
+                    bool ok = false;
+                    if (j < ns) {
+                        x = (int)(cidx[j] % (unsigned)w);
+                        y = (int)(cidx[j] / (unsigned)w);
+                        ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
+                    }
+                    const unsigned live = __ballot_sync(0xffffffffu, ok);
+                    unsigned conf = 0;  // earlier live lanes closer than min_distance
+                    for (unsigned rem = live; rem; rem &= rem - 1) {
+                        const int src = __ffs(rem) - 1;
+                        const int sx = __shfl_sync(0xffffffffu, x, src);
+                        const int sy = __shfl_sync(0xffffffffu, y, src);
+                        if (src < lane) {
+                            const long long dx = x - sx, dy = y - sy;
+                            if ((double)(dx * dx + dy * dy) < md2) conf |= 1u << src;
+                        }
+                    }
+                    unsigned acc = 0;
+                    for (unsigned rem = live; rem; rem &= rem - 1) {
+                        const int k = __ffs(rem) - 1;
+                        const unsigned ck2 = __shfl_sync(0xffffffffu, conf, k);
+                        if (!(ck2 & acc)) acc |= 1u << k;
+                    }
+                    const int room = maxc - nacc;
+                    while (__popc(acc) > room) acc &= ~(1u << (31 - __clz(acc)));
+                    if (acc & (1u << lane)) {
+                        const int slot = nacc + __popc(acc & ((1u << lane) - 1));
+                        axy[slot] = make_short2((short)x, (short)y);
+                        const int cid = ((y - roi.y0) / cell) * gw + (x - roi.x0) / cell;
+                        anext[slot] = atomicExch(&heads[cid], slot);
+                        out_xy[(size_t)d * maxc + slot] = make_double2((double)x, (double)y);
+                        out_score[(size_t)d * maxc + slot] =
+                            __longlong_as_double((long long)ckey[j]);
+                    }
+                    nacc += __popc(acc);
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    S.naccepted = nacc;
+                    if (nacc >= maxc) S.done = 1;
+                }
+            }
+            __syncthreads();
+            if (S.done) break;
+        }
+        if (S.done) break;
+        if (tid == 0) S.b0 = S.b1;
+        __syncthreads();
+    }
+    if (tid == 0) out_n[d] = S.naccepted;
+}
+
+__global__ void gradients_kernel(const uint8_t* __restrict__ f, int w, int h, double* __restrict__ gx,
+                                 double* __restrict__ gy) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w) return;
+    const int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
+    const int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
+    gx[(size_t)y * w + x] = dmul(0.5, dsub((double)f[(size_t)y * w + xp], (double)f[(size_t)y * w + xm]));
+    gy[(size_t)y * w + x] = dmul(0.5, dsub((double)f[(size_t)yp * w + x], (double)f[(size_t)ym * w + x]));
+}
+
+}  // namespace
+
+size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int, int) {
+    size_t b = ((sizeof(SelShared) + 15) & ~size_t(15)) + (sizeof(unsigned long long) + sizeof(unsigned)) * CAP +
+               sizeof(int) * MAX_CELLS;
+    if (cfg.max_corners <= SMEM_CORNERS) b += (sizeof(short2) + sizeof(int)) * cfg.max_corners;
+    return b;
+}
+
+void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
+                   DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
+                   cudaStream_t st) {
+    if (nD <= 0) return;
+    cudaMemsetAsync(s.maxbits, 0, sizeof(unsigned long long) * nD, st);
+    cudaMemsetAsync(s.count, 0, sizeof(unsigned) * nD, st);
+    const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
+    const int half = cfg.block_size / 2;
+    if (half == 1) {
+        dim3 grid((rw + RTW - 1) / RTW, (rh + RTH - 1) / RTH, nD);
+        resp_max_kernel<1><<<grid, 256, 0, st>>>(fr, roi, s.maxbits);
+        cand_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s.maxbits, s.count,
+                                             s.cand_key, s.cand_idx, s.cap);
+    } else if (half == 2) {
+        dim3 grid((rw + RTW - 1) / RTW, (rh + RTH - 1) / RTH, nD);
+        resp_max_kernel<2><<<grid, 256, 0, st>>>(fr, roi, s.maxbits);
+        cand_kernel<2><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s.maxbits, s.count,
+                                             s.cand_key, s.cand_idx, s.cap);
+    } else {
+        dim3 grid((rw + 127) / 128, rh, nD);
+        resp_generic_kernel<<<grid, 128, 0, st>>>(fr, roi, half, 0, 0.0, s.maxbits, s.count,
+                                                  s.cand_key, s.cand_idx, s.cap, nullptr);
+        resp_generic_kernel<<<grid, 128, 0, st>>>(fr, roi, half, 1, cfg.quality_level, s.maxbits,
+                                                  s.count, s.cand_key, s.cand_idx, s.cap, nullptr);
+    }
+    const size_t smem = detect_smem_bytes(cfg, rw, rh);
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    short2* g_axy = nullptr;
+    int* g_anext = nullptr;
+    if (cfg.max_corners > SMEM_CORNERS) {
+        // large budgets keep the accepted list in global scratch (sort_idx tail is free)
+        cudaMallocAsync((void**)&g_axy, sizeof(short2) * (size_t)nD * cfg.max_corners, st);
+        cudaMallocAsync((void**)&g_anext, sizeof(int) * (size_t)nD * cfg.max_corners, st);
+    }
+    select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy,
+                                                 g_anext);
+    if (g_axy) {
+        cudaFreeAsync(g_axy, st);
+        cudaFreeAsync(g_anext, st);
+    }
+}
+
+void launch_gradients(const uint8_t* src, int w, int h, double* gx, double* gy, cudaStream_t st) {
+    dim3 grid((w + 127) / 128, h);
+    gradients_kernel<<<grid, 128, 0, st>>>(src, w, h, gx, gy);
+}
+
+void launch_min_eig(const uint8_t* src, int w, int h, int block, double* out, cudaStream_t st) {
+    PlaneBatch fr{src, (size_t)w * h, w, h};
+    stabgpu_roi all{0, 0, w, h};
+    dim3 grid((w + 127) / 128, h, 1);
+    resp_generic_kernel<<<grid, 128, 0, st>>>(fr, all, block / 2, 2, 0.0, nullptr, nullptr, nullptr,
+                                              nullptr, 0, out);
+}
+
+}  // namespace stabgpu

@@ -1,0 +1,347 @@
+// k_fit.cu — K6 (closed-form rigid/similarity fit) and K6b (RANSAC), one CTA
+// per frame pair, batched over every frame of a chunk.
+//
+// Reference: accumulate/finish (motion.cpp:17-58), estimate_similarity /
+// estimate_rigid (62-76), rms_residual (78-90), extract_delta (92-101).
+// RANSAC has no reference counterpart; its rule is the one
+// restated in oracle/stab_oracle.c (orc_ransac_estimate): counter-based pair
+// sampling, a 2-point minimal model with only correctly rounded + - * / sqrt
+// in a fixed order, inliers by residual^2 <= thr^2, most inliers wins with
+// ties to the lowest hypothesis, fewer than min_tracks inliers falls back to
+// all pairs, then the closed-form fit on the inliers.  Hypotheses are scored
+// one per warp (lanes stride the pairs, popc-reduced counts), so inlier
+// counts are bit-identical to the CPU rule; only the refit's sums are
+// reduced in a different (fixed) order.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace stabgpu {
+
+namespace {
+
+constexpr int FIT_THREADS = 512;
+constexpr int FIT_WARPS = FIT_THREADS / 32;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+struct Model {
+    double a, b, tx, ty;
+};
+
+__device__ __forceinline__ bool minimal_model(const double2* P, const double2* Q, int i, int j,
+                                              bool rigid, Model& m) {
+    const double2 pi = P[i], pj = P[j], qi = Q[i], qj = Q[j];
+    const double mpx = dmul(0.5, dadd(pi.x, pj.x)), mpy = dmul(0.5, dadd(pi.y, pj.y));
+    const double mqx = dmul(0.5, dadd(qi.x, qj.x)), mqy = dmul(0.5, dadd(qi.y, qj.y));
+    const double ax = dsub(pj.x, pi.x), ay = dsub(pj.y, pi.y);
+    const double bx = dsub(qj.x, qi.x), by = dsub(qj.y, qi.y);
+    const double norm = dadd(dmul(ax, ax), dmul(ay, ay));
+    if (norm == 0.0) return false;
+    double a = ddiv(dadd(dmul(ax, bx), dmul(ay, by)), norm);
+    double b = ddiv(dsub(dmul(ax, by), dmul(ay, bx)), norm);
+    if (rigid) {
+        const double r = dsqrt(dadd(dmul(a, a), dmul(b, b)));
+        if (r == 0.0) return false;
+        a = ddiv(a, r);
+        b = ddiv(b, r);
+    }
+    m.a = a;
+    m.b = b;
+    m.tx = dsub(mqx, dsub(dmul(a, mpx), dmul(b, mpy)));
+    m.ty = dsub(mqy, dadd(dmul(b, mpx), dmul(a, mpy)));
+    return true;
+}
+
+__device__ __forceinline__ bool inlier(const Model& m, double2 p, double2 q, double thr2) {
+    const double ex = dsub(q.x, dadd(dsub(dmul(m.a, p.x), dmul(m.b, p.y)), m.tx));
+    const double ey = dsub(q.y, dadd(dadd(dmul(m.b, p.x), dmul(m.a, p.y)), m.ty));
+    return dadd(dmul(ex, ex), dmul(ey, ey)) <= thr2;
+}
+
+// Deterministic block sum (fixed tree: strided partials, butterfly, warps in order).
+__device__ double block_dsum(double v, double* red) {
+    v = warp_dsum(v);
+    const int wid = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < FIT_WARPS; ++w) t = dadd(t, red[w]);
+    return t;
+}
+
+struct FitOut {
+    double tx, ty, theta, s;
+    int status;
+};
+
+// accumulate + estimate_{rigid,similarity} over pairs with mask[k] != 0.
+__device__ FitOut estimate(const double2* P, const double2* Q, const uint8_t* mask, int n, int used,
+                           bool rigid, double* red) {
+    FitOut o{0, 0, 0, 1, STABGPU_OK};
+    if (used < 2) {
+        o.status = STABGPU_DEGENERATE_INPUT;
+        return o;
+    }
+    double sx = 0, sy = 0, dxs = 0, dys = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        if (!mask || mask[k]) {
+            sx = dadd(sx, P[k].x);
+            sy = dadd(sy, P[k].y);
+            dxs = dadd(dxs, Q[k].x);
+            dys = dadd(dys, Q[k].y);
+        }
+    const double dn = (double)used;
+    const double scx = ddiv(block_dsum(sx, red), dn), scy = ddiv(block_dsum(sy, red), dn);
+    const double dcx = ddiv(block_dsum(dxs, red), dn), dcy = ddiv(block_dsum(dys, red), dn);
+    double dot = 0, cross = 0, norm = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        if (!mask || mask[k]) {
+            const double x = dsub(P[k].x, scx), y = dsub(P[k].y, scy);
+            const double xp = dsub(Q[k].x, dcx), yp = dsub(Q[k].y, dcy);
+            dot = dadd(dot, dadd(dmul(x, xp), dmul(y, yp)));
+            cross = dadd(cross, dsub(dmul(x, yp), dmul(y, xp)));
+            norm = dadd(norm, dadd(dmul(x, x), dmul(y, y)));
+        }
+    dot = block_dsum(dot, red);
+    cross = block_dsum(cross, red);
+    norm = block_dsum(norm, red);
+    if (norm == 0.0) {
+        o.status = STABGPU_DEGENERATE_INPUT;
+        return o;
+    }
+    const double theta = atan2(cross, dot);
+    double scale = 1.0;
+    if (!rigid) {
+        scale = ddiv(dadd(dmul(cos(theta), dot), dmul(sin(theta), cross)), norm);
+        if (!(scale > 0.0) || !isfinite(scale)) {
+            o.status = STABGPU_DEGENERATE_INPUT;
+            return o;
+        }
+    }
+    const double c = dmul(scale, cos(theta)), sn = dmul(scale, sin(theta));
+    o.theta = theta;
+    o.s = scale;
+    o.tx = dsub(dcx, dsub(dmul(c, scx), dmul(sn, scy)));
+    o.ty = dsub(dcy, dadd(dmul(sn, scx), dmul(c, scy)));
+    return o;
+}
+
+// rms_residual over all pairs (motion.cpp:78-90, apply = transform.cpp:7-11)
+__device__ double rms(const double2* P, const double2* Q, int n, const FitOut& t, double* red) {
+    const double c = dmul(t.s, cos(t.theta)), sn = dmul(t.s, sin(t.theta));
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const double mx = dadd(dsub(dmul(c, P[k].x), dmul(sn, P[k].y)), t.tx);
+        const double my = dadd(dadd(dmul(sn, P[k].x), dmul(c, P[k].y)), t.ty);
+        const double dx = dsub(Q[k].x, mx), dy = dsub(Q[k].y, my);
+        acc = dadd(acc, dadd(dmul(dx, dx), dmul(dy, dy)));
+    }
+    return dsqrt(ddiv(block_dsum(acc, red), (double)n));
+}
+
+// RANSAC inlier selection; returns the pair count the refit uses and fills mask.
+__device__ int ransac_select(const double2* P, const double2* Q, int n, bool rigid,
+                             const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
+                             uint8_t* mask, int* wbest_c, int* wbest_h, Model* wbest_m) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double thr2 = dmul(rc.threshold, rc.threshold);
+    const uint64_t key = mix64(rc.seed ^ mix64((uint64_t)frame + 0x9e3779b97f4a7c15ULL));
+    int best_c = 0, best_h = -1;
+    Model best_m{0, 0, 0, 0};
+    for (int h = wid; h < rc.iterations; h += FIT_WARPS) {
+        const uint64_t u = mix64(key + (uint64_t)(h + 1) * 0x9e3779b97f4a7c15ULL);
+        const int i = (int)((uint32_t)(u >> 32) % (uint32_t)n);
+        int j = (int)((uint32_t)u % (uint32_t)(n - 1));
+        if (j >= i) ++j;
+        Model m;
+        if (!minimal_model(P, Q, i, j, rigid, m)) continue;
+        int cnt = 0;
+        for (int k = lane; k < n; k += 32) cnt += inlier(m, P[k], Q[k], thr2) ? 1 : 0;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (cnt > best_c) {  // h ascends within a warp: strict > keeps the lowest h
+            best_c = cnt;
+            best_h = h;
+            best_m = m;
+        }
+    }
+    if (lane == 0) {
+        wbest_c[wid] = best_c;
+        wbest_h[wid] = best_h;
+        wbest_m[wid] = best_m;
+    }
+    __syncthreads();
+    int bc = 0, bh = -1;
+    Model bm{0, 0, 0, 0};
+    for (int w = 0; w < FIT_WARPS; ++w) {
+        const int c = wbest_c[w], hh = wbest_h[w];
+        if (hh < 0) continue;
+        if (bh < 0 || c > bc || (c == bc && hh < bh)) {
+            bc = c;
+            bh = hh;
+            bm = wbest_m[w];
+        }
+    }
+    __syncthreads();
+    if (bh < 0 || bc < min_tracks) {
+        for (int k = threadIdx.x; k < n; k += blockDim.x) mask[k] = 1;
+        __syncthreads();
+        return n;
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) mask[k] = inlier(bm, P[k], Q[k], thr2) ? 1 : 0;
+    __syncthreads();
+    return bc;
+}
+
+__global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restrict__ trk_prev,
+                                                          const double2* __restrict__ trk_cur,
+                                                          const int* __restrict__ trk_n, int max_pts,
+                                                          long long frame_index0, stabgpu_config cfg,
+                                                          stabgpu_motion_record* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    __shared__ double red[FIT_WARPS];
+    __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
+    __shared__ Model wbest_m[FIT_WARPS];
+    const int f = blockIdx.x;
+    const int n = trk_n[f];
+    stabgpu_motion_record rec;
+    memset(&rec, 0, sizeof rec);
+    rec.n_tracks = n;
+    rec.rigid.kind = STABGPU_RIGID;
+    rec.similarity.kind = STABGPU_SIMILARITY;
+    stabgpu_motion_record* o = out + f;
+    if (n < cfg.flow.min_tracks) {
+        if (threadIdx.x == 0) {
+            rec.frame_kind = STABGPU_FRAME_SKIPPED;
+            *o = rec;
+        }
+        return;
+    }
+    rec.frame_kind = STABGPU_FRAME_TRACKED;
+    double2* P = reinterpret_cast<double2*>(fsm);
+    double2* Q = P + max_pts;
+    uint8_t* mask = reinterpret_cast<uint8_t*>(Q + max_pts);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        P[k] = trk_prev[(size_t)f * max_pts + k];
+        Q[k] = trk_cur[(size_t)f * max_pts + k];
+    }
+    __syncthreads();
+    const long long frame = frame_index0 + f;
+    const int mode = cfg.selector.mode;
+    FitOut fr{0, 0, 0, 1, STABGPU_OK}, fs{0, 0, 0, 1, STABGPU_OK};
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool rigid = pass == 0;
+        if (rigid && mode == STABGPU_FORCE_SIMILARITY) continue;
+        if (!rigid && mode == STABGPU_FORCE_RIGID) continue;
+        int used = n;
+        const uint8_t* m = nullptr;
+        if (cfg.ransac.iterations > 0) {
+            used = ransac_select(P, Q, n, rigid, cfg.ransac, cfg.flow.min_tracks, frame, mask,
+                                 wbest_c, wbest_h, wbest_m);
+            m = used == n ? nullptr : mask;
+        }
+        const FitOut r = estimate(P, Q, m, n, used, rigid, red);
+        if (rigid) {
+            fr = r;
+            rec.n_inliers_rigid = used;
+        } else {
+            fs = r;
+            rec.n_inliers_similarity = used;
+        }
+        __syncthreads();
+    }
+    if (mode == STABGPU_HYBRID && fr.status == STABGPU_OK && fs.status == STABGPU_OK) {
+        rec.e_rigid = rms(P, Q, n, fr, red);
+        rec.e_similarity = rms(P, Q, n, fs, red);
+    }
+    if (threadIdx.x == 0) {
+        // extract_delta (motion.cpp:92-101)
+        rec.rigid.dx = fr.tx;
+        rec.rigid.dy = fr.ty;
+        rec.rigid.da = fr.theta;
+        rec.rigid.dls = 0.0;
+        rec.similarity.dx = fs.tx;
+        rec.similarity.dy = fs.ty;
+        rec.similarity.da = fs.theta;
+        rec.similarity.dls = log(fs.s);
+        rec.status = fr.status | (fs.status << 8);
+        *o = rec;
+    }
+}
+
+}  // namespace
+
+void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
+                int nframes, long long frame_index0, const stabgpu_config& cfg,
+                stabgpu_motion_record* out, cudaStream_t st) {
+    if (nframes <= 0) return;
+    const size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
+    cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fit_kernel<<<nframes, FIT_THREADS, smem, st>>>(trk_prev, trk_cur, trk_n, max_pts, frame_index0,
+                                                   cfg, out);
+}
+
+}  // namespace stabgpu
+
+namespace stabgpu {
+namespace {
+__global__ void __launch_bounds__(FIT_THREADS) fit_single_kernel(const double2* __restrict__ gP,
+                                                                 const double2* __restrict__ gQ,
+                                                                 int n, int kind,
+                                                                 stabgpu_ransac_cfg rc, int min_tracks,
+                                                                 long long frame, FitResult* out,
+                                                                 uint8_t* __restrict__ gmask) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    __shared__ double red[FIT_WARPS];
+    __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
+    __shared__ Model wbest_m[FIT_WARPS];
+    double2* P = reinterpret_cast<double2*>(fsm);
+    double2* Q = P + n;
+    uint8_t* mask = reinterpret_cast<uint8_t*>(Q + n);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        P[k] = gP[k];
+        Q[k] = gQ[k];
+        mask[k] = 1;
+    }
+    __syncthreads();
+    const bool rigid = kind == STABGPU_RIGID;
+    int used = n;
+    const uint8_t* m = nullptr;
+    if (n >= 2 && rc.iterations > 0) {
+        used = ransac_select(P, Q, n, rigid, rc, min_tracks, frame, mask, wbest_c, wbest_h, wbest_m);
+        m = used == n ? nullptr : mask;
+    }
+    const FitOut r = estimate(P, Q, m, n, used, rigid, red);
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+        if (gmask) gmask[k] = mask[k];
+    if (threadIdx.x == 0) *out = FitResult{r.tx, r.ty, r.theta, r.s, r.status, used};
+}
+
+__global__ void __launch_bounds__(FIT_THREADS) rms_single_kernel(const double2* __restrict__ P,
+                                                                 const double2* __restrict__ Q,
+                                                                 int n, stabgpu_transform t,
+                                                                 double* out) {
+    __shared__ double red[FIT_WARPS];
+    const FitOut f{t.tx, t.ty, t.theta, t.s, 0};
+    const double v = rms(P, Q, n, f, red);
+    if (threadIdx.x == 0) *out = v;
+}
+}  // namespace
+
+void launch_fit_single(const double2* P, const double2* Q, int n, int kind,
+                       const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
+                       FitResult* out, uint8_t* mask, cudaStream_t st) {
+    const size_t smem = (size_t)n * (2 * sizeof(double2) + 1) + 16;
+    cudaFuncSetAttribute(fit_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fit_single_kernel<<<1, FIT_THREADS, smem, st>>>(P, Q, n, kind, rc, min_tracks, frame, out, mask);
+}
+
+void launch_rms_single(const double2* P, const double2* Q, int n, stabgpu_transform t, double* out,
+                       cudaStream_t st) {
+    rms_single_kernel<<<1, FIT_THREADS, 0, st>>>(P, Q, n, t, out);
+}
+}  // namespace stabgpu

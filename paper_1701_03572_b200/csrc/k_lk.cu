@@ -1,0 +1,298 @@
+// k_lk.cu — K5: pyramidal Lucas-Kanade, one warp per feature, forward then
+// backward (forward-backward weeding) in the same warp.
+//
+// Reference: extract_patch (flow.cpp:28-59), build_level_patch (77-126),
+// inside (128-130), track_one (132-227), track_lk (243-256), weed_tracks
+// (258-280).  Every scalar step uses correctly rounded fp64 ops in the
+// reference order; the only departure is the order of the window sums
+// (G tensor and the b vector), which a warp reduces as 32 strided partials
+// plus a butterfly.  That changes results by ~1e-13 px, far inside the 0.01 px
+// tolerance, and every lane ends with identical bits, so the warp's control
+// flow (convergence, divergence, status) stays uniform.
+//
+// Per warp, shared memory holds the extended (2r+3)^2 template patch and the
+// template gradients over the valid window; the valid window is a rectangle
+// (the reference's per-row / per-column clipping is separable), flattened so
+// the 32 lanes stride it densely.  Segments (independent 5-frame tracking
+// chains, grid.y) and features (grid.x) are both batched into one launch.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace stabgpu {
+
+namespace {
+
+struct Level {
+    const uint8_t* px;
+    int w, h;
+};
+
+__device__ __forceinline__ bool inside(const Level& L, double x, double y) {
+    return x >= 0.0 && y >= 0.0 && x <= (double)L.w - 1.0 && y <= (double)L.h - 1.0;
+}
+
+__device__ __forceinline__ double bilerp(const Level& L, int x0, int y0, int i, int j, double w00,
+                                         double w10, double w01, double w11) {
+    // flow.cpp:43-58: clamped indices, shared weights, left-to-right sum
+    const int xa = clampi(x0 + i, 0, L.w - 1), xb = clampi(x0 + i + 1, 0, L.w - 1);
+    const int ya = clampi(y0 + j, 0, L.h - 1), yb = clampi(y0 + j + 1, 0, L.h - 1);
+    const uint8_t* ra = L.px + (size_t)ya * L.w;
+    const uint8_t* rb = L.px + (size_t)yb * L.w;
+    const double a = __ldg(ra + xa), b = __ldg(ra + xb), c = __ldg(rb + xa), d = __ldg(rb + xb);
+    return dadd(dadd(dadd(dmul(w00, a), dmul(w10, b)), dmul(w01, c)), dmul(w11, d));
+}
+
+struct Weights {
+    int x0, y0;
+    double w00, w10, w01, w11;
+};
+
+__device__ __forceinline__ Weights weights_at(double cx, double cy) {
+    Weights W;
+    const double fx0 = floor(cx), fy0 = floor(cy);
+    W.x0 = (int)fx0;
+    W.y0 = (int)fy0;
+    const double fx = dsub(cx, (double)W.x0), fy = dsub(cy, (double)W.y0);
+    W.w00 = dmul(dsub(1.0, fx), dsub(1.0, fy));
+    W.w10 = dmul(fx, dsub(1.0, fy));
+    W.w01 = dmul(dsub(1.0, fx), fy);
+    W.w11 = dmul(fx, fy);
+    return W;
+}
+
+// track_one for one point; called by all 32 lanes of a warp (uniform flow).
+__device__ bool track_warp(const DevPyramid& P, int fprev, int fcur, double px, double py,
+                           const stabgpu_flow_cfg& cfg, double* ext, double* tgx, double* tgy,
+                           double& ox, double& oy, unsigned& iters) {
+    const int lane = threadIdx.x & 31;
+    const int r = cfg.window_radius, side = 2 * r + 1;
+    const int e = r + 1, es = 2 * e + 1;
+    int start_level = 0;
+    for (int l = P.levels - 1; l > 0; --l)
+        if (min(P.w[l], P.h[l]) >= side) {
+            start_level = l;
+            break;
+        }
+    const int min_count = max(25, side * side / 4);
+    const double r2 = (double)r * r, eps2 = dmul(cfg.epsilon, cfg.epsilon);
+    double gfx = 0.0, gfy = 0.0;
+    for (int level = start_level; level >= 0; --level) {
+        const Level pi{P.lvl[level] + (size_t)fprev * P.stride[level], P.w[level], P.h[level]};
+        const Level ci{P.lvl[level] + (size_t)fcur * P.stride[level], P.w[level], P.h[level]};
+        const double scale = (double)(1u << level);
+        const double plx = ddiv(px, scale), ply = ddiv(py, scale);
+        if (!inside(pi, plx, ply)) return false;
+        // ---- build_level_patch (flow.cpp:77-126)
+        const Weights T = weights_at(plx, ply);
+        for (int k = lane; k < es * es; k += 32) {
+            const int jj = k / es, ii = k - jj * es;
+            ext[k] = bilerp(pi, T.x0 - e, T.y0 - e, ii, jj, T.w00, T.w10, T.w01, T.w11);
+        }
+        __syncwarp();
+        // valid rows: 1 <= y0-r+j && y0-r+j+2 <= h-1 ; columns alike
+        const int jv0 = max(0, 1 - T.y0 + r), jv1 = min(side - 1, pi.h - 3 - T.y0 + r);
+        const int iv0 = max(0, 1 - T.x0 + r), iv1 = min(side - 1, pi.w - 3 - T.x0 + r);
+        const int vh = jv1 - jv0 + 1, vw = iv1 - iv0 + 1;
+        const int count = (vh > 0 && vw > 0) ? vh * vw : 0;
+        if (count < min_count) {  // TooSmall (flow.cpp:116-118)
+            if (level == 0) return false;
+            gfx = dmul(gfx, 2.0);
+            gfy = dmul(gfy, 2.0);
+            continue;
+        }
+        const int di = 32 % vw, dj = 32 / vw;
+        double gxx = 0.0, gxy = 0.0, gyy = 0.0;
+        {
+            int j = jv0 + lane / vw, i = iv0 + lane % vw;
+            for (int k = lane; k < count; k += 32) {
+                const double* mid = ext + (j + 1) * es + 1;
+                const double dx = dmul(0.5, dsub(mid[i + 1], mid[i - 1]));
+                const double dy = dmul(0.5, dsub(mid[i + es], mid[i - es]));
+                tgx[k] = dx;
+                tgy[k] = dy;
+                gxx = dadd(gxx, dmul(dx, dx));
+                gxy = dadd(gxy, dmul(dx, dy));
+                gyy = dadd(gyy, dmul(dy, dy));
+                i += di;
+                j += dj;
+                if (i > iv1) {
+                    i -= vw;
+                    ++j;
+                }
+            }
+        }
+        gxx = warp_dsum(gxx);
+        gxy = warp_dsum(gxy);
+        gyy = warp_dsum(gyy);
+        __syncwarp();
+        {
+            const double ht = dmul(0.5, dadd(gxx, gyy)), hd = dmul(0.5, dsub(gxx, gyy));
+            const double me = dsub(ht, dsqrt(dadd(dmul(hd, hd), dmul(gxy, gxy))));
+            if (me < dmul(1e-4, (double)count)) return false;  // Unconditioned
+        }
+        const double det = dsub(dmul(gxx, gyy), dmul(gxy, gxy));
+        double vx = 0.0, vy = 0.0;
+        bool diverged = false;
+        for (int it = 0; it < cfg.max_iterations; ++it) {
+            const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
+            if (!inside(ci, qx, qy)) {
+                diverged = true;
+                break;
+            }
+            ++iters;
+            const Weights C = weights_at(qx, qy);
+            double bx = 0.0, by = 0.0;
+            int j = jv0 + lane / vw, i = iv0 + lane % vw;
+            for (int k = lane; k < count; k += 32) {
+                const double cur = bilerp(ci, C.x0 - r, C.y0 - r, i, j, C.w00, C.w10, C.w01, C.w11);
+                const double d = dsub(ext[(j + 1) * es + i + 1], cur);
+                bx = dadd(bx, dmul(d, tgx[k]));
+                by = dadd(by, dmul(d, tgy[k]));
+                i += di;
+                j += dj;
+                if (i > iv1) {
+                    i -= vw;
+                    ++j;
+                }
+            }
+            bx = warp_dsum(bx);
+            by = warp_dsum(by);
+            const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
+            const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
+            vx = dadd(vx, dx);
+            vy = dadd(vy, dy);
+            if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
+                diverged = true;
+                break;
+            }
+            if (dadd(dmul(dx, dx), dmul(dy, dy)) < eps2) break;
+        }
+        __syncwarp();
+        if (diverged && level == 0) return false;
+        if (!diverged) {
+            gfx = dadd(gfx, vx);
+            gfy = dadd(gfy, vy);
+        }
+        if (level > 0) {
+            gfx = dmul(gfx, 2.0);
+            gfy = dmul(gfy, 2.0);
+        }
+    }
+    const double rx = dadd(px, gfx), ry = dadd(py, gfy);
+    const Level base{P.lvl[0] + (size_t)fcur * P.stride[0], P.w[0], P.h[0]};
+    if (!inside(base, rx, ry)) return false;
+    ox = rx;
+    oy = ry;
+    return true;
+}
+
+__global__ void lk_kernel(LkStep s, stabgpu_flow_cfg cfg, int warps_per_cta, int smem_per_warp) {
+    extern __shared__ __align__(16) double lsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int seg = blockIdx.y;
+    const int k = blockIdx.x * warps_per_cta + warp;
+    const int fprev = s.frame0 + seg * s.seg_len + s.t - 1, fcur = fprev + 1;
+    if (fcur >= s.nframes) return;
+    if (k >= s.npts[seg]) return;
+    const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
+    double* ext = lsm + (size_t)warp * smem_per_warp;
+    double* tgx = ext + es * es;
+    double* tgy = tgx + side * side;
+    const size_t slot = (size_t)seg * s.max_pts + k;
+    const double2 p = s.pts[slot];
+    unsigned iters = 0;
+    double fx = p.x, fy = p.y;
+    bool keep;
+    if (s.mode == 2) {  // weed only: p is the cur point, ref the prev point
+        double bx, by;
+        keep = track_warp(s.pyr, fcur, fprev, p.x, p.y, cfg, ext, tgx, tgy, bx, by, iters);
+        if (keep) {
+            const double2 q = s.ref[slot];
+            const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
+            keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
+        }
+    } else {
+        keep = track_warp(s.pyr, fprev, fcur, p.x, p.y, cfg, ext, tgx, tgy, fx, fy, iters);
+        if (keep && s.mode == 1) {  // weed_tracks: backward re-track and fb test
+            double bx, by;
+            keep = track_warp(s.pyr, fcur, fprev, fx, fy, cfg, ext, tgx, tgy, bx, by, iters);
+            if (keep) {
+                const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
+                keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
+            }
+        }
+    }
+    if (lane == 0) {
+        s.fwd[slot] = make_double2(fx, fy);
+        s.keep[slot] = keep ? 1 : 0;
+        if (s.iter_count) atomicAdd(s.iter_count, (unsigned long long)iters);
+    }
+}
+
+// Ordered compaction per segment (one CTA each).
+__global__ void compact_kernel(LkStep s, double2* __restrict__ next_pts, int* __restrict__ next_n,
+                               double2* __restrict__ trk_prev, double2* __restrict__ trk_cur,
+                               int* __restrict__ trk_n, int trk_frame0) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int seg = blockIdx.x;
+    const int fcur = s.frame0 + seg * s.seg_len + s.t;
+    if (fcur >= s.nframes) return;
+    const int n = s.npts[seg];
+    const int tf = fcur - trk_frame0;  // TrackSet slot of frame fcur
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        const int k = c0 + threadIdx.x;
+        const size_t slot = (size_t)seg * s.max_pts + k;
+        const bool kp = k < n && s.keep[slot];
+        const unsigned b = __ballot_sync(0xffffffffu, kp);
+        if (lane == 0) warp_tot[wid] = __popc(b);
+        __syncthreads();
+        int off = base;
+        for (int w2 = 0; w2 < wid; ++w2) off += warp_tot[w2];
+        off += __popc(b & ((1u << lane) - 1));
+        if (kp) {
+            const double2 c = s.fwd[slot];
+            const size_t o = (size_t)seg * s.max_pts + off;
+            next_pts[o] = c;
+            const size_t to = (size_t)tf * s.max_pts + off;
+            trk_prev[to] = s.pts[slot];
+            trk_cur[to] = c;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w2 = 0; w2 < nw; ++w2) t += warp_tot[w2];
+            base += t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        next_n[seg] = base;
+        trk_n[tf] = base;
+    }
+}
+
+}  // namespace
+
+void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
+    if (s.nseg <= 0 || s.max_pts <= 0) return;
+    const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
+    const int per_warp = es * es + 2 * side * side;  // doubles
+    int wpc = (int)((100 * 1024) / (per_warp * sizeof(double)));
+    wpc = max(1, min(8, wpc));
+    const size_t smem = (size_t)wpc * per_warp * sizeof(double);
+    cudaFuncSetAttribute(lk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((s.max_pts + wpc - 1) / wpc, s.nseg);
+    lk_kernel<<<grid, wpc * 32, smem, st>>>(s, cfg, wpc, per_warp);
+}
+
+void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,
+                    double2* trk_cur, int* trk_n, int trk_frame0, cudaStream_t st) {
+    if (s.nseg <= 0) return;
+    compact_kernel<<<s.nseg, 256, 0, st>>>(s, next_pts, next_n, trk_prev, trk_cur, trk_n, trk_frame0);
+}
+
+}  // namespace stabgpu

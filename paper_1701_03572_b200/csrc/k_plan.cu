@@ -1,0 +1,173 @@
+// k_plan.cu — K7: model-selection scan, trajectory prefix and moving-average
+// smoothing, on the device.
+//
+// Reference: ModelSelector::select / note_skipped (motion.cpp:143-191),
+// MotionStage::step (pipeline.cpp:80-101), Trajectory::append (smoothing.cpp:
+// 16-24), smooth_at (26-46), correction (48-57), delta_to_transform
+// (motion.cpp:103-111).
+//
+// The selector and the running sum are sequential recurrences and are
+// evaluated sequentially (one thread, reference order), which keeps the
+// cumulative path bit-identical to the reference; the scan is incremental so
+// a streaming caller can feed motion records chunk by chunk.  Each smoothed
+// value is an independent window mean, one thread per frame, summed in the
+// reference's ascending order.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace stabgpu {
+
+namespace {
+
+__global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motion, long long first,
+                                 long long count, stabgpu_selector_cfg sel, PlanState* st,
+                                 stabgpu_frame_record* __restrict__ rec, double4* __restrict__ cum,
+                                 int* __restrict__ err) {
+    if (threadIdx.x != 0) return;
+    PlanState s = *st;
+    for (long long f = first; f < first + count; ++f) {
+        const stabgpu_motion_record m = motion[f];
+        stabgpu_frame_record r;
+        memset(&r, 0, sizeof r);
+        r.frame_kind = m.frame_kind;
+        r.n_tracks = m.n_tracks;
+        stabgpu_delta d{0.0, 0.0, 0.0, 0.0, s.current, 0};
+        if (m.frame_kind != STABGPU_FRAME_TRACKED) {
+            // note_skipped (motion.cpp:185-191)
+            if (s.since == 0) s.pending = 1;
+            s.since = (s.since + 1) % sel.dwell;
+            d.kind = s.current;
+            d.skipped = m.frame_kind == STABGPU_FRAME_SKIPPED;
+        } else {
+            if (s.since == 0) s.pending = 1;
+            const int st_r = m.status & 0xff, st_s = (m.status >> 8) & 0xff;
+            int use_rigid;
+            if (sel.mode == STABGPU_FORCE_RIGID || sel.mode == STABGPU_FORCE_SIMILARITY) {
+                use_rigid = sel.mode == STABGPU_FORCE_RIGID;
+                if (s.pending) {
+                    s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
+                    s.pending = 0;
+                    r.decision = 1;
+                }
+                const int e = use_rigid ? st_r : st_s;
+                if (e && *err == 0) *err = e | (int)(f << 4);
+            } else if (s.pending) {
+                if ((st_r || st_s) && *err == 0) *err = (st_r ? st_r : st_s) | (int)(f << 4);
+                use_rigid = m.e_rigid <= dmul(m.e_similarity, dadd(1.0, sel.margin));
+                s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
+                s.pending = 0;
+                r.decision = 1;
+            } else {
+                use_rigid = s.current == STABGPU_RIGID;
+                const int e = use_rigid ? st_r : st_s;
+                if (e && *err == 0) *err = e | (int)(f << 4);
+            }
+            s.since = (s.since + 1) % sel.dwell;
+            d = use_rigid ? m.rigid : m.similarity;
+            d.skipped = 0;
+            r.n_inliers = use_rigid ? m.n_inliers_rigid : m.n_inliers_similarity;
+        }
+        // Trajectory::append (smoothing.cpp:16-24)
+        s.cum[0] = dadd(s.cum[0], d.dx);
+        s.cum[1] = dadd(s.cum[1], d.dy);
+        s.cum[2] = dadd(s.cum[2], d.da);
+        s.cum[3] = dadd(s.cum[3], d.dls);
+        cum[f] = make_double4(s.cum[0], s.cum[1], s.cum[2], s.cum[3]);
+        r.delta = d;
+        rec[f] = r;
+    }
+    s.scanned = first + count;
+    *st = s;
+}
+
+__global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_known,
+                                   long long first, long long count, int radius,
+                                   stabgpu_frame_record* __restrict__ rec, FramePlan* __restrict__ plan) {
+    const long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= first + count) return;
+    const long long lo = i >= radius ? i - radius : 0;
+    const long long hi = min(i + radius, n_known - 1);
+    double sx = 0.0, sy = 0.0, sa = 0.0, sl = 0.0;
+    for (long long j = lo; j <= hi; ++j) {
+        const double4 c = cum[j];
+        sx = dadd(sx, c.x);
+        sy = dadd(sy, c.y);
+        sa = dadd(sa, c.z);
+        sl = dadd(sl, c.w);
+    }
+    const double n = (double)(hi - lo + 1);
+    const double4 ci = cum[i];
+    FramePlan p;
+    p.tx = dsub(ddiv(sx, n), ci.x);
+    p.ty = dsub(ddiv(sy, n), ci.y);
+    p.theta = dsub(ddiv(sa, n), ci.z);
+    p.s = exp(dsub(ddiv(sl, n), ci.w));
+    // warp_similarity / apply_inverse coefficients (image_ops.cpp:121-122, transform.cpp:14-15)
+    p.c = ddiv(cos(p.theta), p.s);
+    p.sn = ddiv(sin(p.theta), p.s);
+    plan[i] = p;
+    stabgpu_transform t{p.tx, p.ty, p.theta, p.s, STABGPU_SIMILARITY};
+    rec[i].correction = t;
+}
+
+}  // namespace
+
+void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long long count,
+                      const stabgpu_config& cfg, PlanState* state, stabgpu_frame_record* rec,
+                      double4* cum, cudaStream_t st) {
+    if (count <= 0) return;
+    // error word lives right after the state
+    plan_scan_kernel<<<1, 32, 0, st>>>(motion, first, count, cfg.selector, state, rec, cum,
+                                       reinterpret_cast<int*>(state + 1));
+}
+
+void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
+                        long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
+                        cudaStream_t st) {
+    (void)complete;
+    if (count <= 0) return;
+    const int tpb = 128;
+    plan_smooth_kernel<<<(unsigned)((count + tpb - 1) / tpb), tpb, 0, st>>>(cum, n_known, first, count,
+                                                                           radius, rec, plan);
+}
+
+}  // namespace stabgpu
+
+namespace stabgpu {
+namespace {
+__global__ void prefix_kernel(const stabgpu_delta* __restrict__ d, long long n, double4* __restrict__ cum) {
+    if (threadIdx.x != 0) return;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    for (long long i = 0; i < n; ++i) {
+        c0 = dadd(c0, d[i].dx);
+        c1 = dadd(c1, d[i].dy);
+        c2 = dadd(c2, d[i].da);
+        c3 = dadd(c3, d[i].dls);
+        cum[i] = make_double4(c0, c1, c2, c3);
+    }
+}
+
+__global__ void plan_from_corr_kernel(const stabgpu_transform* __restrict__ t, long long n,
+                                      FramePlan* __restrict__ plan) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    FramePlan p;
+    p.tx = t[i].tx;
+    p.ty = t[i].ty;
+    p.theta = t[i].theta;
+    p.s = t[i].s;
+    p.c = ddiv(cos(p.theta), p.s);
+    p.sn = ddiv(sin(p.theta), p.s);
+    plan[i] = p;
+}
+}  // namespace
+
+void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream_t st) {
+    if (n > 0) prefix_kernel<<<1, 32, 0, st>>>(d, n, cum);
+}
+
+void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
+                                  cudaStream_t st) {
+    if (n > 0) plan_from_corr_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(corr, n, plan);
+}
+}  // namespace stabgpu

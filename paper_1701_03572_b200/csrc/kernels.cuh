@@ -1,0 +1,127 @@
+// kernels.cuh — host-side launchers of the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stabgpu.h"
+
+namespace stabgpu {
+
+// Batched frame planes: frame f of a plane lives at base + f * stride.
+struct PlaneBatch {
+    const uint8_t* base;
+    size_t stride;
+    int w, h;
+};
+
+// Batched pyramid: level l of frame f at lvl[l] + f * stride[l].
+struct DevPyramid {
+    int levels;
+    int w[STABGPU_MAX_LEVELS], h[STABGPU_MAX_LEVELS];
+    const uint8_t* lvl[STABGPU_MAX_LEVELS];
+    size_t stride[STABGPU_MAX_LEVELS];
+};
+
+// Per-frame plan output consumed by the compose kernels.
+struct FramePlan {
+    double tx, ty, theta, s;  // correction transform (delta_to_transform)
+    double c, sn;             // cos(theta)/s, sin(theta)/s (warp_similarity, image_ops.cpp:121-122)
+};
+
+// Device-resident motion records are the public stabgpu_motion_record.
+
+// ---- K1 pyramid (k_pyramid.cu) ----
+void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst,
+                          size_t dst_stride, int frames, cudaStream_t st);
+
+// ---- K2-K4 detection (k_detect.cu) ----
+struct DetectScratch {
+    unsigned long long* maxbits;  // [nD]
+    unsigned int* count;          // [nD]
+    unsigned int* hist;           // [nD][kBuckets]
+    unsigned long long* cand_key; // [nD][cap]   score bits
+    unsigned int* cand_idx;       // [nD][cap]   y*w + x
+    unsigned long long* sort_key; // [nD][cap]
+    unsigned int* sort_idx;       // [nD][cap]
+    size_t cap;                   // candidates per detection frame (ROI area)
+};
+constexpr int kBuckets = 8192;
+constexpr int kBucketShift = 13;
+size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int roi_w, int roi_h);
+// Detects corners on nD frames at base + d*stride (d = 0..nD-1); writes up to
+// max_corners points per frame (out_xy[d*max + k], out_score) and out_n[d].
+void launch_detect(PlaneBatch frames, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
+                   DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
+                   cudaStream_t st);
+void launch_gradients(const uint8_t* src, int w, int h, double* gx, double* gy, cudaStream_t st);
+void launch_min_eig(const uint8_t* src, int w, int h, int block, double* out, cudaStream_t st);
+
+// ---- K5 LK (k_lk.cu) ----
+struct LkStep {
+    DevPyramid pyr;       // pyramids of all frames of the chunk
+    int frame0;           // chunk-relative frame of segment 0's detection frame
+    int seg_len;          // redetect_interval R
+    int t;                // step within the segment (1..R): prev = frame0 + s*R + t-1
+    int nseg;
+    int max_pts;
+    const double2* pts;   // [nseg][max_pts]
+    const int* npts;      // [nseg]
+    double2* fwd;         // [nseg][max_pts] forward result
+    uint8_t* keep;        // [nseg][max_pts]
+    unsigned long long* iter_count;  // optional LK iteration counter
+    int nframes;          // frames in pyr; a segment is active while cur < nframes
+    int mode;             // 0 track_lk, 1 forward + weed (sequence), 2 weed only
+    const double2* ref;   // mode 2: prev points the backward track must return to
+};
+void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
+// Ordered compaction of kept pairs: TrackSet of frame (frame0 + s*R + t) and
+// the next points of each segment.
+void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,
+                    double2* trk_cur, int* trk_n, int trk_frame0, cudaStream_t st);
+
+// ---- K6 fit + RANSAC (k_fit.cu) ----
+// Fits frames [0, nframes) whose TrackSets are trk_*[f*max_pts ...], trk_n[f].
+void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
+                int nframes, long long frame_index0, const stabgpu_config& cfg,
+                stabgpu_motion_record* out, cudaStream_t st);
+
+// ---- K7 plan (k_plan.cu) ----
+struct PlanState {  // carried across incremental calls (selector + prefix)
+    int current, since, pending, pad;
+    double cum[4];
+    long long scanned;  // motion records consumed
+};
+void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long long count,
+                      const stabgpu_config& cfg, PlanState* state, stabgpu_frame_record* rec,
+                      double4* cum, cudaStream_t st);
+void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
+                        long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
+                        cudaStream_t st);
+
+// ---- K8 compose (k_compose.cu) ----
+void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                    double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
+                    cudaStream_t st);
+void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
+                      cudaStream_t st);
+void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,
+                      cudaStream_t st);
+
+}  // namespace stabgpu
+
+namespace stabgpu {
+// ---- single-call helpers for the per-stage ABI ----
+struct FitResult {
+    double tx, ty, theta, s;
+    int status, used;
+};
+void launch_fit_single(const double2* P, const double2* Q, int n, int kind,
+                       const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
+                       FitResult* out, uint8_t* mask, cudaStream_t st);
+void launch_rms_single(const double2* P, const double2* Q, int n, stabgpu_transform t, double* out,
+                       cudaStream_t st);
+void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream_t st);
+void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
+                                  cudaStream_t st);
+}  // namespace stabgpu

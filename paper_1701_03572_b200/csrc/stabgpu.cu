@@ -1,0 +1,1091 @@
+// stabgpu.cu — C ABI (include/stabgpu.h) and the Stage-I host driver.
+//
+// The driver re-expresses the reference's frame-sequential run_offline
+// (pipeline.cpp:182-235) as a batched schedule that gives identical
+// semantics: tracking state resets at every re-detect frame
+// (flow.cpp:326-330), so the frames split into independent segments
+// [sR, (s+1)R] that are tracked side by side; the selector scan and the
+// trajectory are sequential recurrences over per-frame records and run on the
+// device after all fits; composition is independent per frame.
+//
+// Schedule of one motion chunk (frames first .. first+count):
+//   K1 pyramid levels (all frames, one launch per level)
+//   K2-K4 corners on every segment's first frame (one launch each, batched)
+//   R x { K5 LK forward+backward (all segments)  ->  ordered compaction }
+//   K6 fit (+RANSAC) of every frame pair
+// then K7 scan + smoothing and K8 compose over the sequence.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace stabgpu;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+};
+
+struct stabgpu_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t cin = nullptr, cout = nullptr;
+    std::map<std::string, DevBuf> bufs;
+    bool timing = false;
+    stabgpu_stats stats{};
+    cudaEvent_t ev[16]{};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char b[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof b, fmt, ap);
+    va_end(ap);
+    g_err = b;
+    return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            return set_err(STABGPU_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                           __FILE__, __LINE__);                                       \
+    } while (0)
+
+#define TRY(x)              \
+    do {                    \
+        int r_ = (x);       \
+        if (r_) return r_;  \
+    } while (0)
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(STABGPU_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return STABGPU_OK;
+}
+
+template <typename T>
+T* dbuf(stabgpu_ctx* ctx, const std::string& name, size_t count) {
+    DevBuf& b = ctx->bufs[name];
+    const size_t bytes = count * sizeof(T) + 256;
+    if (b.n < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.n = 0;
+        if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        b.n = bytes;
+    }
+    return static_cast<T*>(b.p);
+}
+
+#define DBUF(T, var, name, count)                                                         \
+    T* var = dbuf<T>(ctx, name, (count));                                                 \
+    if (!var) return set_err(STABGPU_CUDA, "device allocation of %s (%zu x %zu B) failed", \
+                             name, (size_t)(count), sizeof(T))
+
+// ---- validation: the reference's validate() overloads --------------------
+int validate_frame(int w, int h) {  // image_ops.cpp:9-16
+    if (w < STABGPU_MIN_FRAME_DIM || h < STABGPU_MIN_FRAME_DIM)
+        return set_err(STABGPU_INVALID_INPUT, "frame smaller than 16x16");
+    if (w > 32767 || h > 32767) return set_err(STABGPU_INVALID_INPUT, "frame larger than 32767 px");
+    return STABGPU_OK;
+}
+
+int validate_detect(const stabgpu_detect_cfg& c) {  // features.cpp:10-26
+    if (c.max_corners < 8) return set_err(STABGPU_INVALID_CONFIG, "max_corners must be >= 8");
+    if (!(c.quality_level > 0.0 && c.quality_level < 1.0))
+        return set_err(STABGPU_INVALID_CONFIG, "quality_level must lie in (0, 1)");
+    if (c.min_distance < 1.0) return set_err(STABGPU_INVALID_CONFIG, "min_distance must be >= 1");
+    if (c.block_size < 3 || c.block_size % 2 == 0)
+        return set_err(STABGPU_INVALID_CONFIG, "block_size must be odd and >= 3");
+    if (!(c.roi_margin >= 0.0 && c.roi_margin < 0.4))
+        return set_err(STABGPU_INVALID_CONFIG, "roi_margin must lie in [0, 0.4)");
+    return STABGPU_OK;
+}
+
+int validate_flow(const stabgpu_flow_cfg& c) {  // flow.cpp:10-21
+    if (c.window_radius < 1 || c.max_levels < 1 || c.max_iterations < 1 || c.epsilon <= 0.0 ||
+        c.fb_threshold <= 0.0)
+        return set_err(STABGPU_INVALID_CONFIG, "flow parameters must be positive");
+    if (c.redetect_interval < 1) return set_err(STABGPU_INVALID_CONFIG, "redetect_interval must be >= 1");
+    if (c.min_tracks < 4) return set_err(STABGPU_INVALID_CONFIG, "min_tracks must be >= 4");
+    return STABGPU_OK;
+}
+
+int validate_transform(const stabgpu_transform& t) {  // transform.cpp:51-59
+    if (!std::isfinite(t.tx) || !std::isfinite(t.ty) || !std::isfinite(t.theta) ||
+        !std::isfinite(t.s) || t.s <= 0.0)
+        return set_err(STABGPU_INVALID_TRANSFORM,
+                       "similarity transform requires finite parameters and s > 0");
+    if (t.kind == STABGPU_RIGID && t.s != 1.0)
+        return set_err(STABGPU_INVALID_TRANSFORM, "rigid transform must have s == 1");
+    return STABGPU_OK;
+}
+
+int validate_crop(double crop) {
+    if (!(crop >= 0.0 && crop < 0.25))
+        return set_err(STABGPU_INVALID_CONFIG, "crop_ratio must lie in [0, 0.25)");
+    return STABGPU_OK;
+}
+
+int roi_of(int w, int h, double margin, stabgpu_roi* out) {  // features.cpp:28-36
+    const int mx = (int)std::lround(margin * w), my = (int)std::lround(margin * h);
+    *out = {mx, my, w - mx, h - my};
+    if (out->x1 - out->x0 < 32 || out->y1 - out->y0 < 32)
+        return set_err(STABGPU_INVALID_CONFIG, "detection ROI smaller than 32x32");
+    return STABGPU_OK;
+}
+
+// build_pyramid level geometry (image_ops.cpp:62-77)
+int level_dims(int w, int h, int max_levels, int* lw, int* lh) {
+    int L = 1;
+    lw[0] = w;
+    lh[0] = h;
+    while (L < max_levels && L < STABGPU_MAX_LEVELS) {
+        if (lw[L - 1] / 2 < STABGPU_MIN_FRAME_DIM || lh[L - 1] / 2 < STABGPU_MIN_FRAME_DIM) break;
+        lw[L] = lw[L - 1] / 2;
+        lh[L] = lh[L - 1] / 2;
+        ++L;
+    }
+    return L;
+}
+
+FramePlan host_plan(const stabgpu_transform& t) {
+    // warp_similarity coefficients evaluated with the host libm, as the
+    // reference does (image_ops.cpp:121-122)
+    FramePlan p;
+    p.tx = t.tx;
+    p.ty = t.ty;
+    p.theta = t.theta;
+    p.s = t.s;
+    p.c = std::cos(t.theta) / t.s;
+    p.sn = std::sin(t.theta) / t.s;
+    return p;
+}
+
+struct Timer {
+    stabgpu_ctx* ctx;
+    int slot;
+    Timer(stabgpu_ctx* c, int s) : ctx(c), slot(s) {
+        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot], ctx->stream);
+    }
+    ~Timer() {
+        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot + 1], ctx->stream);
+    }
+};
+
+// ---- K1 + K2-K4 + K5 + K6 over frames [first, first+count] ----------------
+// y points at frame `first`; motion receives records for frames
+// first+1 .. first+count at motion[first+1 ...] (and frame 0 when first == 0).
+int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, int w, int h,
+               const stabgpu_config& cfg, stabgpu_motion_record* motion, double* t_ms) {
+    cudaStream_t st = ctx->stream;
+    const int nF = count + 1;
+    const int R = cfg.flow.redetect_interval;
+    const int maxc = cfg.detect.max_corners;
+    const int nseg = (count + R - 1) / R;
+    stabgpu_roi roi;
+    TRY(roi_of(w, h, cfg.detect.roi_margin, &roi));
+    if (first == 0) {
+        stabgpu_motion_record f0;
+        std::memset(&f0, 0, sizeof f0);
+        f0.frame_kind = STABGPU_FRAME_FIRST;
+        CUDA_TRY(cudaMemcpyAsync(motion, &f0, sizeof f0, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));  // f0 is a stack temporary
+    }
+    if (count <= 0) return STABGPU_OK;
+    // ---- K1: pyramid levels
+    DevPyramid P;
+    std::memset(&P, 0, sizeof P);
+    P.levels = level_dims(w, h, cfg.flow.max_levels, P.w, P.h);
+    P.lvl[0] = y;
+    P.stride[0] = (size_t)w * h;
+    {
+        Timer tm(ctx, 0);
+        for (int l = 1; l < P.levels; ++l) {
+            P.stride[l] = (size_t)P.w[l] * P.h[l];
+            DBUF(uint8_t, lv, ("pyr" + std::to_string(l)).c_str(), P.stride[l] * nF);
+            P.lvl[l] = lv;
+            launch_pyramid_level(P.lvl[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1], lv,
+                                 P.stride[l], nF, st);
+            ++ctx->stats.launches;
+        }
+        TRY(check_launch("pyramid"));
+    }
+    // ---- K2-K4: corners on each segment's first frame
+    const size_t cap = (size_t)(roi.x1 - roi.x0) * (roi.y1 - roi.y0);
+    DetectScratch ds;
+    DBUF(unsigned long long, maxbits, "det_max", nseg);
+    DBUF(unsigned int, dcount, "det_count", nseg);
+    DBUF(unsigned long long, ckey, "det_ckey", cap * nseg);
+    DBUF(unsigned int, cidx, "det_cidx", cap * nseg);
+    DBUF(unsigned long long, skey, "det_skey", cap * nseg);
+    DBUF(unsigned int, sidx, "det_sidx", cap * nseg);
+    ds.maxbits = maxbits;
+    ds.count = dcount;
+    ds.hist = nullptr;
+    ds.cand_key = ckey;
+    ds.cand_idx = cidx;
+    ds.sort_key = skey;
+    ds.sort_idx = sidx;
+    ds.cap = cap;
+    DBUF(double2, ptsA, "seg_ptsA", (size_t)nseg * maxc);
+    DBUF(double2, ptsB, "seg_ptsB", (size_t)nseg * maxc);
+    DBUF(int, nA, "seg_nA", nseg);
+    DBUF(int, nB, "seg_nB", nseg);
+    DBUF(double, dscore, "seg_score", (size_t)nseg * maxc);
+    {
+        Timer tm(ctx, 1);
+        PlaneBatch fb{y, (size_t)R * w * h, w, h};
+        launch_detect(fb, nseg, cfg.detect, roi, ds, ptsA, dscore, nA, st);
+        ctx->stats.launches += 3;
+        TRY(check_launch("detect"));
+    }
+    // ---- K5: R tracking steps over all segments
+    DBUF(double2, fwd, "lk_fwd", (size_t)nseg * maxc);
+    DBUF(uint8_t, keep, "lk_keep", (size_t)nseg * maxc);
+    DBUF(double2, trk_prev, "trk_prev", (size_t)count * maxc);
+    DBUF(double2, trk_cur, "trk_cur", (size_t)count * maxc);
+    DBUF(int, trk_n, "trk_n", count);
+    DBUF(unsigned long long, iters, "lk_iters", 1);
+    CUDA_TRY(cudaMemsetAsync(iters, 0, sizeof(unsigned long long), st));
+    {
+        Timer tm(ctx, 2);
+        double2* cur_pts = ptsA;
+        double2* nxt_pts = ptsB;
+        int* cur_n = nA;
+        int* nxt_n = nB;
+        for (int t = 1; t <= R && t <= count; ++t) {
+            LkStep s;
+            s.pyr = P;
+            s.frame0 = 0;
+            s.seg_len = R;
+            s.t = t;
+            s.nseg = nseg;
+            s.max_pts = maxc;
+            s.pts = cur_pts;
+            s.npts = cur_n;
+            s.fwd = fwd;
+            s.keep = keep;
+            s.iter_count = iters;
+            s.nframes = nF;
+            s.mode = 1;
+            s.ref = nullptr;
+            launch_lk(s, cfg.flow, st);
+            launch_compact(s, nxt_pts, nxt_n, trk_prev, trk_cur, trk_n, 1, st);
+            ctx->stats.launches += 2;
+            std::swap(cur_pts, nxt_pts);
+            std::swap(cur_n, nxt_n);
+        }
+        TRY(check_launch("lk"));
+    }
+    // ---- K6: fits
+    {
+        Timer tm(ctx, 3);
+        launch_fit(trk_prev, trk_cur, trk_n, maxc, count, first + 1, cfg, motion + first + 1, st);
+        ++ctx->stats.launches;
+        TRY(check_launch("fit"));
+    }
+    if (ctx->timing && t_ms) {
+        unsigned long long it = 0, nc = 0;
+        CUDA_TRY(cudaMemcpyAsync(&it, iters, sizeof it, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        ctx->stats.lk_iterations += (long long)it;
+        (void)nc;
+        for (int k = 0; k < 4; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->ev[2 * k], ctx->ev[2 * k + 1]);
+            t_ms[k] += ms;
+        }
+    }
+    return STABGPU_OK;
+}
+
+int init_plan_state(stabgpu_ctx* ctx, const stabgpu_config& cfg, PlanState** out) {
+    DBUF(PlanState, ps, "plan_state", 2);  // state + error word
+    PlanState s;
+    std::memset(&s, 0, sizeof s);
+    s.current = cfg.selector.mode == STABGPU_FORCE_SIMILARITY ? STABGPU_SIMILARITY : STABGPU_RIGID;
+    s.since = 0;
+    s.pending = 1;
+    PlanState z[2];
+    z[0] = s;
+    std::memset(&z[1], 0, sizeof z[1]);
+    CUDA_TRY(cudaMemcpyAsync(ps, z, sizeof z, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    *out = ps;
+    return STABGPU_OK;
+}
+
+int plan_error(stabgpu_ctx* ctx, PlanState* ps) {
+    int err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, reinterpret_cast<int*>(ps + 1), sizeof err, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (err) {
+        const int code = err & 0xf;
+        const long long f = err >> 4;
+        return set_err(code, code == STABGPU_DEGENERATE_INPUT
+                                 ? "frame %lld: degenerate point set (all source points coincide or non-positive scale)"
+                                 : "frame %lld: estimation failed",
+                       f);
+    }
+    return STABGPU_OK;
+}
+
+int validate_all(const stabgpu_config& c) {
+    TRY(validate_detect(c.detect));
+    TRY(validate_flow(c.flow));
+    if (c.smooth_radius < 1) return set_err(STABGPU_INVALID_CONFIG, "smoothing radius must be >= 1");
+    if (c.selector.dwell < 1) return set_err(STABGPU_INVALID_CONFIG, "dwell must be >= 1");
+    if (c.selector.margin < 0.0) return set_err(STABGPU_INVALID_CONFIG, "margin must be >= 0");
+    TRY(validate_crop(c.crop_ratio));
+    if (c.queue_capacity < 2 * (size_t)c.smooth_radius + 4)
+        return set_err(STABGPU_INVALID_CONFIG, "queue_capacity must be >= 2*radius + 4");
+    if (c.flow.window_radius > STABGPU_MAX_RADIUS)
+        return set_err(STABGPU_INVALID_CONFIG, "window_radius above 31 is not supported");
+    if (c.ransac.iterations < 0 || (c.ransac.iterations > 0 && !(c.ransac.threshold > 0.0)))
+        return set_err(STABGPU_INVALID_CONFIG, "ransac needs iterations >= 0 and threshold > 0");
+    if (c.selector.mode < 0 || c.selector.mode > 2)
+        return set_err(STABGPU_INVALID_CONFIG, "unknown selection mode");
+    return STABGPU_OK;
+}
+
+int compose_range(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                  long long first, long long count, int w, int h, int cw, int ch,
+                  const FramePlan* plan, double crop, uint8_t* oy, uint8_t* ocb, uint8_t* ocr) {
+    if (count <= 0) return STABGPU_OK;
+    const size_t lo = (size_t)first * w * h, co = (size_t)first * cw * ch;
+    PlaneBatch yb{y + lo, (size_t)w * h, w, h};
+    PlaneBatch bb{cb ? cb + co : nullptr, (size_t)cw * ch, cw, ch};
+    PlaneBatch rb{cr ? cr + co : nullptr, (size_t)cw * ch, cw, ch};
+    launch_compose(yb, bb, rb, plan + first, (int)count, crop, oy + lo, ocb ? ocb + co : nullptr,
+                   ocr ? ocr + co : nullptr, ctx->stream);
+    ctx->stats.launches += (cb && cr) ? 2 : 1;
+    return check_launch("compose");
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char* stabgpu_last_error(void) { return g_err.c_str(); }
+const char* stabgpu_version(void) { return "stabgpu 0.1 (sm_100a)"; }
+
+void stabgpu_default_config(stabgpu_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->detect = {50, 0.01, 10.0, 3, 0.1};
+    c->flow = {10, 4, 30, 0.01, 0.5, 5, 8};
+    c->smooth_radius = 10;
+    c->selector = {20, 0.05, STABGPU_HYBRID};
+    c->ransac = {0, 3.0, 0};
+    c->crop_ratio = 0.04;
+    c->queue_capacity = 64;
+}
+
+int stabgpu_validate_config(const stabgpu_config* c) { return validate_all(*c); }
+
+int stabgpu_create(int device, stabgpu_ctx** out) {
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_err(STABGPU_CUDA, "no CUDA device available (stabgpu has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return set_err(STABGPU_CUDA, "device %d out of range", device);
+    CUDA_TRY(cudaSetDevice(device));
+    stabgpu_ctx* c = new stabgpu_ctx();
+    c->device = device;
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->cin, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->cout, cudaStreamNonBlocking));
+    c->stream = c->own;
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    *out = c;
+    return STABGPU_OK;
+}
+
+int stabgpu_destroy(stabgpu_ctx* c) {
+    if (!c) return STABGPU_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->own);
+    cudaStreamDestroy(c->cin);
+    cudaStreamDestroy(c->cout);
+    delete c;
+    return STABGPU_OK;
+}
+
+int stabgpu_set_stream(stabgpu_ctx* c, void* s) {
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+    return STABGPU_OK;
+}
+
+int stabgpu_synchronize(stabgpu_ctx* c) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return STABGPU_OK;
+}
+
+int stabgpu_enable_timing(stabgpu_ctx* c, int on) {
+    c->timing = on != 0;
+    return STABGPU_OK;
+}
+
+int stabgpu_get_stats(stabgpu_ctx* c, stabgpu_stats* out) {
+    *out = c->stats;
+    return STABGPU_OK;
+}
+
+size_t stabgpu_pyramid_bytes(int w, int h, int max_levels) {
+    int lw[STABGPU_MAX_LEVELS], lh[STABGPU_MAX_LEVELS];
+    if (w < 1 || h < 1 || max_levels < 1) return 0;
+    const int L = level_dims(w, h, max_levels, lw, lh);
+    size_t t = 0;
+    for (int l = 0; l < L; ++l) t += (size_t)lw[l] * lh[l];
+    return t;
+}
+
+// ---- per-stage ABI ----------------------------------------------------
+
+int stabgpu_build_pyramid(stabgpu_ctx* ctx, const uint8_t* src, int w, int h, int max_levels,
+                          stabgpu_pyramid* out) {
+    TRY(validate_frame(w, h));
+    if (max_levels < 1) return set_err(STABGPU_INVALID_INPUT, "max_levels must be >= 1");
+    cudaSetDevice(ctx->device);
+    int lw[STABGPU_MAX_LEVELS], lh[STABGPU_MAX_LEVELS];
+    const int L = level_dims(w, h, max_levels, lw, lh);
+    const size_t total = stabgpu_pyramid_bytes(w, h, max_levels);
+    DBUF(uint8_t, d, "api_pyr", total);
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(d, src, (size_t)w * h, cudaMemcpyHostToDevice, st));
+    size_t off = 0;
+    out->levels = L;
+    for (int l = 0; l < L; ++l) {
+        out->width[l] = lw[l];
+        out->height[l] = lh[l];
+        out->offset[l] = off;
+        if (l > 0) {
+            launch_pyramid_level(d + out->offset[l - 1], 0, lw[l - 1], lh[l - 1], d + off, 0, 1, st);
+            ++ctx->stats.launches;
+        }
+        off += (size_t)lw[l] * lh[l];
+    }
+    TRY(check_launch("pyramid"));
+    CUDA_TRY(cudaMemcpyAsync(out->data, d, total, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_gradients(stabgpu_ctx* ctx, const uint8_t* src, int w, int h, double* gx, double* gy) {
+    TRY(validate_frame(w, h));
+    cudaSetDevice(ctx->device);
+    const size_t n = (size_t)w * h;
+    DBUF(uint8_t, d, "api_img", n);
+    DBUF(double, g, "api_grad", 2 * n);
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
+    launch_gradients(d, w, h, g, g + n, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("gradients"));
+    CUDA_TRY(cudaMemcpyAsync(gx, g, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(gy, g + n, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_min_eig_response(stabgpu_ctx* ctx, const uint8_t* src, int w, int h, int block,
+                             double* out) {
+    TRY(validate_frame(w, h));
+    if (block < 3 || block % 2 == 0)
+        return set_err(STABGPU_INVALID_CONFIG, "block_size must be odd and >= 3");
+    cudaSetDevice(ctx->device);
+    const size_t n = (size_t)w * h;
+    DBUF(uint8_t, d, "api_img", n);
+    DBUF(double, r, "api_resp", n);
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
+    launch_min_eig(d, w, h, block, r, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("min_eig"));
+    CUDA_TRY(cudaMemcpyAsync(out, r, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_detection_roi(int w, int h, double margin, stabgpu_roi* out) {
+    return roi_of(w, h, margin, out);
+}
+
+int stabgpu_detect_corners(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
+                           const stabgpu_detect_cfg* cfg, double* xy, double* score, int* n_out) {
+    *n_out = 0;
+    TRY(validate_frame(w, h));
+    TRY(validate_detect(*cfg));
+    stabgpu_roi roi;
+    TRY(roi_of(w, h, cfg->roi_margin, &roi));
+    cudaSetDevice(ctx->device);
+    const size_t n = (size_t)w * h, cap = (size_t)(roi.x1 - roi.x0) * (roi.y1 - roi.y0);
+    const int maxc = cfg->max_corners;
+    cudaStream_t st = ctx->stream;
+    DBUF(uint8_t, d, "api_img", n);
+    DBUF(unsigned long long, maxbits, "det_max", 1);
+    DBUF(unsigned int, dcount, "det_count", 1);
+    DBUF(unsigned long long, ckey, "det_ckey", cap);
+    DBUF(unsigned int, cidx, "det_cidx", cap);
+    DBUF(unsigned long long, skey, "det_skey", cap);
+    DBUF(unsigned int, sidx, "det_sidx", cap);
+    DBUF(double2, pts, "api_pts", maxc);
+    DBUF(double, sc, "api_score", maxc);
+    DBUF(int, nn, "api_n", 1);
+    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
+    DetectScratch ds{maxbits, dcount, nullptr, ckey, cidx, skey, sidx, cap};
+    PlaneBatch fb{d, n, w, h};
+    launch_detect(fb, 1, *cfg, roi, ds, pts, sc, nn, st);
+    ctx->stats.launches += 3;
+    TRY(check_launch("detect"));
+    int nc = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nc, nn, sizeof nc, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (nc > 0) {
+        CUDA_TRY(cudaMemcpyAsync(xy, pts, sizeof(double2) * nc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(score, sc, sizeof(double) * nc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    *n_out = nc;
+    return STABGPU_OK;
+}
+
+namespace {
+int check_pyramids(const stabgpu_pyramid* a, const stabgpu_pyramid* b) {  // flow.cpp:229-239
+    if (a->levels < 1 || b->levels < 1 || a->levels != b->levels)
+        return set_err(STABGPU_INVALID_INPUT, "pyramids must have matching level counts");
+    for (int i = 0; i < a->levels; ++i)
+        if (a->width[i] != b->width[i] || a->height[i] != b->height[i])
+            return set_err(STABGPU_INVALID_INPUT, "pyramid levels differ in size");
+    return STABGPU_OK;
+}
+
+// Uploads two host pyramids as a 2-frame batched DevPyramid.
+int upload_pair(stabgpu_ctx* ctx, const stabgpu_pyramid* a, const stabgpu_pyramid* b, DevPyramid* P) {
+    std::memset(P, 0, sizeof *P);
+    P->levels = a->levels;
+    cudaStream_t st = ctx->stream;
+    for (int l = 0; l < a->levels; ++l) {
+        P->w[l] = a->width[l];
+        P->h[l] = a->height[l];
+        P->stride[l] = (size_t)a->width[l] * a->height[l];
+        DBUF(uint8_t, d, ("api_pair" + std::to_string(l)).c_str(), 2 * P->stride[l]);
+        CUDA_TRY(cudaMemcpyAsync(d, a->data + a->offset[l], P->stride[l], cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(d + P->stride[l], b->data + b->offset[l], P->stride[l],
+                                 cudaMemcpyHostToDevice, st));
+        P->lvl[l] = d;
+    }
+    return STABGPU_OK;
+}
+
+int run_lk_api(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyramid* cur,
+               const double* pts, const double* ref, int n, const stabgpu_flow_cfg* cfg, int mode,
+               double* out_xy, uint8_t* ok) {
+    TRY(validate_flow(*cfg));
+    TRY(check_pyramids(prev, cur));
+    if (cfg->window_radius > STABGPU_MAX_RADIUS)
+        return set_err(STABGPU_INVALID_CONFIG, "window_radius above 31 is not supported");
+    if (n <= 0) return STABGPU_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DevPyramid P;
+    TRY(upload_pair(ctx, prev, cur, &P));
+    DBUF(double2, dp, "api_lk_pts", n);
+    DBUF(double2, dr, "api_lk_ref", n);
+    DBUF(double2, df, "api_lk_fwd", n);
+    DBUF(uint8_t, dk, "api_lk_keep", n);
+    DBUF(int, dn, "api_lk_n", 1);
+    CUDA_TRY(cudaMemcpyAsync(dp, pts, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    if (ref) CUDA_TRY(cudaMemcpyAsync(dr, ref, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dn, &n, sizeof n, cudaMemcpyHostToDevice, st));
+    LkStep s;
+    s.pyr = P;
+    s.frame0 = 0;
+    s.seg_len = 1;
+    s.t = 1;
+    s.nseg = 1;
+    s.max_pts = n;
+    s.pts = dp;
+    s.npts = dn;
+    s.fwd = df;
+    s.keep = dk;
+    s.iter_count = nullptr;
+    s.nframes = 2;
+    s.mode = mode;
+    s.ref = dr;
+    launch_lk(s, *cfg, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("track_lk"));
+    if (out_xy) CUDA_TRY(cudaMemcpyAsync(out_xy, df, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ok, dk, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+}  // namespace
+
+int stabgpu_track_lk(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyramid* cur,
+                     const double* xy, int n, const stabgpu_flow_cfg* cfg, double* out_xy,
+                     uint8_t* ok) {
+    const int rc = run_lk_api(ctx, prev, cur, xy, nullptr, n, cfg, 0, out_xy, ok);
+    if (rc == STABGPU_OK)  // failed points keep their input position (flow.cpp:162-164)
+        for (int i = 0; i < n; ++i)
+            if (!ok[i]) {
+                out_xy[2 * i] = xy[2 * i];
+                out_xy[2 * i + 1] = xy[2 * i + 1];
+            }
+    return rc;
+}
+
+int stabgpu_weed_tracks(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyramid* cur,
+                        const double* pxy, const double* cxy, int n, const stabgpu_flow_cfg* cfg,
+                        double* kp, double* kc, int* n_out) {
+    *n_out = 0;
+    if (n == 0) return STABGPU_OK;  // weed_tracks returns before track_lk (flow.cpp:264-266)
+    std::vector<uint8_t> keep(n);
+    TRY(run_lk_api(ctx, prev, cur, cxy, pxy, n, cfg, 2, nullptr, keep.data()));
+    int m = 0;
+    for (int i = 0; i < n; ++i)
+        if (keep[i]) {
+            kp[2 * m] = pxy[2 * i];
+            kp[2 * m + 1] = pxy[2 * i + 1];
+            kc[2 * m] = cxy[2 * i];
+            kc[2 * m + 1] = cxy[2 * i + 1];
+            ++m;
+        }
+    *n_out = m;
+    return STABGPU_OK;
+}
+
+namespace {
+int fit_api(stabgpu_ctx* ctx, const double* p, const double* q, int n, int kind,
+            const stabgpu_ransac_cfg* rc, int min_tracks, long long frame, stabgpu_transform* out,
+            uint8_t* inliers, int* n_used) {
+    if (n < 2) return set_err(STABGPU_DEGENERATE_INPUT, "estimation needs at least 2 point pairs");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(double2, dp, "api_fit_p", n);
+    DBUF(double2, dq, "api_fit_q", n);
+    DBUF(uint8_t, dm, "api_fit_m", n);
+    DBUF(FitResult, dr, "api_fit_r", 1);
+    CUDA_TRY(cudaMemcpyAsync(dp, p, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    stabgpu_ransac_cfg off{0, 0.0, 0};
+    launch_fit_single(dp, dq, n, kind, rc ? *rc : off, min_tracks, frame, dr, dm, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("fit"));
+    FitResult r;
+    CUDA_TRY(cudaMemcpyAsync(&r, dr, sizeof r, cudaMemcpyDeviceToHost, st));
+    if (inliers) CUDA_TRY(cudaMemcpyAsync(inliers, dm, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (r.status)
+        return set_err(r.status, "estimation failed: degenerate point set (coincident points or non-positive scale)");
+    out->tx = r.tx;
+    out->ty = r.ty;
+    out->theta = r.theta;
+    out->s = r.s;
+    out->kind = kind == STABGPU_RIGID ? STABGPU_RIGID : STABGPU_SIMILARITY;
+    if (n_used) *n_used = r.used;
+    return STABGPU_OK;
+}
+}  // namespace
+
+int stabgpu_estimate(stabgpu_ctx* ctx, const double* p, const double* q, int n, int kind,
+                     stabgpu_transform* out) {
+    return fit_api(ctx, p, q, n, kind, nullptr, 0, 0, out, nullptr, nullptr);
+}
+
+int stabgpu_ransac_estimate(stabgpu_ctx* ctx, const double* p, const double* q, int n, int kind,
+                            const stabgpu_ransac_cfg* rc, int min_tracks, int64_t frame,
+                            stabgpu_transform* out, uint8_t* inliers, int* n_inliers) {
+    if (rc && (rc->iterations < 0 || (rc->iterations > 0 && !(rc->threshold > 0.0))))
+        return set_err(STABGPU_INVALID_CONFIG, "ransac needs iterations >= 0 and threshold > 0");
+    return fit_api(ctx, p, q, n, kind, rc, min_tracks, frame, out, inliers, n_inliers);
+}
+
+int stabgpu_rms_residual(stabgpu_ctx* ctx, const double* p, const double* q, int n,
+                         const stabgpu_transform* t, double* out) {
+    if (n == 0) return set_err(STABGPU_DEGENERATE_INPUT, "rms_residual needs a non-empty track set");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(double2, dp, "api_fit_p", n);
+    DBUF(double2, dq, "api_fit_q", n);
+    DBUF(double, dr, "api_rms", 1);
+    CUDA_TRY(cudaMemcpyAsync(dp, p, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    launch_rms_single(dp, dq, n, *t, dr, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("rms"));
+    CUDA_TRY(cudaMemcpyAsync(out, dr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+void stabgpu_extract_delta(const stabgpu_transform* t, stabgpu_delta* d) {  // motion.cpp:92-101
+    d->dx = t->tx;
+    d->dy = t->ty;
+    d->da = t->theta;
+    d->dls = t->kind == STABGPU_RIGID ? 0.0 : std::log(t->s);
+    d->kind = t->kind;
+    d->skipped = 0;
+}
+
+void stabgpu_delta_to_transform(double dx, double dy, double da, double dls, stabgpu_transform* t) {
+    t->tx = dx;  // motion.cpp:103-111
+    t->ty = dy;
+    t->theta = da;
+    t->s = std::exp(dls);
+    t->kind = STABGPU_SIMILARITY;
+}
+
+int stabgpu_trajectory_corrections(stabgpu_ctx* ctx, const stabgpu_delta* deltas, int n, int radius,
+                                   stabgpu_transform* out) {
+    if (radius < 1) return set_err(STABGPU_INVALID_CONFIG, "smoothing radius must be >= 1");
+    if (n <= 0) return STABGPU_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(stabgpu_delta, dd, "api_deltas", n);
+    DBUF(double4, cum, "api_cum", n);
+    DBUF(stabgpu_frame_record, rec, "api_rec", n);
+    DBUF(FramePlan, plan, "api_plan", n);
+    CUDA_TRY(cudaMemcpyAsync(dd, deltas, sizeof(stabgpu_delta) * n, cudaMemcpyHostToDevice, st));
+    launch_prefix(dd, n, cum, st);
+    launch_plan_smooth(cum, n, true, 0, n, radius, rec, plan, st);
+    ctx->stats.launches += 2;
+    TRY(check_launch("trajectory"));
+    std::vector<stabgpu_frame_record> h(n);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i) out[i] = h[i].correction;
+    return STABGPU_OK;
+}
+
+int stabgpu_warp_similarity(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
+                            const stabgpu_transform* t, uint8_t* out) {
+    TRY(validate_frame(w, h));
+    TRY(validate_transform(*t));
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t n = (size_t)w * h;
+    DBUF(uint8_t, d, "api_img", n);
+    DBUF(uint8_t, o, "api_out", n);
+    DBUF(FramePlan, plan, "api_plan1", 1);
+    const FramePlan p = host_plan(*t);
+    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(plan, &p, sizeof p, cudaMemcpyHostToDevice, st));
+    launch_warp_only(d, w, h, plan, o, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("warp"));
+    CUDA_TRY(cudaMemcpyAsync(out, o, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_crop_resize(stabgpu_ctx* ctx, const uint8_t* src, int w, int h, double crop,
+                        uint8_t* out) {
+    TRY(validate_frame(w, h));
+    TRY(validate_crop(crop));
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t n = (size_t)w * h;
+    DBUF(uint8_t, d, "api_img", n);
+    DBUF(uint8_t, o, "api_out", n);
+    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
+    launch_crop_only(d, w, h, crop, o, st);
+    ++ctx->stats.launches;
+    TRY(check_launch("crop"));
+    CUDA_TRY(cudaMemcpyAsync(out, o, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_compose_stabilized(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb,
+                               const uint8_t* cr, int w, int h, int cw, int ch,
+                               const stabgpu_transform* t, double crop, uint8_t* oy, uint8_t* ocb,
+                               uint8_t* ocr) {
+    TRY(validate_frame(w, h));
+    TRY(validate_transform(*t));
+    TRY(validate_crop(crop));
+    const bool chroma = cb && cr;
+    if (chroma && (cw < 1 || ch < 1)) return set_err(STABGPU_INVALID_INPUT, "bad chroma geometry");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t n = (size_t)w * h, nc = chroma ? (size_t)cw * ch : 0;
+    DBUF(uint8_t, d, "api_cmp_in", n + 2 * nc);
+    DBUF(uint8_t, o, "api_cmp_out", n + 2 * nc);
+    DBUF(FramePlan, plan, "api_plan1", 1);
+    const FramePlan p = host_plan(*t);
+    CUDA_TRY(cudaMemcpyAsync(plan, &p, sizeof p, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d, y, n, cudaMemcpyHostToDevice, st));
+    if (chroma) {
+        CUDA_TRY(cudaMemcpyAsync(d + n, cb, nc, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(d + n + nc, cr, nc, cudaMemcpyHostToDevice, st));
+    }
+    PlaneBatch yb{d, n, w, h};
+    PlaneBatch bb{chroma ? d + n : nullptr, nc, cw, ch};
+    PlaneBatch rb{chroma ? d + n + nc : nullptr, nc, cw, ch};
+    launch_compose(yb, bb, rb, plan, 1, crop, o, chroma ? o + n : nullptr, chroma ? o + n + nc : nullptr, st);
+    ctx->stats.launches += chroma ? 2 : 1;
+    TRY(check_launch("compose"));
+    CUDA_TRY(cudaMemcpyAsync(oy, o, n, cudaMemcpyDeviceToHost, st));
+    if (chroma) {
+        CUDA_TRY(cudaMemcpyAsync(ocb, o + n, nc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(ocr, o + n + nc, nc, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+// ---- Stage I ------------------------------------------------------------
+
+int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb,
+                                      const uint8_t* cr, int n, int w, int h, int cw, int ch,
+                                      const stabgpu_config* cfgp, uint8_t* oy, uint8_t* ocb,
+                                      uint8_t* ocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(stabgpu_motion_record, motion, "seq_motion", n);
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps));
+    double t_ms[4] = {0, 0, 0, 0};
+    TRY(run_motion(ctx, y, 0, n - 1, w, h, cfg, motion, t_ms));
+    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
+    launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
+    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, st);
+    ctx->stats.launches += 2;
+    TRY(check_launch("plan"));
+    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
+    {
+        Timer tm(ctx, 4);  // events 8, 9
+        TRY(compose_range(ctx, y, cb, cr, 0, n, w, h, cw, ch, plan, cfg.crop_ratio, oy, ocb, ocr));
+    }
+    TRY(plan_error(ctx, ps));
+    if (records)
+        CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n,
+                                 cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (ctx->timing) {
+        float plan_ms = 0.f, comp_ms = 0.f;
+        cudaEventElapsedTime(&plan_ms, ctx->ev[10], ctx->ev[11]);
+        cudaEventElapsedTime(&comp_ms, ctx->ev[8], ctx->ev[9]);
+        ctx->stats.ms_pyramid = t_ms[0];
+        ctx->stats.ms_detect = t_ms[1];
+        ctx->stats.ms_track = t_ms[2];
+        ctx->stats.ms_fit = t_ms[3];
+        ctx->stats.ms_plan = plan_ms;
+        ctx->stats.ms_compose = comp_ms;
+        ctx->stats.ms_total = t_ms[0] + t_ms[1] + t_ms[2] + t_ms[3] + plan_ms + comp_ms;
+    }
+    return STABGPU_OK;
+}
+
+// Host buffers: chunked upload -> motion -> incremental plan -> compose ->
+// download, with the copies on two copy streams so upload, compute and
+// download of different chunks overlap (PCIe is full duplex).
+int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb,
+                               const uint8_t* hcr, int n, int w, int h, int cw, int ch,
+                               const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
+                               uint8_t* hocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const bool chroma = hcb && hcr && hocb && hocr;
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    DBUF(uint8_t, dy, "io_y", fl * n);
+    DBUF(uint8_t, doy, "io_oy", fl * n);
+    uint8_t *dcb = nullptr, *dcr = nullptr, *docb = nullptr, *docr = nullptr;
+    if (chroma) {
+        DBUF(uint8_t, a, "io_cb", fc * n);
+        DBUF(uint8_t, b, "io_cr", fc * n);
+        DBUF(uint8_t, c, "io_ocb", fc * n);
+        DBUF(uint8_t, d, "io_ocr", fc * n);
+        dcb = a;
+        dcr = b;
+        docb = c;
+        docr = d;
+    }
+    DBUF(stabgpu_motion_record, motion, "seq_motion", n);
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps));
+    const int R = cfg.flow.redetect_interval;
+    const int C = R * std::max(1, 60 / R);  // frames per upload chunk
+    const int nchunks = (n + C - 1) / C;
+    std::vector<cudaEvent_t> in_ev(nchunks), out_ev(nchunks + 1);
+    for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : out_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int rc = STABGPU_OK;
+    // uploads, all queued up front on the input copy stream
+    for (int k = 0; k < nchunks && !rc; ++k) {
+        const size_t f0 = (size_t)k * C, nf = std::min<size_t>(C, n - f0);
+        if (cudaMemcpyAsync(dy + f0 * fl, hy + f0 * fl, nf * fl, cudaMemcpyHostToDevice, ctx->cin) ||
+            (chroma && (cudaMemcpyAsync(dcb + f0 * fc, hcb + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin) ||
+                        cudaMemcpyAsync(dcr + f0 * fc, hcr + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin))))
+            rc = set_err(STABGPU_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+        cudaEventRecord(in_ev[k], ctx->cin);
+    }
+    long long seg_done = 0;   // segments whose motion is computed
+    long long known = 0;      // motion records known: frames [0, known)
+    long long composed = 0;   // frames composed and queued for download
+    const long long nseg_total = (n - 1 + R - 1) / R;
+    const int r = cfg.smooth_radius;
+    for (int k = 0; k < nchunks && !rc; ++k) {
+        cudaStreamWaitEvent(st, in_ev[k], 0);
+        const long long arrived = std::min<long long>((long long)(k + 1) * C, n);  // frames [0, arrived)
+        // segments [s*R, min((s+1)R, n-1)] whose last frame has arrived
+        long long seg_end = seg_done;
+        while (seg_end < nseg_total && std::min<long long>((seg_end + 1) * R, n - 1) < arrived) ++seg_end;
+        if (seg_end > seg_done) {
+            const long long first = seg_done * R;
+            const long long last = std::min<long long>(seg_end * R, n - 1);
+            rc = run_motion(ctx, dy + first * fl, first, (int)(last - first), w, h, cfg, motion, nullptr);
+            if (rc) break;
+            launch_plan_scan(motion, known, last + 1 - known, cfg, ps, rec, cum, st);
+            ++ctx->stats.launches;
+            known = last + 1;
+            seg_done = seg_end;
+        }
+        const bool complete = known == n;
+        const long long ready = complete ? n : std::max<long long>(0, known - r);
+        if (ready > composed) {
+            launch_plan_smooth(cum, known, complete, composed, ready - composed, r, rec, plan, st);
+            ++ctx->stats.launches;
+            rc = compose_range(ctx, dy, dcb, dcr, composed, ready - composed, w, h, cw, ch, plan,
+                               cfg.crop_ratio, doy, docb, docr);
+            if (rc) break;
+            cudaEventRecord(out_ev[k], st);
+            cudaStreamWaitEvent(ctx->cout, out_ev[k], 0);
+            const size_t f0 = composed, nf = ready - composed;
+            if (cudaMemcpyAsync(hoy + f0 * fl, doy + f0 * fl, nf * fl, cudaMemcpyDeviceToHost, ctx->cout) ||
+                (chroma && (cudaMemcpyAsync(hocb + f0 * fc, docb + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout) ||
+                            cudaMemcpyAsync(hocr + f0 * fc, docr + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout))))
+                rc = set_err(STABGPU_CUDA, "download failed: %s", cudaGetErrorString(cudaGetLastError()));
+            composed = ready;
+        }
+    }
+    if (!rc && composed != n) rc = set_err(STABGPU_CUDA, "internal: %lld of %d frames composed", composed, n);
+    cudaStreamSynchronize(ctx->cin);
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(ctx->cout);
+    for (auto& e : in_ev) cudaEventDestroy(e);
+    for (auto& e : out_ev) cudaEventDestroy(e);
+    if (rc) return rc;
+    TRY(plan_error(ctx, ps));
+    if (records)
+        CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return check_launch("stabilize_sequence");
+}
+
+// ---- multi-GPU split ------------------------------------------------------
+
+int stabgpu_motion_chunk(stabgpu_ctx* ctx, const uint8_t* dev_y, int64_t first, int count, int w,
+                         int h, const stabgpu_config* cfgp, stabgpu_motion_record* host_out) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    if (count < 0) return set_err(STABGPU_INVALID_INPUT, "negative frame count");
+    if (first % cfg.flow.redetect_interval != 0)
+        return set_err(STABGPU_SEQUENCING, "motion chunks must start on a re-detect frame");
+    cudaSetDevice(ctx->device);
+    DBUF(stabgpu_motion_record, motion, "chunk_motion", (size_t)count + 1);
+    // records are written at motion[first + k]; shift the base so index
+    // `first` lands on motion[0]
+    stabgpu_motion_record* base = motion - first;
+    if (first != 0) {
+        stabgpu_motion_record none;
+        std::memset(&none, 0, sizeof none);
+        none.frame_kind = -1;
+        CUDA_TRY(cudaMemcpyAsync(motion, &none, sizeof none, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    TRY(run_motion(ctx, dev_y, first, count, w, h, cfg, base, nullptr));
+    CUDA_TRY(cudaMemcpyAsync(host_out, motion, sizeof(stabgpu_motion_record) * ((size_t)count + 1),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return STABGPU_OK;
+}
+
+int stabgpu_plan_corrections(stabgpu_ctx* ctx, const stabgpu_motion_record* host_motion, int n,
+                             const stabgpu_config* cfgp, stabgpu_frame_record* host_records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_all(cfg));
+    if (n < 1) return set_err(STABGPU_INVALID_INPUT, "no motion records");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(stabgpu_motion_record, motion, "seq_motion", n);
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    CUDA_TRY(cudaMemcpyAsync(motion, host_motion, sizeof(stabgpu_motion_record) * n,
+                             cudaMemcpyHostToDevice, st));
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps));
+    launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
+    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, st);
+    ctx->stats.launches += 2;
+    TRY(check_launch("plan"));
+    TRY(plan_error(ctx, ps));
+    CUDA_TRY(cudaMemcpyAsync(host_records, rec, sizeof(stabgpu_frame_record) * n,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                           int count, int w, int h, int cw, int ch,
+                           const stabgpu_transform* host_corr, double crop, uint8_t* oy,
+                           uint8_t* ocb, uint8_t* ocr) {
+    TRY(validate_frame(w, h));
+    TRY(validate_crop(crop));
+    if (count <= 0) return STABGPU_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DBUF(stabgpu_transform, corr, "cmp_corr", count);
+    DBUF(FramePlan, plan, "cmp_plan", count);
+    CUDA_TRY(cudaMemcpyAsync(corr, host_corr, sizeof(stabgpu_transform) * count,
+                             cudaMemcpyHostToDevice, st));
+    launch_plan_from_corrections(corr, count, plan, st);
+    ++ctx->stats.launches;
+    TRY(compose_range(ctx, y, cb, cr, 0, count, w, h, cw, ch, plan, crop, oy, ocb, ocr));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""Stage I (whole-sequence) stabilization: the run_offline semantics of the
+reference (pipeline.cpp:182-235) as batched B200 work, on one GPU or sharded
+over the GPUs of one box.
+
+Sharding: tracking state resets at every re-detect frame
+(flow.cpp:326-330), so segments [sR, (s+1)R] are independent.  Rank g owns a
+contiguous run of segments, needs one halo frame at its end, and produces the
+motion records of its frames.  The small records (~100 B/frame) are
+all-gathered (NCCL over NVLink on GPUs, gloo in the CPU tests); every rank
+then runs the sequential selector/trajectory/smoothing scan on identical
+input — bit-identical corrections everywhere — and composes its own frames.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._lib import check, context, load
+from .stab import StabConfig
+
+MOTION_BYTES = C.sizeof(_abi.MotionRecord)
+RECORD_BYTES = C.sizeof(_abi.FrameRecord)
+
+# numpy views of the C records
+DELTA_DT = np.dtype([("dx", "f8"), ("dy", "f8"), ("da", "f8"), ("dls", "f8"), ("kind", "i4"),
+                     ("skipped", "i4")])
+TRANSFORM_DT = np.dtype([("tx", "f8"), ("ty", "f8"), ("theta", "f8"), ("s", "f8"), ("kind", "i4"),
+                         ("pad", "i4")])
+RECORD_DT = np.dtype([("delta", DELTA_DT), ("correction", TRANSFORM_DT), ("frame_kind", "i4"),
+                      ("n_tracks", "i4"), ("n_inliers", "i4"), ("decision", "i4")])
+MOTION_DT = np.dtype([("rigid", DELTA_DT), ("similarity", DELTA_DT), ("e_rigid", "f8"),
+                      ("e_similarity", "f8"), ("frame_kind", "i4"), ("n_tracks", "i4"),
+                      ("n_inliers_rigid", "i4"), ("n_inliers_similarity", "i4"), ("status", "i4"),
+                      ("pad", "i4")])
+assert RECORD_DT.itemsize == RECORD_BYTES, (RECORD_DT.itemsize, RECORD_BYTES)
+assert MOTION_DT.itemsize == MOTION_BYTES, (MOTION_DT.itemsize, MOTION_BYTES)
+
+
+def _vp(x) -> C.c_void_p:
+    """Pointer of a numpy array or torch tensor (None -> NULL)."""
+    if x is None:
+        return C.c_void_p(0)
+    if isinstance(x, np.ndarray):
+        return C.c_void_p(x.ctypes.data)
+    return C.c_void_p(x.data_ptr())
+
+
+# ------------------------------------------------------------- one GPU ------
+def stabilize_sequence(y: np.ndarray, cfg: StabConfig, cb: np.ndarray | None = None,
+                       cr: np.ndarray | None = None, device: int = 0):
+    """Host planes in, host planes out (copies overlapped inside the call).
+
+    y: (n, h, w) uint8; cb/cr: (n, ch, cw) uint8 or None.
+    Returns (out_y, out_cb, out_cr, records) with records a RECORD_DT array."""
+    y = np.ascontiguousarray(y, np.uint8)
+    n, h, w = y.shape
+    oy = np.empty_like(y)
+    ocb = ocr = None
+    ch = cw = 0
+    if cb is not None:
+        cb = np.ascontiguousarray(cb, np.uint8)
+        cr = np.ascontiguousarray(cr, np.uint8)
+        _, ch, cw = cb.shape
+        ocb, ocr = np.empty_like(cb), np.empty_like(cr)
+    rec = np.zeros(n, RECORD_DT)
+    c = cfg.c()
+    check(load().stabgpu_stabilize_sequence(context(device).handle, _vp(y), _vp(cb), _vp(cr), n, w,
+                                            h, cw, ch, C.byref(c), _vp(oy), _vp(ocb), _vp(ocr),
+                                            _vp(rec)))
+    return oy, ocb, ocr, rec
+
+
+def stabilize_sequence_host_buffers(ctx, y, cb, cr, n, w, h, cw, ch, cfg_c, oy, ocb, ocr, rec):
+    """Raw C-ABI call on caller-owned (e.g. pinned torch) host buffers."""
+    check(load().stabgpu_stabilize_sequence(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, w, h, cw, ch,
+                                            C.byref(cfg_c), _vp(oy), _vp(ocb), _vp(ocr), _vp(rec)))
+
+
+def stabilize_sequence_device(y, cfg: StabConfig, cb=None, cr=None, out_y=None, out_cb=None,
+                              out_cr=None, device: int | None = None, records: bool = True):
+    """Device-resident planes (torch CUDA tensors) in and out."""
+    import torch
+
+    n, h, w = y.shape
+    dev = y.device.index if device is None else device
+    out_y = torch.empty_like(y) if out_y is None else out_y
+    ch = cw = 0
+    if cb is not None:
+        _, ch, cw = cb.shape
+        out_cb = torch.empty_like(cb) if out_cb is None else out_cb
+        out_cr = torch.empty_like(cr) if out_cr is None else out_cr
+    rec = np.zeros(n, RECORD_DT) if records else None
+    c = cfg.c()
+    ctx = context(dev)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    check(load().stabgpu_stabilize_sequence_device(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, w, h,
+                                                   cw, ch, C.byref(c), _vp(out_y), _vp(out_cb),
+                                                   _vp(out_cr), _vp(rec)))
+    return out_y, out_cb, out_cr, rec
+
+
+# ------------------------------------------------------------- sharding -----
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    first: int        # first frame (a re-detect frame) of the motion chunk
+    count: int        # frames first+1 .. first+count get motion records here
+    own_begin: int    # frames this rank composes: [own_begin, own_end)
+    own_end: int
+
+    @property
+    def frames_needed(self) -> tuple[int, int]:
+        """Resident frame range [lo, hi) (motion chunk incl. halo, own frames)."""
+        return min(self.first, self.own_begin), max(self.first + self.count + 1, self.own_end)
+
+
+def shard_ranges(n: int, redetect_interval: int, world: int) -> list[Shard]:
+    """Contiguous re-detect-aligned partition of an n-frame sequence."""
+    if n < 2:
+        raise ValueError("stabilization needs at least 2 frames")
+    R = redetect_interval
+    nseg = (n - 1 + R - 1) // R
+    out = []
+    for g in range(world):
+        s0, s1 = nseg * g // world, nseg * (g + 1) // world
+        first = min(s0 * R, n - 1)
+        last = min(s1 * R, n - 1)
+        own_begin = 0 if g == 0 else first + 1
+        own_end = last + 1
+        if s0 == s1:  # more ranks than segments: this rank idles
+            first, last, own_begin, own_end = 0, 0, 0, 0
+        out.append(Shard(g, first, last - first, own_begin, own_end))
+    return out
+
+
+def assemble_motion(n: int, parts: list[tuple[Shard, np.ndarray]]) -> np.ndarray:
+    """Global motion array from per-rank chunks.
+
+    Each part holds count+1 MOTION_DT records: entry 0 is frame `first`
+    (the FIRST record on rank 0, a placeholder elsewhere), entries 1..count
+    are frames first+1 .. first+count."""
+    motion = np.zeros(n, MOTION_DT)
+    seen = np.zeros(n, bool)
+    for sh, rec in parts:
+        if sh.count == 0 and sh.own_end == 0:
+            continue
+        if sh.first == 0:
+            motion[0] = rec[0]
+            seen[0] = True
+        motion[sh.first + 1: sh.first + sh.count + 1] = rec[1: sh.count + 1]
+        seen[sh.first + 1: sh.first + sh.count + 1] = True
+    if not seen.all():
+        raise RuntimeError(f"motion records missing for {int((~seen).sum())} frames")
+    return motion
+
+
+def exchange_motion(local: np.ndarray, max_count: int, group=None, device=None) -> list[np.ndarray]:
+    """All-gather of per-rank motion arrays (padded to max_count+1 records).
+
+    Uses NCCL device buffers when the process group is NCCL, else CPU."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    nbytes = (max_count + 1) * MOTION_BYTES
+    buf = np.zeros(nbytes, np.uint8)
+    raw = local.view(np.uint8)
+    buf[: raw.size] = raw
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", device) if backend == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(buf).to(dev)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t, group=group)
+    return [o.cpu().numpy().view(MOTION_DT) for o in outs]
+
+
+def motion_chunk(y_chunk, first: int, count: int, cfg: StabConfig, device: int = 0) -> np.ndarray:
+    """Motion records of frames first+1..first+count (device frames y_chunk
+    hold frames first..first+count)."""
+    import torch
+
+    _, h, w = y_chunk.shape
+    out = np.zeros(count + 1, MOTION_DT)
+    c = cfg.c()
+    ctx = context(device)
+    ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    check(load().stabgpu_motion_chunk(ctx.handle, _vp(y_chunk), first, count, w, h, C.byref(c),
+                                      _vp(out)))
+    return out
+
+
+def plan_corrections(motion: np.ndarray, cfg: StabConfig, device: int = 0) -> np.ndarray:
+    rec = np.zeros(len(motion), RECORD_DT)
+    c = cfg.c()
+    check(load().stabgpu_plan_corrections(context(device).handle, _vp(motion), len(motion),
+                                          C.byref(c), _vp(rec)))
+    return rec
+
+
+def compose_frames(y, corrections: np.ndarray, crop_ratio: float, cb=None, cr=None, out_y=None,
+                   out_cb=None, out_cr=None, device: int = 0):
+    import torch
+
+    n, h, w = y.shape
+    ch = cw = 0
+    if cb is not None:
+        _, ch, cw = cb.shape
+    corr = np.ascontiguousarray(corrections, TRANSFORM_DT)
+    out_y = torch.empty_like(y) if out_y is None else out_y
+    if cb is not None:
+        out_cb = torch.empty_like(cb) if out_cb is None else out_cb
+        out_cr = torch.empty_like(cr) if out_cr is None else out_cr
+    ctx = context(device)
+    ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    check(load().stabgpu_compose_frames(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, w, h, cw, ch,
+                                        _vp(corr), crop_ratio, _vp(out_y), _vp(out_cb),
+                                        _vp(out_cr)))
+    return out_y, out_cb, out_cr
+
+
+def stabilize_sharded(n: int, local_y, local_first: int, cfg: StabConfig, rank: int, world: int,
+                      local_cb=None, local_cr=None, group=None, device: int = 0):
+    """One rank of the sharded Stage I.  local_* hold frames
+    [local_first, local_first + len) covering shard.frames_needed.
+    Returns (out_y, out_cb, out_cr, records) for the rank's own frames."""
+    shards = shard_ranges(n, cfg.flow.redetect_interval, world)
+    sh = shards[rank]
+    max_count = max(s.count for s in shards)
+    if sh.count > 0:
+        lo = sh.first - local_first
+        mine = motion_chunk(local_y[lo: lo + sh.count + 1], sh.first, sh.count, cfg, device)
+    else:
+        mine = np.zeros(1, MOTION_DT)
+    gathered = exchange_motion(mine, max_count, group, device)
+    motion = assemble_motion(n, [(s, g) for s, g in zip(shards, gathered)])
+    rec = plan_corrections(motion, cfg, device)
+    a, b = sh.own_begin - local_first, sh.own_end - local_first
+    if b <= a:
+        return None, None, None, rec
+    corr = rec["correction"][sh.own_begin: sh.own_end]
+    oy, ob, orr = compose_frames(local_y[a:b], corr, cfg.crop_ratio,
+                                 None if local_cb is None else local_cb[a:b],
+                                 None if local_cr is None else local_cr[a:b], device=device)
+    return oy, ob, orr, rec

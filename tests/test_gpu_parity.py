@@ -1,0 +1,312 @@
+"""GPU (libstabgpu.so) vs the C oracle, stage by stage and end to end.
+
+Bars: integer/byte/index work bit-exact (pyramid, corner sets and scores,
+crop_resize, chroma, RANSAC inlier sets); floating-point LK / fits within
+north_star's tolerances (positions <= 0.01 px, transform parameters <= 1e-3)
+and, in practice, ~1e-9; warped luma within +-1 with the count of +-1 pixels
+bounded (the GPU evaluates the reference's row-incremental coordinate walk
+in closed form)."""
+import numpy as np
+import pytest
+
+from paper_1701_03572_b200 import _abi, pipeline, stab
+from paper_1701_03572_b200.stab import DetectConfig, FlowConfig, RansacConfig
+
+from . import _data, _oracle
+
+pytestmark = pytest.mark.gpu
+
+POS_TOL = 1e-6  # px; north_star allows 0.01
+PARAM_TOL = 1e-6  # north_star allows 1e-3
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return _oracle.oracle()
+
+
+FRAMES = [(_data.noise_frame(97, 61, 1), "noise97x61"), (_data.noise_frame(160, 120, 2), "noise160"),
+          (np.full((40, 50), 77, np.uint8), "flat"), (_data.video(frames=2)[0][1], "video")]
+
+
+@pytest.mark.parametrize("f,name", FRAMES)
+@pytest.mark.parametrize("levels", [1, 3, 6])
+def test_pyramid_bitexact(orc, f, name, levels):
+    g = stab.build_pyramid(f, levels)
+    _, ref = orc.build_pyramid(f, levels)
+    assert g.level_count() == len(ref)
+    for a, b in zip(g.levels, ref):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("f,name", FRAMES)
+def test_gradients_response_bitexact(orc, f, name):
+    gx, gy = stab.gradients(f)
+    ox, oy = orc.gradients(f)
+    assert np.array_equal(gx, ox) and np.array_equal(gy, oy)
+    for block in (3, 5, 7):
+        assert np.array_equal(stab.min_eig_response(f, block).view(np.uint64),
+                              orc.min_eig_response(f, block).view(np.uint64))
+
+
+@pytest.mark.parametrize("f,name", FRAMES)
+@pytest.mark.parametrize("corners,dist,block", [(8, 1.0, 3), (40, 5.0, 3), (200, 12.5, 3),
+                                                (60, 4.0, 5), (30, 7.0, 7)])
+def test_detect_bitexact(orc, f, name, corners, dist, block):
+    cfg = DetectConfig(max_corners=corners, min_distance=dist, block_size=block)
+    xg, sg = stab.detect_corners(f, cfg)
+    xo, so = orc.detect_corners(f, cfg)
+    assert np.array_equal(xg, xo)
+    assert np.array_equal(sg.view(np.uint64), so.view(np.uint64))
+
+
+def test_detect_many_ties(orc):
+    """Large plateaus of identical scores exercise the tie-heavy bucket path."""
+    f = np.zeros((300, 400), np.uint8)
+    f[::8, :] = 255
+    f[:, ::8] = 255
+    for corners, dist in ((5000, 1.0), (300, 3.0)):
+        cfg = DetectConfig(max_corners=corners, min_distance=dist)
+        xg, sg = stab.detect_corners(f, cfg)
+        xo, so = orc.detect_corners(f, cfg)
+        assert np.array_equal(xg, xo) and np.array_equal(sg, so)
+
+
+@pytest.mark.parametrize("w,h", [(1920, 1080), (640, 480)])
+def test_detect_full_size(orc, w, h):
+    y = _data.video(w, h, frames=1, tex=2048, blobs=1600)[0][0]
+    for cfg in (DetectConfig(max_corners=1000, min_distance=15.0),
+                DetectConfig(max_corners=200, min_distance=30.0)):
+        xg, sg = stab.detect_corners(y, cfg)
+        xo, so = orc.detect_corners(y, cfg)
+        assert np.array_equal(xg, xo) and np.array_equal(sg, so)
+
+
+def test_detect_errors():
+    f = _data.noise_frame(64, 64, 3)
+    for cfg in (DetectConfig(max_corners=4), DetectConfig(quality_level=1.0),
+                DetectConfig(min_distance=0.5), DetectConfig(block_size=4),
+                DetectConfig(roi_margin=0.45)):
+        with pytest.raises(stab.InvalidConfigError):
+            stab.detect_corners(f, cfg)
+    with pytest.raises(stab.InvalidInputError):
+        stab.detect_corners(np.zeros((10, 40), np.uint8), DetectConfig())
+    with pytest.raises(stab.InvalidConfigError):  # ROI < 32x32
+        stab.detect_corners(np.zeros((36, 36), np.uint8), DetectConfig())
+    xy, sc = stab.detect_corners(np.full((64, 64), 9, np.uint8), DetectConfig())
+    assert len(xy) == 0  # flat frame: empty, not an error
+
+
+@pytest.mark.parametrize("radius,levels,shift", [(10, 3, 4.0), (15, 5, 8.0), (3, 1, 1.0), (10, 4, 20.0)])
+def test_track_lk(orc, radius, levels, shift):
+    vid = _data.video(320, 240, frames=2, jit_t=shift, tex=512, blobs=200)[0]
+    cfg = FlowConfig(window_radius=radius, max_levels=levels)
+    pts, _ = orc.detect_corners(vid[0], DetectConfig(max_corners=150, min_distance=6.0))
+    rng = np.random.default_rng(5)
+    pts = np.concatenate([pts, rng.uniform(-3, 330, size=(30, 2))])
+    gp = [stab.build_pyramid(vid[i], levels) for i in range(2)]
+    op = [orc.build_pyramid(vid[i], levels)[0] for i in range(2)]
+    pg, okg = stab.track_lk(gp[0], gp[1], pts, cfg)
+    po, oko = orc.track_lk(op[0], op[1], pts, cfg)
+    assert np.array_equal(okg, oko)
+    assert np.abs(pg - po).max() <= POS_TOL
+    ts = stab.weed_tracks(gp[0], gp[1], pts[okg], pg[okg], cfg)
+    kp, kc = orc.weed_tracks(op[0], op[1], pts[oko], po[oko], cfg)
+    assert ts.size() == len(kp)
+    assert np.array_equal(ts.prev_points, kp)
+
+
+def test_track_identical_frames_exact_zero():
+    """test_flow.cpp:24-40: identical frames -> exactly zero flow."""
+    f = _data.video(200, 150, frames=1, tex=256)[0][0]
+    p = stab.build_pyramid(f, 3)
+    pts, _ = stab.detect_corners(f, DetectConfig(max_corners=40))
+    out, ok = stab.track_lk(p, p, pts, FlowConfig(max_levels=3))
+    assert ok.all() and np.array_equal(out, pts)
+
+
+def test_track_integer_shift():
+    """test_flow.cpp:42-62: a (5,3) shift is recovered within 0.2 px for >= 90%."""
+    f = _data.video(240, 180, frames=1, tex=256)[0][0]
+    g = _data.integer_shift(f, 5, 3)
+    pts, _ = stab.detect_corners(f, DetectConfig(max_corners=60, min_distance=8))
+    out, ok = stab.track_lk(stab.build_pyramid(f, 3), stab.build_pyramid(g, 3), pts, FlowConfig(max_levels=3))
+    err = np.hypot(out[:, 0] - pts[:, 0] - 5, out[:, 1] - pts[:, 1] - 3)
+    assert (ok & (err < 0.2)).mean() >= 0.9
+
+
+def _pairs(n, seed, outliers=0.0):
+    rng = np.random.default_rng(seed)
+    p = rng.uniform(0, 300, size=(n, 2))
+    th, s, t = 0.03, 1.02, np.array([4.0, -2.5])
+    R = s * np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+    q = p @ R.T + t + rng.normal(0, 0.3, size=(n, 2))
+    k = int(outliers * n)
+    q[:k] += rng.uniform(-40, 40, size=(k, 2))
+    return np.ascontiguousarray(p), np.ascontiguousarray(q)
+
+
+@pytest.mark.parametrize("kind", [_abi.RIGID, _abi.SIMILARITY])
+@pytest.mark.parametrize("n", [2, 3, 50, 1000])
+def test_estimate(orc, kind, n):
+    p, q = _pairs(n, n)
+    ts = stab.TrackSet(p, q)
+    g = stab.estimate_rigid(ts) if kind == _abi.RIGID else stab.estimate_similarity(ts)
+    _, o = orc.estimate(p, q, kind)
+    assert abs(g.tx - o.tx) < PARAM_TOL and abs(g.ty - o.ty) < PARAM_TOL
+    assert abs(g.theta - o.theta) < 1e-12 and abs(g.s - o.s) < 1e-12 and g.kind == o.kind
+    assert abs(stab.rms_residual(ts, g) - orc.rms_residual(p, q, o)) < 1e-9
+
+
+def test_estimate_degenerate():
+    with pytest.raises(stab.DegenerateInputError):
+        stab.estimate_similarity(stab.TrackSet(np.zeros((5, 2)), np.ones((5, 2))))
+    with pytest.raises(stab.DegenerateInputError):
+        stab.estimate_rigid(stab.TrackSet(np.zeros((1, 2)), np.ones((1, 2))))
+
+
+@pytest.mark.parametrize("kind", [_abi.RIGID, _abi.SIMILARITY])
+@pytest.mark.parametrize("iters,outl", [(0, 0.3), (50, 0.0), (500, 0.3), (1000, 0.7)])
+def test_ransac_inliers_bitexact(orc, kind, iters, outl):
+    p, q = _pairs(700, 11, outl)
+    cfg = RansacConfig(iterations=iters, threshold=3.0, seed=1234)
+    t, mask = stab.ransac_estimate(stab.TrackSet(p, q), kind, cfg, 8, 17)
+    _, to, mo, _ = orc.ransac(p, q, kind, cfg, 8, 17)
+    assert np.array_equal(mask, mo)
+    assert abs(t.tx - to.tx) < PARAM_TOL and abs(t.theta - to.theta) < 1e-12
+
+
+def test_trajectory(orc):
+    rng = np.random.default_rng(3)
+    d = rng.normal(0, 1, size=(257, 4)) * [2, 2, 0.01, 0.005]
+    for radius in (1, 5, 30):
+        g = stab.trajectory_corrections(d, radius)
+        o = orc.trajectory_corrections(d, radius)
+        assert np.array_equal(g[:, :3], o[:, :3])  # sequential sums: bit-exact
+        assert np.abs(g[:, 3] - o[:, 3]).max() <= 2e-16  # exp(): device vs glibc ulp
+
+
+def _offby(a, b):
+    d = np.abs(a.astype(int) - b.astype(int))
+    return int(d.max()), int((d > 0).sum())
+
+
+@pytest.mark.parametrize("t", [(0, 0, 0, 1), (3.0, -2.0, 0.0, 1.0), (2.3, 1.7, 0.02, 1.0),
+                               (-5.5, 4.25, -0.05, 1.03), (0.5, 0.5, 0.3, 0.9)])
+def test_warp_crop_compose(orc, t):
+    y = _data.noise_frame(330, 190, 4)
+    cb = _data.noise_frame(330, 190, 5)
+    cr = _data.noise_frame(165, 95, 6)
+    tt = _abi.Transform(t[0], t[1], t[2], t[3], _abi.SIMILARITY)
+    T = stab.SimilarityTransform(*t, kind=_abi.SIMILARITY)
+    mx, cnt = _offby(stab.warp_similarity(y, T), orc.warp_similarity(y, tt))
+    assert mx <= 1 and cnt <= 4
+    for crop in (0.0, 0.04, 0.2):
+        assert np.array_equal(stab.crop_resize(y, crop), orc.crop_resize(y, crop))
+        gy, gb, gr = stab.compose_stabilized(y, T, crop, cb, cb)
+        oy, ob, orr = orc.compose(y, cb, cb, tt, crop)
+        mx, cnt = _offby(gy, oy)
+        assert mx <= 1 and cnt <= 8
+        assert np.array_equal(gb, ob) and np.array_equal(gr, orr)
+    gy, gb, gr = stab.compose_stabilized(y, T, 0.04, cr, cr)
+    oy, ob, orr = orc.compose(y, cr, cr, tt, 0.04)
+    assert np.array_equal(gb, ob)
+
+
+def test_identity_compose_equals_crop():
+    """test_pipeline.cpp:83-105: identity correction -> crop_resize(input)."""
+    y = _data.noise_frame(256, 144, 9)
+    I = stab.SimilarityTransform()
+    assert np.array_equal(stab.compose_stabilized(y, I, 0.04), stab.crop_resize(y, 0.04))
+    assert np.array_equal(stab.warp_similarity(y, I), y)
+
+
+def test_transform_errors():
+    y = _data.noise_frame(64, 64, 1)
+    with pytest.raises(stab.InvalidTransformError):
+        stab.warp_similarity(y, stab.SimilarityTransform(s=0.0))
+    with pytest.raises(stab.InvalidTransformError):
+        stab.warp_similarity(y, stab.SimilarityTransform(s=1.1, kind=_abi.RIGID))
+    with pytest.raises(stab.InvalidConfigError):
+        stab.crop_resize(y, 0.3)
+
+
+def _compare_records(g, o, tracked_tol=PARAM_TOL):
+    assert np.array_equal(g["frame_kind"], o["frame_kind"])
+    tr = o["frame_kind"] == _abi.FRAME_TRACKED
+    assert np.array_equal(g["n_tracks"][tr], o["n_tracks"][tr])
+    assert np.array_equal(g["n_inliers"], o["n_inliers"])
+    assert np.array_equal(g["decision"], o["decision"])
+    assert np.array_equal(g["delta"]["kind"], o["delta"]["kind"])
+    assert np.array_equal(g["delta"]["skipped"], o["delta"]["skipped"])
+    for k in ("dx", "dy", "da", "dls"):
+        assert np.abs(g["delta"][k] - o["delta"][k]).max() <= tracked_tol, k
+    for k in ("tx", "ty", "theta", "s"):
+        assert np.abs(g["correction"][k] - o["correction"][k]).max() <= tracked_tol, k
+
+
+@pytest.mark.parametrize("mode", ["rigid", "similarity", "hybrid"])
+@pytest.mark.parametrize("ransac", [0, 300])
+def test_sequence(orc, mode, ransac):
+    y, cb, cr = _data.video(frames=41, objects=2, jit_t=3.0, color=True)
+    cfg = _data.small_cfg(_data.MODES[mode], ransac=ransac)
+    gy, gb, gr, gr_rec = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    oy, ob, orr, o_rec = orc.stabilize_sequence(y, cfg, cb, cr)
+    _compare_records(gr_rec, o_rec)
+    mx, cnt = _offby(gy, oy)
+    assert mx <= 1 and cnt <= 0.0005 * gy.size
+    for a, b in ((gb, ob), (gr, orr)):
+        mx, cnt = _offby(a, b)
+        assert mx <= 1 and cnt <= 0.0005 * a.size
+
+
+def test_sequence_device_equals_host_path():
+    import torch
+    y, cb, cr = _data.video(frames=37, objects=1, color=True)
+    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    hy, hb, hr, hrec = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    dev = [torch.from_numpy(a).cuda() for a in (y, cb, cr)]
+    dy, db, dr, drec = pipeline.stabilize_sequence_device(dev[0], cfg, dev[1], dev[2])
+    torch.cuda.synchronize()
+    assert np.array_equal(dy.cpu().numpy(), hy) and np.array_equal(db.cpu().numpy(), hb)
+    assert np.array_equal(dr.cpu().numpy(), hr)
+    assert hrec.tobytes() == drec.tobytes()
+
+
+def test_sharded_equals_single():
+    """The per-rank split (motion chunks + gathered plan + own compose), run
+    for every rank in one process, reproduces the one-GPU run bitwise."""
+    import torch
+    y = _data.video(frames=53, objects=1)[0]
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=100)
+    dy = torch.from_numpy(y).cuda()
+    ref_y, _, _, ref_rec = pipeline.stabilize_sequence_device(dy, cfg)
+    for world in (2, 3, 4, 11):
+        shards = pipeline.shard_ranges(len(y), cfg.flow.redetect_interval, world)
+        parts = []
+        for sh in shards:
+            if sh.count:
+                parts.append((sh, pipeline.motion_chunk(dy[sh.first: sh.first + sh.count + 1], sh.first, sh.count, cfg)))
+            else:
+                parts.append((sh, np.zeros(1, pipeline.MOTION_DT)))
+        motion = pipeline.assemble_motion(len(y), parts)
+        rec = pipeline.plan_corrections(motion, cfg)
+        assert rec.tobytes() == ref_rec.tobytes()
+        out = torch.empty_like(dy)
+        for sh in shards:
+            if sh.own_end > sh.own_begin:
+                oy, _, _ = pipeline.compose_frames(dy[sh.own_begin: sh.own_end],
+                                                   rec["correction"][sh.own_begin: sh.own_end], cfg.crop_ratio)
+                out[sh.own_begin: sh.own_end] = oy
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_y)
+
+
+def test_sequence_errors():
+    y = _data.video(frames=12)[0]
+    cfg = _data.small_cfg()
+    cfg.smooth_radius = 40  # queue_capacity 64 < 2*40+4
+    with pytest.raises(stab.InvalidConfigError):
+        pipeline.stabilize_sequence(y, cfg)
+    with pytest.raises(stab.InvalidInputError):
+        pipeline.stabilize_sequence(y[:1], _data.small_cfg())
