@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) luma_kernel(PlaneBatch in, const FramePla
     if (y >= h) return;
     const int x = X0 + tx;
     uint8_t* row = dst + (size_t)y * w;
-    if (x + 3 < w && (w & 3) == 0) {
+    if (x + 3 < w && ((reinterpret_cast<uintptr_t>(row + x) & 3) == 0)) {
         __stcs(reinterpret_cast<unsigned*>(row + x),
                (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
     } else {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) chroma_kernel(PlaneBatch cb, PlaneBatch c
                 v = sample_bilinear(src, cw, ch, px, py);
             o[k] = round_u8(v);
         }
-        if (i0 + 3 < npx && (npx & 3) == 0) {
+        if (i0 + 3 < npx && ((reinterpret_cast<uintptr_t>(out + i0) & 3) == 0)) {
             __stcs(reinterpret_cast<unsigned*>(out + i0),
                    (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
         } else {

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) pyramid_level_kernel(const uint8_t* __res
     }
     uint8_t* d = dst + (size_t)blockIdx.z * dst_stride + (size_t)oy * ow;
     const int ox = ox0 + j4;
-    if (ox + 3 < ow && (ow & 3) == 0) {
+    if (ox + 3 < ow && ((reinterpret_cast<uintptr_t>(d + ox) & 3) == 0)) {
         *reinterpret_cast<uchar4*>(d + ox) = make_uchar4(o[0], o[1], o[2], o[3]);
     } else {
         for (int k = 0; k < 4; ++k)
