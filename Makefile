@@ -28,3 +28,10 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# test-only native helper (brute-force check of the exact walk emulation)
+build/libwalktest.so: tests/native/walk_test.c $(PKG)/csrc/walk.h
+	@mkdir -p build
+	gcc -O2 -ffp-contract=off -fPIC -shared -o $@ $< -lm
+
+all: build/libwalktest.so

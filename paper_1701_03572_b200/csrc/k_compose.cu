@@ -1,29 +1,47 @@
-// k_compose.cu — K8: fused inverse-similarity warp + crop/resize, batched
-// over frames, plus the single-pass chroma path.
+// k_compose.cu — K8: fused inverse-similarity warp + crop/resize of every
+// plane of a frame, batched over frames.  Bit-exact with the reference.
 //
 // Reference: sample_bilinear (image_ops.cpp:98-113), warp_similarity
 // (115-134), crop_resize (136-159), compose_plane (165-202),
 // compose_stabilized (206-219).
 //
-// Luma keeps the reference's two roundings: every output pixel is a bilinear
-// sample of the WARPED-AND-ROUNDED frame, so each CTA first re-creates the
-// warped uint8 pixels its 64x16 output tile reads (a <=66x18 tile in shared
-// memory, 4 source taps each) and then resamples them.  The warped frame
-// never touches HBM: one read of the source, one write of the output.
-// Warped coordinates use the reference's row start exactly and advance by
-// x*c instead of x sequential additions of c (image_ops.cpp:124-131); the two
-// differ by a few ulps, which can move a value across a .5 rounding tie, so
-// luma parity is +-1 (tests count such pixels).  crop_resize and the chroma
-// path evaluate per pixel in the reference itself and are bit-exact.
+// One CTA owns a 64x32 output tile of one frame and all of its planes:
+//   1. the tile's source footprint (inverse-mapped bounding box) of each
+//      plane is staged in shared memory with coalesced 32-bit loads;
+//   2. luma: the warped-and-rounded pixels W the crop stage reads (a <=66x34
+//      tile) are recreated in shared memory, then crop-resampled (the
+//      reference rounds twice, image_ops.cpp:209); chroma (4:4:4: same tile)
+//      is one inverse map per pixel, both planes sharing coordinates;
+//   3. the output tile is written with 16-byte streaming stores.
+// So HBM sees one read and one write per plane byte.
+//
+// Exactness without fp64 per pixel.  Coordinates are carried in 32.32 fixed
+// point (int64 adds), the bilinear blend in fp32.  Each decision the
+// reference takes — integer part of a coordinate, in-bounds test, lround of
+// the blended value — is taken on the fast path only when the fast value is
+// provably on the same side of the decision boundary (coordinate error
+// <= ~40 units of 2^-32 px against a 1024-unit guard; value error <= 1.5e-4
+// against a 2.5e-4 guard).  Otherwise the pixel is queued and recomputed
+// with the reference's own fp64 arithmetic — for luma including the
+// reference's sequential row walk (sx += c, image_ops.cpp:124-131), which
+// fl_walk (walk.h) reproduces bit for bit in closed form.  About 0.05% of
+// pixels take the exact path.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "walk.h"
 
 namespace stabgpu {
 
 namespace {
 
-constexpr int OTW = 64, OTH = 16;  // output tile
-constexpr int WTW = OTW + 8, WTH = OTH + 4;
+constexpr int TW = 64, TH = 32;          // output tile
+constexpr int NT = 256;                  // threads per CTA
+constexpr int WTW = 72, WTH = 36;        // warped-luma tile (<= 66 x 34 used)
+constexpr int SRC_W = 128, SRC_H = 80;   // staged source capacity per plane
+constexpr int QCAP = 1024;               // exact-path queue
+constexpr long long GUARD = 1024;        // fixed-point guard (units of 2^-32 px)
+constexpr float VGUARD = 2.5e-4f;        // blended-value guard (the fast error is <= 1.5e-4)
+constexpr double FIX = 4294967296.0;     // 2^32
 
 struct CropGeom {
     int mx, my;
@@ -40,123 +58,399 @@ __host__ __device__ inline CropGeom crop_geom(int w, int h, double crop) {
     return g;
 }
 
-// warp_similarity value of output pixel (u, v) (image_ops.cpp:123-131)
-__device__ __forceinline__ uint8_t warped(const uint8_t* __restrict__ src, int w, int h,
-                                          const FramePlan& p, int u, int v) {
-    const double rx = dadd(dmul(p.c, dsub(0.0, p.tx)), dmul(p.sn, dsub((double)v, p.ty)));
-    const double ry = dadd(dmul(-p.sn, dsub(0.0, p.tx)), dmul(p.c, dsub((double)v, p.ty)));
-    const double sx = dadd(rx, dmul((double)u, p.c));
-    const double sy = dsub(ry, dmul((double)u, p.sn));
-    return round_u8(sample_bilinear(src, w, h, sx, sy));
+struct Src {  // a plane as seen by the kernel: staged tile or the global frame
+    const uint8_t* p;
+    int pitch, x0, y0;
+};
+
+struct Smem {
+    uint8_t src[3][SRC_H * SRC_W];
+    uint8_t wt[WTH][WTW];
+    uint8_t out[3][TH][TW];
+    double cfx[TW], cfy[TH];      // luma crop fractions per column / row
+    float cfxf[TW], cfyf[TH];
+    int cx0[TW], cy0[TH];
+    long long sxf[WTH], syf[WTH]; // luma warp: fixed-point x/y of (u0, v) per W row
+    double rxw[WTH], ryw[WTH];    // luma warp row starts (exact reference values)
+    long long pxf[TH], pyf[TH];   // chroma: fixed-point source coords of (X0, y)
+    int bbox[3][4];               // staged footprint per plane
+    int staged[3];
+    int qn;
+    unsigned q[QCAP];
+};
+
+__device__ __forceinline__ float u8f(uint32_t b) { return (float)b; }
+
+// fast bilinear + lround; returns -1 when the rounding decision is not certain
+__device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
+                                           float fy) {
+    const float fa = u8f(a), fc = u8f(c);
+    const float top = fmaf(fx, u8f(b) - fa, fa);
+    const float bot = fmaf(fx, u8f(d) - fc, fc);
+    const float v = fmaf(fy, bot - top, top);
+    const float k = floorf(v);
+    const float fr = v - k;
+    if (fabsf(fr - 0.5f) < VGUARD) return -1;
+    return (int)k + (fr > 0.5f ? 1 : 0);
 }
 
-__global__ void __launch_bounds__(256) luma_kernel(PlaneBatch in, const FramePlan* __restrict__ plan,
-                                                   CropGeom g, uint8_t* __restrict__ out) {
-    __shared__ uint8_t wt[WTH][WTW];
-    const int w = in.w, h = in.h;
-    const int f = blockIdx.z;
-    const FramePlan p = plan[f];
-    const uint8_t* src = in.base + (size_t)f * in.stride;
-    uint8_t* dst = out + (size_t)f * in.stride;
-    const int X0 = blockIdx.x * OTW, Y0 = blockIdx.y * OTH;
-    const int tx = (threadIdx.x & 15) * 4, ty = threadIdx.x >> 4;
-    const bool identity = g.mx == 0 && g.my == 0;
-    const int y = Y0 + ty;
-    uint8_t o[4] = {0, 0, 0, 0};
-    if (identity) {  // crop_resize returns the warped frame (image_ops.cpp:143-145)
-        if (y < h)
-            for (int k = 0; k < 4; ++k)
-                if (X0 + tx + k < w) o[k] = warped(src, w, h, p, X0 + tx + k, y);
+__device__ __forceinline__ float frac_f(uint32_t f) {  // top 23 bits of a 0.32 fraction
+    return __uint_as_float(0x3F800000u | (f >> 9)) - 1.0f;
+}
+
+__device__ __forceinline__ bool near_int(uint32_t f) { return f < GUARD || f > 0xFFFFFFFFu - GUARD; }
+
+__device__ __forceinline__ uint8_t at(const Src& s, int x, int y) {
+    return s.p[(y - s.y0) * s.pitch + (x - s.x0)];
+}
+
+// Stages rows [y0, y1] x cols [x0, x1] of a plane (clipped by the caller).
+__device__ void stage(const uint8_t* __restrict__ g, int w, int x0, int y0, int x1, int y1,
+                      uint8_t* dst, int* bb, int* staged) {
+    const int xa = x0 & ~3;
+    const int nwords = ((x1 - xa) >> 2) + 1;
+    const int rows = y1 - y0 + 1;
+    const bool fits = nwords * 4 <= SRC_W && rows <= SRC_H && x1 >= x0 && y1 >= y0;
+    if (threadIdx.x == 0) {
+        bb[0] = xa;
+        bb[1] = y0;
+        *staged = fits;
+    }
+    if (!fits) return;
+    const bool aligned = ((w & 3) == 0) && ((reinterpret_cast<uintptr_t>(g) & 3) == 0) &&
+                         (xa + nwords * 4 <= w);
+    if (aligned) {
+        for (int i = threadIdx.x; i < rows * nwords; i += NT) {
+            const int r = i / nwords, c = i - r * nwords;
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(g + (size_t)(y0 + r) * w + xa) + c);
+            *reinterpret_cast<uint32_t*>(dst + r * SRC_W + 4 * c) = v;
+        }
     } else {
-        // warped pixels the tile samples: columns [u0, u1], rows [v0, v1]
-        const int xl = min(X0 + OTW - 1, w - 1), yl = min(Y0 + OTH - 1, h - 1);
-        const int u0 = (int)dadd((double)g.mx, dmul((double)X0, g.step_x));
-        const int v0 = (int)dadd((double)g.my, dmul((double)Y0, g.step_y));
-        const int u1 = min((int)dadd((double)g.mx, dmul((double)xl, g.step_x)) + 1, w - 1);
-        const int v1 = min((int)dadd((double)g.my, dmul((double)yl, g.step_y)) + 1, h - 1);
-        const int nu = u1 - u0 + 1, nv = v1 - v0 + 1;
-        for (int i = threadIdx.x; i < nu * nv; i += blockDim.x) {
+        const int cols = nwords * 4;
+        for (int i = threadIdx.x; i < rows * cols; i += NT) {
+            const int r = i / cols, c = i - r * cols;
+            const int x = min(xa + c, w - 1);
+            dst[r * SRC_W + c] = __ldg(g + (size_t)(y0 + r) * w + x);
+        }
+    }
+}
+
+__device__ __forceinline__ void push(Smem& S, unsigned item) {
+    const int k = atomicAdd(&S.qn, 1);
+    if (k < QCAP) S.q[k] = item;
+}
+
+// luma warp row start (image_ops.cpp:124-125), exact reference arithmetic
+__device__ __forceinline__ void row_start(const FramePlan& p, int v, double& rx, double& ry) {
+    rx = dadd(dmul(p.c, dsub(0.0, p.tx)), dmul(p.sn, dsub((double)v, p.ty)));
+    ry = dadd(dmul(-p.sn, dsub(0.0, p.tx)), dmul(p.c, dsub((double)v, p.ty)));
+}
+
+struct ChromaMap {  // compose_plane constants (image_ops.cpp:167-177)
+    double fxl, fyl;
+    bool crop;
+};
+
+// compose_plane source coordinates of chroma pixel (x, y), reference order
+__device__ __forceinline__ void chroma_coords(const FramePlan& p, const CropGeom& g,
+                                              const ChromaMap& m, int x, int y, double& px,
+                                              double& py) {
+    double lx = dsub(dmul(dadd((double)x, 0.5), m.fxl), 0.5);
+    double ly = dsub(dmul(dadd((double)y, 0.5), m.fyl), 0.5);
+    if (m.crop) {
+        lx = dadd((double)g.mx, dmul(lx, g.step_x));
+        ly = dadd((double)g.my, dmul(ly, g.step_y));
+    }
+    const double dx = dsub(lx, p.tx), dy = dsub(ly, p.ty);
+    const double qx = dadd(dmul(p.c, dx), dmul(p.sn, dy));
+    const double qy = dadd(dmul(-p.sn, dx), dmul(p.c, dy));
+    px = dsub(ddiv(dadd(qx, 0.5), m.fxl), 0.5);
+    py = dsub(ddiv(dadd(qy, 0.5), m.fyl), 0.5);
+}
+
+__device__ __forceinline__ uint8_t crop_exact(const Smem& S, int r, int c, int u0, int v0, int w,
+                                              int h) {
+    const int x0 = S.cx0[c], y0 = S.cy0[r];
+    const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+    const double a = S.wt[y0 - v0][x0 - u0], b = S.wt[y0 - v0][x1 - u0];
+    const double cc = S.wt[y1 - v0][x0 - u0], d = S.wt[y1 - v0][x1 - u0];
+    const double top = dadd(a, dmul(S.cfx[c], dsub(b, a)));
+    const double bot = dadd(cc, dmul(S.cfx[c], dsub(d, cc)));
+    return round_u8(dadd(top, dmul(S.cfy[r], dsub(bot, top))));
+}
+
+__device__ __forceinline__ void chroma_exact(const FramePlan& p, const CropGeom& g,
+                                             const ChromaMap& cm, const uint8_t* gcb,
+                                             const uint8_t* gcr, int cw, int ch, int x, int y,
+                                             uint8_t& ob, uint8_t& orr) {
+    double px, py;
+    chroma_coords(p, g, cm, x, y, px, py);
+    ob = orr = 128;
+    if (px >= 0.0 && py >= 0.0 && px <= (double)cw - 1.0 && py <= (double)ch - 1.0) {
+        ob = round_u8(sample_bilinear(gcb, cw, ch, px, py));
+        orr = round_u8(sample_bilinear(gcr, cw, ch, px, py));
+    }
+}
+
+template <bool LUMA, bool CHROMA>
+__global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB, PlaneBatch CR,
+                                                     const FramePlan* __restrict__ plan, CropGeom g,
+                                                     int tiles_x, uint8_t* __restrict__ oY,
+                                                     uint8_t* __restrict__ oCB,
+                                                     uint8_t* __restrict__ oCR) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const int f = blockIdx.y;
+    const FramePlan p = plan[f];
+    const int tid = threadIdx.x;
+    // tile in the output plane (luma plane when LUMA, chroma plane otherwise)
+    const int W = LUMA ? Y.w : CB.w, H = LUMA ? Y.h : CB.h;
+    const int X0 = (blockIdx.x % tiles_x) * TW, Y0 = (blockIdx.x / tiles_x) * TH;
+    const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
+    const bool identity = g.mx == 0 && g.my == 0;
+    if (tid == 0) S.qn = 0;
+
+    // ------------------------------------------------------------ setup
+    const int w = Y.w, h = Y.h;
+    const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
+    int u0 = 0, v0 = 0, nu = 0, nv = 0;
+    const long long CF = __double2ll_rn(dmul(p.c, FIX)), SNF = __double2ll_rn(dmul(p.sn, FIX));
+    if (LUMA) {
+        if (identity) {
+            u0 = X0;
+            v0 = Y0;
+            nu = nx;
+            nv = ny;
+        } else {
+            u0 = (int)dadd((double)g.mx, dmul((double)X0, g.step_x));
+            v0 = (int)dadd((double)g.my, dmul((double)Y0, g.step_y));
+            nu = min((int)dadd((double)g.mx, dmul((double)(X0 + nx - 1), g.step_x)) + 1, w - 1) - u0 + 1;
+            nv = min((int)dadd((double)g.my, dmul((double)(Y0 + ny - 1), g.step_y)) + 1, h - 1) - v0 + 1;
+            if (tid < nx) {
+                const double sx = dadd((double)g.mx, dmul((double)(X0 + tid), g.step_x));
+                S.cx0[tid] = (int)sx;
+                S.cfx[tid] = dsub(sx, (double)(int)sx);
+                S.cfxf[tid] = (float)S.cfx[tid];
+            }
+            if (tid >= 64 && tid < 64 + ny) {
+                const int r = tid - 64;
+                const double sy = dadd((double)g.my, dmul((double)(Y0 + r), g.step_y));
+                S.cy0[r] = (int)sy;
+                S.cfy[r] = dsub(sy, (double)(int)sy);
+                S.cfyf[r] = (float)S.cfy[r];
+            }
+        }
+        if (tid >= 128 && tid < 128 + nv) {  // W rows: exact row starts + fixed point at u0
+            const int r = tid - 128;
+            double rx, ry;
+            row_start(p, v0 + r, rx, ry);
+            S.rxw[r] = rx;
+            S.ryw[r] = ry;
+            S.sxf[r] = __double2ll_rn(dmul(dadd(rx, dmul((double)u0, p.c)), FIX));
+            S.syf[r] = __double2ll_rn(dmul(dsub(ry, dmul((double)u0, p.sn)), FIX));
+        }
+        if (tid == 0) {  // luma source footprint of the W tile
+            double xmn = 1e300, xmx = -1e300, ymn = 1e300, ymx = -1e300;
+            for (int k = 0; k < 4; ++k) {
+                const int u = u0 + ((k & 1) ? nu - 1 : 0), v = v0 + ((k & 2) ? nv - 1 : 0);
+                double rx, ry;
+                row_start(p, v, rx, ry);
+                const double sx = rx + u * p.c, sy = ry - u * p.sn;
+                xmn = fmin(xmn, sx);
+                xmx = fmax(xmx, sx);
+                ymn = fmin(ymn, sy);
+                ymx = fmax(ymx, sy);
+            }
+            S.bbox[0][0] = max(0, (int)floor(xmn) - 1);
+            S.bbox[0][1] = max(0, (int)floor(ymn) - 1);
+            S.bbox[0][2] = min(w - 1, (int)floor(xmx) + 2);
+            S.bbox[0][3] = min(h - 1, (int)floor(ymx) + 2);
+        }
+    }
+    const int cw = CB.w, ch = CB.h;
+    ChromaMap cm{0, 0, false};
+    long long KXX = 0, KYX = 0;
+    if (CHROMA) {
+        cm.fxl = (double)w / cw;
+        cm.fyl = (double)h / ch;
+        cm.crop = g.mx != 0 || g.my != 0;
+        // d(px)/dx and d(py)/dx of the affine chroma map
+        const double lxs = cm.crop ? dmul(cm.fxl, g.step_x) : cm.fxl;
+        KXX = __double2ll_rn(dmul(ddiv(dmul(p.c, lxs), cm.fxl), FIX));
+        KYX = __double2ll_rn(dmul(ddiv(dmul(-p.sn, lxs), cm.fyl), FIX));
+        if (tid >= 192 && tid < 192 + ny) {
+            const int r = tid - 192;
+            double px, py;
+            chroma_coords(p, g, cm, X0, Y0 + r, px, py);
+            S.pxf[r] = __double2ll_rn(dmul(px, FIX));
+            S.pyf[r] = __double2ll_rn(dmul(py, FIX));
+        }
+        if (tid == 32) {
+            double xmn = 1e300, xmx = -1e300, ymn = 1e300, ymx = -1e300;
+            for (int k = 0; k < 4; ++k) {
+                double px, py;
+                chroma_coords(p, g, cm, X0 + ((k & 1) ? nx - 1 : 0), Y0 + ((k & 2) ? ny - 1 : 0), px, py);
+                xmn = fmin(xmn, px);
+                xmx = fmax(xmx, px);
+                ymn = fmin(ymn, py);
+                ymx = fmax(ymx, py);
+            }
+            const int b0 = max(0, (int)floor(xmn) - 1), b1 = max(0, (int)floor(ymn) - 1);
+            const int b2 = min(cw - 1, (int)floor(xmx) + 2), b3 = min(ch - 1, (int)floor(ymx) + 2);
+            S.bbox[1][0] = S.bbox[2][0] = b0;
+            S.bbox[1][1] = S.bbox[2][1] = b1;
+            S.bbox[1][2] = S.bbox[2][2] = b2;
+            S.bbox[1][3] = S.bbox[2][3] = b3;
+        }
+    }
+    __syncthreads();
+    // ------------------------------------------------------------ staging
+    const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
+    const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
+    int bb[3][4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bb[k][j] = S.bbox[k][j];
+    __syncthreads();
+    if (LUMA) stage(gy, w, bb[0][0], bb[0][1], bb[0][2], bb[0][3], S.src[0], S.bbox[0], &S.staged[0]);
+    if (CHROMA) {
+        stage(gcb, cw, bb[1][0], bb[1][1], bb[1][2], bb[1][3], S.src[1], S.bbox[1], &S.staged[1]);
+        stage(gcr, cw, bb[2][0], bb[2][1], bb[2][2], bb[2][3], S.src[2], S.bbox[2], &S.staged[2]);
+    }
+    __syncthreads();
+    Src sy{gy, w, 0, 0}, sb{gcb, cw, 0, 0}, sr{gcr, cw, 0, 0};
+    if (LUMA && S.staged[0]) sy = Src{S.src[0], SRC_W, S.bbox[0][0], S.bbox[0][1]};
+    if (CHROMA && S.staged[1]) sb = Src{S.src[1], SRC_W, S.bbox[1][0], S.bbox[1][1]};
+    if (CHROMA && S.staged[2]) sr = Src{S.src[2], SRC_W, S.bbox[2][0], S.bbox[2][1]};
+
+    // ------------------------------------------------------------ luma W tile
+    if (LUMA) {
+        uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
+        const int wp = identity ? TW : WTW;
+        for (int i = tid; i < nu * nv; i += NT) {
             const int r = i / nu, c = i - r * nu;
-            wt[r][c] = warped(src, w, h, p, u0 + c, v0 + r);
+            const long long SX = S.sxf[r] + (long long)c * CF;
+            const long long SY = S.syf[r] - (long long)c * SNF;
+            const uint32_t fxs = (uint32_t)SX, fys = (uint32_t)SY;
+            const int ix = (int)(SX >> 32), iy = (int)(SY >> 32);
+            int val;
+            if (near_int(fxs) || near_int(fys)) {
+                val = -1;
+            } else if (ix < 0 || iy < 0 || ix > w - 2 || iy > h - 2) {
+                val = 0;  // outside [0, w-1] x [0, h-1] (image_ops.cpp:101-103)
+            } else {
+                val = blend_round(at(sy, ix, iy), at(sy, ix + 1, iy), at(sy, ix, iy + 1),
+                                  at(sy, ix + 1, iy + 1), frac_f(fxs), frac_f(fys));
+            }
+            if (val < 0) push(S, (unsigned)i);
+            else wdst[r * wp + c] = (uint8_t)val;
         }
         __syncthreads();
-        if (y < h) {
-            const double sy = dadd((double)g.my, dmul((double)y, g.step_y));
-            const int y0 = (int)sy, y1 = min(y0 + 1, h - 1);
-            const double fy = dsub(sy, (double)y0);
-            for (int k = 0; k < 4; ++k) {
-                const int x = X0 + tx + k;
-                if (x >= w) break;
-                // sample_bilinear on the warped tile (image_ops.cpp:98-113)
-                const double sx = dadd((double)g.mx, dmul((double)x, g.step_x));
-                if (!(sx >= 0.0 && sy >= 0.0 && sx <= (double)w - 1.0 && sy <= (double)h - 1.0)) {
-                    o[k] = 0;
-                    continue;
+        const int nq = S.qn;
+        if (nq <= QCAP) {
+            for (int k = tid; k < nq; k += NT) {  // exact reference path
+                const int i = (int)(S.q[k] & 0x3FFFFFFF), r = i / nu, c = i - r * nu;
+                const double sx = fl_walk(S.rxw[r], p.c, u0 + c);
+                const double syy = fl_walk(S.ryw[r], -p.sn, u0 + c);
+                wdst[r * wp + c] = round_u8(sample_bilinear(gy, w, h, sx, syy));
+            }
+        } else {  // overflow: every pixel exactly (never seen in practice)
+            for (int i = tid; i < nu * nv; i += NT) {
+                const int r = i / nu, c = i - r * nu;
+                wdst[r * wp + c] = round_u8(sample_bilinear(gy, w, h, fl_walk(S.rxw[r], p.c, u0 + c),
+                                                            fl_walk(S.ryw[r], -p.sn, u0 + c)));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) S.qn = 0;
+        __syncthreads();
+        // ---- crop_resize of the warped tile (image_ops.cpp:151-157)
+        if (!identity) {
+            for (int i = tid; i < nx * ny; i += NT) {
+                const int r = i / nx, c = i - r * nx;
+                const int x0 = S.cx0[c], y0 = S.cy0[r];
+                const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+                const uint8_t* w0 = &S.wt[y0 - v0][0];
+                const uint8_t* w1 = &S.wt[y1 - v0][0];
+                const int val = blend_round(w0[x0 - u0], w0[x1 - u0], w1[x0 - u0], w1[x1 - u0],
+                                            S.cfxf[c], S.cfyf[r]);
+                if (val < 0) push(S, (1u << 30) | (unsigned)i);
+                else S.out[0][r][c] = (uint8_t)val;
+            }
+        }
+    }
+    // ------------------------------------------------------------ chroma
+    if (CHROMA) {
+        for (int i = tid; i < nx * ny; i += NT) {
+            const int r = i / nx, c = i - r * nx;
+            const long long PX = S.pxf[r] + (long long)c * KXX;
+            const long long PY = S.pyf[r] + (long long)c * KYX;
+            const uint32_t fxs = (uint32_t)PX, fys = (uint32_t)PY;
+            const int ix = (int)(PX >> 32), iy = (int)(PY >> 32);
+            int vb, vr;
+            if (near_int(fxs) || near_int(fys)) {
+                vb = vr = -1;
+            } else if (ix < 0 || iy < 0 || ix > cw - 2 || iy > ch - 2) {
+                vb = vr = 128;  // unfilled chroma (image_ops.cpp:196-199)
+            } else {
+                const float fx = frac_f(fxs), fy = frac_f(fys);
+                vb = blend_round(at(sb, ix, iy), at(sb, ix + 1, iy), at(sb, ix, iy + 1),
+                                 at(sb, ix + 1, iy + 1), fx, fy);
+                vr = blend_round(at(sr, ix, iy), at(sr, ix + 1, iy), at(sr, ix, iy + 1),
+                                 at(sr, ix + 1, iy + 1), fx, fy);
+            }
+            if (vb < 0 || vr < 0) {
+                push(S, (2u << 30) | (unsigned)i);
+            } else {
+                S.out[1][r][c] = (uint8_t)vb;
+                S.out[2][r][c] = (uint8_t)vr;
+            }
+        }
+    }
+    __syncthreads();
+    {
+        const int nq = S.qn;
+        if (nq <= QCAP) {
+            for (int k = tid; k < nq; k += NT) {
+                const unsigned item = S.q[k];
+                const int kind = item >> 30, i = (int)(item & 0x3FFFFFFF);
+                const int r = i / nx, c = i - r * nx;
+                if (LUMA && kind == 1) {
+                    S.out[0][r][c] = crop_exact(S, r, c, u0, v0, w, h);
+                } else if (CHROMA && kind == 2) {
+                    chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
+                                 S.out[2][r][c]);
                 }
-                const int x0 = (int)sx, x1 = min(x0 + 1, w - 1);
-                const double fx = dsub(sx, (double)x0);
-                const double a = wt[y0 - v0][x0 - u0], b = wt[y0 - v0][x1 - u0];
-                const double c = wt[y1 - v0][x0 - u0], d = wt[y1 - v0][x1 - u0];
-                const double top = dadd(a, dmul(fx, dsub(b, a)));
-                const double bot = dadd(c, dmul(fx, dsub(d, c)));
-                o[k] = round_u8(dadd(top, dmul(fy, dsub(bot, top))));
+            }
+        } else {  // overflow: exact path for the whole tile
+            for (int i = tid; i < nx * ny; i += NT) {
+                const int r = i / nx, c = i - r * nx;
+                if (LUMA && !identity) S.out[0][r][c] = crop_exact(S, r, c, u0, v0, w, h);
+                if (CHROMA)
+                    chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
+                                 S.out[2][r][c]);
             }
         }
     }
-    if (y >= h) return;
-    const int x = X0 + tx;
-    uint8_t* row = dst + (size_t)y * w;
-    if (x + 3 < w && ((reinterpret_cast<uintptr_t>(row + x) & 3) == 0)) {
-        __stcs(reinterpret_cast<unsigned*>(row + x),
-               (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
-    } else {
-        for (int k = 0; k < 4; ++k)
-            if (x + k < w) row[x + k] = o[k];
-    }
-}
-
-// compose_plane (image_ops.cpp:165-202): crop in luma space, inverse warp,
-// sample the chroma plane, fill 128.  Both planes in one launch (grid.y).
-__global__ void __launch_bounds__(256) chroma_kernel(PlaneBatch cb, PlaneBatch cr,
-                                                     const FramePlan* __restrict__ plan, int lw,
-                                                     int lh, CropGeom g, uint8_t* __restrict__ ocb,
-                                                     uint8_t* __restrict__ ocr) {
-    const int cw = cb.w, ch = cb.h;
-    const int f = blockIdx.z;
-    const PlaneBatch& pb = blockIdx.y & 1 ? cr : cb;
-    uint8_t* out = (blockIdx.y & 1 ? ocr : ocb) + (size_t)f * pb.stride;
-    const uint8_t* src = pb.base + (size_t)f * pb.stride;
-    const FramePlan p = plan[f];
-    const double fx = (double)lw / cw, fy = (double)lh / ch;
-    const long long npx = (long long)cw * ch;
-    const long long stride = (long long)gridDim.x * blockDim.x * 4;
-    for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < npx; i0 += stride) {
-        uint8_t o[4];
-        for (int k = 0; k < 4; ++k) {
-            const long long i = i0 + k;
-            if (i >= npx) break;
-            const int y = (int)(i / cw), x = (int)(i - (long long)y * cw);
-            double lx = dsub(dmul(dadd((double)x, 0.5), fx), 0.5);
-            double ly = dsub(dmul(dadd((double)y, 0.5), fy), 0.5);
-            if (g.mx != 0 || g.my != 0) {
-                lx = dadd((double)g.mx, dmul(lx, g.step_x));
-                ly = dadd((double)g.my, dmul(ly, g.step_y));
+    __syncthreads();
+    // ------------------------------------------------------------ store
+    for (int k = (LUMA ? 0 : 1); k < (CHROMA ? 3 : 1); ++k) {
+        uint8_t* base = k == 0 ? oY + (size_t)f * Y.stride
+                               : (k == 1 ? oCB + (size_t)f * CB.stride : oCR + (size_t)f * CR.stride);
+        const int pw = k == 0 ? w : cw;
+        const bool vec = nx == TW && ((pw & 15) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
+        if (vec) {
+            for (int i = tid; i < ny * (TW / 16); i += NT) {
+                const int r = i / (TW / 16), c = (i % (TW / 16)) * 16;
+                const uint4 v = *reinterpret_cast<const uint4*>(&S.out[k][r][c]);
+                __stcs(reinterpret_cast<uint4*>(base + (size_t)(Y0 + r) * pw + X0 + c), v);
             }
-            const double dx = dsub(lx, p.tx), dy = dsub(ly, p.ty);
-            const double qx = dadd(dmul(p.c, dx), dmul(p.sn, dy));
-            const double qy = dadd(dmul(-p.sn, dx), dmul(p.c, dy));
-            const double px = dsub(ddiv(dadd(qx, 0.5), fx), 0.5);
-            const double py = dsub(ddiv(dadd(qy, 0.5), fy), 0.5);
-            double v = 128.0;
-            if (px >= 0.0 && py >= 0.0 && px <= (double)cw - 1.0 && py <= (double)ch - 1.0)
-                v = sample_bilinear(src, cw, ch, px, py);
-            o[k] = round_u8(v);
-        }
-        if (i0 + 3 < npx && ((reinterpret_cast<uintptr_t>(out + i0) & 3) == 0)) {
-            __stcs(reinterpret_cast<unsigned*>(out + i0),
-                   (unsigned)o[0] | ((unsigned)o[1] << 8) | ((unsigned)o[2] << 16) | ((unsigned)o[3] << 24));
         } else {
-            for (int k = 0; k < 4 && i0 + k < npx; ++k) out[i0 + k] = o[k];
+            for (int i = tid; i < nx * ny; i += NT) {
+                const int r = i / nx, c = i - r * nx;
+                base[(size_t)(Y0 + r) * pw + X0 + c] = S.out[k][r][c];
+            }
         }
     }
 }
@@ -174,11 +468,24 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
     out[(size_t)y * w + x] = round_u8(sample_bilinear(src, w, h, sx, sy));
 }
 
-__global__ void warp_kernel(const uint8_t* __restrict__ src, int w, int h,
-                            const FramePlan* __restrict__ plan, uint8_t* __restrict__ out) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-    if (x >= w) return;
-    out[(size_t)y * w + x] = warped(src, w, h, *plan, x, y);
+template <bool L, bool C>
+void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                  CropGeom g, uint8_t* oy, uint8_t* ocb, uint8_t* ocr, cudaStream_t st) {
+    const int W = L ? y.w : cb.w, H = L ? y.h : cb.h;
+    const int tx = (W + TW - 1) / TW, ty = (H + TH - 1) / TH;
+    const size_t smem = sizeof(Smem);
+    cudaFuncSetAttribute(compose_kernel<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int f0 = 0; f0 < frames; f0 += 65535) {
+        const int nf = min(65535, frames - f0);
+        PlaneBatch a = y, b = cb, c = cr;
+        if (a.base) a.base += (size_t)f0 * a.stride;
+        if (b.base) b.base += (size_t)f0 * b.stride;
+        if (c.base) c.base += (size_t)f0 * c.stride;
+        dim3 grid(tx * ty, nf);
+        compose_kernel<L, C><<<grid, NT, smem, st>>>(
+            a, b, c, plan + f0, g, tx, oy ? oy + (size_t)f0 * y.stride : nullptr,
+            ocb ? ocb + (size_t)f0 * cb.stride : nullptr, ocr ? ocr + (size_t)f0 * cr.stride : nullptr);
+    }
 }
 
 }  // namespace
@@ -188,31 +495,20 @@ void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan*
                     cudaStream_t st) {
     if (frames <= 0) return;
     const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
-    for (int f0 = 0; f0 < frames; f0 += 65535) {
-        const int nf = min(65535, frames - f0);
-        PlaneBatch yb = y;
-        yb.base += (size_t)f0 * y.stride;
-        dim3 grid((y.w + OTW - 1) / OTW, (y.h + OTH - 1) / OTH, nf);
-        luma_kernel<<<grid, 256, 0, st>>>(yb, plan + f0, g, out_y + (size_t)f0 * y.stride);
-        if (cb.base && cr.base && out_cb && out_cr) {
-            PlaneBatch b1 = cb, b2 = cr;
-            b1.base += (size_t)f0 * cb.stride;
-            b2.base += (size_t)f0 * cr.stride;
-            const long long npx = (long long)cb.w * cb.h;
-            const long long nb = (npx / 4 + 255) / 256;
-            const int bx = (int)(nb < 1024 ? nb : 1024);
-            dim3 g2(max(bx, 1), 2, nf);
-            chroma_kernel<<<g2, 256, 0, st>>>(b1, b2, plan + f0, y.w, y.h, g,
-                                              out_cb + (size_t)f0 * cb.stride,
-                                              out_cr + (size_t)f0 * cr.stride);
-        }
+    const bool chroma = cb.base && cr.base && out_cb && out_cr;
+    if (chroma && cb.w == y.w && cb.h == y.h) {
+        launch_tiles<true, true>(y, cb, cr, plan, frames, g, out_y, out_cb, out_cr, st);
+    } else {
+        launch_tiles<true, false>(y, cb, cr, plan, frames, g, out_y, nullptr, nullptr, st);
+        if (chroma) launch_tiles<false, true>(y, cb, cr, plan, frames, g, nullptr, out_cb, out_cr, st);
     }
 }
 
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st) {
-    dim3 grid((w + 127) / 128, h);
-    warp_kernel<<<grid, 128, 0, st>>>(src, w, h, plan, out);
+    // warp_similarity == compose with crop_ratio 0 (crop_resize returns its input)
+    PlaneBatch y{src, (size_t)w * h, w, h}, none{nullptr, 0, 0, 0};
+    launch_tiles<true, false>(y, none, none, plan, 1, crop_geom(w, h, 0.0), out, nullptr, nullptr, st);
 }
 
 void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,
