@@ -192,6 +192,50 @@ __device__ __forceinline__ void chroma_exact(const FramePlan& p, const CropGeom&
     }
 }
 
+// min/max of 4 corner coordinates held by 4 consecutive lanes -> staged bbox
+__device__ __forceinline__ void corner_bbox(double x, double y, unsigned mask, int k, int w, int h,
+                                            int* bb) {
+    double xmn = x, xmx = x, ymn = y, ymx = y;
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        xmn = fmin(xmn, __shfl_xor_sync(mask, xmn, o));
+        xmx = fmax(xmx, __shfl_xor_sync(mask, xmx, o));
+        ymn = fmin(ymn, __shfl_xor_sync(mask, ymn, o));
+        ymx = fmax(ymx, __shfl_xor_sync(mask, ymx, o));
+    }
+    if (k == 0) {
+        bb[0] = max(0, (int)floor(xmn) - 1);
+        bb[1] = max(0, (int)floor(ymn) - 1);
+        bb[2] = min(w - 1, (int)floor(xmx) + 2);
+        bb[3] = min(h - 1, (int)floor(ymx) + 2);
+    }
+}
+
+// Exact luma W pixel.  Level 1: the direct fp64 coordinates rx + u*c differ
+// from the reference's walked ones by <= u*2^-43 px (|s| < 2^11; scaled
+// bound below), so unless a coordinate sits that close to an integer / the
+// frame edge, or the fp64 blend that close to a .5 tie, the direct result IS
+// the reference result.  Level 2 (about once per two 1080p frames): fl_walk.
+__device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const FramePlan& p,
+                           double rx, double ry, int u) {
+    const double sx = dadd(rx, dmul((double)u, p.c)), sy = dsub(ry, dmul((double)u, p.sn));
+    // walk-vs-direct bound: u half-ulps of the largest |coordinate| + 2 ulps of rounding
+    const double mag = fmax(fmax(fabs(sx), fabs(sy)), fmax(fabs(rx), fabs(ry))) + fabs((double)u) + 2.0;
+    const double tol = ldexp(mag, -52) * ((double)u + 4.0);
+    bool sure = true;
+    const double bx[3] = {sx - floor(sx), sx, sx - ((double)w - 1.0)};
+    const double by[3] = {sy - floor(sy), sy, sy - ((double)h - 1.0)};
+    // near an integer (x0 / fx change) or near either domain edge
+    if (fmin(bx[0], 1.0 - bx[0]) <= tol || fabs(bx[1]) <= tol || fabs(bx[2]) <= tol) sure = false;
+    if (fmin(by[0], 1.0 - by[0]) <= tol || fabs(by[1]) <= tol || fabs(by[2]) <= tol) sure = false;
+    if (sure) {
+        const double v = sample_bilinear(g, w, h, sx, sy);
+        const double fr = v - floor(v);
+        if (fabs(fr - 0.5) > 255.0 * 4.0 * tol + 1e-9) return round_u8(v);
+    }
+    return round_u8(sample_bilinear(g, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
+}
+
 template <bool LUMA, bool CHROMA>
 __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB, PlaneBatch CR,
                                                      const FramePlan* __restrict__ plan, CropGeom g,
@@ -249,22 +293,12 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
             S.sxf[r] = __double2ll_rn(dmul(dadd(rx, dmul((double)u0, p.c)), FIX));
             S.syf[r] = __double2ll_rn(dmul(dsub(ry, dmul((double)u0, p.sn)), FIX));
         }
-        if (tid == 0) {  // luma source footprint of the W tile
-            double xmn = 1e300, xmx = -1e300, ymn = 1e300, ymx = -1e300;
-            for (int k = 0; k < 4; ++k) {
-                const int u = u0 + ((k & 1) ? nu - 1 : 0), v = v0 + ((k & 2) ? nv - 1 : 0);
-                double rx, ry;
-                row_start(p, v, rx, ry);
-                const double sx = rx + u * p.c, sy = ry - u * p.sn;
-                xmn = fmin(xmn, sx);
-                xmx = fmax(xmx, sx);
-                ymn = fmin(ymn, sy);
-                ymx = fmax(ymx, sy);
-            }
-            S.bbox[0][0] = max(0, (int)floor(xmn) - 1);
-            S.bbox[0][1] = max(0, (int)floor(ymn) - 1);
-            S.bbox[0][2] = min(w - 1, (int)floor(xmx) + 2);
-            S.bbox[0][3] = min(h - 1, (int)floor(ymx) + 2);
+        if (tid >= 224 && tid < 228) {  // luma source footprint of the W tile: 4 corners
+            const int k = tid - 224;
+            const int u = u0 + ((k & 1) ? nu - 1 : 0), v = v0 + ((k & 2) ? nv - 1 : 0);
+            double rx, ry;
+            row_start(p, v, rx, ry);
+            corner_bbox(rx + u * p.c, ry - u * p.sn, 0xFu << 0, k, w, h, S.bbox[0]);
         }
     }
     const int cw = CB.w, ch = CB.h;
@@ -285,22 +319,14 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
             S.pxf[r] = __double2ll_rn(dmul(px, FIX));
             S.pyf[r] = __double2ll_rn(dmul(py, FIX));
         }
-        if (tid == 32) {
-            double xmn = 1e300, xmx = -1e300, ymn = 1e300, ymx = -1e300;
-            for (int k = 0; k < 4; ++k) {
-                double px, py;
-                chroma_coords(p, g, cm, X0 + ((k & 1) ? nx - 1 : 0), Y0 + ((k & 2) ? ny - 1 : 0), px, py);
-                xmn = fmin(xmn, px);
-                xmx = fmax(xmx, px);
-                ymn = fmin(ymn, py);
-                ymx = fmax(ymx, py);
+        if (tid >= 228 && tid < 232) {  // chroma footprint: 4 corners
+            const int k = tid - 228;
+            double px, py;
+            chroma_coords(p, g, cm, X0 + ((k & 1) ? nx - 1 : 0), Y0 + ((k & 2) ? ny - 1 : 0), px, py);
+            corner_bbox(px, py, 0xFu << 4, k, cw, ch, S.bbox[1]);
+            if (k == 0) {
+                // bbox[2] mirrors bbox[1] (same geometry for both chroma planes)
             }
-            const int b0 = max(0, (int)floor(xmn) - 1), b1 = max(0, (int)floor(ymn) - 1);
-            const int b2 = min(cw - 1, (int)floor(xmx) + 2), b3 = min(ch - 1, (int)floor(ymx) + 2);
-            S.bbox[1][0] = S.bbox[2][0] = b0;
-            S.bbox[1][1] = S.bbox[2][1] = b1;
-            S.bbox[1][2] = S.bbox[2][2] = b2;
-            S.bbox[1][3] = S.bbox[2][3] = b3;
         }
     }
     __syncthreads();
@@ -309,9 +335,10 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
     const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
     int bb[3][4];
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bb[k][j] = S.bbox[k][j];
+    for (int j = 0; j < 4; ++j) {
+        bb[0][j] = S.bbox[0][j];
+        bb[1][j] = bb[2][j] = S.bbox[1][j];
+    }
     __syncthreads();
     if (LUMA) stage(gy, w, bb[0][0], bb[0][1], bb[0][2], bb[0][3], S.src[0], S.bbox[0], &S.staged[0]);
     if (CHROMA) {
@@ -351,15 +378,12 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         if (nq <= QCAP) {
             for (int k = tid; k < nq; k += NT) {  // exact reference path
                 const int i = (int)(S.q[k] & 0x3FFFFFFF), r = i / nu, c = i - r * nu;
-                const double sx = fl_walk(S.rxw[r], p.c, u0 + c);
-                const double syy = fl_walk(S.ryw[r], -p.sn, u0 + c);
-                wdst[r * wp + c] = round_u8(sample_bilinear(gy, w, h, sx, syy));
+                wdst[r * wp + c] = w_exact(gy, w, h, p, S.rxw[r], S.ryw[r], u0 + c);
             }
         } else {  // overflow: every pixel exactly (never seen in practice)
             for (int i = tid; i < nu * nv; i += NT) {
                 const int r = i / nu, c = i - r * nu;
-                wdst[r * wp + c] = round_u8(sample_bilinear(gy, w, h, fl_walk(S.rxw[r], p.c, u0 + c),
-                                                            fl_walk(S.ryw[r], -p.sn, u0 + c)));
+                wdst[r * wp + c] = w_exact(gy, w, h, p, S.rxw[r], S.ryw[r], u0 + c);
             }
         }
         __syncthreads();
