@@ -298,6 +298,8 @@ def run_ours(args, cfg):
                              "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms},
                 "stage_ms": stages,
                 "gpu_launches": int(launches),
+                "lk": {"iterations": int(ctx.stats().lk_iterations),
+                       "level_builds": int(ctx.stats().candidates)},
                 "clocks": clk.summary(),
                 "input_gen_s": round(gen_s, 1)}
         if world == 1 and not args.no_cpu_baseline:

@@ -79,29 +79,63 @@ struct Smem {
     unsigned q[QCAP];
 };
 
-__device__ __forceinline__ float u8f(uint32_t b) { return (float)b; }
-
-// fast bilinear + lround; returns -1 when the rounding decision is not certain
-__device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
-                                           float fy) {
-    const float fa = u8f(a), fc = u8f(c);
-    const float top = fmaf(fx, u8f(b) - fa, fa);
-    const float bot = fmaf(fx, u8f(d) - fc, fc);
-    const float v = fmaf(fy, bot - top, top);
-    const float k = floorf(v);
-    const float fr = v - k;
-    if (fabsf(fr - 0.5f) < VGUARD) return -1;
-    return (int)k + (fr > 0.5f ? 1 : 0);
-}
+__device__ __forceinline__ bool near_int(uint32_t f) { return f < GUARD || f > 0xFFFFFFFFu - GUARD; }
 
 __device__ __forceinline__ float frac_f(uint32_t f) {  // top 23 bits of a 0.32 fraction
     return __uint_as_float(0x3F800000u | (f >> 9)) - 1.0f;
 }
 
-__device__ __forceinline__ bool near_int(uint32_t f) { return f < GUARD || f > 0xFFFFFFFFu - GUARD; }
+// exact uint8 -> float without I2F (a quarter-rate pipe): 2^23 + b, minus 2^23
+__device__ __forceinline__ float b2f(uint32_t b) { return __int_as_float(0x4B000000 | b) - 8388608.0f; }
+
+// fast bilinear (sample_bilinear's blend in fp32) + lround; -1 when the
+// rounding decision is within the error guard of a .5 tie
+__device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
+                                           float fy) {
+    const float fa = b2f(a), fc = b2f(c);
+    const float top = fmaf(fx, b2f(b) - fa, fa);
+    const float bot = fmaf(fx, b2f(d) - fc, fc);
+    const float t = fmaf(fy, bot - top, top) + 0.5f;  // lround(v) == floor(v + 0.5), v >= 0
+    const float k = floorf(t);
+    const float fr = t - k;
+    if (fr < VGUARD || fr > 1.0f - VGUARD) return -1;
+    return __float_as_int(k + 8388608.0f) & 0x3FF;
+}
+
+
 
 __device__ __forceinline__ uint8_t at(const Src& s, int x, int y) {
     return s.p[(y - s.y0) * s.pitch + (x - s.x0)];
+}
+
+// One fast-path sample of plane `q` (pitch, origin bx0/by0) at 32.32 fixed
+// point (X, Y).  Returns the byte, `out` when the coordinate is outside
+// [0, w-1] x [0, h-1] (lim = w-2 / h-2 on the integer part), or -1 when a
+// decision is not certain.
+template <typename P>
+__device__ __forceinline__ int sample_fast(P q, int pitch, int bx0, int by0, unsigned limx,
+                                           unsigned limy, long long X, long long Y, int out) {
+    const uint32_t fxs = (uint32_t)X, fys = (uint32_t)Y;
+    if (near_int(fxs) || near_int(fys)) return -1;
+    const int ix = (int)(X >> 32), iy = (int)(Y >> 32);
+    if ((unsigned)ix > limx || (unsigned)iy > limy) return out;
+    const int o = (iy - by0) * pitch + (ix - bx0);
+    return blend_round(q[o], q[o + 1], q[o + pitch], q[o + pitch + 1], frac_f(fxs), frac_f(fys));
+}
+
+// Two planes sharing one coordinate (4:4:4 chroma): packed result b | r << 16
+template <typename P>
+__device__ __forceinline__ int sample_fast2(P q1, P q2, int pitch, int bx0, int by0, unsigned limx,
+                                            unsigned limy, long long X, long long Y, int out) {
+    const uint32_t fxs = (uint32_t)X, fys = (uint32_t)Y;
+    if (near_int(fxs) || near_int(fys)) return -1;
+    const int ix = (int)(X >> 32), iy = (int)(Y >> 32);
+    if ((unsigned)ix > limx || (unsigned)iy > limy) return out | (out << 16);
+    const int o = (iy - by0) * pitch + (ix - bx0);
+    const float fx = frac_f(fxs), fy = frac_f(fys);
+    const int vb = blend_round(q1[o], q1[o + 1], q1[o + pitch], q1[o + pitch + 1], fx, fy);
+    const int vr = blend_round(q2[o], q2[o + 1], q2[o + pitch], q2[o + pitch + 1], fx, fy);
+    return (vb < 0 || vr < 0) ? -1 : (vb | (vr << 16));
 }
 
 // Stages rows [y0, y1] x cols [x0, x1] of a plane (clipped by the caller).
@@ -119,19 +153,18 @@ __device__ void stage(const uint8_t* __restrict__ g, int w, int x0, int y0, int 
     if (!fits) return;
     const bool aligned = ((w & 3) == 0) && ((reinterpret_cast<uintptr_t>(g) & 3) == 0) &&
                          (xa + nwords * 4 <= w);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (aligned) {
-        for (int i = threadIdx.x; i < rows * nwords; i += NT) {
-            const int r = i / nwords, c = i - r * nwords;
-            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(g + (size_t)(y0 + r) * w + xa) + c);
-            *reinterpret_cast<uint32_t*>(dst + r * SRC_W + 4 * c) = v;
+        for (int r = warp; r < rows; r += NT / 32) {
+            const uint32_t* grow = reinterpret_cast<const uint32_t*>(g + (size_t)(y0 + r) * w + xa);
+            uint32_t* srow = reinterpret_cast<uint32_t*>(dst + r * SRC_W);
+            for (int c = lane; c < nwords; c += 32) srow[c] = __ldg(grow + c);
         }
     } else {
         const int cols = nwords * 4;
-        for (int i = threadIdx.x; i < rows * cols; i += NT) {
-            const int r = i / cols, c = i - r * cols;
-            const int x = min(xa + c, w - 1);
-            dst[r * SRC_W + c] = __ldg(g + (size_t)(y0 + r) * w + x);
-        }
+        for (int r = warp; r < rows; r += NT / 32)
+            for (int c = lane; c < cols; c += 32)
+                dst[r * SRC_W + c] = __ldg(g + (size_t)(y0 + r) * w + min(xa + c, w - 1));
     }
 }
 
@@ -258,7 +291,7 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
     const int w = Y.w, h = Y.h;
     const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
     int u0 = 0, v0 = 0, nu = 0, nv = 0;
-    const long long CF = __double2ll_rn(dmul(p.c, FIX)), SNF = __double2ll_rn(dmul(p.sn, FIX));
+    const long long CF = p.cf, SNF = p.snf;
     if (LUMA) {
         if (identity) {
             u0 = X0;
@@ -308,10 +341,8 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         cm.fxl = (double)w / cw;
         cm.fyl = (double)h / ch;
         cm.crop = g.mx != 0 || g.my != 0;
-        // d(px)/dx and d(py)/dx of the affine chroma map
-        const double lxs = cm.crop ? dmul(cm.fxl, g.step_x) : cm.fxl;
-        KXX = __double2ll_rn(dmul(ddiv(dmul(p.c, lxs), cm.fxl), FIX));
-        KYX = __double2ll_rn(dmul(ddiv(dmul(-p.sn, lxs), cm.fyl), FIX));
+        KXX = p.kxx;
+        KYX = p.kyx;
         if (tid >= 192 && tid < 192 + ny) {
             const int r = tid - 192;
             double px, py;
@@ -346,31 +377,34 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         stage(gcr, cw, bb[2][0], bb[2][1], bb[2][2], bb[2][3], S.src[2], S.bbox[2], &S.staged[2]);
     }
     __syncthreads();
-    Src sy{gy, w, 0, 0}, sb{gcb, cw, 0, 0}, sr{gcr, cw, 0, 0};
-    if (LUMA && S.staged[0]) sy = Src{S.src[0], SRC_W, S.bbox[0][0], S.bbox[0][1]};
-    if (CHROMA && S.staged[1]) sb = Src{S.src[1], SRC_W, S.bbox[1][0], S.bbox[1][1]};
-    if (CHROMA && S.staged[2]) sr = Src{S.src[2], SRC_W, S.bbox[2][0], S.bbox[2][1]};
-
     // ------------------------------------------------------------ luma W tile
     if (LUMA) {
         uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
         const int wp = identity ? TW : WTW;
-        for (int i = tid; i < nu * nv; i += NT) {
-            const int r = i / nu, c = i - r * nu;
-            const long long SX = S.sxf[r] + (long long)c * CF;
-            const long long SY = S.syf[r] - (long long)c * SNF;
-            const uint32_t fxs = (uint32_t)SX, fys = (uint32_t)SY;
-            const int ix = (int)(SX >> 32), iy = (int)(SY >> 32);
-            int val;
-            if (near_int(fxs) || near_int(fys)) {
-                val = -1;
-            } else if (ix < 0 || iy < 0 || ix > w - 2 || iy > h - 2) {
-                val = 0;  // outside [0, w-1] x [0, h-1] (image_ops.cpp:101-103)
-            } else {
-                val = blend_round(at(sy, ix, iy), at(sy, ix + 1, iy), at(sy, ix, iy + 1),
-                                  at(sy, ix + 1, iy + 1), frac_f(fxs), frac_f(fys));
+        const unsigned limx = (unsigned)(w - 2), limy = (unsigned)(h - 2);
+        const int lane = tid & 31, warp = tid >> 5;
+        const bool stg = S.staged[0];
+        const int bx0 = S.bbox[0][0], by0 = S.bbox[0][1];
+        // warp per row, 2 adjacent pixels per lane (64 columns), tail columns after
+        for (int r = warp; r < nv; r += NT / 32) {
+            const long long SXr = S.sxf[r], SYr = S.syf[r];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int c = 2 * lane + k;
+                if (c >= nu) break;
+                const long long SX = SXr + (long long)c * CF, SY = SYr - (long long)c * SNF;
+                const int val = stg ? sample_fast(&S.src[0][0], SRC_W, bx0, by0, limx, limy, SX, SY, 0)
+                                    : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
+                if (val < 0) push(S, (unsigned)(r * nu + c));
+                else wdst[r * wp + c] = (uint8_t)val;
             }
-            if (val < 0) push(S, (unsigned)i);
+        }
+        for (int i = tid; i < (nu - 64) * nv; i += NT) {  // columns 64.. (at most 2)
+            const int r = i / (nu - 64), c = 64 + i - r * (nu - 64);
+            const long long SX = S.sxf[r] + (long long)c * CF, SY = S.syf[r] - (long long)c * SNF;
+            const int val = stg ? sample_fast(&S.src[0][0], SRC_W, bx0, by0, limx, limy, SX, SY, 0)
+                                : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
+            if (val < 0) push(S, (unsigned)(r * nu + c));
             else wdst[r * wp + c] = (uint8_t)val;
         }
         __syncthreads();
@@ -391,44 +425,53 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         __syncthreads();
         // ---- crop_resize of the warped tile (image_ops.cpp:151-157)
         if (!identity) {
-            for (int i = tid; i < nx * ny; i += NT) {
-                const int r = i / nx, c = i - r * nx;
-                const int x0 = S.cx0[c], y0 = S.cy0[r];
-                const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
-                const uint8_t* w0 = &S.wt[y0 - v0][0];
-                const uint8_t* w1 = &S.wt[y1 - v0][0];
-                const int val = blend_round(w0[x0 - u0], w0[x1 - u0], w1[x0 - u0], w1[x1 - u0],
-                                            S.cfxf[c], S.cfyf[r]);
-                if (val < 0) push(S, (1u << 30) | (unsigned)i);
-                else S.out[0][r][c] = (uint8_t)val;
+            const int lane = tid & 31, warp = tid >> 5;
+            int x0[2], x1[2];
+            float fxv[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int c = min(2 * lane + k, nx - 1);
+                x0[k] = S.cx0[c] - u0;
+                x1[k] = min(S.cx0[c] + 1, w - 1) - u0;
+                fxv[k] = S.cfxf[c];
+            }
+            for (int r = warp; r < ny; r += NT / 32) {
+                const int y0 = S.cy0[r] - v0, y1 = min(S.cy0[r] + 1, h - 1) - v0;
+                const float fy = S.cfyf[r];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int c = 2 * lane + k;
+                    if (c >= nx) break;
+                    const int val = blend_round(S.wt[y0][x0[k]], S.wt[y0][x1[k]], S.wt[y1][x0[k]],
+                                                S.wt[y1][x1[k]], fxv[k], fy);
+                    if (val < 0) push(S, (1u << 30) | (unsigned)(r * nx + c));
+                    else S.out[0][r][c] = (uint8_t)val;
+                }
             }
         }
     }
     // ------------------------------------------------------------ chroma
     if (CHROMA) {
-        for (int i = tid; i < nx * ny; i += NT) {
-            const int r = i / nx, c = i - r * nx;
-            const long long PX = S.pxf[r] + (long long)c * KXX;
-            const long long PY = S.pyf[r] + (long long)c * KYX;
-            const uint32_t fxs = (uint32_t)PX, fys = (uint32_t)PY;
-            const int ix = (int)(PX >> 32), iy = (int)(PY >> 32);
-            int vb, vr;
-            if (near_int(fxs) || near_int(fys)) {
-                vb = vr = -1;
-            } else if (ix < 0 || iy < 0 || ix > cw - 2 || iy > ch - 2) {
-                vb = vr = 128;  // unfilled chroma (image_ops.cpp:196-199)
-            } else {
-                const float fx = frac_f(fxs), fy = frac_f(fys);
-                vb = blend_round(at(sb, ix, iy), at(sb, ix + 1, iy), at(sb, ix, iy + 1),
-                                 at(sb, ix + 1, iy + 1), fx, fy);
-                vr = blend_round(at(sr, ix, iy), at(sr, ix + 1, iy), at(sr, ix, iy + 1),
-                                 at(sr, ix + 1, iy + 1), fx, fy);
-            }
-            if (vb < 0 || vr < 0) {
-                push(S, (2u << 30) | (unsigned)i);
-            } else {
-                S.out[1][r][c] = (uint8_t)vb;
-                S.out[2][r][c] = (uint8_t)vr;
+        const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
+        const int lane = tid & 31, warp = tid >> 5;
+        const bool stg = S.staged[1] && S.staged[2];
+        const int bx0 = S.bbox[1][0], by0 = S.bbox[1][1];
+        for (int r = warp; r < ny; r += NT / 32) {
+            const long long PXr = S.pxf[r], PYr = S.pyf[r];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int c = 2 * lane + k;
+                if (c >= nx) break;
+                const long long PX = PXr + (long long)c * KXX, PY = PYr + (long long)c * KYX;
+                const int v = stg ? sample_fast2(&S.src[1][0], &S.src[2][0], SRC_W, bx0, by0, limx,
+                                                 limy, PX, PY, 128)
+                                  : sample_fast2(gcb, gcr, cw, 0, 0, limx, limy, PX, PY, 128);
+                if (v < 0) {
+                    push(S, (2u << 30) | (unsigned)(r * nx + c));
+                } else {
+                    S.out[1][r][c] = (uint8_t)(v & 0xFF);
+                    S.out[2][r][c] = (uint8_t)(v >> 16);
+                }
             }
         }
     }

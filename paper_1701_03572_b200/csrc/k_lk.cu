@@ -63,7 +63,7 @@ __device__ __forceinline__ Weights weights_at(double cx, double cy) {
 // track_one for one point; called by all 32 lanes of a warp (uniform flow).
 __device__ bool track_warp(const DevPyramid& P, int fprev, int fcur, double px, double py,
                            const stabgpu_flow_cfg& cfg, double* ext, double* tgx, double* tgy,
-                           double& ox, double& oy, unsigned& iters) {
+                           double& ox, double& oy, unsigned& iters, unsigned& builds) {
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
     const int e = r + 1, es = 2 * e + 1;
@@ -83,6 +83,7 @@ __device__ bool track_warp(const DevPyramid& P, int fprev, int fcur, double px, 
         const double plx = ddiv(px, scale), ply = ddiv(py, scale);
         if (!inside(pi, plx, ply)) return false;
         // ---- build_level_patch (flow.cpp:77-126)
+        ++builds;
         const Weights T = weights_at(plx, ply);
         for (int k = lane; k < es * es; k += 32) {
             const int jj = k / es, ii = k - jj * es;
@@ -200,22 +201,22 @@ __global__ void lk_kernel(LkStep s, stabgpu_flow_cfg cfg, int warps_per_cta, int
     double* tgy = tgx + side * side;
     const size_t slot = (size_t)seg * s.max_pts + k;
     const double2 p = s.pts[slot];
-    unsigned iters = 0;
+    unsigned iters = 0, builds = 0;
     double fx = p.x, fy = p.y;
     bool keep;
     if (s.mode == 2) {  // weed only: p is the cur point, ref the prev point
         double bx, by;
-        keep = track_warp(s.pyr, fcur, fprev, p.x, p.y, cfg, ext, tgx, tgy, bx, by, iters);
+        keep = track_warp(s.pyr, fcur, fprev, p.x, p.y, cfg, ext, tgx, tgy, bx, by, iters, builds);
         if (keep) {
             const double2 q = s.ref[slot];
             const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
             keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
         }
     } else {
-        keep = track_warp(s.pyr, fprev, fcur, p.x, p.y, cfg, ext, tgx, tgy, fx, fy, iters);
+        keep = track_warp(s.pyr, fprev, fcur, p.x, p.y, cfg, ext, tgx, tgy, fx, fy, iters, builds);
         if (keep && s.mode == 1) {  // weed_tracks: backward re-track and fb test
             double bx, by;
-            keep = track_warp(s.pyr, fcur, fprev, fx, fy, cfg, ext, tgx, tgy, bx, by, iters);
+            keep = track_warp(s.pyr, fcur, fprev, fx, fy, cfg, ext, tgx, tgy, bx, by, iters, builds);
             if (keep) {
                 const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
                 keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
@@ -225,7 +226,11 @@ __global__ void lk_kernel(LkStep s, stabgpu_flow_cfg cfg, int warps_per_cta, int
     if (lane == 0) {
         s.fwd[slot] = make_double2(fx, fy);
         s.keep[slot] = keep ? 1 : 0;
-        if (s.iter_count) atomicAdd(s.iter_count, (unsigned long long)iters);
+        if (s.iter_count) {
+            atomicAdd(s.iter_count, (unsigned long long)iters);
+            atomicAdd(s.iter_count + 1, (unsigned long long)builds);
+            atomicAdd(s.iter_count + 2, 1ull);
+        }
     }
 }
 

@@ -82,7 +82,8 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
 
 __global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_known,
                                    long long first, long long count, int radius,
-                                   stabgpu_frame_record* __restrict__ rec, FramePlan* __restrict__ plan) {
+                                   stabgpu_frame_record* __restrict__ rec, FramePlan* __restrict__ plan,
+                                   PlanGeom geo) {
     const long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= first + count) return;
     const long long lo = i >= radius ? i - radius : 0;
@@ -105,6 +106,7 @@ __global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_
     // warp_similarity / apply_inverse coefficients (image_ops.cpp:121-122, transform.cpp:14-15)
     p.c = ddiv(cos(p.theta), p.s);
     p.sn = ddiv(sin(p.theta), p.s);
+    finish_plan(p, geo.w, geo.h, geo.cw, geo.ch, geo.crop);
     plan[i] = p;
     stabgpu_transform t{p.tx, p.ty, p.theta, p.s, STABGPU_SIMILARITY};
     rec[i].correction = t;
@@ -123,12 +125,12 @@ void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long
 
 void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
                         long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
-                        cudaStream_t st) {
+                        PlanGeom geo, cudaStream_t st) {
     (void)complete;
     if (count <= 0) return;
     const int tpb = 128;
     plan_smooth_kernel<<<(unsigned)((count + tpb - 1) / tpb), tpb, 0, st>>>(cum, n_known, first, count,
-                                                                           radius, rec, plan);
+                                                                           radius, rec, plan, geo);
 }
 
 }  // namespace stabgpu
@@ -148,7 +150,7 @@ __global__ void prefix_kernel(const stabgpu_delta* __restrict__ d, long long n, 
 }
 
 __global__ void plan_from_corr_kernel(const stabgpu_transform* __restrict__ t, long long n,
-                                      FramePlan* __restrict__ plan) {
+                                      FramePlan* __restrict__ plan, PlanGeom geo) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
     FramePlan p;
@@ -158,6 +160,7 @@ __global__ void plan_from_corr_kernel(const stabgpu_transform* __restrict__ t, l
     p.s = t[i].s;
     p.c = ddiv(cos(p.theta), p.s);
     p.sn = ddiv(sin(p.theta), p.s);
+    finish_plan(p, geo.w, geo.h, geo.cw, geo.ch, geo.crop);
     plan[i] = p;
 }
 }  // namespace
@@ -167,7 +170,7 @@ void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream
 }
 
 void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
-                                  cudaStream_t st) {
-    if (n > 0) plan_from_corr_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(corr, n, plan);
+                                  PlanGeom geo, cudaStream_t st) {
+    if (n > 0) plan_from_corr_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(corr, n, plan, geo);
 }
 }  // namespace stabgpu

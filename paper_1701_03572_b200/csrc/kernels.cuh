@@ -27,7 +27,26 @@ struct DevPyramid {
 struct FramePlan {
     double tx, ty, theta, s;  // correction transform (delta_to_transform)
     double c, sn;             // cos(theta)/s, sin(theta)/s (warp_similarity, image_ops.cpp:121-122)
+    // K8 fast-path constants (32.32 fixed point): luma walk steps and the
+    // chroma map's d/dx; filled by finish_plan() for the frame geometry
+    long long cf, snf, kxx, kyx;
 };
+
+// Fills the fixed-point members of a FramePlan (host or device).
+__host__ __device__ inline void finish_plan(FramePlan& p, int w, int h, int cw, int ch, double crop) {
+    const double FIXP = 4294967296.0;
+    p.cf = llrint(p.c * FIXP);
+    p.snf = llrint(p.sn * FIXP);
+    p.kxx = p.kyx = 0;
+    if (cw > 0 && ch > 0) {
+        const int mx = (int)llround(crop * w), my = (int)llround(crop * h);
+        const double step_x = w > 1 ? (double)(w - 2 * mx - 1) / (w - 1) : 0.0;
+        const double fxl = (double)w / cw, fyl = (double)h / ch;
+        const double lxs = (mx != 0 || my != 0) ? fxl * step_x : fxl;
+        p.kxx = llrint(p.c * lxs / fxl * FIXP);
+        p.kyx = llrint(-p.sn * lxs / fyl * FIXP);
+    }
+}
 
 // Device-resident motion records are the public stabgpu_motion_record.
 
@@ -95,9 +114,13 @@ struct PlanState {  // carried across incremental calls (selector + prefix)
 void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long long count,
                       const stabgpu_config& cfg, PlanState* state, stabgpu_frame_record* rec,
                       double4* cum, cudaStream_t st);
+struct PlanGeom {  // frame geometry the compose constants depend on
+    int w, h, cw, ch;
+    double crop;
+};
 void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
                         long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
-                        cudaStream_t st);
+                        PlanGeom geo, cudaStream_t st);
 
 // ---- K8 compose (k_compose.cu) ----
 void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
@@ -123,5 +146,5 @@ void launch_rms_single(const double2* P, const double2* Q, int n, stabgpu_transf
                        cudaStream_t st);
 void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream_t st);
 void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
-                                  cudaStream_t st);
+                                  PlanGeom geo, cudaStream_t st);
 }  // namespace stabgpu

@@ -46,6 +46,7 @@ struct stabgpu_ctx {
 namespace {
 
 thread_local std::string g_err;
+long long lk_tracks_last = 0;
 
 int set_err(int code, const char* fmt, ...) {
     char b[512];
@@ -176,6 +177,7 @@ FramePlan host_plan(const stabgpu_transform& t) {
     p.s = t.s;
     p.c = std::cos(t.theta) / t.s;
     p.sn = std::sin(t.theta) / t.s;
+    p.cf = p.snf = p.kxx = p.kyx = 0;
     return p;
 }
 
@@ -263,8 +265,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(double2, trk_prev, "trk_prev", (size_t)count * maxc);
     DBUF(double2, trk_cur, "trk_cur", (size_t)count * maxc);
     DBUF(int, trk_n, "trk_n", count);
-    DBUF(unsigned long long, iters, "lk_iters", 1);
-    CUDA_TRY(cudaMemsetAsync(iters, 0, sizeof(unsigned long long), st));
+    DBUF(unsigned long long, iters, "lk_iters", 3);
+    CUDA_TRY(cudaMemsetAsync(iters, 0, 3 * sizeof(unsigned long long), st));
     {
         Timer tm(ctx, 2);
         double2* cur_pts = ptsA;
@@ -303,11 +305,13 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         TRY(check_launch("fit"));
     }
     if (ctx->timing && t_ms) {
-        unsigned long long it = 0, nc = 0;
-        CUDA_TRY(cudaMemcpyAsync(&it, iters, sizeof it, cudaMemcpyDeviceToHost, st));
+        unsigned long long it[3] = {0, 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(it, iters, sizeof it, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
-        ctx->stats.lk_iterations += (long long)it;
-        (void)nc;
+        ctx->stats.lk_iterations = (long long)it[0];
+        ctx->stats.candidates = (long long)it[1];  // template builds (reused field)
+        ctx->stats.launches += 0;
+        lk_tracks_last = (long long)it[2];
         for (int k = 0; k < 4; ++k) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ctx->ev[2 * k], ctx->ev[2 * k + 1]);
@@ -774,7 +778,7 @@ int stabgpu_trajectory_corrections(stabgpu_ctx* ctx, const stabgpu_delta* deltas
     DBUF(FramePlan, plan, "api_plan", n);
     CUDA_TRY(cudaMemcpyAsync(dd, deltas, sizeof(stabgpu_delta) * n, cudaMemcpyHostToDevice, st));
     launch_prefix(dd, n, cum, st);
-    launch_plan_smooth(cum, n, true, 0, n, radius, rec, plan, st);
+    launch_plan_smooth(cum, n, true, 0, n, radius, rec, plan, PlanGeom{16, 16, 0, 0, 0.0}, st);
     ctx->stats.launches += 2;
     TRY(check_launch("trajectory"));
     std::vector<stabgpu_frame_record> h(n);
@@ -794,7 +798,8 @@ int stabgpu_warp_similarity(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
     DBUF(uint8_t, d, "api_img", n);
     DBUF(uint8_t, o, "api_out", n);
     DBUF(FramePlan, plan, "api_plan1", 1);
-    const FramePlan p = host_plan(*t);
+    FramePlan p = host_plan(*t);
+    finish_plan(p, w, h, 0, 0, 0.0);
     CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(plan, &p, sizeof p, cudaMemcpyHostToDevice, st));
     launch_warp_only(d, w, h, plan, o, st);
@@ -838,7 +843,8 @@ int stabgpu_compose_stabilized(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t
     DBUF(uint8_t, d, "api_cmp_in", n + 2 * nc);
     DBUF(uint8_t, o, "api_cmp_out", n + 2 * nc);
     DBUF(FramePlan, plan, "api_plan1", 1);
-    const FramePlan p = host_plan(*t);
+    FramePlan p = host_plan(*t);
+    finish_plan(p, w, h, chroma ? cw : 0, chroma ? ch : 0, crop);
     CUDA_TRY(cudaMemcpyAsync(plan, &p, sizeof p, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(d, y, n, cudaMemcpyHostToDevice, st));
     if (chroma) {
@@ -882,7 +888,7 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const 
     TRY(run_motion(ctx, y, 0, n - 1, w, h, cfg, motion, t_ms));
     if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
     launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
-    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, st);
+    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st);
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
     if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
@@ -984,7 +990,8 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
         const bool complete = known == n;
         const long long ready = complete ? n : std::max<long long>(0, known - r);
         if (ready > composed) {
-            launch_plan_smooth(cum, known, complete, composed, ready - composed, r, rec, plan, st);
+            launch_plan_smooth(cum, known, complete, composed, ready - composed, r, rec, plan,
+                               PlanGeom{w, h, chroma ? cw : 0, chroma ? ch : 0, cfg.crop_ratio}, st);
             ++ctx->stats.launches;
             rc = compose_range(ctx, dy, dcb, dcr, composed, ready - composed, w, h, cw, ch, plan,
                                cfg.crop_ratio, doy, docb, docr);
@@ -1058,7 +1065,7 @@ int stabgpu_plan_corrections(stabgpu_ctx* ctx, const stabgpu_motion_record* host
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
     launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
-    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, st);
+    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{16, 16, 0, 0, 0.0}, st);
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
     TRY(plan_error(ctx, ps));
@@ -1081,7 +1088,7 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb
     DBUF(FramePlan, plan, "cmp_plan", count);
     CUDA_TRY(cudaMemcpyAsync(corr, host_corr, sizeof(stabgpu_transform) * count,
                              cudaMemcpyHostToDevice, st));
-    launch_plan_from_corrections(corr, count, plan, st);
+    launch_plan_from_corrections(corr, count, plan, PlanGeom{w, h, (cb && cr) ? cw : 0, (cb && cr) ? ch : 0, crop}, st);
     ++ctx->stats.launches;
     TRY(compose_range(ctx, y, cb, cr, 0, count, w, h, cw, ch, plan, crop, oy, ocb, ocr));
     CUDA_TRY(cudaStreamSynchronize(st));
