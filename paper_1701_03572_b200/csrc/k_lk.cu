@@ -15,6 +15,8 @@
 // (the reference's per-row / per-column clipping is separable), flattened so
 // the 32 lanes stride it densely.  Segments (independent 5-frame tracking
 // chains, grid.y) and features (grid.x) are both batched into one launch.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -187,6 +189,244 @@ __device__ bool track_warp(const DevPyramid& P, int fprev, int fcur, double px, 
     return true;
 }
 
+
+// ---------------------------------------------------------------------------
+// Fast path for windows up to 31x31 (r <= 15): lanes are window columns, rows
+// are rolled through registers, and the bilinear patch is evaluated in its
+// separable form (horizontal lerp per image row, vertical lerp per window
+// row), so each window entry costs one byte load, one shuffle and a handful
+// of fp64 ops instead of four clamped 64-bit gathers.  Rounding differs from
+// the reference's weighted form by ~1e-13 (tolerance-level, like the sums).
+
+__device__ __forceinline__ double u2d(uint32_t b) {  // exact u8 -> double, no I2F
+    return __hiloint2double(0x43300000, (int)b) - 4503599627370496.0;
+}
+
+__device__ __forceinline__ uint32_t px_at(const Level& L, int x, int y, bool interior) {
+    if (!interior) {
+        x = clampi(x, 0, L.w - 1);
+        y = clampi(y, 0, L.h - 1);
+    }
+    return __ldg(L.px + (size_t)y * L.w + x);
+}
+
+__device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
+                                const stabgpu_flow_cfg& cfg, double* tv, double* tgx, double* tgy,
+                                double& ox, double& oy, unsigned& iters, unsigned& builds) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int r = cfg.window_radius, side = 2 * r + 1;
+    const int e = r + 1, es = 2 * e + 1;  // extended template patch (flow.cpp:79-81)
+    int start_level = 0;
+    for (int l = P.levels - 1; l > 0; --l)
+        if (min(P.w[l], P.h[l]) >= side) {
+            start_level = l;
+            break;
+        }
+    const int min_count = max(25, side * side / 4);
+    const double r2 = (double)r * r, eps2 = dmul(cfg.epsilon, cfg.epsilon);
+    double gfx = 0.0, gfy = 0.0;
+    for (int level = start_level; level >= 0; --level) {
+        const Level pi{P.lvl[level] + (size_t)fprev * P.stride[level], P.w[level], P.h[level]};
+        const Level ci{P.lvl[level] + (size_t)fcur * P.stride[level], P.w[level], P.h[level]};
+        const double scale = (double)(1u << level);
+        const double plx = ddiv(px, scale), ply = ddiv(py, scale);
+        if (!inside(pi, plx, ply)) return false;
+        const int x0 = (int)floor(plx), y0 = (int)floor(ply);
+        // valid window (flow.cpp:95-103): rows 1 <= y0-r+j <= h-3, columns alike
+        const int jv0 = max(0, 1 - y0 + r), jv1 = min(side - 1, pi.h - 3 - y0 + r);
+        const int iv0 = max(0, 1 - x0 + r), iv1 = min(side - 1, pi.w - 3 - x0 + r);
+        const int vh = jv1 - jv0 + 1, vw = iv1 - iv0 + 1;
+        const int count = (vh > 0 && vw > 0) ? vh * vw : 0;
+        if (count < min_count) {  // TooSmall (flow.cpp:116-118) depends on the count only
+            if (level == 0) return false;
+            gfx = dmul(gfx, 2.0);
+            gfy = dmul(gfy, 2.0);
+            continue;
+        }
+        ++builds;
+        // ---- template (build_level_patch): lane L <-> extended column L
+        const double fx = dsub(plx, (double)x0), fy = dsub(ply, (double)y0);
+        const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
+        const bool tin = xb >= 0 && yb >= 0 && xb + es + 1 <= pi.w - 1 && yb + es <= pi.h - 1;
+        const bool xtra = es > 31 && lane == 31;  // es == 33: lane 31 also owns column 32
+        double hprev = 0.0, hprev_x = 0.0;
+        double eA = 0.0, eB = 0.0, eBx = 0.0;  // extended rows m-2, m-1 (and col 32 of m-1)
+        double gxx = 0.0, gxy = 0.0, gyy = 0.0;
+        for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
+            const int yy = yb + k;
+            const uint32_t pb = lane <= min(es, 31) ? px_at(pi, xb + lane, yy, tin) : 0u;
+            uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+            double h = 0.0, hx = 0.0;
+            if (xtra) {
+                const uint32_t p32 = px_at(pi, xb + 32, yy, tin), p33 = px_at(pi, xb + 33, yy, tin);
+                qb = p32;
+                const double a = u2d(p32);
+                hx = fma(fx, u2d(p33) - a, a);
+            }
+            {
+                const double a = u2d(pb);
+                h = fma(fx, u2d(qb) - a, a);
+            }
+            if (k >= 1) {
+                const int m = k - 1;  // extended row m
+                const double ev = fma(fy, h - hprev, hprev);
+                const double evx = xtra ? fma(fy, hx - hprev_x, hprev_x) : 0.0;
+                if (m >= 2) {  // template row j = m-2 from extended rows m-2, m-1, m
+                    const int j = m - 2;
+                    double right = __shfl_down_sync(FULL, eB, 1);
+                    const double left = __shfl_up_sync(FULL, eB, 1);
+                    if (xtra) right = eBx;
+                    const int i = lane - 1;
+                    if (j >= jv0 && j <= jv1 && i >= iv0 && i <= iv1) {
+                        const double dx = 0.5 * (right - left);
+                        const double dy = 0.5 * (ev - eA);
+                        const int o = (j - jv0) * vw + (i - iv0);
+                        tv[o] = eB;
+                        tgx[o] = dx;
+                        tgy[o] = dy;
+                        gxx = fma(dx, dx, gxx);
+                        gxy = fma(dx, dy, gxy);
+                        gyy = fma(dy, dy, gyy);
+                    }
+                }
+                eA = eB;
+                eB = ev;
+                eBx = evx;
+            }
+            hprev = h;
+            hprev_x = hx;
+        }
+        gxx = warp_dsum(gxx);
+        gxy = warp_dsum(gxy);
+        gyy = warp_dsum(gyy);
+        __syncwarp();
+        {
+            const double ht = dmul(0.5, dadd(gxx, gyy)), hd = dmul(0.5, dsub(gxx, gyy));
+            const double me = dsub(ht, dsqrt(dadd(dmul(hd, hd), dmul(gxy, gxy))));
+            if (me < dmul(1e-4, (double)count)) return false;  // Unconditioned
+        }
+        const double det = dsub(dmul(gxx, gyy), dmul(gxy, gxy));
+        // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
+        double vx = 0.0, vy = 0.0;
+        bool diverged = false;
+        const bool col = lane < vw;
+        for (int it = 0; it < cfg.max_iterations; ++it) {
+            const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
+            if (!inside(ci, qx, qy)) {
+                diverged = true;
+                break;
+            }
+            ++iters;
+            const int qx0 = (int)floor(qx), qy0 = (int)floor(qy);
+            const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
+            const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
+            const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
+            double bx = 0.0, by = 0.0, hp = 0.0;
+            const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
+            for (int k = 0; k <= vh; ++k) {
+                uint32_t pb = 0;
+                if (lane <= vw) pb = cin ? __ldg(rowp) : px_at(ci, cx + lane, cy + k, false);
+                rowp += ci.w;
+                const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+                const double a = u2d(pb);
+                const double h = fma(cfx, u2d(qb) - a, a);
+                if (k >= 1 && col) {
+                    const double cur = fma(cfy, h - hp, hp);
+                    const int o = (k - 1) * vw + lane;
+                    const double d = tv[o] - cur;
+                    bx = fma(d, tgx[o], bx);
+                    by = fma(d, tgy[o], by);
+                }
+                hp = h;
+            }
+            bx = warp_dsum(bx);
+            by = warp_dsum(by);
+            const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
+            const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
+            vx = dadd(vx, dx);
+            vy = dadd(vy, dy);
+            if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
+                diverged = true;
+                break;
+            }
+            if (dadd(dmul(dx, dx), dmul(dy, dy)) < eps2) break;
+        }
+        __syncwarp();
+        if (diverged && level == 0) return false;
+        if (!diverged) {
+            gfx = dadd(gfx, vx);
+            gfy = dadd(gfy, vy);
+        }
+        if (level > 0) {
+            gfx = dmul(gfx, 2.0);
+            gfy = dmul(gfy, 2.0);
+        }
+    }
+    const double rx = dadd(px, gfx), ry = dadd(py, gfy);
+    const Level base{P.lvl[0] + (size_t)fcur * P.stride[0], P.w[0], P.h[0]};
+    if (!inside(base, rx, ry)) return false;
+    ox = rx;
+    oy = ry;
+    return true;
+}
+
+// Persistent warps: each warp pulls (segment, point) work items from a global
+// counter, so early-exiting points never leave a warp slot idle.
+__global__ void __launch_bounds__(256) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
+                                                      unsigned* __restrict__ work, int smem_per_warp) {
+    extern __shared__ __align__(16) double lsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int side = 2 * cfg.window_radius + 1;
+    double* tv = lsm + (size_t)warp * smem_per_warp;
+    double* tgx = tv + side * side;
+    double* tgy = tgx + side * side;
+    const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
+    while (true) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(work, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= total) break;
+        const int seg = (int)(item / (unsigned)s.max_pts), k = (int)(item % (unsigned)s.max_pts);
+        const int fprev = s.frame0 + seg * s.seg_len + s.t - 1, fcur = fprev + 1;
+        if (fcur >= s.nframes || k >= s.npts[seg]) continue;
+        const size_t slot = (size_t)seg * s.max_pts + k;
+        const double2 p = s.pts[slot];
+        unsigned iters = 0, builds = 0;
+        double fx = p.x, fy = p.y;
+        bool keep;
+        if (s.mode == 2) {
+            double bx, by;
+            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tv, tgx, tgy, bx, by, iters, builds);
+            if (keep) {
+                const double2 q = s.ref[slot];
+                const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
+                keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
+            }
+        } else {
+            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tv, tgx, tgy, fx, fy, iters, builds);
+            if (keep && s.mode == 1) {
+                double bx, by;
+                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tv, tgx, tgy, bx, by, iters, builds);
+                if (keep) {
+                    const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
+                    keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
+                }
+            }
+        }
+        if (lane == 0) {
+            s.fwd[slot] = make_double2(fx, fy);
+            s.keep[slot] = keep ? 1 : 0;
+            if (s.iter_count) {
+                atomicAdd(s.iter_count, (unsigned long long)iters);
+                atomicAdd(s.iter_count + 1, (unsigned long long)builds);
+                atomicAdd(s.iter_count + 2, 1ull);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void lk_kernel(LkStep s, stabgpu_flow_cfg cfg, int warps_per_cta, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -285,6 +525,22 @@ __global__ void compact_kernel(LkStep s, double2* __restrict__ next_pts, int* __
 void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (s.nseg <= 0 || s.max_pts <= 0) return;
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
+    if (r <= 15) {
+        const int per_warp = 3 * side * side;  // doubles: template value + gradients
+        const int wpc = 4;
+        const size_t smem = (size_t)wpc * per_warp * sizeof(double);
+        cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk_fast_kernel, wpc * 32, smem);
+        cudaMemsetAsync(s.work, 0, sizeof(unsigned), st);
+        const long long items = (long long)s.nseg * s.max_pts;
+        const long long want = (items + wpc - 1) / wpc;
+        const int grid = (int)std::min<long long>(want, (long long)sms * std::max(per_sm, 1));
+        lk_fast_kernel<<<grid, wpc * 32, smem, st>>>(s, cfg, s.work, per_warp);
+        return;
+    }
     const int per_warp = es * es + 2 * side * side;  // doubles
     int wpc = (int)((100 * 1024) / (per_warp * sizeof(double)));
     wpc = max(1, min(8, wpc));

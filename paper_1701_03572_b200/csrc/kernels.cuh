@@ -92,6 +92,7 @@ struct LkStep {
     int nframes;          // frames in pyr; a segment is active while cur < nframes
     int mode;             // 0 track_lk, 1 forward + weed (sequence), 2 weed only
     const double2* ref;   // mode 2: prev points the backward track must return to
+    unsigned* work;       // persistent-warp work counter (zeroed by launch_lk)
 };
 void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
 // Ordered compaction of kept pairs: TrackSet of frame (frame0 + s*R + t) and

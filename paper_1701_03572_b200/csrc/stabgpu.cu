@@ -266,6 +266,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(double2, trk_cur, "trk_cur", (size_t)count * maxc);
     DBUF(int, trk_n, "trk_n", count);
     DBUF(unsigned long long, iters, "lk_iters", 3);
+    DBUF(unsigned, lk_work, "lk_work", 1);
     CUDA_TRY(cudaMemsetAsync(iters, 0, 3 * sizeof(unsigned long long), st));
     {
         Timer tm(ctx, 2);
@@ -289,6 +290,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
             s.nframes = nF;
             s.mode = 1;
             s.ref = nullptr;
+            s.work = lk_work;
             launch_lk(s, cfg.flow, st);
             launch_compact(s, nxt_pts, nxt_n, trk_prev, trk_cur, trk_n, 1, st);
             ctx->stats.launches += 2;
@@ -624,6 +626,7 @@ int run_lk_api(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyra
     DBUF(double2, df, "api_lk_fwd", n);
     DBUF(uint8_t, dk, "api_lk_keep", n);
     DBUF(int, dn, "api_lk_n", 1);
+    DBUF(unsigned, lk_work, "lk_work", 1);
     CUDA_TRY(cudaMemcpyAsync(dp, pts, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
     if (ref) CUDA_TRY(cudaMemcpyAsync(dr, ref, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dn, &n, sizeof n, cudaMemcpyHostToDevice, st));
@@ -642,6 +645,7 @@ int run_lk_api(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyra
     s.nframes = 2;
     s.mode = mode;
     s.ref = dr;
+    s.work = lk_work;
     launch_lk(s, *cfg, st);
     ++ctx->stats.launches;
     TRY(check_launch("track_lk"));
