@@ -253,49 +253,60 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         double hprev = 0.0, hprev_x = 0.0;
         double eA = 0.0, eB = 0.0, eBx = 0.0;  // extended rows m-2, m-1 (and col 32 of m-1)
         double gxx = 0.0, gxy = 0.0, gyy = 0.0;
-        for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
-            const int yy = yb + k;
-            const uint32_t pb = lane <= min(es, 31) ? px_at(pi, xb + lane, yy, tin) : 0u;
-            uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-            double h = 0.0, hx = 0.0;
-            if (xtra) {
-                const uint32_t p32 = px_at(pi, xb + 32, yy, tin), p33 = px_at(pi, xb + 33, yy, tin);
-                qb = p32;
-                const double a = u2d(p32);
-                hx = fma(fx, u2d(p33) - a, a);
-            }
-            {
-                const double a = u2d(pb);
-                h = fma(fx, u2d(qb) - a, a);
-            }
-            if (k >= 1) {
-                const int m = k - 1;  // extended row m
-                const double ev = fma(fy, h - hprev, hprev);
-                const double evx = xtra ? fma(fy, hx - hprev_x, hprev_x) : 0.0;
-                if (m >= 2) {  // template row j = m-2 from extended rows m-2, m-1, m
-                    const int j = m - 2;
-                    double right = __shfl_down_sync(FULL, eB, 1);
-                    const double left = __shfl_up_sync(FULL, eB, 1);
-                    if (xtra) right = eBx;
-                    const int i = lane - 1;
-                    if (j >= jv0 && j <= jv1 && i >= iv0 && i <= iv1) {
-                        const double dx = 0.5 * (right - left);
-                        const double dy = 0.5 * (ev - eA);
-                        const int o = (j - jv0) * vw + (i - iv0);
-                        tv[o] = eB;
-                        tgx[o] = dx;
-                        tgy[o] = dy;
-                        gxx = fma(dx, dx, gxx);
-                        gxy = fma(dx, dy, gxy);
-                        gyy = fma(dy, dy, gyy);
-                    }
+        for (int k0 = 0; k0 <= es; k0 += 8) {  // image rows yb .. yb+es, 8 loads in flight
+            uint32_t tbv[8], tx32[8], tx33[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + u;
+                tbv[u] = (lane <= min(es, 31) && k <= es) ? px_at(pi, xb + lane, yb + k, tin) : 0u;
+                tx32[u] = tx33[u] = 0u;
+                if (xtra && k <= es) {
+                    tx32[u] = px_at(pi, xb + 32, yb + k, tin);
+                    tx33[u] = px_at(pi, xb + 33, yb + k, tin);
                 }
-                eA = eB;
-                eB = ev;
-                eBx = evx;
             }
-            hprev = h;
-            hprev_x = hx;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + u;
+                if (k > es) break;
+                uint32_t qb = __shfl_down_sync(FULL, tbv[u], 1);
+                double hx = 0.0;
+                if (xtra) {
+                    qb = tx32[u];
+                    const double a = u2d(tx32[u]);
+                    hx = fma(fx, u2d(tx33[u]) - a, a);
+                }
+                const double a = u2d(tbv[u]);
+                const double h = fma(fx, u2d(qb) - a, a);
+                if (k >= 1) {
+                    const int m = k - 1;  // extended row m
+                    const double ev = fma(fy, h - hprev, hprev);
+                    const double evx = xtra ? fma(fy, hx - hprev_x, hprev_x) : 0.0;
+                    if (m >= 2) {  // template row j = m-2 from extended rows m-2, m-1, m
+                        const int j = m - 2;
+                        double right = __shfl_down_sync(FULL, eB, 1);
+                        const double left = __shfl_up_sync(FULL, eB, 1);
+                        if (xtra) right = eBx;
+                        const int i = lane - 1;
+                        if (j >= jv0 && j <= jv1 && i >= iv0 && i <= iv1) {
+                            const double dx = 0.5 * (right - left);
+                            const double dy = 0.5 * (ev - eA);
+                            const int o = (j - jv0) * vw + (i - iv0);
+                            tv[o] = eB;
+                            tgx[o] = dx;
+                            tgy[o] = dy;
+                            gxx = fma(dx, dx, gxx);
+                            gxy = fma(dx, dy, gxy);
+                            gyy = fma(dy, dy, gyy);
+                        }
+                    }
+                    eA = eB;
+                    eB = ev;
+                    eBx = evx;
+                }
+                hprev = h;
+                hprev_x = hx;
+            }
         }
         gxx = warp_dsum(gxx);
         gxy = warp_dsum(gxy);
@@ -324,21 +335,34 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
             double bx = 0.0, by = 0.0, hp = 0.0;
             const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
-            for (int k = 0; k <= vh; ++k) {
-                uint32_t pb = 0;
-                if (lane <= vw) pb = cin ? __ldg(rowp) : px_at(ci, cx + lane, cy + k, false);
-                rowp += ci.w;
-                const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-                const double a = u2d(pb);
-                const double h = fma(cfx, u2d(qb) - a, a);
-                if (k >= 1 && col) {
-                    const double cur = fma(cfy, h - hp, hp);
-                    const int o = (k - 1) * vw + lane;
-                    const double d = tv[o] - cur;
-                    bx = fma(d, tgx[o], bx);
-                    by = fma(d, tgy[o], by);
+            const bool ld = lane <= vw;
+            // rows in batches of 8: the 8 loads are in flight together
+            for (int k0 = 0; k0 <= vh; k0 += 8) {
+                uint32_t pbv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u;
+                    pbv[u] = 0;
+                    if (ld && k <= vh) pbv[u] = cin ? __ldg(rowp + (size_t)u * ci.w)
+                                                    : px_at(ci, cx + lane, cy + k, false);
                 }
-                hp = h;
+                rowp += (size_t)8 * ci.w;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u;
+                    if (k > vh) break;
+                    const uint32_t qb = __shfl_down_sync(FULL, pbv[u], 1);
+                    const double a = u2d(pbv[u]);
+                    const double h = fma(cfx, u2d(qb) - a, a);
+                    if (k >= 1 && col) {
+                        const double cur = fma(cfy, h - hp, hp);
+                        const int o = (k - 1) * vw + lane;
+                        const double d = tv[o] - cur;
+                        bx = fma(d, tgx[o], bx);
+                        by = fma(d, tgy[o], by);
+                    }
+                    hp = h;
+                }
             }
             bx = warp_dsum(bx);
             by = warp_dsum(by);
@@ -373,7 +397,7 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
 
 // Persistent warps: each warp pulls (segment, point) work items from a global
 // counter, so early-exiting points never leave a warp slot idle.
-__global__ void __launch_bounds__(256) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
+__global__ void __launch_bounds__(128, 5) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
