@@ -211,7 +211,7 @@ __device__ __forceinline__ uint32_t px_at(const Level& L, int x, int y, bool int
 }
 
 __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
-                                const stabgpu_flow_cfg& cfg, double* tv, double* tgx, double* tgy,
+                                const stabgpu_flow_cfg& cfg, double* tgx, double* tgy,
                                 double& ox, double& oy, unsigned& iters, unsigned& builds) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -245,72 +245,69 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             continue;
         }
         ++builds;
-        // ---- template (build_level_patch): lane L <-> extended column L
+        // ---- template (build_level_patch): lane L <-> extended column L, rows rolled.
+        // Stored: gradients over the valid window (row stride vw); the template
+        // values enter only through T = sum(tval * grad), accumulated here.
         const double fx = dsub(plx, (double)x0), fy = dsub(ply, (double)y0);
         const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
         const bool tin = xb >= 0 && yb >= 0 && xb + es + 1 <= pi.w - 1 && yb + es <= pi.h - 1;
         const bool xtra = es > 31 && lane == 31;  // es == 33: lane 31 also owns column 32
-        double hprev = 0.0, hprev_x = 0.0;
-        double eA = 0.0, eB = 0.0, eBx = 0.0;  // extended rows m-2, m-1 (and col 32 of m-1)
-        double gxx = 0.0, gxy = 0.0, gyy = 0.0;
-        for (int k0 = 0; k0 <= es; k0 += 8) {  // image rows yb .. yb+es, 8 loads in flight
-            uint32_t tbv[8], tx32[8], tx33[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = k0 + u;
-                tbv[u] = (lane <= min(es, 31) && k <= es) ? px_at(pi, xb + lane, yb + k, tin) : 0u;
-                tx32[u] = tx33[u] = 0u;
-                if (xtra && k <= es) {
-                    tx32[u] = px_at(pi, xb + 32, yb + k, tin);
-                    tx33[u] = px_at(pi, xb + 33, yb + k, tin);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = k0 + u;
-                if (k > es) break;
-                uint32_t qb = __shfl_down_sync(FULL, tbv[u], 1);
-                double hx = 0.0;
+        const bool tld = lane <= min(es, 31);
+        const int ti = lane - 1;  // template column of this lane
+        const bool tcol = ti >= iv0 && ti <= iv1;
+        double hprev = 0.0, hprev_x = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
+        double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
+        uint32_t nb = tld ? px_at(pi, xb + lane, yb, tin) : 0u;
+        uint32_t nx32 = xtra ? px_at(pi, xb + 32, yb, tin) : 0u, nx33 = xtra ? px_at(pi, xb + 33, yb, tin) : 0u;
+        for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
+            const uint32_t pb = nb, p32 = nx32, p33 = nx33;
+            if (k < es) {  // prefetch the next row
+                nb = tld ? px_at(pi, xb + lane, yb + k + 1, tin) : 0u;
                 if (xtra) {
-                    qb = tx32[u];
-                    const double a = u2d(tx32[u]);
-                    hx = fma(fx, u2d(tx33[u]) - a, a);
+                    nx32 = px_at(pi, xb + 32, yb + k + 1, tin);
+                    nx33 = px_at(pi, xb + 33, yb + k + 1, tin);
                 }
-                const double a = u2d(tbv[u]);
-                const double h = fma(fx, u2d(qb) - a, a);
-                if (k >= 1) {
-                    const int m = k - 1;  // extended row m
-                    const double ev = fma(fy, h - hprev, hprev);
-                    const double evx = xtra ? fma(fy, hx - hprev_x, hprev_x) : 0.0;
-                    if (m >= 2) {  // template row j = m-2 from extended rows m-2, m-1, m
-                        const int j = m - 2;
-                        double right = __shfl_down_sync(FULL, eB, 1);
-                        const double left = __shfl_up_sync(FULL, eB, 1);
-                        if (xtra) right = eBx;
-                        const int i = lane - 1;
-                        if (j >= jv0 && j <= jv1 && i >= iv0 && i <= iv1) {
-                            const double dx = 0.5 * (right - left);
-                            const double dy = 0.5 * (ev - eA);
-                            const int o = (j - jv0) * vw + (i - iv0);
-                            tv[o] = eB;
-                            tgx[o] = dx;
-                            tgy[o] = dy;
-                            gxx = fma(dx, dx, gxx);
-                            gxy = fma(dx, dy, gxy);
-                            gyy = fma(dy, dy, gyy);
-                        }
-                    }
-                    eA = eB;
-                    eB = ev;
-                    eBx = evx;
-                }
-                hprev = h;
-                hprev_x = hx;
             }
+            uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+            double hx = 0.0;
+            if (xtra) {
+                qb = p32;
+                const double a = u2d(p32);
+                hx = fma(fx, u2d(p33) - a, a);
+            }
+            const double a = u2d(pb);
+            const double h = fma(fx, u2d(qb) - a, a);
+            if (k >= 1) {
+                const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
+                const double evx = fma(fy, hx - hprev_x, hprev_x);
+                const int j = k - 3;  // template row from extended rows k-3, k-2, k-1
+                double right = __shfl_down_sync(FULL, eB, 1);
+                const double left = __shfl_up_sync(FULL, eB, 1);
+                if (xtra) right = eBx;
+                if (j >= jv0 && j <= jv1 && tcol) {
+                    const double dx = 0.5 * (right - left);
+                    const double dy = 0.5 * (ev - eA);
+                    const int o = (j - jv0) * vw + (ti - iv0);
+                    tgx[o] = dx;
+                    tgy[o] = dy;
+                    gxx = fma(dx, dx, gxx);
+                    gxy = fma(dx, dy, gxy);
+                    gyy = fma(dy, dy, gyy);
+                    tx = fma(eB, dx, tx);
+                    ty = fma(eB, dy, ty);
+                }
+                eA = eB;
+                eB = ev;
+                eBx = evx;
+            }
+            hprev = h;
+            hprev_x = hx;
         }
         gxx = warp_dsum(gxx);
         gxy = warp_dsum(gxy);
         gyy = warp_dsum(gyy);
+        tx = warp_dsum(tx);
+        ty = warp_dsum(ty);
         __syncwarp();
         {
             const double ht = dmul(0.5, dadd(gxx, gyy)), hd = dmul(0.5, dsub(gxx, gyy));
@@ -321,7 +318,9 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
         double vx = 0.0, vy = 0.0;
         bool diverged = false;
-        const bool col = lane < vw;
+        const bool col = lane < vw, ld = lane <= vw;
+        const double* gxl = tgx + (col ? lane : 0);
+        const double* gyl = tgy + (col ? lane : 0);
         for (int it = 0; it < cfg.max_iterations; ++it) {
             const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
             if (!inside(ci, qx, qy)) {
@@ -333,39 +332,27 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
             const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
             const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
-            double bx = 0.0, by = 0.0, hp = 0.0;
+            // sum(cur * grad); b = T - that
+            double sx = 0.0, sy = 0.0, hp = 0.0;
             const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
-            const bool ld = lane <= vw;
-            // rows in batches of 8: the 8 loads are in flight together
-            for (int k0 = 0; k0 <= vh; k0 += 8) {
-                uint32_t pbv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = k0 + u;
-                    pbv[u] = 0;
-                    if (ld && k <= vh) pbv[u] = cin ? __ldg(rowp + (size_t)u * ci.w)
-                                                    : px_at(ci, cx + lane, cy + k, false);
+            uint32_t nb = ld ? (cin ? __ldg(rowp) : px_at(ci, cx + lane, cy, false)) : 0u;
+            for (int k = 0; k <= vh; ++k) {
+                const uint32_t pb = nb;
+                rowp += ci.w;
+                if (k < vh && ld) nb = cin ? __ldg(rowp) : px_at(ci, cx + lane, cy + k + 1, false);
+                const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+                const double a = u2d(pb);
+                const double h = fma(cfx, u2d(qb) - a, a);
+                if (k >= 1 && col) {
+                    const double cur = fma(cfy, h - hp, hp);
+                    const int o = (k - 1) * vw;
+                    sx = fma(cur, gxl[o], sx);
+                    sy = fma(cur, gyl[o], sy);
                 }
-                rowp += (size_t)8 * ci.w;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = k0 + u;
-                    if (k > vh) break;
-                    const uint32_t qb = __shfl_down_sync(FULL, pbv[u], 1);
-                    const double a = u2d(pbv[u]);
-                    const double h = fma(cfx, u2d(qb) - a, a);
-                    if (k >= 1 && col) {
-                        const double cur = fma(cfy, h - hp, hp);
-                        const int o = (k - 1) * vw + lane;
-                        const double d = tv[o] - cur;
-                        bx = fma(d, tgx[o], bx);
-                        by = fma(d, tgy[o], by);
-                    }
-                    hp = h;
-                }
+                hp = h;
             }
-            bx = warp_dsum(bx);
-            by = warp_dsum(by);
+            const double bx = tx - warp_dsum(sx);
+            const double by = ty - warp_dsum(sy);
             const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
             const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
             vx = dadd(vx, dx);
@@ -397,13 +384,12 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
 
 // Persistent warps: each warp pulls (segment, point) work items from a global
 // counter, so early-exiting points never leave a warp slot idle.
-__global__ void __launch_bounds__(128, 5) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
+__global__ void __launch_bounds__(128) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int side = 2 * cfg.window_radius + 1;
-    double* tv = lsm + (size_t)warp * smem_per_warp;
-    double* tgx = tv + side * side;
+    double* tgx = lsm + (size_t)warp * smem_per_warp;
     double* tgy = tgx + side * side;
     const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
     while (true) {
@@ -421,17 +407,17 @@ __global__ void __launch_bounds__(128, 5) lk_fast_kernel(LkStep s, stabgpu_flow_
         bool keep;
         if (s.mode == 2) {
             double bx, by;
-            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tv, tgx, tgy, bx, by, iters, builds);
+            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tgx, tgy, bx, by, iters, builds);
             if (keep) {
                 const double2 q = s.ref[slot];
                 const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
                 keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
             }
         } else {
-            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tv, tgx, tgy, fx, fy, iters, builds);
+            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tgx, tgy, fx, fy, iters, builds);
             if (keep && s.mode == 1) {
                 double bx, by;
-                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tv, tgx, tgy, bx, by, iters, builds);
+                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tgx, tgy, bx, by, iters, builds);
                 if (keep) {
                     const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
                     keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
@@ -550,7 +536,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (s.nseg <= 0 || s.max_pts <= 0) return;
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
-        const int per_warp = 3 * side * side;  // doubles: template value + gradients
+        const int per_warp = 2 * side * side;  // doubles: template gradients
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
