@@ -202,12 +202,59 @@ __device__ __forceinline__ double u2d(uint32_t b) {  // exact u8 -> double, no I
     return __hiloint2double(0x43300000, (int)b) - 4503599627370496.0;
 }
 
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t px_at(const Level& L, int x, int y, bool interior) {
     if (!interior) {
         x = clampi(x, 0, L.w - 1);
         y = clampi(y, 0, L.h - 1);
     }
     return __ldg(L.px + (size_t)y * L.w + x);
+}
+
+
+// sum over the valid window of cur(j, i) * grad(j, i), lane L <-> column
+// cx + L (lane vw only supplies the right neighbour).  INTERIOR: the
+// (vh+1) x (vw+1) source block lies inside the image, so no clamping.
+template <bool INTERIOR>
+__device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw, int vh,
+                                         double cfx, double cfy, uint32_t gx_addr,
+                                         uint32_t gy_addr, double& sx, double& sy) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool ld = lane <= vw, col = lane < vw;
+    const uint32_t rstep = (uint32_t)vw * 8u;
+    const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
+    auto load = [&](int k) -> uint32_t {
+        if (!ld) return 0u;
+        if (INTERIOR) return __ldg(rowp + (size_t)k * ci.w);
+        return px_at(ci, cx + lane, cy + k, false);
+    };
+    uint32_t pb = load(0), nb = load(1);
+    double hp;
+    {
+        const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+        const double a = u2d(pb);
+        hp = fma(cfx, u2d(qb) - a, a);
+    }
+    for (int k = 1; k <= vh; ++k) {
+        pb = nb;
+        if (k < vh) nb = load(k + 1);
+        const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+        const double a = u2d(pb);
+        const double h = fma(cfx, u2d(qb) - a, a);
+        const double cur = fma(cfy, h - hp, hp);
+        const double cm = col ? cur : 0.0;
+        sx = fma(cm, lds_f64(gx_addr), sx);
+        sy = fma(cm, lds_f64(gy_addr), sy);
+        gx_addr += rstep;
+        gy_addr += rstep;
+        hp = h;
+    }
 }
 
 __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
@@ -318,9 +365,9 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
         double vx = 0.0, vy = 0.0;
         bool diverged = false;
-        const bool col = lane < vw, ld = lane <= vw;
-        const double* gxl = tgx + (col ? lane : 0);
-        const double* gyl = tgy + (col ? lane : 0);
+        const int lc = lane < vw ? lane : 0;
+        const uint32_t gxa = (uint32_t)__cvta_generic_to_shared(tgx + lc);
+        const uint32_t gya = (uint32_t)__cvta_generic_to_shared(tgy + lc);
         for (int it = 0; it < cfg.max_iterations; ++it) {
             const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
             if (!inside(ci, qx, qy)) {
@@ -333,24 +380,9 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
             const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
             // sum(cur * grad); b = T - that
-            double sx = 0.0, sy = 0.0, hp = 0.0;
-            const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
-            uint32_t nb = ld ? (cin ? __ldg(rowp) : px_at(ci, cx + lane, cy, false)) : 0u;
-            for (int k = 0; k <= vh; ++k) {
-                const uint32_t pb = nb;
-                rowp += ci.w;
-                if (k < vh && ld) nb = cin ? __ldg(rowp) : px_at(ci, cx + lane, cy + k + 1, false);
-                const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-                const double a = u2d(pb);
-                const double h = fma(cfx, u2d(qb) - a, a);
-                if (k >= 1 && col) {
-                    const double cur = fma(cfy, h - hp, hp);
-                    const int o = (k - 1) * vw;
-                    sx = fma(cur, gxl[o], sx);
-                    sy = fma(cur, gyl[o], sy);
-                }
-                hp = h;
-            }
+            double sx = 0.0, sy = 0.0;
+            if (cin) row_pass<true>(ci, cx, cy, vw, vh, cfx, cfy, gxa, gya, sx, sy);
+            else row_pass<false>(ci, cx, cy, vw, vh, cfx, cfy, gxa, gya, sx, sy);
             const double bx = tx - warp_dsum(sx);
             const double by = ty - warp_dsum(sy);
             const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
