@@ -257,6 +257,88 @@ __device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw
     }
 }
 
+
+// build_level_patch over the extended (es x es) patch: lane L <-> extended
+// column L (XTRA: es == 33, lane 31 also owns column 32), image rows rolled
+// through registers.  Writes the template gradients over the valid window
+// (row stride vw) and accumulates G and T = sum(template value * gradient).
+template <bool INTERIOR, bool XTRA>
+__device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, int es, double fx,
+                                              double fy, int jv0, int jv1, int iv0, int iv1,
+                                              uint32_t gxa, uint32_t gya, double& gxx, double& gxy,
+                                              double& gyy, double& tx, double& ty) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool tld = lane <= (es < 31 ? es : 31);
+    const bool xtra = XTRA && lane == 31;
+    const int ti = lane - 1;  // template column of this lane
+    const bool tcol = ti >= iv0 && ti <= iv1;
+    const int vw = iv1 - iv0 + 1;
+    const uint32_t rstep = (uint32_t)vw * 8u;
+    const uint32_t coff = (uint32_t)((tcol ? ti - iv0 : 0) * 8);
+    gxa += coff;
+    gya += coff;
+    auto load = [&](int x, int k) -> uint32_t {
+        if (INTERIOR) return __ldg(pi.px + (size_t)(yb + k) * pi.w + x);
+        return px_at(pi, x, yb + k, false);
+    };
+    uint32_t nb = tld ? load(xb + lane, 0) : 0u;
+    uint32_t n32 = 0, n33 = 0;
+    if (XTRA && xtra) {
+        n32 = load(xb + 32, 0);
+        n33 = load(xb + 33, 0);
+    }
+    double hprev = 0.0, hprevx = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
+    for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
+        const uint32_t pb = nb, p32 = n32, p33 = n33;
+        if (k < es) {
+            if (tld) nb = load(xb + lane, k + 1);
+            if (XTRA && xtra) {
+                n32 = load(xb + 32, k + 1);
+                n33 = load(xb + 33, k + 1);
+            }
+        }
+        uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+        double hx = 0.0;
+        if (XTRA) {
+            if (xtra) qb = p32;
+            const double a = u2d(p32);
+            hx = fma(fx, u2d(p33) - a, a);
+        }
+        const double a = u2d(pb);
+        const double h = fma(fx, u2d(qb) - a, a);
+        if (k >= 1) {
+            const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
+            double evx = 0.0;
+            if (XTRA) evx = fma(fy, hx - hprevx, hprevx);
+            if (k >= 3) {  // template row j = k-3 from extended rows k-3, k-2, k-1
+                const int j = k - 3;
+                double right = __shfl_down_sync(FULL, eB, 1);
+                const double left = __shfl_up_sync(FULL, eB, 1);
+                if (XTRA && xtra) right = eBx;
+                const bool ok = tcol && j >= jv0 && j <= jv1;
+                const double dx = ok ? 0.5 * (right - left) : 0.0;
+                const double dy = ok ? 0.5 * (ev - eA) : 0.0;
+                if (ok) {
+                    const uint32_t ro = (uint32_t)(j - jv0) * rstep;
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(gxa + ro), "d"(dx));
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(gya + ro), "d"(dy));
+                }
+                gxx = fma(dx, dx, gxx);
+                gxy = fma(dx, dy, gxy);
+                gyy = fma(dy, dy, gyy);
+                tx = fma(eB, dx, tx);
+                ty = fma(eB, dy, ty);
+            }
+            eA = eB;
+            eB = ev;
+            if (XTRA) eBx = evx;
+        }
+        hprev = h;
+        if (XTRA) hprevx = hx;
+    }
+}
+
 __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
                                 const stabgpu_flow_cfg& cfg, double* tgx, double* tgy,
                                 double& ox, double& oy, unsigned& iters, unsigned& builds) {
@@ -298,57 +380,15 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         const double fx = dsub(plx, (double)x0), fy = dsub(ply, (double)y0);
         const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
         const bool tin = xb >= 0 && yb >= 0 && xb + es + 1 <= pi.w - 1 && yb + es <= pi.h - 1;
-        const bool xtra = es > 31 && lane == 31;  // es == 33: lane 31 also owns column 32
-        const bool tld = lane <= min(es, 31);
-        const int ti = lane - 1;  // template column of this lane
-        const bool tcol = ti >= iv0 && ti <= iv1;
-        double hprev = 0.0, hprev_x = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
         double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
-        uint32_t nb = tld ? px_at(pi, xb + lane, yb, tin) : 0u;
-        uint32_t nx32 = xtra ? px_at(pi, xb + 32, yb, tin) : 0u, nx33 = xtra ? px_at(pi, xb + 33, yb, tin) : 0u;
-        for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
-            const uint32_t pb = nb, p32 = nx32, p33 = nx33;
-            if (k < es) {  // prefetch the next row
-                nb = tld ? px_at(pi, xb + lane, yb + k + 1, tin) : 0u;
-                if (xtra) {
-                    nx32 = px_at(pi, xb + 32, yb + k + 1, tin);
-                    nx33 = px_at(pi, xb + 33, yb + k + 1, tin);
-                }
-            }
-            uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-            double hx = 0.0;
-            if (xtra) {
-                qb = p32;
-                const double a = u2d(p32);
-                hx = fma(fx, u2d(p33) - a, a);
-            }
-            const double a = u2d(pb);
-            const double h = fma(fx, u2d(qb) - a, a);
-            if (k >= 1) {
-                const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
-                const double evx = fma(fy, hx - hprev_x, hprev_x);
-                const int j = k - 3;  // template row from extended rows k-3, k-2, k-1
-                double right = __shfl_down_sync(FULL, eB, 1);
-                const double left = __shfl_up_sync(FULL, eB, 1);
-                if (xtra) right = eBx;
-                if (j >= jv0 && j <= jv1 && tcol) {
-                    const double dx = 0.5 * (right - left);
-                    const double dy = 0.5 * (ev - eA);
-                    const int o = (j - jv0) * vw + (ti - iv0);
-                    tgx[o] = dx;
-                    tgy[o] = dy;
-                    gxx = fma(dx, dx, gxx);
-                    gxy = fma(dx, dy, gxy);
-                    gyy = fma(dy, dy, gyy);
-                    tx = fma(eB, dx, tx);
-                    ty = fma(eB, dy, ty);
-                }
-                eA = eB;
-                eB = ev;
-                eBx = evx;
-            }
-            hprev = h;
-            hprev_x = hx;
+        const uint32_t gxa0 = (uint32_t)__cvta_generic_to_shared(tgx);
+        const uint32_t gya0 = (uint32_t)__cvta_generic_to_shared(tgy);
+        if (es > 31) {
+            if (tin) template_pass<true, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
+            else template_pass<false, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
+        } else {
+            if (tin) template_pass<true, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
+            else template_pass<false, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
         }
         gxx = warp_dsum(gxx);
         gxy = warp_dsum(gxy);
