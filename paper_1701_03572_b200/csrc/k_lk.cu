@@ -241,6 +241,7 @@ __device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw
         const double a = u2d(pb);
         hp = fma(cfx, u2d(qb) - a, a);
     }
+#pragma unroll 2
     for (int k = 1; k <= vh; ++k) {
         pb = nb;
         if (k < vh) nb = load(k + 1);
@@ -289,6 +290,7 @@ __device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, i
         n33 = load(xb + 33, 0);
     }
     double hprev = 0.0, hprevx = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
+#pragma unroll 2
     for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
         const uint32_t pb = nb, p32 = n32, p33 = n33;
         if (k < es) {
