@@ -128,7 +128,7 @@ def shard_ranges(n: int, redetect_interval: int, world: int) -> list[Shard]:
         s0, s1 = nseg * g // world, nseg * (g + 1) // world
         first = min(s0 * R, n - 1)
         last = min(s1 * R, n - 1)
-        own_begin = 0 if g == 0 else first + 1
+        own_begin = 0 if s0 == 0 else first + 1
         own_end = last + 1
         if s0 == s1:  # more ranks than segments: this rank idles
             first, last, own_begin, own_end = 0, 0, 0, 0
