@@ -8,7 +8,7 @@ CSRC     := $(wildcard $(PKG)/csrc/*.cu)
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CSRC))
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/stabgpu.h
 
-all: $(PKG)/libstabgpu.so $(PKG)/synth/libvideogen.so oracle
+all: $(PKG)/libstabgpu.so $(PKG)/synth/libvideogen.so oracle shim
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
@@ -23,11 +23,14 @@ $(PKG)/synth/libvideogen.so: $(PKG)/synth/videogen.c
 oracle:
 	$(MAKE) -C oracle
 
+shim: $(PKG)/libstabgpu.so
+	$(MAKE) -C shim
+
 clean:
 	rm -rf build $(PKG)/libstabgpu.so $(PKG)/synth/libvideogen.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle shim clean
 
 # test-only native helper (brute-force check of the exact walk emulation)
 build/libwalktest.so: tests/native/walk_test.c $(PKG)/csrc/walk.h
