@@ -15,13 +15,15 @@
 //   3. the output tile is written with 16-byte streaming stores.
 // So HBM sees one read and one write per plane byte.
 //
-// Exactness without fp64 per pixel.  Coordinates are carried in 32.32 fixed
-// point (int64 adds), the bilinear blend in fp32.  Each decision the
+// Exactness without fp64 per pixel.  Coordinates are carried in 16.48 fixed
+// point (int64 multiply-adds), the bilinear blend in fp32.  Each decision the
 // reference takes — integer part of a coordinate, in-bounds test, lround of
 // the blended value — is taken on the fast path only when the fast value is
 // provably on the same side of the decision boundary (coordinate error
-// <= ~40 units of 2^-32 px against a 1024-unit guard; value error <= 1.5e-4
-// against a 2.5e-4 guard).  Otherwise the pixel is queued and recomputed
+// < 2^-29 px against a 2.4e-7 px guard; value error <= 1.5e-4 against a
+// 2.5e-4 guard).  Per-row fixed-point starts (16.48) and the crop tables are
+// computed once per frame / geometry by compose_prep_kernel, so a tile's
+// setup is a handful of loads.  Otherwise the pixel is queued and recomputed
 // with the reference's own fp64 arithmetic — for luma including the
 // reference's sequential row walk (sx += c, image_ops.cpp:124-131), which
 // fl_walk (walk.h) reproduces bit for bit in closed form.  About 0.05% of
@@ -39,9 +41,9 @@ constexpr int NT = 256;                  // threads per CTA
 constexpr int WTW = 72, WTH = 36;        // warped-luma tile (<= 66 x 34 used)
 constexpr int SRC_W = 128, SRC_H = 80;   // staged source capacity per plane
 constexpr int QCAP = 1024;               // exact-path queue
-constexpr long long GUARD = 1024;        // fixed-point guard (units of 2^-32 px)
+constexpr uint32_t GUARD = 1024;         // coordinate guard, units of 2^-32 px
 constexpr float VGUARD = 2.5e-4f;        // blended-value guard (the fast error is <= 1.5e-4)
-constexpr double FIX = 4294967296.0;     // 2^32
+constexpr double FIX48 = 281474976710656.0;  // 2^48
 
 struct CropGeom {
     int mx, my;
@@ -58,22 +60,25 @@ __host__ __device__ inline CropGeom crop_geom(int w, int h, double crop) {
     return g;
 }
 
-struct Src {  // a plane as seen by the kernel: staged tile or the global frame
-    const uint8_t* p;
-    int pitch, x0, y0;
+// Per-launch tables (compose_prep_kernel).
+struct Tables {
+    long long *rxf, *ryf;  // [frames][h]  luma warp row starts at u = 0 (16.48)
+    long long *pxf, *pyf;  // [frames][ch] chroma source coords of (0, y) (16.48)
+    int *cx0, *cy0;        // crop_resize integer parts per column [w] / row [h]
+    double *cfx, *cfy;     // and fractions
+    int h, ch;
 };
 
 struct Smem {
     uint8_t src[3][SRC_H * SRC_W];
     uint8_t wt[WTH][WTW];
     uint8_t out[3][TH][TW];
-    double cfx[TW], cfy[TH];      // luma crop fractions per column / row
+    double cfx[TW], cfy[TH];
     float cfxf[TW], cfyf[TH];
     int cx0[TW], cy0[TH];
-    long long sxf[WTH], syf[WTH]; // luma warp: fixed-point x/y of (u0, v) per W row
-    double rxw[WTH], ryw[WTH];    // luma warp row starts (exact reference values)
-    long long pxf[TH], pyf[TH];   // chroma: fixed-point source coords of (X0, y)
-    int bbox[3][4];               // staged footprint per plane
+    long long sxf[WTH], syf[WTH];  // luma row starts of the W tile rows
+    long long pxf[TH], pyf[TH];    // chroma rows of the tile
+    int bbox[3][4];
     int staged[3];
     int qn;
     unsigned q[QCAP];
@@ -102,34 +107,27 @@ __device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, u
     return __float_as_int(k + 8388608.0f) & 0x3FF;
 }
 
-
-
-__device__ __forceinline__ uint8_t at(const Src& s, int x, int y) {
-    return s.p[(y - s.y0) * s.pitch + (x - s.x0)];
-}
-
-// One fast-path sample of plane `q` (pitch, origin bx0/by0) at 32.32 fixed
-// point (X, Y).  Returns the byte, `out` when the coordinate is outside
-// [0, w-1] x [0, h-1] (lim = w-2 / h-2 on the integer part), or -1 when a
-// decision is not certain.
+// One fast-path sample of plane q (pitch, origin bx0/by0) at 16.48 (X, Y).
+// Returns the byte, `out` outside [0, w-1] x [0, h-1] (lim = w-2 / h-2 on
+// the integer part), or -1 when a decision is not certain.
 template <typename P>
 __device__ __forceinline__ int sample_fast(P q, int pitch, int bx0, int by0, unsigned limx,
                                            unsigned limy, long long X, long long Y, int out) {
-    const uint32_t fxs = (uint32_t)X, fys = (uint32_t)Y;
+    const uint32_t fxs = (uint32_t)(X >> 16), fys = (uint32_t)(Y >> 16);
     if (near_int(fxs) || near_int(fys)) return -1;
-    const int ix = (int)(X >> 32), iy = (int)(Y >> 32);
+    const int ix = (int)(X >> 48), iy = (int)(Y >> 48);
     if ((unsigned)ix > limx || (unsigned)iy > limy) return out;
     const int o = (iy - by0) * pitch + (ix - bx0);
     return blend_round(q[o], q[o + 1], q[o + pitch], q[o + pitch + 1], frac_f(fxs), frac_f(fys));
 }
 
-// Two planes sharing one coordinate (4:4:4 chroma): packed result b | r << 16
+// Two planes sharing one coordinate (chroma): packed result b | r << 16
 template <typename P>
 __device__ __forceinline__ int sample_fast2(P q1, P q2, int pitch, int bx0, int by0, unsigned limx,
                                             unsigned limy, long long X, long long Y, int out) {
-    const uint32_t fxs = (uint32_t)X, fys = (uint32_t)Y;
+    const uint32_t fxs = (uint32_t)(X >> 16), fys = (uint32_t)(Y >> 16);
     if (near_int(fxs) || near_int(fys)) return -1;
-    const int ix = (int)(X >> 32), iy = (int)(Y >> 32);
+    const int ix = (int)(X >> 48), iy = (int)(Y >> 48);
     if ((unsigned)ix > limx || (unsigned)iy > limy) return out | (out << 16);
     const int o = (iy - by0) * pitch + (ix - bx0);
     const float fx = frac_f(fxs), fy = frac_f(fys);
@@ -138,7 +136,8 @@ __device__ __forceinline__ int sample_fast2(P q1, P q2, int pitch, int bx0, int 
     return (vb < 0 || vr < 0) ? -1 : (vb | (vr << 16));
 }
 
-// Stages rows [y0, y1] x cols [x0, x1] of a plane (clipped by the caller).
+// Stages rows [y0, y1] x cols [x0, x1] of a plane (already clipped): warp per
+// row, lanes over 32-bit words.
 __device__ void stage(const uint8_t* __restrict__ g, int w, int x0, int y0, int x1, int y1,
                       uint8_t* dst, int* bb, int* staged) {
     const int xa = x0 & ~3;
@@ -184,6 +183,10 @@ struct ChromaMap {  // compose_plane constants (image_ops.cpp:167-177)
     bool crop;
 };
 
+__device__ __forceinline__ ChromaMap chroma_map(int w, int h, int cw, int ch, const CropGeom& g) {
+    return ChromaMap{(double)w / cw, (double)h / ch, g.mx != 0 || g.my != 0};
+}
+
 // compose_plane source coordinates of chroma pixel (x, y), reference order
 __device__ __forceinline__ void chroma_coords(const FramePlan& p, const CropGeom& g,
                                               const ChromaMap& m, int x, int y, double& px,
@@ -199,6 +202,30 @@ __device__ __forceinline__ void chroma_coords(const FramePlan& p, const CropGeom
     const double qy = dadd(dmul(-p.sn, dx), dmul(p.c, dy));
     px = dsub(ddiv(dadd(qx, 0.5), m.fxl), 0.5);
     py = dsub(ddiv(dadd(qy, 0.5), m.fyl), 0.5);
+}
+
+// Exact luma W pixel.  Level 1: the direct fp64 coordinates rx + u*c differ
+// from the reference's walked ones by <= (u+2) half-ulps, so unless a
+// coordinate sits that close to an integer / the frame edge, or the fp64
+// blend that close to a .5 tie, the direct result IS the reference result.
+// Level 2 (about once per two 1080p frames): fl_walk, the exact walk.
+__device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const FramePlan& p, int u,
+                           int v) {
+    double rx, ry;
+    row_start(p, v, rx, ry);
+    const double sx = dadd(rx, dmul((double)u, p.c)), sy = dsub(ry, dmul((double)u, p.sn));
+    const double mag = fmax(fmax(fabs(sx), fabs(sy)), fmax(fabs(rx), fabs(ry))) + fabs((double)u) + 2.0;
+    const double tol = ldexp(mag, -52) * ((double)u + 4.0);
+    bool sure = true;
+    const double fxx = sx - floor(sx), fyy = sy - floor(sy);
+    if (fmin(fxx, 1.0 - fxx) <= tol || fabs(sx) <= tol || fabs(sx - ((double)w - 1.0)) <= tol) sure = false;
+    if (fmin(fyy, 1.0 - fyy) <= tol || fabs(sy) <= tol || fabs(sy - ((double)h - 1.0)) <= tol) sure = false;
+    if (sure) {
+        const double val = sample_bilinear(g, w, h, sx, sy);
+        const double fr = val - floor(val);
+        if (fabs(fr - 0.5) > 255.0 * 4.0 * tol + 1e-9) return round_u8(val);
+    }
+    return round_u8(sample_bilinear(g, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
 }
 
 __device__ __forceinline__ uint8_t crop_exact(const Smem& S, int r, int c, int u0, int v0, int w,
@@ -225,156 +252,141 @@ __device__ __forceinline__ void chroma_exact(const FramePlan& p, const CropGeom&
     }
 }
 
-// min/max of 4 corner coordinates held by 4 consecutive lanes -> staged bbox
-__device__ __forceinline__ void corner_bbox(double x, double y, unsigned mask, int k, int w, int h,
-                                            int* bb) {
-    double xmn = x, xmx = x, ymn = y, ymx = y;
-#pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
-        xmn = fmin(xmn, __shfl_xor_sync(mask, xmn, o));
-        xmx = fmax(xmx, __shfl_xor_sync(mask, xmx, o));
-        ymn = fmin(ymn, __shfl_xor_sync(mask, ymn, o));
-        ymx = fmax(ymx, __shfl_xor_sync(mask, ymx, o));
+// Per-frame row tables + (frame 0) crop tables.
+__global__ void compose_prep_kernel(const FramePlan* __restrict__ plan, int w, int h, int cw, int ch,
+                                    CropGeom g, Tables T) {
+    const int f = blockIdx.y;
+    const FramePlan p = plan[f];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < h) {
+        double rx, ry;
+        row_start(p, i, rx, ry);
+        T.rxf[(size_t)f * h + i] = __double2ll_rn(dmul(rx, FIX48));
+        T.ryf[(size_t)f * h + i] = __double2ll_rn(dmul(ry, FIX48));
     }
-    if (k == 0) {
-        bb[0] = max(0, (int)floor(xmn) - 1);
-        bb[1] = max(0, (int)floor(ymn) - 1);
-        bb[2] = min(w - 1, (int)floor(xmx) + 2);
-        bb[3] = min(h - 1, (int)floor(ymx) + 2);
+    if (T.pxf && i < ch) {
+        double px, py;
+        chroma_coords(p, g, chroma_map(w, h, cw, ch, g), 0, i, px, py);
+        T.pxf[(size_t)f * ch + i] = __double2ll_rn(dmul(px, FIX48));
+        T.pyf[(size_t)f * ch + i] = __double2ll_rn(dmul(py, FIX48));
     }
-}
-
-// Exact luma W pixel.  Level 1: the direct fp64 coordinates rx + u*c differ
-// from the reference's walked ones by <= u*2^-43 px (|s| < 2^11; scaled
-// bound below), so unless a coordinate sits that close to an integer / the
-// frame edge, or the fp64 blend that close to a .5 tie, the direct result IS
-// the reference result.  Level 2 (about once per two 1080p frames): fl_walk.
-__device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const FramePlan& p,
-                           double rx, double ry, int u) {
-    const double sx = dadd(rx, dmul((double)u, p.c)), sy = dsub(ry, dmul((double)u, p.sn));
-    // walk-vs-direct bound: u half-ulps of the largest |coordinate| + 2 ulps of rounding
-    const double mag = fmax(fmax(fabs(sx), fabs(sy)), fmax(fabs(rx), fabs(ry))) + fabs((double)u) + 2.0;
-    const double tol = ldexp(mag, -52) * ((double)u + 4.0);
-    bool sure = true;
-    const double bx[3] = {sx - floor(sx), sx, sx - ((double)w - 1.0)};
-    const double by[3] = {sy - floor(sy), sy, sy - ((double)h - 1.0)};
-    // near an integer (x0 / fx change) or near either domain edge
-    if (fmin(bx[0], 1.0 - bx[0]) <= tol || fabs(bx[1]) <= tol || fabs(bx[2]) <= tol) sure = false;
-    if (fmin(by[0], 1.0 - by[0]) <= tol || fabs(by[1]) <= tol || fabs(by[2]) <= tol) sure = false;
-    if (sure) {
-        const double v = sample_bilinear(g, w, h, sx, sy);
-        const double fr = v - floor(v);
-        if (fabs(fr - 0.5) > 255.0 * 4.0 * tol + 1e-9) return round_u8(v);
+    if (f == 0) {
+        if (i < w) {  // crop_resize columns (image_ops.cpp:150-155)
+            const double sx = dadd((double)g.mx, dmul((double)i, g.step_x));
+            T.cx0[i] = (int)sx;
+            T.cfx[i] = dsub(sx, (double)(int)sx);
+        }
+        if (i < h) {
+            const double sy = dadd((double)g.my, dmul((double)i, g.step_y));
+            T.cy0[i] = (int)sy;
+            T.cfy[i] = dsub(sy, (double)(int)sy);
+        }
     }
-    return round_u8(sample_bilinear(g, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
 }
 
 template <bool LUMA, bool CHROMA>
 __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB, PlaneBatch CR,
                                                      const FramePlan* __restrict__ plan, CropGeom g,
-                                                     int tiles_x, uint8_t* __restrict__ oY,
+                                                     Tables T, int tiles_x, uint8_t* __restrict__ oY,
                                                      uint8_t* __restrict__ oCB,
                                                      uint8_t* __restrict__ oCR) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int f = blockIdx.y;
     const FramePlan p = plan[f];
-    const int tid = threadIdx.x;
-    // tile in the output plane (luma plane when LUMA, chroma plane otherwise)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = LUMA ? Y.w : CB.w, H = LUMA ? Y.h : CB.h;
     const int X0 = (blockIdx.x % tiles_x) * TW, Y0 = (blockIdx.x / tiles_x) * TH;
     const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
     const bool identity = g.mx == 0 && g.my == 0;
-    if (tid == 0) S.qn = 0;
-
-    // ------------------------------------------------------------ setup
-    const int w = Y.w, h = Y.h;
+    const int w = Y.w, h = Y.h, cw = CB.w, ch = CB.h;
     const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
-    int u0 = 0, v0 = 0, nu = 0, nv = 0;
-    const long long CF = p.cf, SNF = p.snf;
+    const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
+    const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
+    // ------------------------------------------------------------ setup (loads only)
+    int u0 = X0, v0 = Y0, nu = nx, nv = ny;
+    if (LUMA && !identity) {
+        u0 = __ldg(T.cx0 + X0);
+        v0 = __ldg(T.cy0 + Y0);
+        nu = min(__ldg(T.cx0 + X0 + nx - 1) + 1, w - 1) - u0 + 1;
+        nv = min(__ldg(T.cy0 + Y0 + ny - 1) + 1, h - 1) - v0 + 1;
+    }
+    if (tid == 0) S.qn = 0;
     if (LUMA) {
-        if (identity) {
-            u0 = X0;
-            v0 = Y0;
-            nu = nx;
-            nv = ny;
-        } else {
-            u0 = (int)dadd((double)g.mx, dmul((double)X0, g.step_x));
-            v0 = (int)dadd((double)g.my, dmul((double)Y0, g.step_y));
-            nu = min((int)dadd((double)g.mx, dmul((double)(X0 + nx - 1), g.step_x)) + 1, w - 1) - u0 + 1;
-            nv = min((int)dadd((double)g.my, dmul((double)(Y0 + ny - 1), g.step_y)) + 1, h - 1) - v0 + 1;
+        if (!identity) {
             if (tid < nx) {
-                const double sx = dadd((double)g.mx, dmul((double)(X0 + tid), g.step_x));
-                S.cx0[tid] = (int)sx;
-                S.cfx[tid] = dsub(sx, (double)(int)sx);
+                S.cx0[tid] = __ldg(T.cx0 + X0 + tid);
+                S.cfx[tid] = __ldg(T.cfx + X0 + tid);
                 S.cfxf[tid] = (float)S.cfx[tid];
-            }
-            if (tid >= 64 && tid < 64 + ny) {
-                const int r = tid - 64;
-                const double sy = dadd((double)g.my, dmul((double)(Y0 + r), g.step_y));
-                S.cy0[r] = (int)sy;
-                S.cfy[r] = dsub(sy, (double)(int)sy);
-                S.cfyf[r] = (float)S.cfy[r];
+            } else if (tid >= 64 && tid < 64 + ny) {
+                S.cy0[tid - 64] = __ldg(T.cy0 + Y0 + tid - 64);
+                S.cfy[tid - 64] = __ldg(T.cfy + Y0 + tid - 64);
+                S.cfyf[tid - 64] = (float)S.cfy[tid - 64];
             }
         }
-        if (tid >= 128 && tid < 128 + nv) {  // W rows: exact row starts + fixed point at u0
-            const int r = tid - 128;
-            double rx, ry;
-            row_start(p, v0 + r, rx, ry);
-            S.rxw[r] = rx;
-            S.ryw[r] = ry;
-            S.sxf[r] = __double2ll_rn(dmul(dadd(rx, dmul((double)u0, p.c)), FIX));
-            S.syf[r] = __double2ll_rn(dmul(dsub(ry, dmul((double)u0, p.sn)), FIX));
+        if (tid >= 128 && tid < 128 + nv) {
+            S.sxf[tid - 128] = __ldg(T.rxf + (size_t)f * h + v0 + tid - 128);
+            S.syf[tid - 128] = __ldg(T.ryf + (size_t)f * h + v0 + tid - 128);
         }
-        if (tid >= 224 && tid < 228) {  // luma source footprint of the W tile: 4 corners
-            const int k = tid - 224;
-            const int u = u0 + ((k & 1) ? nu - 1 : 0), v = v0 + ((k & 2) ? nv - 1 : 0);
-            double rx, ry;
-            row_start(p, v, rx, ry);
-            corner_bbox(rx + u * p.c, ry - u * p.sn, 0xFu << 0, k, w, h, S.bbox[0]);
+        if (warp == 7 && lane < 4) {  // luma footprint of the W tile: 4 corners
+            const int u = u0 + ((lane & 1) ? nu - 1 : 0), v = v0 + ((lane & 2) ? nv - 1 : 0);
+            const long long X = __ldg(T.rxf + (size_t)f * h + v) + (long long)u * p.cf;
+            const long long Yv = __ldg(T.ryf + (size_t)f * h + v) - (long long)u * p.snf;
+            int xmn = (int)(X >> 48), xmx = xmn, ymn = (int)(Yv >> 48), ymx = ymn;
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                xmn = min(xmn, __shfl_xor_sync(0xFu, xmn, o));
+                xmx = max(xmx, __shfl_xor_sync(0xFu, xmx, o));
+                ymn = min(ymn, __shfl_xor_sync(0xFu, ymn, o));
+                ymx = max(ymx, __shfl_xor_sync(0xFu, ymx, o));
+            }
+            if (lane == 0) {
+                S.bbox[0][0] = max(0, xmn - 1);
+                S.bbox[0][1] = max(0, ymn - 1);
+                S.bbox[0][2] = min(w - 1, xmx + 2);
+                S.bbox[0][3] = min(h - 1, ymx + 2);
+            }
         }
     }
-    const int cw = CB.w, ch = CB.h;
-    ChromaMap cm{0, 0, false};
-    long long KXX = 0, KYX = 0;
     if (CHROMA) {
-        cm.fxl = (double)w / cw;
-        cm.fyl = (double)h / ch;
-        cm.crop = g.mx != 0 || g.my != 0;
-        KXX = p.kxx;
-        KYX = p.kyx;
         if (tid >= 192 && tid < 192 + ny) {
-            const int r = tid - 192;
-            double px, py;
-            chroma_coords(p, g, cm, X0, Y0 + r, px, py);
-            S.pxf[r] = __double2ll_rn(dmul(px, FIX));
-            S.pyf[r] = __double2ll_rn(dmul(py, FIX));
+            S.pxf[tid - 192] = __ldg(T.pxf + (size_t)f * ch + Y0 + tid - 192);
+            S.pyf[tid - 192] = __ldg(T.pyf + (size_t)f * ch + Y0 + tid - 192);
         }
-        if (tid >= 228 && tid < 232) {  // chroma footprint: 4 corners
-            const int k = tid - 228;
-            double px, py;
-            chroma_coords(p, g, cm, X0 + ((k & 1) ? nx - 1 : 0), Y0 + ((k & 2) ? ny - 1 : 0), px, py);
-            corner_bbox(px, py, 0xFu << 4, k, cw, ch, S.bbox[1]);
+        if (warp == 7 && lane >= 4 && lane < 8) {  // chroma footprint: 4 corners
+            const int k = lane - 4;
+            const int x = X0 + ((k & 1) ? nx - 1 : 0), y = Y0 + ((k & 2) ? ny - 1 : 0);
+            const long long X = __ldg(T.pxf + (size_t)f * ch + y) + (long long)x * p.kxx;
+            const long long Yv = __ldg(T.pyf + (size_t)f * ch + y) + (long long)x * p.kyx;
+            int xmn = (int)(X >> 48), xmx = xmn, ymn = (int)(Yv >> 48), ymx = ymn;
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                xmn = min(xmn, __shfl_xor_sync(0xF0u, xmn, o));
+                xmx = max(xmx, __shfl_xor_sync(0xF0u, xmx, o));
+                ymn = min(ymn, __shfl_xor_sync(0xF0u, ymn, o));
+                ymx = max(ymx, __shfl_xor_sync(0xF0u, ymx, o));
+            }
             if (k == 0) {
-                // bbox[2] mirrors bbox[1] (same geometry for both chroma planes)
+                S.bbox[1][0] = max(0, xmn - 1);
+                S.bbox[1][1] = max(0, ymn - 1);
+                S.bbox[1][2] = min(cw - 1, xmx + 2);
+                S.bbox[1][3] = min(ch - 1, ymx + 2);
             }
         }
     }
     __syncthreads();
     // ------------------------------------------------------------ staging
-    const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
-    const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
-    int bb[3][4];
+    int bb0[4], bb1[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        bb[0][j] = S.bbox[0][j];
-        bb[1][j] = bb[2][j] = S.bbox[1][j];
+        bb0[j] = S.bbox[0][j];
+        bb1[j] = S.bbox[1][j];
     }
     __syncthreads();
-    if (LUMA) stage(gy, w, bb[0][0], bb[0][1], bb[0][2], bb[0][3], S.src[0], S.bbox[0], &S.staged[0]);
+    if (LUMA) stage(gy, w, bb0[0], bb0[1], bb0[2], bb0[3], S.src[0], S.bbox[0], &S.staged[0]);
     if (CHROMA) {
-        stage(gcb, cw, bb[1][0], bb[1][1], bb[1][2], bb[1][3], S.src[1], S.bbox[1], &S.staged[1]);
-        stage(gcr, cw, bb[2][0], bb[2][1], bb[2][2], bb[2][3], S.src[2], S.bbox[2], &S.staged[2]);
+        stage(gcb, cw, bb1[0], bb1[1], bb1[2], bb1[3], S.src[1], S.bbox[1], &S.staged[1]);
+        stage(gcr, cw, bb1[0], bb1[1], bb1[2], bb1[3], S.src[2], S.bbox[2], &S.staged[2]);
     }
     __syncthreads();
     // ------------------------------------------------------------ luma W tile
@@ -382,9 +394,9 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
         const int wp = identity ? TW : WTW;
         const unsigned limx = (unsigned)(w - 2), limy = (unsigned)(h - 2);
-        const int lane = tid & 31, warp = tid >> 5;
         const bool stg = S.staged[0];
         const int bx0 = S.bbox[0][0], by0 = S.bbox[0][1];
+        const long long CF = p.cf, SNF = p.snf;
         // warp per row, 2 adjacent pixels per lane (64 columns), tail columns after
         for (int r = warp; r < nv; r += NT / 32) {
             const long long SXr = S.sxf[r], SYr = S.syf[r];
@@ -392,7 +404,8 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
             for (int k = 0; k < 2; ++k) {
                 const int c = 2 * lane + k;
                 if (c >= nu) break;
-                const long long SX = SXr + (long long)c * CF, SY = SYr - (long long)c * SNF;
+                const long long u = u0 + c;
+                const long long SX = SXr + u * CF, SY = SYr - u * SNF;
                 const int val = stg ? sample_fast(&S.src[0][0], SRC_W, bx0, by0, limx, limy, SX, SY, 0)
                                     : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
                 if (val < 0) push(S, (unsigned)(r * nu + c));
@@ -401,7 +414,8 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         }
         for (int i = tid; i < (nu - 64) * nv; i += NT) {  // columns 64.. (at most 2)
             const int r = i / (nu - 64), c = 64 + i - r * (nu - 64);
-            const long long SX = S.sxf[r] + (long long)c * CF, SY = S.syf[r] - (long long)c * SNF;
+            const long long u = u0 + c;
+            const long long SX = S.sxf[r] + u * CF, SY = S.syf[r] - u * SNF;
             const int val = stg ? sample_fast(&S.src[0][0], SRC_W, bx0, by0, limx, limy, SX, SY, 0)
                                 : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
             if (val < 0) push(S, (unsigned)(r * nu + c));
@@ -412,12 +426,12 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         if (nq <= QCAP) {
             for (int k = tid; k < nq; k += NT) {  // exact reference path
                 const int i = (int)(S.q[k] & 0x3FFFFFFF), r = i / nu, c = i - r * nu;
-                wdst[r * wp + c] = w_exact(gy, w, h, p, S.rxw[r], S.ryw[r], u0 + c);
+                wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
             }
         } else {  // overflow: every pixel exactly (never seen in practice)
             for (int i = tid; i < nu * nv; i += NT) {
                 const int r = i / nu, c = i - r * nu;
-                wdst[r * wp + c] = w_exact(gy, w, h, p, S.rxw[r], S.ryw[r], u0 + c);
+                wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
             }
         }
         __syncthreads();
@@ -425,7 +439,6 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         __syncthreads();
         // ---- crop_resize of the warped tile (image_ops.cpp:151-157)
         if (!identity) {
-            const int lane = tid & 31, warp = tid >> 5;
             int x0[2], x1[2];
             float fxv[2];
 #pragma unroll
@@ -451,18 +464,20 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         }
     }
     // ------------------------------------------------------------ chroma
+    const ChromaMap cm = chroma_map(w, h, cw, ch, g);
     if (CHROMA) {
         const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
-        const int lane = tid & 31, warp = tid >> 5;
         const bool stg = S.staged[1] && S.staged[2];
         const int bx0 = S.bbox[1][0], by0 = S.bbox[1][1];
+        const long long KX = p.kxx, KY = p.kyx;
         for (int r = warp; r < ny; r += NT / 32) {
             const long long PXr = S.pxf[r], PYr = S.pyf[r];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int c = 2 * lane + k;
                 if (c >= nx) break;
-                const long long PX = PXr + (long long)c * KXX, PY = PYr + (long long)c * KYX;
+                const long long x = X0 + c;
+                const long long PX = PXr + x * KX, PY = PYr + x * KY;
                 const int v = stg ? sample_fast2(&S.src[1][0], &S.src[2][0], SRC_W, bx0, by0, limx,
                                                  limy, PX, PY, 128)
                                   : sample_fast2(gcb, gcr, cw, 0, 0, limx, limy, PX, PY, 128);
@@ -509,15 +524,13 @@ __global__ void __launch_bounds__(NT) compose_kernel(PlaneBatch Y, PlaneBatch CB
         const bool vec = nx == TW && ((pw & 15) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
         if (vec) {
             for (int i = tid; i < ny * (TW / 16); i += NT) {
-                const int r = i / (TW / 16), c = (i % (TW / 16)) * 16;
+                const int r = i >> 2, c = (i & 3) * 16;
                 const uint4 v = *reinterpret_cast<const uint4*>(&S.out[k][r][c]);
                 __stcs(reinterpret_cast<uint4*>(base + (size_t)(Y0 + r) * pw + X0 + c), v);
             }
         } else {
-            for (int i = tid; i < nx * ny; i += NT) {
-                const int r = i / nx, c = i - r * nx;
-                base[(size_t)(Y0 + r) * pw + X0 + c] = S.out[k][r][c];
-            }
+            for (int r = warp; r < ny; r += NT / 32)
+                for (int c = lane; c < nx; c += 32) base[(size_t)(Y0 + r) * pw + X0 + c] = S.out[k][r][c];
         }
     }
 }
@@ -537,7 +550,8 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
 
 template <bool L, bool C>
 void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
-                  CropGeom g, uint8_t* oy, uint8_t* ocb, uint8_t* ocr, cudaStream_t st) {
+                  CropGeom g, const Tables& T, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
+                  cudaStream_t st) {
     const int W = L ? y.w : cb.w, H = L ? y.h : cb.h;
     const int tx = (W + TW - 1) / TW, ty = (H + TH - 1) / TH;
     const size_t smem = sizeof(Smem);
@@ -548,11 +562,65 @@ void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* p
         if (a.base) a.base += (size_t)f0 * a.stride;
         if (b.base) b.base += (size_t)f0 * b.stride;
         if (c.base) c.base += (size_t)f0 * c.stride;
+        Tables t = T;
+        t.rxf += (size_t)f0 * T.h;
+        t.ryf += (size_t)f0 * T.h;
+        if (t.pxf) {
+            t.pxf += (size_t)f0 * T.ch;
+            t.pyf += (size_t)f0 * T.ch;
+        }
         dim3 grid(tx * ty, nf);
         compose_kernel<L, C><<<grid, NT, smem, st>>>(
-            a, b, c, plan + f0, g, tx, oy ? oy + (size_t)f0 * y.stride : nullptr,
+            a, b, c, plan + f0, g, t, tx, oy ? oy + (size_t)f0 * y.stride : nullptr,
             ocb ? ocb + (size_t)f0 * cb.stride : nullptr, ocr ? ocr + (size_t)f0 * cr.stride : nullptr);
     }
+}
+
+void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                 double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr, cudaStream_t st) {
+    if (frames <= 0) return;
+    const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
+    const bool chroma = cb.base && cr.base && out_cb && out_cr;
+    const int w = y.w, h = y.h, cw = chroma ? cb.w : 0, ch = chroma ? cb.h : 0;
+    // per-launch tables, stream-ordered allocation
+    const size_t nrow = (size_t)frames * h, ncrow = (size_t)frames * ch;
+    const size_t bytes = sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) + 256;
+    char* buf = nullptr;
+    cudaMallocAsync((void**)&buf, bytes, st);
+    Tables T;
+    long long* q = reinterpret_cast<long long*>(buf);
+    T.rxf = q;
+    T.ryf = q + nrow;
+    T.pxf = chroma ? q + 2 * nrow : nullptr;
+    T.pyf = chroma ? q + 2 * nrow + ncrow : nullptr;
+    double* dd = reinterpret_cast<double*>(q + 2 * nrow + 2 * ncrow);
+    T.cfx = dd;
+    T.cfy = dd + w;
+    int* ii = reinterpret_cast<int*>(dd + w + h);
+    T.cx0 = ii;
+    T.cy0 = ii + w;
+    T.h = h;
+    T.ch = ch;
+    const int rows = max(max(h, ch), w);
+    for (int f0 = 0; f0 < frames; f0 += 65535) {
+        const int nf = min(65535, frames - f0);
+        Tables t = T;
+        t.rxf += (size_t)f0 * h;
+        t.ryf += (size_t)f0 * h;
+        if (t.pxf) {
+            t.pxf += (size_t)f0 * ch;
+            t.pyf += (size_t)f0 * ch;
+        }
+        dim3 grid((rows + 127) / 128, nf);
+        compose_prep_kernel<<<grid, 128, 0, st>>>(plan + f0, w, h, cw, ch, g, t);
+    }
+    if (chroma && cb.w == y.w && cb.h == y.h) {
+        launch_tiles<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st);
+    } else {
+        launch_tiles<true, false>(y, cb, cr, plan, frames, g, T, out_y, nullptr, nullptr, st);
+        if (chroma) launch_tiles<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st);
+    }
+    cudaFreeAsync(buf, st);
 }
 
 }  // namespace
@@ -560,22 +628,14 @@ void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* p
 void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
                     double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
                     cudaStream_t st) {
-    if (frames <= 0) return;
-    const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
-    const bool chroma = cb.base && cr.base && out_cb && out_cr;
-    if (chroma && cb.w == y.w && cb.h == y.h) {
-        launch_tiles<true, true>(y, cb, cr, plan, frames, g, out_y, out_cb, out_cr, st);
-    } else {
-        launch_tiles<true, false>(y, cb, cr, plan, frames, g, out_y, nullptr, nullptr, st);
-        if (chroma) launch_tiles<false, true>(y, cb, cr, plan, frames, g, nullptr, out_cb, out_cr, st);
-    }
+    run_compose(y, cb, cr, plan, frames, crop_ratio, out_y, out_cb, out_cr, st);
 }
 
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st) {
     // warp_similarity == compose with crop_ratio 0 (crop_resize returns its input)
     PlaneBatch y{src, (size_t)w * h, w, h}, none{nullptr, 0, 0, 0};
-    launch_tiles<true, false>(y, none, none, plan, 1, crop_geom(w, h, 0.0), out, nullptr, nullptr, st);
+    run_compose(y, none, none, plan, 1, 0.0, out, nullptr, nullptr, st);
 }
 
 void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,

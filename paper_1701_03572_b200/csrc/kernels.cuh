@@ -27,14 +27,14 @@ struct DevPyramid {
 struct FramePlan {
     double tx, ty, theta, s;  // correction transform (delta_to_transform)
     double c, sn;             // cos(theta)/s, sin(theta)/s (warp_similarity, image_ops.cpp:121-122)
-    // K8 fast-path constants (32.32 fixed point): luma walk steps and the
+    // K8 fast-path steps in 16.48 fixed point: luma walk increments and the
     // chroma map's d/dx; filled by finish_plan() for the frame geometry
     long long cf, snf, kxx, kyx;
 };
 
 // Fills the fixed-point members of a FramePlan (host or device).
 __host__ __device__ inline void finish_plan(FramePlan& p, int w, int h, int cw, int ch, double crop) {
-    const double FIXP = 4294967296.0;
+    const double FIXP = 281474976710656.0;  // 2^48
     p.cf = llrint(p.c * FIXP);
     p.snf = llrint(p.sn * FIXP);
     p.kxx = p.kyx = 0;
