@@ -28,6 +28,13 @@
 // reference's sequential row walk (sx += c, image_ops.cpp:124-131), which
 // fl_walk (walk.h) reproduces bit for bit in closed form.  About 0.05% of
 // pixels take the exact path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "walk.h"
@@ -66,8 +73,18 @@ struct Tables {
     long long *pxf, *pyf;  // [frames][ch] chroma source coords of (0, y) (16.48)
     int *cx0, *cy0;        // crop_resize integer parts per column [w] / row [h]
     double *cfx, *cfy;     // and fractions
+    int4* tiles;           // [frames][tiles] TMA tile parameters (TileParams), or null
     int h, ch;
 };
+
+// Per-tile parameters of the TMA kernel, precomputed one thread per tile:
+// W region and the TMA box origins of the luma / chroma source footprints.
+struct TileParams {
+    int u0, v0, nu, nv;
+    int lbx, lby, cbx, cby;
+    int lfit, cfit, pad0, pad1;
+};
+static_assert(sizeof(TileParams) == 48, "TileParams is 3 x int4");
 
 struct Smem {
     uint8_t src[3][SRC_H * SRC_W];
@@ -167,6 +184,11 @@ __device__ void stage(const uint8_t* __restrict__ g, int w, int x0, int y0, int 
     }
 }
 
+__device__ __forceinline__ void push_q(int& qn, unsigned* q, unsigned item) {
+    const int k = atomicAdd(&qn, 1);
+    if (k < QCAP) q[k] = item;
+}
+
 __device__ __forceinline__ void push(Smem& S, unsigned item) {
     const int k = atomicAdd(&S.qn, 1);
     if (k < QCAP) S.q[k] = item;
@@ -226,6 +248,19 @@ __device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const Fr
         if (fabs(fr - 0.5) > 255.0 * 4.0 * tol + 1e-9) return round_u8(val);
     }
     return round_u8(sample_bilinear(g, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
+}
+
+__device__ __forceinline__ uint8_t crop_exact_t(const uint8_t (*wt)[WTW], const int* cx0,
+                                                const int* cy0, const double* cfx,
+                                                const double* cfy, int r, int c, int u0, int v0,
+                                                int w, int h) {
+    const int x0 = cx0[c], y0 = cy0[r];
+    const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+    const double a = wt[y0 - v0][x0 - u0], b = wt[y0 - v0][x1 - u0];
+    const double cc = wt[y1 - v0][x0 - u0], d = wt[y1 - v0][x1 - u0];
+    const double top = dadd(a, dmul(cfx[c], dsub(b, a)));
+    const double bot = dadd(cc, dmul(cfx[c], dsub(d, cc)));
+    return round_u8(dadd(top, dmul(cfy[r], dsub(bot, top))));
 }
 
 __device__ __forceinline__ uint8_t crop_exact(const Smem& S, int r, int c, int u0, int v0, int w,
@@ -548,6 +583,385 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
     out[(size_t)y * w + x] = round_u8(sample_bilinear(src, w, h, sx, sy));
 }
 
+
+// ===================================================================== TMA
+// Persistent variant: each CTA walks tiles t = blockIdx.x + k*gridDim.x; the
+// source footprints of tile t+1 are fetched by TMA (cp.async.bulk.tensor, one
+// instruction per plane) into the other half of a double buffer while tile
+// t is computed; an mbarrier per buffer carries the transaction bytes.
+constexpr int BW = 80, BH = 48;  // TMA box per plane (footprint of a 64x32 tile up to ~10 deg)
+
+struct SmemT {
+    alignas(128) uint8_t box[2][3][BH * BW];
+    uint8_t wt[WTH][WTW];
+    alignas(16) uint8_t out[3][TH][TW];
+    double cfx[TW], cfy[TH];
+    float cfxf[TW], cfyf[TH];
+    int cx0[TW], cy0[TH];
+    long long sxf[WTH], syf[WTH];
+    long long pxf[TH], pyf[TH];
+    TileParams tp[2];
+    unsigned long long mbar[2];
+    int qn;
+    unsigned q[QCAP];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, int x, int y, int f,
+                                          uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(f), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    }
+}
+
+// one thread per (frame, tile): W region + TMA box origins (integer math on the row tables)
+__global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames, int tiles_x,
+                                 int tiles_y, int W, int H, int w, int h, int cw, int ch,
+                                 CropGeom g, Tables T, int luma, int chroma) {
+    const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long tpf = (long long)tiles_x * tiles_y;
+    if (id >= tpf * frames) return;
+    const int f = (int)(id / tpf), t = (int)(id - f * tpf);
+    const int X0 = (t % tiles_x) * TW, Y0 = (t / tiles_x) * TH;
+    const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
+    const FramePlan p = plan[f];
+    TileParams tp;
+    memset(&tp, 0, sizeof tp);
+    const bool identity = g.mx == 0 && g.my == 0;
+    if (luma) {
+        int u0 = X0, v0 = Y0, nu = nx, nv = ny;
+        if (!identity) {
+            u0 = T.cx0[X0];
+            v0 = T.cy0[Y0];
+            nu = min(T.cx0[X0 + nx - 1] + 1, w - 1) - u0 + 1;
+            nv = min(T.cy0[Y0 + ny - 1] + 1, h - 1) - v0 + 1;
+        }
+        tp.u0 = u0;
+        tp.v0 = v0;
+        tp.nu = nu;
+        tp.nv = nv;
+        int xmn = INT_MAX, xmx = INT_MIN, ymn = INT_MAX, ymx = INT_MIN;
+        for (int k = 0; k < 4; ++k) {
+            const int u = u0 + ((k & 1) ? nu - 1 : 0), v = v0 + ((k & 2) ? nv - 1 : 0);
+            const long long X = T.rxf[(size_t)f * h + v] + (long long)u * p.cf;
+            const long long Yv = T.ryf[(size_t)f * h + v] - (long long)u * p.snf;
+            xmn = min(xmn, (int)(X >> 48));
+            xmx = max(xmx, (int)(X >> 48));
+            ymn = min(ymn, (int)(Yv >> 48));
+            ymx = max(ymx, (int)(Yv >> 48));
+        }
+        tp.lbx = xmn - 1;
+        tp.lby = ymn - 1;
+        tp.lfit = (xmx + 2) - tp.lbx < BW && (ymx + 2) - tp.lby < BH;
+    }
+    if (chroma) {
+        int xmn = INT_MAX, xmx = INT_MIN, ymn = INT_MAX, ymx = INT_MIN;
+        for (int k = 0; k < 4; ++k) {
+            const int x = X0 + ((k & 1) ? nx - 1 : 0), y = Y0 + ((k & 2) ? ny - 1 : 0);
+            const long long X = T.pxf[(size_t)f * ch + y] + (long long)x * p.kxx;
+            const long long Yv = T.pyf[(size_t)f * ch + y] + (long long)x * p.kyx;
+            xmn = min(xmn, (int)(X >> 48));
+            xmx = max(xmx, (int)(X >> 48));
+            ymn = min(ymn, (int)(Yv >> 48));
+            ymx = max(ymx, (int)(Yv >> 48));
+        }
+        tp.cbx = xmn - 1;
+        tp.cby = ymn - 1;
+        tp.cfit = (xmx + 2) - tp.cbx < BW && (ymx + 2) - tp.cby < BH;
+    }
+    int4* dst = T.tiles + 3 * id;
+    const int4* src = reinterpret_cast<const int4*>(&tp);
+    dst[0] = src[0];
+    dst[1] = src[1];
+    dst[2] = src[2];
+}
+
+template <bool LUMA, bool CHROMA>
+__global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
+    PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
+    Tables T, int tiles_x, int tiles_y, int frames, const __grid_constant__ CUtensorMap mapY,
+    const __grid_constant__ CUtensorMap mapCB, const __grid_constant__ CUtensorMap mapCR,
+    uint8_t* __restrict__ oY, uint8_t* __restrict__ oCB, uint8_t* __restrict__ oCR) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = LUMA ? Y.w : CB.w, H = LUMA ? Y.h : CB.h;
+    const int w = Y.w, h = Y.h, cw = CB.w, ch = CB.h;
+    const bool identity = g.mx == 0 && g.my == 0;
+    const long long tpf = (long long)tiles_x * tiles_y;
+    const long long total = tpf * frames;
+    const uint32_t bytes_l = LUMA ? BW * BH : 0, bytes_c = CHROMA ? 2 * BW * BH : 0;
+
+    auto issue = [&](long long t, int b) {  // thread 0: params + TMA of tile t into buffer b
+        const int4* src = T.tiles + 3 * t;
+        int4* dst = reinterpret_cast<int4*>(&S.tp[b]);
+        dst[0] = src[0];
+        dst[1] = src[1];
+        dst[2] = src[2];
+        const TileParams& tp = S.tp[b];
+        const int f = (int)(t / tpf);
+        const uint32_t bar = smem_u32(&S.mbar[b]);
+        const uint32_t bytes = (LUMA && tp.lfit ? bytes_l : 0) + (CHROMA && tp.cfit ? bytes_c : 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        if (LUMA && tp.lfit) tma_load3(smem_u32(&S.box[b][0][0]), &mapY, tp.lbx, tp.lby, f, bar);
+        if (CHROMA && tp.cfit) {
+            tma_load3(smem_u32(&S.box[b][1][0]), &mapCB, tp.cbx, tp.cby, f, bar);
+            tma_load3(smem_u32(&S.box[b][2][0]), &mapCR, tp.cbx, tp.cby, f, bar);
+        }
+    };
+    long long t = blockIdx.x;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (t < total) issue(t, 0);
+    }
+    __syncthreads();
+    for (int k = 0; t < total; ++k, t += gridDim.x) {
+        const int b = k & 1;
+        const long long tn = t + gridDim.x;
+        if (tid == 0 && tn < total) issue(tn, b ^ 1);
+        const int f = (int)(t / tpf), ti = (int)(t - f * tpf);
+        const int X0 = (ti % tiles_x) * TW, Y0 = (ti / tiles_x) * TH;
+        const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
+        const FramePlan p = plan[f];
+        const TileParams tp = S.tp[b];
+        const int u0 = tp.u0, v0 = tp.v0, nu = tp.nu, nv = tp.nv;
+        const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
+        const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
+        const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
+        if (tid == 0) S.qn = 0;
+        if (LUMA) {
+            if (!identity) {
+                if (tid < nx) {
+                    S.cx0[tid] = __ldg(T.cx0 + X0 + tid);
+                    S.cfx[tid] = __ldg(T.cfx + X0 + tid);
+                    S.cfxf[tid] = (float)S.cfx[tid];
+                } else if (tid >= 64 && tid < 64 + ny) {
+                    S.cy0[tid - 64] = __ldg(T.cy0 + Y0 + tid - 64);
+                    S.cfy[tid - 64] = __ldg(T.cfy + Y0 + tid - 64);
+                    S.cfyf[tid - 64] = (float)S.cfy[tid - 64];
+                }
+            }
+            if (tid >= 128 && tid < 128 + nv) {
+                S.sxf[tid - 128] = __ldg(T.rxf + (size_t)f * h + v0 + tid - 128);
+                S.syf[tid - 128] = __ldg(T.ryf + (size_t)f * h + v0 + tid - 128);
+            }
+        }
+        if (CHROMA && tid >= 192 && tid < 192 + ny) {
+            S.pxf[tid - 192] = __ldg(T.pxf + (size_t)f * ch + Y0 + tid - 192);
+            S.pyf[tid - 192] = __ldg(T.pyf + (size_t)f * ch + Y0 + tid - 192);
+        }
+        mbar_wait(smem_u32(&S.mbar[b]), (uint32_t)((k >> 1) & 1));
+        __syncthreads();
+        // ---------------------------------------------------- luma W tile
+        if (LUMA) {
+            uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
+            const int wp = identity ? TW : WTW;
+            const unsigned limx = (unsigned)(w - 2), limy = (unsigned)(h - 2);
+            const bool stg = tp.lfit;
+            const long long CF = p.cf, SNF = p.snf;
+            const uint8_t* sb = &S.box[b][0][0];
+            for (int i = tid; i < nv * 68; i += NT) {  // 68 = 17 groups of 4 columns? flat row-major
+                const int r = i / 68, c = i - r * 68;
+                if (c >= nu) continue;
+                const long long u = u0 + c;
+                const long long SX = S.sxf[r] + u * CF, SY = S.syf[r] - u * SNF;
+                const int val = stg ? sample_fast(sb, BW, tp.lbx, tp.lby, limx, limy, SX, SY, 0)
+                                    : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
+                if (val < 0) push_q(S.qn, S.q, (unsigned)(r * nu + c));
+                else wdst[r * wp + c] = (uint8_t)val;
+            }
+            __syncthreads();
+            const int nq = S.qn;
+            if (nq <= QCAP) {
+                for (int q = tid; q < nq; q += NT) {
+                    const int i = (int)(S.q[q] & 0x3FFFFFFF), r = i / nu, c = i - r * nu;
+                    wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
+                }
+            } else {
+                for (int i = tid; i < nu * nv; i += NT) {
+                    const int r = i / nu, c = i - r * nu;
+                    wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) S.qn = 0;
+            __syncthreads();
+            if (!identity) {
+                int x0[2], x1[2];
+                float fxv[2];
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const int c = min(2 * lane + kk, nx - 1);
+                    x0[kk] = S.cx0[c] - u0;
+                    x1[kk] = min(S.cx0[c] + 1, w - 1) - u0;
+                    fxv[kk] = S.cfxf[c];
+                }
+                for (int r = warp; r < ny; r += NT / 32) {
+                    const int y0 = S.cy0[r] - v0, y1 = min(S.cy0[r] + 1, h - 1) - v0;
+                    const float fy = S.cfyf[r];
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int c = 2 * lane + kk;
+                        if (c >= nx) break;
+                        const int val = blend_round(S.wt[y0][x0[kk]], S.wt[y0][x1[kk]], S.wt[y1][x0[kk]],
+                                                    S.wt[y1][x1[kk]], fxv[kk], fy);
+                        if (val < 0) push_q(S.qn, S.q, (1u << 30) | (unsigned)(r * nx + c));
+                        else S.out[0][r][c] = (uint8_t)val;
+                    }
+                }
+            }
+        }
+        // ---------------------------------------------------- chroma
+        const ChromaMap cm = chroma_map(w, h, cw, ch, g);
+        if (CHROMA) {
+            const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
+            const bool stg = tp.cfit;
+            const long long KX = p.kxx, KY = p.kyx;
+            const uint8_t* s1 = &S.box[b][1][0];
+            const uint8_t* s2 = &S.box[b][2][0];
+            for (int r = warp; r < ny; r += NT / 32) {
+                const long long PXr = S.pxf[r], PYr = S.pyf[r];
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const int c = 2 * lane + kk;
+                    if (c >= nx) break;
+                    const long long x = X0 + c;
+                    const long long PX = PXr + x * KX, PY = PYr + x * KY;
+                    const int v = stg ? sample_fast2(s1, s2, BW, tp.cbx, tp.cby, limx, limy, PX, PY, 128)
+                                      : sample_fast2(gcb, gcr, cw, 0, 0, limx, limy, PX, PY, 128);
+                    if (v < 0) {
+                        push_q(S.qn, S.q, (2u << 30) | (unsigned)(r * nx + c));
+                    } else {
+                        S.out[1][r][c] = (uint8_t)(v & 0xFF);
+                        S.out[2][r][c] = (uint8_t)(v >> 16);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        {
+            const int nq = S.qn;
+            if (nq <= QCAP) {
+                for (int q = tid; q < nq; q += NT) {
+                    const unsigned item = S.q[q];
+                    const int kind = item >> 30, i = (int)(item & 0x3FFFFFFF);
+                    const int r = i / nx, c = i - r * nx;
+                    if (LUMA && kind == 1) {
+                        S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
+                    } else if (CHROMA && kind == 2) {
+                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
+                                     S.out[2][r][c]);
+                    }
+                }
+            } else {
+                for (int i = tid; i < nx * ny; i += NT) {
+                    const int r = i / nx, c = i - r * nx;
+                    if (LUMA && !identity)
+                        S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
+                    if (CHROMA)
+                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
+                                     S.out[2][r][c]);
+                }
+            }
+        }
+        __syncthreads();
+        for (int kp = (LUMA ? 0 : 1); kp < (CHROMA ? 3 : 1); ++kp) {
+            uint8_t* base = kp == 0 ? oY + (size_t)f * Y.stride
+                                    : (kp == 1 ? oCB + (size_t)f * CB.stride : oCR + (size_t)f * CR.stride);
+            const int pw = kp == 0 ? w : cw;
+            if (nx == TW) {  // 16-byte stores (pitch % 16 == 0 is a TMA precondition)
+                for (int i = tid; i < ny * (TW / 16); i += NT) {
+                    const int r = i >> 2, c = (i & 3) * 16;
+                    const uint4 v = *reinterpret_cast<const uint4*>(&S.out[kp][r][c]);
+                    __stcs(reinterpret_cast<uint4*>(base + (size_t)(Y0 + r) * pw + X0 + c), v);
+                }
+            } else {
+                for (int r = warp; r < ny; r += NT / 32)
+                    for (int c = lane; c < nx; c += 32) base[(size_t)(Y0 + r) * pw + X0 + c] = S.out[kp][r][c];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+typedef PFN_cuTensorMapEncodeTiled_v12000 EncodeFn;
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const uint8_t* base, int w, int h, int frames) {
+    EncodeFn enc = get_encode();
+    if (!enc || !base) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {(cuuint64_t)w, (cuuint64_t)w * h};
+    const cuuint32_t box[3] = {BW, BH, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA eligibility: 16-byte aligned planes with 16-byte pitches
+bool tma_ok(const PlaneBatch& p) {
+    return p.base && (p.w % 16) == 0 && (reinterpret_cast<uintptr_t>(p.base) % 16) == 0 &&
+           (p.stride % 16) == 0 && p.stride == (size_t)p.w * p.h;
+}
+
+template <bool L, bool C>
+bool launch_tma(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                CropGeom g, Tables T, uint8_t* oy, uint8_t* ocb, uint8_t* ocr, cudaStream_t st) {
+    if ((L && !tma_ok(y)) || (C && (!tma_ok(cb) || !tma_ok(cr)))) return false;
+    CUtensorMap my, mb, mr;
+    memset(&my, 0, sizeof my);
+    memset(&mb, 0, sizeof mb);
+    memset(&mr, 0, sizeof mr);
+    if (L && !make_map(&my, y.base, y.w, y.h, frames)) return false;
+    if (C && (!make_map(&mb, cb.base, cb.w, cb.h, frames) || !make_map(&mr, cr.base, cr.w, cr.h, frames)))
+        return false;
+    const int W = L ? y.w : cb.w, H = L ? y.h : cb.h;
+    const int tx = (W + TW - 1) / TW, ty = (H + TH - 1) / TH;
+    const long long total = (long long)tx * ty * frames;
+    tile_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plan, frames, tx, ty, W, H, y.w, y.h,
+                                                                    cb.w, cb.h, g, T, L ? 1 : 0, C ? 1 : 0);
+    const size_t smem = sizeof(SmemT);
+    cudaFuncSetAttribute(compose_tma_kernel<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, compose_tma_kernel<L, C>, NT, smem);
+    const long long grid = std::min<long long>(total, (long long)sms * std::max(per, 1));
+    compose_tma_kernel<L, C><<<(unsigned)grid, NT, smem, st>>>(y, cb, cr, plan, g, T, tx, ty, frames, my, mb, mr,
+                                                               oy, ocb, ocr);
+    return true;
+}
+
 template <bool L, bool C>
 void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
                   CropGeom g, const Tables& T, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
@@ -584,7 +998,13 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
     const int w = y.w, h = y.h, cw = chroma ? cb.w : 0, ch = chroma ? cb.h : 0;
     // per-launch tables, stream-ordered allocation
     const size_t nrow = (size_t)frames * h, ncrow = (size_t)frames * ch;
-    const size_t bytes = sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) + 256;
+    const int tw_tiles = ((chroma && !(cb.w == y.w && cb.h == y.h)) ? std::max((w + TW - 1) / TW, (cw + TW - 1) / TW)
+                                                                       : (w + TW - 1) / TW);
+    const int th_tiles = ((chroma && !(cb.w == y.w && cb.h == y.h)) ? std::max((h + TH - 1) / TH, (ch + TH - 1) / TH)
+                                                                       : (h + TH - 1) / TH);
+    const size_t ntiles = (size_t)tw_tiles * th_tiles * frames;
+    const size_t bytes = sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) +
+                         sizeof(TileParams) * ntiles + 512;
     char* buf = nullptr;
     cudaMallocAsync((void**)&buf, bytes, st);
     Tables T;
@@ -601,6 +1021,7 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
     T.cy0 = ii + w;
     T.h = h;
     T.ch = ch;
+    T.tiles = reinterpret_cast<int4*>(((uintptr_t)(ii + w + h) + 15) & ~uintptr_t(15));
     const int rows = max(max(h, ch), w);
     for (int f0 = 0; f0 < frames; f0 += 65535) {
         const int nf = min(65535, frames - f0);
@@ -614,11 +1035,16 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
         dim3 grid((rows + 127) / 128, nf);
         compose_prep_kernel<<<grid, 128, 0, st>>>(plan + f0, w, h, cw, ch, g, t);
     }
+    const bool frames_ok = frames <= 65535;
     if (chroma && cb.w == y.w && cb.h == y.h) {
-        launch_tiles<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st);
+        if (!(frames_ok && launch_tma<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st)))
+            launch_tiles<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st);
     } else {
-        launch_tiles<true, false>(y, cb, cr, plan, frames, g, T, out_y, nullptr, nullptr, st);
-        if (chroma) launch_tiles<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st);
+        if (!(frames_ok && launch_tma<true, false>(y, cb, cr, plan, frames, g, T, out_y, nullptr, nullptr, st)))
+            launch_tiles<true, false>(y, cb, cr, plan, frames, g, T, out_y, nullptr, nullptr, st);
+        if (chroma &&
+            !(frames_ok && launch_tma<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st)))
+            launch_tiles<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st);
     }
     cudaFreeAsync(buf, st);
 }
