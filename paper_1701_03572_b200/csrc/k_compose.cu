@@ -589,7 +589,11 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
 // source footprints of tile t+1 are fetched by TMA (cp.async.bulk.tensor, one
 // instruction per plane) into the other half of a double buffer while tile
 // t is computed; an mbarrier per buffer carries the transaction bytes.
-constexpr int BW = 80, BH = 48;  // TMA box per plane (footprint of a 64x32 tile up to ~10 deg)
+// TMA box per plane: the footprint of a 64x32 tile (up to ~10 degrees at
+// scale ~1) plus 16 columns, because the box's x origin must be 16-byte
+// aligned for uint8 tensors (an unaligned origin raises an illegal
+// instruction on sm_100).
+constexpr int BW = 96, BH = 48;
 
 struct SmemT {
     alignas(128) uint8_t box[2][3][BH * BW];
@@ -665,7 +669,7 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
             ymn = min(ymn, (int)(Yv >> 48));
             ymx = max(ymx, (int)(Yv >> 48));
         }
-        tp.lbx = xmn - 1;
+        tp.lbx = (xmn - 1) & ~15;
         tp.lby = ymn - 1;
         tp.lfit = (xmx + 2) - tp.lbx < BW && (ymx + 2) - tp.lby < BH;
     }
@@ -680,7 +684,7 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
             ymn = min(ymn, (int)(Yv >> 48));
             ymx = max(ymx, (int)(Yv >> 48));
         }
-        tp.cbx = xmn - 1;
+        tp.cbx = (xmn - 1) & ~15;
         tp.cby = ymn - 1;
         tp.cfit = (xmx + 2) - tp.cbx < BW && (ymx + 2) - tp.cby < BH;
     }
