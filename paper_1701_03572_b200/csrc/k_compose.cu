@@ -107,21 +107,23 @@ __device__ __forceinline__ float frac_f(uint32_t f) {  // top 23 bits of a 0.32 
     return __uint_as_float(0x3F800000u | (f >> 9)) - 1.0f;
 }
 
-// exact uint8 -> float without I2F (a quarter-rate pipe): 2^23 + b, minus 2^23
-__device__ __forceinline__ float b2f(uint32_t b) { return __int_as_float(0x4B000000 | b) - 8388608.0f; }
+// uint8 -> 256 + b as fp32 in one LEA (0x43800000 | b << 15), no I2F.
+__device__ __forceinline__ float b256(uint32_t b) { return __uint_as_float(0x43800000u | (b << 15)); }
 
-// fast bilinear (sample_bilinear's blend in fp32) + lround; -1 when the
-// rounding decision is within the error guard of a .5 tie
+// fast bilinear (sample_bilinear's blend) in the 256-offset fp32 domain +
+// lround; -1 when the rounding decision is within the error guard of a .5
+// tie.  In [256, 512) differences are exact (Sterbenz) and each rounding is
+// <= 2^-16, so the fast value is within 1.1e-4 of the reference's fp64 value.
 __device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
                                            float fy) {
-    const float fa = b2f(a), fc = b2f(c);
-    const float top = fmaf(fx, b2f(b) - fa, fa);
-    const float bot = fmaf(fx, b2f(d) - fc, fc);
-    const float t = fmaf(fy, bot - top, top) + 0.5f;  // lround(v) == floor(v + 0.5), v >= 0
-    const float k = floorf(t);
-    const float fr = t - k;
-    if (fr < VGUARD || fr > 1.0f - VGUARD) return -1;
-    return __float_as_int(k + 8388608.0f) & 0x3FF;
+    const float fa = b256(a), fc = b256(c);
+    const float top = fmaf(fx, b256(b) - fa, fa);
+    const float bot = fmaf(fx, b256(d) - fc, fc);
+    const float v = fmaf(fy, bot - top, top);  // 256 + value
+    const float m = v + 8388608.0f;             // nearest integer (ties are guarded below)
+    const float dv = v - (m - 8388608.0f);      // in [-0.5, 0.5]
+    if (fabsf(dv) > 0.5f - VGUARD) return -1;
+    return __float_as_int(m) & 0xFF;            // (256 + k) mod 256 == k, k <= 255
 }
 
 // One fast-path sample of plane q (pitch, origin bx0/by0) at 16.48 (X, Y).
@@ -600,14 +602,14 @@ struct SmemT {
     uint8_t wt[WTH][WTW];
     alignas(16) uint8_t out[3][TH][TW];
     double cfx[TW], cfy[TH];
-    float cfxf[TW], cfyf[TH];
+    float cfyf[TH];
     int cx0[TW], cy0[TH];
     long long sxf[WTH], syf[WTH];
     long long pxf[TH], pyf[TH];
     TileParams tp[2];
     unsigned long long mbar[2];
-    int qn;
-    unsigned q[QCAP];
+    int qw, qc;            // exact-path queues: W pixels / crop + chroma pixels
+    unsigned q_w[QCAP], q_c[QCAP];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -695,6 +697,147 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
     dst[2] = src[2];
 }
 
+__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+// Warp-aggregated push of the lanes whose fast decision was not certain.
+// Every lane of the warp must call it (loops around it are warp-uniform).
+__device__ __forceinline__ void push_bad(int* qn, unsigned* q, bool bad, unsigned item) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, bad);
+    if (m == 0) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(qn, __popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    if (bad) {
+        const int k = base + __popc(m & ((1u << lane) - 1));
+        if (k < QCAP) q[k] = item;
+    }
+}
+
+// fast blend + lround of 4 bytes; sets bad when the rounding is not certain
+__device__ __forceinline__ uint32_t blend_bad(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
+                                              float fy, bool& bad) {
+    const float fa = b256(a), fc = b256(c);
+    const float top = fmaf(fx, b256(b) - fa, fa);
+    const float bot = fmaf(fx, b256(d) - fc, fc);
+    const float v = fmaf(fy, bot - top, top);
+    const float m = v + 8388608.0f;
+    bad |= fabsf(v - (m - 8388608.0f)) > 0.5f - VGUARD;
+    return (uint32_t)__float_as_int(m) & 0xFFu;
+}
+
+// Fast-path coordinate decode of a 16.48 point: fractions, integer parts,
+// in-bounds test; bad when a coordinate is within the guard of an integer.
+struct Pt {
+    float fx, fy;
+    int ix, iy;
+    bool inb;
+};
+
+__device__ __forceinline__ Pt decode(long long X, long long Y, unsigned limx, unsigned limy, bool valid,
+                                     bool& bad) {
+    Pt t;
+    const uint32_t fxs = (uint32_t)(X >> 16), fys = (uint32_t)(Y >> 16);
+    bad = valid && ((fxs + GUARD) < 2 * GUARD || (fys + GUARD) < 2 * GUARD);
+    t.ix = (int)(X >> 48);
+    t.iy = (int)(Y >> 48);
+    t.inb = valid && (unsigned)t.ix <= limx && (unsigned)t.iy <= limy;
+    t.fx = frac_f(fxs);
+    t.fy = frac_f(fys);
+    return t;
+}
+
+// One fast-path sample, branch-free: out-of-frame lanes read offset 0 and
+// take `outv`; bad when a decision is not certain.
+template <typename P>
+__device__ __forceinline__ uint32_t px1(P src, int pitch, int obase, long long X, long long Yc, unsigned limx,
+                                        unsigned limy, bool valid, uint32_t outv, bool& bad) {
+    const Pt t = decode(X, Yc, limx, limy, valid, bad);
+    const int o = t.inb ? t.iy * pitch + t.ix + obase : 0;
+    bool vb = false;
+    const uint32_t v = blend_bad(src[o], src[o + 1], src[o + pitch], src[o + pitch + 1], t.fx, t.fy, vb);
+    bad = bad || (t.inb && vb);
+    return t.inb ? v : outv;
+}
+
+// Two planes sharing a coordinate (chroma): b | r << 8
+template <typename P>
+__device__ __forceinline__ uint32_t px2(P s1, P s2, int pitch, int obase, long long X, long long Yc,
+                                        unsigned limx, unsigned limy, bool valid, bool& bad) {
+    const Pt t = decode(X, Yc, limx, limy, valid, bad);
+    const int o = t.inb ? t.iy * pitch + t.ix + obase : 0;
+    bool vb = false;
+    const uint32_t b = blend_bad(s1[o], s1[o + 1], s1[o + pitch], s1[o + pitch + 1], t.fx, t.fy, vb);
+    const uint32_t r = blend_bad(s2[o], s2[o + 1], s2[o + pitch], s2[o + pitch + 1], t.fx, t.fy, vb);
+    bad = bad || (t.inb && vb);
+    return t.inb ? (b | (r << 8)) : 0x8080u;
+}
+
+// Luma W rows (warp per row, lane per column): src is the staged TMA box
+// (pitch BW, obase = -(lby*BW + lbx)) or the global frame (pitch w, obase 0).
+// The two 32-column halves are computed together (independent chains), and
+// one ballot decides whether anything needs the exact path.
+template <typename P>
+__device__ __forceinline__ void w_rows(P src, int pitch, int obase, const long long* sxf, const long long* syf,
+                                       uint32_t wdst, int wp, int nu, int nv, long long uCF, long long uSN,
+                                       long long CF32, long long SN32, unsigned limx, unsigned limy, int* qn,
+                                       unsigned* q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool v0 = lane < nu, v1 = lane + 32 < nu, has2 = nu > 64;
+    for (int r = warp; r < nv; r += NT / 32) {
+        const long long SXr = sxf[r] + uCF, SYr = syf[r] - uSN;
+        const uint32_t wrow = wdst + r * wp + lane;
+        bool b0, b1, b2 = false;
+        const uint32_t a0 = px1(src, pitch, obase, SXr, SYr, limx, limy, v0, 0u, b0);
+        const uint32_t a1 = px1(src, pitch, obase, SXr + CF32, SYr - SN32, limx, limy, v1, 0u, b1);
+        if (v0) sts_u8(wrow, a0);
+        if (v1) sts_u8(wrow + 32, a1);
+        if (has2) {  // rare third half (nu = 65 .. 66)
+            const bool v2 = lane + 64 < nu;
+            const uint32_t a2 = px1(src, pitch, obase, SXr + 2 * CF32, SYr - 2 * SN32, limx, limy, v2, 0u, b2);
+            if (v2) sts_u8(wrow + 64, a2);
+        }
+        if (__ballot_sync(0xFFFFFFFFu, b0 || b1 || b2)) {
+            const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
+            push_bad(qn, q, b0, it);
+            push_bad(qn, q, b1, it + 32);
+            push_bad(qn, q, b2, it + 64);
+        }
+    }
+}
+
+// Chroma rows: both planes share one coordinate per pixel.
+template <typename P>
+__device__ __forceinline__ void chroma_rows(P s1, P s2, int pitch, int obase, const long long* pxf,
+                                            const long long* pyf, uint32_t o1, uint32_t o2, int nx,
+                                            int ny, long long xKX, long long xKY, long long KX32, long long KY32,
+                                            unsigned limx, unsigned limy, int* qn, unsigned* q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool v0 = lane < nx, v1 = lane + 32 < nx;
+    for (int r = warp; r < ny; r += NT / 32) {
+        const long long PXr = pxf[r] + xKX, PYr = pyf[r] + xKY;
+        const uint32_t orow = r * TW + lane;
+        bool b0, b1;
+        const uint32_t a0 = px2(s1, s2, pitch, obase, PXr, PYr, limx, limy, v0, b0);
+        const uint32_t a1 = px2(s1, s2, pitch, obase, PXr + KX32, PYr + KY32, limx, limy, v1, b1);
+        if (v0) {
+            sts_u8(o1 + orow, a0 & 0xFF);
+            sts_u8(o2 + orow, a0 >> 8);
+        }
+        if (v1) {
+            sts_u8(o1 + orow + 32, a1 & 0xFF);
+            sts_u8(o2 + orow + 32, a1 >> 8);
+        }
+        if (__ballot_sync(0xFFFFFFFFu, b0 || b1)) {
+            const unsigned it = (2u << 30) | ((unsigned)r << 8) | (unsigned)lane;
+            push_bad(qn, q, b0, it);
+            push_bad(qn, q, b1, it + 32);
+        }
+    }
+}
+
 template <bool LUMA, bool CHROMA>
 __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
     PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
@@ -737,6 +880,7 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
         if (t < total) issue(t, 0);
     }
     __syncthreads();
+    const ChromaMap cm = chroma_map(w, h, cw, ch, g);
     for (int k = 0; t < total; ++k, t += gridDim.x) {
         const int b = k & 1;
         const long long tn = t + gridDim.x;
@@ -750,13 +894,15 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
         const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
         const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
         const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
-        if (tid == 0) S.qn = 0;
+        if (tid == 0) {
+            S.qw = 0;
+            S.qc = 0;
+        }
         if (LUMA) {
             if (!identity) {
                 if (tid < nx) {
                     S.cx0[tid] = __ldg(T.cx0 + X0 + tid);
                     S.cfx[tid] = __ldg(T.cfx + X0 + tid);
-                    S.cfxf[tid] = (float)S.cfx[tid];
                 } else if (tid >= 64 && tid < 64 + ny) {
                     S.cy0[tid - 64] = __ldg(T.cy0 + Y0 + tid - 64);
                     S.cfy[tid - 64] = __ldg(T.cfy + Y0 + tid - 64);
@@ -774,29 +920,39 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
         }
         mbar_wait(smem_u32(&S.mbar[b]), (uint32_t)((k >> 1) & 1));
         __syncthreads();
-        // ---------------------------------------------------- luma W tile
+        // ------------------------------------------- phase A: W and chroma, fast path
+        uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
+        const int wp = identity ? TW : WTW;
         if (LUMA) {
-            uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
-            const int wp = identity ? TW : WTW;
             const unsigned limx = (unsigned)(w - 2), limy = (unsigned)(h - 2);
-            const bool stg = tp.lfit;
-            const long long CF = p.cf, SNF = p.snf;
-            const uint8_t* sb = &S.box[b][0][0];
-            for (int i = tid; i < nv * 68; i += NT) {  // 68 = 17 groups of 4 columns? flat row-major
-                const int r = i / 68, c = i - r * 68;
-                if (c >= nu) continue;
-                const long long u = u0 + c;
-                const long long SX = S.sxf[r] + u * CF, SY = S.syf[r] - u * SNF;
-                const int val = stg ? sample_fast(sb, BW, tp.lbx, tp.lby, limx, limy, SX, SY, 0)
-                                    : sample_fast(gy, w, 0, 0, limx, limy, SX, SY, 0);
-                if (val < 0) push_q(S.qn, S.q, (unsigned)(r * nu + c));
-                else wdst[r * wp + c] = (uint8_t)val;
-            }
-            __syncthreads();
-            const int nq = S.qn;
+            const long long uCF = (long long)(u0 + lane) * p.cf, uSN = (long long)(u0 + lane) * p.snf;
+            const uint32_t wsm = smem_u32(wdst);
+            if (tp.lfit)
+                w_rows(&S.box[b][0][0], BW, -(tp.lby * BW + tp.lbx), S.sxf, S.syf, wsm, wp, nu, nv, uCF, uSN,
+                       32 * p.cf, 32 * p.snf, limx, limy, &S.qw, S.q_w);
+            else
+                w_rows(gy, w, 0, S.sxf, S.syf, wsm, wp, nu, nv, uCF, uSN, 32 * p.cf, 32 * p.snf, limx, limy,
+                       &S.qw, S.q_w);
+        }
+        if (CHROMA) {
+            const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
+            const long long xKX = (long long)(X0 + lane) * p.kxx, xKY = (long long)(X0 + lane) * p.kyx;
+            if (tp.cfit)
+                chroma_rows(&S.box[b][1][0], &S.box[b][2][0], BW, -(tp.cby * BW + tp.cbx), S.pxf, S.pyf,
+                            smem_u32(S.out[1]), smem_u32(S.out[2]), nx, ny, xKX, xKY, 32 * p.kxx, 32 * p.kyx,
+                            limx, limy, &S.qc, S.q_c);
+            else
+                chroma_rows(gcb, gcr, cw, 0, S.pxf, S.pyf, smem_u32(S.out[1]), smem_u32(S.out[2]), nx, ny, xKX,
+                            xKY, 32 * p.kxx, 32 * p.kyx, limx, limy, &S.qc, S.q_c);
+        }
+        __syncthreads();
+        // ------------------------------------------- phase B: exact W pixels
+        if (LUMA) {
+            const int nq = S.qw;
             if (nq <= QCAP) {
                 for (int q = tid; q < nq; q += NT) {
-                    const int i = (int)(S.q[q] & 0x3FFFFFFF), r = i / nu, c = i - r * nu;
+                    const unsigned item = S.q_w[q];
+                    const int r = (int)(item >> 8), c = (int)(item & 0xFF);
                     wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
                 }
             } else {
@@ -805,74 +961,52 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
                     wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
                 }
             }
-            __syncthreads();
-            if (tid == 0) S.qn = 0;
-            __syncthreads();
-            if (!identity) {
-                int x0[2], x1[2];
-                float fxv[2];
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    const int c = min(2 * lane + kk, nx - 1);
-                    x0[kk] = S.cx0[c] - u0;
-                    x1[kk] = min(S.cx0[c] + 1, w - 1) - u0;
-                    fxv[kk] = S.cfxf[c];
-                }
-                for (int r = warp; r < ny; r += NT / 32) {
-                    const int y0 = S.cy0[r] - v0, y1 = min(S.cy0[r] + 1, h - 1) - v0;
-                    const float fy = S.cfyf[r];
-#pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        const int c = 2 * lane + kk;
-                        if (c >= nx) break;
-                        const int val = blend_round(S.wt[y0][x0[kk]], S.wt[y0][x1[kk]], S.wt[y1][x0[kk]],
-                                                    S.wt[y1][x1[kk]], fxv[kk], fy);
-                        if (val < 0) push_q(S.qn, S.q, (1u << 30) | (unsigned)(r * nx + c));
-                        else S.out[0][r][c] = (uint8_t)val;
-                    }
-                }
-            }
         }
-        // ---------------------------------------------------- chroma
-        const ChromaMap cm = chroma_map(w, h, cw, ch, g);
-        if (CHROMA) {
-            const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
-            const bool stg = tp.cfit;
-            const long long KX = p.kxx, KY = p.kyx;
-            const uint8_t* s1 = &S.box[b][1][0];
-            const uint8_t* s2 = &S.box[b][2][0];
-            for (int r = warp; r < ny; r += NT / 32) {
-                const long long PXr = S.pxf[r], PYr = S.pyf[r];
+        // ------------------------------------------- phase C: crop_resize of W, fast path
+        if (LUMA && !identity) {
+            __syncthreads();
+            int x0[2], x1[2];
+            float fxv[2];
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    const int c = 2 * lane + kk;
-                    if (c >= nx) break;
-                    const long long x = X0 + c;
-                    const long long PX = PXr + x * KX, PY = PYr + x * KY;
-                    const int v = stg ? sample_fast2(s1, s2, BW, tp.cbx, tp.cby, limx, limy, PX, PY, 128)
-                                      : sample_fast2(gcb, gcr, cw, 0, 0, limx, limy, PX, PY, 128);
-                    if (v < 0) {
-                        push_q(S.qn, S.q, (2u << 30) | (unsigned)(r * nx + c));
-                    } else {
-                        S.out[1][r][c] = (uint8_t)(v & 0xFF);
-                        S.out[2][r][c] = (uint8_t)(v >> 16);
-                    }
+            for (int j = 0; j < 2; ++j) {
+                const int c = min(lane + 32 * j, nx - 1);
+                x0[j] = S.cx0[c] - u0;
+                x1[j] = min(S.cx0[c] + 1, w - 1) - u0;
+                fxv[j] = (float)S.cfx[c];
+            }
+            const bool c0 = lane < nx, c1 = lane + 32 < nx;
+            const uint32_t o0 = smem_u32(S.out[0]) + lane;
+            for (int r = warp; r < ny; r += NT / 32) {
+                const int cy = S.cy0[r];
+                const uint8_t* row0 = S.wt[cy - v0];
+                const uint8_t* row1 = S.wt[min(cy + 1, h - 1) - v0];
+                const float fy = S.cfyf[r];
+                bool b0 = false, b1 = false;
+                const uint32_t a0 = blend_bad(row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]], fxv[0], fy, b0);
+                const uint32_t a1 = blend_bad(row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]], fxv[1], fy, b1);
+                b0 = b0 && c0;
+                b1 = b1 && c1;
+                if (c0) sts_u8(o0 + r * TW, a0);
+                if (c1) sts_u8(o0 + r * TW + 32, a1);
+                if (__ballot_sync(0xFFFFFFFFu, b0 || b1)) {
+                    const unsigned it = (1u << 30) | ((unsigned)r << 8) | (unsigned)lane;
+                    push_bad(&S.qc, S.q_c, b0, it);
+                    push_bad(&S.qc, S.q_c, b1, it + 32);
                 }
             }
         }
         __syncthreads();
+        // ------------------------------------------- phase D: exact crop + chroma pixels
         {
-            const int nq = S.qn;
+            const int nq = S.qc;
             if (nq <= QCAP) {
                 for (int q = tid; q < nq; q += NT) {
-                    const unsigned item = S.q[q];
-                    const int kind = item >> 30, i = (int)(item & 0x3FFFFFFF);
-                    const int r = i / nx, c = i - r * nx;
+                    const unsigned item = S.q_c[q];
+                    const int kind = item >> 30, r = (int)((item >> 8) & 0xFF), c = (int)(item & 0xFF);
                     if (LUMA && kind == 1) {
                         S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
                     } else if (CHROMA && kind == 2) {
-                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
-                                     S.out[2][r][c]);
+                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c], S.out[2][r][c]);
                     }
                 }
             } else {
@@ -881,8 +1015,7 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
                     if (LUMA && !identity)
                         S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
                     if (CHROMA)
-                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c],
-                                     S.out[2][r][c]);
+                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c], S.out[2][r][c]);
                 }
             }
         }

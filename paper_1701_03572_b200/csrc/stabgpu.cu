@@ -16,6 +16,7 @@
 // then K7 scan + smoothing and K8 compose over the sequence.
 #include <cmath>
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -424,6 +425,13 @@ int stabgpu_create(int device, stabgpu_ctx** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cout, cudaStreamNonBlocking));
     c->stream = c->own;
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    // Per-launch tables come from the stream-ordered allocator; keep freed
+    // blocks mapped so repeated launches do not remap device memory.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return STABGPU_OK;
 }
