@@ -30,19 +30,25 @@ __device__ __forceinline__ uint8_t round_u8(double v) {
     return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
 }
 
-// sample_bilinear, image_ops.cpp:98-113 (0 outside [0,w-1]x[0,h-1]).
-__device__ __forceinline__ double sample_bilinear(const uint8_t* __restrict__ f, int w, int h,
-                                                  double px, double py) {
+// sample_bilinear, image_ops.cpp:98-113 (0 outside [0,w-1]x[0,h-1]), with
+// the pixel fetch abstracted (global frame or a staged shared-memory copy).
+template <typename F>
+__device__ __forceinline__ double bilinear_f(F fetch, int w, int h, double px, double py) {
     const double xmax = (double)w - 1.0, ymax = (double)h - 1.0;
     if (!(px >= 0.0 && py >= 0.0 && px <= xmax && py <= ymax)) return 0.0;
     const int x0 = (int)px, y0 = (int)py;
     const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
     const double fx = dsub(px, (double)x0), fy = dsub(py, (double)y0);
-    const double a = f[(size_t)y0 * w + x0], b = f[(size_t)y0 * w + x1];
-    const double c = f[(size_t)y1 * w + x0], d = f[(size_t)y1 * w + x1];
+    const double a = fetch(x0, y0), b = fetch(x1, y0);
+    const double c = fetch(x0, y1), d = fetch(x1, y1);
     const double top = dadd(a, dmul(fx, dsub(b, a)));
     const double bot = dadd(c, dmul(fx, dsub(d, c)));
     return dadd(top, dmul(fy, dsub(bot, top)));
+}
+
+__device__ __forceinline__ double sample_bilinear(const uint8_t* __restrict__ f, int w, int h,
+                                                  double px, double py) {
+    return bilinear_f([=](int x, int y) { return (double)f[(size_t)y * w + x]; }, w, h, px, py);
 }
 
 // Positive doubles order like their bit patterns.

@@ -49,7 +49,7 @@ constexpr int WTW = 72, WTH = 36;        // warped-luma tile (<= 66 x 34 used)
 constexpr int SRC_W = 128, SRC_H = 80;   // staged source capacity per plane
 constexpr int QCAP = 1024;               // exact-path queue
 constexpr uint32_t GUARD = 1024;         // coordinate guard, units of 2^-32 px
-constexpr float VGUARD = 2.5e-4f;        // blended-value guard (the fast error is <= 1.5e-4)
+constexpr float VGUARD = 1.0e-4f;        // blended-value guard (the fast error is <= 6.1e-5)
 constexpr double FIX48 = 281474976710656.0;  // 2^48
 
 struct CropGeom {
@@ -103,8 +103,10 @@ struct Smem {
 
 __device__ __forceinline__ bool near_int(uint32_t f) { return f < GUARD || f > 0xFFFFFFFFu - GUARD; }
 
-__device__ __forceinline__ float frac_f(uint32_t f) {  // top 23 bits of a 0.32 fraction
-    return __uint_as_float(0x3F800000u | (f >> 9)) - 1.0f;
+// 0.32 fraction -> fp32 within 2^-24: top 23 bits, centred on the dropped
+// bits ((1 + m 2^-23) - (1 - 2^-24) is exact).
+__device__ __forceinline__ float frac_f(uint32_t f) {
+    return __uint_as_float(0x3F800000u | (f >> 9)) - 0.99999994f;
 }
 
 // uint8 -> 256 + b as fp32 in one LEA (0x43800000 | b << 15), no I2F.
@@ -112,8 +114,10 @@ __device__ __forceinline__ float b256(uint32_t b) { return __uint_as_float(0x438
 
 // fast bilinear (sample_bilinear's blend) in the 256-offset fp32 domain +
 // lround; -1 when the rounding decision is within the error guard of a .5
-// tie.  In [256, 512) differences are exact (Sterbenz) and each rounding is
-// <= 2^-16, so the fast value is within 1.1e-4 of the reference's fp64 value.
+// tie.  Error budget against the reference's fp64 value: in [256, 512)
+// differences are exact (Sterbenz) and the three fma roundings contribute
+// <= 2 * 2^-16 to v; the fractions are within 2^-24 (+1e-9 px coordinate
+// error), <= 255 * 2^-24 each.  Total <= 6.1e-5 < VGUARD.
 __device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
                                            float fy) {
     const float fa = b256(a), fc = b256(c);
@@ -233,8 +237,9 @@ __device__ __forceinline__ void chroma_coords(const FramePlan& p, const CropGeom
 // coordinate sits that close to an integer / the frame edge, or the fp64
 // blend that close to a .5 tie, the direct result IS the reference result.
 // Level 2 (about once per two 1080p frames): fl_walk, the exact walk.
-__device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const FramePlan& p, int u,
-                           int v) {
+// `fetch(x, y)` reads the source frame (global, or the staged TMA box).
+template <typename F>
+__device__ uint8_t w_exact_f(F fetch, int w, int h, const FramePlan& p, int u, int v) {
     double rx, ry;
     row_start(p, v, rx, ry);
     const double sx = dadd(rx, dmul((double)u, p.c)), sy = dsub(ry, dmul((double)u, p.sn));
@@ -245,11 +250,15 @@ __device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const Fr
     if (fmin(fxx, 1.0 - fxx) <= tol || fabs(sx) <= tol || fabs(sx - ((double)w - 1.0)) <= tol) sure = false;
     if (fmin(fyy, 1.0 - fyy) <= tol || fabs(sy) <= tol || fabs(sy - ((double)h - 1.0)) <= tol) sure = false;
     if (sure) {
-        const double val = sample_bilinear(g, w, h, sx, sy);
+        const double val = bilinear_f(fetch, w, h, sx, sy);
         const double fr = val - floor(val);
         if (fabs(fr - 0.5) > 255.0 * 4.0 * tol + 1e-9) return round_u8(val);
     }
-    return round_u8(sample_bilinear(g, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
+    return round_u8(bilinear_f(fetch, w, h, fl_walk(rx, p.c, u), fl_walk(ry, -p.sn, u)));
+}
+
+__device__ uint8_t w_exact(const uint8_t* __restrict__ g, int w, int h, const FramePlan& p, int u, int v) {
+    return w_exact_f([=](int x, int y) { return (double)g[(size_t)y * w + x]; }, w, h, p, u, v);
 }
 
 __device__ __forceinline__ uint8_t crop_exact_t(const uint8_t (*wt)[WTW], const int* cx0,
@@ -276,17 +285,25 @@ __device__ __forceinline__ uint8_t crop_exact(const Smem& S, int r, int c, int u
     return round_u8(dadd(top, dmul(S.cfy[r], dsub(bot, top))));
 }
 
-__device__ __forceinline__ void chroma_exact(const FramePlan& p, const CropGeom& g,
-                                             const ChromaMap& cm, const uint8_t* gcb,
-                                             const uint8_t* gcr, int cw, int ch, int x, int y,
-                                             uint8_t& ob, uint8_t& orr) {
+template <typename F1, typename F2>
+__device__ __forceinline__ void chroma_exact_f(const FramePlan& p, const CropGeom& g, const ChromaMap& cm,
+                                               F1 f1, F2 f2, int cw, int ch, int x, int y, uint8_t& ob,
+                                               uint8_t& orr) {
     double px, py;
     chroma_coords(p, g, cm, x, y, px, py);
     ob = orr = 128;
     if (px >= 0.0 && py >= 0.0 && px <= (double)cw - 1.0 && py <= (double)ch - 1.0) {
-        ob = round_u8(sample_bilinear(gcb, cw, ch, px, py));
-        orr = round_u8(sample_bilinear(gcr, cw, ch, px, py));
+        ob = round_u8(bilinear_f(f1, cw, ch, px, py));
+        orr = round_u8(bilinear_f(f2, cw, ch, px, py));
     }
+}
+
+__device__ __forceinline__ void chroma_exact(const FramePlan& p, const CropGeom& g,
+                                             const ChromaMap& cm, const uint8_t* gcb,
+                                             const uint8_t* gcr, int cw, int ch, int x, int y,
+                                             uint8_t& ob, uint8_t& orr) {
+    chroma_exact_f(p, g, cm, [=](int xx, int yy) { return (double)gcb[(size_t)yy * cw + xx]; },
+                   [=](int xx, int yy) { return (double)gcr[(size_t)yy * cw + xx]; }, cw, ch, x, y, ob, orr);
 }
 
 // Per-frame row tables + (frame 0) crop tables.
@@ -595,21 +612,17 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
 // scale ~1) plus 16 columns, because the box's x origin must be 16-byte
 // aligned for uint8 tensors (an unaligned origin raises an illegal
 // instruction on sm_100).
-constexpr int BW = 96, BH = 48;
+constexpr int BW = 96, BH = 80;
+constexpr int TTH = 64;            // TMA path output tile: TW x TTH
+constexpr int TWTH = 68;           // its W tile rows (<= 66 used)
+constexpr int QW = 64;  // per-warp exact-path queue
 
 struct SmemT {
-    alignas(128) uint8_t box[2][3][BH * BW];
-    uint8_t wt[WTH][WTW];
-    alignas(16) uint8_t out[3][TH][TW];
-    double cfx[TW], cfy[TH];
-    float cfyf[TH];
-    int cx0[TW], cy0[TH];
-    long long sxf[WTH], syf[WTH];
-    long long pxf[TH], pyf[TH];
-    TileParams tp[2];
+    alignas(128) uint8_t box[2][3][BH * BW];  // TMA source footprints, double-buffered
+    uint8_t wt[2][TWTH][WTW];                 // warped luma of the tile, double-buffered
+    TileParams tp[3];  // tile k uses tp[k % 3]; tile k+2's are in flight (cp.async)
     unsigned long long mbar[2];
-    int qw, qc;            // exact-path queues: W pixels / crop + chroma pixels
-    unsigned q_w[QCAP], q_c[QCAP];
+    unsigned wq[NT / 32][QW];  // per-warp queues of pixels for the exact path
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -643,8 +656,8 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
     const long long tpf = (long long)tiles_x * tiles_y;
     if (id >= tpf * frames) return;
     const int f = (int)(id / tpf), t = (int)(id - f * tpf);
-    const int X0 = (t % tiles_x) * TW, Y0 = (t / tiles_x) * TH;
-    const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
+    const int X0 = (t % tiles_x) * TW, Y0 = (t / tiles_x) * TTH;
+    const int nx = min(TW, W - X0), ny = min(TTH, H - Y0);
     const FramePlan p = plan[f];
     TileParams tp;
     memset(&tp, 0, sizeof tp);
@@ -701,18 +714,15 @@ __device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
-// Warp-aggregated push of the lanes whose fast decision was not certain.
-// Every lane of the warp must call it (loops around it are warp-uniform).
-__device__ __forceinline__ void push_bad(int* qn, unsigned* q, bool bad, unsigned item) {
+__device__ __forceinline__ void stg_u8(uint8_t* p, uint32_t v) { __stcs(p, (uint8_t)v); }
+
+// Per-warp queue push (warp-uniform count, no atomics).  All lanes call it.
+__device__ __forceinline__ void wq_push(unsigned* q, int& qn, bool bad, unsigned item) {
     const unsigned m = __ballot_sync(0xFFFFFFFFu, bad);
-    if (m == 0) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(qn, __popc(m));
-    base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    if (bad) {
-        const int k = base + __popc(m & ((1u << lane) - 1));
-        if (k < QCAP) q[k] = item;
+    if (m) {
+        const int pos = qn + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+        if (bad && pos < QW) q[pos] = item;
+        qn += __popc(m);
     }
 }
 
@@ -775,69 +785,124 @@ __device__ __forceinline__ uint32_t px2(P s1, P s2, int pitch, int obase, long l
     return t.inb ? (b | (r << 8)) : 0x8080u;
 }
 
-// Luma W rows (warp per row, lane per column): src is the staged TMA box
-// (pitch BW, obase = -(lby*BW + lbx)) or the global frame (pitch w, obase 0).
-// The two 32-column halves are computed together (independent chains), and
-// one ballot decides whether anything needs the exact path.
+// ---- exact reference paths, out of line (taken by ~1% of warp rows) ----
+__device__ __noinline__ uint32_t w_exact_tile(const FramePlan* __restrict__ plan, int f, const uint8_t* box,
+                                              int lbx, int lby, int fit, const uint8_t* gy, int w, int h, int u,
+                                              int v) {
+    const FramePlan p = plan[f];
+    if (fit) return w_exact_f([=](int x, int y) { return (double)box[(y - lby) * BW + x - lbx]; }, w, h, p, u, v);
+    return w_exact(gy, w, h, p, u, v);
+}
+
+__device__ __noinline__ uint32_t chroma_exact_tile(const FramePlan* __restrict__ plan, int f, CropGeom g,
+                                                   const uint8_t* b1, const uint8_t* b2, int cbx, int cby, int fit,
+                                                   const uint8_t* gcb, const uint8_t* gcr, int w, int h, int cw,
+                                                   int ch, int x, int y) {
+    const FramePlan p = plan[f];
+    const ChromaMap cm = chroma_map(w, h, cw, ch, g);
+    uint8_t ob, orr;
+    if (fit)
+        chroma_exact_f(p, g, cm, [=](int xx, int yy) { return (double)b1[(yy - cby) * BW + xx - cbx]; },
+                       [=](int xx, int yy) { return (double)b2[(yy - cby) * BW + xx - cbx]; }, cw, ch, x, y, ob,
+                       orr);
+    else
+        chroma_exact(p, g, cm, gcb, gcr, cw, ch, x, y, ob, orr);
+    return ob | ((uint32_t)orr << 8);
+}
+
+// crop_resize pixel (image_ops.cpp:151-157) of output (X, Y) from the W tile
+__device__ __noinline__ uint32_t crop_exact_tile(const uint8_t* wt, const Tables T, int X, int Y, int u0, int v0,
+                                                 int w, int h) {
+    const int x0 = T.cx0[X], y0 = T.cy0[Y];
+    const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+    const double a = wt[(y0 - v0) * WTW + x0 - u0], b = wt[(y0 - v0) * WTW + x1 - u0];
+    const double cc = wt[(y1 - v0) * WTW + x0 - u0], d = wt[(y1 - v0) * WTW + x1 - u0];
+    const double top = dadd(a, dmul(T.cfx[X], dsub(b, a)));
+    const double bot = dadd(cc, dmul(T.cfx[X], dsub(d, cc)));
+    return round_u8(dadd(top, dmul(T.cfy[Y], dsub(bot, top))));
+}
+
+// Luma W rows of a tile (warp per row, lane per column) into the shared W
+// tile; src is the staged TMA box (pitch BW, obase = -(lby*BW + lbx)) or the
+// global frame (pitch w, obase 0).  Returns the warp's queue length.
 template <typename P>
-__device__ __forceinline__ void w_rows(P src, int pitch, int obase, const long long* sxf, const long long* syf,
-                                       uint32_t wdst, int wp, int nu, int nv, long long uCF, long long uSN,
-                                       long long CF32, long long SN32, unsigned limx, unsigned limy, int* qn,
-                                       unsigned* q) {
+__device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long long* __restrict__ rxf,
+                                        const long long* __restrict__ ryf, uint32_t wsm, int nu, int nv,
+                                        long long uCF, long long uSN, long long CF32, long long SN32,
+                                        unsigned limx, unsigned limy, unsigned* q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool v0 = lane < nu, v1 = lane + 32 < nu, has2 = nu > 64;
-    for (int r = warp; r < nv; r += NT / 32) {
-        const long long SXr = sxf[r] + uCF, SYr = syf[r] - uSN;
-        const uint32_t wrow = wdst + r * wp + lane;
+    int qn = 0;
+    uint32_t row = wsm + warp * WTW + lane;
+    long long rx = __ldg(rxf + min(warp, nv - 1)), ry = __ldg(ryf + min(warp, nv - 1));
+    for (int r = warp; r < nv; r += NT / 32, row += (NT / 32) * WTW) {
+        const long long SXr = rx + uCF, SYr = ry - uSN;
+        rx = __ldg(rxf + min(r + NT / 32, nv - 1));  // next row's starts, one iteration ahead
+        ry = __ldg(ryf + min(r + NT / 32, nv - 1));
         bool b0, b1, b2 = false;
         const uint32_t a0 = px1(src, pitch, obase, SXr, SYr, limx, limy, v0, 0u, b0);
         const uint32_t a1 = px1(src, pitch, obase, SXr + CF32, SYr - SN32, limx, limy, v1, 0u, b1);
-        if (v0) sts_u8(wrow, a0);
-        if (v1) sts_u8(wrow + 32, a1);
+        if (v0) sts_u8(row, a0);
+        if (v1) sts_u8(row + 32, a1);
         if (has2) {  // rare third half (nu = 65 .. 66)
             const bool v2 = lane + 64 < nu;
             const uint32_t a2 = px1(src, pitch, obase, SXr + 2 * CF32, SYr - 2 * SN32, limx, limy, v2, 0u, b2);
-            if (v2) sts_u8(wrow + 64, a2);
+            if (v2) sts_u8(row + 64, a2);
         }
-        if (__ballot_sync(0xFFFFFFFFu, b0 || b1 || b2)) {
+        if (__any_sync(0xFFFFFFFFu, b0 || b1 || b2)) {
             const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
-            push_bad(qn, q, b0, it);
-            push_bad(qn, q, b1, it + 32);
-            push_bad(qn, q, b2, it + 64);
+            wq_push(q, qn, b0, it);
+            wq_push(q, qn, b1, it + 32);
+            wq_push(q, qn, b2, it + 64);
         }
     }
+    return qn;
 }
 
-// Chroma rows: both planes share one coordinate per pixel.
+// Chroma rows of a tile straight to the output planes (both planes share
+// one coordinate per pixel).  Returns the warp's queue length.
 template <typename P>
-__device__ __forceinline__ void chroma_rows(P s1, P s2, int pitch, int obase, const long long* pxf,
-                                            const long long* pyf, uint32_t o1, uint32_t o2, int nx,
-                                            int ny, long long xKX, long long xKY, long long KX32, long long KY32,
-                                            unsigned limx, unsigned limy, int* qn, unsigned* q) {
+__device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, const long long* __restrict__ pxf,
+                                             const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int cw,
+                                             int nx, int ny, long long xKX, long long xKY, long long KX32,
+                                             long long KY32, unsigned limx, unsigned limy, unsigned* q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool v0 = lane < nx, v1 = lane + 32 < nx;
-    for (int r = warp; r < ny; r += NT / 32) {
-        const long long PXr = pxf[r] + xKX, PYr = pyf[r] + xKY;
-        const uint32_t orow = r * TW + lane;
+    int qn = 0;
+    const size_t step = (size_t)(NT / 32) * cw;
+    uint8_t* pb = ob + (size_t)warp * cw + lane;
+    uint8_t* pr = orr + (size_t)warp * cw + lane;
+    long long px = __ldg(pxf + min(warp, ny - 1)), py = __ldg(pyf + min(warp, ny - 1));
+    for (int r = warp; r < ny; r += NT / 32, pb += step, pr += step) {
+        const long long PXr = px + xKX, PYr = py + xKY;
+        px = __ldg(pxf + min(r + NT / 32, ny - 1));
+        py = __ldg(pyf + min(r + NT / 32, ny - 1));
         bool b0, b1;
         const uint32_t a0 = px2(s1, s2, pitch, obase, PXr, PYr, limx, limy, v0, b0);
         const uint32_t a1 = px2(s1, s2, pitch, obase, PXr + KX32, PYr + KY32, limx, limy, v1, b1);
         if (v0) {
-            sts_u8(o1 + orow, a0 & 0xFF);
-            sts_u8(o2 + orow, a0 >> 8);
+            stg_u8(pb, a0 & 0xFF);
+            stg_u8(pr, a0 >> 8);
         }
         if (v1) {
-            sts_u8(o1 + orow + 32, a1 & 0xFF);
-            sts_u8(o2 + orow + 32, a1 >> 8);
+            stg_u8(pb + 32, a1 & 0xFF);
+            stg_u8(pr + 32, a1 >> 8);
         }
-        if (__ballot_sync(0xFFFFFFFFu, b0 || b1)) {
-            const unsigned it = (2u << 30) | ((unsigned)r << 8) | (unsigned)lane;
-            push_bad(qn, q, b0, it);
-            push_bad(qn, q, b1, it + 32);
+        if (__any_sync(0xFFFFFFFFu, b0 || b1)) {
+            const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
+            wq_push(q, qn, b0, it);
+            wq_push(q, qn, b1, it + 32);
         }
     }
+    return qn;
 }
 
+// Persistent TMA compose.  Per tile: every warp waits on the tile's mbarrier,
+// computes W rows (-> shared wt) and chroma rows (-> global), one CTA
+// barrier, then crop_resize rows of W (-> global).  Undecidable pixels take
+// the exact reference path inline (the warp diverges for them only).  wt is
+// double-buffered and the TMA box of tile k+2 is issued only after the
+// barrier of tile k+1, so a fast warp may run ahead into the next tile.
 template <bool LUMA, bool CHROMA>
 __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
     PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
@@ -853,14 +918,20 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
     const long long tpf = (long long)tiles_x * tiles_y;
     const long long total = tpf * frames;
     const uint32_t bytes_l = LUMA ? BW * BH : 0, bytes_c = CHROMA ? 2 * BW * BH : 0;
+    constexpr unsigned FULL = 0xFFFFFFFFu;
 
-    auto issue = [&](long long t, int b) {  // thread 0: params + TMA of tile t into buffer b
-        const int4* src = T.tiles + 3 * t;
-        int4* dst = reinterpret_cast<int4*>(&S.tp[b]);
-        dst[0] = src[0];
-        dst[1] = src[1];
-        dst[2] = src[2];
-        const TileParams& tp = S.tp[b];
+    auto prefetch = [&](long long t, int slot) {  // thread 0: tile t's params -> tp[slot], async
+        const char* src = reinterpret_cast<const char*>(T.tiles + 3 * t);
+        const uint32_t dst = smem_u32(&S.tp[slot]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(src + 16 * i)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto issue = [&](long long t, int b, int slot) {  // thread 0: TMA of tile t into buffer b
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        const TileParams& tp = S.tp[slot];
         const int f = (int)(t / tpf);
         const uint32_t bar = smem_u32(&S.mbar[b]);
         const uint32_t bytes = (LUMA && tp.lfit ? bytes_l : 0) + (CHROMA && tp.cfit ? bytes_c : 0);
@@ -877,165 +948,169 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (t < total) issue(t, 0);
+        if (t < total) {
+            prefetch(t, 0);
+            issue(t, 0, 0);
+            if (t + gridDim.x < total) prefetch(t + gridDim.x, 1);
+        }
     }
     __syncthreads();
-    const ChromaMap cm = chroma_map(w, h, cw, ch, g);
     for (int k = 0; t < total; ++k, t += gridDim.x) {
         const int b = k & 1;
         const long long tn = t + gridDim.x;
-        if (tid == 0 && tn < total) issue(tn, b ^ 1);
+        if (tid == 0 && tn < total) {
+            issue(tn, b ^ 1, (k + 1) % 3);
+            if (tn + gridDim.x < total) prefetch(tn + gridDim.x, (k + 2) % 3);
+        }
         const int f = (int)(t / tpf), ti = (int)(t - f * tpf);
-        const int X0 = (ti % tiles_x) * TW, Y0 = (ti / tiles_x) * TH;
-        const int nx = min(TW, W - X0), ny = min(TH, H - Y0);
-        const FramePlan p = plan[f];
-        const TileParams tp = S.tp[b];
+        const int X0 = (ti % tiles_x) * TW, Y0 = (ti / tiles_x) * TTH;
+        const int nx = min(TW, W - X0), ny = min(TTH, H - Y0);
+        const TileParams tp = S.tp[k % 3];
         const int u0 = tp.u0, v0 = tp.v0, nu = tp.nu, nv = tp.nv;
+        const long long cf = plan[f].cf, snf = plan[f].snf, kxx = plan[f].kxx, kyx = plan[f].kyx;
         const uint8_t* gy = LUMA ? Y.base + (size_t)f * Y.stride : nullptr;
         const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
         const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
-        if (tid == 0) {
-            S.qw = 0;
-            S.qc = 0;
-        }
-        if (LUMA) {
-            if (!identity) {
-                if (tid < nx) {
-                    S.cx0[tid] = __ldg(T.cx0 + X0 + tid);
-                    S.cfx[tid] = __ldg(T.cfx + X0 + tid);
-                } else if (tid >= 64 && tid < 64 + ny) {
-                    S.cy0[tid - 64] = __ldg(T.cy0 + Y0 + tid - 64);
-                    S.cfy[tid - 64] = __ldg(T.cfy + Y0 + tid - 64);
-                    S.cfyf[tid - 64] = (float)S.cfy[tid - 64];
-                }
-            }
-            if (tid >= 128 && tid < 128 + nv) {
-                S.sxf[tid - 128] = __ldg(T.rxf + (size_t)f * h + v0 + tid - 128);
-                S.syf[tid - 128] = __ldg(T.ryf + (size_t)f * h + v0 + tid - 128);
-            }
-        }
-        if (CHROMA && tid >= 192 && tid < 192 + ny) {
-            S.pxf[tid - 192] = __ldg(T.pxf + (size_t)f * ch + Y0 + tid - 192);
-            S.pyf[tid - 192] = __ldg(T.pyf + (size_t)f * ch + Y0 + tid - 192);
-        }
+        const uint8_t* wt = &S.wt[b][0][0];
         mbar_wait(smem_u32(&S.mbar[b]), (uint32_t)((k >> 1) & 1));
-        __syncthreads();
-        // ------------------------------------------- phase A: W and chroma, fast path
-        uint8_t* wdst = identity ? &S.out[0][0][0] : &S.wt[0][0];
-        const int wp = identity ? TW : WTW;
+        // ------------------------------------------- W rows -> wt[b]
         if (LUMA) {
             const unsigned limx = (unsigned)(w - 2), limy = (unsigned)(h - 2);
-            const long long uCF = (long long)(u0 + lane) * p.cf, uSN = (long long)(u0 + lane) * p.snf;
-            const uint32_t wsm = smem_u32(wdst);
+            const long long uCF = (long long)(u0 + lane) * cf, uSN = (long long)(u0 + lane) * snf;
+            const long long* rxf = T.rxf + (size_t)f * h + v0;
+            const long long* ryf = T.ryf + (size_t)f * h + v0;
+            const uint8_t* bx = &S.box[b][0][0];
+            const uint32_t wsm = smem_u32(wt);
+            int qn;
             if (tp.lfit)
-                w_rows(&S.box[b][0][0], BW, -(tp.lby * BW + tp.lbx), S.sxf, S.syf, wsm, wp, nu, nv, uCF, uSN,
-                       32 * p.cf, 32 * p.snf, limx, limy, &S.qw, S.q_w);
+                qn = w_rows_q(bx, BW, -(tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf,
+                              limx, limy, S.wq[warp]);
             else
-                w_rows(gy, w, 0, S.sxf, S.syf, wsm, wp, nu, nv, uCF, uSN, 32 * p.cf, 32 * p.snf, limx, limy,
-                       &S.qw, S.q_w);
+                qn = w_rows_q(gy, w, 0, rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf, limx, limy,
+                              S.wq[warp]);
+            if (__any_sync(FULL, qn > 0)) {  // exact pixels of this warp's rows, lanes in parallel
+                __syncwarp();
+                const int nq = qn <= QW ? qn : ((nv - warp + 7) / 8) * nu;
+                for (int i = lane; i < nq; i += 32) {
+                    int r, c;
+                    if (qn <= QW) {
+                        const unsigned it = S.wq[warp][i];
+                        r = (int)(it >> 8);
+                        c = (int)(it & 0xFF);
+                    } else {  // queue overflow: every pixel of this warp's rows
+                        r = warp + 8 * (i / nu);
+                        c = i % nu;
+                    }
+                    sts_u8(wsm + r * WTW + c, w_exact_tile(plan, f, bx, tp.lbx, tp.lby, tp.lfit, gy, w, h, u0 + c,
+                                                           v0 + r));
+                }
+                __syncwarp();
+            }
         }
+        // ------------------------------------------- chroma rows -> global
         if (CHROMA) {
             const unsigned limx = (unsigned)(cw - 2), limy = (unsigned)(ch - 2);
-            const long long xKX = (long long)(X0 + lane) * p.kxx, xKY = (long long)(X0 + lane) * p.kyx;
+            const long long xKX = (long long)(X0 + lane) * kxx, xKY = (long long)(X0 + lane) * kyx;
+            const long long* pxf = T.pxf + (size_t)f * ch + Y0;
+            const long long* pyf = T.pyf + (size_t)f * ch + Y0;
+            const uint8_t* b1p = &S.box[b][1][0];
+            const uint8_t* b2p = &S.box[b][2][0];
+            uint8_t* ob = oCB + (size_t)f * CB.stride + (size_t)Y0 * cw + X0;
+            uint8_t* orr = oCR + (size_t)f * CR.stride + (size_t)Y0 * cw + X0;
+            int qn;
             if (tp.cfit)
-                chroma_rows(&S.box[b][1][0], &S.box[b][2][0], BW, -(tp.cby * BW + tp.cbx), S.pxf, S.pyf,
-                            smem_u32(S.out[1]), smem_u32(S.out[2]), nx, ny, xKX, xKY, 32 * p.kxx, 32 * p.kyx,
-                            limx, limy, &S.qc, S.q_c);
+                qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY,
+                                   32 * kxx, 32 * kyx, limx, limy, S.wq[warp]);
             else
-                chroma_rows(gcb, gcr, cw, 0, S.pxf, S.pyf, smem_u32(S.out[1]), smem_u32(S.out[2]), nx, ny, xKX,
-                            xKY, 32 * p.kxx, 32 * p.kyx, limx, limy, &S.qc, S.q_c);
+                qn = chroma_rows_q(gcb, gcr, cw, 0, pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY, 32 * kxx, 32 * kyx,
+                                   limx, limy, S.wq[warp]);
+            if (__any_sync(FULL, qn > 0)) {
+                __syncwarp();
+                const int nq = qn <= QW ? qn : ((ny - warp + 7) / 8) * nx;
+                for (int i = lane; i < nq; i += 32) {
+                    int r, c;
+                    if (qn <= QW) {
+                        const unsigned it = S.wq[warp][i];
+                        r = (int)(it >> 8);
+                        c = (int)(it & 0xFF);
+                    } else {
+                        r = warp + 8 * (i / nx);
+                        c = i % nx;
+                    }
+                    const uint32_t v = chroma_exact_tile(plan, f, g, b1p, b2p, tp.cbx, tp.cby, tp.cfit, gcb, gcr, w,
+                                                         h, cw, ch, X0 + c, Y0 + r);
+                    const size_t o = (size_t)r * cw + c;
+                    stg_u8(ob + o, v & 0xFF);
+                    stg_u8(orr + o, v >> 8);
+                }
+                __syncwarp();
+            }
         }
-        __syncthreads();
-        // ------------------------------------------- phase B: exact W pixels
+        __syncthreads();  // wt[b] complete; box[b] free for tile k+2 after this
+        // ------------------------------------------- crop_resize of W -> global
         if (LUMA) {
-            const int nq = S.qw;
-            if (nq <= QCAP) {
-                for (int q = tid; q < nq; q += NT) {
-                    const unsigned item = S.q_w[q];
-                    const int r = (int)(item >> 8), c = (int)(item & 0xFF);
-                    wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
+            uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + lane;
+            const bool c0 = lane < nx, c1 = lane + 32 < nx;
+            if (identity) {
+                for (int r = warp; r < ny; r += NT / 32) {
+                    if (c0) stg_u8(oy + (size_t)r * w, wt[r * WTW + lane]);
+                    if (c1) stg_u8(oy + (size_t)r * w + 32, wt[r * WTW + lane + 32]);
                 }
             } else {
-                for (int i = tid; i < nu * nv; i += NT) {
-                    const int r = i / nu, c = i - r * nu;
-                    wdst[r * wp + c] = w_exact(gy, w, h, p, u0 + c, v0 + r);
-                }
-            }
-        }
-        // ------------------------------------------- phase C: crop_resize of W, fast path
-        if (LUMA && !identity) {
-            __syncthreads();
-            int x0[2], x1[2];
-            float fxv[2];
+                int x0[2], x1[2];
+                float fxv[2];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int c = min(lane + 32 * j, nx - 1);
-                x0[j] = S.cx0[c] - u0;
-                x1[j] = min(S.cx0[c] + 1, w - 1) - u0;
-                fxv[j] = (float)S.cfx[c];
-            }
-            const bool c0 = lane < nx, c1 = lane + 32 < nx;
-            const uint32_t o0 = smem_u32(S.out[0]) + lane;
-            for (int r = warp; r < ny; r += NT / 32) {
-                const int cy = S.cy0[r];
-                const uint8_t* row0 = S.wt[cy - v0];
-                const uint8_t* row1 = S.wt[min(cy + 1, h - 1) - v0];
-                const float fy = S.cfyf[r];
-                bool b0 = false, b1 = false;
-                const uint32_t a0 = blend_bad(row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]], fxv[0], fy, b0);
-                const uint32_t a1 = blend_bad(row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]], fxv[1], fy, b1);
-                b0 = b0 && c0;
-                b1 = b1 && c1;
-                if (c0) sts_u8(o0 + r * TW, a0);
-                if (c1) sts_u8(o0 + r * TW + 32, a1);
-                if (__ballot_sync(0xFFFFFFFFu, b0 || b1)) {
-                    const unsigned it = (1u << 30) | ((unsigned)r << 8) | (unsigned)lane;
-                    push_bad(&S.qc, S.q_c, b0, it);
-                    push_bad(&S.qc, S.q_c, b1, it + 32);
+                for (int j = 0; j < 2; ++j) {
+                    const int c = X0 + min(lane + 32 * j, nx - 1);
+                    const int cx = __ldg(T.cx0 + c);
+                    x0[j] = cx - u0;
+                    x1[j] = min(cx + 1, w - 1) - u0;
+                    fxv[j] = (float)__ldg(T.cfx + c);
                 }
-            }
-        }
-        __syncthreads();
-        // ------------------------------------------- phase D: exact crop + chroma pixels
-        {
-            const int nq = S.qc;
-            if (nq <= QCAP) {
-                for (int q = tid; q < nq; q += NT) {
-                    const unsigned item = S.q_c[q];
-                    const int kind = item >> 30, r = (int)((item >> 8) & 0xFF), c = (int)(item & 0xFF);
-                    if (LUMA && kind == 1) {
-                        S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
-                    } else if (CHROMA && kind == 2) {
-                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c], S.out[2][r][c]);
+                int qn = 0;
+                const size_t step = (size_t)(NT / 32) * w;
+                uint8_t* py = oy + (size_t)warp * w;
+                int ncy = __ldg(T.cy0 + Y0 + min(warp, ny - 1));
+                double ncfy = __ldg(T.cfy + Y0 + min(warp, ny - 1));
+                for (int r = warp; r < ny; r += NT / 32, py += step) {
+                    const int cy = ncy;
+                    const float fy = (float)ncfy;
+                    ncy = __ldg(T.cy0 + Y0 + min(r + NT / 32, ny - 1));
+                    ncfy = __ldg(T.cfy + Y0 + min(r + NT / 32, ny - 1));
+                    const uint8_t* row0 = wt + (cy - v0) * WTW;
+                    const uint8_t* row1 = wt + (min(cy + 1, h - 1) - v0) * WTW;
+                    bool b0 = false, b1 = false;
+                    const uint32_t a0 = blend_bad(row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]], fxv[0], fy, b0);
+                    const uint32_t a1 = blend_bad(row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]], fxv[1], fy, b1);
+                    if (c0) stg_u8(py, a0);
+                    if (c1) stg_u8(py + 32, a1);
+                    b0 = b0 && c0;
+                    b1 = b1 && c1;
+                    if (__any_sync(FULL, b0 || b1)) {
+                        const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
+                        wq_push(S.wq[warp], qn, b0, it);
+                        wq_push(S.wq[warp], qn, b1, it + 32);
                     }
                 }
-            } else {
-                for (int i = tid; i < nx * ny; i += NT) {
-                    const int r = i / nx, c = i - r * nx;
-                    if (LUMA && !identity)
-                        S.out[0][r][c] = crop_exact_t(S.wt, S.cx0, S.cy0, S.cfx, S.cfy, r, c, u0, v0, w, h);
-                    if (CHROMA)
-                        chroma_exact(p, g, cm, gcb, gcr, cw, ch, X0 + c, Y0 + r, S.out[1][r][c], S.out[2][r][c]);
+                if (__any_sync(FULL, qn > 0)) {
+                    __syncwarp();
+                    const int nq = qn <= QW ? qn : ((ny - warp + 7) / 8) * nx;
+                    for (int i = lane; i < nq; i += 32) {
+                        int r, c;
+                        if (qn <= QW) {
+                            const unsigned it = S.wq[warp][i];
+                            r = (int)(it >> 8);
+                            c = (int)(it & 0xFF);
+                        } else {
+                            r = warp + 8 * (i / nx);
+                            c = i % nx;
+                        }
+                        stg_u8(oy + (size_t)r * w + c - lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
+                    }
+                    __syncwarp();
                 }
             }
         }
-        __syncthreads();
-        for (int kp = (LUMA ? 0 : 1); kp < (CHROMA ? 3 : 1); ++kp) {
-            uint8_t* base = kp == 0 ? oY + (size_t)f * Y.stride
-                                    : (kp == 1 ? oCB + (size_t)f * CB.stride : oCR + (size_t)f * CR.stride);
-            const int pw = kp == 0 ? w : cw;
-            if (nx == TW) {  // 16-byte stores (pitch % 16 == 0 is a TMA precondition)
-                for (int i = tid; i < ny * (TW / 16); i += NT) {
-                    const int r = i >> 2, c = (i & 3) * 16;
-                    const uint4 v = *reinterpret_cast<const uint4*>(&S.out[kp][r][c]);
-                    __stcs(reinterpret_cast<uint4*>(base + (size_t)(Y0 + r) * pw + X0 + c), v);
-                }
-            } else {
-                for (int r = warp; r < ny; r += NT / 32)
-                    for (int c = lane; c < nx; c += 32) base[(size_t)(Y0 + r) * pw + X0 + c] = S.out[kp][r][c];
-            }
-        }
-        __syncthreads();
     }
 }
 
@@ -1083,7 +1158,7 @@ bool launch_tma(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pla
     if (C && (!make_map(&mb, cb.base, cb.w, cb.h, frames) || !make_map(&mr, cr.base, cr.w, cr.h, frames)))
         return false;
     const int W = L ? y.w : cb.w, H = L ? y.h : cb.h;
-    const int tx = (W + TW - 1) / TW, ty = (H + TH - 1) / TH;
+    const int tx = (W + TW - 1) / TW, ty = (H + TTH - 1) / TTH;
     const long long total = (long long)tx * ty * frames;
     tile_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plan, frames, tx, ty, W, H, y.w, y.h,
                                                                     cb.w, cb.h, g, T, L ? 1 : 0, C ? 1 : 0);
