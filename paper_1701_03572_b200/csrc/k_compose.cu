@@ -785,6 +785,34 @@ __device__ __forceinline__ uint32_t px2(P s1, P s2, int pitch, int obase, long l
     return t.inb ? (b | (r << 8)) : 0x8080u;
 }
 
+// Two fast blends at once on the packed fp32x2 pipe (FFMA2/FADD2): the
+// same arithmetic as blend_bad, lane-wise.  Returns rp | rq << 8.
+struct Q4 {
+    uint32_t a, b, c, d;
+};
+
+__device__ __forceinline__ float2 sub2(float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); }
+
+__device__ __forceinline__ uint32_t blend2_bad(const Q4& p, const Q4& q, float2 fx, float2 fy, bool& badp,
+                                               bool& badq) {
+    const float2 fa = make_float2(b256(p.a), b256(q.a)), fb = make_float2(b256(p.b), b256(q.b));
+    const float2 fc = make_float2(b256(p.c), b256(q.c)), fd = make_float2(b256(p.d), b256(q.d));
+    const float2 top = __ffma2_rn(fx, sub2(fb, fa), fa);
+    const float2 bot = __ffma2_rn(fx, sub2(fd, fc), fc);
+    const float2 v = __ffma2_rn(fy, sub2(bot, top), top);
+    const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
+    const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
+    badp = fabsf(dv.x) > 0.5f - VGUARD;
+    badq = fabsf(dv.y) > 0.5f - VGUARD;
+    return (__float_as_uint(m.x) & 0xFFu) | ((__float_as_uint(m.y) & 0xFFu) << 8);
+}
+
+template <typename P>
+__device__ __forceinline__ Q4 fetch4(P src, int pitch, int obase, const Pt& t) {
+    const int o = t.inb ? t.iy * pitch + t.ix + obase : 0;
+    return Q4{src[o], src[o + 1], src[o + pitch], src[o + pitch + 1]};
+}
+
 // ---- exact reference paths, out of line (taken by ~1% of warp rows) ----
 __device__ __noinline__ uint32_t w_exact_tile(const FramePlan* __restrict__ plan, int f, const uint8_t* box,
                                               int lbx, int lby, int fit, const uint8_t* gy, int w, int h, int u,
@@ -839,11 +867,15 @@ __device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long 
         const long long SXr = rx + uCF, SYr = ry - uSN;
         rx = __ldg(rxf + min(r + NT / 32, nv - 1));  // next row's starts, one iteration ahead
         ry = __ldg(ryf + min(r + NT / 32, nv - 1));
-        bool b0, b1, b2 = false;
-        const uint32_t a0 = px1(src, pitch, obase, SXr, SYr, limx, limy, v0, 0u, b0);
-        const uint32_t a1 = px1(src, pitch, obase, SXr + CF32, SYr - SN32, limx, limy, v1, 0u, b1);
-        if (v0) sts_u8(row, a0);
-        if (v1) sts_u8(row + 32, a1);
+        bool b0, b1, b2 = false, e0, e1;
+        const Pt t0 = decode(SXr, SYr, limx, limy, v0, b0);
+        const Pt t1 = decode(SXr + CF32, SYr - SN32, limx, limy, v1, b1);
+        const uint32_t pr = blend2_bad(fetch4(src, pitch, obase, t0), fetch4(src, pitch, obase, t1),
+                                       make_float2(t0.fx, t1.fx), make_float2(t0.fy, t1.fy), e0, e1);
+        b0 = b0 || (t0.inb && e0);
+        b1 = b1 || (t1.inb && e1);
+        if (v0) sts_u8(row, t0.inb ? (pr & 0xFF) : 0u);
+        if (v1) sts_u8(row + 32, t1.inb ? (pr >> 8) : 0u);
         if (has2) {  // rare third half (nu = 65 .. 66)
             const bool v2 = lane + 64 < nu;
             const uint32_t a2 = px1(src, pitch, obase, SXr + 2 * CF32, SYr - 2 * SN32, limx, limy, v2, 0u, b2);
@@ -877,9 +909,16 @@ __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, c
         const long long PXr = px + xKX, PYr = py + xKY;
         px = __ldg(pxf + min(r + NT / 32, ny - 1));
         py = __ldg(pyf + min(r + NT / 32, ny - 1));
-        bool b0, b1;
-        const uint32_t a0 = px2(s1, s2, pitch, obase, PXr, PYr, limx, limy, v0, b0);
-        const uint32_t a1 = px2(s1, s2, pitch, obase, PXr + KX32, PYr + KY32, limx, limy, v1, b1);
+        bool b0, b1, e0, e1, e2, e3;
+        const Pt t0 = decode(PXr, PYr, limx, limy, v0, b0);
+        const Pt t1 = decode(PXr + KX32, PYr + KY32, limx, limy, v1, b1);
+        const uint32_t p0 = blend2_bad(fetch4(s1, pitch, obase, t0), fetch4(s2, pitch, obase, t0),
+                                       make_float2(t0.fx, t0.fx), make_float2(t0.fy, t0.fy), e0, e1);
+        const uint32_t p1 = blend2_bad(fetch4(s1, pitch, obase, t1), fetch4(s2, pitch, obase, t1),
+                                       make_float2(t1.fx, t1.fx), make_float2(t1.fy, t1.fy), e2, e3);
+        b0 = b0 || (t0.inb && (e0 || e1));
+        b1 = b1 || (t1.inb && (e2 || e3));
+        const uint32_t a0 = t0.inb ? p0 : 0x8080u, a1 = t1.inb ? p1 : 0x8080u;
         if (v0) {
             stg_u8(pb, a0 & 0xFF);
             stg_u8(pr, a0 >> 8);
@@ -1079,9 +1118,11 @@ __global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
                     ncfy = __ldg(T.cfy + Y0 + min(r + NT / 32, ny - 1));
                     const uint8_t* row0 = wt + (cy - v0) * WTW;
                     const uint8_t* row1 = wt + (min(cy + 1, h - 1) - v0) * WTW;
-                    bool b0 = false, b1 = false;
-                    const uint32_t a0 = blend_bad(row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]], fxv[0], fy, b0);
-                    const uint32_t a1 = blend_bad(row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]], fxv[1], fy, b1);
+                    bool b0, b1;
+                    const uint32_t pr = blend2_bad(Q4{row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]]},
+                                                   Q4{row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]]},
+                                                   make_float2(fxv[0], fxv[1]), make_float2(fy, fy), b0, b1);
+                    const uint32_t a0 = pr & 0xFF, a1 = pr >> 8;
                     if (c0) stg_u8(py, a0);
                     if (c1) stg_u8(py + 32, a1);
                     b0 = b0 && c0;
