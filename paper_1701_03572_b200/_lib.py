@@ -14,7 +14,7 @@ import threading
 from . import _abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstabgpu.so")
+LIB_PATH = os.environ.get("STABGPU_LIB", os.path.join(_HERE, "libstabgpu.so"))
 
 _lib = None
 _lock = threading.Lock()

@@ -217,43 +217,52 @@ __device__ __forceinline__ uint32_t px_at(const Level& L, int x, int y, bool int
 }
 
 
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+
 // sum over the valid window of cur(j, i) * grad(j, i), lane L <-> column
-// cx + L (lane vw only supplies the right neighbour).  INTERIOR: the
-// (vh+1) x (vw+1) source block lies inside the image, so no clamping.
+// cx + L (lane vw only supplies the right neighbour).  The gradients are a
+// [vh][32] array of {gx, gy} with zeros in columns >= vw, so every lane
+// accumulates unconditionally.  Image rows are prefetched four ahead (the
+// loads are independent of the arithmetic), clamped to the last row.
+// INTERIOR: the (vh+1) x (vw+1) source block lies inside the image.
 template <bool INTERIOR>
-__device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw, int vh,
-                                         double cfx, double cfy, uint32_t gx_addr,
-                                         uint32_t gy_addr, double& sx, double& sy) {
+__device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw, int vh, double cfx,
+                                         double cfy, uint32_t g_addr, double& sx, double& sy) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const bool ld = lane <= vw, col = lane < vw;
-    const uint32_t rstep = (uint32_t)vw * 8u;
-    const uint8_t* rowp = ci.px + (size_t)cy * ci.w + cx + lane;
-    auto load = [&](int k) -> uint32_t {
-        if (!ld) return 0u;
+    const bool ld = lane <= vw;
+    const int xl = cx + (ld ? lane : 0);
+    const uint8_t* rowp = ci.px + (size_t)cy * ci.w + xl;
+    auto load = [&](int k) -> uint32_t {  // image row cy + min(k, vh)
+        k = min(k, vh);
         if (INTERIOR) return __ldg(rowp + (size_t)k * ci.w);
-        return px_at(ci, cx + lane, cy + k, false);
+        return px_at(ci, xl, cy + k, false);
     };
-    uint32_t pb = load(0), nb = load(1);
+    uint32_t b0 = load(0), b1 = load(1), b2 = load(2), b3 = load(3), b4 = load(4);
     double hp;
     {
-        const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-        const double a = u2d(pb);
+        const uint32_t qb = __shfl_down_sync(FULL, b0, 1);
+        const double a = u2d(b0);
         hp = fma(cfx, u2d(qb) - a, a);
     }
-#pragma unroll 2
     for (int k = 1; k <= vh; ++k) {
-        pb = nb;
-        if (k < vh) nb = load(k + 1);
+        const uint32_t pb = b1;
+        b1 = b2;
+        b2 = b3;
+        b3 = b4;
+        b4 = load(k + 4);
         const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
         const double a = u2d(pb);
         const double h = fma(cfx, u2d(qb) - a, a);
         const double cur = fma(cfy, h - hp, hp);
-        const double cm = col ? cur : 0.0;
-        sx = fma(cm, lds_f64(gx_addr), sx);
-        sy = fma(cm, lds_f64(gy_addr), sy);
-        gx_addr += rstep;
-        gy_addr += rstep;
+        const double2 g = lds_f64x2(g_addr);
+        sx = fma(cur, g.x, sx);
+        sy = fma(cur, g.y, sy);
+        g_addr += 32 * 16;
         hp = h;
     }
 }
@@ -266,19 +275,15 @@ __device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw
 template <bool INTERIOR, bool XTRA>
 __device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, int es, double fx,
                                               double fy, int jv0, int jv1, int iv0, int iv1,
-                                              uint32_t gxa, uint32_t gya, double& gxx, double& gxy,
-                                              double& gyy, double& tx, double& ty) {
+                                              uint32_t ga, double& gxx, double& gxy, double& gyy,
+                                              double& tx, double& ty) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const bool tld = lane <= (es < 31 ? es : 31);
     const bool xtra = XTRA && lane == 31;
     const int ti = lane - 1;  // template column of this lane
     const bool tcol = ti >= iv0 && ti <= iv1;
-    const int vw = iv1 - iv0 + 1;
-    const uint32_t rstep = (uint32_t)vw * 8u;
-    const uint32_t coff = (uint32_t)((tcol ? ti - iv0 : 0) * 8);
-    gxa += coff;
-    gya += coff;
+    ga += (uint32_t)((tcol ? ti - iv0 : 0) * 16);
     auto load = [&](int x, int k) -> uint32_t {
         if (INTERIOR) return __ldg(pi.px + (size_t)(yb + k) * pi.w + x);
         return px_at(pi, x, yb + k, false);
@@ -321,11 +326,9 @@ __device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, i
                 const bool ok = tcol && j >= jv0 && j <= jv1;
                 const double dx = ok ? 0.5 * (right - left) : 0.0;
                 const double dy = ok ? 0.5 * (ev - eA) : 0.0;
-                if (ok) {
-                    const uint32_t ro = (uint32_t)(j - jv0) * rstep;
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(gxa + ro), "d"(dx));
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(gya + ro), "d"(dy));
-                }
+                if (ok)
+                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga + (uint32_t)(j - jv0) * 512u), "d"(dx),
+                                 "d"(dy));
                 gxx = fma(dx, dx, gxx);
                 gxy = fma(dx, dy, gxy);
                 gyy = fma(dy, dy, gyy);
@@ -342,8 +345,8 @@ __device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, i
 }
 
 __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
-                                const stabgpu_flow_cfg& cfg, double* tgx, double* tgy,
-                                double& ox, double& oy, unsigned& iters, unsigned& builds) {
+                                const stabgpu_flow_cfg& cfg, double* tg, double& ox, double& oy,
+                                unsigned& iters, unsigned& builds) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
@@ -383,15 +386,18 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
         const bool tin = xb >= 0 && yb >= 0 && xb + es + 1 <= pi.w - 1 && yb + es <= pi.h - 1;
         double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
-        const uint32_t gxa0 = (uint32_t)__cvta_generic_to_shared(tgx);
-        const uint32_t gya0 = (uint32_t)__cvta_generic_to_shared(tgy);
+        const uint32_t ga0 = (uint32_t)__cvta_generic_to_shared(tg);
         if (es > 31) {
-            if (tin) template_pass<true, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
-            else template_pass<false, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
+            if (tin) template_pass<true, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
+            else template_pass<false, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
         } else {
-            if (tin) template_pass<true, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
-            else template_pass<false, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, gxa0, gya0, gxx, gxy, gyy, tx, ty);
+            if (tin) template_pass<true, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
+            else template_pass<false, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
         }
+        if (lane >= vw)  // zero gradient columns outside the valid window
+            for (int j = 0; j < vh; ++j)
+                asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(ga0 + (uint32_t)j * 512u + lane * 16u),
+                             "d"(0.0));
         gxx = warp_dsum(gxx);
         gxy = warp_dsum(gxy);
         gyy = warp_dsum(gyy);
@@ -407,9 +413,7 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
         double vx = 0.0, vy = 0.0;
         bool diverged = false;
-        const int lc = lane < vw ? lane : 0;
-        const uint32_t gxa = (uint32_t)__cvta_generic_to_shared(tgx + lc);
-        const uint32_t gya = (uint32_t)__cvta_generic_to_shared(tgy + lc);
+        const uint32_t ga = ga0 + lane * 16u;
         for (int it = 0; it < cfg.max_iterations; ++it) {
             const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
             if (!inside(ci, qx, qy)) {
@@ -423,8 +427,8 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
             // sum(cur * grad); b = T - that
             double sx = 0.0, sy = 0.0;
-            if (cin) row_pass<true>(ci, cx, cy, vw, vh, cfx, cfy, gxa, gya, sx, sy);
-            else row_pass<false>(ci, cx, cy, vw, vh, cfx, cfy, gxa, gya, sx, sy);
+            if (cin) row_pass<true>(ci, cx, cy, vw, vh, cfx, cfy, ga, sx, sy);
+            else row_pass<false>(ci, cx, cy, vw, vh, cfx, cfy, ga, sx, sy);
             const double bx = tx - warp_dsum(sx);
             const double by = ty - warp_dsum(sy);
             const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
@@ -462,9 +466,7 @@ __global__ void __launch_bounds__(128) lk_fast_kernel(LkStep s, stabgpu_flow_cfg
                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int side = 2 * cfg.window_radius + 1;
-    double* tgx = lsm + (size_t)warp * smem_per_warp;
-    double* tgy = tgx + side * side;
+    double* tg = lsm + (size_t)warp * smem_per_warp;
     const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
     while (true) {
         unsigned item = 0;
@@ -481,17 +483,17 @@ __global__ void __launch_bounds__(128) lk_fast_kernel(LkStep s, stabgpu_flow_cfg
         bool keep;
         if (s.mode == 2) {
             double bx, by;
-            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tgx, tgy, bx, by, iters, builds);
+            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tg, bx, by, iters, builds);
             if (keep) {
                 const double2 q = s.ref[slot];
                 const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
                 keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
             }
         } else {
-            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tgx, tgy, fx, fy, iters, builds);
+            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tg, fx, fy, iters, builds);
             if (keep && s.mode == 1) {
                 double bx, by;
-                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tgx, tgy, bx, by, iters, builds);
+                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tg, bx, by, iters, builds);
                 if (keep) {
                     const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
                     keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
@@ -610,7 +612,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (s.nseg <= 0 || s.max_pts <= 0) return;
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
-        const int per_warp = 2 * side * side;  // doubles: template gradients
+        const int per_warp = side * 32 * 2;  // doubles: template gradients {gx, gy}[side][32]
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
