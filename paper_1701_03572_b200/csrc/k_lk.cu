@@ -16,6 +16,7 @@
 // the 32 lanes stride it densely.  Segments (independent 5-frame tracking
 // chains, grid.y) and features (grid.x) are both batched into one launch.
 #include <algorithm>
+#include <climits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -223,46 +224,92 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
     return v;
 }
 
-// sum over the valid window of cur(j, i) * grad(j, i), lane L <-> column
-// cx + L (lane vw only supplies the right neighbour).  The gradients are a
-// [vh][32] array of {gx, gy} with zeros in columns >= vw, so every lane
-// accumulates unconditionally.  Image rows are prefetched four ahead (the
-// loads are independent of the arithmetic), clamped to the last row.
-// INTERIOR: the (vh+1) x (vw+1) source block lies inside the image.
-template <bool INTERIOR>
-__device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw, int vh, double cfx,
-                                         double cfy, uint32_t g_addr, double& sx, double& sy) {
-    const unsigned FULL = 0xffffffffu;
+// Current-frame window staging.  The iterations of one level read the
+// (vh+1) x (vw+1) source block around the moving estimate; it is copied once
+// into a per-warp shared tile with a margin of SM_MARGIN pixels (clamped at
+// the image border exactly as the reference's clamped fetches), and re-copied
+// only when the estimate leaves the staged region.  Every lane's byte loads
+// are independent, so the global latency is paid once per staging instead of
+// once per row.
+constexpr int SM_MARGIN = 3;
+constexpr int SM_PITCH = 48;  // bytes per staged row (>= 32 + 1 + 2 * margin + 3)
+constexpr int SM_ROWS = 40;   // >= 32 + 2 * margin
+
+// Copies image block [x0, x0+sw) x [y0, y0+sh) (clamped at the border) to a
+// per-warp shared tile (row pitch SM_PITCH) and returns the tile column of
+// image column x0.  Interior blocks of 4-byte-aligned rows go as aligned
+// 32-bit words, several rows per warp instruction (lane -> (row, word)); the
+// border case goes byte by byte with the reference's clamped indices.
+__device__ __forceinline__ int stage_block(const Level& L, int x0, int y0, int sw, int sh, uint8_t* dst) {
     const int lane = threadIdx.x & 31;
-    const bool ld = lane <= vw;
-    const int xl = cx + (ld ? lane : 0);
-    const uint8_t* rowp = ci.px + (size_t)cy * ci.w + xl;
-    auto load = [&](int k) -> uint32_t {  // image row cy + min(k, vh)
-        k = min(k, vh);
-        if (INTERIOR) return __ldg(rowp + (size_t)k * ci.w);
-        return px_at(ci, xl, cy + k, false);
-    };
-    uint32_t b0 = load(0), b1 = load(1), b2 = load(2), b3 = load(3), b4 = load(4);
+    const int xw = x0 & ~3;
+    const int nw = ((x0 + sw - 1) >> 2) - (xw >> 2) + 1;  // words per row (<= SM_PITCH / 4)
+    const bool words = ((L.w & 3) == 0) && ((reinterpret_cast<uintptr_t>(L.px) & 3) == 0) && x0 >= 0 &&
+                       y0 >= 0 && xw + 4 * nw <= L.w && y0 + sh <= L.h;
+    if (words) {
+        const int rpp = 32 / nw, lr = lane / nw, lw = lane - lr * nw;
+        if (lr < rpp) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(L.px + (size_t)(y0 + lr) * L.w + xw) + lw;
+            uint32_t* d = reinterpret_cast<uint32_t*>(dst + lr * SM_PITCH) + lw;
+            const size_t sstep = (size_t)rpp * (L.w >> 2);
+            const int dstep = rpp * (SM_PITCH / 4);
+            int r = lr;
+            for (; r + 3 * rpp < sh; r += 4 * rpp) {  // four loads in flight
+                const uint32_t a = __ldg(src), b = __ldg(src + sstep), c = __ldg(src + 2 * sstep),
+                               e = __ldg(src + 3 * sstep);
+                d[0] = a;
+                d[dstep] = b;
+                d[2 * dstep] = c;
+                d[3 * dstep] = e;
+                src += 4 * sstep;
+                d += 4 * dstep;
+            }
+            for (; r < sh; r += rpp) {
+                *d = __ldg(src);
+                src += sstep;
+                d += dstep;
+            }
+        }
+        return x0 - xw;
+    }
+    for (int i = lane; i < sw * sh; i += 32) {
+        const int r = i / sw, c = i - r * sw;
+        dst[r * SM_PITCH + c] =
+            __ldg(L.px + (size_t)clampi(y0 + r, 0, L.h - 1) * L.w + clampi(x0 + c, 0, L.w - 1));
+    }
+    return 0;
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// sum over the valid window of cur(j, i) * grad(j, i), lane L <-> column
+// L of the staged block at shared address `src` (row pitch SM_PITCH).  The
+// gradients are a [vh][32] array of {gx, gy} with zeros in columns >= vw, so
+// every lane accumulates unconditionally.
+__device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx, double cfy, const double2* g,
+                                         double& sx, double& sy) {
+    const int lane = threadIdx.x & 31;
+    src += lane;
+    g += lane;
     double hp;
     {
-        const uint32_t qb = __shfl_down_sync(FULL, b0, 1);
-        const double a = u2d(b0);
-        hp = fma(cfx, u2d(qb) - a, a);
+        const double a = u2d(src[0]);
+        hp = fma(cfx, u2d(src[1]) - a, a);
     }
+#pragma unroll 4
     for (int k = 1; k <= vh; ++k) {
-        const uint32_t pb = b1;
-        b1 = b2;
-        b2 = b3;
-        b3 = b4;
-        b4 = load(k + 4);
-        const uint32_t qb = __shfl_down_sync(FULL, pb, 1);
-        const double a = u2d(pb);
-        const double h = fma(cfx, u2d(qb) - a, a);
+        src += SM_PITCH;
+        const double a = u2d(src[0]);
+        const double h = fma(cfx, u2d(src[1]) - a, a);
         const double cur = fma(cfy, h - hp, hp);
-        const double2 g = lds_f64x2(g_addr);
-        sx = fma(cur, g.x, sx);
-        sy = fma(cur, g.y, sy);
-        g_addr += 32 * 16;
+        const double2 gg = *g;
+        sx = fma(cur, gg.x, sx);
+        sy = fma(cur, gg.y, sy);
+        g += 32;
         hp = h;
     }
 }
@@ -272,48 +319,28 @@ __device__ __forceinline__ void row_pass(const Level& ci, int cx, int cy, int vw
 // column L (XTRA: es == 33, lane 31 also owns column 32), image rows rolled
 // through registers.  Writes the template gradients over the valid window
 // (row stride vw) and accumulates G and T = sum(template value * gradient).
-template <bool INTERIOR, bool XTRA>
-__device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, int es, double fx,
-                                              double fy, int jv0, int jv1, int iv0, int iv1,
-                                              uint32_t ga, double& gxx, double& gxy, double& gyy,
-                                              double& tx, double& ty) {
+template <bool XTRA>
+__device__ __forceinline__ void template_pass(const uint8_t* src, int es, double fx, double fy, int jv0, int jv1,
+                                              int iv0, int iv1, uint32_t ga, double& gxx, double& gxy,
+                                              double& gyy, double& tx, double& ty) {
+    // src: staged image block of rows yb .. yb+es, columns xb .. xb+es+1
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const bool tld = lane <= (es < 31 ? es : 31);
     const bool xtra = XTRA && lane == 31;
     const int ti = lane - 1;  // template column of this lane
     const bool tcol = ti >= iv0 && ti <= iv1;
     ga += (uint32_t)((tcol ? ti - iv0 : 0) * 16);
-    auto load = [&](int x, int k) -> uint32_t {
-        if (INTERIOR) return __ldg(pi.px + (size_t)(yb + k) * pi.w + x);
-        return px_at(pi, x, yb + k, false);
-    };
-    uint32_t nb = tld ? load(xb + lane, 0) : 0u;
-    uint32_t n32 = 0, n33 = 0;
-    if (XTRA && xtra) {
-        n32 = load(xb + 32, 0);
-        n33 = load(xb + 33, 0);
-    }
+    src += lane;
     double hprev = 0.0, hprevx = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
 #pragma unroll 2
-    for (int k = 0; k <= es; ++k) {  // image rows yb .. yb+es
-        const uint32_t pb = nb, p32 = n32, p33 = n33;
-        if (k < es) {
-            if (tld) nb = load(xb + lane, k + 1);
-            if (XTRA && xtra) {
-                n32 = load(xb + 32, k + 1);
-                n33 = load(xb + 33, k + 1);
-            }
-        }
-        uint32_t qb = __shfl_down_sync(FULL, pb, 1);
+    for (int k = 0; k <= es; ++k, src += SM_PITCH) {  // image rows yb .. yb+es
         double hx = 0.0;
-        if (XTRA) {
-            if (xtra) qb = p32;
-            const double a = u2d(p32);
-            hx = fma(fx, u2d(p33) - a, a);
+        if (XTRA) {  // lane 31 also carries extended column 32 (from image columns 32, 33)
+            const double a = u2d(src[1]);
+            hx = fma(fx, u2d(src[2]) - a, a);
         }
-        const double a = u2d(pb);
-        const double h = fma(fx, u2d(qb) - a, a);
+        const double a = u2d(src[0]);
+        const double h = fma(fx, u2d(src[1]) - a, a);
         if (k >= 1) {
             const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
             double evx = 0.0;
@@ -345,8 +372,9 @@ __device__ __forceinline__ void template_pass(const Level& pi, int xb, int yb, i
 }
 
 __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
-                                const stabgpu_flow_cfg& cfg, double* tg, double& ox, double& oy,
-                                unsigned& iters, unsigned& builds) {
+                                const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, double& ox,
+                                double& oy, unsigned& iters, unsigned& builds) {
+    const uint32_t stg_a = (uint32_t)__cvta_generic_to_shared(stg);
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
@@ -384,18 +412,15 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         // values enter only through T = sum(tval * grad), accumulated here.
         const double fx = dsub(plx, (double)x0), fy = dsub(ply, (double)y0);
         const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
-        const bool tin = xb >= 0 && yb >= 0 && xb + es + 1 <= pi.w - 1 && yb + es <= pi.h - 1;
         double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
         const uint32_t ga0 = (uint32_t)__cvta_generic_to_shared(tg);
-        if (es > 31) {
-            if (tin) template_pass<true, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-            else template_pass<false, true>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-        } else {
-            if (tin) template_pass<true, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-            else template_pass<false, false>(pi, xb, yb, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-        }
-        if (lane >= vw)  // zero gradient columns outside the valid window
-            for (int j = 0; j < vh; ++j)
+        __syncwarp();
+        const int toff = stage_block(pi, xb, yb, es + 2, es + 1, stg);
+        __syncwarp();
+        if (es > 31) template_pass<true>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
+        else template_pass<false>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
+        for (int j = 0; j < vh; ++j)  // zero gradient columns outside the valid window
+            if (lane >= vw)
                 asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(ga0 + (uint32_t)j * 512u + lane * 16u),
                              "d"(0.0));
         gxx = warp_dsum(gxx);
@@ -414,6 +439,8 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         double vx = 0.0, vy = 0.0;
         bool diverged = false;
         const uint32_t ga = ga0 + lane * 16u;
+        const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
+        int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
         for (int it = 0; it < cfg.max_iterations; ++it) {
             const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
             if (!inside(ci, qx, qy)) {
@@ -424,11 +451,16 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             const int qx0 = (int)floor(qx), qy0 = (int)floor(qy);
             const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
             const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
-            const bool cin = cx >= 0 && cy >= 0 && cx + vw <= ci.w - 1 && cy + vh <= ci.h - 1;
+            if (cx < sx0 || cy < sy0 || cx + vw + 1 > sx0 + sw || cy + vh + 1 > sy0 + sh) {
+                sx0 = cx - SM_MARGIN;
+                sy0 = cy - SM_MARGIN;
+                __syncwarp();
+                soff = stage_block(ci, sx0, sy0, sw, sh, stg);
+                __syncwarp();
+            }
             // sum(cur * grad); b = T - that
             double sx = 0.0, sy = 0.0;
-            if (cin) row_pass<true>(ci, cx, cy, vw, vh, cfx, cfy, ga, sx, sy);
-            else row_pass<false>(ci, cx, cy, vw, vh, cfx, cfy, ga, sx, sy);
+            row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, reinterpret_cast<const double2*>(tg), sx, sy);
             const double bx = tx - warp_dsum(sx);
             const double by = ty - warp_dsum(sy);
             const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
@@ -462,11 +494,12 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
 
 // Persistent warps: each warp pulls (segment, point) work items from a global
 // counter, so early-exiting points never leave a warp slot idle.
-__global__ void __launch_bounds__(128) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
+__global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_cfg cfg,
                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* tg = lsm + (size_t)warp * smem_per_warp;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * 32 * (2 * cfg.window_radius + 1));
     const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
     while (true) {
         unsigned item = 0;
@@ -480,25 +513,28 @@ __global__ void __launch_bounds__(128) lk_fast_kernel(LkStep s, stabgpu_flow_cfg
         const double2 p = s.pts[slot];
         unsigned iters = 0, builds = 0;
         double fx = p.x, fy = p.y;
-        bool keep;
-        if (s.mode == 2) {
-            double bx, by;
-            keep = track_warp_fast(s.pyr, fcur, fprev, p.x, p.y, cfg, tg, bx, by, iters, builds);
-            if (keep) {
-                const double2 q = s.ref[slot];
-                const double ex = dsub(bx, q.x), ey = dsub(by, q.y);
-                keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
+        // one call site (code size): mode 0 = forward, 1 = forward + backward,
+        // 2 = backward from the current point against s.ref
+        const int passes = s.mode == 1 ? 2 : 1;
+        int fa = s.mode == 2 ? fcur : fprev, fb = s.mode == 2 ? fprev : fcur;
+        double ax = p.x, ay = p.y, ox = 0.0, oy = 0.0;
+        bool keep = true;
+        for (int pass = 0; pass < passes && keep; ++pass) {
+            keep = track_warp_fast(s.pyr, fa, fb, ax, ay, cfg, tg, stg, ox, oy, iters, builds);
+            if (keep && pass == 0 && s.mode != 2) {
+                fx = ox;
+                fy = oy;
             }
-        } else {
-            keep = track_warp_fast(s.pyr, fprev, fcur, p.x, p.y, cfg, tg, fx, fy, iters, builds);
-            if (keep && s.mode == 1) {
-                double bx, by;
-                keep = track_warp_fast(s.pyr, fcur, fprev, fx, fy, cfg, tg, bx, by, iters, builds);
-                if (keep) {
-                    const double ex = dsub(bx, p.x), ey = dsub(by, p.y);
-                    keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
-                }
-            }
+            const int t = fa;
+            fa = fb;
+            fb = t;
+            ax = ox;
+            ay = oy;
+        }
+        if (keep && s.mode != 0) {  // forward-backward test (flow.cpp weed_tracks)
+            const double2 q = s.mode == 2 ? s.ref[slot] : p;
+            const double ex = dsub(ox, q.x), ey = dsub(oy, q.y);
+            keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= dmul(cfg.fb_threshold, cfg.fb_threshold);
         }
         if (lane == 0) {
             s.fwd[slot] = make_double2(fx, fy);
@@ -612,7 +648,8 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (s.nseg <= 0 || s.max_pts <= 0) return;
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
-        const int per_warp = side * 32 * 2;  // doubles: template gradients {gx, gy}[side][32]
+        // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
+        const int per_warp = side * 32 * 2 + SM_ROWS * SM_PITCH / 8;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
