@@ -300,18 +300,35 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
         const double a = u2d(src[0]);
         hp = fma(cfx, u2d(src[1]) - a, a);
     }
-#pragma unroll 4
-    for (int k = 1; k <= vh; ++k) {
-        src += SM_PITCH;
-        const double a = u2d(src[0]);
-        const double h = fma(cfx, u2d(src[1]) - a, a);
-        const double cur = fma(cfy, h - hp, hp);
-        const double2 gg = *g;
-        sx = fma(cur, gg.x, sx);
-        sy = fma(cur, gg.y, sy);
-        g += 32;
-        hp = h;
+    // two partial sums per component (even / odd rows) halve the dependent
+    // DFMA chain; combined once at the end
+    double sx1 = 0.0, sy1 = 0.0;
+    int k = 1;
+#pragma unroll 2
+    for (; k + 1 <= vh; k += 2) {
+        const double a0 = u2d(src[SM_PITCH]), a1 = u2d(src[2 * SM_PITCH]);
+        const double h0 = fma(cfx, u2d(src[SM_PITCH + 1]) - a0, a0);
+        const double h1 = fma(cfx, u2d(src[2 * SM_PITCH + 1]) - a1, a1);
+        const double c0 = fma(cfy, h0 - hp, hp), c1 = fma(cfy, h1 - h0, h0);
+        const double2 g0 = g[0], g1 = g[32];
+        sx = fma(c0, g0.x, sx);
+        sy = fma(c0, g0.y, sy);
+        sx1 = fma(c1, g1.x, sx1);
+        sy1 = fma(c1, g1.y, sy1);
+        src += 2 * SM_PITCH;
+        g += 64;
+        hp = h1;
     }
+    if (k <= vh) {
+        const double a = u2d(src[SM_PITCH]);
+        const double h = fma(cfx, u2d(src[SM_PITCH + 1]) - a, a);
+        const double c = fma(cfy, h - hp, hp);
+        const double2 gg = g[0];
+        sx = fma(c, gg.x, sx);
+        sy = fma(c, gg.y, sy);
+    }
+    sx += sx1;
+    sy += sy1;
 }
 
 
