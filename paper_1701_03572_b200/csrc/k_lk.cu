@@ -291,10 +291,10 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 // gradients are a [vh][32] array of {gx, gy} with zeros in columns >= vw, so
 // every lane accumulates unconditionally.
 __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx, double cfy, const double2* g,
-                                         double& sx, double& sy) {
+                                         int gstep, double& sx, double& sy) {
+    // g: this lane's gradient column (row step gstep), or a zero slot (step 0)
     const int lane = threadIdx.x & 31;
     src += lane;
-    g += lane;
     double hp;
     {
         const double a = u2d(src[0]);
@@ -310,13 +310,13 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
         const double h0 = fma(cfx, u2d(src[SM_PITCH + 1]) - a0, a0);
         const double h1 = fma(cfx, u2d(src[2 * SM_PITCH + 1]) - a1, a1);
         const double c0 = fma(cfy, h0 - hp, hp), c1 = fma(cfy, h1 - h0, h0);
-        const double2 g0 = g[0], g1 = g[32];
+        const double2 g0 = g[0], g1 = g[gstep];
         sx = fma(c0, g0.x, sx);
         sy = fma(c0, g0.y, sy);
         sx1 = fma(c1, g1.x, sx1);
         sy1 = fma(c1, g1.y, sy1);
         src += 2 * SM_PITCH;
-        g += 64;
+        g += 2 * gstep;
         hp = h1;
     }
     if (k <= vh) {
@@ -338,7 +338,7 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
 // (row stride vw) and accumulates G and T = sum(template value * gradient).
 template <bool XTRA>
 __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double fx, double fy, int jv0, int jv1,
-                                              int iv0, int iv1, uint32_t ga, double& gxx, double& gxy,
+                                              int iv0, int iv1, uint32_t ga, uint32_t grow, double& gxx, double& gxy,
                                               double& gyy, double& tx, double& ty) {
     // src: staged image block of rows yb .. yb+es, columns xb .. xb+es+1
     const unsigned FULL = 0xffffffffu;
@@ -371,7 +371,7 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
                 const double dx = ok ? 0.5 * (right - left) : 0.0;
                 const double dy = ok ? 0.5 * (ev - eA) : 0.0;
                 if (ok)
-                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga + (uint32_t)(j - jv0) * 512u), "d"(dx),
+                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga + (uint32_t)(j - jv0) * grow), "d"(dx),
                                  "d"(dy));
                 gxx = fma(dx, dx, gxx);
                 gxy = fma(dx, dy, gxy);
@@ -434,12 +434,11 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         __syncwarp();
         const int toff = stage_block(pi, xb, yb, es + 2, es + 1, stg);
         __syncwarp();
-        if (es > 31) template_pass<true>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-        else template_pass<false>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, gxx, gxy, gyy, tx, ty);
-        for (int j = 0; j < vh; ++j)  // zero gradient columns outside the valid window
-            if (lane >= vw)
-                asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(ga0 + (uint32_t)j * 512u + lane * 16u),
-                             "d"(0.0));
+        const uint32_t grow = (uint32_t)vw * 16u;  // gradients: [vh][vw] {gx, gy}, then a zero slot
+        if (es > 31) template_pass<true>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
+        else template_pass<false>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
+        if (lane == 0)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(ga0 + (uint32_t)(vh * vw) * 16u), "d"(0.0));
         gxx = warp_dsum(gxx);
         gxy = warp_dsum(gxy);
         gyy = warp_dsum(gyy);
@@ -455,7 +454,9 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
         double vx = 0.0, vy = 0.0;
         bool diverged = false;
-        const uint32_t ga = ga0 + lane * 16u;
+        // lanes past the valid window read the zero slot (row step 0)
+        const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
+        const int gstep = lane < vw ? vw : 0;
         const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
         int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
         for (int it = 0; it < cfg.max_iterations; ++it) {
@@ -477,7 +478,7 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
             }
             // sum(cur * grad); b = T - that
             double sx = 0.0, sy = 0.0;
-            row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, reinterpret_cast<const double2*>(tg), sx, sy);
+            row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, gcol, gstep, sx, sy);
             const double bx = tx - warp_dsum(sx);
             const double by = ty - warp_dsum(sy);
             const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
@@ -516,7 +517,8 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* tg = lsm + (size_t)warp * smem_per_warp;
-    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * 32 * (2 * cfg.window_radius + 1));
+    const int side = 2 * cfg.window_radius + 1;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * (side * side + 1));
     const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
     while (true) {
         unsigned item = 0;
@@ -666,7 +668,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
         // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
-        const int per_warp = side * 32 * 2 + SM_ROWS * SM_PITCH / 8;
+        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
