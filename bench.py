@@ -151,7 +151,7 @@ def run_reference_arm(args, cfg):
     value = sample / (ms / 1000.0)
     desc = f"first {sample} of {n_total} frames of {args.config}, reference stage functions on {threads} threads"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
             "config": workload(args, cfg), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -291,7 +291,7 @@ def run_ours(args, cfg):
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": fb * n,
                         "d2h_bytes_per_step": fb * n + n * pipeline.RECORD_BYTES,
                         "ms_per_step": ms_e2e},
-                "roofline": {"bound": "hbm", "kernel": "K8 compose (luma_kernel + chroma_kernel)",
+                "roofline": {"bound": "hbm", "kernel": "K8 compose_tma_kernel (fused warp + crop/resize, all planes)",
                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": (achieved / hbm) if achieved else None, "traffic": None,
                              "peak_source": peak_src,
