@@ -34,6 +34,19 @@ METRIC = "stabilized frames/s at 1080p (1/2/4/8 B200); kernel % of HBM roofline"
 UNIT = "frames/s"
 
 
+def compose_traffic(spec, planes, frames):
+    """DRAM bytes (read + write) of one compose launch, from the committed ncu
+    --set full capture (profiles/compose_traffic.json), scaled per frame."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "compose_traffic.json")
+    try:
+        t = json.load(open(p))
+    except (OSError, ValueError):
+        return None
+    if (t["width"], t["height"], t["planes"]) != (spec.width, spec.height, planes):
+        return None
+    return (t["dram_bytes_read"] + t["dram_bytes_write"]) * frames / t["frames_per_launch"]
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -293,7 +306,8 @@ def run_ours(args, cfg):
                         "ms_per_step": ms_e2e},
                 "roofline": {"bound": "hbm", "kernel": "K8 compose_tma_kernel (fused warp + crop/resize, all planes)",
                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                             "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                             "frac": (achieved / hbm) if achieved else None,
+                             "traffic": compose_traffic(spec, planes, sh.own_end - sh.own_begin if world > 1 else n),
                              "peak_source": peak_src,
                              "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms},
                 "stage_ms": stages,
