@@ -388,11 +388,17 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
     }
 }
 
-__device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
-                                const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, double& ox,
-                                double& oy, unsigned& iters, unsigned& builds) {
-    const uint32_t stg_a = (uint32_t)__cvta_generic_to_shared(stg);
-    const unsigned FULL = 0xffffffffu;
+// Pyramidal track_one (flow.cpp:132-227) of up to two trackers that share one
+// template: the patch around (px, py) in frame ft.  Tracker 0 follows the
+// point into frame f0, tracker 1 (when f1 >= 0) into frame f1.  Both walk the
+// levels coarse to fine with their own guesses; each level's template is
+// built once (staged block -> gradients, G and T) and both trackers iterate on
+// it.  Tracker j's success and result go to ok[j], o[j]; iteration counts to
+// it[j].  A template failure (outside / TooSmall at level 0 / Unconditioned)
+// fails both, exactly as it fails a lone track_one.
+__device__ void track_dual(const DevPyramid& P, int ft, double px, double py, int f0, int f1,
+                           const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, bool& ok0, bool& ok1,
+                           double2& o0, double2& o1, unsigned& it0, unsigned& it1, unsigned& builds) {
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
     const int e = r + 1, es = 2 * e + 1;  // extended template patch (flow.cpp:79-81)
@@ -404,13 +410,16 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         }
     const int min_count = max(25, side * side / 4);
     const double r2 = (double)r * r, eps2 = dmul(cfg.epsilon, cfg.epsilon);
-    double gfx = 0.0, gfy = 0.0;
+    const int nt = f1 >= 0 ? 2 : 1;
+    // per-tracker guesses in scalars (no local-memory arrays)
+    double gx0 = 0.0, gy0 = 0.0, gx1 = 0.0, gy1 = 0.0;
+    bool al0 = true, al1 = f1 >= 0;
+    ok0 = ok1 = false;
     for (int level = start_level; level >= 0; --level) {
-        const Level pi{P.lvl[level] + (size_t)fprev * P.stride[level], P.w[level], P.h[level]};
-        const Level ci{P.lvl[level] + (size_t)fcur * P.stride[level], P.w[level], P.h[level]};
+        const Level pi{P.lvl[level] + (size_t)ft * P.stride[level], P.w[level], P.h[level]};
         const double scale = (double)(1u << level);
         const double plx = ddiv(px, scale), ply = ddiv(py, scale);
-        if (!inside(pi, plx, ply)) return false;
+        if (!inside(pi, plx, ply)) return;
         const int x0 = (int)floor(plx), y0 = (int)floor(ply);
         // valid window (flow.cpp:95-103): rows 1 <= y0-r+j <= h-3, columns alike
         const int jv0 = max(0, 1 - y0 + r), jv1 = min(side - 1, pi.h - 3 - y0 + r);
@@ -418,15 +427,17 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         const int vh = jv1 - jv0 + 1, vw = iv1 - iv0 + 1;
         const int count = (vh > 0 && vw > 0) ? vh * vw : 0;
         if (count < min_count) {  // TooSmall (flow.cpp:116-118) depends on the count only
-            if (level == 0) return false;
-            gfx = dmul(gfx, 2.0);
-            gfy = dmul(gfy, 2.0);
+            if (level == 0) return;
+            gx0 = dmul(gx0, 2.0);
+            gy0 = dmul(gy0, 2.0);
+            gx1 = dmul(gx1, 2.0);
+            gy1 = dmul(gy1, 2.0);
             continue;
         }
         ++builds;
-        // ---- template (build_level_patch): lane L <-> extended column L, rows rolled.
-        // Stored: gradients over the valid window (row stride vw); the template
-        // values enter only through T = sum(tval * grad), accumulated here.
+        // ---- template (build_level_patch): lane L <-> extended column L.
+        // Stored: gradients over the valid window; the template values enter
+        // only through T = sum(tval * grad), accumulated here.
         const double fx = dsub(plx, (double)x0), fy = dsub(ply, (double)y0);
         const int xb = x0 - e, yb = y0 - e;  // image origin of the extended patch
         double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
@@ -448,66 +459,113 @@ __device__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double
         {
             const double ht = dmul(0.5, dadd(gxx, gyy)), hd = dmul(0.5, dsub(gxx, gyy));
             const double me = dsub(ht, dsqrt(dadd(dmul(hd, hd), dmul(gxy, gxy))));
-            if (me < dmul(1e-4, (double)count)) return false;  // Unconditioned
+            if (me < dmul(1e-4, (double)count)) return;  // Unconditioned
         }
         const double det = dsub(dmul(gxx, gyy), dmul(gxy, gxy));
-        // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
-        double vx = 0.0, vy = 0.0;
-        bool diverged = false;
         // lanes past the valid window read the zero slot (row step 0)
         const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
         const int gstep = lane < vw ? vw : 0;
         const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
-        int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
-        for (int it = 0; it < cfg.max_iterations; ++it) {
-            const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
-            if (!inside(ci, qx, qy)) {
-                diverged = true;
-                break;
+#pragma unroll 1
+        for (int j = 0; j < nt; ++j) {
+            if (!(j ? al1 : al0)) continue;
+            const int fc = j == 0 ? f0 : f1;
+            const Level ci{P.lvl[level] + (size_t)fc * P.stride[level], P.w[level], P.h[level]};
+            double gfx = j ? gx1 : gx0, gfy = j ? gy1 : gy0;
+            unsigned nit = 0;
+            // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
+            double vx = 0.0, vy = 0.0;
+            bool diverged = false;
+            int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
+            for (int k = 0; k < cfg.max_iterations; ++k) {
+                const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
+                if (!inside(ci, qx, qy)) {
+                    diverged = true;
+                    break;
+                }
+                ++nit;
+                const int qx0 = (int)floor(qx), qy0 = (int)floor(qy);
+                const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
+                const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
+                if (cx < sx0 || cy < sy0 || cx + vw + 1 > sx0 + sw || cy + vh + 1 > sy0 + sh) {
+                    sx0 = cx - SM_MARGIN;
+                    sy0 = cy - SM_MARGIN;
+                    __syncwarp();
+                    soff = stage_block(ci, sx0, sy0, sw, sh, stg);
+                    __syncwarp();
+                }
+                // sum(cur * grad); b = T - that
+                double sx = 0.0, sy = 0.0;
+                row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, gcol, gstep, sx, sy);
+                const double bx = tx - warp_dsum(sx);
+                const double by = ty - warp_dsum(sy);
+                const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
+                const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
+                vx = dadd(vx, dx);
+                vy = dadd(vy, dy);
+                if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
+                    diverged = true;
+                    break;
+                }
+                if (dadd(dmul(dx, dx), dmul(dy, dy)) < eps2) break;
             }
-            ++iters;
-            const int qx0 = (int)floor(qx), qy0 = (int)floor(qy);
-            const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
-            const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
-            if (cx < sx0 || cy < sy0 || cx + vw + 1 > sx0 + sw || cy + vh + 1 > sy0 + sh) {
-                sx0 = cx - SM_MARGIN;
-                sy0 = cy - SM_MARGIN;
-                __syncwarp();
-                soff = stage_block(ci, sx0, sy0, sw, sh, stg);
-                __syncwarp();
+            __syncwarp();
+            if (j) it1 += nit;
+            else it0 += nit;
+            if (diverged && level == 0) {
+                if (j) al1 = false;
+                else al0 = false;
+                continue;
             }
-            // sum(cur * grad); b = T - that
-            double sx = 0.0, sy = 0.0;
-            row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, gcol, gstep, sx, sy);
-            const double bx = tx - warp_dsum(sx);
-            const double by = ty - warp_dsum(sy);
-            const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
-            const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
-            vx = dadd(vx, dx);
-            vy = dadd(vy, dy);
-            if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
-                diverged = true;
-                break;
+            if (!diverged) {
+                gfx = dadd(gfx, vx);
+                gfy = dadd(gfy, vy);
             }
-            if (dadd(dmul(dx, dx), dmul(dy, dy)) < eps2) break;
+            if (level > 0) {
+                gfx = dmul(gfx, 2.0);
+                gfy = dmul(gfy, 2.0);
+            }
+            if (j) {
+                gx1 = gfx;
+                gy1 = gfy;
+            } else {
+                gx0 = gfx;
+                gy0 = gfy;
+            }
         }
-        __syncwarp();
-        if (diverged && level == 0) return false;
-        if (!diverged) {
-            gfx = dadd(gfx, vx);
-            gfy = dadd(gfy, vy);
-        }
-        if (level > 0) {
-            gfx = dmul(gfx, 2.0);
-            gfy = dmul(gfy, 2.0);
+        if (!al0 && !al1) return;
+    }
+    const Level b0{P.lvl[0] + (size_t)f0 * P.stride[0], P.w[0], P.h[0]};
+    if (al0) {
+        const double rx = dadd(px, gx0), ry = dadd(py, gy0);
+        if (inside(b0, rx, ry)) {
+            ok0 = true;
+            o0 = make_double2(rx, ry);
         }
     }
-    const double rx = dadd(px, gfx), ry = dadd(py, gfy);
-    const Level base{P.lvl[0] + (size_t)fcur * P.stride[0], P.w[0], P.h[0]};
-    if (!inside(base, rx, ry)) return false;
-    ox = rx;
-    oy = ry;
-    return true;
+    if (al1) {
+        const Level b1{P.lvl[0] + (size_t)f1 * P.stride[0], P.w[0], P.h[0]};
+        const double rx = dadd(px, gx1), ry = dadd(py, gy1);
+        if (inside(b1, rx, ry)) {
+            ok1 = true;
+            o1 = make_double2(rx, ry);
+        }
+    }
+}
+
+__device__ __forceinline__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
+                                                const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg,
+                                                double& ox, double& oy, unsigned& iters, unsigned& builds) {
+    bool ok0, ok1;
+    double2 o0, o1;
+    unsigned it0 = 0, it1 = 0;
+    track_dual(P, fprev, px, py, fcur, -1, cfg, tg, stg, ok0, ok1, o0, o1, it0, it1, builds);
+    iters += it0;
+    if (ok0) {
+        ox = o0.x;
+        oy = o0.y;
+    }
+    return ok0;
 }
 
 // Persistent warps: each warp pulls (segment, point) work items from a global
@@ -563,6 +621,80 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
                 atomicAdd(s.iter_count + 1, (unsigned long long)builds);
                 atomicAdd(s.iter_count + 2, 1ull);
             }
+        }
+        __syncwarp();
+    }
+}
+
+// Whole tracking chain of one detected point through its segment (all R
+// steps of Tracker::advance, pipeline.cpp / flow.cpp:243-280) in one warp.
+// Step t's backward track (weed_tracks: template in frame t around f_t) and
+// step t+1's forward track (track_lk: the same template, since the kept
+// point f_t is the next step's start) share one template build per level.
+// The forward t+1 result is used only when step t keeps the point, and its
+// iterations are counted only then, so the counters match a step-by-step run.
+__global__ void __launch_bounds__(128, 4) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
+                                                          unsigned* __restrict__ work, int smem_per_warp) {
+    extern __shared__ __align__(16) double lsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* tg = lsm + (size_t)warp * smem_per_warp;
+    const int side = 2 * cfg.window_radius + 1;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * (side * side + 1));
+    const unsigned total = (unsigned)c.nseg * (unsigned)c.max_pts;
+    const size_t plane = (size_t)c.nseg * c.max_pts;
+    const double thr2 = dmul(cfg.fb_threshold, cfg.fb_threshold);
+    while (true) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(work, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= total) break;
+        const int seg = (int)(item / (unsigned)c.max_pts), k = (int)(item % (unsigned)c.max_pts);
+        const int b0 = seg * c.R;  // detection frame of the segment (chunk-relative)
+        if (b0 + 1 >= c.nframes || k >= c.npts[seg]) continue;
+        const size_t slot = (size_t)seg * c.max_pts + k;
+        double2 p = c.pts[slot], f = p;
+        unsigned its = 0, blds = 0, tracks = 0;
+        bool ok0, ok1;
+        double2 o0, o1;
+        // round 0: step 1 forward (template in b0 at p, target b0+1).  Round
+        // t >= 1: template in frame b0+t at f_t; tracker 0 = step t backward
+        // into b0+t-1, tracker 1 = step t+1 forward into b0+t+1 (if any).
+        // One call site keeps the kernel small (instruction cache).
+        int t = 0, ft = b0, f0 = b0 + 1, f1 = -1;
+        double2 q = p;
+        while (true) {
+            unsigned it0 = 0, it1 = 0;
+            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, ok0, ok1, o0, o1, it0, it1, blds);
+            its += it0;
+            if (t == 0) {
+                if (!ok0) break;
+                f = o0;
+            } else {
+                bool keep = ok0;
+                if (keep) {
+                    const double ex = dsub(o0.x, p.x), ey = dsub(o0.y, p.y);
+                    keep = dadd(dmul(ex, ex), dmul(ey, ey)) <= thr2;
+                }
+                if (!keep) break;
+                if (lane == 0) c.alive[(size_t)(t - 1) * plane + slot] = 1;
+                if (f1 < 0) break;
+                its += it1;
+                if (!ok1) break;
+                p = f;
+                f = o1;
+            }
+            ++t;
+            ++tracks;
+            if (lane == 0) c.pos[(size_t)(t - 1) * plane + slot] = f;
+            ft = b0 + t;
+            q = f;
+            f0 = ft - 1;
+            f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
+        }
+        if (lane == 0 && c.iter_count) {
+            atomicAdd(c.iter_count, (unsigned long long)its);
+            atomicAdd(c.iter_count + 1, (unsigned long long)blds);
+            atomicAdd(c.iter_count + 2, (unsigned long long)tracks);
         }
         __syncwarp();
     }
@@ -690,6 +822,25 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     cudaFuncSetAttribute(lk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((s.max_pts + wpc - 1) / wpc, s.nseg);
     lk_kernel<<<grid, wpc * 32, smem, st>>>(s, cfg, wpc, per_warp);
+}
+
+void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
+    if (c.nseg <= 0 || c.max_pts <= 0) return;
+    const int side = 2 * cfg.window_radius + 1;
+    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8;  // doubles
+    const int wpc = 4;
+    const size_t smem = (size_t)wpc * per_warp * sizeof(double);
+    cudaFuncSetAttribute(lk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk_chain_kernel, wpc * 32, smem);
+    cudaMemsetAsync(c.work, 0, sizeof(unsigned), st);
+    cudaMemsetAsync(c.alive, 0, (size_t)c.R * c.nseg * c.max_pts, st);
+    const long long items = (long long)c.nseg * c.max_pts;
+    const long long want = (items + wpc - 1) / wpc;
+    const int grid = (int)std::min<long long>(want, (long long)sms * std::max(per_sm, 1));
+    lk_chain_kernel<<<grid, wpc * 32, smem, st>>>(c, cfg, c.work, per_warp);
 }
 
 void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,

@@ -95,6 +95,20 @@ struct LkStep {
     unsigned* work;       // persistent-warp work counter (zeroed by launch_lk)
 };
 void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
+// Whole-segment tracking chains (r <= 15): every detected point of every
+// segment through all R steps in one launch.  pos/alive are [R][nseg][max_pts]
+// (step t at index t-1): the point after step t and whether step t kept it.
+struct LkChain {
+    DevPyramid pyr;
+    int R, nseg, max_pts, nframes;
+    const double2* pts;  // [nseg][max_pts] detected points (frame seg*R)
+    const int* npts;     // [nseg]
+    double2* pos;
+    uint8_t* alive;      // zeroed by launch_lk_chain
+    unsigned long long* iter_count;
+    unsigned* work;
+};
+void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st);
 // Ordered compaction of kept pairs: TrackSet of frame (frame0 + s*R + t) and
 // the next points of each segment.
 void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,

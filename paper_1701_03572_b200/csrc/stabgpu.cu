@@ -14,6 +14,7 @@
 //   R x { K5 LK forward+backward (all segments)  ->  ordered compaction }
 //   K6 fit (+RANSAC) of every frame pair
 // then K7 scan + smoothing and K8 compose over the sequence.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -269,7 +270,45 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(unsigned long long, iters, "lk_iters", 3);
     DBUF(unsigned, lk_work, "lk_work", 1);
     CUDA_TRY(cudaMemsetAsync(iters, 0, 3 * sizeof(unsigned long long), st));
-    {
+    if (cfg.flow.window_radius <= 15) {
+        // whole-segment chains in one launch, then one ordered compaction per step
+        Timer tm(ctx, 2);
+        const int steps = std::min(R, count);
+        DBUF(double2, pos, "lk_pos", (size_t)steps * nseg * maxc);
+        DBUF(uint8_t, alive, "lk_alive", (size_t)steps * nseg * maxc);
+        LkChain c;
+        c.pyr = P;
+        c.R = R;
+        c.nseg = nseg;
+        c.max_pts = maxc;
+        c.nframes = nF;
+        c.pts = ptsA;
+        c.npts = nA;
+        c.pos = pos;
+        c.alive = alive;
+        c.iter_count = iters;
+        c.work = lk_work;
+        launch_lk_chain(c, cfg.flow, st);
+        ++ctx->stats.launches;
+        const size_t plane = (size_t)nseg * maxc;
+        for (int t = 1; t <= steps; ++t) {
+            LkStep s;
+            std::memset(&s, 0, sizeof s);
+            s.frame0 = 0;
+            s.seg_len = R;
+            s.t = t;
+            s.nseg = nseg;
+            s.max_pts = maxc;
+            s.pts = t == 1 ? ptsA : pos + (size_t)(t - 2) * plane;
+            s.npts = nA;
+            s.fwd = pos + (size_t)(t - 1) * plane;
+            s.keep = alive + (size_t)(t - 1) * plane;
+            s.nframes = nF;
+            launch_compact(s, ptsB, nB, trk_prev, trk_cur, trk_n, 1, st);
+            ++ctx->stats.launches;
+        }
+        TRY(check_launch("lk"));
+    } else {
         Timer tm(ctx, 2);
         double2* cur_pts = ptsA;
         double2* nxt_pts = ptsB;
