@@ -199,6 +199,13 @@ __device__ bool track_warp(const DevPyramid& P, int fprev, int fcur, double px, 
 // of fp64 ops instead of four clamped 64-bit gathers.  Rounding differs from
 // the reference's weighted form by ~1e-13 (tolerance-level, like the sums).
 
+// horizontal lerp a + f*(b - a) of two bytes: b - a is taken exactly between
+// the 2^52-magic doubles (one DADD saved), a = magic - 2^52 exactly
+__device__ __forceinline__ double hlerp(uint32_t a, uint32_t b, double f) {
+    const double ma = __hiloint2double(0x43300000, (int)a), mb = __hiloint2double(0x43300000, (int)b);
+    return fma(f, mb - ma, ma - 4503599627370496.0);
+}
+
 __device__ __forceinline__ double u2d(uint32_t b) {  // exact u8 -> double, no I2F
     return __hiloint2double(0x43300000, (int)b) - 4503599627370496.0;
 }
@@ -297,8 +304,7 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
     src += lane;
     double hp;
     {
-        const double a = u2d(src[0]);
-        hp = fma(cfx, u2d(src[1]) - a, a);
+        hp = hlerp(src[0], src[1], cfx);
     }
     // two partial sums per component (even / odd rows) halve the dependent
     // DFMA chain; combined once at the end
@@ -306,9 +312,8 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
     int k = 1;
 #pragma unroll 2
     for (; k + 1 <= vh; k += 2) {
-        const double a0 = u2d(src[SM_PITCH]), a1 = u2d(src[2 * SM_PITCH]);
-        const double h0 = fma(cfx, u2d(src[SM_PITCH + 1]) - a0, a0);
-        const double h1 = fma(cfx, u2d(src[2 * SM_PITCH + 1]) - a1, a1);
+        const double h0 = hlerp(src[SM_PITCH], src[SM_PITCH + 1], cfx);
+        const double h1 = hlerp(src[2 * SM_PITCH], src[2 * SM_PITCH + 1], cfx);
         const double c0 = fma(cfy, h0 - hp, hp), c1 = fma(cfy, h1 - h0, h0);
         const double2 g0 = g[0], g1 = g[gstep];
         sx = fma(c0, g0.x, sx);
@@ -320,8 +325,7 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
         hp = h1;
     }
     if (k <= vh) {
-        const double a = u2d(src[SM_PITCH]);
-        const double h = fma(cfx, u2d(src[SM_PITCH + 1]) - a, a);
+        const double h = hlerp(src[SM_PITCH], src[SM_PITCH + 1], cfx);
         const double c = fma(cfy, h - hp, hp);
         const double2 gg = g[0];
         sx = fma(c, gg.x, sx);
@@ -353,11 +357,9 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
     for (int k = 0; k <= es; ++k, src += SM_PITCH) {  // image rows yb .. yb+es
         double hx = 0.0;
         if (XTRA) {  // lane 31 also carries extended column 32 (from image columns 32, 33)
-            const double a = u2d(src[1]);
-            hx = fma(fx, u2d(src[2]) - a, a);
+            hx = hlerp(src[1], src[2], fx);
         }
-        const double a = u2d(src[0]);
-        const double h = fma(fx, u2d(src[1]) - a, a);
+        const double h = hlerp(src[0], src[1], fx);
         if (k >= 1) {
             const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
             double evx = 0.0;
