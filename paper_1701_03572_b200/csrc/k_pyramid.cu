@@ -83,17 +83,113 @@ __global__ void __launch_bounds__(256) pyramid_level_kernel(const uint8_t* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-streaming variant (rows 8-byte aligned, w % 8 == 0).  A thread owns
+// 4 adjacent output columns (8 input columns) and walks a band of output rows
+// top to bottom.  Each input row is read once: 8 bytes per thread, the halo
+// words from the neighbour lanes.  The horizontal filter runs on packed
+// 16-bit pairs (two outputs per register: sums stay below 2^16 — horizontal
+// <= 16*255, vertical <= 256*255), the last five filtered rows stay in
+// registers, and (acc + 128) >> 8 is byte 1 of each 16-bit lane.
+constexpr int SPT = 128;   // threads per CTA: 512 output columns
+constexpr int SBAND = 32;  // output rows per CTA
+
+__device__ __forceinline__ uint32_t ev(uint32_t wd) { return wd & 0x00FF00FFu; }  // (b0, b2)
+__device__ __forceinline__ uint32_t od(uint32_t wd) { return (wd >> 8) & 0x00FF00FFu; }  // (b1, b3)
+__device__ __forceinline__ uint32_t fun16(uint32_t lo, uint32_t hi) { return __funnelshift_r(lo, hi, 16); }
+
+// one input row: words L (cols -4..-1), X (0..3), Y (4..7), R (8..11) ->
+// packed horizontal sums of outputs (0, 1) and (2, 3) (input cols 0, 2, 4, 6)
+__device__ __forceinline__ void hrow(uint32_t L, uint32_t X, uint32_t Y, uint32_t R, uint32_t& a, uint32_t& b) {
+    const uint32_t eL = ev(L), oL = od(L), eX = ev(X), oX = od(X), eY = ev(Y), oY = od(Y), eR = ev(R);
+    const uint32_t m2a = fun16(eL, eX), m1a = fun16(oL, oX), p2a = fun16(eX, eY);  // (-2,0) (-1,1) (2,4)
+    const uint32_t m1b = fun16(oX, oY), p2b = fun16(eY, eR);                        // (3,5) (6,8)
+    a = (m2a + p2a) + 4u * (m1a + oX) + 6u * eX;
+    b = (p2a + p2b) + 4u * (m1b + oY) + 6u * eY;
+}
+
+__device__ __forceinline__ void srow(const uint8_t* __restrict__ f, int w, int h, int y, int t, int lane, bool act,
+                                     bool left_edge, bool right_edge, uint32_t& a, uint32_t& b) {
+    y = min(max(y, 0), h - 1);
+    const uint8_t* rp = f + (size_t)y * w + 8 * t;
+    uint2 xy = make_uint2(0u, 0u);
+    if (act) xy = __ldg(reinterpret_cast<const uint2*>(rp));
+    uint32_t L = __shfl_up_sync(0xFFFFFFFFu, xy.y, 1);
+    uint32_t R = __shfl_down_sync(0xFFFFFFFFu, xy.x, 1);
+    if (lane == 0 && !left_edge && act) L = __ldg(reinterpret_cast<const uint32_t*>(rp - 4));
+    if (lane == 31 && !right_edge && act) R = __ldg(reinterpret_cast<const uint32_t*>(rp + 8));
+    if (left_edge) L = (xy.x & 0xFFu) * 0x01010101u;  // clamp: col 0
+    if (right_edge) R = (xy.y >> 24) * 0x01010101u;    // clamp: col w-1 (= 8t+7)
+    hrow(L, xy.x, xy.y, R, a, b);
+}
+
+__global__ void __launch_bounds__(SPT) pyramid_stream_kernel(const uint8_t* __restrict__ src, size_t src_stride,
+                                                              int w, int h, uint8_t* __restrict__ dst,
+                                                              size_t dst_stride) {
+    const int ow = w / 2, oh = h / 2;
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * SPT + threadIdx.x;  // output columns 4t .. 4t+3
+    const int oy0 = blockIdx.y * SBAND, oy1 = min(oy0 + SBAND, oh);
+    const uint8_t* f = src + (size_t)blockIdx.z * src_stride;
+    uint8_t* d = dst + (size_t)blockIdx.z * dst_stride;
+    const bool act = 8 * t < w;
+    const bool left_edge = t == 0, right_edge = 8 * t + 8 >= w;
+#define ROW(Y, A, B) srow(f, w, h, (Y), t, lane, act, left_edge, right_edge, A, B)
+    uint32_t a0, a1, a2, a3, a4, b0, b1, b2, b3, b4;  // filtered rows 2oy-2 .. 2oy+2
+    ROW(2 * oy0 - 2, a0, b0);
+    ROW(2 * oy0 - 1, a1, b1);
+    ROW(2 * oy0, a2, b2);
+    ROW(2 * oy0 + 1, a3, b3);
+    ROW(2 * oy0 + 2, a4, b4);
+    const bool vec = act && 4 * t + 3 < ow;
+    for (int oy = oy0; oy < oy1; ++oy) {
+        const uint32_t va = (a0 + a4) + 4u * (a1 + a3) + 6u * a2 + 0x00800080u;
+        const uint32_t vb = (b0 + b4) + 4u * (b1 + b3) + 6u * b2 + 0x00800080u;
+        const uint32_t o = __byte_perm(va, vb, 0x7531);  // byte 1 of each 16-bit lane
+        uint8_t* op = d + (size_t)oy * ow + 4 * t;
+        if (vec) {
+            *reinterpret_cast<uint32_t*>(op) = o;
+        } else if (act) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (4 * t + k < ow) op[k] = (uint8_t)(o >> (8 * k));
+        }
+        if (oy + 1 < oy1) {
+            a0 = a2;
+            b0 = b2;
+            a1 = a3;
+            b1 = b3;
+            a2 = a4;
+            b2 = b4;
+            ROW(2 * oy + 3, a3, b3);
+            ROW(2 * oy + 4, a4, b4);
+        }
+    }
+}
+#undef ROW
+
 }  // namespace
 
 void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst,
                           size_t dst_stride, int frames, cudaStream_t st) {
     const int ow = w / 2, oh = h / 2;
     if (frames <= 0 || ow <= 0 || oh <= 0) return;
+    // streaming kernel: 8-byte aligned rows and frames, 4-byte aligned output rows
+    const bool stream = (w % 8) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 8) == 0 &&
+                        (src_stride % 8) == 0 && (reinterpret_cast<uintptr_t>(dst) % 4) == 0 &&
+                        (dst_stride % 4) == 0;
     for (int f0 = 0; f0 < frames; f0 += 65535) {
         const int nf = min(65535, frames - f0);
-        dim3 grid((ow + TW - 1) / TW, (oh + TH - 1) / TH, nf);
-        pyramid_level_kernel<<<grid, 256, 0, st>>>(src + (size_t)f0 * src_stride, src_stride, w, h,
-                                                   dst + (size_t)f0 * dst_stride, dst_stride);
+        if (stream) {
+            const int threads = (w / 8 + 31) / 32 * 32;
+            dim3 grid((threads + SPT - 1) / SPT, (oh + SBAND - 1) / SBAND, nf);
+            pyramid_stream_kernel<<<grid, SPT, 0, st>>>(src + (size_t)f0 * src_stride, src_stride, w, h,
+                                                        dst + (size_t)f0 * dst_stride, dst_stride);
+        } else {
+            dim3 grid((ow + TW - 1) / TW, (oh + TH - 1) / TH, nf);
+            pyramid_level_kernel<<<grid, 256, 0, st>>>(src + (size_t)f0 * src_stride, src_stride, w, h,
+                                                       dst + (size_t)f0 * dst_stride, dst_stride);
+        }
     }
 }
 

@@ -27,9 +27,17 @@ def orc():
 
 FRAMES = [(_data.noise_frame(97, 61, 1), "noise97x61"), (_data.noise_frame(160, 120, 2), "noise160"),
           (np.full((40, 50), 77, np.uint8), "flat"), (_data.video(frames=2)[0][1], "video")]
+# extremes of the packed 16-bit pyramid lanes (all-255, 0/255 checkerboard),
+# the benchmark frame size, and a width that is a multiple of 8 but not of 16
+PYR_FRAMES = FRAMES + [
+    (np.full((64, 128), 255, np.uint8), "sat255"),
+    (((np.indices((96, 176)).sum(axis=0) % 2) * 255).astype(np.uint8), "checker"),
+    (_data.noise_frame(1920, 1080, 3), "noise1080p"),
+    (_data.noise_frame(200, 72, 4), "noise200x72"),
+]
 
 
-@pytest.mark.parametrize("f,name", FRAMES)
+@pytest.mark.parametrize("f,name", PYR_FRAMES)
 @pytest.mark.parametrize("levels", [1, 3, 6])
 def test_pyramid_bitexact(orc, f, name, levels):
     g = stab.build_pyramid(f, levels)
