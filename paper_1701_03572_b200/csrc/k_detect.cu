@@ -26,6 +26,7 @@
 //     sequential rank-order rule exactly, including the early stop at
 //     max_corners.  A bucket holding more than 4096 candidates (large ties)
 //     is merge-sorted in global memory first.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -151,6 +152,157 @@ __global__ void __launch_bounds__(256) cand_kernel(PlaneBatch fr, stabgpu_roi ro
             cand_idx[pos] = (unsigned)((Y0 + ty) * fr.w + X0 + tx);
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming response (block_size 3): a warp owns 30 output columns (lanes
+// 1..30; lanes 0 and 31 carry the box halo) and walks a band of rows.  Image
+// values roll through registers (row r-1, r, r+1), horizontal neighbours come
+// by shuffle, integer products are box-summed horizontally by shuffle and
+// vertically over the last three rows.  min_eig is first evaluated in fp32
+// with a rigorous bound |r32 - r| <= 2^-22 * half_trace (inputs are exact in
+// fp32); only pixels the bound cannot decide take the exact
+// fp64 reference arithmetic (min_eig_q).
+constexpr int SW_COLS = 30;  // output columns per warp
+constexpr int SW_BAND = 64;  // output rows per CTA
+constexpr float SW_EPS = 1.9073486328125e-06f;  // 2^-19: 8x the proven bound
+
+__device__ __forceinline__ unsigned resp_bin(float r) { return min(__float_as_uint(r) >> 20, (unsigned)kRespBins - 1); }
+
+// MODE 0: exact per-frame max (bits) + histogram of fp32 responses.
+// MODE 1: candidates r >= lo[d] (or the threshold itself when redo) with r > 0.
+template <int MODE>
+__global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu_roi roi, double quality,
+                                                          DetectScratch s, int redo) {
+    __shared__ unsigned sh[MODE == 0 ? kRespBins : 1];
+    const int d = blockIdx.z;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double lo = 0.0;
+    float lo32 = 0.0f;
+    if (MODE == 1) {
+        if (redo && !(s.flags[d] & 2)) return;
+        const unsigned long long mb = s.maxbits[d];
+        if (mb == 0) return;  // max_response <= 0: no corners (features.cpp:103-105)
+        lo = redo ? dmul(quality, __longlong_as_double((long long)mb)) : s.lo[d];
+        lo32 = __double2float_rd(lo);
+    } else {
+        for (int i = threadIdx.x; i < kRespBins; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+    }
+    const uint8_t* f = fr.base + (size_t)d * fr.stride;
+    const int w = fr.w, h = fr.h;
+    const int x = roi.x0 + (blockIdx.x * 8 + warp) * SW_COLS - 1 + lane;
+    const bool out_col = lane >= 1 && lane <= SW_COLS && x < roi.x1;
+    const bool in_x = x >= 0 && x < w;
+    const int xc = clampi(x, 0, w - 1), xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
+    const int Y0 = roi.y0 + blockIdx.y * SW_BAND, Y1 = min(Y0 + SW_BAND, roi.y1);
+    auto ld = [&](int xx, int r) -> int { return __ldg(f + (size_t)clampi(r, 0, h - 1) * w + xx); };
+    int Im = ld(xc, Y0 - 2), I0 = ld(xc, Y0 - 1);
+    int axx = 0, axy = 0, ayy = 0, bxx = 0, bxy = 0, byy = 0;  // box rows r-2, r-1
+    unsigned long long best = 0;
+    float best_low = -1.0f;
+    for (int r = Y0 - 1; r <= Y1; ++r) {
+        const int Ip = ld(xc, r + 1);
+        int L = __shfl_up_sync(0xFFFFFFFFu, I0, 1), R = __shfl_down_sync(0xFFFFFFFFu, I0, 1);
+        if (lane == 0) L = ld(xl, r);
+        if (lane == 31) R = ld(xr, r);
+        if (x <= 0) L = I0;      // gradients clamp at the frame edge (image_ops.cpp:79-96)
+        if (x >= w - 1) R = I0;
+        const bool inr = in_x && r >= 0 && r < h;  // products outside the frame are zero
+        const int gx = inr ? R - L : 0, gy = inr ? Ip - Im : 0;
+        int pxx = gx * gx, pxy = gx * gy, pyy = gy * gy;
+        pxx += __shfl_up_sync(0xFFFFFFFFu, pxx, 1) + __shfl_down_sync(0xFFFFFFFFu, pxx, 1);
+        pxy += __shfl_up_sync(0xFFFFFFFFu, pxy, 1) + __shfl_down_sync(0xFFFFFFFFu, pxy, 1);
+        pyy += __shfl_up_sync(0xFFFFFFFFu, pyy, 1) + __shfl_down_sync(0xFFFFFFFFu, pyy, 1);
+        const int y = r - 1;  // output row whose window is rows r-2 .. r
+        bool keep = false;
+        unsigned long long key = 0;
+        if (y >= Y0 && out_col) {
+            const int sxx = axx + bxx + pxx, sxy = axy + bxy + pxy, syy = ayy + byy + pyy;
+            const float fxx = (float)sxx * 0.25f, fxy = (float)sxy * 0.25f, fyy = (float)syy * 0.25f;
+            const float ht = 0.5f * (fxx + fyy), hd = 0.5f * (fxx - fyy);
+            const float r32 = ht - __fsqrt_rn(hd * hd + fxy * fxy);
+            const float e = ht * SW_EPS + 1e-30f;
+            if (MODE == 0) {
+                if (r32 > 0.0f) atomicAdd(&sh[resp_bin(r32)], 1u);
+                if (r32 + e >= best_low && r32 + e > 0.0f) {
+                    const double rr = min_eig_q(sxx, sxy, syy);
+                    if (rr > 0.0) best = max(best, dbits(rr));
+                }
+                best_low = fmaxf(best_low, r32 - e);
+            } else if (r32 + e >= lo32) {
+                const double rr = min_eig_q(sxx, sxy, syy);
+                keep = rr >= lo && rr > 0.0;
+                key = dbits(rr);
+            }
+        }
+        if (MODE == 1) {
+            const unsigned ball = __ballot_sync(0xFFFFFFFFu, keep);
+            if (ball) {
+                unsigned base = 0;
+                if (lane == __ffs(ball) - 1) base = atomicAdd(&s.count[d], (unsigned)__popc(ball));
+                base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ball) - 1);
+                if (keep) {
+                    const size_t pos = (size_t)d * s.cap + base + __popc(ball & ((1u << lane) - 1));
+                    s.cand_key[pos] = key;
+                    s.cand_idx[pos] = (unsigned)(y * w + x);
+                }
+            }
+        }
+        axx = bxx;
+        axy = bxy;
+        ayy = byy;
+        bxx = pxx;
+        bxy = pxy;
+        byy = pyy;
+        Im = I0;
+        I0 = Ip;
+    }
+    if (MODE == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+        if (lane == 0 && best) atomicMax(&s.maxbits[d], best);
+        __syncthreads();
+        for (int i = threadIdx.x; i < kRespBins; i += blockDim.x)
+            if (sh[i]) atomicAdd(&s.hist[(size_t)d * kRespBins + i], sh[i]);
+    }
+}
+
+// Per frame: candidate cut lo >= quality * max such that about `keep`
+// candidates lie above it (from the fp32 histogram; any lo >= the threshold is
+// exact because the kept set is then a prefix of the reference's sorted
+// candidate list, and select falls back to the full list when the prefix runs
+// out before max_corners).
+__global__ void resp_cut_kernel(double quality, DetectScratch s, unsigned keep) {
+    const int d = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    const unsigned long long mb = s.maxbits[d];
+    unsigned char fl = 0;
+    double lo = 0.0;
+    if (mb != 0) {
+        const double thr = dmul(quality, __longlong_as_double((long long)mb));
+        lo = thr;
+        unsigned cum = 0;
+        const unsigned* hs = s.hist + (size_t)d * kRespBins;
+        for (int b = kRespBins - 1; b > 0; --b) {
+            cum += hs[b];
+            if (cum >= keep) {
+                const double edge = (double)__uint_as_float((unsigned)b << 20);
+                if (edge > thr) {
+                    lo = edge;
+                    fl = 1;
+                }
+                break;
+            }
+        }
+    }
+    s.lo[d] = lo;
+    s.flags[d] = fl;
+}
+
+__global__ void resp_redo_reset_kernel(DetectScratch s) {
+    const int d = blockIdx.x;
+    if (threadIdx.x == 0 && (s.flags[d] & 2)) s.count[d] = 0;
 }
 
 // Generic block size (any odd >= 3): direct evaluation from global memory.
@@ -337,8 +489,9 @@ __device__ void global_merge_sort(unsigned long long* key, unsigned* idx, unsign
 __global__ void __launch_bounds__(SEL_THREADS, 1)
     select_kernel(stabgpu_detect_cfg cfg, stabgpu_roi roi, int w, DetectScratch s,
                   double2* __restrict__ out_xy, double* __restrict__ out_score,
-                  int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext) {
+                  int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext, int redo) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (redo && !(s.flags ? (s.flags[blockIdx.x] & 2) : 0)) return;
     SelShared& S = *reinterpret_cast<SelShared*>(smem);
     unsigned char* p = smem + ((sizeof(SelShared) + 15) & ~size_t(15));
     unsigned long long* ckey = reinterpret_cast<unsigned long long*>(p);
@@ -364,7 +517,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     const unsigned n = s.count[d];
     const unsigned long long mb = s.maxbits[d];
     if (n == 0 || mb == 0) {
-        if (tid == 0) out_n[d] = 0;
+        if (tid == 0) {
+            out_n[d] = 0;
+            // a cut list came out empty although the threshold list is not: redo
+            if (!redo && s.flags && (s.flags[d] & 1) && mb != 0) s.flags[d] |= 2;
+        }
         return;
     }
     const unsigned maxf = __float_as_uint(__double2float_rn(__longlong_as_double((long long)mb)));
@@ -549,7 +706,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
         if (tid == 0) S.b0 = S.b1;
         __syncthreads();
     }
-    if (tid == 0) out_n[d] = S.naccepted;
+    if (tid == 0) {
+        out_n[d] = S.naccepted;
+        // the cut prefix ran out before max_corners: redo from the full list
+        if (!redo && s.flags && (s.flags[d] & 1) && S.naccepted < maxc) s.flags[d] |= 2;
+    }
 }
 
 __global__ void gradients_kernel(const uint8_t* __restrict__ f, int w, int h, double* __restrict__ gx,
@@ -579,7 +740,15 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     cudaMemsetAsync(s.count, 0, sizeof(unsigned) * nD, st);
     const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
     const int half = cfg.block_size / 2;
-    if (half == 1) {
+    const bool fast = half == 1 && s.hist && s.lo && s.flags;
+    if (fast) {
+        cudaMemsetAsync(s.hist, 0, sizeof(unsigned) * kRespBins * (size_t)nD, st);
+        dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
+        resp_stream_kernel<0><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 0);
+        const unsigned keep = (unsigned)std::max(4096, 16 * cfg.max_corners);
+        resp_cut_kernel<<<nD, 32, 0, st>>>(cfg.quality_level, s, keep);
+        resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 0);
+    } else if (half == 1) {
         dim3 grid((rw + RTW - 1) / RTW, (rh + RTH - 1) / RTH, nD);
         resp_max_kernel<1><<<grid, 256, 0, st>>>(fr, roi, s.maxbits);
         cand_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s.maxbits, s.count,
@@ -605,8 +774,17 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
         cudaMallocAsync((void**)&g_axy, sizeof(short2) * (size_t)nD * cfg.max_corners, st);
         cudaMallocAsync((void**)&g_anext, sizeof(int) * (size_t)nD * cfg.max_corners, st);
     }
-    select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy,
-                                                 g_anext);
+    DetectScratch sf = s;
+    if (!fast) sf.flags = nullptr;
+    select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy,
+                                                 g_anext, 0);
+    if (fast) {  // frames whose cut prefix ran out: full candidate list (usually none)
+        resp_redo_reset_kernel<<<nD, 32, 0, st>>>(s);
+        dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
+        resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 1);
+        select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy,
+                                                     g_anext, 1);
+    }
     if (g_axy) {
         cudaFreeAsync(g_axy, st);
         cudaFreeAsync(g_anext, st);

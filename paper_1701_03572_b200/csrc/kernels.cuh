@@ -58,13 +58,16 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
 struct DetectScratch {
     unsigned long long* maxbits;  // [nD]
     unsigned int* count;          // [nD]
-    unsigned int* hist;           // [nD][kBuckets]
+    unsigned int* hist;           // [nD][kRespBins] response histogram (fast path), or null
     unsigned long long* cand_key; // [nD][cap]   score bits
     unsigned int* cand_idx;       // [nD][cap]   y*w + x
     unsigned long long* sort_key; // [nD][cap]
     unsigned int* sort_idx;       // [nD][cap]
     size_t cap;                   // candidates per detection frame (ROI area)
+    double* lo;                   // [nD] candidate cut (>= quality * max), fast path
+    unsigned char* flags;         // [nD] bit 0: cut above the threshold, bit 1: redo
 };
+constexpr int kRespBins = 2048;
 constexpr int kBuckets = 8192;
 constexpr int kBucketShift = 13;
 size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int roi_w, int roi_h);

@@ -241,14 +241,19 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(unsigned int, cidx, "det_cidx", cap * nseg);
     DBUF(unsigned long long, skey, "det_skey", cap * nseg);
     DBUF(unsigned int, sidx, "det_sidx", cap * nseg);
+    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins * nseg);
+    DBUF(double, dlo, "det_lo", nseg);
+    DBUF(unsigned char, dflags, "det_flags", nseg);
     ds.maxbits = maxbits;
     ds.count = dcount;
-    ds.hist = nullptr;
+    ds.hist = dhist;
     ds.cand_key = ckey;
     ds.cand_idx = cidx;
     ds.sort_key = skey;
     ds.sort_idx = sidx;
     ds.cap = cap;
+    ds.lo = dlo;
+    ds.flags = dflags;
     DBUF(double2, ptsA, "seg_ptsA", (size_t)nseg * maxc);
     DBUF(double2, ptsB, "seg_ptsB", (size_t)nseg * maxc);
     DBUF(int, nA, "seg_nA", nseg);
@@ -611,7 +616,10 @@ int stabgpu_detect_corners(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
     DBUF(double, sc, "api_score", maxc);
     DBUF(int, nn, "api_n", 1);
     CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
-    DetectScratch ds{maxbits, dcount, nullptr, ckey, cidx, skey, sidx, cap};
+    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins);
+    DBUF(double, dlo, "det_lo", 1);
+    DBUF(unsigned char, dflags, "det_flags", 1);
+    DetectScratch ds{maxbits, dcount, dhist, ckey, cidx, skey, sidx, cap, dlo, dflags};
     PlaneBatch fb{d, n, w, h};
     launch_detect(fb, 1, *cfg, roi, ds, pts, sc, nn, st);
     ctx->stats.launches += 3;
