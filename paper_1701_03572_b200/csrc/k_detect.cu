@@ -165,9 +165,39 @@ __global__ void __launch_bounds__(256) cand_kernel(PlaneBatch fr, stabgpu_roi ro
 // fp64 reference arithmetic (min_eig_q).
 constexpr int SW_COLS = 30;  // output columns per warp
 constexpr int SW_BAND = 64;  // output rows per CTA
-constexpr float SW_EPS = 1.9073486328125e-06f;  // 2^-19: 8x the proven bound
+constexpr float SW_EPS = 7.62939453125e-06f;  // 2^-17: >= 8x the bound with sqrt.approx (rel. err. <= 2^-21)
 
 __device__ __forceinline__ unsigned resp_bin(float r) { return min(__float_as_uint(r) >> 20, (unsigned)kRespBins - 1); }
+
+__device__ __forceinline__ float sqrt_approx(float v) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+// The CTA's band (rows Y0-2 .. Y1+1, 256 columns from a 16-byte aligned xb)
+// is staged in shared memory first — 16-byte loads for interior blocks, byte
+// loads with the reference's clamped indices at the frame edges — so the row
+// loop only reads shared memory; staged values outside the frame are the
+// clamped pixels, which is exactly what the gradient clamps read.
+constexpr int SB_W = 272;                 // staged columns (>= 15 + 8 * 30 + 2 + 1)
+constexpr int SB_H = SW_BAND + 4;         // staged rows
+
+// Appends a warp's buffered candidates to the frame's list (one atomic).
+__device__ __forceinline__ int flush_cands(DetectScratch& s, int d, const unsigned long long* key,
+                                           const unsigned* idx, int n) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&s.count[d], (unsigned)n);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int k = lane; k < n; k += 32) {
+        s.cand_key[(size_t)d * s.cap + base + k] = key[k];
+        s.cand_idx[(size_t)d * s.cap + base + k] = idx[k];
+    }
+    __syncwarp();
+    return 0;
+}
 
 // MODE 0: exact per-frame max (bits) + histogram of fp32 responses.
 // MODE 1: candidates r >= lo[d] (or the threshold itself when redo) with r > 0.
@@ -175,39 +205,59 @@ template <int MODE>
 __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu_roi roi, double quality,
                                                           DetectScratch s, int redo) {
     __shared__ unsigned sh[MODE == 0 ? kRespBins : 1];
+    __shared__ __align__(16) uint8_t band[SB_H][SB_W];
+    constexpr int WB = MODE == 1 ? 128 : 1;  // per-warp candidate buffer (flushed with one atomic)
+    __shared__ unsigned long long wkey[8][WB];
+    __shared__ unsigned widx[8][WB];
     const int d = blockIdx.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double lo = 0.0;
-    float lo32 = 0.0f;
     if (MODE == 1) {
         if (redo && !(s.flags[d] & 2)) return;
         const unsigned long long mb = s.maxbits[d];
         if (mb == 0) return;  // max_response <= 0: no corners (features.cpp:103-105)
         lo = redo ? dmul(quality, __longlong_as_double((long long)mb)) : s.lo[d];
-        lo32 = __double2float_rd(lo);
     } else {
         for (int i = threadIdx.x; i < kRespBins; i += blockDim.x) sh[i] = 0;
-        __syncthreads();
     }
+    const float lo32 = __double2float_rd(lo);
     const uint8_t* f = fr.base + (size_t)d * fr.stride;
     const int w = fr.w, h = fr.h;
-    const int x = roi.x0 + (blockIdx.x * 8 + warp) * SW_COLS - 1 + lane;
+    const int Y0 = roi.y0 + blockIdx.y * SW_BAND, Y1 = min(Y0 + SW_BAND, roi.y1);
+    const int xs = roi.x0 + blockIdx.x * 8 * SW_COLS - 1;  // first column the CTA touches
+    const int xb = xs & ~15;
+    const int rows = (Y1 + 1) - (Y0 - 2) + 1;
+    // ---- stage the band
+    const bool inner = xb >= 0 && xb + SB_W <= w && Y0 - 2 >= 0 && Y1 + 1 <= h - 1 && (w & 15) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(f) & 15) == 0);
+    if (inner) {
+        for (int i = threadIdx.x; i < rows * (SB_W / 16); i += blockDim.x) {
+            const int r = i / (SB_W / 16), c = i - r * (SB_W / 16);
+            *reinterpret_cast<uint4*>(&band[r][16 * c]) =
+                __ldg(reinterpret_cast<const uint4*>(f + (size_t)(Y0 - 2 + r) * w + xb) + c);
+        }
+    } else {
+        for (int i = threadIdx.x; i < rows * SB_W; i += blockDim.x) {
+            const int r = i / SB_W, c = i - r * SB_W;
+            band[r][c] = __ldg(f + (size_t)clampi(Y0 - 2 + r, 0, h - 1) * w + clampi(xb + c, 0, w - 1));
+        }
+    }
+    __syncthreads();
+    // ---- rows
+    const int x = xs + warp * SW_COLS + lane;  // lanes 0 and 31 carry the box halo
+    const int c = x - xb;                      // 0 .. 256 (c + 1 <= 257 < SB_W)
     const bool out_col = lane >= 1 && lane <= SW_COLS && x < roi.x1;
     const bool in_x = x >= 0 && x < w;
-    const int xc = clampi(x, 0, w - 1), xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
-    const int Y0 = roi.y0 + blockIdx.y * SW_BAND, Y1 = min(Y0 + SW_BAND, roi.y1);
-    auto ld = [&](int xx, int r) -> int { return __ldg(f + (size_t)clampi(r, 0, h - 1) * w + xx); };
-    int Im = ld(xc, Y0 - 2), I0 = ld(xc, Y0 - 1);
+    const uint8_t* bp = &band[0][0] + c;       // band row k at bp + k * SB_W
+    int Im = bp[0], I0 = bp[SB_W];             // rows Y0-2, Y0-1
     int axx = 0, axy = 0, ayy = 0, bxx = 0, bxy = 0, byy = 0;  // box rows r-2, r-1
     unsigned long long best = 0;
     float best_low = -1.0f;
-    for (int r = Y0 - 1; r <= Y1; ++r) {
-        const int Ip = ld(xc, r + 1);
-        int L = __shfl_up_sync(0xFFFFFFFFu, I0, 1), R = __shfl_down_sync(0xFFFFFFFFu, I0, 1);
-        if (lane == 0) L = ld(xl, r);
-        if (lane == 31) R = ld(xr, r);
-        if (x <= 0) L = I0;      // gradients clamp at the frame edge (image_ops.cpp:79-96)
-        if (x >= w - 1) R = I0;
+    int qn = 0;                     // MODE 1: warp buffer fill (warp-uniform)
+    const uint8_t* rp = bp + SB_W;  // row r
+#pragma unroll 2
+    for (int r = Y0 - 1; r <= Y1; ++r, rp += SB_W) {
+        const int L = rp[-1], R = rp[1], Ip = rp[SB_W];
         const bool inr = in_x && r >= 0 && r < h;  // products outside the frame are zero
         const int gx = inr ? R - L : 0, gy = inr ? Ip - Im : 0;
         int pxx = gx * gx, pxy = gx * gy, pyy = gy * gy;
@@ -219,12 +269,17 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         unsigned long long key = 0;
         if (y >= Y0 && out_col) {
             const int sxx = axx + bxx + pxx, sxy = axy + bxy + pxy, syy = ayy + byy + pyy;
-            const float fxx = (float)sxx * 0.25f, fxy = (float)sxy * 0.25f, fyy = (float)syy * 0.25f;
+            const float fxx = (float)sxx, fxy = (float)sxy, fyy = (float)syy;  // exact (< 2^24)
+            // 4 * (half trace, half difference): the quarter scaling is folded in
             const float ht = 0.5f * (fxx + fyy), hd = 0.5f * (fxx - fyy);
-            const float r32 = ht - __fsqrt_rn(hd * hd + fxy * fxy);
+            const float r32 = 0.25f * (ht - sqrt_approx(fmaf(hd, hd, fxy * fxy)));
             const float e = ht * SW_EPS + 1e-30f;
             if (MODE == 0) {
-                if (r32 > 0.0f) atomicAdd(&sh[resp_bin(r32)], 1u);
+                if ((y & 3) == 0 && r32 > 0.0f) {  // histogram steers the cut only: every 4th row, x4
+                    const unsigned bin = resp_bin(r32);
+                    const unsigned peers = __match_any_sync(__activemask(), bin);
+                    if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], 4u * __popc(peers));
+                }
                 if (r32 + e >= best_low && r32 + e > 0.0f) {
                     const double rr = min_eig_q(sxx, sxy, syy);
                     if (rr > 0.0) best = max(best, dbits(rr));
@@ -239,14 +294,15 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         if (MODE == 1) {
             const unsigned ball = __ballot_sync(0xFFFFFFFFu, keep);
             if (ball) {
-                unsigned base = 0;
-                if (lane == __ffs(ball) - 1) base = atomicAdd(&s.count[d], (unsigned)__popc(ball));
-                base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ball) - 1);
-                if (keep) {
-                    const size_t pos = (size_t)d * s.cap + base + __popc(ball & ((1u << lane) - 1));
-                    s.cand_key[pos] = key;
-                    s.cand_idx[pos] = (unsigned)(y * w + x);
+                if (qn + __popc(ball) > WB) {  // flush the warp's buffer (rare)
+                    qn = flush_cands(s, d, wkey[warp], widx[warp], qn);
                 }
+                if (keep) {
+                    const int k = qn + __popc(ball & ((1u << lane) - 1));
+                    wkey[warp][k] = key;
+                    widx[warp][k] = (unsigned)(y * w + x);
+                }
+                qn += __popc(ball);
             }
         }
         axx = bxx;
@@ -258,6 +314,7 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         Im = I0;
         I0 = Ip;
     }
+    if (MODE == 1 && qn) flush_cands(s, d, wkey[warp], widx[warp], qn);
     if (MODE == 0) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
