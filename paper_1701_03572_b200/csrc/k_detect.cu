@@ -213,10 +213,12 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double lo = 0.0;
     if (MODE == 1) {
-        if (redo && !(s.flags[d] & 2)) return;
-        const unsigned long long mb = s.maxbits[d];
-        if (mb == 0) return;  // max_response <= 0: no corners (features.cpp:103-105)
-        lo = redo ? dmul(quality, __longlong_as_double((long long)mb)) : s.lo[d];
+        if (redo) {
+            if (!(s.flags[d] & 2)) return;
+            lo = dmul(quality, __longlong_as_double((long long)s.maxbits[d]));
+        } else {
+            lo = s.lo[d];
+        }
     } else {
         for (int i = threadIdx.x; i < kRespBins; i += blockDim.x) sh[i] = 0;
     }
@@ -280,15 +282,12 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
                     const unsigned peers = __match_any_sync(__activemask(), bin);
                     if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], 4u * __popc(peers));
                 }
-                if (r32 + e >= best_low && r32 + e > 0.0f) {
-                    const double rr = min_eig_q(sxx, sxy, syy);
-                    if (rr > 0.0) best = max(best, dbits(rr));
-                }
-                best_low = fmaxf(best_low, r32 - e);
+                best_low = fmaxf(best_low, r32 - e);  // max(r32 - e) <= exact max response
             } else if (r32 + e >= lo32) {
                 const double rr = min_eig_q(sxx, sxy, syy);
                 keep = rr >= lo && rr > 0.0;
                 key = dbits(rr);
+                if (keep) best = max(best, key);  // exact max: the max pixel is always kept
             }
         }
         if (MODE == 1) {
@@ -314,47 +313,49 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         Im = I0;
         I0 = Ip;
     }
-    if (MODE == 1 && qn) flush_cands(s, d, wkey[warp], widx[warp], qn);
-    if (MODE == 0) {
+    if (MODE == 1) {
+        if (qn) flush_cands(s, d, wkey[warp], widx[warp], qn);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
         if (lane == 0 && best) atomicMax(&s.maxbits[d], best);
+    }
+    if (MODE == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best_low = fmaxf(best_low, __shfl_xor_sync(0xFFFFFFFFu, best_low, o));
+        if (lane == 0 && best_low > 0.0f) atomicMax(&s.mlo[d], __float_as_uint(best_low));
         __syncthreads();
         for (int i = threadIdx.x; i < kRespBins; i += blockDim.x)
             if (sh[i]) atomicAdd(&s.hist[(size_t)d * kRespBins + i], sh[i]);
     }
 }
 
-// Per frame: candidate cut lo >= quality * max such that about `keep`
-// candidates lie above it (from the fp32 histogram; any lo >= the threshold is
-// exact because the kept set is then a prefix of the reference's sorted
-// candidate list, and select falls back to the full list when the prefix runs
-// out before max_corners).
+// Per frame: candidate cut lo such that about `keep` candidates lie above it
+// (fp32 histogram), clamped to [quality * M, M] where M = s.mlo (a proven
+// lower bound of the exact max response), so the max pixel is always kept and
+// MODE 1 finds the exact max.  Exactness: the kept set {r >= lo} is a prefix
+// of the reference's score order; select drops r < quality * max and falls
+// back to the full list when lo > quality * max and the prefix runs out before
+// max_corners.
 __global__ void resp_cut_kernel(double quality, DetectScratch s, unsigned keep) {
     const int d = blockIdx.x;
     if (threadIdx.x != 0) return;
-    const unsigned long long mb = s.maxbits[d];
-    unsigned char fl = 0;
+    const double m = (double)__uint_as_float(s.mlo[d]);
     double lo = 0.0;
-    if (mb != 0) {
-        const double thr = dmul(quality, __longlong_as_double((long long)mb));
-        lo = thr;
+    if (m > 0.0) {
+        lo = dmul(quality, m);
         unsigned cum = 0;
         const unsigned* hs = s.hist + (size_t)d * kRespBins;
         for (int b = kRespBins - 1; b > 0; --b) {
             cum += hs[b];
             if (cum >= keep) {
                 const double edge = (double)__uint_as_float((unsigned)b << 20);
-                if (edge > thr) {
-                    lo = edge;
-                    fl = 1;
-                }
+                lo = fmin(fmax(edge, lo), m);
                 break;
             }
         }
     }
     s.lo[d] = lo;
-    s.flags[d] = fl;
+    s.flags[d] = 0;
 }
 
 __global__ void resp_redo_reset_kernel(DetectScratch s) {
@@ -573,11 +574,15 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned n = s.count[d];
     const unsigned long long mb = s.maxbits[d];
+    // candidates below quality * max are not the reference's (the fast path's
+    // cut may keep a few); a cut above the threshold is a prefix (may redo)
+    const double thr = mb ? dmul(cfg.quality_level, __longlong_as_double((long long)mb)) : 0.0;
+    const unsigned long long thrb = dbits(thr);
+    const bool cut = s.flags && s.lo[d] > thr;
     if (n == 0 || mb == 0) {
         if (tid == 0) {
             out_n[d] = 0;
-            // a cut list came out empty although the threshold list is not: redo
-            if (!redo && s.flags && (s.flags[d] & 1) && mb != 0) s.flags[d] |= 2;
+            if (!redo && cut && mb != 0) s.flags[d] |= 2;
         }
         return;
     }
@@ -590,7 +595,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     // ---- histogram + exclusive scan + scatter into bucket order
     for (int b = tid; b < kBuckets; b += SEL_THREADS) cursor[b] = 0;
     __syncthreads();
-    for (unsigned i = tid; i < n; i += SEL_THREADS) atomicAdd(&cursor[bucket_of(ck[i], maxf)], 1u);
+    for (unsigned i = tid; i < n; i += SEL_THREADS)
+        if (ck[i] >= thrb) atomicAdd(&cursor[bucket_of(ck[i], maxf)], 1u);
     __syncthreads();
     {
         constexpr int PER = kBuckets / SEL_THREADS;  // 8
@@ -607,11 +613,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
             cursor[tid * PER + k] = off;
             off += v[k];
         }
-        if (tid == 0) S.bstart[kBuckets] = n;
+        if (tid == 0) S.bstart[kBuckets] = S.total;
     }
     __syncthreads();
     for (unsigned i = tid; i < n; i += SEL_THREADS) {
         const unsigned long long k = ck[i];
+        if (k < thrb) continue;
         const unsigned pos = atomicAdd(&cursor[bucket_of(k, maxf)], 1u);
         sk[pos] = k;
         si[pos] = ci[i];
@@ -766,7 +773,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     if (tid == 0) {
         out_n[d] = S.naccepted;
         // the cut prefix ran out before max_corners: redo from the full list
-        if (!redo && s.flags && (s.flags[d] & 1) && S.naccepted < maxc) s.flags[d] |= 2;
+        if (!redo && cut && S.naccepted < maxc) s.flags[d] |= 2;
     }
 }
 
@@ -797,9 +804,10 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     cudaMemsetAsync(s.count, 0, sizeof(unsigned) * nD, st);
     const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
     const int half = cfg.block_size / 2;
-    const bool fast = half == 1 && s.hist && s.lo && s.flags;
+    const bool fast = half == 1 && s.hist && s.lo && s.flags && s.mlo;
     if (fast) {
         cudaMemsetAsync(s.hist, 0, sizeof(unsigned) * kRespBins * (size_t)nD, st);
+        cudaMemsetAsync(s.mlo, 0, sizeof(unsigned) * (size_t)nD, st);
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<0><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 0);
         const unsigned keep = (unsigned)std::max(4096, 16 * cfg.max_corners);

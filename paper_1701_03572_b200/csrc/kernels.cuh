@@ -64,8 +64,9 @@ struct DetectScratch {
     unsigned long long* sort_key; // [nD][cap]
     unsigned int* sort_idx;       // [nD][cap]
     size_t cap;                   // candidates per detection frame (ROI area)
-    double* lo;                   // [nD] candidate cut (>= quality * max), fast path
-    unsigned char* flags;         // [nD] bit 0: cut above the threshold, bit 1: redo
+    double* lo;                   // [nD] candidate cut (fast path)
+    unsigned char* flags;         // [nD] bit 1: redo with the full candidate list
+    unsigned* mlo;                // [nD] fp32 bits of a lower bound of the max response
 };
 constexpr int kRespBins = 2048;
 constexpr int kBuckets = 8192;

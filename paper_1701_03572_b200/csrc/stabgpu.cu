@@ -244,6 +244,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins * nseg);
     DBUF(double, dlo, "det_lo", nseg);
     DBUF(unsigned char, dflags, "det_flags", nseg);
+    DBUF(unsigned, dmlo, "det_mlo", nseg);
     ds.maxbits = maxbits;
     ds.count = dcount;
     ds.hist = dhist;
@@ -254,6 +255,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     ds.cap = cap;
     ds.lo = dlo;
     ds.flags = dflags;
+    ds.mlo = dmlo;
     DBUF(double2, ptsA, "seg_ptsA", (size_t)nseg * maxc);
     DBUF(double2, ptsB, "seg_ptsB", (size_t)nseg * maxc);
     DBUF(int, nA, "seg_nA", nseg);
@@ -619,7 +621,8 @@ int stabgpu_detect_corners(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
     DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins);
     DBUF(double, dlo, "det_lo", 1);
     DBUF(unsigned char, dflags, "det_flags", 1);
-    DetectScratch ds{maxbits, dcount, dhist, ckey, cidx, skey, sidx, cap, dlo, dflags};
+    DBUF(unsigned, dmlo, "det_mlo", 1);
+    DetectScratch ds{maxbits, dcount, dhist, ckey, cidx, skey, sidx, cap, dlo, dflags, dmlo};
     PlaneBatch fb{d, n, w, h};
     launch_detect(fb, 1, *cfg, roi, ds, pts, sc, nn, st);
     ctx->stats.launches += 3;
