@@ -410,6 +410,13 @@ __global__ void resp_generic_kernel(PlaneBatch fr, stabgpu_roi roi, int half, in
 
 constexpr int SEL_THREADS = 1024;
 constexpr int CAP = 4096;       // chunk capacity (candidates sorted per pass)
+#ifndef SEL_CHUNK
+#define SEL_CHUNK 1024
+#endif
+// whole buckets are grouped into chunks of about SEL_CHUNK candidates: small
+// chunks let the parallel grid prefilter see more accepted corners, so the
+// serial warp greedy examines fewer candidates
+constexpr int CHUNK = SEL_CHUNK;
 constexpr int MAX_CELLS = 8192; // accepted-corner grid cells
 constexpr int SMEM_CORNERS = 8192;
 
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
             if (b0 >= kBuckets) {
                 S.done = 1;
             } else {
-                const unsigned limit = S.bstart[b0] + CAP;
+                const unsigned limit = S.bstart[b0] + CHUNK;
                 int lo = b0 + 1, hi = kBuckets;  // largest b1 with bstart[b1] <= limit
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
