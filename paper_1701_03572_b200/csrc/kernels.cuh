@@ -28,8 +28,9 @@ struct FramePlan {
     double tx, ty, theta, s;  // correction transform (delta_to_transform)
     double c, sn;             // cos(theta)/s, sin(theta)/s (warp_similarity, image_ops.cpp:121-122)
     // K8 fast-path steps in 16.48 fixed point: luma walk increments and the
-    // chroma map's d/dx; filled by finish_plan() for the frame geometry
-    long long cf, snf, kxx, kyx;
+    // chroma map's d/dx (kxx, kyx) and d/dy (kxy, kyy); filled by
+    // finish_plan() for the frame geometry
+    long long cf, snf, kxx, kyx, kxy, kyy;
 };
 
 // Fills the fixed-point members of a FramePlan (host or device).
@@ -37,14 +38,18 @@ __host__ __device__ inline void finish_plan(FramePlan& p, int w, int h, int cw, 
     const double FIXP = 281474976710656.0;  // 2^48
     p.cf = llrint(p.c * FIXP);
     p.snf = llrint(p.sn * FIXP);
-    p.kxx = p.kyx = 0;
+    p.kxx = p.kyx = p.kxy = p.kyy = 0;
     if (cw > 0 && ch > 0) {
         const int mx = (int)llround(crop * w), my = (int)llround(crop * h);
         const double step_x = w > 1 ? (double)(w - 2 * mx - 1) / (w - 1) : 0.0;
+        const double step_y = h > 1 ? (double)(h - 2 * my - 1) / (h - 1) : 0.0;
         const double fxl = (double)w / cw, fyl = (double)h / ch;
-        const double lxs = (mx != 0 || my != 0) ? fxl * step_x : fxl;
+        const bool crop_on = mx != 0 || my != 0;
+        const double lxs = crop_on ? fxl * step_x : fxl, lys = crop_on ? fyl * step_y : fyl;
         p.kxx = llrint(p.c * lxs / fxl * FIXP);
         p.kyx = llrint(-p.sn * lxs / fyl * FIXP);
+        p.kxy = llrint(p.sn * lys / fxl * FIXP);
+        p.kyy = llrint(p.c * lys / fyl * FIXP);
     }
 }
 

@@ -179,7 +179,7 @@ FramePlan host_plan(const stabgpu_transform& t) {
     p.s = t.s;
     p.c = std::cos(t.theta) / t.s;
     p.sn = std::sin(t.theta) / t.s;
-    p.cf = p.snf = p.kxx = p.kyx = 0;
+    p.cf = p.snf = p.kxx = p.kyx = p.kxy = p.kyy = 0;
     return p;
 }
 

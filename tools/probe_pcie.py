@@ -16,3 +16,17 @@ def both():
     with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
 c = t(both)
 print(f"H2D {n/a/1e9:.1f} GB/s  D2H {n/b/1e9:.1f} GB/s  overlapped {2*n/c/1e9:.1f} GB/s total ({n/c/1e9:.1f} each)")
+# several concurrent copies per direction (several copy engines?)
+for k in (2, 4):
+    ss = [torch.cuda.Stream() for _ in range(2 * k)]
+    part = n // k
+    def multi():
+        for i in range(k):
+            with torch.cuda.stream(ss[i]): d[i * part:(i + 1) * part].copy_(h[i * part:(i + 1) * part], non_blocking=True)
+            with torch.cuda.stream(ss[k + i]): h2[i * part:(i + 1) * part].copy_(d2[i * part:(i + 1) * part], non_blocking=True)
+    def multi_h2d():
+        for i in range(k):
+            with torch.cuda.stream(ss[i]): d[i * part:(i + 1) * part].copy_(h[i * part:(i + 1) * part], non_blocking=True)
+    e = t(multi_h2d)
+    c = t(multi)
+    print(f"{k} streams/dir: H2D alone {n/e/1e9:.1f} GB/s; overlapped {n/c/1e9:.1f} GB/s each direction")
