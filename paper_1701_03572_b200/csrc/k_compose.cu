@@ -941,7 +941,7 @@ __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, c
 // double-buffered and the TMA box of tile k+2 is issued only after the
 // barrier of tile k+1, so a fast warp may run ahead into the next tile.
 template <bool LUMA, bool CHROMA>
-__global__ void __launch_bounds__(NT, 3) compose_tma_kernel(
+__global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
     PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
     Tables T, int tiles_x, int tiles_y, int frames, const __grid_constant__ CUtensorMap mapY,
     const __grid_constant__ CUtensorMap mapCB, const __grid_constant__ CUtensorMap mapCR,
