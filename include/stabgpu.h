@@ -301,6 +301,31 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* dev_y, const uint8_t
                            const stabgpu_transform* host_corrections, double crop_ratio,
                            uint8_t* dev_out_y, uint8_t* dev_out_cb, uint8_t* dev_out_cr);
 
+/* ---- Stage II: streaming (one frame at a time) ------------------------
+ * Replaces run_streaming (pipeline.hpp:72-76 / pipeline.cpp:237-365) and the
+ * MotionStage -> CompensationPlanner -> compose loop of run_offline
+ * (pipeline.cpp:182-235): frames are pushed one at a time; a frame's
+ * correction is released with the reference's CompensationPlanner rule
+ * (nothing before 2r motion estimates unless the stream ended, then every
+ * frame whose smoothing window is complete, pipeline.cpp:137-150), so the
+ * latency is exactly r frames and the first emission happens at frame 2r.
+ * The released frames are bit-identical to Stage I (stabilize_sequence).
+ * Planes are host pointers (pitch = width).  After every push / finish the
+ * caller pops the ready frames in arrival order. */
+typedef struct stabgpu_stream stabgpu_stream;
+
+int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfg, int w, int h, int cw, int ch,
+                          stabgpu_stream** out);
+/* Motion estimate of the next frame; *n_ready = frames ready to pop. */
+int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                        int* n_ready);
+/* End of stream: releases the remaining frames (at least 2 frames pushed). */
+int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready);
+/* Oldest ready frame (its index, planes and record); STABGPU_SEQUENCING if none. */
+int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* out_y, uint8_t* out_cb,
+                       uint8_t* out_cr, stabgpu_frame_record* record);
+int stabgpu_stream_destroy(stabgpu_stream* s);
+
 /* ---- instrumentation (bench / tests) -------------------------------- */
 /* Per-kernel-family device time of the last sequence call (ms, CUDA events
  * on the launching stream) and the number of kernel launches it issued. */

@@ -120,6 +120,11 @@ PROTOTYPES = {
     "stabgpu_motion_chunk": (I, [V, V, C.c_int64, I, I, I, P(Config), V]),
     "stabgpu_plan_corrections": (I, [V, V, I, P(Config), V]),
     "stabgpu_compose_frames": (I, [V, V, V, V, I, I, I, I, I, V, C.c_double, V, V, V]),
+    "stabgpu_stream_create": (I, [V, P(Config), I, I, I, I, P(V)]),
+    "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
+    "stabgpu_stream_finish": (I, [V, c_ip]),
+    "stabgpu_stream_pop": (I, [V, P(C.c_int64), V, V, V, V]),
+    "stabgpu_stream_destroy": (I, [V]),
     "stabgpu_get_stats": (I, [V, P(Stats)]),
     "stabgpu_enable_timing": (I, [V, I]),
 }

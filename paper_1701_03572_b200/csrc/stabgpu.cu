@@ -1157,4 +1157,300 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb
     return STABGPU_OK;
 }
 
+// ---- Stage II streaming ---------------------------------------------------
 }  // extern "C"
+
+// The streaming object owns its device memory (independent of the context's
+// Stage I buffers).  Frame-indexed records grow geometrically; frames live in
+// a ring of 2r + R + 2 slots (a frame is needed until its correction is
+// released, at most 2r frames after it arrived).
+struct stabgpu_stream {
+    stabgpu_ctx* ctx = nullptr;
+    stabgpu_config cfg{};
+    int w = 0, h = 0, cw = 0, ch = 0;
+    bool chroma = false, complete = false;
+    int cap = 0, ocap = 0;       // input / output ring slots
+    long long pushed = 0, next = 0;  // frames pushed, next frame to release
+    std::vector<void*> allocs;
+    // frames
+    uint8_t *ring_y = nullptr, *ring_cb = nullptr, *ring_cr = nullptr;
+    uint8_t *out_y = nullptr, *out_cb = nullptr, *out_cr = nullptr;
+    std::vector<long long> ready;    // released frame indices not yet popped (FIFO)
+    size_t ready_head = 0;
+    // motion state: two-frame pyramid (prev at 0, cur at 1)
+    DevPyramid P{};
+    stabgpu_roi roi{};
+    DetectScratch ds{};
+    double2 *pts = nullptr, *nxt = nullptr, *fwd = nullptr, *trk_prev = nullptr, *trk_cur = nullptr;
+    int *npts = nullptr, *nnxt = nullptr, *trk_n = nullptr;
+    double* score = nullptr;
+    uint8_t* keep = nullptr;
+    unsigned* work = nullptr;
+    // frame-indexed (grown on demand)
+    long long fcap = 0;
+    stabgpu_motion_record* motion = nullptr;
+    stabgpu_frame_record* rec = nullptr;
+    double4* cum = nullptr;
+    FramePlan* plan = nullptr;
+    PlanState* ps = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int salloc(stabgpu_stream* s, T** p, size_t count) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, count * sizeof(T) + 256) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(STABGPU_CUDA, "stream: device allocation of %zu bytes failed", count * sizeof(T));
+    }
+    s->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return STABGPU_OK;
+}
+
+// grows the frame-indexed arrays to hold frame index `need - 1`
+int stream_grow(stabgpu_stream* s, long long need) {
+    if (need <= s->fcap) return STABGPU_OK;
+    long long nc = std::max<long long>(256, s->fcap);
+    while (nc < need) nc *= 2;
+    cudaStream_t st = s->ctx->stream;
+    stabgpu_motion_record* m;
+    stabgpu_frame_record* r;
+    double4* c;
+    FramePlan* pl;
+    TRY(salloc(s, &m, nc));
+    TRY(salloc(s, &r, nc));
+    TRY(salloc(s, &c, nc));
+    TRY(salloc(s, &pl, nc));
+    if (s->fcap) {
+        CUDA_TRY(cudaMemcpyAsync(m, s->motion, sizeof(*m) * s->fcap, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(r, s->rec, sizeof(*r) * s->fcap, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(c, s->cum, sizeof(*c) * s->fcap, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(pl, s->plan, sizeof(*pl) * s->fcap, cudaMemcpyDeviceToDevice, st));
+    }
+    s->motion = m;
+    s->rec = r;
+    s->cum = c;
+    s->plan = pl;
+    s->fcap = nc;  // the old blocks stay allocated until destroy (stream-ordered reuse is not needed)
+    return STABGPU_OK;
+}
+
+// composes released frame i into output slot i % ocap and queues it
+int stream_release(stabgpu_stream* s, long long i) {
+    cudaStream_t st = s->ctx->stream;
+    const int r = s->cfg.smooth_radius;
+    launch_plan_smooth(s->cum, s->pushed, s->complete, i, 1, r, s->rec, s->plan,
+                       PlanGeom{s->w, s->h, s->chroma ? s->cw : 0, s->chroma ? s->ch : 0, s->cfg.crop_ratio}, st);
+    const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch;
+    const size_t in = (size_t)(i % s->cap), o = (size_t)(i % s->ocap);
+    PlaneBatch yb{s->ring_y + in * fl, fl, s->w, s->h};
+    PlaneBatch bb{s->chroma ? s->ring_cb + in * fc : nullptr, fc, s->cw, s->ch};
+    PlaneBatch rb{s->chroma ? s->ring_cr + in * fc : nullptr, fc, s->cw, s->ch};
+    launch_compose(yb, bb, rb, s->plan + i, 1, s->cfg.crop_ratio, s->out_y + o * fl,
+                   s->chroma ? s->out_cb + o * fc : nullptr, s->chroma ? s->out_cr + o * fc : nullptr, st);
+    s->ctx->stats.launches += 2;
+    s->ready.push_back(i);
+    return check_launch("stream compose");
+}
+
+// CompensationPlanner::release (pipeline.cpp:137-150)
+int stream_release_ready(stabgpu_stream* s) {
+    const int r = s->cfg.smooth_radius;
+    if (!s->complete && s->pushed < 2LL * r) return STABGPU_OK;
+    while (s->next < s->pushed && (s->complete || s->next + r < s->pushed)) {
+        if ((long long)(s->ready.size() - s->ready_head) >= s->ocap)
+            return set_err(STABGPU_SEQUENCING, "stream: %d released frames not popped", s->ocap);
+        TRY(stream_release(s, s->next));
+        ++s->next;
+    }
+    return STABGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, int h, int cw, int ch,
+                          stabgpu_stream** out) {
+    *out = nullptr;
+    if (!ctx) return set_err(STABGPU_INVALID_INPUT, "stream: null context");
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    cudaSetDevice(ctx->device);
+    auto* s = new stabgpu_stream();
+    s->ctx = ctx;
+    s->cfg = cfg;
+    s->w = w;
+    s->h = h;
+    s->chroma = cw > 0 && ch > 0;
+    s->cw = s->chroma ? cw : 0;
+    s->ch = s->chroma ? ch : 0;
+    const int r = cfg.smooth_radius, R = cfg.flow.redetect_interval, maxc = cfg.detect.max_corners;
+    s->cap = 2 * r + R + 2;
+    s->ocap = 2 * r + 2;
+    int rc = STABGPU_OK;
+    auto fail = [&](int code) {
+        stabgpu_stream_destroy(s);
+        return code;
+    };
+    const size_t fl = (size_t)w * h, fc = (size_t)s->cw * s->ch;
+    if ((rc = salloc(s, &s->ring_y, fl * s->cap)) || (rc = salloc(s, &s->out_y, fl * s->ocap))) return fail(rc);
+    if (s->chroma && ((rc = salloc(s, &s->ring_cb, fc * s->cap)) || (rc = salloc(s, &s->ring_cr, fc * s->cap)) ||
+                      (rc = salloc(s, &s->out_cb, fc * s->ocap)) || (rc = salloc(s, &s->out_cr, fc * s->ocap))))
+        return fail(rc);
+    // two-frame pyramid
+    s->P.levels = level_dims(w, h, cfg.flow.max_levels, s->P.w, s->P.h);
+    for (int l = 0; l < s->P.levels; ++l) {
+        uint8_t* lv;
+        s->P.stride[l] = (size_t)s->P.w[l] * s->P.h[l];
+        if ((rc = salloc(s, &lv, 2 * s->P.stride[l]))) return fail(rc);
+        s->P.lvl[l] = lv;
+    }
+    // detection scratch (one frame)
+    if ((rc = roi_of(w, h, cfg.detect.roi_margin, &s->roi))) return fail(rc);
+    const size_t cap = (size_t)(s->roi.x1 - s->roi.x0) * (s->roi.y1 - s->roi.y0);
+    DetectScratch& d = s->ds;
+    d.cap = cap;
+    if ((rc = salloc(s, &d.maxbits, 1)) || (rc = salloc(s, &d.count, 1)) || (rc = salloc(s, &d.hist, kRespBins)) ||
+        (rc = salloc(s, &d.cand_key, cap)) || (rc = salloc(s, &d.cand_idx, cap)) ||
+        (rc = salloc(s, &d.sort_key, cap)) || (rc = salloc(s, &d.sort_idx, cap)) || (rc = salloc(s, &d.lo, 1)) ||
+        (rc = salloc(s, &d.flags, 1)) || (rc = salloc(s, &d.mlo, 1)))
+        return fail(rc);
+    if ((rc = salloc(s, &s->pts, maxc)) || (rc = salloc(s, &s->nxt, maxc)) || (rc = salloc(s, &s->fwd, maxc)) ||
+        (rc = salloc(s, &s->trk_prev, maxc)) || (rc = salloc(s, &s->trk_cur, maxc)) ||
+        (rc = salloc(s, &s->npts, 1)) || (rc = salloc(s, &s->nnxt, 1)) || (rc = salloc(s, &s->trk_n, 1)) ||
+        (rc = salloc(s, &s->score, maxc)) || (rc = salloc(s, &s->keep, maxc)) || (rc = salloc(s, &s->work, 1)))
+        return fail(rc);
+    if ((rc = stream_grow(s, 256))) return fail(rc);
+    if ((rc = init_plan_state(ctx, cfg, &s->ps))) return fail(rc);
+    // init_plan_state keeps its state in a context buffer: give the stream its own copy
+    PlanState* own;
+    if ((rc = salloc(s, &own, 2))) return fail(rc);
+    if (cudaMemcpyAsync(own, s->ps, 2 * sizeof(PlanState), cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+        return fail(set_err(STABGPU_CUDA, "stream: state copy failed"));
+    s->ps = own;
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return fail(set_err(STABGPU_CUDA, "stream: %s", cudaGetErrorString(cudaGetLastError())));
+    *out = s;
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int* n_ready) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    if (s->complete) return set_err(STABGPU_SEQUENCING, "stream: push after finish");
+    if (!y || (s->chroma && (!cb || !cr))) return set_err(STABGPU_INVALID_INPUT, "stream: missing planes");
+    stabgpu_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const stabgpu_config& cfg = s->cfg;
+    const long long f = s->pushed;
+    const int R = cfg.flow.redetect_interval, maxc = cfg.detect.max_corners;
+    if (s->next + s->cap <= f)  // cannot happen with the release rule; guards the ring
+        return set_err(STABGPU_SEQUENCING, "stream: input ring overrun");
+    TRY(stream_grow(s, f + 1));
+    const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch;
+    const size_t slot = (size_t)(f % s->cap);
+    uint8_t* fy = s->ring_y + slot * fl;
+    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyHostToDevice, st));
+    if (s->chroma) {
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyHostToDevice, st));
+    }
+    // K1: the pyramid of the current frame into slot 1
+    DevPyramid& P = s->P;
+    CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(P.lvl[0]) + P.stride[0], fy, fl, cudaMemcpyDeviceToDevice, st));
+    for (int l = 1; l < P.levels; ++l)
+        launch_pyramid_level(P.lvl[l - 1] + P.stride[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1],
+                             const_cast<uint8_t*>(P.lvl[l]) + P.stride[l], P.stride[l], 1, st);
+    ctx->stats.launches += P.levels - 1;
+    PlaneBatch cur{P.lvl[0] + P.stride[0], fl, s->w, s->h};
+    if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88) + detection (flow.cpp:303-308)
+        stabgpu_motion_record f0;
+        std::memset(&f0, 0, sizeof f0);
+        f0.frame_kind = STABGPU_FRAME_FIRST;
+        CUDA_TRY(cudaMemcpyAsync(s->motion, &f0, sizeof f0, cudaMemcpyHostToDevice, st));
+        launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
+        CUDA_TRY(cudaStreamSynchronize(st));  // f0 is a stack temporary
+    } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
+        LkStep k;
+        std::memset(&k, 0, sizeof k);
+        k.pyr = P;
+        k.frame0 = 0;
+        k.seg_len = R;
+        k.t = 1;
+        k.nseg = 1;
+        k.max_pts = maxc;
+        k.pts = s->pts;
+        k.npts = s->npts;
+        k.fwd = s->fwd;
+        k.keep = s->keep;
+        k.nframes = 2;
+        k.mode = 1;
+        k.work = s->work;
+        launch_lk(k, cfg.flow, st);
+        launch_compact(k, s->nxt, s->nnxt, s->trk_prev, s->trk_cur, s->trk_n, 1, st);
+        launch_fit(s->trk_prev, s->trk_cur, s->trk_n, maxc, 1, f, cfg, s->motion + f, st);
+        std::swap(s->pts, s->nxt);
+        std::swap(s->npts, s->nnxt);
+        if (f % R == 0) launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
+        ctx->stats.launches += 3 + (f % R == 0 ? 3 : 0);
+    }
+    // K7: selector + trajectory prefix for this frame
+    launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
+    // the current pyramid becomes the previous one
+    for (int l = 0; l < P.levels; ++l)
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(P.lvl[l]), P.lvl[l] + P.stride[l], P.stride[l],
+                                 cudaMemcpyDeviceToDevice, st));
+    TRY(check_launch("stream push"));
+    s->pushed = f + 1;
+    TRY(stream_release_ready(s));
+    if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    if (s->pushed < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    cudaSetDevice(s->ctx->device);
+    s->complete = true;
+    TRY(stream_release_ready(s));
+    if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
+                       stabgpu_frame_record* record) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    if (s->ready_head >= s->ready.size()) return set_err(STABGPU_SEQUENCING, "stream: no frame ready");
+    cudaSetDevice(s->ctx->device);
+    cudaStream_t st = s->ctx->stream;
+    const long long i = s->ready[s->ready_head++];
+    if (s->ready_head == s->ready.size()) {
+        s->ready.clear();
+        s->ready_head = 0;
+    }
+    const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch, o = (size_t)(i % s->ocap);
+    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDeviceToHost, st));
+    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDeviceToHost, st));
+    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDeviceToHost, st));
+    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    TRY(plan_error(s->ctx, s->ps));
+    if (index) *index = i;
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_destroy(stabgpu_stream* s) {
+    if (!s) return STABGPU_OK;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    for (void* p : s->allocs) cudaFree(p);
+    delete s;
+    return STABGPU_OK;
+}
+
+}  // extern "C"
+

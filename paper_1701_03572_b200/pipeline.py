@@ -245,3 +245,62 @@ def stabilize_sharded(n: int, local_y, local_first: int, cfg: StabConfig, rank: 
                                  None if local_cb is None else local_cb[a:b],
                                  None if local_cr is None else local_cr[a:b], device=device)
     return oy, ob, orr, rec
+
+
+# ------------------------------------------------------------ Stage II -----
+class StreamStabilizer:
+    """Stage II (one frame at a time): the reference's run_offline /
+    run_streaming loop (pipeline.cpp:182-365) over the C ABI stream object.
+
+    push() estimates the new frame's motion and returns the frames whose
+    corrections became releasable (CompensationPlanner rule: none before 2r
+    estimates, then every frame whose smoothing window is complete); finish()
+    releases the rest.  Each released frame is (index, y, cb, cr, record) and
+    is bit-identical to Stage I's output for that frame."""
+
+    def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0):
+        self.w, self.h, self.cw, self.ch = w, h, cw, ch
+        self._c = cfg.c()
+        self._lib = load()
+        self._ctx = context(device)
+        self._h = C.c_void_p()
+        check(self._lib.stabgpu_stream_create(self._ctx.handle, C.byref(self._c), w, h, cw, ch,
+                                              C.byref(self._h)))
+
+    def _pop_all(self, n: int):
+        out = []
+        for _ in range(n):
+            idx = C.c_int64()
+            y = np.empty((self.h, self.w), np.uint8)
+            cb = cr = None
+            if self.cw:
+                cb = np.empty((self.ch, self.cw), np.uint8)
+                cr = np.empty((self.ch, self.cw), np.uint8)
+            rec = np.zeros(1, RECORD_DT)
+            check(self._lib.stabgpu_stream_pop(self._h, C.byref(idx), _vp(y), _vp(cb), _vp(cr), _vp(rec)))
+            out.append((idx.value, y, cb, cr, rec[0]))
+        return out
+
+    def push(self, y: np.ndarray, cb: np.ndarray | None = None, cr: np.ndarray | None = None):
+        y = np.ascontiguousarray(y, np.uint8)
+        cb = None if cb is None else np.ascontiguousarray(cb, np.uint8)
+        cr = None if cr is None else np.ascontiguousarray(cr, np.uint8)
+        n = C.c_int()
+        check(self._lib.stabgpu_stream_push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
+        return self._pop_all(n.value)
+
+    def finish(self):
+        n = C.c_int()
+        check(self._lib.stabgpu_stream_finish(self._h, C.byref(n)))
+        return self._pop_all(n.value)
+
+    def close(self):
+        if self._h:
+            self._lib.stabgpu_stream_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -340,3 +340,65 @@ def test_sequence_errors():
         pipeline.stabilize_sequence(y, cfg)
     with pytest.raises(stab.InvalidInputError):
         pipeline.stabilize_sequence(y[:1], _data.small_cfg())
+
+
+def _release_schedule(n, r):
+    """CompensationPlanner::release (pipeline.cpp:137-150): frames released
+    after each push (0-based) and at finish."""
+    out, nxt = [], 0
+    for k in range(n):
+        size = k + 1
+        rel = []
+        if size >= 2 * r:
+            while nxt < size and nxt + r < size:
+                rel.append(nxt)
+                nxt += 1
+        out.append(rel)
+    return out, list(range(nxt, n))
+
+
+@pytest.mark.parametrize("mode,ransac,smooth", [("similarity", 0, 5), ("hybrid", 200, 4), ("rigid", 100, 9)])
+def test_stream_equals_stage1(mode, ransac, smooth):
+    """Stage II (push one frame at a time) releases frames on the reference's
+    schedule (latency r, first emission at 2r) and each released frame and
+    record is bit-identical to Stage I."""
+    y, cb, cr = _data.video(frames=41, objects=2, jit_t=3.0, color=True)
+    cfg = _data.small_cfg(_data.MODES[mode], ransac=ransac, smooth=smooth)
+    sy, sb, sr, srec = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    n, (h, w) = len(y), y.shape[1:]
+    s = pipeline.StreamStabilizer(cfg, w, h, cb.shape[2], cb.shape[1])
+    sched, tail = _release_schedule(n, cfg.smooth_radius)
+    got = []
+    for k in range(n):
+        rel = s.push(y[k], cb[k], cr[k])
+        assert [r[0] for r in rel] == sched[k], k
+        got += rel
+    rel = s.finish()
+    assert [r[0] for r in rel] == tail
+    got += rel
+    s.close()
+    assert [g[0] for g in got] == list(range(n))
+    for i, gy, gb, gr, grec in got:
+        assert np.array_equal(gy, sy[i]) and np.array_equal(gb, sb[i]) and np.array_equal(gr, sr[i]), i
+        assert grec.tobytes() == srec[i].tobytes(), i
+
+
+def test_stream_gray_and_errors():
+    y = _data.video(frames=14)[0]
+    cfg = _data.small_cfg(smooth=3)
+    sy, _, _, srec = pipeline.stabilize_sequence(y, cfg)
+    s = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1])
+    got = []
+    for f in y:
+        got += s.push(f)
+    got += s.finish()
+    assert [g[0] for g in got] == list(range(len(y)))
+    assert all(np.array_equal(g[1], sy[g[0]]) for g in got)
+    with pytest.raises(stab.SequencingError):
+        s.push(y[0])  # push after finish
+    s.close()
+    one = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1])
+    assert one.push(y[0]) == []
+    with pytest.raises(stab.InvalidInputError):
+        one.finish()  # fewer than 2 frames
+    one.close()
