@@ -326,6 +326,28 @@ int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* out_y, uint8_
                        uint8_t* out_cr, stabgpu_frame_record* record);
 int stabgpu_stream_destroy(stabgpu_stream* s);
 
+/* ---- colour I/O and evaluation ---------------------
+ * Device-resident, n frames of w x h (pitch = width).  RGB is interleaved
+ * 8-bit.  Conversions are the reference's BT.601 full-range formulas
+ * (media_io.cpp:75-89 yuv_to_rgb / chroma_cb / chroma_cr, 568-570
+ * luma_bt601), bit-exact. */
+int stabgpu_rgb_to_ycbcr(stabgpu_ctx* ctx, const uint8_t* dev_rgb, int n, int w, int h,
+                         uint8_t* dev_y, uint8_t* dev_cb, uint8_t* dev_cr);
+int stabgpu_ycbcr_to_rgb(stabgpu_ctx* ctx, const uint8_t* dev_y, const uint8_t* dev_cb,
+                         const uint8_t* dev_cr, int n, int w, int h, uint8_t* dev_rgb);
+/* Stage I on interleaved RGB host frames (4:4:4 after conversion), output
+ * RGB host frames: upload, conversion, run_offline semantics, conversion of
+ * the composed planes back to RGB, download (media_io load/save around
+ * run_offline). */
+int stabgpu_stabilize_sequence_rgb(stabgpu_ctx* ctx, const uint8_t* host_rgb, int n, int w, int h,
+                                   const stabgpu_config* cfg, uint8_t* host_out_rgb,
+                                   stabgpu_frame_record* records);
+/* psnr_pair (synth_eval.cpp:214-240) support: the exact integer sum of
+ * squared differences of frames (k-1, k) over the cropped region, k = 1..n-1,
+ * and the pixel count of that region (host_sse has n-1 entries). */
+int stabgpu_interframe_sse(stabgpu_ctx* ctx, const uint8_t* dev_y, int n, int w, int h,
+                           double crop_ratio, uint64_t* host_sse, int64_t* host_count);
+
 /* ---- instrumentation (bench / tests) -------------------------------- */
 /* Per-kernel-family device time of the last sequence call (ms, CUDA events
  * on the launching stream) and the number of kernel launches it issued. */

@@ -32,6 +32,7 @@
 #include "stab/pipeline.hpp"
 #include "stab/smoothing.hpp"
 #include "stab/stream.hpp"
+#include "stab/synth_eval.hpp"
 
 namespace {
 
@@ -800,6 +801,64 @@ int ref_plan_corrections(const stabgpu_motion_record* motion, int n, const stabg
     }
     traj.mark_complete();
     for (int f = 0; f < n; ++f) put_transform(*traj.correction(f, sc.smooth), &rec[f].correction);
+    GUARD_END
+}
+
+
+// ---- evaluation (synth_eval.cpp:214-349) ----------------------------------
+static std::vector<stab::VideoFrame> frames_of(const uint8_t* y, int n, int w, int h) {
+    std::vector<stab::VideoFrame> v(n);
+    for (int i = 0; i < n; ++i) {
+        v[i].luma = stab::GrayFrame(w, h, i);  // Tracker requires increasing frame indices
+        std::memcpy(v[i].luma.pixels.data(), y + (size_t)i * w * h, (size_t)w * h);
+    }
+    return v;
+}
+
+int ref_psnr_pair(const uint8_t* a, const uint8_t* b, int w, int h, double crop, double* out) {
+    GUARD_BEGIN
+    stab::GrayFrame fa(w, h), fb(w, h);
+    std::memcpy(fa.pixels.data(), a, (size_t)w * h);
+    std::memcpy(fb.pixels.data(), b, (size_t)w * h);
+    *out = stab::psnr_pair(fa, fb, crop);
+    GUARD_END
+}
+
+int ref_reestimate_deltas(const uint8_t* y, int n, int w, int h, stabgpu_delta* out) {
+    GUARD_BEGIN
+    const std::vector<stab::DeltaParams> d = stab::reestimate_deltas(frames_of(y, n, w, h));
+    for (size_t i = 0; i < d.size(); ++i) put_delta(d[i], &out[i]);
+    GUARD_END
+}
+
+// out: psnr before, after; jitter before (dx dy da dls); jitter after; truth
+// rmse (4); has_truth; frames_skipped
+int ref_score(const uint8_t* orig, const uint8_t* stabilized, int n, int w, int h, const stabgpu_delta* truth,
+              const stabgpu_delta* est, int nt, double crop, double* out) {
+    GUARD_BEGIN
+    auto deltas = [&](const stabgpu_delta* d) {
+        std::vector<stab::DeltaParams> v;
+        for (int i = 0; d && i < nt; ++i) {
+            stab::DeltaParams p;
+            p.dx = d[i].dx;
+            p.dy = d[i].dy;
+            p.da = d[i].da;
+            p.dls = d[i].dls;
+            p.kind = d[i].kind == STABGPU_RIGID ? stab::ModelKind::Rigid : stab::ModelKind::Similarity;
+            p.skipped = d[i].skipped != 0;
+            v.push_back(p);
+        }
+        return v;
+    };
+    const stab::EvalReport r = stab::score(frames_of(orig, n, w, h), frames_of(stabilized, n, w, h), deltas(truth),
+                                           deltas(est), crop);
+    const double vals[16] = {r.mean_psnr_before, r.mean_psnr_after, r.jitter_energy_before.dx,
+                             r.jitter_energy_before.dy, r.jitter_energy_before.da, r.jitter_energy_before.dls,
+                             r.jitter_energy_after.dx, r.jitter_energy_after.dy, r.jitter_energy_after.da,
+                             r.jitter_energy_after.dls, r.truth_recovery_rmse.dx, r.truth_recovery_rmse.dy,
+                             r.truth_recovery_rmse.da, r.truth_recovery_rmse.dls, r.has_truth ? 1.0 : 0.0,
+                             (double)r.frames_skipped};
+    std::memcpy(out, vals, sizeof vals);
     GUARD_END
 }
 

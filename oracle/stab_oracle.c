@@ -1089,3 +1089,46 @@ int orc_stabilize_sequence(const uint8_t* y, const uint8_t* cb, const uint8_t* c
     free(corr);
     return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* BT.601 full-range conversions (media_io.cpp:75-89, 568-570) and the
+ * inter-frame PSNR pair (synth_eval.cpp:214-240). */
+static uint8_t clamp_lround(double v) {
+    const long r = lround(v);
+    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+}
+
+void orc_rgb_to_ycbcr(const uint8_t* rgb, size_t npx, uint8_t* y, uint8_t* cb, uint8_t* cr) {
+    for (size_t i = 0; i < npx; ++i) {
+        const unsigned r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+        y[i] = (uint8_t)((299 * r + 587 * g + 114 * b + 500) / 1000); /* luma_bt601 */
+        cb[i] = clamp_lround(128.0 - 0.168736 * r - 0.331264 * g + 0.5 * b);
+        cr[i] = clamp_lround(128.0 + 0.5 * r - 0.418688 * g - 0.081312 * b);
+    }
+}
+
+void orc_ycbcr_to_rgb(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, size_t npx, uint8_t* rgb) {
+    for (size_t i = 0; i < npx; ++i) {
+        const double du = cb[i] - 128.0, dv = cr[i] - 128.0;
+        rgb[3 * i] = clamp_lround(y[i] + 1.402 * dv);
+        rgb[3 * i + 1] = clamp_lround(y[i] - 0.344136 * du - 0.714136 * dv);
+        rgb[3 * i + 2] = clamp_lround(y[i] + 1.772 * du);
+    }
+}
+
+int orc_psnr_pair(const uint8_t* a, const uint8_t* b, int w, int h, double crop, double* out) {
+    if (!(crop >= 0.0 && crop < 0.5)) return fail(STABGPU_INVALID_CONFIG, "psnr crop_ratio must lie in [0, 0.5)");
+    const int mx = (int)lround(crop * w), my = (int)lround(crop * h);
+    double acc = 0.0;
+    long long n = 0;
+    for (int y = my; y < h - my; ++y)
+        for (int x = mx; x < w - mx; ++x) {
+            const double d = (double)a[(size_t)y * w + x] - b[(size_t)y * w + x];
+            acc += d * d;
+            ++n;
+        }
+    if (n == 0) return fail(STABGPU_INVALID_INPUT, "PSNR crop region is empty");
+    const double mse = acc / (double)n;
+    *out = mse == 0.0 ? INFINITY : 10.0 * log10(255.0 * 255.0 / mse);
+    return STABGPU_OK;
+}

@@ -57,6 +57,11 @@ int orc_compose_stabilized(const uint8_t* y, const uint8_t* cb, const uint8_t* c
 int orc_stabilize_sequence(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int n, int w,
                            int h, int cw, int ch, const stabgpu_config* cfg, uint8_t* oy,
                            uint8_t* ocb, uint8_t* ocr, stabgpu_frame_record* records);
+/* BT.601 full-range colour conversions (media_io.cpp:75-89, 568-570) and
+ * psnr_pair (synth_eval.cpp:214-240). */
+void orc_rgb_to_ycbcr(const uint8_t* rgb, size_t npx, uint8_t* y, uint8_t* cb, uint8_t* cr);
+void orc_ycbcr_to_rgb(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, size_t npx, uint8_t* rgb);
+int orc_psnr_pair(const uint8_t* a, const uint8_t* b, int w, int h, double crop, double* out);
 const char* orc_last_error(void);
 
 #ifdef __cplusplus

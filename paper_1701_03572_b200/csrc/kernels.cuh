@@ -171,4 +171,11 @@ void launch_rms_single(const double2* P, const double2* Q, int n, stabgpu_transf
 void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream_t st);
 void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
                                   PlanGeom geo, cudaStream_t st);
+// ---- colour conversion + evaluation (k_eval.cu) ----
+void launch_rgb_to_ycbcr(const uint8_t* rgb, size_t npx, uint8_t* y, uint8_t* cb, uint8_t* cr, cudaStream_t st);
+void launch_ycbcr_to_rgb(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, size_t npx, uint8_t* rgb,
+                         cudaStream_t st);
+void launch_interframe_sse(const uint8_t* frames, int n, int w, int h, int mx, int my, unsigned long long* sse,
+                           cudaStream_t st);
+
 }  // namespace stabgpu

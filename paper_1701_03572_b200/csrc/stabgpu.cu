@@ -1452,5 +1452,89 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
     return STABGPU_OK;
 }
 
+
+// ---- colour I/O + evaluation -----------------------------------------------
+int stabgpu_rgb_to_ycbcr(stabgpu_ctx* ctx, const uint8_t* rgb, int n, int w, int h, uint8_t* y, uint8_t* cb,
+                         uint8_t* cr) {
+    TRY(validate_frame(w, h));
+    if (n < 0) return set_err(STABGPU_INVALID_INPUT, "negative frame count");
+    cudaSetDevice(ctx->device);
+    launch_rgb_to_ycbcr(rgb, (size_t)n * w * h, y, cb, cr, ctx->stream);
+    ++ctx->stats.launches;
+    TRY(check_launch("rgb_to_ycbcr"));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return STABGPU_OK;
+}
+
+int stabgpu_ycbcr_to_rgb(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int n, int w,
+                         int h, uint8_t* rgb) {
+    TRY(validate_frame(w, h));
+    if (n < 0) return set_err(STABGPU_INVALID_INPUT, "negative frame count");
+    cudaSetDevice(ctx->device);
+    launch_ycbcr_to_rgb(y, cb, cr, (size_t)n * w * h, rgb, ctx->stream);
+    ++ctx->stats.launches;
+    TRY(check_launch("ycbcr_to_rgb"));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return STABGPU_OK;
+}
+
+int stabgpu_stabilize_sequence_rgb(stabgpu_ctx* ctx, const uint8_t* host_rgb, int n, int w, int h,
+                                   const stabgpu_config* cfg, uint8_t* host_out_rgb,
+                                   stabgpu_frame_record* records) {
+    TRY(validate_all(*cfg));
+    TRY(validate_frame(w, h));
+    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t fl = (size_t)w * h;
+    DBUF(uint8_t, rgb, "rgb_io", 3 * fl * n);
+    DBUF(uint8_t, y, "rgb_y", fl * n);
+    DBUF(uint8_t, cb, "rgb_cb", fl * n);
+    DBUF(uint8_t, cr, "rgb_cr", fl * n);
+    DBUF(uint8_t, oy, "rgb_oy", fl * n);
+    DBUF(uint8_t, ocb, "rgb_ocb", fl * n);
+    DBUF(uint8_t, ocr, "rgb_ocr", fl * n);
+    // chunked upload + conversion (copy engine and SMs overlap across chunks)
+    const int C = 64;
+    std::vector<cudaEvent_t> ev((n + C - 1) / C);
+    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int k = 0, f0 = 0; f0 < n; ++k, f0 += C) {
+        const size_t nf = std::min(C, n - f0);
+        CUDA_TRY(cudaMemcpyAsync(rgb + 3 * fl * f0, host_rgb + 3 * fl * f0, 3 * fl * nf, cudaMemcpyHostToDevice,
+                                 ctx->cin));
+        cudaEventRecord(ev[k], ctx->cin);
+        cudaStreamWaitEvent(st, ev[k], 0);
+        launch_rgb_to_ycbcr(rgb + 3 * fl * f0, fl * nf, y + fl * f0, cb + fl * f0, cr + fl * f0, st);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    TRY(check_launch("rgb_to_ycbcr"));
+    TRY(stabgpu_stabilize_sequence_device(ctx, y, cb, cr, n, w, h, w, h, cfg, oy, ocb, ocr, records));
+    launch_ycbcr_to_rgb(oy, ocb, ocr, fl * n, rgb, st);
+    TRY(check_launch("ycbcr_to_rgb"));
+    CUDA_TRY(cudaMemcpyAsync(host_out_rgb, rgb, 3 * fl * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ctx->stats.launches += 2;
+    return STABGPU_OK;
+}
+
+int stabgpu_interframe_sse(stabgpu_ctx* ctx, const uint8_t* y, int n, int w, int h, double crop,
+                           uint64_t* host_sse, int64_t* host_count) {
+    if (!(crop >= 0.0 && crop < 0.5)) return set_err(STABGPU_INVALID_CONFIG, "psnr crop_ratio must lie in [0, 0.5)");
+    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "inter-frame PSNR needs at least 2 frames");
+    if (w < 1 || h < 1) return set_err(STABGPU_INVALID_INPUT, "empty frames");
+    const int mx = (int)std::lround(crop * w), my = (int)std::lround(crop * h);
+    const long long count = (long long)std::max(0, w - 2 * mx) * std::max(0, h - 2 * my);
+    if (count == 0) return set_err(STABGPU_INVALID_INPUT, "PSNR crop region is empty");
+    cudaSetDevice(ctx->device);
+    DBUF(unsigned long long, sse, "eval_sse", (size_t)n - 1);
+    launch_interframe_sse(y, n, w, h, mx, my, sse, ctx->stream);
+    ++ctx->stats.launches;
+    TRY(check_launch("interframe_sse"));
+    CUDA_TRY(cudaMemcpyAsync(host_sse, sse, sizeof(uint64_t) * (n - 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (host_count) *host_count = count;
+    return STABGPU_OK;
+}
+
 }  // extern "C"
 

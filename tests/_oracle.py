@@ -221,3 +221,65 @@ def reference() -> CpuImpl:
 
 def have_reference() -> bool:
     return os.path.exists(REF)
+
+
+def colour_and_psnr(lib_path: str, prefix: str):
+    """(rgb_to_ycbcr, ycbcr_to_rgb, psnr_pair) of liboracle / libstabref."""
+    lib = C.CDLL(lib_path)
+    f1 = getattr(lib, prefix + "rgb_to_ycbcr")
+    f1.argtypes, f1.restype = [V, C.c_size_t, V, V, V], None
+    f2 = getattr(lib, prefix + "ycbcr_to_rgb")
+    f2.argtypes, f2.restype = [V, V, V, C.c_size_t, V], None
+    f3 = getattr(lib, prefix + "psnr_pair")
+    f3.argtypes, f3.restype = [V, V, I, I, D, P(D)], I
+
+    def rgb_to_ycbcr(rgb):
+        rgb = np.ascontiguousarray(rgb, np.uint8)
+        npx = rgb.size // 3
+        y, cb, cr = (np.empty(rgb.shape[:-1], np.uint8) for _ in range(3))
+        f1(_vp(rgb), npx, _vp(y), _vp(cb), _vp(cr))
+        return y, cb, cr
+
+    def ycbcr_to_rgb(y, cb, cr):
+        y, cb, cr = (np.ascontiguousarray(a, np.uint8) for a in (y, cb, cr))
+        out = np.empty(y.shape + (3,), np.uint8)
+        f2(_vp(y), _vp(cb), _vp(cr), y.size, _vp(out))
+        return out
+
+    def psnr_pair(a, b, crop):
+        a, b = np.ascontiguousarray(a, np.uint8), np.ascontiguousarray(b, np.uint8)
+        out = C.c_double()
+        rc = f3(_vp(a), _vp(b), a.shape[1], a.shape[0], crop, C.byref(out))
+        if rc:
+            raise ValueError(rc)
+        return out.value
+
+    return rgb_to_ycbcr, ycbcr_to_rgb, psnr_pair
+
+
+def ref_eval():
+    """libstabref's reestimate_deltas / score (synth_eval.cpp)."""
+    lib = C.CDLL(REF)
+    re_ = lib.ref_reestimate_deltas
+    re_.argtypes, re_.restype = [V, I, I, I, V], I
+    sc = lib.ref_score
+    sc.argtypes, sc.restype = [V, V, I, I, I, V, V, I, D, V], I
+    from paper_1701_03572_b200.pipeline import DELTA_DT
+
+    def reestimate(y):
+        y = np.ascontiguousarray(y, np.uint8)
+        out = np.zeros(len(y), DELTA_DT)
+        assert re_(_vp(y), y.shape[0], y.shape[2], y.shape[1], _vp(out)) == 0
+        return out
+
+    def score(orig, stab, truth, est, crop):
+        orig, stab = np.ascontiguousarray(orig, np.uint8), np.ascontiguousarray(stab, np.uint8)
+        out = np.zeros(16)
+        truth = None if truth is None else np.ascontiguousarray(truth)  # record views are strided
+        est = None if est is None else np.ascontiguousarray(est)
+        nt = 0 if truth is None else len(truth)
+        assert sc(_vp(orig), _vp(stab), orig.shape[0], orig.shape[2], orig.shape[1], _vp(truth), _vp(est), nt,
+                  crop, _vp(out)) == 0
+        return out
+
+    return reestimate, score

@@ -402,3 +402,81 @@ def test_stream_gray_and_errors():
     with pytest.raises(stab.InvalidInputError):
         one.finish()  # fewer than 2 frames
     one.close()
+
+
+# ------------------------------------------------ colour I/O + evaluation ----
+def test_colour_conversions_exhaustive_gpu():
+    """Device BT.601 conversions (k_eval.cu) against the pinned C restatement,
+    for every RGB and every YCbCr triple."""
+    import torch
+    from paper_1701_03572_b200 import evaluate
+    o1, o2, _ = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
+    v = np.arange(1 << 24, dtype=np.uint32)
+    trip = np.stack([(v >> 16) & 255, (v >> 8) & 255, v & 255], axis=-1).astype(np.uint8).reshape(16, 1024, 1024, 3)
+    gy, gb, gr = evaluate.rgb_to_ycbcr(trip)
+    oy, ob, orr = o1(trip)
+    assert np.array_equal(gy.cpu().numpy(), oy) and np.array_equal(gb.cpu().numpy(), ob)
+    assert np.array_equal(gr.cpu().numpy(), orr)
+    g = evaluate.ycbcr_to_rgb(trip[..., 0], trip[..., 1], trip[..., 2])
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cpu().numpy(), o2(trip[..., 0], trip[..., 1], trip[..., 2]))
+
+
+def test_stabilize_rgb_equals_planes():
+    """RGB in / RGB out (media_io load -> run_offline -> save) equals the
+    plane path with the reference conversions around it."""
+    from paper_1701_03572_b200 import _abi as A
+    from paper_1701_03572_b200._lib import check, context, load
+    import ctypes as C
+    o1, o2, _ = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
+    y, cb, cr = _data.video(frames=23, objects=1, color=True)
+    rgb = o2(y, cb, cr)  # a plausible RGB source
+    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    py, pb, pr = o1(rgb)
+    sy, sb, sr, srec = pipeline.stabilize_sequence(py, cfg, pb, pr)
+    want = o2(sy, sb, sr)
+    out = np.empty_like(rgb)
+    rec = np.zeros(len(rgb), pipeline.RECORD_DT)
+    c = cfg.c()
+    n, h, w = y.shape
+    check(load().stabgpu_stabilize_sequence_rgb(context(0).handle, C.c_void_p(rgb.ctypes.data), n, w, h, C.byref(c),
+                                                C.c_void_p(out.ctypes.data), C.c_void_p(rec.ctypes.data)))
+    assert np.array_equal(out, want)
+    assert rec.tobytes() == srec.tobytes()
+
+
+@pytest.mark.parametrize("crop", [0.0, 0.04])
+def test_interframe_psnr_bitexact(crop):
+    from paper_1701_03572_b200 import evaluate
+    _, _, opsnr = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
+    y = _data.video(frames=9, jit_t=3.0)[0]
+    y[4] = y[3]  # an identical pair: infinite PSNR
+    g = evaluate.interframe_psnr(y, crop)
+    want = [opsnr(y[i - 1], y[i], crop) for i in range(1, len(y))]
+    assert g == want
+
+
+@pytest.mark.skipif(not _oracle.have_reference(), reason="reference library not built")
+def test_score_matches_reference():
+    """evaluate.score (synth_eval.cpp:303-349) against the reference's own
+    score(): PSNRs bit-identical, jitter energies within tracking tolerance."""
+    from paper_1701_03572_b200 import evaluate
+    reest, rscore = _oracle.ref_eval()
+    y = _data.video(w=192, h=144, frames=21, jit_t=3.0)[0]
+    cfg = _data.small_cfg(_data.MODES["similarity"])
+    sy, _, _, rec = pipeline.stabilize_sequence(y, cfg)
+    truth = rec["delta"].copy()
+    truth["dx"] += 0.01  # any truth vector exercises the recovery RMSE
+    est = rec["delta"]
+    g = evaluate.score(y, sy, truth, est, crop_ratio=0.04)
+    r = rscore(y, sy, truth, est, 0.04)
+    assert g.mean_psnr_before == r[0] and g.mean_psnr_after == r[1]
+    assert np.allclose(g.jitter_energy_before, r[2:6], rtol=0, atol=1e-6)
+    assert np.allclose(g.jitter_energy_after, r[6:10], rtol=0, atol=1e-6)
+    assert np.allclose(g.truth_recovery_rmse, r[10:14], rtol=0, atol=1e-12)
+    assert g.has_truth == bool(r[14]) and g.frames_skipped == int(r[15])
+    d = evaluate.reestimate_deltas(y)
+    rd = reest(y)
+    for k in ("dx", "dy", "da", "dls"):
+        assert np.abs(d[k] - rd[k]).max() <= 1e-6, k
+    assert np.array_equal(d["skipped"], rd["skipped"])

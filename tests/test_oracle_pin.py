@@ -197,3 +197,24 @@ def test_sequence_matches_run_offline(impls):
                               deltas, corr, None))
     assert np.array_equal(oy, ry) and np.array_equal(ob, rb) and np.array_equal(orr, rr)
     assert all(corr[i].tx == rec["correction"]["tx"][i] for i in range(n))
+
+
+def test_colour_conversions_exhaustive():
+    """The C restatement of BT.601 (media_io.cpp:75-89, 568-570) against the
+    reference's own functions, for every RGB and every YCbCr triple."""
+    o1, o2, _ = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
+    r1, r2, _ = _oracle.colour_and_psnr(_oracle.REF, "ref_")
+    v = np.arange(1 << 24, dtype=np.uint32)
+    trip = np.stack([(v >> 16) & 255, (v >> 8) & 255, v & 255], axis=-1).astype(np.uint8).reshape(4096, 4096, 3)
+    for a, b in zip(o1(trip), r1(trip)):
+        assert np.array_equal(a, b)
+    assert np.array_equal(o2(trip[..., 0], trip[..., 1], trip[..., 2]), r2(trip[..., 0], trip[..., 1], trip[..., 2]))
+
+
+@pytest.mark.parametrize("crop", [0.0, 0.04, 0.3])
+def test_psnr_pair_matches_reference(crop):
+    _, _, opsnr = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
+    _, _, rpsnr = _oracle.colour_and_psnr(_oracle.REF, "ref_")
+    a, b = _data.noise_frame(97, 61, 1), _data.noise_frame(97, 61, 2)
+    assert opsnr(a, b, crop) == rpsnr(a, b, crop)
+    assert opsnr(a, a, crop) == rpsnr(a, a, crop) == float("inf")
