@@ -480,3 +480,21 @@ def test_score_matches_reference():
     for k in ("dx", "dy", "da", "dls"):
         assert np.abs(d[k] - rd[k]).max() <= 1e-6, k
     assert np.array_equal(d["skipped"], rd["skipped"])
+
+
+@pytest.mark.parametrize("w,h", [(192, 144), (193, 145)])
+def test_sequence_420_chroma(orc, w, h):
+    """Y4M 4:2:0 chroma geometry ((w+1)/2 x (h+1)/2, media_io.cpp:139-145)
+    through the whole Stage I: compose_plane's chroma scaling
+    (image_ops.cpp:165-202) on every frame."""
+    y, cb, cr = _data.video(w=w, h=h, frames=17, objects=1, jit_t=3.0, color=True)
+    cb2 = np.ascontiguousarray(cb[:, ::2, ::2])
+    cr2 = np.ascontiguousarray(cr[:, ::2, ::2])
+    assert cb2.shape[1:] == ((h + 1) // 2, (w + 1) // 2)
+    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    gy, gb, gr, grec = pipeline.stabilize_sequence(y, cfg, cb2, cr2)
+    oy, ob, orr, orec = orc.stabilize_sequence(y, cfg, cb2, cr2)
+    _compare_records(grec, orec)
+    for a, b in ((gy, oy), (gb, ob), (gr, orr)):
+        mx, cnt = _offby(a, b)
+        assert mx <= 1 and cnt <= 0.0005 * a.size
