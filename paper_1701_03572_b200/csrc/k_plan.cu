@@ -23,10 +23,27 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
                                  long long count, stabgpu_selector_cfg sel, PlanState* st,
                                  stabgpu_frame_record* __restrict__ rec, double4* __restrict__ cum,
                                  int* __restrict__ err) {
-    if (threadIdx.x != 0) return;
+    // The recurrence runs on lane 0; the whole warp stages the next 32 motion
+    // records in shared memory first (one record per lane, loads in flight
+    // together), so lane 0 never waits on a dependent global load per frame.
+    constexpr int RW = sizeof(stabgpu_motion_record) / 8;  // 15 eight-byte words
+    __shared__ unsigned long long buf[32][RW];
+    const int lane = threadIdx.x & 31;
     PlanState s = *st;
-    for (long long f = first; f < first + count; ++f) {
-        const stabgpu_motion_record m = motion[f];
+    for (long long f0 = first; f0 < first + count; f0 += 32) {
+        const long long nf = min(32LL, first + count - f0);
+        if (lane < nf) {
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(motion + f0 + lane);
+            unsigned long long v[RW];
+#pragma unroll
+            for (int k = 0; k < RW; ++k) v[k] = src[k];
+#pragma unroll
+            for (int k = 0; k < RW; ++k) buf[lane][k] = v[k];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (long long f = f0; f < f0 + nf; ++f) {
+        const stabgpu_motion_record m = *reinterpret_cast<const stabgpu_motion_record*>(buf[f - f0]);
         stabgpu_frame_record r;
         memset(&r, 0, sizeof r);
         r.frame_kind = m.frame_kind;
@@ -75,9 +92,14 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
         cum[f] = make_double4(s.cum[0], s.cum[1], s.cum[2], s.cum[3]);
         r.delta = d;
         rec[f] = r;
+            }
+        }
+        __syncwarp();
     }
-    s.scanned = first + count;
-    *st = s;
+    if (lane == 0) {
+        s.scanned = first + count;
+        *st = s;
+    }
 }
 
 __global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_known,
