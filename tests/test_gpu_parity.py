@@ -498,3 +498,16 @@ def test_sequence_420_chroma(orc, w, h):
     for a, b in ((gy, oy), (gb, ob), (gr, orr)):
         mx, cnt = _offby(a, b)
         assert mx <= 1 and cnt <= 0.0005 * a.size
+
+
+@pytest.mark.parametrize("radius", [3, 15, 20])
+def test_sequence_lk_windows(orc, radius):
+    """Stage I with the chain kernel at its window extremes (3, 15: the
+    33-column template path) and the generic kernel above 31x31 (r = 20)."""
+    y = _data.video(w=256, h=192, frames=16, jit_t=3.0, tex=512, blobs=200)[0]
+    cfg = _data.small_cfg(_data.MODES["similarity"], radius=radius, levels=3)
+    gy, _, _, grec = pipeline.stabilize_sequence(y, cfg)
+    oy, _, _, orec = orc.stabilize_sequence(y, cfg)
+    _compare_records(grec, orec)
+    mx, cnt = _offby(gy, oy)
+    assert mx <= 1 and cnt <= 0.0005 * gy.size
