@@ -612,9 +612,9 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
 // scale ~1) plus 16 columns, because the box's x origin must be 16-byte
 // aligned for uint8 tensors (an unaligned origin raises an illegal
 // instruction on sm_100).
-constexpr int BW = 96, BH = 80;
-constexpr int TTH = 64;            // TMA path output tile: TW x TTH
-constexpr int TWTH = 68;           // its W tile rows (<= 66 used)
+constexpr int BW = 96, BH = 144;
+constexpr int TTH = 128;           // TMA path output tile: TW x TTH
+constexpr int TWTH = 132;          // its W tile rows (<= 130 used)
 constexpr int QW = 64;  // per-warp exact-path queue
 
 struct SmemT {
