@@ -211,11 +211,12 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
     __shared__ unsigned widx[8][WB];
     const int d = blockIdx.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double lo = 0.0;
+    double lo = 0.0, hi_excl = 0.0;  // redo: the band [threshold, first cut) not yet listed
     if (MODE == 1) {
         if (redo) {
             if (!(s.flags[d] & 2)) return;
             lo = dmul(quality, __longlong_as_double((long long)s.maxbits[d]));
+            hi_excl = s.lo[d];
         } else {
             lo = s.lo[d];
         }
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
                 best_low = fmaxf(best_low, r32 - e);  // max(r32 - e) <= exact max response
             } else if (r32 + e >= lo32) {
                 const double rr = min_eig_q(sxx, sxy, syy);
-                keep = rr >= lo && rr > 0.0;
+                keep = rr >= lo && rr > 0.0 && (!redo || rr < hi_excl);
                 key = dbits(rr);
                 if (keep) best = max(best, key);  // exact max: the max pixel is always kept
             }
@@ -468,6 +469,7 @@ struct SelShared {
     int done;
     int gw, gh, cell;
     int b0, b1, big;
+    int chunk;  // adaptive chunk size (candidates grouped per pass)
 };
 
 // bitonic sort of n (power of two) keys in shared memory, (score desc, idx asc)
@@ -587,9 +589,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     const unsigned long long thrb = dbits(thr);
     const bool cut = s.flags && s.lo[d] > thr;
     if (n == 0 || mb == 0) {
-        if (tid == 0) {
+        if (tid == 0 && !redo) {  // (redo: the first pass's corners stand)
             out_n[d] = 0;
-            if (!redo && cut && mb != 0) s.flags[d] |= 2;
+            if (cut && mb != 0) s.flags[d] |= 2;
         }
         return;
     }
@@ -641,6 +643,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
         S.naccepted = 0;
         S.done = 0;
         S.b0 = 0;
+        S.chunk = CHUNK;
     }
     __syncthreads();
     for (int c = tid; c < S.gw * S.gh; c += SEL_THREADS) heads[c] = -1;
@@ -648,6 +651,21 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
     __syncthreads();
     const double md2 = dmul(cfg.min_distance, cfg.min_distance);
     const int gw = S.gw, gh = S.gh, cell = S.cell;
+    if (redo) {
+        // continue after the first pass: its corners are the reference's first
+        // out_n corners (the cut list was a prefix), so they seed the grid and
+        // only the band below the first cut is scanned
+        const int n0 = out_n[d];
+        for (int k = tid; k < n0; k += SEL_THREADS) {
+            const double2 q = out_xy[(size_t)d * maxc + k];
+            const int x = (int)q.x, y = (int)q.y;
+            axy[k] = make_short2((short)x, (short)y);
+            anext[k] = atomicExch(&heads[((y - roi.y0) / cell) * gw + (x - roi.x0) / cell], k);
+        }
+        if (tid == 0) S.naccepted = n0;
+        __threadfence_block();
+        __syncthreads();
+    }
 
     while (true) {
         // ---- next chunk of whole buckets [b0, b1) with <= CAP candidates
@@ -658,7 +676,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
             if (b0 >= kBuckets) {
                 S.done = 1;
             } else {
-                const unsigned limit = S.bstart[b0] + CHUNK;
+                const unsigned limit = S.bstart[b0] + S.chunk;
                 int lo = b0 + 1, hi = kBuckets;  // largest b1 with bstart[b1] <= limit
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
@@ -700,6 +718,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
             }
             const unsigned off = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
             const unsigned ns = S.total;
+            // adapt the chunk: few survivors -> larger chunks (fewer passes);
+            // many -> smaller ones (more prefiltering before the serial greedy)
+            if (tid == 0) {
+                if (ns < 64 && S.chunk < CAP) S.chunk *= 2;
+                else if (ns > 512 && S.chunk > 256) S.chunk /= 2;
+            }
             {
                 unsigned o = off;
 #pragma unroll
