@@ -45,6 +45,7 @@ namespace {
 
 constexpr int TW = 64, TH = 32;          // output tile
 constexpr int NT = 256;                  // threads per CTA
+constexpr int NW = NT / 32;              // warps per CTA (row stride of the warp-per-row loops)
 constexpr int WTW = 72, WTH = 36;        // warped-luma tile (<= 66 x 34 used)
 constexpr int SRC_W = 128, SRC_H = 80;   // staged source capacity per plane
 constexpr int QCAP = 1024;               // exact-path queue
@@ -1022,13 +1023,13 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             int qn;
             if (tp.lfit)
                 qn = w_rows_q(bx, BW, -(tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf,
-                              8 * snf, 8 * cf, limx, limy, S.wq[warp]);
+                              NW * snf, NW * cf, limx, limy, S.wq[warp]);
             else
-                qn = w_rows_q(gy, w, 0, rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf, 8 * snf, 8 * cf, limx,
+                qn = w_rows_q(gy, w, 0, rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf, NW * snf, NW * cf, limx,
                               limy, S.wq[warp]);
             if (__any_sync(FULL, qn > 0)) {  // exact pixels of this warp's rows, lanes in parallel
                 __syncwarp();
-                const int nq = qn <= QW ? qn : ((nv - warp + 7) / 8) * nu;
+                const int nq = qn <= QW ? qn : ((nv - warp + NW - 1) / NW) * nu;
                 for (int i = lane; i < nq; i += 32) {
                     int r, c;
                     if (qn <= QW) {
@@ -1036,7 +1037,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                         r = (int)(it >> 8);
                         c = (int)(it & 0xFF);
                     } else {  // queue overflow: every pixel of this warp's rows
-                        r = warp + 8 * (i / nu);
+                        r = warp + NW * (i / nu);
                         c = i % nu;
                     }
                     sts_u8(wsm + r * WTW + c, w_exact_tile(plan, f, bx, tp.lbx, tp.lby, tp.lfit, gy, w, h, u0 + c,
@@ -1058,13 +1059,13 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             int qn;
             if (tp.cfit)
                 qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY,
-                                   32 * kxx, 32 * kyx, 8 * kxy, 8 * kyy, limx, limy, S.wq[warp]);
+                                   32 * kxx, 32 * kyx, NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
             else
                 qn = chroma_rows_q(gcb, gcr, cw, 0, pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY, 32 * kxx, 32 * kyx,
-                                   8 * kxy, 8 * kyy, limx, limy, S.wq[warp]);
+                                   NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
             if (__any_sync(FULL, qn > 0)) {
                 __syncwarp();
-                const int nq = qn <= QW ? qn : ((ny - warp + 7) / 8) * nx;
+                const int nq = qn <= QW ? qn : ((ny - warp + NW - 1) / NW) * nx;
                 for (int i = lane; i < nq; i += 32) {
                     int r, c;
                     if (qn <= QW) {
@@ -1072,7 +1073,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                         r = (int)(it >> 8);
                         c = (int)(it & 0xFF);
                     } else {
-                        r = warp + 8 * (i / nx);
+                        r = warp + NW * (i / nx);
                         c = i % nx;
                     }
                     const uint32_t v = chroma_exact_tile(plan, f, g, b1p, b2p, tp.cbx, tp.cby, tp.cfit, gcb, gcr, w,
@@ -1143,7 +1144,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 }
                 if (__any_sync(FULL, qn > 0)) {
                     __syncwarp();
-                    const int nq = qn <= QW ? qn : ((ny - warp + 7) / 8) * nx;
+                    const int nq = qn <= QW ? qn : ((ny - warp + NW - 1) / NW) * nx;
                     for (int i = lane; i < nq; i += 32) {
                         int r, c;
                         if (qn <= QW) {
@@ -1151,7 +1152,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                             r = (int)(it >> 8);
                             c = (int)(it & 0xFF);
                         } else {
-                            r = warp + 8 * (i / nx);
+                            r = warp + NW * (i / nx);
                             c = i % nx;
                         }
                         stg_u8(oy + (size_t)r * w + c - lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
