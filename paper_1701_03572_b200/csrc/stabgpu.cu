@@ -234,17 +234,20 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     }
     // ---- K2-K4: corners on each segment's first frame
     const size_t cap = (size_t)(roi.x1 - roi.x0) * (roi.y1 - roi.y0);
+    // detection frames go in batches whose candidate scratch (24 B x ROI area
+    // per frame, the worst case) stays under ~8 GB however long the sequence
+    const int dbatch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nseg, (8ull << 30) / (24 * cap)));
     DetectScratch ds;
-    DBUF(unsigned long long, maxbits, "det_max", nseg);
-    DBUF(unsigned int, dcount, "det_count", nseg);
-    DBUF(unsigned long long, ckey, "det_ckey", cap * nseg);
-    DBUF(unsigned int, cidx, "det_cidx", cap * nseg);
-    DBUF(unsigned long long, skey, "det_skey", cap * nseg);
-    DBUF(unsigned int, sidx, "det_sidx", cap * nseg);
-    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins * nseg);
-    DBUF(double, dlo, "det_lo", nseg);
-    DBUF(unsigned char, dflags, "det_flags", nseg);
-    DBUF(unsigned, dmlo, "det_mlo", nseg);
+    DBUF(unsigned long long, maxbits, "det_max", dbatch);
+    DBUF(unsigned int, dcount, "det_count", dbatch);
+    DBUF(unsigned long long, ckey, "det_ckey", cap * dbatch);
+    DBUF(unsigned int, cidx, "det_cidx", cap * dbatch);
+    DBUF(unsigned long long, skey, "det_skey", cap * dbatch);
+    DBUF(unsigned int, sidx, "det_sidx", cap * dbatch);
+    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins * dbatch);
+    DBUF(double, dlo, "det_lo", dbatch);
+    DBUF(unsigned char, dflags, "det_flags", dbatch);
+    DBUF(unsigned, dmlo, "det_mlo", dbatch);
     ds.maxbits = maxbits;
     ds.count = dcount;
     ds.hist = dhist;
@@ -263,9 +266,13 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(double, dscore, "seg_score", (size_t)nseg * maxc);
     {
         Timer tm(ctx, 1);
-        PlaneBatch fb{y, (size_t)R * w * h, w, h};
-        launch_detect(fb, nseg, cfg.detect, roi, ds, ptsA, dscore, nA, st);
-        ctx->stats.launches += 3;
+        for (int d0 = 0; d0 < nseg; d0 += dbatch) {
+            const int nd = std::min(dbatch, nseg - d0);
+            PlaneBatch fb{y + (size_t)d0 * R * w * h, (size_t)R * w * h, w, h};
+            launch_detect(fb, nd, cfg.detect, roi, ds, ptsA + (size_t)d0 * maxc, dscore + (size_t)d0 * maxc,
+                          nA + d0, st);
+            ctx->stats.launches += 7;
+        }
         TRY(check_launch("detect"));
     }
     // ---- K5: R tracking steps over all segments
