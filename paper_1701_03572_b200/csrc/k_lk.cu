@@ -225,6 +225,14 @@ __device__ __forceinline__ uint32_t px_at(const Level& L, int x, int y, bool int
 }
 
 
+// per-warp 2x2 system in shared memory, reloaded per use (volatile: keeps the
+// six doubles out of the register file across the iteration loop)
+__device__ __forceinline__ double ldsv(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
@@ -399,7 +407,7 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
 // it[j].  A template failure (outside / TooSmall at level 0 / Unconditioned)
 // fails both, exactly as it fails a lone track_one.
 __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, int f0, int f1,
-                           const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, bool& ok0, bool& ok1,
+                           const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, double* sys, bool& ok0, bool& ok1,
                            double2& o0, double2& o1, unsigned& it0, unsigned& it1, unsigned& builds) {
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
@@ -463,7 +471,18 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             const double me = dsub(ht, dsqrt(dadd(dmul(hd, hd), dmul(gxy, gxy))));
             if (me < dmul(1e-4, (double)count)) return;  // Unconditioned
         }
-        const double det = dsub(dmul(gxx, gyy), dmul(gxy, gxy));
+        {
+            const double det = dsub(dmul(gxx, gyy), dmul(gxy, gxy));
+            if (lane == 0) {
+                sys[0] = gxx;
+                sys[1] = gxy;
+                sys[2] = gyy;
+                sys[3] = tx;
+                sys[4] = ty;
+                sys[5] = det;
+            }
+            __syncwarp();
+        }
         // lanes past the valid window read the zero slot (row step 0)
         const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
         const int gstep = lane < vw ? vw : 0;
@@ -499,10 +518,11 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 // sum(cur * grad); b = T - that
                 double sx = 0.0, sy = 0.0;
                 row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, gcol, gstep, sx, sy);
-                const double bx = tx - warp_dsum(sx);
-                const double by = ty - warp_dsum(sy);
-                const double dx = ddiv(dsub(dmul(gyy, bx), dmul(gxy, by)), det);
-                const double dy = ddiv(dsub(dmul(gxx, by), dmul(gxy, bx)), det);
+                const double bx = ldsv(sys + 3) - warp_dsum(sx);
+                const double by = ldsv(sys + 4) - warp_dsum(sy);
+                const double sxx = ldsv(sys), sxy = ldsv(sys + 1), syy = ldsv(sys + 2), sdet = ldsv(sys + 5);
+                const double dx = ddiv(dsub(dmul(syy, bx), dmul(sxy, by)), sdet);
+                const double dy = ddiv(dsub(dmul(sxx, by), dmul(sxy, bx)), sdet);
                 vx = dadd(vx, dx);
                 vy = dadd(vy, dy);
                 if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
@@ -561,7 +581,8 @@ __device__ __forceinline__ bool track_warp_fast(const DevPyramid& P, int fprev, 
     bool ok0, ok1;
     double2 o0, o1;
     unsigned it0 = 0, it1 = 0;
-    track_dual(P, fprev, px, py, fcur, -1, cfg, tg, stg, ok0, ok1, o0, o1, it0, it1, builds);
+    track_dual(P, fprev, px, py, fcur, -1, cfg, tg, stg, reinterpret_cast<double*>(stg + SM_ROWS * SM_PITCH), ok0, ok1,
+               o0, o1, it0, it1, builds);
     iters += it0;
     if (ok0) {
         ox = o0.x;
@@ -635,7 +656,7 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
 // point f_t is the next step's start) share one template build per level.
 // The forward t+1 result is used only when step t keeps the point, and its
 // iterations are counted only then, so the counters match a step-by-step run.
-__global__ void __launch_bounds__(128, 4) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
+__global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
                                                           unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -666,7 +687,8 @@ __global__ void __launch_bounds__(128, 4) lk_chain_kernel(LkChain c, stabgpu_flo
         double2 q = p;
         while (true) {
             unsigned it0 = 0, it1 = 0;
-            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, ok0, ok1, o0, o1, it0, it1, blds);
+            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, reinterpret_cast<double*>(stg + SM_ROWS * SM_PITCH),
+                       ok0, ok1, o0, o1, it0, it1, blds);
             its += it0;
             if (t == 0) {
                 if (!ok0) break;
@@ -802,7 +824,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
         // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
-        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8;
+        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 8;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -829,7 +851,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
 void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (c.nseg <= 0 || c.max_pts <= 0) return;
     const int side = 2 * cfg.window_radius + 1;
-    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8;  // doubles
+    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 8;  // doubles (+ the 2x2 system)
     const int wpc = 4;
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
     cudaFuncSetAttribute(lk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
