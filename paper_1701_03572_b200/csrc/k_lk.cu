@@ -480,6 +480,8 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 sys[3] = tx;
                 sys[4] = ty;
                 sys[5] = det;
+                sys[6] = plx;
+                sys[7] = ply;
             }
             __syncwarp();
         }
@@ -499,7 +501,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             bool diverged = false;
             int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
             for (int k = 0; k < cfg.max_iterations; ++k) {
-                const double qx = dadd(dadd(plx, gfx), vx), qy = dadd(dadd(ply, gfy), vy);
+                const double qx = dadd(dadd(ldsv(sys + 6), gfx), vx), qy = dadd(dadd(ldsv(sys + 7), gfy), vy);
                 if (!inside(ci, qx, qy)) {
                     diverged = true;
                     break;
