@@ -331,6 +331,112 @@ def run_ours(args, cfg):
     return 0
 
 
+# ------------------------------------------------------------ c5 streams ---
+def run_streams(args, cfg, group=64):
+    """BASELINE configs[4]: 256 independent 1280x720 streams of 240 frames,
+    round-robin over ranks (no collective).  One step = every stream of this
+    rank, stabilized through stabgpu_stabilize_streams_device in groups of
+    `group` streams (one launch per stage per group); e2e = the same through
+    the host-buffer entry point (pinned input, a reused pinned output group
+    buffer, copies overlapped inside the call)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_03572_b200 import _lib, pipeline
+    from paper_1701_03572_b200.synth import Video
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = cfg.video
+    mine = pipeline.streams_of_rank(spec.streams, rank, world)
+    S, F, h, w = len(mine), spec.frames, spec.height, spec.width
+    t0 = time.time()
+    host = torch.empty((S, F, h, w), dtype=torch.uint8, pin_memory=True)
+    for i, k in enumerate(mine):
+        Video(spec, stream=k).render(0, F, out=[host[i]])
+    gen_s = time.time() - t0
+    G = min(group, S)
+    ctx = _lib.context(local)
+    ctx.enable_timing(True)
+    stream = torch.cuda.current_stream(local)
+    ctx.set_stream(stream.cuda_stream)
+    dev = host.cuda()
+    dout = torch.empty((G, F, h, w), dtype=torch.uint8, device="cuda")
+    hout = torch.empty((G, F, h, w), dtype=torch.uint8, pin_memory=True)
+    cfg_c = cfg.stab.c()
+    rec = np.zeros((G, F), pipeline.RECORD_DT)
+
+    def step_device():
+        for g0 in range(0, S, G):
+            ns = min(G, S - g0)
+            pipeline.stabilize_streams_device(dev[g0:g0 + ns], cfg.stab, out_y=dout[:ns], records=False)
+
+    def step_e2e():
+        for g0 in range(0, S, G):
+            ns = min(G, S - g0)
+            pipeline.stabilize_streams_host_buffers(ctx, host[g0:g0 + ns], None, None, ns, F, w, h, 0, 0,
+                                                    cfg_c, hout[:ns], None, None, rec[:ns])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        launches0 = ctx.stats().launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+        ev1.record(stream)
+        barrier()
+        ms = ev0.elapsed_time(ev1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, (ctx.stats().launches - launches0) // max(steps, 1)
+
+    with ClockSampler(local) as clk:
+        ms_dev, launches = timed(step_device, args.steps, args.warmup)
+    ms_e2e, _ = timed(step_e2e, max(1, min(args.steps, 2)), 1)
+    total = spec.streams * F  # frames all ranks process per step
+    if rank == 0:
+        st = ctx.stats()
+        line = {"metric": METRIC, "value": total / (ms_dev / 1000.0), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE generator, host C, seed ^ stream)",
+                "config": {"workload": f"BASELINE c5: {cfg.name}", "streams": spec.streams,
+                           "frames_per_stream": F, "width": w, "height": h,
+                           "max_corners": cfg.stab.detect.max_corners, "levels": cfg.stab.flow.max_levels,
+                           "model": "rigid", "streams_per_call": G,
+                           "parallelism": f"streams round-robin x{world}" if world > 1 else "1 GPU",
+                           "l2": f"{S * F * w * h / 1e9:.1f} GB of input per step >> 126 MB L2",
+                           "seed": hex(spec.seed)},
+                "e2e": {"value": total / (ms_e2e / 1000.0), "unit": UNIT,
+                        "h2d_bytes_per_step": S * F * w * h,
+                        "d2h_bytes_per_step": S * F * (w * h + pipeline.RECORD_BYTES),
+                        "ms_per_step": ms_e2e},
+                "stage_ms_last_group": dict(zip(["pyramid", "detect", "track", "fit", "plan", "compose"],
+                                                [round(float(x), 3) for x in (
+                                                    st.ms_pyramid, st.ms_detect, st.ms_track, st.ms_fit,
+                                                    st.ms_plan, st.ms_compose)])),
+                "gpu_launches": int(launches), "clocks": clk.summary(), "input_gen_s": round(gen_s, 1)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -339,14 +445,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=0, help="c5: override the stream count (quick runs)")
     args = ap.parse_args()
     from paper_1701_03572_b200.synth import CONFIGS
 
     cfg = CONFIGS[args.config]
-    if args.config == "c5":
-        raise SystemExit("c5 (multi-stream) is a parity config; bench runs c1-c4")
     if args.impl == "reference":
+        if args.config == "c5":
+            raise SystemExit("--impl reference runs c1-c4 (c5 streams are c2-like sequences)")
         return run_reference_arm(args, cfg)
+    if args.config == "c5":
+        if args.streams:
+            cfg.video.streams = args.streams
+        return run_streams(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -268,6 +268,24 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* dev_y, co
                                       uint8_t* dev_out_cb, uint8_t* dev_out_cr,
                                       stabgpu_frame_record* host_records);
 
+/* ---- Multi-stream Stage I (BASELINE configs[4]: many independent
+ * sequences per GPU).  n_streams sequences of `frames` frames each, laid out
+ * stream-major ([stream][frame][h][w], chroma likewise).  Each stream's
+ * output and records (n_streams*frames entries, stream-major) equal
+ * run_offline (pipeline.cpp:182-235) on that stream alone; the RANSAC seed
+ * is the frame's index within its stream.  All streams share one launch per
+ * stage.  Errors name the stream ("stream k frame f: ..."). */
+int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* host_y, const uint8_t* host_cb,
+                              const uint8_t* host_cr, int n_streams, int frames, int w, int h,
+                              int cw, int ch, const stabgpu_config* cfg, uint8_t* host_out_y,
+                              uint8_t* host_out_cb, uint8_t* host_out_cr,
+                              stabgpu_frame_record* records);
+int stabgpu_stabilize_streams_device(stabgpu_ctx* ctx, const uint8_t* dev_y, const uint8_t* dev_cb,
+                                     const uint8_t* dev_cr, int n_streams, int frames, int w, int h,
+                                     int cw, int ch, const stabgpu_config* cfg, uint8_t* dev_out_y,
+                                     uint8_t* dev_out_cb, uint8_t* dev_out_cr,
+                                     stabgpu_frame_record* host_records);
+
 /* ---- Stage I split for multi-GPU sharding (§8e of SURVEY.md) ----------
  * Motion estimation for frames (first, first+count] of a sequence whose
  * frame `first` is a re-detect frame (first % redetect_interval == 0).

@@ -117,6 +117,8 @@ PROTOTYPES = {
     "stabgpu_trajectory_corrections": (I, [V, V, I, I, V]),
     "stabgpu_stabilize_sequence": (I, [V, V, V, V, I, I, I, I, I, P(Config), V, V, V, V]),
     "stabgpu_stabilize_sequence_device": (I, [V, V, V, V, I, I, I, I, I, P(Config), V, V, V, V]),
+    "stabgpu_stabilize_streams": (I, [V, V, V, V, I, I, I, I, I, I, P(Config), V, V, V, V]),
+    "stabgpu_stabilize_streams_device": (I, [V, V, V, V, I, I, I, I, I, I, P(Config), V, V, V, V]),
     "stabgpu_motion_chunk": (I, [V, V, C.c_int64, I, I, I, P(Config), V]),
     "stabgpu_plan_corrections": (I, [V, V, I, P(Config), V]),
     "stabgpu_compose_frames": (I, [V, V, V, V, I, I, I, I, I, V, C.c_double, V, V, V]),

@@ -201,15 +201,29 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
                                                           const double2* __restrict__ trk_cur,
                                                           const int* __restrict__ trk_n, int max_pts,
                                                           long long frame_index0, stabgpu_config cfg,
-                                                          stabgpu_motion_record* __restrict__ out) {
+                                                          stabgpu_motion_record* __restrict__ out,
+                                                          long long stream_frames) {
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ double red[FIT_WARPS];
     __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
     __shared__ Model wbest_m[FIT_WARPS];
     const int f = blockIdx.x;
-    const int n = trk_n[f];
     stabgpu_motion_record rec;
     memset(&rec, 0, sizeof rec);
+    // multi-stream chunk: the frame's index within its own stream (the RANSAC
+    // seed), and stream starts are first frames (MotionStage::step, pipeline.cpp:84-88)
+    long long frame = frame_index0 + f;
+    if (stream_frames > 0) {
+        frame %= stream_frames;
+        if (frame == 0) {
+            if (threadIdx.x == 0) {
+                rec.frame_kind = STABGPU_FRAME_FIRST;
+                out[f] = rec;
+            }
+            return;
+        }
+    }
+    const int n = trk_n[f];
     rec.n_tracks = n;
     rec.rigid.kind = STABGPU_RIGID;
     rec.similarity.kind = STABGPU_SIMILARITY;
@@ -230,7 +244,6 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
         Q[k] = trk_cur[(size_t)f * max_pts + k];
     }
     __syncthreads();
-    const long long frame = frame_index0 + f;
     const int mode = cfg.selector.mode;
     FitOut fr{0, 0, 0, 1, STABGPU_OK}, fs{0, 0, 0, 1, STABGPU_OK};
     for (int pass = 0; pass < 2; ++pass) {
@@ -277,12 +290,12 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
 
 void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
-                stabgpu_motion_record* out, cudaStream_t st) {
+                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames) {
     if (nframes <= 0) return;
     const size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
     cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fit_kernel<<<nframes, FIT_THREADS, smem, st>>>(trk_prev, trk_cur, trk_n, max_pts, frame_index0,
-                                                   cfg, out);
+                                                   cfg, out, stream_frames);
 }
 
 }  // namespace stabgpu

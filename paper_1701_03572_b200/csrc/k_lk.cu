@@ -609,8 +609,8 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= total) break;
         const int seg = (int)(item / (unsigned)s.max_pts), k = (int)(item % (unsigned)s.max_pts);
-        const int fprev = s.frame0 + seg * s.seg_len + s.t - 1, fcur = fprev + 1;
-        if (fcur >= s.nframes || k >= s.npts[seg]) continue;
+        const int fprev = s.frame0 + seg_base(seg, s.seg_len, s.F, s.nsps) + s.t - 1, fcur = fprev + 1;
+        if (fcur >= s.frame0 + seg_end(seg, s.F, s.nsps, s.nframes - s.frame0) || k >= s.npts[seg]) continue;
         const size_t slot = (size_t)seg * s.max_pts + k;
         const double2 p = s.pts[slot];
         unsigned iters = 0, builds = 0;
@@ -658,6 +658,9 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
 // point f_t is the next step's start) share one template build per level.
 // The forward t+1 result is used only when step t keeps the point, and its
 // iterations are counted only then, so the counters match a step-by-step run.
+// MS: several streams per chunk (segment map; step count parked in shared
+// memory).  The one-stream instance keeps the map in kernel parameters.
+template <bool MS>
 __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
                                                           unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
@@ -674,11 +677,21 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= total) break;
         const int seg = (int)(item / (unsigned)c.max_pts), k = (int)(item % (unsigned)c.max_pts);
-        const int b0 = seg * c.R;  // detection frame of the segment (chunk-relative)
-        if (b0 + 1 >= c.nframes || k >= c.npts[seg]) continue;
+        int b0;  // detection frame of the segment (chunk-relative)
+        if (MS) {
+            b0 = seg_base(seg, c.R, c.F, c.nsps);
+            // steps this segment may take, parked in shared memory (registers are full)
+            const int nst = min(c.R, seg_end(seg, c.F, c.nsps, c.nframes) - 1 - b0);
+            if (nst <= 0 || k >= c.npts[seg]) continue;
+            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 8 * 8) = nst;
+            __syncwarp();
+        } else {
+            b0 = seg * c.R;
+            if (b0 + 1 >= c.nframes || k >= c.npts[seg]) continue;
+        }
         const size_t slot = (size_t)seg * c.max_pts + k;
         double2 p = c.pts[slot], f = p;
-        unsigned its = 0, blds = 0, tracks = 0;
+        unsigned its = 0, blds = 0;
         bool ok0, ok1;
         double2 o0, o1;
         // round 0: step 1 forward (template in b0 at p, target b0+1).  Round
@@ -709,18 +722,23 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
                 p = f;
                 f = o1;
             }
-            ++t;
-            ++tracks;
+            ++t;  // also the count of forward tracks run
             if (lane == 0) c.pos[(size_t)(t - 1) * plane + slot] = f;
-            ft = b0 + t;
+            if (MS)
+                ++ft;  // b0 + t (b0 need not stay live)
+            else
+                ft = b0 + t;
             q = f;
             f0 = ft - 1;
-            f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
+            if (MS)
+                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 8 * 8) ? ft + 1 : -1;
+            else
+                f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
         }
         if (lane == 0 && c.iter_count) {
             atomicAdd(c.iter_count, (unsigned long long)its);
             atomicAdd(c.iter_count + 1, (unsigned long long)blds);
-            atomicAdd(c.iter_count + 2, (unsigned long long)tracks);
+            atomicAdd(c.iter_count + 2, (unsigned long long)t);
         }
         __syncwarp();
     }
@@ -731,8 +749,8 @@ __global__ void lk_kernel(LkStep s, stabgpu_flow_cfg cfg, int warps_per_cta, int
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = blockIdx.y;
     const int k = blockIdx.x * warps_per_cta + warp;
-    const int fprev = s.frame0 + seg * s.seg_len + s.t - 1, fcur = fprev + 1;
-    if (fcur >= s.nframes) return;
+    const int fprev = s.frame0 + seg_base(seg, s.seg_len, s.F, s.nsps) + s.t - 1, fcur = fprev + 1;
+    if (fcur >= s.frame0 + seg_end(seg, s.F, s.nsps, s.nframes - s.frame0)) return;
     if (k >= s.npts[seg]) return;
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     double* ext = lsm + (size_t)warp * smem_per_warp;
@@ -780,8 +798,8 @@ __global__ void compact_kernel(LkStep s, double2* __restrict__ next_pts, int* __
     __shared__ int warp_tot[32];
     __shared__ int base;
     const int seg = blockIdx.x;
-    const int fcur = s.frame0 + seg * s.seg_len + s.t;
-    if (fcur >= s.nframes) return;
+    const int fcur = s.frame0 + seg_base(seg, s.seg_len, s.F, s.nsps) + s.t;
+    if (fcur >= s.frame0 + seg_end(seg, s.F, s.nsps, s.nframes - s.frame0)) return;
     const int n = s.npts[seg];
     const int tf = fcur - trk_frame0;  // TrackSet slot of frame fcur
     if (threadIdx.x == 0) base = 0;
@@ -853,20 +871,22 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
 void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (c.nseg <= 0 || c.max_pts <= 0) return;
     const int side = 2 * cfg.window_radius + 1;
-    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 8;  // doubles (+ the 2x2 system)
+    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 10;  // doubles (+ the 2x2 system, step count; even: 16 B aligned)
     const int wpc = 4;
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
-    cudaFuncSetAttribute(lk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool multi = c.nsps != c.nseg;  // several streams in the chunk
+    auto kern = multi ? lk_chain_kernel<true> : lk_chain_kernel<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk_chain_kernel, wpc * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, smem);
     cudaMemsetAsync(c.work, 0, sizeof(unsigned), st);
     cudaMemsetAsync(c.alive, 0, (size_t)c.R * c.nseg * c.max_pts, st);
     const long long items = (long long)c.nseg * c.max_pts;
     const long long want = (items + wpc - 1) / wpc;
     const int grid = (int)std::min<long long>(want, (long long)sms * std::max(per_sm, 1));
-    lk_chain_kernel<<<grid, wpc * 32, smem, st>>>(c, cfg, c.work, per_warp);
+    kern<<<grid, wpc * 32, smem, st>>>(c, cfg, c.work, per_warp);
 }
 
 void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,

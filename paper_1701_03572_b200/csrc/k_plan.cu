@@ -22,13 +22,19 @@ namespace {
 __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motion, long long first,
                                  long long count, stabgpu_selector_cfg sel, PlanState* st,
                                  stabgpu_frame_record* __restrict__ rec, double4* __restrict__ cum,
-                                 int* __restrict__ err) {
+                                 int* __restrict__ err, long long stride) {
     // The recurrence runs on lane 0; the whole warp stages the next 32 motion
     // records in shared memory first (one record per lane, loads in flight
     // together), so lane 0 never waits on a dependent global load per frame.
     constexpr int RW = sizeof(stabgpu_motion_record) / 8;  // 15 eight-byte words
     __shared__ unsigned long long buf[32][RW];
     const int lane = threadIdx.x & 31;
+    // one block per independent stream
+    motion += blockIdx.x * stride;
+    rec += blockIdx.x * stride;
+    cum += blockIdx.x * stride;
+    st += blockIdx.x;
+    err += blockIdx.x;
     PlanState s = *st;
     for (long long f0 = first; f0 < first + count; f0 += 32) {
         const long long nf = min(32LL, first + count - f0);
@@ -105,11 +111,13 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
 __global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_known,
                                    long long first, long long count, int radius,
                                    stabgpu_frame_record* __restrict__ rec, FramePlan* __restrict__ plan,
-                                   PlanGeom geo) {
+                                   PlanGeom geo, long long sf) {
     const long long i = first + blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= first + count) return;
-    const long long lo = i >= radius ? i - radius : 0;
-    const long long hi = min(i + radius, n_known - 1);
+    // window clipped to the frame's own stream (sf frames per stream, n_known each)
+    const long long base = sf ? i - i % sf : 0;
+    const long long lo = i - base >= radius ? i - radius : base;
+    const long long hi = min(i + radius, base + n_known - 1);
     double sx = 0.0, sy = 0.0, sa = 0.0, sl = 0.0;
     for (long long j = lo; j <= hi; ++j) {
         const double4 c = cum[j];
@@ -138,21 +146,22 @@ __global__ void plan_smooth_kernel(const double4* __restrict__ cum, long long n_
 
 void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long long count,
                       const stabgpu_config& cfg, PlanState* state, stabgpu_frame_record* rec,
-                      double4* cum, cudaStream_t st) {
-    if (count <= 0) return;
-    // error word lives right after the state
-    plan_scan_kernel<<<1, 32, 0, st>>>(motion, first, count, cfg.selector, state, rec, cum,
-                                       reinterpret_cast<int*>(state + 1));
+                      double4* cum, cudaStream_t st, int n_streams, long long stream_stride, int* err) {
+    if (count <= 0 || n_streams <= 0) return;
+    // default error word: right after the state
+    plan_scan_kernel<<<n_streams, 32, 0, st>>>(motion, first, count, cfg.selector, state, rec, cum,
+                                               err ? err : reinterpret_cast<int*>(state + 1), stream_stride);
 }
 
 void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
                         long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
-                        PlanGeom geo, cudaStream_t st) {
+                        PlanGeom geo, cudaStream_t st, long long stream_frames) {
     (void)complete;
     if (count <= 0) return;
     const int tpb = 128;
     plan_smooth_kernel<<<(unsigned)((count + tpb - 1) / tpb), tpb, 0, st>>>(cum, n_known, first, count,
-                                                                           radius, rec, plan, geo);
+                                                                           radius, rec, plan, geo,
+                                                                           stream_frames);
 }
 
 }  // namespace stabgpu

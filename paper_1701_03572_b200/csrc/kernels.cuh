@@ -102,7 +102,20 @@ struct LkStep {
     int mode;             // 0 track_lk, 1 forward + weed (sequence), 2 weed only
     const double2* ref;   // mode 2: prev points the backward track must return to
     unsigned* work;       // persistent-warp work counter (zeroed by launch_lk)
+    // multi-stream map (seg_base/seg_end below); nsps == 0: one stream
+    int F = 0, nsps = 0;
 };
+// Segment -> frame map of a chunk holding independent streams of F frames
+// each (stream-major).  Stream k is cut into nsps segments of R steps from
+// its own frame 0, so segment s starts at frame (s/nsps)*F + (s%nsps)*R and
+// its chain may not step past (s/nsps)*F + F - 1.  One stream: F = all
+// frames of the chunk, nsps = nseg.
+__host__ __device__ inline int seg_base(int seg, int R, int F, int nsps) {
+    return nsps ? (seg / nsps) * F + (seg % nsps) * R : seg * R;
+}
+__host__ __device__ inline int seg_end(int seg, int F, int nsps, int nframes) {
+    return nsps ? (seg / nsps) * F + F : nframes;
+}
 void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
 // Whole-segment tracking chains (r <= 15): every detected point of every
 // segment through all R steps in one launch.  pos/alive are [R][nseg][max_pts]
@@ -110,7 +123,8 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
 struct LkChain {
     DevPyramid pyr;
     int R, nseg, max_pts, nframes;
-    const double2* pts;  // [nseg][max_pts] detected points (frame seg*R)
+    int F, nsps;         // segment map (seg_base / seg_end)
+    const double2* pts;  // [nseg][max_pts] detected points (frame seg_base(seg))
     const int* npts;     // [nseg]
     double2* pos;
     uint8_t* alive;      // zeroed by launch_lk_chain
@@ -127,7 +141,7 @@ void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* tr
 // Fits frames [0, nframes) whose TrackSets are trk_*[f*max_pts ...], trk_n[f].
 void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
-                stabgpu_motion_record* out, cudaStream_t st);
+                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames = 0);
 
 // ---- K7 plan (k_plan.cu) ----
 struct PlanState {  // carried across incremental calls (selector + prefix)
@@ -135,16 +149,20 @@ struct PlanState {  // carried across incremental calls (selector + prefix)
     double cum[4];
     long long scanned;  // motion records consumed
 };
+// n_streams > 1: independent scans of streams k = 0..n_streams-1, whose
+// records start at k*stream_stride, with states state[k] and error words
+// err[k] (default: the word after state[0]).
 void launch_plan_scan(const stabgpu_motion_record* motion, long long first, long long count,
                       const stabgpu_config& cfg, PlanState* state, stabgpu_frame_record* rec,
-                      double4* cum, cudaStream_t st);
+                      double4* cum, cudaStream_t st, int n_streams = 1, long long stream_stride = 0,
+                      int* err = nullptr);
 struct PlanGeom {  // frame geometry the compose constants depend on
     int w, h, cw, ch;
     double crop;
 };
 void launch_plan_smooth(const double4* cum, long long n_known, bool complete, long long first,
                         long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
-                        PlanGeom geo, cudaStream_t st);
+                        PlanGeom geo, cudaStream_t st, long long stream_frames = 0);
 
 // ---- K8 compose (k_compose.cu) ----
 void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,

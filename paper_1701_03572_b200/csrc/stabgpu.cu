@@ -19,6 +19,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -197,22 +198,25 @@ struct Timer {
 // ---- K1 + K2-K4 + K5 + K6 over frames [first, first+count] ----------------
 // y points at frame `first`; motion receives records for frames
 // first+1 .. first+count at motion[first+1 ...] (and frame 0 when first == 0).
+// n_streams > 1 (first == 0): the count+1 frames are n_streams independent
+// sequences of equal length, stream-major; each is segmented from its own
+// frame 0 and its first frame gets a FIRST record, exactly as if it were run
+// alone.
 int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, int w, int h,
-               const stabgpu_config& cfg, stabgpu_motion_record* motion, double* t_ms) {
+               const stabgpu_config& cfg, stabgpu_motion_record* motion, double* t_ms,
+               int n_streams = 1) {
     cudaStream_t st = ctx->stream;
     const int nF = count + 1;
     const int R = cfg.flow.redetect_interval;
     const int maxc = cfg.detect.max_corners;
-    const int nseg = (count + R - 1) / R;
+    const int F = nF / n_streams;             // frames per stream
+    const int nsps = (F - 1 + R - 1) / R;     // segments per stream
+    const int nseg = n_streams * nsps;
+    const bool uniform = n_streams == 1 || F % R == 0;  // seg_base(s) == s*R
     stabgpu_roi roi;
     TRY(roi_of(w, h, cfg.detect.roi_margin, &roi));
-    if (first == 0) {
-        stabgpu_motion_record f0;
-        std::memset(&f0, 0, sizeof f0);
-        f0.frame_kind = STABGPU_FRAME_FIRST;
-        CUDA_TRY(cudaMemcpyAsync(motion, &f0, sizeof f0, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaStreamSynchronize(st));  // f0 is a stack temporary
-    }
+    static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
+    if (first == 0) CUDA_TRY(cudaMemsetAsync(motion, 0, sizeof(stabgpu_motion_record), st));
     if (count <= 0) return STABGPU_OK;
     // ---- K1: pyramid levels
     DevPyramid P;
@@ -266,12 +270,17 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(double, dscore, "seg_score", (size_t)nseg * maxc);
     {
         Timer tm(ctx, 1);
-        for (int d0 = 0; d0 < nseg; d0 += dbatch) {
-            const int nd = std::min(dbatch, nseg - d0);
-            PlaneBatch fb{y + (size_t)d0 * R * w * h, (size_t)R * w * h, w, h};
-            launch_detect(fb, nd, cfg.detect, roi, ds, ptsA + (size_t)d0 * maxc, dscore + (size_t)d0 * maxc,
-                          nA + d0, st);
-            ctx->stats.launches += 7;
+        // detection frames are R apart within a stream (and across streams
+        // when F is a multiple of R): batches never straddle a gap
+        const int run = uniform ? nseg : nsps;
+        for (int s0 = 0; s0 < nseg; s0 += run) {
+            for (int d0 = s0; d0 < s0 + run; d0 += dbatch) {
+                const int nd = std::min(dbatch, s0 + run - d0);
+                PlaneBatch fb{y + (size_t)seg_base(d0, R, F, nsps) * w * h, (size_t)R * w * h, w, h};
+                launch_detect(fb, nd, cfg.detect, roi, ds, ptsA + (size_t)d0 * maxc,
+                              dscore + (size_t)d0 * maxc, nA + d0, st);
+                ctx->stats.launches += 7;
+            }
         }
         TRY(check_launch("detect"));
     }
@@ -287,7 +296,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     if (cfg.flow.window_radius <= 15) {
         // whole-segment chains in one launch, then one ordered compaction per step
         Timer tm(ctx, 2);
-        const int steps = std::min(R, count);
+        const int steps = std::min(R, F - 1);
         DBUF(double2, pos, "lk_pos", (size_t)steps * nseg * maxc);
         DBUF(uint8_t, alive, "lk_alive", (size_t)steps * nseg * maxc);
         LkChain c;
@@ -296,6 +305,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         c.nseg = nseg;
         c.max_pts = maxc;
         c.nframes = nF;
+        c.F = F;
+        c.nsps = nsps;
         c.pts = ptsA;
         c.npts = nA;
         c.pos = pos;
@@ -318,6 +329,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
             s.fwd = pos + (size_t)(t - 1) * plane;
             s.keep = alive + (size_t)(t - 1) * plane;
             s.nframes = nF;
+            s.F = F;
+            s.nsps = nsps;
             launch_compact(s, ptsB, nB, trk_prev, trk_cur, trk_n, 1, st);
             ++ctx->stats.launches;
         }
@@ -328,8 +341,10 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         double2* nxt_pts = ptsB;
         int* cur_n = nA;
         int* nxt_n = nB;
-        for (int t = 1; t <= R && t <= count; ++t) {
+        for (int t = 1; t <= R && t < F; ++t) {
             LkStep s;
+            s.F = F;
+            s.nsps = nsps;
             s.pyr = P;
             s.frame0 = 0;
             s.seg_len = R;
@@ -356,7 +371,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     // ---- K6: fits
     {
         Timer tm(ctx, 3);
-        launch_fit(trk_prev, trk_cur, trk_n, maxc, count, first + 1, cfg, motion + first + 1, st);
+        launch_fit(trk_prev, trk_cur, trk_n, maxc, count, first + 1, cfg, motion + first + 1, st,
+                   n_streams > 1 ? F : 0);
         ++ctx->stats.launches;
         TRY(check_launch("fit"));
     }
@@ -377,34 +393,37 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     return STABGPU_OK;
 }
 
-int init_plan_state(stabgpu_ctx* ctx, const stabgpu_config& cfg, PlanState** out) {
-    DBUF(PlanState, ps, "plan_state", 2);  // state + error word
+// n states followed by n error words (for n == 1: the state, then its word)
+int init_plan_state(stabgpu_ctx* ctx, const stabgpu_config& cfg, PlanState** out, int n = 1) {
+    DBUF(PlanState, ps, "plan_state", 2 * (size_t)n);
     PlanState s;
     std::memset(&s, 0, sizeof s);
     s.current = cfg.selector.mode == STABGPU_FORCE_SIMILARITY ? STABGPU_SIMILARITY : STABGPU_RIGID;
     s.since = 0;
     s.pending = 1;
-    PlanState z[2];
-    z[0] = s;
-    std::memset(&z[1], 0, sizeof z[1]);
-    CUDA_TRY(cudaMemcpyAsync(ps, z, sizeof z, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<PlanState> z(2 * (size_t)n);
+    std::memset(z.data(), 0, z.size() * sizeof(PlanState));
+    for (int k = 0; k < n; ++k) z[k] = s;
+    CUDA_TRY(cudaMemcpyAsync(ps, z.data(), z.size() * sizeof(PlanState), cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     *out = ps;
     return STABGPU_OK;
 }
 
-int plan_error(stabgpu_ctx* ctx, PlanState* ps) {
-    int err = 0;
-    CUDA_TRY(cudaMemcpyAsync(&err, reinterpret_cast<int*>(ps + 1), sizeof err, cudaMemcpyDeviceToHost,
-                             ctx->stream));
+int plan_error(stabgpu_ctx* ctx, PlanState* ps, int n = 1) {
+    std::vector<int> err(n, 0);
+    CUDA_TRY(cudaMemcpyAsync(err.data(), reinterpret_cast<int*>(ps + n), n * sizeof(int),
+                             cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (err) {
-        const int code = err & 0xf;
-        const long long f = err >> 4;
+    for (int k = 0; k < n; ++k) {
+        if (!err[k]) continue;
+        const int code = err[k] & 0xf;
+        const long long f = err[k] >> 4;
+        const std::string where = n > 1 ? "stream " + std::to_string(k) + " " : std::string();
         return set_err(code, code == STABGPU_DEGENERATE_INPUT
-                                 ? "frame %lld: degenerate point set (all source points coincide or non-positive scale)"
-                                 : "frame %lld: estimation failed",
-                       f);
+                                 ? "%sframe %lld: degenerate point set (all source points coincide or non-positive scale)"
+                                 : "%sframe %lld: estimation failed",
+                       where.c_str(), f);
     }
     return STABGPU_OK;
 }
@@ -982,6 +1001,199 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const 
         ctx->stats.ms_compose = comp_ms;
         ctx->stats.ms_total = t_ms[0] + t_ms[1] + t_ms[2] + t_ms[3] + plan_ms + comp_ms;
     }
+    return STABGPU_OK;
+}
+
+// ---- multi-stream Stage I (BASELINE c5) -----------------------------------
+// n_streams independent sequences of `frames` frames each, stream-major.
+// Every stage runs once over all of them: one pyramid launch per level, the
+// detections batched, one LK chain launch over every segment of every stream,
+// one fit launch, one scan block per stream, one compose launch.  Each
+// stream's output and records equal run_offline (pipeline.cpp:182-235) on
+// that stream alone.
+}  // extern "C"
+namespace {
+int validate_streams(const stabgpu_config& cfg, int n_streams, int frames, int w, int h) {
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    if (n_streams < 1) return set_err(STABGPU_INVALID_INPUT, "n_streams must be >= 1");
+    if (frames < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    if ((long long)n_streams * frames > INT32_MAX / 2)
+        return set_err(STABGPU_INVALID_INPUT, "too many frames in one call");
+    return STABGPU_OK;
+}
+
+// One group of streams on ctx->stream, queued without a host sync.  motion,
+// rec, cum, plan point at the group's first frame; ps / err at its first
+// stream's state and error word.
+int streams_group(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                  int S, int F, int w, int h, int cw, int ch, const stabgpu_config& cfg, uint8_t* oy,
+                  uint8_t* ocb, uint8_t* ocr, stabgpu_motion_record* motion, stabgpu_frame_record* rec,
+                  double4* cum, FramePlan* plan, PlanState* ps, int* err, double* t_ms,
+                  float* plan_ms, float* comp_ms) {
+    cudaStream_t st = ctx->stream;
+    const long long n = (long long)S * F;
+    TRY(run_motion(ctx, y, 0, (int)(n - 1), w, h, cfg, motion, t_ms, S));
+    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
+    launch_plan_scan(motion, 0, F, cfg, ps, rec, cum, st, S, F, err);
+    launch_plan_smooth(cum, F, true, 0, n, cfg.smooth_radius, rec, plan,
+                       PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st, F);
+    ctx->stats.launches += 2;
+    TRY(check_launch("plan"));
+    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
+    {
+        Timer tm(ctx, 4);
+        TRY(compose_range(ctx, y, cb, cr, 0, n, w, h, cw, ch, plan, cfg.crop_ratio, oy, ocb, ocr));
+    }
+    if (ctx->timing && t_ms) {
+        float a = 0.f, b = 0.f;
+        CUDA_TRY(cudaEventSynchronize(ctx->ev[9]));
+        cudaEventElapsedTime(&a, ctx->ev[10], ctx->ev[11]);
+        cudaEventElapsedTime(&b, ctx->ev[8], ctx->ev[9]);
+        *plan_ms += a;
+        *comp_ms += b;
+    }
+    return STABGPU_OK;
+}
+
+void streams_stats(stabgpu_ctx* ctx, const double* t_ms, float plan_ms, float comp_ms) {
+    if (!ctx->timing) return;
+    ctx->stats.ms_pyramid = t_ms[0];
+    ctx->stats.ms_detect = t_ms[1];
+    ctx->stats.ms_track = t_ms[2];
+    ctx->stats.ms_fit = t_ms[3];
+    ctx->stats.ms_plan = plan_ms;
+    ctx->stats.ms_compose = comp_ms;
+    ctx->stats.ms_total = t_ms[0] + t_ms[1] + t_ms[2] + t_ms[3] + plan_ms + comp_ms;
+}
+}  // namespace
+extern "C" {
+
+int stabgpu_stabilize_streams_device(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb,
+                                     const uint8_t* cr, int n_streams, int frames, int w, int h,
+                                     int cw, int ch, const stabgpu_config* cfgp, uint8_t* oy,
+                                     uint8_t* ocb, uint8_t* ocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_streams(cfg, n_streams, frames, w, h));
+    const bool chroma = cb && cr && ocb && ocr;
+    if (!chroma) cb = cr = nullptr;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const long long n = (long long)n_streams * frames;
+    DBUF(stabgpu_motion_record, motion, "seq_motion", n);
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps, n_streams));
+    double t_ms[4] = {0, 0, 0, 0};
+    float plan_ms = 0.f, comp_ms = 0.f;
+    TRY(streams_group(ctx, y, cb, cr, n_streams, frames, w, h, cw, ch, cfg, oy, ocb, ocr, motion, rec,
+                      cum, plan, ps, reinterpret_cast<int*>(ps + n_streams), t_ms, &plan_ms, &comp_ms));
+    TRY(plan_error(ctx, ps, n_streams));
+    if (records)
+        CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    streams_stats(ctx, t_ms, plan_ms, comp_ms);
+    return STABGPU_OK;
+}
+
+// Host buffers: groups of streams (about 2 GB of luma each) flow through two
+// device slots, so the upload of group g+1 and the download of group g-1
+// overlap the compute of group g.
+int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb,
+                              const uint8_t* hcr, int n_streams, int frames, int w, int h, int cw,
+                              int ch, const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
+                              uint8_t* hocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_streams(cfg, n_streams, frames, w, h));
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const bool chroma = hcb && hcr && hocb && hocr;
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    const size_t sl = fl * frames, sc = fc * frames;  // bytes per stream and plane
+    int G = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_streams, (2ull << 30) / (sl + 2 * sc)));
+    if (const char* e = std::getenv("STABGPU_STREAMS_PER_GROUP"))  // test knob: force small groups
+        G = std::max(1, std::min(n_streams, std::atoi(e)));
+    const int ngroups = (n_streams + G - 1) / G;
+    const long long n = (long long)n_streams * frames;
+    uint8_t *dy[2], *doy[2], *dcb[2] = {nullptr, nullptr}, *dcr[2] = {nullptr, nullptr},
+            *docb[2] = {nullptr, nullptr}, *docr[2] = {nullptr, nullptr};
+    for (int k = 0; k < 2; ++k) {
+        const std::string t = std::to_string(k);
+        dy[k] = dbuf<uint8_t>(ctx, ("ms_y" + t).c_str(), sl * G);
+        doy[k] = dbuf<uint8_t>(ctx, ("ms_oy" + t).c_str(), sl * G);
+        if (!dy[k] || !doy[k]) return set_err(STABGPU_CUDA, "device allocation of stream slots failed");
+        if (chroma) {
+            dcb[k] = dbuf<uint8_t>(ctx, ("ms_cb" + t).c_str(), sc * G);
+            dcr[k] = dbuf<uint8_t>(ctx, ("ms_cr" + t).c_str(), sc * G);
+            docb[k] = dbuf<uint8_t>(ctx, ("ms_ocb" + t).c_str(), sc * G);
+            docr[k] = dbuf<uint8_t>(ctx, ("ms_ocr" + t).c_str(), sc * G);
+            if (!dcb[k] || !dcr[k] || !docb[k] || !docr[k])
+                return set_err(STABGPU_CUDA, "device allocation of stream slots failed");
+        }
+    }
+    DBUF(stabgpu_motion_record, motion, "seq_motion", n);
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps, n_streams));
+    int* err = reinterpret_cast<int*>(ps + n_streams);
+    // in_ev[g]: group g uploaded; done_ev[g]: group g computed (its input slot
+    // is free); out_ev[g]: group g downloaded (its output slot is free)
+    std::vector<cudaEvent_t> in_ev(ngroups), done_ev(ngroups), out_ev(ngroups);
+    for (int g = 0; g < ngroups; ++g) {
+        CUDA_TRY(cudaEventCreateWithFlags(&in_ev[g], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&done_ev[g], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&out_ev[g], cudaEventDisableTiming));
+    }
+    auto upload = [&](int g) -> int {
+        const int k = g & 1, s0 = g * G, ns = std::min(G, n_streams - s0);
+        if (g >= 2) cudaStreamWaitEvent(ctx->cin, done_ev[g - 2], 0);
+        if (cudaMemcpyAsync(dy[k], hy + s0 * sl, ns * sl, cudaMemcpyHostToDevice, ctx->cin) ||
+            (chroma && (cudaMemcpyAsync(dcb[k], hcb + s0 * sc, ns * sc, cudaMemcpyHostToDevice, ctx->cin) ||
+                        cudaMemcpyAsync(dcr[k], hcr + s0 * sc, ns * sc, cudaMemcpyHostToDevice, ctx->cin))))
+            return set_err(STABGPU_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+        cudaEventRecord(in_ev[g], ctx->cin);
+        return STABGPU_OK;
+    };
+    double t_ms[4] = {0, 0, 0, 0};
+    float plan_ms = 0.f, comp_ms = 0.f;
+    int rc = upload(0);
+    if (!rc && ngroups > 1) rc = upload(1);
+    for (int g = 0; g < ngroups && !rc; ++g) {
+        const int k = g & 1, s0 = g * G, ns = std::min(G, n_streams - s0);
+        const long long f0 = (long long)s0 * frames;
+        cudaStreamWaitEvent(st, in_ev[g], 0);
+        if (g >= 2) cudaStreamWaitEvent(st, out_ev[g - 2], 0);
+        rc = streams_group(ctx, dy[k], dcb[k], dcr[k], ns, frames, w, h, cw, ch, cfg, doy[k], docb[k],
+                           docr[k], motion + f0, rec + f0, cum + f0, plan + f0, ps + s0, err + s0,
+                           t_ms, &plan_ms, &comp_ms);
+        if (rc) break;
+        cudaEventRecord(done_ev[g], st);
+        if (g + 2 < ngroups && (rc = upload(g + 2))) break;
+        cudaStreamWaitEvent(ctx->cout, done_ev[g], 0);
+        if (cudaMemcpyAsync(hoy + s0 * sl, doy[k], ns * sl, cudaMemcpyDeviceToHost, ctx->cout) ||
+            (chroma && (cudaMemcpyAsync(hocb + s0 * sc, docb[k], ns * sc, cudaMemcpyDeviceToHost, ctx->cout) ||
+                        cudaMemcpyAsync(hocr + s0 * sc, docr[k], ns * sc, cudaMemcpyDeviceToHost, ctx->cout))))
+            rc = set_err(STABGPU_CUDA, "download failed: %s", cudaGetErrorString(cudaGetLastError()));
+        cudaEventRecord(out_ev[g], ctx->cout);
+    }
+    cudaStreamSynchronize(ctx->cin);
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(ctx->cout);
+    for (int g = 0; g < ngroups; ++g) {
+        cudaEventDestroy(in_ev[g]);
+        cudaEventDestroy(done_ev[g]);
+        cudaEventDestroy(out_ev[g]);
+    }
+    if (rc) return rc;
+    TRY(plan_error(ctx, ps, n_streams));
+    if (records)
+        CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    streams_stats(ctx, t_ms, plan_ms, comp_ms);
     return STABGPU_OK;
 }
 

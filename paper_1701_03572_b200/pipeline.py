@@ -102,6 +102,70 @@ def stabilize_sequence_device(y, cfg: StabConfig, cb=None, cr=None, out_y=None, 
     return out_y, out_cb, out_cr, rec
 
 
+# ------------------------------------------------------- many streams ------
+def stabilize_streams(y: np.ndarray, cfg: StabConfig, cb: np.ndarray | None = None,
+                      cr: np.ndarray | None = None, device: int = 0):
+    """BASELINE configs[4]: S independent sequences of F frames each.
+
+    y: (S, F, h, w) uint8; cb/cr: (S, F, ch, cw) or None.  Every stream is
+    stabilized exactly as run_offline would on that stream alone; all streams
+    share one launch per stage.  Returns (out_y, out_cb, out_cr, records) with
+    records of shape (S, F)."""
+    y = np.ascontiguousarray(y, np.uint8)
+    S, F, h, w = y.shape
+    oy = np.empty_like(y)
+    ocb = ocr = None
+    ch = cw = 0
+    if cb is not None:
+        cb = np.ascontiguousarray(cb, np.uint8)
+        cr = np.ascontiguousarray(cr, np.uint8)
+        ch, cw = cb.shape[2:]
+        ocb, ocr = np.empty_like(cb), np.empty_like(cr)
+    rec = np.zeros((S, F), RECORD_DT)
+    c = cfg.c()
+    check(load().stabgpu_stabilize_streams(context(device).handle, _vp(y), _vp(cb), _vp(cr), S, F, w,
+                                           h, cw, ch, C.byref(c), _vp(oy), _vp(ocb), _vp(ocr),
+                                           _vp(rec)))
+    return oy, ocb, ocr, rec
+
+
+def stabilize_streams_host_buffers(ctx, y, cb, cr, S, F, w, h, cw, ch, cfg_c, oy, ocb, ocr, rec):
+    """Raw C-ABI call on caller-owned (e.g. pinned torch) host buffers."""
+    check(load().stabgpu_stabilize_streams(ctx.handle, _vp(y), _vp(cb), _vp(cr), S, F, w, h, cw, ch,
+                                           C.byref(cfg_c), _vp(oy), _vp(ocb), _vp(ocr), _vp(rec)))
+
+
+def stabilize_streams_device(y, cfg: StabConfig, cb=None, cr=None, out_y=None, out_cb=None,
+                             out_cr=None, device: int | None = None, records: bool = True):
+    """Device-resident (S, F, h, w) torch CUDA tensors in and out."""
+    import torch
+
+    S, F, h, w = y.shape
+    dev = y.device.index if device is None else device
+    out_y = torch.empty_like(y) if out_y is None else out_y
+    ch = cw = 0
+    if cb is not None:
+        ch, cw = cb.shape[2:]
+        out_cb = torch.empty_like(cb) if out_cb is None else out_cb
+        out_cr = torch.empty_like(cr) if out_cr is None else out_cr
+    rec = np.zeros((S, F), RECORD_DT) if records else None
+    c = cfg.c()
+    ctx = context(dev)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    check(load().stabgpu_stabilize_streams_device(ctx.handle, _vp(y), _vp(cb), _vp(cr), S, F, w, h,
+                                                  cw, ch, C.byref(c), _vp(out_y), _vp(out_cb),
+                                                  _vp(out_cr), _vp(rec)))
+    return out_y, out_cb, out_cr, rec
+
+
+def streams_of_rank(n_streams: int, rank: int, world: int) -> list[int]:
+    """Round-robin assignment of independent streams to ranks (BASELINE
+    configs[4]).  Streams share nothing, so there is no collective."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return list(range(rank, n_streams, world))
+
+
 # ------------------------------------------------------------- sharding -----
 @dataclass(frozen=True)
 class Shard:

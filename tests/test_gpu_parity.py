@@ -511,3 +511,68 @@ def test_sequence_lk_windows(orc, radius):
     _compare_records(grec, orec)
     mx, cnt = _offby(gy, oy)
     assert mx <= 1 and cnt <= 0.0005 * gy.size
+
+
+# ---- multi-stream Stage I (BASELINE configs[4]) ------------------------------
+def _streams(S, frames, color=True, seed=20):
+    vids = [_data.video(frames=frames, objects=1, color=color, seed=seed + k, jit_t=2.0 + k)
+            for k in range(S)]
+    y = np.stack([v[0] for v in vids])
+    if not color:
+        return y, None, None
+    return y, np.stack([v[1] for v in vids]), np.stack([v[2] for v in vids])
+
+
+@pytest.mark.parametrize("frames,mode,ransac", [(25, "hybrid", 200), (23, "rigid", 100),
+                                                (21, "similarity", 0), (2, "similarity", 0)])
+def test_streams_equal_each_stream_alone(orc, frames, mode, ransac):
+    """Every stream of a batched call is bitwise the one-sequence run of that
+    stream (records and planes), and matches the CPU oracle.  frames=25 takes
+    the strided detection batch (F % R == 0), 23 and 21 the per-stream one."""
+    S = 4
+    y, cb, cr = _streams(S, frames)
+    cfg = _data.small_cfg(_data.MODES[mode], ransac=ransac)
+    gy, gb, gr, rec = pipeline.stabilize_streams(y, cfg, cb, cr)
+    assert rec.shape == (S, frames)
+    for k in range(S):
+        sy, sb, sr, srec = pipeline.stabilize_sequence(y[k], cfg, cb[k], cr[k])
+        assert rec[k].tobytes() == srec.tobytes(), k
+        assert np.array_equal(gy[k], sy) and np.array_equal(gb[k], sb) and np.array_equal(gr[k], sr), k
+    for k in (0, S - 1):
+        oy, ob, orr, o_rec = orc.stabilize_sequence(y[k], cfg, cb[k], cr[k])
+        _compare_records(rec[k], o_rec)
+        mx, cnt = _offby(gy[k], oy)
+        assert mx <= 1 and cnt <= 0.0005 * oy.size
+
+
+def test_streams_grouped_host_path_and_device(monkeypatch):
+    """The host entry point moves groups of streams through two device slots;
+    forcing 2 streams per group (3 groups) must not change a byte, and the
+    device-resident entry point agrees."""
+    import torch
+    S, F = 5, 16
+    y, _, _ = _streams(S, F, color=False, seed=40)
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=50)
+    ay, _, _, arec = pipeline.stabilize_streams(y, cfg)
+    monkeypatch.setenv("STABGPU_STREAMS_PER_GROUP", "2")
+    by, _, _, brec = pipeline.stabilize_streams(y, cfg)
+    assert np.array_equal(ay, by) and arec.tobytes() == brec.tobytes()
+    dy, _, _, drec = pipeline.stabilize_streams_device(torch.from_numpy(y).cuda(), cfg)
+    torch.cuda.synchronize()
+    assert np.array_equal(dy.cpu().numpy(), ay) and drec.tobytes() == arec.tobytes()
+    for k in range(S):
+        sy, _, _, srec = pipeline.stabilize_sequence(y[k], cfg)
+        assert np.array_equal(ay[k], sy) and arec[k].tobytes() == srec.tobytes()
+
+
+def test_streams_errors():
+    y, _, _ = _streams(2, 8, color=False)
+    cfg = _data.small_cfg()
+    with pytest.raises(stab.InvalidInputError):
+        pipeline.stabilize_streams(y[:, :1], cfg)
+    with pytest.raises(stab.InvalidInputError):
+        pipeline.stabilize_streams(y[:0], cfg)
+    bad = _data.small_cfg()
+    bad.smooth_radius = 40
+    with pytest.raises(stab.InvalidConfigError):
+        pipeline.stabilize_streams(y, bad)

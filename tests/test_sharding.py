@@ -34,6 +34,19 @@ def test_shard_ranges_partition(n, R, world):
     assert (own == 1).all()  # each frame composed once
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("S", [1, 7, 256])
+def test_streams_of_rank_round_robin(S, world):
+    got = [pipeline.streams_of_rank(S, g, world) for g in range(world)]
+    flat = sorted(k for part in got for k in part)
+    assert flat == list(range(S))  # every stream on exactly one rank
+    assert max(map(len, got)) - min(map(len, got)) <= 1  # balanced
+    for g, part in enumerate(got):
+        assert all(k % world == g for k in part)
+    with pytest.raises(ValueError):
+        pipeline.streams_of_rank(S, world, world)
+
+
 def _ref_motion(y, first, count, cfg):
     ref = _oracle.reference()
     out = np.zeros(count + 1, pipeline.MOTION_DT)
