@@ -398,6 +398,18 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
     }
 }
 
+// a / b correctly rounded, given y = RN(1/b): q0 = RN(a*y) is within one ulp
+// of a/b, r = a - q0*b is exact in one FMA, and RN(q0 + r*y) = RN(a/b)
+// (Markstein's final correction step; b = det is a normal number bounded away
+// from 0 by the Unconditioned test, and a/b is far from the underflow range).
+// Three DP ops instead of the ~30-instruction IEEE division sequence; the
+// bits equal __ddiv_rn(a, b).
+__device__ __forceinline__ double div_rn_recip(double a, double b, double y) {
+    const double q0 = dmul(a, y);
+    const double r = fma(-q0, b, a);
+    return fma(r, y, q0);
+}
+
 // Pyramidal track_one (flow.cpp:132-227) of up to two trackers that share one
 // template: the patch around (px, py) in frame ft.  Tracker 0 follows the
 // point into frame f0, tracker 1 (when f1 >= 0) into frame f1.  Both walk the
@@ -482,6 +494,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 sys[5] = det;
                 sys[6] = plx;
                 sys[7] = ply;
+                sys[8] = ddiv(1.0, det);  // RN(1/det), for div_rn_recip
             }
             __syncwarp();
         }
@@ -523,8 +536,9 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 const double bx = ldsv(sys + 3) - warp_dsum(sx);
                 const double by = ldsv(sys + 4) - warp_dsum(sy);
                 const double sxx = ldsv(sys), sxy = ldsv(sys + 1), syy = ldsv(sys + 2), sdet = ldsv(sys + 5);
-                const double dx = ddiv(dsub(dmul(syy, bx), dmul(sxy, by)), sdet);
-                const double dy = ddiv(dsub(dmul(sxx, by), dmul(sxy, bx)), sdet);
+                const double rdet = ldsv(sys + 8);
+                const double dx = div_rn_recip(dsub(dmul(syy, bx), dmul(sxy, by)), sdet, rdet);
+                const double dy = div_rn_recip(dsub(dmul(sxx, by), dmul(sxy, bx)), sdet, rdet);
                 vx = dadd(vx, dx);
                 vy = dadd(vy, dy);
                 if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
@@ -683,7 +697,7 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
             // steps this segment may take, parked in shared memory (registers are full)
             const int nst = min(c.R, seg_end(seg, c.F, c.nsps, c.nframes) - 1 - b0);
             if (nst <= 0 || k >= c.npts[seg]) continue;
-            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 8 * 8) = nst;
+            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 9 * 8) = nst;
             __syncwarp();
         } else {
             b0 = seg * c.R;
@@ -731,7 +745,7 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
             q = f;
             f0 = ft - 1;
             if (MS)
-                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 8 * 8) ? ft + 1 : -1;
+                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 9 * 8) ? ft + 1 : -1;
             else
                 f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
         }
@@ -844,7 +858,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
         // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
-        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 8;
+        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 10;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
