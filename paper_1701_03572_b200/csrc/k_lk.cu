@@ -343,6 +343,79 @@ __device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx,
     sy += sy1;
 }
 
+// Correlation sums of one integer window position.  With cur(j, i) the
+// bilinear sample at (cy + j + fy, cx + i + fx) and P the staged pixels,
+//   sum_{j,i} g(j,i) cur(j,i) = lerp_y(lerp_x(S00, S10), lerp_x(S01, S11))
+// where S_uv = sum_{j,i} g(j,i) P(j+v, i+u) (lerp_x(a, b) = a + fx (b - a)).
+// The S_uv depend on the integer position only, so an iteration that stays in
+// the previous iteration's cell (about half of them) reuses them and costs a
+// dozen fp64 ops instead of a window pass.  Lane C <-> pixel column C
+// (0..vw); per gradient row R: S00 += P(R,C) g(R,C), S10 += P(R,C) g(R,C-1),
+// S01 += P(R+1,C) g(R,C), S11 += P(R+1,C) g(R,C-1).  The same products as the
+// bilinear form, summed in another order (tolerance-level, ~1e-13 px).
+// Returns the eight lane partials in s[0..7] = {S00, S10, S01, S11} x {x, y}.
+__device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const double2* ga, int sa, const double2* gb,
+                                          int sb, double* s) {
+    // ga: column C of the gradients (or the zero slot), gb: column C-1 (or the zero slot)
+    const int lane = threadIdx.x & 31;
+    src += lane;
+    double p0 = u2d(src[0]);
+    double a0x = 0.0, a0y = 0.0, b0x = 0.0, b0y = 0.0, a1x = 0.0, a1y = 0.0, b1x = 0.0, b1y = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < vh; ++k) {
+        src += SM_PITCH;
+        const double p1 = u2d(src[0]);
+        const double2 g = ga[0], h = gb[0];
+        a0x = fma(p0, g.x, a0x);
+        a0y = fma(p0, g.y, a0y);
+        b0x = fma(p0, h.x, b0x);
+        b0y = fma(p0, h.y, b0y);
+        a1x = fma(p1, g.x, a1x);
+        a1y = fma(p1, g.y, a1y);
+        b1x = fma(p1, h.x, b1x);
+        b1y = fma(p1, h.y, b1y);
+        ga += sa;
+        gb += sb;
+        p0 = p1;
+    }
+    s[0] = a0x;
+    s[1] = b0x;
+    s[2] = a1x;
+    s[3] = b1x;
+    s[4] = a0y;
+    s[5] = b0y;
+    s[6] = a1y;
+    s[7] = b1y;
+}
+
+// Warp totals of eight values by reduce-scatter (18 shuffles instead of 80):
+// each xor step halves the set a lane carries.  Lane l ends with the total of
+// value (l >> 2) & 7; lanes with l % 4 == 0 store it to out[(l >> 2) & 7].
+__device__ __forceinline__ void warp_dsum8_store(const double* v, double* out) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+    double w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double send = h4 ? v[k] : v[k + 4], keep = h4 ? v[k + 4] : v[k];
+        w[k] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+    double u[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double send = h3 ? w[k] : w[k + 2], keep = h3 ? w[k + 2] : w[k];
+        u[k] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    double z;
+    {
+        const double send = h2 ? u[0] : u[1], keep = h2 ? u[1] : u[0];
+        z = keep + __shfl_xor_sync(FULL, send, 4);
+    }
+    z += __shfl_xor_sync(FULL, z, 2);
+    z += __shfl_xor_sync(FULL, z, 1);
+    if ((lane & 3) == 0) out[(lane >> 2) & 7] = z;
+}
 
 // build_level_patch over the extended (es x es) patch: lane L <-> extended
 // column L (XTRA: es == 33, lane 31 also owns column 32), image rows rolled
@@ -498,9 +571,12 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             }
             __syncwarp();
         }
-        // lanes past the valid window read the zero slot (row step 0)
+        // lanes past the valid window read the zero slot (row step 0); gcolm is
+        // the column left of this lane's (corr_pass)
         const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
         const int gstep = lane < vw ? vw : 0;
+        const double2* gcolm = reinterpret_cast<const double2*>(tg) + (lane >= 1 && lane <= vw ? lane - 1 : vh * vw);
+        const int gstepm = lane >= 1 && lane <= vw ? vw : 0;
         const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
 #pragma unroll 1
         for (int j = 0; j < nt; ++j) {
@@ -513,6 +589,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             double vx = 0.0, vy = 0.0;
             bool diverged = false;
             int sx0 = INT_MIN / 2, sy0 = INT_MIN / 2, soff = 0;  // staged region origin (none yet)
+            int ccx = INT_MIN / 2, ccy = INT_MIN / 2;  // window cell whose S_uv are in sys[10..17]
             for (int k = 0; k < cfg.max_iterations; ++k) {
                 const double qx = dadd(dadd(ldsv(sys + 6), gfx), vx), qy = dadd(dadd(ldsv(sys + 7), gfy), vy);
                 if (!inside(ci, qx, qy)) {
@@ -523,18 +600,28 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 const int qx0 = (int)floor(qx), qy0 = (int)floor(qy);
                 const double cfx = dsub(qx, (double)qx0), cfy = dsub(qy, (double)qy0);
                 const int cx = qx0 - r + iv0, cy = qy0 - r + jv0;  // image origin of the valid window
-                if (cx < sx0 || cy < sy0 || cx + vw + 1 > sx0 + sw || cy + vh + 1 > sy0 + sh) {
-                    sx0 = cx - SM_MARGIN;
-                    sy0 = cy - SM_MARGIN;
+                if (cx != ccx || cy != ccy) {  // new cell: correlation sums S_uv
+                    if (cx < sx0 || cy < sy0 || cx + vw + 1 > sx0 + sw || cy + vh + 1 > sy0 + sh) {
+                        sx0 = cx - SM_MARGIN;
+                        sy0 = cy - SM_MARGIN;
+                        __syncwarp();
+                        soff = stage_block(ci, sx0, sy0, sw, sh, stg);
+                        __syncwarp();
+                    }
+                    double sv[8];
+                    corr_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, gcol, gstep, gcolm, gstepm, sv);
+                    warp_dsum8_store(sv, sys + 10);
                     __syncwarp();
-                    soff = stage_block(ci, sx0, sy0, sw, sh, stg);
-                    __syncwarp();
+                    ccx = cx;
+                    ccy = cy;
                 }
-                // sum(cur * grad); b = T - that
-                double sx = 0.0, sy = 0.0;
-                row_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, cfx, cfy, gcol, gstep, sx, sy);
-                const double bx = ldsv(sys + 3) - warp_dsum(sx);
-                const double by = ldsv(sys + 4) - warp_dsum(sy);
+                // sum(cur * grad) from the cell's S_uv; b = T - that
+                const double tx0 = fma(cfx, ldsv(sys + 11) - ldsv(sys + 10), ldsv(sys + 10));
+                const double tx1 = fma(cfx, ldsv(sys + 13) - ldsv(sys + 12), ldsv(sys + 12));
+                const double ty0 = fma(cfx, ldsv(sys + 15) - ldsv(sys + 14), ldsv(sys + 14));
+                const double ty1 = fma(cfx, ldsv(sys + 17) - ldsv(sys + 16), ldsv(sys + 16));
+                const double bx = ldsv(sys + 3) - fma(cfy, tx1 - tx0, tx0);
+                const double by = ldsv(sys + 4) - fma(cfy, ty1 - ty0, ty0);
                 const double sxx = ldsv(sys), sxy = ldsv(sys + 1), syy = ldsv(sys + 2), sdet = ldsv(sys + 5);
                 const double rdet = ldsv(sys + 8);
                 const double dx = div_rn_recip(dsub(dmul(syy, bx), dmul(sxy, by)), sdet, rdet);
@@ -697,7 +784,7 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
             // steps this segment may take, parked in shared memory (registers are full)
             const int nst = min(c.R, seg_end(seg, c.F, c.nsps, c.nframes) - 1 - b0);
             if (nst <= 0 || k >= c.npts[seg]) continue;
-            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 9 * 8) = nst;
+            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 18 * 8) = nst;
             __syncwarp();
         } else {
             b0 = seg * c.R;
@@ -745,7 +832,7 @@ __global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flo
             q = f;
             f0 = ft - 1;
             if (MS)
-                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 9 * 8) ? ft + 1 : -1;
+                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 18 * 8) ? ft + 1 : -1;
             else
                 f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
         }
@@ -858,7 +945,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
         // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
-        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 10;
+        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -885,7 +972,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
 void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (c.nseg <= 0 || c.max_pts <= 0) return;
     const int side = 2 * cfg.window_radius + 1;
-    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 10;  // doubles (+ the 2x2 system, step count; even: 16 B aligned)
+    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;  // doubles (+ system, S_uv, step count; even: 16 B aligned)
     const int wpc = 4;
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
     const bool multi = c.nsps != c.nseg;  // several streams in the chunk
