@@ -761,11 +761,14 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
 // iterations are counted only then, so the counters match a step-by-step run.
 // MS: several streams per chunk (segment map; step count parked in shared
 // memory).  The one-stream instance keeps the map in kernel parameters.
+// One warp per CTA (20 per SM): the warp's shared region is the CTA's, so its
+// address is uniform and cheap to rematerialise under the 96-register cap.
+constexpr int CH_WPC = 1, CH_CTAS = 20;
 template <bool MS>
-__global__ void __launch_bounds__(128, 5) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
-                                                          unsigned* __restrict__ work, int smem_per_warp) {
+__global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
+                                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = CH_WPC == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* tg = lsm + (size_t)warp * smem_per_warp;
     const int side = 2 * cfg.window_radius + 1;
     uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * (side * side + 1));
@@ -973,7 +976,7 @@ void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t
     if (c.nseg <= 0 || c.max_pts <= 0) return;
     const int side = 2 * cfg.window_radius + 1;
     const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;  // doubles (+ system, S_uv, step count; even: 16 B aligned)
-    const int wpc = 4;
+    const int wpc = CH_WPC;
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
     const bool multi = c.nsps != c.nseg;  // several streams in the chunk
     auto kern = multi ? lk_chain_kernel<true> : lk_chain_kernel<false>;
