@@ -262,7 +262,10 @@ __device__ __forceinline__ int stage_block(const Level& L, int x0, int y0, int s
     const bool words = ((L.w & 3) == 0) && ((reinterpret_cast<uintptr_t>(L.px) & 3) == 0) && x0 >= 0 &&
                        y0 >= 0 && xw + 4 * nw <= L.w && y0 + sh <= L.h;
     if (words) {
-        const int rpp = 32 / nw, lr = lane / nw, lw = lane - lr * nw;
+        // small quotients by reciprocal: floor((a + 0.5) / nw) == a / nw for
+        // 0 <= a <= 32, nw <= 32, with a margin far above the RCP error
+        const float rn = __fdividef(1.0f, (float)nw);
+        const int rpp = (int)(32.5f * rn), lr = (int)(((float)lane + 0.5f) * rn), lw = lane - lr * nw;
         if (lr < rpp) {
             const uint32_t* src = reinterpret_cast<const uint32_t*>(L.px + (size_t)(y0 + lr) * L.w + xw) + lw;
             uint32_t* d = reinterpret_cast<uint32_t*>(dst + lr * SM_PITCH) + lw;
