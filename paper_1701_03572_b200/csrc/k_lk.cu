@@ -304,48 +304,6 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     return v;
 }
 
-// sum over the valid window of cur(j, i) * grad(j, i), lane L <-> column
-// L of the staged block at shared address `src` (row pitch SM_PITCH).  The
-// gradients are a [vh][32] array of {gx, gy} with zeros in columns >= vw, so
-// every lane accumulates unconditionally.
-__device__ __forceinline__ void row_pass(const uint8_t* src, int vh, double cfx, double cfy, const double2* g,
-                                         int gstep, double& sx, double& sy) {
-    // g: this lane's gradient column (row step gstep), or a zero slot (step 0)
-    const int lane = threadIdx.x & 31;
-    src += lane;
-    double hp;
-    {
-        hp = hlerp(src[0], src[1], cfx);
-    }
-    // two partial sums per component (even / odd rows) halve the dependent
-    // DFMA chain; combined once at the end
-    double sx1 = 0.0, sy1 = 0.0;
-    int k = 1;
-#pragma unroll 2
-    for (; k + 1 <= vh; k += 2) {
-        const double h0 = hlerp(src[SM_PITCH], src[SM_PITCH + 1], cfx);
-        const double h1 = hlerp(src[2 * SM_PITCH], src[2 * SM_PITCH + 1], cfx);
-        const double c0 = fma(cfy, h0 - hp, hp), c1 = fma(cfy, h1 - h0, h0);
-        const double2 g0 = g[0], g1 = g[gstep];
-        sx = fma(c0, g0.x, sx);
-        sy = fma(c0, g0.y, sy);
-        sx1 = fma(c1, g1.x, sx1);
-        sy1 = fma(c1, g1.y, sy1);
-        src += 2 * SM_PITCH;
-        g += 2 * gstep;
-        hp = h1;
-    }
-    if (k <= vh) {
-        const double h = hlerp(src[SM_PITCH], src[SM_PITCH + 1], cfx);
-        const double c = fma(cfy, h - hp, hp);
-        const double2 gg = g[0];
-        sx = fma(c, gg.x, sx);
-        sy = fma(c, gg.y, sy);
-    }
-    sx += sx1;
-    sy += sy1;
-}
-
 // Correlation sums of one integer window position.  With cur(j, i) the
 // bilinear sample at (cy + j + fy, cx + i + fx) and P the staged pixels,
 //   sum_{j,i} g(j,i) cur(j,i) = lerp_y(lerp_x(S00, S10), lerp_x(S01, S11))
@@ -391,7 +349,7 @@ __device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const doub
     s[7] = b1y;
 }
 
-// Warp totals of eight values by reduce-scatter (18 shuffles instead of 80):
+// Halved warp totals of eight values by reduce-scatter (18 shuffles instead of 80):
 // each xor step halves the set a lane carries.  Lane l ends with the total of
 // value (l >> 2) & 7; lanes with l % 4 == 0 store it to out[(l >> 2) & 7].
 __device__ __forceinline__ void warp_dsum8_store(const double* v, double* out) {
@@ -417,15 +375,20 @@ __device__ __forceinline__ void warp_dsum8_store(const double* v, double* out) {
     }
     z += __shfl_xor_sync(FULL, z, 2);
     z += __shfl_xor_sync(FULL, z, 1);
-    if ((lane & 3) == 0) out[(lane >> 2) & 7] = z;
+    if ((lane & 3) == 0) out[(lane >> 2) & 7] = 0.5 * z;  // gradients are stored doubled
 }
 
 // build_level_patch over the extended (es x es) patch: lane L <-> extended
 // column L (XTRA: es == 33, lane 31 also owns column 32), image rows rolled
 // through registers.  Writes the template gradients over the valid window
 // (row stride vw) and accumulates G and T = sum(template value * gradient).
+// Only the image rows the valid rows need are visited (jv0 .. jv1+3).  The
+// central differences are stored and summed unscaled (right - left, not
+// 0.5 * (right - left)); scaling by a power of two commutes with every
+// rounding, so G * 1/4, T * 1/2 and the correlation sums * 1/2 are bitwise
+// the scaled results.
 template <bool XTRA>
-__device__ __forceinline__ void template_pass(const uint8_t* src, int es, double fx, double fy, int jv0, int jv1,
+__device__ __forceinline__ void template_pass(const uint8_t* src, double fx, double fy, int jv0, int jv1,
                                               int iv0, int iv1, uint32_t ga, uint32_t grow, double& gxx, double& gxy,
                                               double& gyy, double& tx, double& ty) {
     // src: staged image block of rows yb .. yb+es, columns xb .. xb+es+1
@@ -435,42 +398,49 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, int es, double
     const int ti = lane - 1;  // template column of this lane
     const bool tcol = ti >= iv0 && ti <= iv1;
     ga += (uint32_t)((tcol ? ti - iv0 : 0) * 16);
-    src += lane;
-    double hprev = 0.0, hprevx = 0.0, eA = 0.0, eB = 0.0, eBx = 0.0;
+    src += lane + jv0 * SM_PITCH;
+    // extended rows jv0 (eA) and jv0 + 1 (eB) from image rows jv0 .. jv0+2
+    double hp = hlerp(src[0], src[1], fx), hpx = 0.0;
+    if (XTRA) hpx = hlerp(src[1], src[2], fx);
+    double h = hlerp(src[SM_PITCH], src[SM_PITCH + 1], fx), hx = 0.0;
+    if (XTRA) hx = hlerp(src[SM_PITCH + 1], src[SM_PITCH + 2], fx);
+    double eA = fma(fy, h - hp, hp), eAx = 0.0;
+    if (XTRA) eAx = fma(fy, hx - hpx, hpx);
+    hp = h;
+    hpx = hx;
+    h = hlerp(src[2 * SM_PITCH], src[2 * SM_PITCH + 1], fx);
+    if (XTRA) hx = hlerp(src[2 * SM_PITCH + 1], src[2 * SM_PITCH + 2], fx);
+    double eB = fma(fy, h - hp, hp), eBx = 0.0;
+    if (XTRA) eBx = fma(fy, hx - hpx, hpx);
+    (void)eAx;
+    hp = h;
+    hpx = hx;
+    src += 3 * SM_PITCH;
 #pragma unroll 2
-    for (int k = 0; k <= es; ++k, src += SM_PITCH) {  // image rows yb .. yb+es
-        double hx = 0.0;
-        if (XTRA) {  // lane 31 also carries extended column 32 (from image columns 32, 33)
-            hx = hlerp(src[1], src[2], fx);
-        }
-        const double h = hlerp(src[0], src[1], fx);
-        if (k >= 1) {
-            const double ev = fma(fy, h - hprev, hprev);  // extended row k-1
-            double evx = 0.0;
-            if (XTRA) evx = fma(fy, hx - hprevx, hprevx);
-            if (k >= 3) {  // template row j = k-3 from extended rows k-3, k-2, k-1
-                const int j = k - 3;
-                double right = __shfl_down_sync(FULL, eB, 1);
-                const double left = __shfl_up_sync(FULL, eB, 1);
-                if (XTRA && xtra) right = eBx;
-                const bool ok = tcol && j >= jv0 && j <= jv1;
-                const double dx = ok ? 0.5 * (right - left) : 0.0;
-                const double dy = ok ? 0.5 * (ev - eA) : 0.0;
-                if (ok)
-                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga + (uint32_t)(j - jv0) * grow), "d"(dx),
-                                 "d"(dy));
-                gxx = fma(dx, dx, gxx);
-                gxy = fma(dx, dy, gxy);
-                gyy = fma(dy, dy, gyy);
-                tx = fma(eB, dx, tx);
-                ty = fma(eB, dy, ty);
-            }
-            eA = eB;
-            eB = ev;
-            if (XTRA) eBx = evx;
-        }
-        hprev = h;
-        if (XTRA) hprevx = hx;
+    for (int j = jv0; j <= jv1; ++j, src += SM_PITCH) {  // template row j: extended rows j .. j+2
+        h = hlerp(src[0], src[1], fx);
+        if (XTRA) hx = hlerp(src[1], src[2], fx);
+        const double ev = fma(fy, h - hp, hp);  // extended row j + 2
+        double evx = 0.0;
+        if (XTRA) evx = fma(fy, hx - hpx, hpx);
+        double right = __shfl_down_sync(FULL, eB, 1);
+        const double left = __shfl_up_sync(FULL, eB, 1);
+        if (XTRA && xtra) right = eBx;
+        const double dx = tcol ? right - left : 0.0;  // 2 * gradient
+        const double dy = tcol ? ev - eA : 0.0;
+        if (tcol)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga), "d"(dx), "d"(dy));
+        ga += grow;
+        gxx = fma(dx, dx, gxx);
+        gxy = fma(dx, dy, gxy);
+        gyy = fma(dy, dy, gyy);
+        tx = fma(eB, dx, tx);
+        ty = fma(eB, dy, ty);
+        eA = eB;
+        eB = ev;
+        if (XTRA) eBx = evx;
+        hp = h;
+        if (XTRA) hpx = hx;
     }
 }
 
@@ -544,15 +514,16 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
         const int toff = stage_block(pi, xb, yb, es + 2, es + 1, stg);
         __syncwarp();
         const uint32_t grow = (uint32_t)vw * 16u;  // gradients: [vh][vw] {gx, gy}, then a zero slot
-        if (es > 31) template_pass<true>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
-        else template_pass<false>(stg + toff, es, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
+        if (es > 31) template_pass<true>(stg + toff, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
+        else template_pass<false>(stg + toff, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
         if (lane == 0)
             asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(ga0 + (uint32_t)(vh * vw) * 16u), "d"(0.0));
-        gxx = warp_dsum(gxx);
-        gxy = warp_dsum(gxy);
-        gyy = warp_dsum(gyy);
-        tx = warp_dsum(tx);
-        ty = warp_dsum(ty);
+        // the pass summed unscaled differences: exact power-of-two rescale
+        gxx = 0.25 * warp_dsum(gxx);
+        gxy = 0.25 * warp_dsum(gxy);
+        gyy = 0.25 * warp_dsum(gyy);
+        tx = 0.5 * warp_dsum(tx);
+        ty = 0.5 * warp_dsum(ty);
         __syncwarp();
         {
             const double ht = dmul(0.5, dadd(gxx, gyy)), hd = dmul(0.5, dsub(gxx, gyy));
