@@ -47,6 +47,36 @@ def compose_traffic(spec, planes, frames):
     return (t["dram_bytes_read"] + t["dram_bytes_write"]) * frames / t["frames_per_launch"]
 
 
+def kernel_rooflines(spec, stab_cfg, frames, c, hbm):
+    """HBM fraction of the other bandwidth-class stages (north_star: pyramid,
+    corner and warp kernels).  Algorithmic bytes per SURVEY.md 8(d):
+    K1 = W*H + sum_{l>=1} W_l*H_l per frame (read the base once, write each
+    level once); K2/K3 = 2 (W_roi+4)(H_roi+4) per detection frame (response
+    pass + exact pass; the stage time also holds K4's greedy select)."""
+    if frames <= 0:
+        return None
+    from paper_1701_03572_b200 import stab
+
+    w, h = spec.width, spec.height
+    pyr = w * h
+    lw, lh = w, h
+    for _ in range(1, stab_cfg.flow.max_levels):
+        if lw // 2 < 16 or lh // 2 < 16:  # image_ops.cpp:71
+            break
+        lw, lh = lw // 2, lh // 2
+        pyr += lw * lh
+    roi = stab.detection_roi((h, w), stab_cfg.detect.roi_margin)
+    ndet = (frames - 1 + stab_cfg.flow.redetect_interval - 1) // stab_cfg.flow.redetect_interval
+    det = 2 * (roi.x1 - roi.x0 + 4) * (roi.y1 - roi.y0 + 4)
+    out = {}
+    for name, per, units, ms in (("K1 pyramid", pyr, frames, c[0]), ("K2-K4 detect", det, ndet, c[1])):
+        if ms > 0:
+            gbs = per * units / (ms / 1000.0) / 1e9
+            out[name] = {"alg_bytes_per_unit": per, "units": units, "ms": round(float(ms), 3),
+                         "achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm, 4)}
+    return out
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -310,6 +340,7 @@ def run_ours(args, cfg):
                              "traffic": compose_traffic(spec, planes, sh.own_end - sh.own_begin if world > 1 else n),
                              "peak_source": peak_src,
                              "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms},
+                "kernels": kernel_rooflines(spec, cfg.stab, n if world == 1 else 0, c, hbm),
                 "stage_ms": stages,
                 "gpu_launches": int(launches),
                 "lk": {"iterations": int(ctx.stats().lk_iterations),

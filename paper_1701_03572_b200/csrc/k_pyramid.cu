@@ -6,9 +6,16 @@
 // borders.  All arithmetic is integer, so any evaluation order is exact; the
 // kernel computes only the even columns the vertical pass consumes.
 //
-// One CTA = a 64x16 tile of output pixels of one frame (grid.z = frame).
-// The (2*16+3) x (2*64+3) input window is staged in shared memory with
-// 32-bit loads when the tile is interior and rows are 4-byte aligned.
+// Three kernels, chosen by alignment:
+//  * pyramid_bulk_kernel (rows 16-byte aligned): persistent CTAs stream
+//    (frame, band) items into shared memory with one cp.async.bulk each,
+//    double-buffered behind mbarriers, and filter from shared memory;
+//  * pyramid_stream_kernel (rows 8-byte aligned): register streaming, one
+//    thread per 4 output columns walking a band of rows;
+//  * pyramid_level_kernel (any width): a 64x16 output tile per CTA with its
+//    (2*16+3) x (2*64+3) input window staged in shared memory.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -108,6 +115,7 @@ __device__ __forceinline__ void hrow(uint32_t L, uint32_t X, uint32_t Y, uint32_
     b = (p2a + p2b) + 4u * (m1b + oY) + 6u * eY;
 }
 
+
 __device__ __forceinline__ void srow(const uint8_t* __restrict__ f, int w, int h, int y, int t, int lane, bool act,
                                      bool left_edge, bool right_edge, uint32_t& a, uint32_t& b) {
     y = min(max(y, 0), h - 1);
@@ -168,12 +176,140 @@ __global__ void __launch_bounds__(SPT) pyramid_stream_kernel(const uint8_t* __re
 }
 #undef ROW
 
+// ---------------------------------------------------------------------------
+// Bulk-copy variant (rows 16-byte aligned, w % 16 == 0): a persistent CTA
+// walks (frame, band) items.  A band's input rows are one contiguous range of
+// the frame, so ONE cp.async.bulk per item moves them into shared memory,
+// double-buffered behind an mbarrier: item k+1 streams in while item k is
+// filtered from shared memory.  That keeps ~96 KB per SM in flight, which the
+// register-streaming kernel (a few 8-byte loads per thread) cannot.
+// Threads = (column group of 4 outputs, row group); each row group walks its
+// rows with the same packed 16-bit filter as the streaming kernel.
+constexpr int BT = 512;             // threads per CTA
+constexpr int BBUF = 96 * 1024;     // bytes per input buffer (two per CTA)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void brow(const uint8_t* rp, int cg, int w, uint32_t& a, uint32_t& b) {
+    const uint2 xy = *reinterpret_cast<const uint2*>(rp + 8 * cg);
+    const uint32_t L = cg > 0 ? *reinterpret_cast<const uint32_t*>(rp + 8 * cg - 4) : (xy.x & 0xFFu) * 0x01010101u;
+    const uint32_t R = 8 * cg + 8 < w ? *reinterpret_cast<const uint32_t*>(rp + 8 * cg + 8)
+                                      : (xy.y >> 24) * 0x01010101u;
+    hrow(L, xy.x, xy.y, R, a, b);
+}
+
+__global__ void __launch_bounds__(BT, 1) pyramid_bulk_kernel(const uint8_t* __restrict__ src, size_t src_stride,
+                                                              int w, int h, uint8_t* __restrict__ dst,
+                                                              size_t dst_stride, int frames, int band, int rgroups) {
+    extern __shared__ __align__(128) uint8_t pyr_smem[];
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const int ow = w / 2, oh = h / 2;
+    const int nb = (oh + band - 1) / band;
+    const long long total = (long long)nb * frames;
+    const int tid = threadIdx.x;
+    const int ncg = ow / 4;
+    auto issue = [&](long long item, int buf) {
+        const int f = (int)(item / nb), b = (int)(item - (long long)f * nb);
+        const int oy0 = b * band, oy1 = min(oy0 + band, oh);
+        const int lo = max(0, 2 * oy0 - 2), hi = min(h - 1, 2 * oy1);
+        const uint32_t bytes = (uint32_t)(hi - lo + 1) * (uint32_t)w;
+        const uint32_t bar = su32(&mbar[buf]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                su32(pyr_smem + buf * BBUF)),
+            "l"(src + (size_t)f * src_stride + (size_t)lo * w), "r"(bytes), "r"(bar)
+            : "memory");
+    };
+    long long item = blockIdx.x;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (item < total) issue(item, 0);
+    }
+    __syncthreads();
+    const int per = (band + rgroups - 1) / rgroups;  // output rows per row group
+    for (int k = 0; item < total; ++k, item += gridDim.x) {
+        const int buf = k & 1;
+        if (tid == 0 && item + gridDim.x < total) issue(item + gridDim.x, buf ^ 1);
+        const int f = (int)(item / nb), b = (int)(item - (long long)f * nb);
+        const int oy0 = b * band, oy1 = min(oy0 + band, oh);
+        const int lo = max(0, 2 * oy0 - 2);
+        {
+            const uint32_t bar = su32(&mbar[buf]), phase = (uint32_t)((k >> 1) & 1);
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done)
+                    : "r"(bar), "r"(phase)
+                    : "memory");
+        }
+        const uint8_t* sb = pyr_smem + buf * BBUF;
+        uint8_t* d = dst + (size_t)f * dst_stride;
+        for (int u = tid; u < ncg * rgroups; u += BT) {
+            const int cg = u % ncg, rg = u / ncg;
+            const int r0 = oy0 + rg * per, r1 = min(r0 + per, oy1);
+            if (r0 >= r1) continue;
+#define BROW(Y, A, B) brow(sb + (size_t)(clampi((Y), 0, h - 1) - lo) * w, cg, w, A, B)
+            uint32_t a0, a1, a2, a3, a4, b0, b1, b2, b3, b4;
+            BROW(2 * r0 - 2, a0, b0);
+            BROW(2 * r0 - 1, a1, b1);
+            BROW(2 * r0, a2, b2);
+            BROW(2 * r0 + 1, a3, b3);
+            BROW(2 * r0 + 2, a4, b4);
+            for (int oy = r0;; ) {
+                const uint32_t va = (a0 + a4) + 4u * (a1 + a3) + 6u * a2 + 0x00800080u;
+                const uint32_t vb = (b0 + b4) + 4u * (b1 + b3) + 6u * b2 + 0x00800080u;
+                *reinterpret_cast<uint32_t*>(d + (size_t)oy * ow + 4 * cg) = __byte_perm(va, vb, 0x7531);
+                if (++oy >= r1) break;
+                a0 = a2;
+                b0 = b2;
+                a1 = a3;
+                b1 = b3;
+                a2 = a4;
+                b2 = b4;
+                BROW(2 * oy + 1, a3, b3);
+                BROW(2 * oy + 2, a4, b4);
+            }
+#undef BROW
+        }
+        __syncthreads();  // buffer `buf` is refilled by the issue of iteration k + 1
+    }
+}
+
 }  // namespace
 
 void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst,
                           size_t dst_stride, int frames, cudaStream_t st) {
     const int ow = w / 2, oh = h / 2;
     if (frames <= 0 || ow <= 0 || oh <= 0) return;
+    // bulk-copy kernel: 16-byte aligned rows and frames, 4-byte aligned output rows,
+    // at least 16 input rows (2 * band + 4 with band >= 6) per buffer
+    const char* ver_env = std::getenv("STABGPU_PYR_KERNEL");  // tuning: 0 = register-streaming kernel
+    const int ver = ver_env ? std::atoi(ver_env) : 1;
+    const int band = std::min(oh, (BBUF / w - 4) / 2);
+    const bool bulk = ver != 0 && (w % 16) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+                      (src_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(dst) % 4) == 0 &&
+                      (dst_stride % 4) == 0 && band >= 6;
+    if (bulk) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(pyramid_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * BBUF);
+        }
+        const int ncg = ow / 4;
+        const int rgroups = std::max(1, std::min(band, BT / ncg));
+        const long long items = (long long)((oh + band - 1) / band) * frames;
+        const int grid = (int)std::min<long long>(items, sms);
+        pyramid_bulk_kernel<<<grid, BT, 2 * BBUF, st>>>(src, src_stride, w, h, dst, dst_stride, frames, band,
+                                                        rgroups);
+        return;
+    }
     // streaming kernel: 8-byte aligned rows and frames, 4-byte aligned output rows
     const bool stream = (w % 8) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 8) == 0 &&
                         (src_stride % 8) == 0 && (reinterpret_cast<uintptr_t>(dst) % 4) == 0 &&

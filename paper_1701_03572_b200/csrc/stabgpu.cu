@@ -230,8 +230,10 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
             P.stride[l] = (size_t)P.w[l] * P.h[l];
             DBUF(uint8_t, lv, ("pyr" + std::to_string(l)).c_str(), P.stride[l] * nF);
             P.lvl[l] = lv;
-            launch_pyramid_level(P.lvl[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1], lv,
-                                 P.stride[l], nF, st);
+        }
+        for (int l = 1; l < P.levels; ++l) {
+            launch_pyramid_level(P.lvl[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1],
+                                 const_cast<uint8_t*>(P.lvl[l]), P.stride[l], nF, st);
             ++ctx->stats.launches;
         }
         TRY(check_launch("pyramid"));
@@ -1757,3 +1759,10 @@ int stabgpu_interframe_sse(stabgpu_ctx* ctx, const uint8_t* y, int n, int w, int
 
 }  // extern "C"
 
+
+// Profiling hook (tools/probe_pyramid.py), not part of the public ABI: one K1
+// level over a frame batch on a caller stream, device pointers.
+extern "C" __attribute__((visibility("default"))) void stabgpu_debug_pyramid_level(
+    const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst, size_t dst_stride, int frames, void* stream) {
+    stabgpu::launch_pyramid_level(src, src_stride, w, h, dst, dst_stride, frames, (cudaStream_t)stream);
+}

@@ -47,6 +47,31 @@ def test_pyramid_bitexact(orc, f, name, levels):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("w,h,n", [(1920, 1080, 5), (352, 291, 37), (160, 37, 300), (3840, 64, 3)])
+def test_pyramid_level_batches(orc, w, h, n):
+    """K1 over a frame batch (the Stage I layout): the bulk-copy kernel's
+    bands, row groups, odd heights and item counts beyond the grid."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1701_03572_b200 import _lib
+
+    rng = np.random.default_rng(w * h + n)
+    frames = rng.integers(0, 256, size=(n, h, w), dtype=np.uint8)
+    frames[0] = 255
+    src = torch.from_numpy(frames).cuda()
+    ow, oh = w // 2, h // 2
+    dst = torch.empty((n, oh, ow), dtype=torch.uint8, device="cuda")
+    _lib.load().stabgpu_debug_pyramid_level(C.c_void_p(src.data_ptr()), C.c_size_t(w * h), w, h,
+                                            C.c_void_p(dst.data_ptr()), C.c_size_t(ow * oh), n,
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    got = dst.cpu().numpy()
+    for i in sorted({0, 1, n // 2, n - 1}):
+        _, ref = orc.build_pyramid(frames[i], 2)
+        assert np.array_equal(got[i], ref[1]), i
+
+
 @pytest.mark.parametrize("f,name", FRAMES)
 def test_gradients_response_bitexact(orc, f, name):
     gx, gy = stab.gradients(f)
