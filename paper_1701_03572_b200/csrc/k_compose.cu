@@ -1107,35 +1107,59 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     fxv[j] = (float)__ldg(T.cfx + c);
                 }
                 const bool xin = __all_sync(FULL, x1[0] == x0[0] + 1 && x1[1] == x0[1] + 1);
+                const float2 fx2 = make_float2(fxv[0], fxv[1]);
+                // horizontal lerps of W row `row` at the lane's two columns
+                // (crop_resize's top / bot, image_ops.cpp:151-156)
+                auto hl = [&](int row) {
+                    const uint8_t* rp = wt + (row - v0) * WTW;
+                    uint32_t a0, b0, a1, b1;
+                    if (xin) {
+                        a0 = rp[x0[0]];
+                        b0 = rp[x0[0] + 1];
+                        a1 = rp[x0[1]];
+                        b1 = rp[x0[1] + 1];
+                    } else {
+                        a0 = rp[x0[0]];
+                        b0 = rp[x1[0]];
+                        a1 = rp[x0[1]];
+                        b1 = rp[x1[1]];
+                    }
+                    const float2 fa = make_float2(b256(a0), b256(a1)), fb = make_float2(b256(b0), b256(b1));
+                    return __ffma2_rn(fx2, sub2(fb, fa), fa);
+                };
+                // each warp walks a contiguous run of output rows: cy0 advances by
+                // 0 or 1 per row (step < 1), so a row's top lerp is the previous
+                // row's bottom (or both are reused) — ~0.92 new lerps per row
                 int qn = 0;
-                const size_t step = (size_t)(NT / 32) * w;
-                uint8_t* py = oy + (size_t)warp * w;
-                int ncy = __ldg(T.cy0 + Y0 + min(warp, ny - 1));
-                double ncfy = __ldg(T.cfy + Y0 + min(warp, ny - 1));
-                for (int r = warp; r < ny; r += NT / 32, py += step) {
+                const int per = (ny + NW - 1) / NW;
+                const int rb = warp * per, re = min(rb + per, ny);
+                uint8_t* py = oy + (size_t)rb * w;
+                int trow = -1;
+                float2 top = make_float2(0.f, 0.f), bot = top;
+                int ncy = __ldg(T.cy0 + Y0 + min(rb, ny - 1));
+                double ncfy = __ldg(T.cfy + Y0 + min(rb, ny - 1));
+                for (int r = rb; r < re; ++r, py += w) {
                     const int cy = ncy;
                     const float fy = (float)ncfy;
-                    ncy = __ldg(T.cy0 + Y0 + min(r + NT / 32, ny - 1));
-                    ncfy = __ldg(T.cfy + Y0 + min(r + NT / 32, ny - 1));
-                    const uint8_t* row0 = wt + (cy - v0) * WTW;
-                    bool b0, b1;
-                    uint32_t pr;
-                    if (xin && cy + 1 <= h - 1) {  // x1 = x0 + 1, y1 = y0 + 1: immediate offsets
-                        const uint8_t* p0 = row0 + x0[0];
-                        const uint8_t* p1 = row0 + x0[1];
-                        pr = blend2_bad(Q4{p0[0], p0[1], p0[WTW], p0[WTW + 1]}, Q4{p1[0], p1[1], p1[WTW], p1[WTW + 1]},
-                                        make_float2(fxv[0], fxv[1]), make_float2(fy, fy), b0, b1);
-                    } else {
-                        const uint8_t* row1 = wt + (min(cy + 1, h - 1) - v0) * WTW;
-                        pr = blend2_bad(Q4{row0[x0[0]], row0[x1[0]], row1[x0[0]], row1[x1[0]]},
-                                        Q4{row0[x0[1]], row0[x1[1]], row1[x0[1]], row1[x1[1]]},
-                                        make_float2(fxv[0], fxv[1]), make_float2(fy, fy), b0, b1);
+                    ncy = __ldg(T.cy0 + Y0 + min(r + 1, ny - 1));
+                    ncfy = __ldg(T.cfy + Y0 + min(r + 1, ny - 1));
+                    if (cy != trow) {
+                        if (trow >= 0 && cy == trow + 1) {
+                            top = bot;  // the previous bottom row (min(trow + 1, h - 1) = cy) is this top row
+                        } else {
+                            top = hl(cy);
+                        }
+                        bot = hl(min(cy + 1, h - 1));
+                        trow = cy;
                     }
-                    const uint32_t a0 = pr & 0xFF, a1 = pr >> 8;
+                    const float2 v = __ffma2_rn(make_float2(fy, fy), sub2(bot, top), top);
+                    const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
+                    const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
+                    const uint32_t a0 = __float_as_uint(m.x) & 0xFFu, a1 = __float_as_uint(m.y) & 0xFFu;
                     if (c0) stg_u8(py, a0);
                     if (c1) stg_u8(py + 32, a1);
-                    b0 = b0 && c0;
-                    b1 = b1 && c1;
+                    const bool b0 = c0 && fabsf(dv.x) > 0.5f - VGUARD;
+                    const bool b1 = c1 && fabsf(dv.y) > 0.5f - VGUARD;
                     if (__any_sync(FULL, b0 || b1)) {
                         const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
                         wq_push(S.wq[warp], qn, b0, it);
@@ -1144,15 +1168,15 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 }
                 if (__any_sync(FULL, qn > 0)) {
                     __syncwarp();
-                    const int nq = qn <= QW ? qn : ((ny - warp + NW - 1) / NW) * nx;
+                    const int nq = qn <= QW ? qn : (re - rb) * nx;
                     for (int i = lane; i < nq; i += 32) {
                         int r, c;
                         if (qn <= QW) {
                             const unsigned it = S.wq[warp][i];
                             r = (int)(it >> 8);
                             c = (int)(it & 0xFF);
-                        } else {
-                            r = warp + NW * (i / nx);
+                        } else {  // queue overflow: every pixel of this warp's rows
+                            r = rb + i / nx;
                             c = i % nx;
                         }
                         stg_u8(oy + (size_t)r * w + c - lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
