@@ -615,6 +615,7 @@ __global__ void crop_kernel(const uint8_t* __restrict__ src, int w, int h, CropG
 // instruction on sm_100).
 constexpr int BW = 96, BH = 144;
 constexpr int TTH = 128;           // TMA path output tile: TW x TTH
+static_assert((TTH + NW - 1) / NW <= 32, "the crop loop shuffles one row table entry per lane");
 constexpr int TWTH = 132;          // its W tile rows (<= 130 used)
 constexpr int QW = 64;  // per-warp exact-path queue
 
@@ -851,9 +852,60 @@ __device__ __noinline__ uint32_t crop_exact_tile(const uint8_t* wt, const Tables
     return round_u8(dadd(top, dmul(T.cfy[Y], dsub(bot, top))));
 }
 
+// ---- 32.32 coordinates for the row loops --------------------------------
+// The row loops carry coordinates as 32.32 fixed point with the integer part
+// biased by -1 (hi word = ix - 1, lo word = the fraction), converted once per
+// tile from the 16.48 tables: every step is one 64-bit add and the integer
+// part / fraction are register halves.  Error against the reference
+// coordinate: <= 2^-32 per conversion, <= 2^-32 per 8-row step (16 per
+// tile), plus the tables' ~1e-13: < 5e-9 px.
+//
+// Interior fast path: when the biased integer part lies in [0, w-4] (ix in
+// [1, w-3]) the reference's sample is in bounds with x1 = x0 + 1 whichever
+// side of an integer the exact coordinate falls, and the bilinear blend is
+// continuous across that integer (fraction ~0 with x0 = ix equals fraction
+// ~1 with x0 = ix - 1 to within 255 * 5e-9), so no coordinate guard is
+// needed: only the blended value's .5-tie guard (VGUARD) decides.  A warp row
+// with any valid non-interior pixel takes the guarded decode (decode32).
+constexpr long long ONE32 = 1LL << 32;
+
+__device__ __forceinline__ long long to32(long long x48) { return (x48 >> 16) - ONE32; }
+
+__device__ __forceinline__ int hi32(long long x) { return (int)(x >> 32); }
+
+// Guarded decode of a biased 32.32 point (the rows with frame-edge pixels).
+__device__ __forceinline__ Pt decode32(long long X, long long Y, unsigned limx, unsigned limy, bool valid,
+                                       bool& bad) {
+    Pt t;
+    const uint32_t fxs = (uint32_t)X, fys = (uint32_t)Y;
+    bad = valid && ((fxs + GUARD) < 2 * GUARD || (fys + GUARD) < 2 * GUARD);
+    t.ix = hi32(X) + 1;
+    t.iy = hi32(Y) + 1;
+    t.inb = valid && (unsigned)t.ix <= limx && (unsigned)t.iy <= limy;
+    t.fx = frac_f(fxs);
+    t.fy = frac_f(fys);
+    return t;
+}
+
+// interior test on the biased integer parts (limx = w - 2: biased <= w - 4)
+__device__ __forceinline__ bool inner32(long long X, long long Y, unsigned limx, unsigned limy) {
+    return ((unsigned)hi32(X) <= limx - 2) & ((unsigned)hi32(Y) <= limy - 2);
+}
+
+template <typename P>
+__device__ __forceinline__ Q4 fetch4i(P src, int pitch, int ob1, long long X, long long Y, bool valid) {
+    const int o = valid ? hi32(Y) * pitch + hi32(X) + ob1 : 0;  // ob1 = obase + pitch + 1
+    return Q4{src[o], src[o + 1], src[o + pitch], src[o + pitch + 1]};
+}
+
+__device__ __forceinline__ float2 frac2(long long X0, long long X1) {
+    return make_float2(frac_f((uint32_t)X0), frac_f((uint32_t)X1));
+}
+
 // Luma W rows of a tile (warp per row, lane per column) into the shared W
 // tile; src is the staged TMA box (pitch BW, obase = -(lby*BW + lbx)) or the
-// global frame (pitch w, obase 0).  Returns the warp's queue length.
+// global frame (pitch w, obase 0).  Table and step inputs are 16.48.
+// Returns the warp's queue length.
 template <typename P>
 __device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long long* __restrict__ rxf,
                                         const long long* __restrict__ ryf, uint32_t wsm, int nu, int nv,
@@ -862,25 +914,41 @@ __device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long 
                                         unsigned* q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool v0 = lane < nu, v1 = lane + 32 < nu, has2 = nu > 64;
+    const int ob1 = obase + pitch + 1;
     int qn = 0;
     uint32_t row = wsm + warp * WTW + lane;
-    // the warp's first row start from the table, then exact 16.48 steps of
-    // 8 rows (d rx/dv = sn, d ry/dv = c: the error stays ~1e-13 px)
-    long long SXr = __ldg(rxf + min(warp, nv - 1)) + uCF, SYr = __ldg(ryf + min(warp, nv - 1)) - uSN;
-    for (int r = warp; r < nv; r += NT / 32, row += (NT / 32) * WTW, SXr += RSX, SYr += RSY) {
-        bool b0, b1, b2 = false, e0, e1;
-        const Pt t0 = decode(SXr, SYr, limx, limy, v0, b0);
-        const Pt t1 = decode(SXr + CF32, SYr - SN32, limx, limy, v1, b1);
-        const uint32_t pr = blend2_bad(fetch4(src, pitch, obase, t0), fetch4(src, pitch, obase, t1),
-                                       make_float2(t0.fx, t1.fx), make_float2(t0.fy, t1.fy), e0, e1);
-        b0 = b0 || (t0.inb && e0);
-        b1 = b1 || (t1.inb && e1);
-        if (v0) sts_u8(row, t0.inb ? (pr & 0xFF) : 0u);
-        if (v1) sts_u8(row + 32, t1.inb ? (pr >> 8) : 0u);
+    // the warp's first row start from the table, then 8-row steps
+    long long SX = to32(__ldg(rxf + min(warp, nv - 1)) + uCF), SY = to32(__ldg(ryf + min(warp, nv - 1)) - uSN);
+    const long long cx = CF32 >> 16, cy = SN32 >> 16, rsx = RSX >> 16, rsy = RSY >> 16;
+    for (int r = warp; r < nv; r += NW, row += NW * WTW, SX += rsx, SY += rsy) {
+        const long long X1 = SX + cx, Y1 = SY - cy;
+        bool b0, b1, b2 = false;
+        if (__all_sync(0xFFFFFFFFu, (!v0 | inner32(SX, SY, limx, limy)) & (!v1 | inner32(X1, Y1, limx, limy)))) {
+            const uint32_t pr = blend2_bad(fetch4i(src, pitch, ob1, SX, SY, v0), fetch4i(src, pitch, ob1, X1, Y1, v1),
+                                           frac2(SX, X1), frac2(SY, Y1), b0, b1);
+            b0 = b0 && v0;
+            b1 = b1 && v1;
+            if (v0) sts_u8(row, pr & 0xFF);
+            if (v1) sts_u8(row + 32, pr >> 8);
+        } else {
+            bool e0, e1;
+            const Pt t0 = decode32(SX, SY, limx, limy, v0, b0);
+            const Pt t1 = decode32(X1, Y1, limx, limy, v1, b1);
+            const uint32_t pr = blend2_bad(fetch4(src, pitch, obase, t0), fetch4(src, pitch, obase, t1),
+                                           make_float2(t0.fx, t1.fx), make_float2(t0.fy, t1.fy), e0, e1);
+            b0 = b0 || (t0.inb && e0);
+            b1 = b1 || (t1.inb && e1);
+            if (v0) sts_u8(row, t0.inb ? (pr & 0xFF) : 0u);
+            if (v1) sts_u8(row + 32, t1.inb ? (pr >> 8) : 0u);
+        }
         if (has2) {  // rare third half (nu = 65 .. 66)
             const bool v2 = lane + 64 < nu;
-            const uint32_t a2 = px1(src, pitch, obase, SXr + 2 * CF32, SYr - 2 * SN32, limx, limy, v2, 0u, b2);
-            if (v2) sts_u8(row + 64, a2);
+            const Pt t2 = decode32(SX + 2 * cx, SY - 2 * cy, limx, limy, v2, b2);
+            const int o = t2.inb ? t2.iy * pitch + t2.ix + obase : 0;
+            bool e2 = false;
+            const uint32_t a2 = blend_bad(src[o], src[o + 1], src[o + pitch], src[o + pitch + 1], t2.fx, t2.fy, e2);
+            b2 = b2 || (t2.inb && e2);
+            if (v2) sts_u8(row + 64, t2.inb ? a2 : 0u);
         }
         if (__any_sync(0xFFFFFFFFu, b0 || b1 || b2)) {
             const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
@@ -893,7 +961,8 @@ __device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long 
 }
 
 // Chroma rows of a tile straight to the output planes (both planes share
-// one coordinate per pixel).  Returns the warp's queue length.
+// one coordinate per pixel).  Table and step inputs are 16.48.  Returns the
+// warp's queue length.
 template <typename P>
 __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, const long long* __restrict__ pxf,
                                              const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int cw,
@@ -902,22 +971,38 @@ __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, c
                                              unsigned limy, unsigned* q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool v0 = lane < nx, v1 = lane + 32 < nx;
+    const int ob1 = obase + pitch + 1;
     int qn = 0;
-    const size_t step = (size_t)(NT / 32) * cw;
+    const size_t step = (size_t)NW * cw;
     uint8_t* pb = ob + (size_t)warp * cw + lane;
     uint8_t* pr = orr + (size_t)warp * cw + lane;
-    long long PXr = __ldg(pxf + min(warp, ny - 1)) + xKX, PYr = __ldg(pyf + min(warp, ny - 1)) + xKY;
-    for (int r = warp; r < ny; r += NT / 32, pb += step, pr += step, PXr += RSX, PYr += RSY) {
+    long long PX = to32(__ldg(pxf + min(warp, ny - 1)) + xKX), PY = to32(__ldg(pyf + min(warp, ny - 1)) + xKY);
+    const long long kx = KX32 >> 16, ky = KY32 >> 16, rsx = RSX >> 16, rsy = RSY >> 16;
+    for (int r = warp; r < ny; r += NW, pb += step, pr += step, PX += rsx, PY += rsy) {
+        const long long X1 = PX + kx, Y1 = PY + ky;
         bool b0, b1, e0, e1, e2, e3;
-        const Pt t0 = decode(PXr, PYr, limx, limy, v0, b0);
-        const Pt t1 = decode(PXr + KX32, PYr + KY32, limx, limy, v1, b1);
-        const uint32_t p0 = blend2_bad(fetch4(s1, pitch, obase, t0), fetch4(s2, pitch, obase, t0),
-                                       make_float2(t0.fx, t0.fx), make_float2(t0.fy, t0.fy), e0, e1);
-        const uint32_t p1 = blend2_bad(fetch4(s1, pitch, obase, t1), fetch4(s2, pitch, obase, t1),
-                                       make_float2(t1.fx, t1.fx), make_float2(t1.fy, t1.fy), e2, e3);
-        b0 = b0 || (t0.inb && (e0 || e1));
-        b1 = b1 || (t1.inb && (e2 || e3));
-        const uint32_t a0 = t0.inb ? p0 : 0x8080u, a1 = t1.inb ? p1 : 0x8080u;
+        uint32_t a0, a1;
+        if (__all_sync(0xFFFFFFFFu, (!v0 | inner32(PX, PY, limx, limy)) & (!v1 | inner32(X1, Y1, limx, limy)))) {
+            const float fx0 = frac_f((uint32_t)PX), fy0 = frac_f((uint32_t)PY);
+            const float fx1 = frac_f((uint32_t)X1), fy1 = frac_f((uint32_t)Y1);
+            a0 = blend2_bad(fetch4i(s1, pitch, ob1, PX, PY, v0), fetch4i(s2, pitch, ob1, PX, PY, v0),
+                            make_float2(fx0, fx0), make_float2(fy0, fy0), e0, e1);
+            a1 = blend2_bad(fetch4i(s1, pitch, ob1, X1, Y1, v1), fetch4i(s2, pitch, ob1, X1, Y1, v1),
+                            make_float2(fx1, fx1), make_float2(fy1, fy1), e2, e3);
+            b0 = v0 && (e0 || e1);
+            b1 = v1 && (e2 || e3);
+        } else {
+            const Pt t0 = decode32(PX, PY, limx, limy, v0, b0);
+            const Pt t1 = decode32(X1, Y1, limx, limy, v1, b1);
+            const uint32_t p0 = blend2_bad(fetch4(s1, pitch, obase, t0), fetch4(s2, pitch, obase, t0),
+                                           make_float2(t0.fx, t0.fx), make_float2(t0.fy, t0.fy), e0, e1);
+            const uint32_t p1 = blend2_bad(fetch4(s1, pitch, obase, t1), fetch4(s2, pitch, obase, t1),
+                                           make_float2(t1.fx, t1.fx), make_float2(t1.fy, t1.fy), e2, e3);
+            b0 = b0 || (t0.inb && (e0 || e1));
+            b1 = b1 || (t1.inb && (e2 || e3));
+            a0 = t0.inb ? p0 : 0x8080u;
+            a1 = t1.inb ? p1 : 0x8080u;
+        }
         if (v0) {
             stg_u8(pb, a0 & 0xFF);
             stg_u8(pr, a0 >> 8);
@@ -1127,25 +1212,25 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     const float2 fa = make_float2(b256(a0), b256(a1)), fb = make_float2(b256(b0), b256(b1));
                     return __ffma2_rn(fx2, sub2(fb, fa), fa);
                 };
-                // each warp walks a contiguous run of output rows: cy0 advances by
-                // 0 or 1 per row (step < 1), so a row's top lerp is the previous
-                // row's bottom (or both are reused) — ~0.92 new lerps per row
+                // each warp walks a contiguous run of output rows (<= 32): cy0
+                // advances by 0 or 1 per row (step < 1), so the new bottom lerp is
+                // the only one computed per row; a row with the same cy0 keeps
+                // both.  The run's cy0 / fy come from one load per lane + shuffles.
                 int qn = 0;
                 const int per = (ny + NW - 1) / NW;
                 const int rb = warp * per, re = min(rb + per, ny);
                 uint8_t* py = oy + (size_t)rb * w;
-                int trow = -1;
-                float2 top = make_float2(0.f, 0.f), bot = top;
-                int ncy = __ldg(T.cy0 + Y0 + min(rb, ny - 1));
-                double ncfy = __ldg(T.cfy + Y0 + min(rb, ny - 1));
+                const int myr = min(rb + lane, ny - 1);
+                const int mycy = __ldg(T.cy0 + Y0 + myr);
+                const float myfy = (float)__ldg(T.cfy + Y0 + myr);
+                int trow = __shfl_sync(FULL, mycy, 0);
+                float2 top = hl(trow), bot = hl(min(trow + 1, h - 1));
                 for (int r = rb; r < re; ++r, py += w) {
-                    const int cy = ncy;
-                    const float fy = (float)ncfy;
-                    ncy = __ldg(T.cy0 + Y0 + min(r + 1, ny - 1));
-                    ncfy = __ldg(T.cfy + Y0 + min(r + 1, ny - 1));
+                    const int cy = __shfl_sync(FULL, mycy, r - rb);
+                    const float fy = __shfl_sync(FULL, myfy, r - rb);
                     if (cy != trow) {
-                        if (trow >= 0 && cy == trow + 1) {
-                            top = bot;  // the previous bottom row (min(trow + 1, h - 1) = cy) is this top row
+                        if (cy == trow + 1) {  // the previous bottom row min(trow + 1, h - 1) = cy
+                            top = bot;
                         } else {
                             top = hl(cy);
                         }
@@ -1158,9 +1243,9 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     const uint32_t a0 = __float_as_uint(m.x) & 0xFFu, a1 = __float_as_uint(m.y) & 0xFFu;
                     if (c0) stg_u8(py, a0);
                     if (c1) stg_u8(py + 32, a1);
-                    const bool b0 = c0 && fabsf(dv.x) > 0.5f - VGUARD;
-                    const bool b1 = c1 && fabsf(dv.y) > 0.5f - VGUARD;
-                    if (__any_sync(FULL, b0 || b1)) {
+                    const bool b0 = c0 & (fabsf(dv.x) > 0.5f - VGUARD);
+                    const bool b1 = c1 & (fabsf(dv.y) > 0.5f - VGUARD);
+                    if (__any_sync(FULL, b0 | b1)) {
                         const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
                         wq_push(S.wq[warp], qn, b0, it);
                         wq_push(S.wq[warp], qn, b1, it + 32);
