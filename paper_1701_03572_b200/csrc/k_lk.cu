@@ -310,34 +310,36 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 // where S_uv = sum_{j,i} g(j,i) P(j+v, i+u) (lerp_x(a, b) = a + fx (b - a)).
 // The S_uv depend on the integer position only, so an iteration that stays in
 // the previous iteration's cell (about half of them) reuses them and costs a
-// dozen fp64 ops instead of a window pass.  Lane C <-> pixel column C
-// (0..vw); per gradient row R: S00 += P(R,C) g(R,C), S10 += P(R,C) g(R,C-1),
-// S01 += P(R+1,C) g(R,C), S11 += P(R+1,C) g(R,C-1).  The same products as the
-// bilinear form, summed in another order (tolerance-level, ~1e-13 px).
+// dozen fp64 ops instead of a window pass.  Lane C <-> gradient column C
+// (0..vw-1; lanes past the window read the zero slot); per gradient row R:
+// S00 += P(R,C) g(R,C), S10 += P(R,C+1) g(R,C), S01 += P(R+1,C) g(R,C),
+// S11 += P(R+1,C+1) g(R,C).  Each lane loads its gradient once per row (one
+// 16-byte LDS) and two pixel bytes; the pixel row R+1 carries over as row R.
+// The same products as the bilinear form, summed in another order
+// (tolerance-level, ~1e-13 px).
 // Returns the eight lane partials in s[0..7] = {S00, S10, S01, S11} x {x, y}.
-__device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const double2* ga, int sa, const double2* gb,
-                                          int sb, double* s) {
-    // ga: column C of the gradients (or the zero slot), gb: column C-1 (or the zero slot)
+__device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const double2* ga, int sa, double* s) {
+    // ga: column C of the gradients (or the zero slot, row step sa = 0)
     const int lane = threadIdx.x & 31;
     src += lane;
-    double p0 = u2d(src[0]);
+    double p0 = u2d(src[0]), q0 = u2d(src[1]);
     double a0x = 0.0, a0y = 0.0, b0x = 0.0, b0y = 0.0, a1x = 0.0, a1y = 0.0, b1x = 0.0, b1y = 0.0;
 #pragma unroll 2
     for (int k = 0; k < vh; ++k) {
         src += SM_PITCH;
-        const double p1 = u2d(src[0]);
-        const double2 g = ga[0], h = gb[0];
+        const double p1 = u2d(src[0]), q1 = u2d(src[1]);
+        const double2 g = ga[0];
         a0x = fma(p0, g.x, a0x);
         a0y = fma(p0, g.y, a0y);
-        b0x = fma(p0, h.x, b0x);
-        b0y = fma(p0, h.y, b0y);
+        b0x = fma(q0, g.x, b0x);
+        b0y = fma(q0, g.y, b0y);
         a1x = fma(p1, g.x, a1x);
         a1y = fma(p1, g.y, a1y);
-        b1x = fma(p1, h.x, b1x);
-        b1y = fma(p1, h.y, b1y);
+        b1x = fma(q1, g.x, b1x);
+        b1y = fma(q1, g.y, b1y);
         ga += sa;
-        gb += sb;
         p0 = p1;
+        q0 = q1;
     }
     s[0] = a0x;
     s[1] = b0x;
@@ -545,12 +547,9 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             }
             __syncwarp();
         }
-        // lanes past the valid window read the zero slot (row step 0); gcolm is
-        // the column left of this lane's (corr_pass)
+        // lanes past the valid window read the zero slot (row step 0)
         const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
         const int gstep = lane < vw ? vw : 0;
-        const double2* gcolm = reinterpret_cast<const double2*>(tg) + (lane >= 1 && lane <= vw ? lane - 1 : vh * vw);
-        const int gstepm = lane >= 1 && lane <= vw ? vw : 0;
         const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
 #pragma unroll 1
         for (int j = 0; j < nt; ++j) {
@@ -583,7 +582,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                         __syncwarp();
                     }
                     double sv[8];
-                    corr_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, gcol, gstep, gcolm, gstepm, sv);
+                    corr_pass(stg + soff + (cy - sy0) * SM_PITCH + (cx - sx0), vh, gcol, gstep, sv);
                     warp_dsum8_store(sv, sys + 10);
                     __syncwarp();
                     ccx = cx;
