@@ -181,12 +181,11 @@ __global__ void __launch_bounds__(SPT) pyramid_stream_kernel(const uint8_t* __re
 // walks (frame, band) items.  A band's input rows are one contiguous range of
 // the frame, so ONE cp.async.bulk per item moves them into shared memory,
 // double-buffered behind an mbarrier: item k+1 streams in while item k is
-// filtered from shared memory.  That keeps ~96 KB per SM in flight, which the
+// filtered from shared memory.  That keeps ~96 KB per SM in flight (two CTAs of two 48 KB buffers, or one of two 96 KB buffers for rows wider than ~3 KB), which the
 // register-streaming kernel (a few 8-byte loads per thread) cannot.
 // Threads = (column group of 4 outputs, row group); each row group walks its
 // rows with the same packed 16-bit filter as the streaming kernel.
-constexpr int BT = 512;             // threads per CTA
-constexpr int BBUF = 96 * 1024;     // bytes per input buffer (two per CTA)
+// BT threads per CTA, BBUF bytes per input buffer (two per CTA), MINB CTAs per SM
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -198,7 +197,8 @@ __device__ __forceinline__ void brow(const uint8_t* rp, int cg, int w, uint32_t&
     hrow(L, xy.x, xy.y, R, a, b);
 }
 
-__global__ void __launch_bounds__(BT, 1) pyramid_bulk_kernel(const uint8_t* __restrict__ src, size_t src_stride,
+template <int BT, int BBUF, int MINB>
+__global__ void __launch_bounds__(BT, MINB) pyramid_bulk_kernel(const uint8_t* __restrict__ src, size_t src_stride,
                                                               int w, int h, uint8_t* __restrict__ dst,
                                                               size_t dst_stride, int frames, int band, int rgroups) {
     extern __shared__ __align__(128) uint8_t pyr_smem[];
@@ -280,6 +280,27 @@ __global__ void __launch_bounds__(BT, 1) pyramid_bulk_kernel(const uint8_t* __re
     }
 }
 
+template <int BT, int BBUF, int MINB>
+void launch_bulk(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst, size_t dst_stride, int frames,
+                 cudaStream_t st) {
+    const int ow = w / 2, oh = h / 2;
+    const int band = std::min(oh, (BBUF / w - 4) / 2);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(pyramid_bulk_kernel<BT, BBUF, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * BBUF);
+    }
+    const int ncg = ow / 4;
+    const int rgroups = std::max(1, std::min(band, BT / ncg));
+    const long long items = (long long)((oh + band - 1) / band) * frames;
+    const int grid = (int)std::min<long long>(items, (long long)sms * MINB);
+    pyramid_bulk_kernel<BT, BBUF, MINB>
+        <<<grid, BT, 2 * BBUF, st>>>(src, src_stride, w, h, dst, dst_stride, frames, band, rgroups);
+}
+
 }  // namespace
 
 void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst,
@@ -290,24 +311,17 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
     // at least 16 input rows (2 * band + 4 with band >= 6) per buffer
     const char* ver_env = std::getenv("STABGPU_PYR_KERNEL");  // tuning: 0 = register-streaming kernel
     const int ver = ver_env ? std::atoi(ver_env) : 1;
-    const int band = std::min(oh, (BBUF / w - 4) / 2);
+    const int band = std::min(oh, (96 * 1024 / w - 4) / 2);  // the largest buffer below
     const bool bulk = ver != 0 && (w % 16) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
                       (src_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(dst) % 4) == 0 &&
                       (dst_stride % 4) == 0 && band >= 6;
     if (bulk) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(pyramid_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * BBUF);
-        }
-        const int ncg = ow / 4;
-        const int rgroups = std::max(1, std::min(band, BT / ncg));
-        const long long items = (long long)((oh + band - 1) / band) * frames;
-        const int grid = (int)std::min<long long>(items, sms);
-        pyramid_bulk_kernel<<<grid, BT, 2 * BBUF, st>>>(src, src_stride, w, h, dst, dst_stride, frames, band,
-                                                        rgroups);
+        // two 48 KB buffers per CTA, two CTAs per SM (one CTA's loads overlap the
+        // other's filtering); rows wider than ~3 KB take two 96 KB buffers
+        if ((48 * 1024 / w - 4) / 2 >= 6)
+            launch_bulk<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
+        else
+            launch_bulk<512, 96 * 1024, 1>(src, src_stride, w, h, dst, dst_stride, frames, st);
         return;
     }
     // streaming kernel: 8-byte aligned rows and frames, 4-byte aligned output rows
