@@ -271,21 +271,22 @@ __device__ __forceinline__ int stage_block(const Level& L, int x0, int y0, int s
             uint32_t* d = reinterpret_cast<uint32_t*>(dst + lr * SM_PITCH) + lw;
             const size_t sstep = (size_t)rpp * (L.w >> 2);
             const int dstep = rpp * (SM_PITCH / 4);
-            int r = lr;
-            for (; r + 3 * rpp < sh; r += 4 * rpp) {  // four loads in flight
-                const uint32_t a = __ldg(src), b = __ldg(src + sstep), c = __ldg(src + 2 * sstep),
-                               e = __ldg(src + 3 * sstep);
-                d[0] = a;
-                d[dstep] = b;
-                d[2 * dstep] = c;
-                d[3 * dstep] = e;
+            // this lane's rows lr, lr + rpp, ...: passes of four predicated
+            // loads, all issued before the first store (a 28-row window at
+            // rpp = 4 is two passes, i.e. two global latencies)
+            const int nr = (sh - lr + rpp - 1) / rpp;
+            for (int base = 0; base < nr; base += 4) {
+                uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+                v0 = __ldg(src);
+                if (base + 1 < nr) v1 = __ldg(src + sstep);
+                if (base + 2 < nr) v2 = __ldg(src + 2 * sstep);
+                if (base + 3 < nr) v3 = __ldg(src + 3 * sstep);
+                d[0] = v0;
+                if (base + 1 < nr) d[dstep] = v1;
+                if (base + 2 < nr) d[2 * dstep] = v2;
+                if (base + 3 < nr) d[3 * dstep] = v3;
                 src += 4 * sstep;
                 d += 4 * dstep;
-            }
-            for (; r < sh; r += rpp) {
-                *d = __ldg(src);
-                src += sstep;
-                d += dstep;
             }
         }
         return x0 - xw;
