@@ -325,11 +325,21 @@ __device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const doub
     src += lane;
     double p0 = u2d(src[0]), q0 = u2d(src[1]);
     double a0x = 0.0, a0y = 0.0, b0x = 0.0, b0y = 0.0, a1x = 0.0, a1y = 0.0, b1x = 0.0, b1y = 0.0;
+    // software-pipelined: row k+1's gradient and pixel bytes are loaded while
+    // row k's products issue (the last prefetch reads one row past the
+    // window, inside the warp's shared area, and is discarded)
+    src += SM_PITCH;
+    uint32_t pn = src[0], qn = src[1];
+    double2 gn = ga[0];
 #pragma unroll 2
     for (int k = 0; k < vh; ++k) {
+        const double2 g = gn;
+        const double p1 = u2d(pn), q1 = u2d(qn);
+        ga += sa;
         src += SM_PITCH;
-        const double p1 = u2d(src[0]), q1 = u2d(src[1]);
-        const double2 g = ga[0];
+        gn = ga[0];
+        pn = src[0];
+        qn = src[1];
         a0x = fma(p0, g.x, a0x);
         a0y = fma(p0, g.y, a0y);
         b0x = fma(q0, g.x, b0x);
@@ -338,7 +348,6 @@ __device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const doub
         a1y = fma(p1, g.y, a1y);
         b1x = fma(q1, g.x, b1x);
         b1y = fma(q1, g.y, b1y);
-        ga += sa;
         p0 = p1;
         q0 = q1;
     }
