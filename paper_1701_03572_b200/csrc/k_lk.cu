@@ -428,10 +428,19 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
     hp = h;
     hpx = hx;
     src += 3 * SM_PITCH;
+    // software-pipelined: image row j+3's bytes are loaded while row j's
+    // template values are formed (the last prefetch reads one row past the
+    // staged block, inside the warp's shared area, and is discarded)
+    uint32_t n0 = src[0], n1 = src[1], n2 = XTRA ? src[2] : 0u;
 #pragma unroll 2
-    for (int j = jv0; j <= jv1; ++j, src += SM_PITCH) {  // template row j: extended rows j .. j+2
-        h = hlerp(src[0], src[1], fx);
-        if (XTRA) hx = hlerp(src[1], src[2], fx);
+    for (int j = jv0; j <= jv1; ++j) {  // template row j: extended rows j .. j+2
+        const uint32_t c0 = n0, c1 = n1, c2 = n2;
+        src += SM_PITCH;
+        n0 = src[0];
+        n1 = src[1];
+        if (XTRA) n2 = src[2];
+        h = hlerp(c0, c1, fx);
+        if (XTRA) hx = hlerp(c1, c2, fx);
         const double ev = fma(fy, h - hp, hp);  // extended row j + 2
         double evx = 0.0;
         if (XTRA) evx = fma(fy, hx - hpx, hpx);
