@@ -447,8 +447,10 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
         double right = __shfl_down_sync(FULL, eB, 1);
         const double left = __shfl_up_sync(FULL, eB, 1);
         if (XTRA && xtra) right = eBx;
-        const double dx = tcol ? right - left : 0.0;  // 2 * gradient
-        const double dy = tcol ? ev - eA : 0.0;
+        // 2 * gradient; lanes outside the template columns accumulate finite
+        // junk that is dropped after the loop (no per-row select)
+        const double dx = right - left;
+        const double dy = ev - eA;
         if (tcol)
             asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga), "d"(dx), "d"(dy));
         ga += grow;
@@ -463,6 +465,7 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
         hp = h;
         if (XTRA) hpx = hx;
     }
+    if (!tcol) gxx = gxy = gyy = tx = ty = 0.0;
 }
 
 // a / b correctly rounded, given y = RN(1/b): q0 = RN(a*y) is within one ulp
