@@ -1,0 +1,52 @@
+"""Stage II at a benchmark config with pinned host buffers, straight through
+the C ABI (push frame k from a pinned array, pop into a pinned array)."""
+import ctypes as C
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1701_03572_b200 import pipeline, synth
+from paper_1701_03572_b200._lib import load, context
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+cfg = synth.CONFIGS[name]
+planes = synth.Video(cfg.video).render(0, n)
+pin = [torch.from_numpy(p).pin_memory() for p in planes]
+outp = [torch.empty_like(p).pin_memory() for p in pin]
+h, w = planes[0].shape[1:]
+col = len(planes) == 3
+cw, ch = (planes[1].shape[2], planes[1].shape[1]) if col else (0, 0)
+lib = load()
+ctx = context(0)
+c = cfg.stab.c()
+hs = C.c_void_p()
+assert lib.stabgpu_stream_create(ctx.handle, C.byref(c), w, h, cw, ch, C.byref(hs)) == 0
+rec = np.zeros(1, pipeline.RECORD_DT)
+vp = lambda t, k: C.c_void_p(t[k].data_ptr())
+def pop_all(k):
+    for _ in range(k):
+        idx = C.c_int64()
+        j = 0
+        # pop into the slot of the frame index (learned after the call: use a scratch slot first)
+        assert lib.stabgpu_stream_pop(hs, C.byref(idx), vp(outp[0], pop_all.n % n),
+                                      vp(outp[1], pop_all.n % n) if col else None,
+                                      vp(outp[2], pop_all.n % n) if col else None,
+                                      C.c_void_p(rec.ctypes.data)) == 0
+        pop_all.n += 1
+pop_all.n = 0
+lat = []
+nr = C.c_int()
+t0 = time.perf_counter()
+for k in range(n):
+    t1 = time.perf_counter()
+    assert lib.stabgpu_stream_push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
+                                   vp(pin[2], k) if col else None, C.byref(nr)) == 0
+    pop_all(nr.value)
+    lat.append(time.perf_counter() - t1)
+assert lib.stabgpu_stream_finish(hs, C.byref(nr)) == 0
+pop_all(nr.value)
+dt = time.perf_counter() - t0
+lib.stabgpu_stream_destroy(hs)
+lat = np.array(lat) * 1e3
+print(f"{name} pinned: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
+      f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out")
