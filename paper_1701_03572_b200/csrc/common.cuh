@@ -11,6 +11,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
 #include "../../include/stabgpu.h"
 
 namespace stabgpu {
@@ -69,6 +74,68 @@ __device__ __forceinline__ double warp_dsum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+// ---- host: launch facts cached per (kernel, device) ------------------------
+// The attribute and occupancy queries cost microseconds each; Stage II
+// launches every kernel once per frame, so they are asked once.
+struct LaunchCache {
+    std::mutex m;
+    std::map<std::tuple<const void*, int, int, size_t>, int> occ;  // (fn, dev, threads, smem) -> blocks/SM
+    std::map<std::pair<const void*, int>, size_t> smem;             // (fn, dev) -> opted-in dynamic smem
+    std::map<int, int> sms;
+};
+
+inline LaunchCache& launch_cache() {
+    static LaunchCache c;
+    return c;
+}
+
+inline int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+inline int sm_count() {
+    LaunchCache& c = launch_cache();
+    const int d = cur_device();
+    std::lock_guard<std::mutex> g(c.m);
+    auto it = c.sms.find(d);
+    if (it != c.sms.end()) return it->second;
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    c.sms[d] = n;
+    return n;
+}
+
+// opt the kernel in to `bytes` of dynamic shared memory (only when it grows)
+template <typename K>
+inline void ensure_smem(K* fn, size_t bytes) {
+    LaunchCache& c = launch_cache();
+    const auto key = std::make_pair(reinterpret_cast<const void*>(fn), cur_device());
+    std::lock_guard<std::mutex> g(c.m);
+    auto it = c.smem.find(key);
+    if (it != c.smem.end() && it->second >= bytes) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    c.smem[key] = bytes;
+}
+
+template <typename K>
+inline int blocks_per_sm(K* fn, int threads, size_t bytes) {
+    LaunchCache& c = launch_cache();
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(fn), cur_device(), threads, bytes);
+    {
+        std::lock_guard<std::mutex> g(c.m);
+        auto it = c.occ.find(key);
+        if (it != c.occ.end()) return it->second;
+    }
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, bytes);
+    per = per > 0 ? per : 1;
+    std::lock_guard<std::mutex> g(c.m);
+    c.occ[key] = per;
+    return per;
 }
 
 }  // namespace stabgpu

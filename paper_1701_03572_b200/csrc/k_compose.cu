@@ -1322,11 +1322,8 @@ bool launch_tma(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pla
     tile_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plan, frames, tx, ty, W, H, y.w, y.h,
                                                                     cb.w, cb.h, g, T, L ? 1 : 0, C ? 1 : 0);
     const size_t smem = sizeof(SmemT);
-    cudaFuncSetAttribute(compose_tma_kernel<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, compose_tma_kernel<L, C>, NT, smem);
+    ensure_smem(compose_tma_kernel<L, C>, smem);
+    const int sms = sm_count(), per = blocks_per_sm(compose_tma_kernel<L, C>, NT, smem);
     const long long grid = std::min<long long>(total, (long long)sms * std::max(per, 1));
     compose_tma_kernel<L, C><<<(unsigned)grid, NT, smem, st>>>(y, cb, cr, plan, g, T, tx, ty, frames, my, mb, mr,
                                                                oy, ocb, ocr);
@@ -1340,7 +1337,7 @@ void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* p
     const int W = L ? y.w : cb.w, H = L ? y.h : cb.h;
     const int tx = (W + TW - 1) / TW, ty = (H + TH - 1) / TH;
     const size_t smem = sizeof(Smem);
-    cudaFuncSetAttribute(compose_kernel<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(compose_kernel<L, C>, smem);
     for (int f0 = 0; f0 < frames; f0 += 65535) {
         const int nf = min(65535, frames - f0);
         PlaneBatch a = y, b = cb, c = cr;

@@ -862,7 +862,7 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
                                                   s.count, s.cand_key, s.cand_idx, s.cap, nullptr);
     }
     const size_t smem = detect_smem_bytes(cfg, rw, rh);
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(select_kernel, smem);
     short2* g_axy = nullptr;
     int* g_anext = nullptr;
     if (cfg.max_corners > SMEM_CORNERS) {

@@ -293,7 +293,7 @@ void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_
                 stabgpu_motion_record* out, cudaStream_t st, long long stream_frames) {
     if (nframes <= 0) return;
     const size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
-    cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(fit_kernel, smem);
     fit_kernel<<<nframes, FIT_THREADS, smem, st>>>(trk_prev, trk_cur, trk_n, max_pts, frame_index0,
                                                    cfg, out, stream_frames);
 }
@@ -349,7 +349,7 @@ void launch_fit_single(const double2* P, const double2* Q, int n, int kind,
                        const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
                        FitResult* out, uint8_t* mask, cudaStream_t st) {
     const size_t smem = (size_t)n * (2 * sizeof(double2) + 1) + 16;
-    cudaFuncSetAttribute(fit_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(fit_single_kernel, smem);
     fit_single_kernel<<<1, FIT_THREADS, smem, st>>>(P, Q, n, kind, rc, min_tracks, frame, out, mask);
 }
 

@@ -946,11 +946,8 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
         const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
-        cudaFuncSetAttribute(lk_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk_fast_kernel, wpc * 32, smem);
+        ensure_smem(lk_fast_kernel, smem);
+        const int sms = sm_count(), per_sm = blocks_per_sm(lk_fast_kernel, wpc * 32, smem);
         cudaMemsetAsync(s.work, 0, sizeof(unsigned), st);
         const long long items = (long long)s.nseg * s.max_pts;
         const long long want = (items + wpc - 1) / wpc;
@@ -962,7 +959,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     int wpc = (int)((100 * 1024) / (per_warp * sizeof(double)));
     wpc = max(1, min(8, wpc));
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
-    cudaFuncSetAttribute(lk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(lk_kernel, smem);
     dim3 grid((s.max_pts + wpc - 1) / wpc, s.nseg);
     lk_kernel<<<grid, wpc * 32, smem, st>>>(s, cfg, wpc, per_warp);
 }
@@ -975,11 +972,8 @@ void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
     const bool multi = c.nsps != c.nseg;  // several streams in the chunk
     auto kern = multi ? lk_chain_kernel<true> : lk_chain_kernel<false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpc * 32, smem);
+    ensure_smem(kern, smem);
+    const int sms = sm_count(), per_sm = blocks_per_sm(kern, wpc * 32, smem);
     cudaMemsetAsync(c.work, 0, sizeof(unsigned), st);
     cudaMemsetAsync(c.alive, 0, (size_t)c.R * c.nseg * c.max_pts, st);
     const long long items = (long long)c.nseg * c.max_pts;

@@ -285,14 +285,8 @@ void launch_bulk(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* d
                  cudaStream_t st) {
     const int ow = w / 2, oh = h / 2;
     const int band = std::min(oh, (BBUF / w - 4) / 2);
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(pyramid_bulk_kernel<BT, BBUF, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * BBUF);
-    }
+    ensure_smem(pyramid_bulk_kernel<BT, BBUF, MINB>, 2 * BBUF);
+    const int sms = sm_count();
     const int ncg = ow / 4;
     const int rgroups = std::max(1, std::min(band, BT / ncg));
     const long long items = (long long)((oh + band - 1) / band) * frames;
