@@ -40,8 +40,6 @@ struct stabgpu_ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t cin = nullptr, cout = nullptr;
-    cudaStream_t aux = nullptr;                       // K1 runs here, beside K2-K4
-    cudaEvent_t fork = nullptr, join = nullptr;
     std::map<std::string, DevBuf> bufs;
     bool timing = false;
     stabgpu_stats stats{};
@@ -189,12 +187,11 @@ FramePlan host_plan(const stabgpu_transform& t) {
 struct Timer {
     stabgpu_ctx* ctx;
     int slot;
-    cudaStream_t st;
-    Timer(stabgpu_ctx* c, int s, cudaStream_t on = nullptr) : ctx(c), slot(s), st(on ? on : c->stream) {
-        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot], st);
+    Timer(stabgpu_ctx* c, int s) : ctx(c), slot(s) {
+        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot], ctx->stream);
     }
     ~Timer() {
-        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot + 1], st);
+        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot + 1], ctx->stream);
     }
 };
 
@@ -227,26 +224,20 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     P.levels = level_dims(w, h, cfg.flow.max_levels, P.w, P.h);
     P.lvl[0] = y;
     P.stride[0] = (size_t)w * h;
-    // K1 reads only the frames and feeds only K5, so it runs on the auxiliary
-    // stream beside K2-K4 (HBM-bound next to issue-bound); K5 joins on it
-    for (int l = 1; l < P.levels; ++l) {
-        P.stride[l] = (size_t)P.w[l] * P.h[l];
-        DBUF(uint8_t, lv, ("pyr" + std::to_string(l)).c_str(), P.stride[l] * nF);
-        P.lvl[l] = lv;
-    }
-    const cudaStream_t pst = ctx->aux;
-    CUDA_TRY(cudaEventRecord(ctx->fork, st));
-    CUDA_TRY(cudaStreamWaitEvent(pst, ctx->fork, 0));
     {
-        Timer tm(ctx, 0, pst);
+        Timer tm(ctx, 0);
+        for (int l = 1; l < P.levels; ++l) {
+            P.stride[l] = (size_t)P.w[l] * P.h[l];
+            DBUF(uint8_t, lv, ("pyr" + std::to_string(l)).c_str(), P.stride[l] * nF);
+            P.lvl[l] = lv;
+        }
         for (int l = 1; l < P.levels; ++l) {
             launch_pyramid_level(P.lvl[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1],
-                                 const_cast<uint8_t*>(P.lvl[l]), P.stride[l], nF, pst);
+                                 const_cast<uint8_t*>(P.lvl[l]), P.stride[l], nF, st);
             ++ctx->stats.launches;
         }
         TRY(check_launch("pyramid"));
     }
-    CUDA_TRY(cudaEventRecord(ctx->join, pst));
     // ---- K2-K4: corners on each segment's first frame
     const size_t cap = (size_t)(roi.x1 - roi.x0) * (roi.y1 - roi.y0);
     // detection frames go in batches whose candidate scratch (24 B x ROI area
@@ -295,8 +286,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         }
         TRY(check_launch("detect"));
     }
-    // ---- K5: R tracking steps over all segments (after K1 on the aux stream)
-    CUDA_TRY(cudaStreamWaitEvent(st, ctx->join, 0));
+    // ---- K5: R tracking steps over all segments
     DBUF(double2, fwd, "lk_fwd", (size_t)nseg * maxc);
     DBUF(uint8_t, keep, "lk_keep", (size_t)nseg * maxc);
     DBUF(double2, trk_prev, "trk_prev", (size_t)count * maxc);
@@ -507,9 +497,6 @@ int stabgpu_create(int device, stabgpu_ctx** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cin, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cout, cudaStreamNonBlocking));
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     c->stream = c->own;
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
     // Per-launch tables come from the stream-ordered allocator; keep freed
@@ -533,9 +520,6 @@ int stabgpu_destroy(stabgpu_ctx* c) {
     cudaStreamDestroy(c->own);
     cudaStreamDestroy(c->cin);
     cudaStreamDestroy(c->cout);
-    cudaStreamDestroy(c->aux);
-    cudaEventDestroy(c->fork);
-    cudaEventDestroy(c->join);
     delete c;
     return STABGPU_OK;
 }
