@@ -303,10 +303,8 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
     if (frames <= 0 || ow <= 0 || oh <= 0) return;
     // bulk-copy kernel: 16-byte aligned rows and frames, 4-byte aligned output rows,
     // at least 16 input rows (2 * band + 4 with band >= 6) per buffer
-    const char* ver_env = std::getenv("STABGPU_PYR_KERNEL");  // tuning: 0 = register-streaming kernel
-    const int ver = ver_env ? std::atoi(ver_env) : 1;
     const int band = std::min(oh, (96 * 1024 / w - 4) / 2);  // the largest buffer below
-    const bool bulk = ver != 0 && (w % 16) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+    const bool bulk = (w % 16) == 0 && (ow % 4) == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
                       (src_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(dst) % 4) == 0 &&
                       (dst_stride % 4) == 0 && band >= 6;
     if (bulk) {
