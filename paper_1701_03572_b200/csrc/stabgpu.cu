@@ -1522,9 +1522,11 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     if (s->chroma && ((rc = salloc(s, &s->ring_cb, fc * s->cap)) || (rc = salloc(s, &s->ring_cr, fc * s->cap)) ||
                       (rc = salloc(s, &s->out_cb, fc * s->ocap)) || (rc = salloc(s, &s->out_cr, fc * s->ocap))))
         return fail(rc);
-    // two-frame pyramid
+    // two-frame pyramid for levels >= 1 (frame f in slot f & 1); level 0 is
+    // the input ring itself
     s->P.levels = level_dims(w, h, cfg.flow.max_levels, s->P.w, s->P.h);
-    for (int l = 0; l < s->P.levels; ++l) {
+    s->P.stride[0] = (size_t)w * h;
+    for (int l = 1; l < s->P.levels; ++l) {
         uint8_t* lv;
         s->P.stride[l] = (size_t)s->P.w[l] * s->P.h[l];
         if ((rc = salloc(s, &lv, 2 * s->P.stride[l]))) return fail(rc);
@@ -1580,14 +1582,27 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyHostToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyHostToDevice, st));
     }
-    // K1: the pyramid of the current frame into slot 1
+    // K1: the pyramid of the current frame, levels >= 1 into slot f & 1; no
+    // copies: level 0 stays in the ring, and the tracker sees (previous,
+    // current) through a pyramid view whose frame stride is the signed
+    // distance between the two slots
     DevPyramid& P = s->P;
-    CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(P.lvl[0]) + P.stride[0], fy, fl, cudaMemcpyDeviceToDevice, st));
+    const int cs = (int)(f & 1), ps = cs ^ 1;
     for (int l = 1; l < P.levels; ++l)
-        launch_pyramid_level(P.lvl[l - 1] + P.stride[l - 1], P.stride[l - 1], P.w[l - 1], P.h[l - 1],
-                             const_cast<uint8_t*>(P.lvl[l]) + P.stride[l], P.stride[l], 1, st);
+        launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
+                             P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, st);
     ctx->stats.launches += P.levels - 1;
-    PlaneBatch cur{P.lvl[0] + P.stride[0], fl, s->w, s->h};
+    PlaneBatch cur{fy, fl, s->w, s->h};
+    DevPyramid V = P;  // frame 0 = previous, frame 1 = current
+    if (f > 0) {
+        const uint8_t* py = s->ring_y + (size_t)((f - 1) % s->cap) * fl;
+        V.lvl[0] = py;
+        V.stride[0] = (size_t)(fy - py);  // two's complement: a wrapped ring gives a negative distance
+        for (int l = 1; l < P.levels; ++l) {
+            V.lvl[l] = P.lvl[l] + ps * P.stride[l];
+            V.stride[l] = (size_t)((ptrdiff_t)(cs - ps) * (ptrdiff_t)P.stride[l]);
+        }
+    }
     if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88) + detection (flow.cpp:303-308)
         stabgpu_motion_record f0;
         std::memset(&f0, 0, sizeof f0);
@@ -1598,7 +1613,7 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
         LkStep k;
         std::memset(&k, 0, sizeof k);
-        k.pyr = P;
+        k.pyr = V;
         k.frame0 = 0;
         k.seg_len = R;
         k.t = 1;
@@ -1621,10 +1636,6 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     }
     // K7: selector + trajectory prefix for this frame
     launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
-    // the current pyramid becomes the previous one
-    for (int l = 0; l < P.levels; ++l)
-        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(P.lvl[l]), P.lvl[l] + P.stride[l], P.stride[l],
-                                 cudaMemcpyDeviceToDevice, st));
     TRY(check_launch("stream push"));
     s->pushed = f + 1;
     TRY(stream_release_ready(s));
