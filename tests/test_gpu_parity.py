@@ -108,11 +108,13 @@ def test_detect_many_ties(orc):
 def test_detect_cut_redo(orc):
     """A strong textured patch holds far more candidates than the greedy can
     accept under a large min_distance, so the fp32-histogram cut prefix runs
-    out before max_corners and the full-list redo path must take over."""
+    out before max_corners and the full-list redo path must take over
+    ((100, 20), (300, 12)); (60, 40) is dense enough (exclusion discs cover
+    the ROI more than twice) that selection skips the cut altogether."""
     rng = np.random.default_rng(7)
     f = (rng.integers(118, 138, size=(320, 320))).astype(np.uint8)   # weak texture
     f[100:220, 100:220] = rng.integers(0, 256, size=(120, 120))      # strong patch
-    for corners, dist in ((60, 40.0), (20, 25.0), (300, 12.0)):
+    for corners, dist in ((60, 40.0), (20, 25.0), (300, 12.0), (100, 20.0)):
         cfg = DetectConfig(max_corners=corners, min_distance=dist, roi_margin=0.0)
         xg, sg = stab.detect_corners(f, cfg)
         xo, so = orc.detect_corners(f, cfg)
