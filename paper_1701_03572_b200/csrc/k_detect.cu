@@ -15,7 +15,7 @@
 //     bit pattern (responses are >= 0, so bit order == value order).
 // K3 (cand_kernel): recomputes the response (cheaper than writing an 8 B/px
 //     map), keeps r >= quality*max && r > 0, warp-ballot compaction.
-// K4 (select_kernel): one 1024-thread CTA per detection frame.  Candidates
+// K4 (select_kernel): one 512-thread CTA per detection frame (two per SM).  Candidates
 //     are bucketed by a monotone 13-bit-truncated float key (histogram +
 //     scatter in shared memory), then consumed in score order in chunks of
 //     <= 4096: each chunk is first tested against the accepted-corner grid
@@ -409,8 +409,11 @@ __global__ void resp_generic_kernel(PlaneBatch fr, stabgpu_roi roi, int half, in
 
 // ---------------------------------------------------------------- K4 ----
 
-constexpr int SEL_THREADS = 1024;
-constexpr int CAP = 4096;       // chunk capacity (candidates sorted per pass)
+// Two shapes of the select CTA: 1024 threads with 4096-candidate chunks
+// (fastest per frame), or 512 threads with 3072-candidate chunks in ~110 KB
+// of shared memory, two frames per SM, so a batch with more frames than SMs
+// runs its serial greedies (one warp per frame) two at a time on every SM.
+constexpr int CAP_MAX = 4096;
 #ifndef SEL_CHUNK
 #define SEL_CHUNK 1024
 #endif
@@ -433,9 +436,9 @@ __device__ __forceinline__ bool before(unsigned long long ka, unsigned ia, unsig
     return ka > kb || (ka == kb && ia < ib);
 }
 
-// Block-wide exclusive scan of one value per thread (1024 threads).
+// Block-wide exclusive scan of one value per thread (up to 1024 threads).
 __device__ unsigned block_excl_scan(unsigned v, unsigned* warp_tot, unsigned* total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     unsigned x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -445,7 +448,7 @@ __device__ unsigned block_excl_scan(unsigned v, unsigned* warp_tot, unsigned* to
     if (lane == 31) warp_tot[wid] = x;
     __syncthreads();
     if (wid == 0) {
-        unsigned t = warp_tot[lane];
+        unsigned t = lane < nw ? warp_tot[lane] : 0u;
         unsigned s = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -513,7 +516,7 @@ __device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const 
 
 // In-place stable-free merge sort of [0, m) by (score desc, idx asc) in
 // global memory, ping-ponging with tmp (keys are unique, so rank-merging is
-// exact).  Used only for buckets larger than CAP.
+// exact).  Used only for buckets larger than the chunk capacity.
 __device__ void global_merge_sort(unsigned long long* key, unsigned* idx, unsigned long long* tkey,
                                   unsigned* tidx, unsigned m) {
     unsigned long long *sk = key, *dk = tkey;
@@ -553,10 +556,13 @@ __device__ void global_merge_sort(unsigned long long* key, unsigned* idx, unsign
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(SEL_THREADS, 1)
+template <int SEL_THREADS, int CAP>
+__global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     select_kernel(stabgpu_detect_cfg cfg, stabgpu_roi roi, int w, DetectScratch s,
                   double2* __restrict__ out_xy, double* __restrict__ out_score,
                   int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext, int redo) {
+    static_assert(12 * CAP >= 4 * kBuckets, "the bucket cursor aliases the chunk arrays");
+    static_assert(kBuckets % SEL_THREADS == 0 && CAP % SEL_THREADS == 0, "per-thread strides");
     extern __shared__ __align__(16) unsigned char smem[];
     if (redo && !(s.flags ? (s.flags[blockIdx.x] & 2) : 0)) return;
     SelShared& S = *reinterpret_cast<SelShared*>(smem);
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
         if (ck[i] >= thrb) atomicAdd(&cursor[bucket_of(ck[i], maxf)], 1u);
     __syncthreads();
     {
-        constexpr int PER = kBuckets / SEL_THREADS;  // 8
+        constexpr int PER = kBuckets / SEL_THREADS;
         unsigned v[PER], sum = 0;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
@@ -721,7 +727,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
             // adapt the chunk: few survivors -> larger chunks (fewer passes);
             // many -> smaller ones (more prefiltering before the serial greedy)
             if (tid == 0) {
-                if (ns < 64 && S.chunk < CAP) S.chunk *= 2;
+                if (ns < 64 && S.chunk < CAP) S.chunk = min(2 * S.chunk, CAP);  // whole chunks stay <= CAP
                 else if (ns > 512 && S.chunk > 256) S.chunk /= 2;
             }
             {
@@ -820,12 +826,14 @@ __global__ void gradients_kernel(const uint8_t* __restrict__ f, int w, int h, do
 
 }  // namespace
 
-size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int, int) {
-    size_t b = ((sizeof(SelShared) + 15) & ~size_t(15)) + (sizeof(unsigned long long) + sizeof(unsigned)) * CAP +
+size_t select_smem_bytes(const stabgpu_detect_cfg& cfg, int cap) {
+    size_t b = ((sizeof(SelShared) + 15) & ~size_t(15)) + (sizeof(unsigned long long) + sizeof(unsigned)) * cap +
                sizeof(int) * MAX_CELLS;
     if (cfg.max_corners <= SMEM_CORNERS) b += (sizeof(short2) + sizeof(int)) * cfg.max_corners;
     return b;
 }
+
+size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int, int) { return select_smem_bytes(cfg, CAP_MAX); }
 
 void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
                    DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
@@ -869,8 +877,13 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
         resp_generic_kernel<<<grid, 128, 0, st>>>(fr, roi, half, 1, cfg.quality_level, s.maxbits,
                                                   s.count, s.cand_key, s.cand_idx, s.cap, nullptr);
     }
-    const size_t smem = detect_smem_bytes(cfg, rw, rh);
-    ensure_smem(select_kernel, smem);
+    // two 512-thread CTAs per SM when the batch outnumbers the SMs and both fit
+    const size_t smem_small = select_smem_bytes(cfg, 3072);
+    const bool pair = nD > sm_count() && 2 * (smem_small + 1024) <= 228 * 1024;
+    const size_t smem = pair ? smem_small : select_smem_bytes(cfg, CAP_MAX);
+    auto sel = pair ? select_kernel<512, 3072> : select_kernel<1024, CAP_MAX>;
+    const int sel_threads = pair ? 512 : 1024;
+    ensure_smem(sel, smem);
     short2* g_axy = nullptr;
     int* g_anext = nullptr;
     if (cfg.max_corners > SMEM_CORNERS) {
@@ -880,14 +893,12 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     }
     DetectScratch sf = s;
     if (!fast) sf.flags = nullptr;
-    select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy,
-                                                 g_anext, 0);
+    sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy, g_anext, 0);
     if (fast) {  // frames whose cut prefix ran out: full candidate list (usually none)
         resp_redo_reset_kernel<<<nD, 32, 0, st>>>(s);
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 1);
-        select_kernel<<<nD, SEL_THREADS, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy,
-                                                     g_anext, 1);
+        sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy, g_anext, 1);
     }
     if (g_axy) {
         cudaFreeAsync(g_axy, st);

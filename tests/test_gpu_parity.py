@@ -317,6 +317,21 @@ def test_sequence(orc, mode, ransac):
         assert mx <= 1 and cnt <= 0.0005 * a.size
 
 
+def test_sequence_many_detection_frames(orc):
+    """More detection frames than SMs: K4 runs as two 512-thread CTAs per SM
+    (3072-candidate chunks) instead of one 1024-thread CTA; same corners."""
+    import torch
+
+    n = 5 * (torch.cuda.get_device_properties(0).multi_processor_count + 12) + 1
+    y = _data.video(frames=n, objects=1, jit_t=3.0)[0]
+    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    gy, _, _, grec = pipeline.stabilize_sequence(y, cfg)
+    oy, _, _, orec = orc.stabilize_sequence(y, cfg)
+    _compare_records(grec, orec)
+    mx, cnt = _offby(gy, oy)
+    assert mx <= 1 and cnt <= 0.0005 * gy.size
+
+
 def test_sequence_device_equals_host_path():
     import torch
     y, cb, cr = _data.video(frames=37, objects=1, color=True)
