@@ -77,6 +77,34 @@ def kernel_rooflines(spec, stab_cfg, frames, c, hbm):
     return out
 
 
+def compose_issue(spec, planes, frames, ms):
+    """K8's fraction of the SM issue rate (its actual limiter): warp
+    instructions per launch from the committed ncu capture, scaled per frame,
+    over the measured launch time, against 4 schedulers x SMs x SM clock."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "compose_traffic.json")
+    try:
+        t = json.load(open(p))
+        inst = t["warp_instructions"] * frames / t["frames_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+    if (t["width"], t["height"], t["planes"]) != (spec.width, spec.height, planes) or not ms:
+        return None
+    import torch
+
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        mhz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()),
+                                               pynvml.NVML_CLOCK_SM)
+    except Exception:
+        mhz = 1965
+    peak = props.multi_processor_count * 4 * mhz * 1e6
+    return {"warp_instructions": inst, "peak_warp_inst_per_s": peak, "frac": inst / (ms / 1000.0) / peak,
+            "source": "ncu smsp__inst_executed.sum (profiles/compose_traffic.json)"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -339,7 +367,9 @@ def run_ours(args, cfg):
                              "frac": (achieved / hbm) if achieved else None,
                              "traffic": compose_traffic(spec, planes, sh.own_end - sh.own_begin if world > 1 else n),
                              "peak_source": peak_src,
-                             "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms},
+                             "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms,
+                             "issue": compose_issue(spec, planes, sh.own_end - sh.own_begin if world > 1 else n,
+                                                    comp_ms)},
                 "kernels": kernel_rooflines(spec, cfg.stab, n if world == 1 else 0, c, hbm),
                 "stage_ms": stages,
                 "gpu_launches": int(launches),
