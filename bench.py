@@ -256,9 +256,14 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":  # functional check of the N > 1 path on fewer GPUs (not a measurement)
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     n = cfg.video.frames
     spec = cfg.video
     planes = 3 if spec.color else 1
@@ -330,7 +335,7 @@ def run_ours(args, cfg):
         barrier()
         ms = ev0.elapsed_time(ev1) / steps
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device="cuda" if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         launches = (ctx.stats().launches - launches0) // max(steps, 1)
@@ -409,9 +414,14 @@ def run_streams(args, cfg, group=64):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":  # functional check of the N > 1 path on fewer GPUs (not a measurement)
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     spec = cfg.video
     mine = pipeline.streams_of_rank(spec.streams, rank, world)
     S, F, h, w = len(mine), spec.frames, spec.height, spec.width
@@ -460,7 +470,7 @@ def run_streams(args, cfg, group=64):
         barrier()
         ms = ev0.elapsed_time(ev1) / steps
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device="cuda" if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, (ctx.stats().launches - launches0) // max(steps, 1)
@@ -501,6 +511,8 @@ def run_streams(args, cfg, group=64):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the multi-rank code path on fewer GPUs than ranks (functional check only)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
