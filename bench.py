@@ -351,7 +351,8 @@ def run_ours(args, cfg):
     line = None
     if rank == 0:
         hbm, peak_src = peaks()
-        c = np.array(comp).mean(axis=0) if comp and world == 1 else np.zeros(6)
+        # per-stage times of this rank (rank 0 when sharded)
+        c = np.array(comp).mean(axis=0) if comp else np.zeros(6)
         # dominant HBM-bound kernel family: K8 compose (luma warp+crop and chroma),
         # algorithmic bytes = one read + one write of every plane of every frame
         alg = 2.0 * fb * (sh.own_end - sh.own_begin if world > 1 else n)
@@ -375,7 +376,7 @@ def run_ours(args, cfg):
                              "alg_bytes_per_launch": alg, "ms_per_launch": comp_ms,
                              "issue": compose_issue(spec, planes, sh.own_end - sh.own_begin if world > 1 else n,
                                                     comp_ms)},
-                "kernels": kernel_rooflines(spec, cfg.stab, n if world == 1 else 0, c, hbm),
+                "kernels": kernel_rooflines(spec, cfg.stab, n if world == 1 else count, c, hbm),
                 "stage_ms": stages,
                 "gpu_launches": int(launches),
                 "lk": {"iterations": int(ctx.stats().lk_iterations),

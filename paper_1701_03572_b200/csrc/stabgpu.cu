@@ -1325,10 +1325,17 @@ int stabgpu_motion_chunk(stabgpu_ctx* ctx, const uint8_t* dev_y, int64_t first, 
         CUDA_TRY(cudaMemcpyAsync(motion, &none, sizeof none, cudaMemcpyHostToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     }
-    TRY(run_motion(ctx, dev_y, first, count, w, h, cfg, base, nullptr));
+    double t_ms[4] = {0, 0, 0, 0};
+    TRY(run_motion(ctx, dev_y, first, count, w, h, cfg, base, t_ms));
     CUDA_TRY(cudaMemcpyAsync(host_out, motion, sizeof(stabgpu_motion_record) * ((size_t)count + 1),
                              cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->timing) {  // stage times of this chunk (a sharded rank's motion)
+        ctx->stats.ms_pyramid = t_ms[0];
+        ctx->stats.ms_detect = t_ms[1];
+        ctx->stats.ms_track = t_ms[2];
+        ctx->stats.ms_fit = t_ms[3];
+    }
     return STABGPU_OK;
 }
 
@@ -1347,14 +1354,21 @@ int stabgpu_plan_corrections(stabgpu_ctx* ctx, const stabgpu_motion_record* host
                              cudaMemcpyHostToDevice, st));
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
+    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
     launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
     launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{16, 16, 0, 0, 0.0}, st);
+    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
     TRY(plan_error(ctx, ps));
     CUDA_TRY(cudaMemcpyAsync(host_records, rec, sizeof(stabgpu_frame_record) * n,
                              cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (ctx->timing) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[10], ctx->ev[11]);
+        ctx->stats.ms_plan = ms;
+    }
     return STABGPU_OK;
 }
 
@@ -1373,8 +1387,16 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb
                              cudaMemcpyHostToDevice, st));
     launch_plan_from_corrections(corr, count, plan, PlanGeom{w, h, (cb && cr) ? cw : 0, (cb && cr) ? ch : 0, crop}, st);
     ++ctx->stats.launches;
-    TRY(compose_range(ctx, y, cb, cr, 0, count, w, h, cw, ch, plan, crop, oy, ocb, ocr));
+    {
+        Timer tm(ctx, 4);
+        TRY(compose_range(ctx, y, cb, cr, 0, count, w, h, cw, ch, plan, crop, oy, ocb, ocr));
+    }
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (ctx->timing) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
+        ctx->stats.ms_compose = ms;
+    }
     return STABGPU_OK;
 }
 
