@@ -12,6 +12,8 @@
 // one per warp (lanes stride the pairs, popc-reduced counts), so inlier
 // counts are bit-identical to the CPU rule; only the refit's sums are
 // reduced in a different (fixed) order.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -145,56 +147,123 @@ __device__ double rms(const double2* P, const double2* Q, int n, const FitOut& t
 }
 
 // RANSAC inlier selection; returns the pair count the refit uses and fills mask.
-__device__ int ransac_select(const double2* P, const double2* Q, int n, bool rigid,
-                             const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
-                             uint8_t* mask, int* wbest_c, int* wbest_h, Model* wbest_m) {
+// Hypothesis h's minimal sample (counter-based: the same pair wherever h is scored)
+__device__ __forceinline__ bool hypothesis(const double2* P, const double2* Q, int n, bool rigid, uint64_t key, int h,
+                                           Model& m) {
+    const uint64_t u = mix64(key + (uint64_t)(h + 1) * 0x9e3779b97f4a7c15ULL);
+    const int i = (int)((uint32_t)(u >> 32) % (uint32_t)n);
+    int j = (int)((uint32_t)u % (uint32_t)(n - 1));
+    if (j >= i) ++j;
+    return minimal_model(P, Q, i, j, rigid, m);
+}
+
+__device__ __forceinline__ uint64_t ransac_key(const stabgpu_ransac_cfg& rc, long long frame) {
+    return mix64(rc.seed ^ mix64((uint64_t)frame + 0x9e3779b97f4a7c15ULL));
+}
+
+// Scores hypotheses h = first, first + stride, ... (ascending per warp) and
+// returns the CTA's best (count, h): most inliers, ties to the lowest h;
+// h = -1 when no hypothesis had a valid minimal model.
+__device__ int2 ransac_score(const double2* P, const double2* Q, int n, bool rigid, const stabgpu_ransac_cfg& rc,
+                             long long frame, int first, int stride, int* wbest_c, int* wbest_h) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double thr2 = dmul(rc.threshold, rc.threshold);
-    const uint64_t key = mix64(rc.seed ^ mix64((uint64_t)frame + 0x9e3779b97f4a7c15ULL));
+    const uint64_t key = ransac_key(rc, frame);
     int best_c = 0, best_h = -1;
-    Model best_m{0, 0, 0, 0};
-    for (int h = wid; h < rc.iterations; h += FIT_WARPS) {
-        const uint64_t u = mix64(key + (uint64_t)(h + 1) * 0x9e3779b97f4a7c15ULL);
-        const int i = (int)((uint32_t)(u >> 32) % (uint32_t)n);
-        int j = (int)((uint32_t)u % (uint32_t)(n - 1));
-        if (j >= i) ++j;
+    for (int h = first + wid; h < rc.iterations; h += stride) {
         Model m;
-        if (!minimal_model(P, Q, i, j, rigid, m)) continue;
+        if (!hypothesis(P, Q, n, rigid, key, h, m)) continue;
         int cnt = 0;
         for (int k = lane; k < n; k += 32) cnt += inlier(m, P[k], Q[k], thr2) ? 1 : 0;
         cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (cnt > best_c) {  // h ascends within a warp: strict > keeps the lowest h
             best_c = cnt;
             best_h = h;
-            best_m = m;
         }
     }
     if (lane == 0) {
         wbest_c[wid] = best_c;
         wbest_h[wid] = best_h;
-        wbest_m[wid] = best_m;
     }
     __syncthreads();
     int bc = 0, bh = -1;
-    Model bm{0, 0, 0, 0};
     for (int w = 0; w < FIT_WARPS; ++w) {
         const int c = wbest_c[w], hh = wbest_h[w];
         if (hh < 0) continue;
         if (bh < 0 || c > bc || (c == bc && hh < bh)) {
             bc = c;
             bh = hh;
-            bm = wbest_m[w];
         }
     }
     __syncthreads();
+    return make_int2(bc, bh);
+}
+
+// Given the winning (count, h): the inlier mask of its model (all pairs when
+// no hypothesis won or it has fewer than min_tracks inliers); returns the
+// number of pairs the refit uses.
+__device__ int ransac_finish(const double2* P, const double2* Q, int n, bool rigid, const stabgpu_ransac_cfg& rc,
+                             int min_tracks, long long frame, int2 best, uint8_t* mask) {
+    const int bc = best.x, bh = best.y;
     if (bh < 0 || bc < min_tracks) {
         for (int k = threadIdx.x; k < n; k += blockDim.x) mask[k] = 1;
         __syncthreads();
         return n;
     }
+    Model bm;
+    hypothesis(P, Q, n, rigid, ransac_key(rc, frame), bh, bm);  // valid: it was scored
+    const double thr2 = dmul(rc.threshold, rc.threshold);
     for (int k = threadIdx.x; k < n; k += blockDim.x) mask[k] = inlier(bm, P[k], Q[k], thr2) ? 1 : 0;
     __syncthreads();
     return bc;
+}
+
+__device__ int ransac_select(const double2* P, const double2* Q, int n, bool rigid,
+                             const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
+                             uint8_t* mask, int* wbest_c, int* wbest_h) {
+    const int2 best = ransac_score(P, Q, n, rigid, rc, frame, 0, FIT_WARPS, wbest_c, wbest_h);
+    return ransac_finish(P, Q, n, rigid, rc, min_tracks, frame, best, mask);
+}
+
+// Best of several scoring CTAs' results (most inliers, ties to the lowest h).
+__device__ int2 merge_best(const int2* r, int k) {
+    int bc = 0, bh = -1;
+    for (int i = 0; i < k; ++i)
+        if (r[i].y >= 0 && (bh < 0 || r[i].x > bc || (r[i].x == bc && r[i].y < bh))) {
+            bc = r[i].x;
+            bh = r[i].y;
+        }
+    return make_int2(bc, bh);
+}
+
+// Single frame (Stage II): the hypotheses of one fit spread over G CTAs.
+// CTA g scores h = 16 g + w, 16 g + w + 16 G, ... (warp w); the fit CTA merges
+// the G results, which is the same argmax (ties to the lowest h) as one CTA.
+// best[g] (rigid pass) and best[G + g] (similarity pass).
+__global__ void __launch_bounds__(FIT_THREADS) ransac_score_kernel(const double2* __restrict__ trk_prev,
+                                                                   const double2* __restrict__ trk_cur,
+                                                                   const int* __restrict__ trk_n, long long frame,
+                                                                   stabgpu_config cfg, int2* __restrict__ best) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
+    const int n = trk_n[0];
+    const int G = gridDim.x, g = blockIdx.x;
+    if (n < cfg.flow.min_tracks) return;
+    double2* P = reinterpret_cast<double2*>(fsm);
+    double2* Q = P + n;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        P[k] = trk_prev[k];
+        Q[k] = trk_cur[k];
+    }
+    __syncthreads();
+    const int mode = cfg.selector.mode;
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool rigid = pass == 0;
+        if (rigid && mode == STABGPU_FORCE_SIMILARITY) continue;
+        if (!rigid && mode == STABGPU_FORCE_RIGID) continue;
+        const int2 r = ransac_score(P, Q, n, rigid, cfg.ransac, frame, FIT_WARPS * g, FIT_WARPS * G, wbest_c, wbest_h);
+        if (threadIdx.x == 0) best[pass * G + g] = r;
+    }
 }
 
 __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restrict__ trk_prev,
@@ -202,11 +271,11 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
                                                           const int* __restrict__ trk_n, int max_pts,
                                                           long long frame_index0, stabgpu_config cfg,
                                                           stabgpu_motion_record* __restrict__ out,
-                                                          long long stream_frames) {
+                                                          long long stream_frames, const int2* __restrict__ pre,
+                                                          int pre_ctas) {
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ double red[FIT_WARPS];
     __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
-    __shared__ Model wbest_m[FIT_WARPS];
     const int f = blockIdx.x;
     stabgpu_motion_record rec;
     memset(&rec, 0, sizeof rec);
@@ -253,8 +322,12 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
         int used = n;
         const uint8_t* m = nullptr;
         if (cfg.ransac.iterations > 0) {
-            used = ransac_select(P, Q, n, rigid, cfg.ransac, cfg.flow.min_tracks, frame, mask,
-                                 wbest_c, wbest_h, wbest_m);
+            if (pre)  // hypotheses scored by ransac_score_kernel (one frame)
+                used = ransac_finish(P, Q, n, rigid, cfg.ransac, cfg.flow.min_tracks, frame,
+                                     merge_best(pre + pass * pre_ctas, pre_ctas), mask);
+            else
+                used = ransac_select(P, Q, n, rigid, cfg.ransac, cfg.flow.min_tracks, frame, mask, wbest_c,
+                                     wbest_h);
             m = used == n ? nullptr : mask;
         }
         const FitOut r = estimate(P, Q, m, n, used, rigid, red);
@@ -290,12 +363,22 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
 
 void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
-                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames) {
+                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames, int2* pre_scratch) {
     if (nframes <= 0) return;
     const size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
     ensure_smem(fit_kernel, smem);
+    const int2* pre = nullptr;
+    int G = 0;
+    if (nframes == 1 && pre_scratch && cfg.ransac.iterations > 0 && stream_frames == 0) {
+        // one frame: spread its hypotheses over G CTAs (one per warp), then fit
+        G = std::min(kFitPreCtas, (cfg.ransac.iterations + FIT_WARPS - 1) / FIT_WARPS);
+        const size_t ssm = (size_t)max_pts * 2 * sizeof(double2);
+        ensure_smem(ransac_score_kernel, ssm);
+        ransac_score_kernel<<<G, FIT_THREADS, ssm, st>>>(trk_prev, trk_cur, trk_n, frame_index0, cfg, pre_scratch);
+        pre = pre_scratch;
+    }
     fit_kernel<<<nframes, FIT_THREADS, smem, st>>>(trk_prev, trk_cur, trk_n, max_pts, frame_index0,
-                                                   cfg, out, stream_frames);
+                                                   cfg, out, stream_frames, pre, G);
 }
 
 }  // namespace stabgpu
@@ -311,7 +394,6 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_single_kernel(const double2* 
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ double red[FIT_WARPS];
     __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
-    __shared__ Model wbest_m[FIT_WARPS];
     double2* P = reinterpret_cast<double2*>(fsm);
     double2* Q = P + n;
     uint8_t* mask = reinterpret_cast<uint8_t*>(Q + n);
@@ -325,7 +407,7 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_single_kernel(const double2* 
     int used = n;
     const uint8_t* m = nullptr;
     if (n >= 2 && rc.iterations > 0) {
-        used = ransac_select(P, Q, n, rigid, rc, min_tracks, frame, mask, wbest_c, wbest_h, wbest_m);
+        used = ransac_select(P, Q, n, rigid, rc, min_tracks, frame, mask, wbest_c, wbest_h);
         m = used == n ? nullptr : mask;
     }
     const FitOut r = estimate(P, Q, m, n, used, rigid, red);

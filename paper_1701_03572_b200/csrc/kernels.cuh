@@ -139,9 +139,13 @@ void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* tr
 
 // ---- K6 fit + RANSAC (k_fit.cu) ----
 // Fits frames [0, nframes) whose TrackSets are trk_*[f*max_pts ...], trk_n[f].
+// pre_scratch (2 * kFitPreCtas int2): with nframes == 1, RANSAC's hypotheses are
+// scored by kFitPreCtas CTAs first (Stage II), then the fit CTA merges them
+constexpr int kFitPreCtas = 32;
 void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
-                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames = 0);
+                stabgpu_motion_record* out, cudaStream_t st, long long stream_frames = 0,
+                int2* pre_scratch = nullptr);
 
 // ---- K7 plan (k_plan.cu) ----
 struct PlanState {  // carried across incremental calls (selector + prefix)

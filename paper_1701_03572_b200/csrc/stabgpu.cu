@@ -1426,6 +1426,7 @@ struct stabgpu_stream {
     DetectScratch ds{};
     double2 *pts = nullptr, *nxt = nullptr, *fwd = nullptr, *trk_prev = nullptr, *trk_cur = nullptr;
     int *npts = nullptr, *nnxt = nullptr, *trk_n = nullptr;
+    int2* fit_pre = nullptr;  // per-CTA RANSAC results of the one-frame fit
     double* score = nullptr;
     uint8_t* keep = nullptr;
     unsigned* work = nullptr;
@@ -1567,7 +1568,8 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     if ((rc = salloc(s, &s->pts, maxc)) || (rc = salloc(s, &s->nxt, maxc)) || (rc = salloc(s, &s->fwd, maxc)) ||
         (rc = salloc(s, &s->trk_prev, maxc)) || (rc = salloc(s, &s->trk_cur, maxc)) ||
         (rc = salloc(s, &s->npts, 1)) || (rc = salloc(s, &s->nnxt, 1)) || (rc = salloc(s, &s->trk_n, 1)) ||
-        (rc = salloc(s, &s->score, maxc)) || (rc = salloc(s, &s->keep, maxc)) || (rc = salloc(s, &s->work, 1)))
+        (rc = salloc(s, &s->score, maxc)) || (rc = salloc(s, &s->keep, maxc)) || (rc = salloc(s, &s->work, 1)) ||
+        (rc = salloc(s, &s->fit_pre, 2 * kFitPreCtas)))
         return fail(rc);
     if ((rc = stream_grow(s, 256))) return fail(rc);
     if ((rc = init_plan_state(ctx, cfg, &s->ps))) return fail(rc);
@@ -1650,7 +1652,7 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         k.work = s->work;
         launch_lk(k, cfg.flow, st);
         launch_compact(k, s->nxt, s->nnxt, s->trk_prev, s->trk_cur, s->trk_n, 1, st);
-        launch_fit(s->trk_prev, s->trk_cur, s->trk_n, maxc, 1, f, cfg, s->motion + f, st);
+        launch_fit(s->trk_prev, s->trk_cur, s->trk_n, maxc, 1, f, cfg, s->motion + f, st, 0, s->fit_pre);
         std::swap(s->pts, s->nxt);
         std::swap(s->npts, s->nnxt);
         if (f % R == 0) launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
