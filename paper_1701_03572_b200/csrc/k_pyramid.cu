@@ -185,6 +185,53 @@ __global__ void __launch_bounds__(SPT) pyramid_stream_kernel(const uint8_t* __re
 // register-streaming kernel (a few 8-byte loads per thread) cannot.
 // Threads = (column group of 4 outputs, row group); each row group walks its
 // rows with the same packed 16-bit filter as the streaming kernel.
+// Output rows [r0, r1) of one 4-column group from a staged band (cb = the
+// group's first byte in the band's row lo; olast = offset of the band's last
+// staged row).  Row pointers advance by 2w per output row; only the bottom
+// row of the frame can clamp (one min).  EDGE: the warp holds the first or
+// last column group (clamped neighbour words); interior warps load both
+// neighbour words unconditionally.
+template <bool EDGE>
+__device__ __forceinline__ void band_rows(const uint8_t* cb, int w, int h, int lo, int olast, int r0, int r1,
+                                          uint32_t* op, int ostep, bool hasL, bool hasR) {
+    auto brow = [&](const uint8_t* rp, uint32_t& a, uint32_t& b) {
+        const uint2 xy = *reinterpret_cast<const uint2*>(rp);
+        uint32_t L, R;
+        if (EDGE) {
+            L = hasL ? *reinterpret_cast<const uint32_t*>(rp - 4) : (xy.x & 0xFFu) * 0x01010101u;
+            R = hasR ? *reinterpret_cast<const uint32_t*>(rp + 8) : (xy.y >> 24) * 0x01010101u;
+        } else {
+            L = *reinterpret_cast<const uint32_t*>(rp - 4);
+            R = *reinterpret_cast<const uint32_t*>(rp + 8);
+        }
+        hrow(L, xy.x, xy.y, R, a, b);
+    };
+    auto rowp = [&](int y) { return cb + (clampi(y, 0, h - 1) - lo) * w; };
+    uint32_t a0, a1, a2, a3, a4, b0, b1, b2, b3, b4;
+    brow(rowp(2 * r0 - 2), a0, b0);
+    brow(rowp(2 * r0 - 1), a1, b1);
+    brow(rowp(2 * r0), a2, b2);
+    brow(rowp(2 * r0 + 1), a3, b3);
+    brow(rowp(2 * r0 + 2), a4, b4);
+    const uint8_t* last = cb + olast;
+    const uint8_t* rp = cb + (2 * r0 + 3 - lo) * w;  // row 2oy+1 of the next output row
+    for (int oy = r0;; rp += 2 * w, op += ostep) {
+        const uint32_t va = (a0 + a4) + 4u * (a1 + a3) + 6u * a2 + 0x00800080u;
+        const uint32_t vb = (b0 + b4) + 4u * (b1 + b3) + 6u * b2 + 0x00800080u;
+        *op = __byte_perm(va, vb, 0x7531);
+        if (++oy >= r1) break;
+        a0 = a2;
+        b0 = b2;
+        a1 = a3;
+        b1 = b3;
+        a2 = a4;
+        b2 = b4;
+        brow(rp, a3, b3);
+        const uint8_t* rq = rp + w;
+        brow(rq < last ? rq : last, a4, b4);
+    }
+}
+
 // BT threads per CTA, BBUF bytes per input buffer (two per CTA), MINB CTAs per SM
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -249,32 +296,18 @@ __global__ void __launch_bounds__(BT, MINB) pyramid_bulk_kernel(const uint8_t* _
         }
         const uint8_t* sb = pyr_smem + buf * BBUF;
         uint8_t* d = dst + (size_t)f * dst_stride;
+        const int olast = (min(h - 1, 2 * oy1) - lo) * w;
         for (int u = tid; u < ncg * rgroups; u += BT) {
             const int cg = u % ncg, rg = u / ncg;
             const int r0 = oy0 + rg * per, r1 = min(r0 + per, oy1);
+            const bool hasL = cg > 0, hasR = 8 * cg + 8 < w;
+            const bool edge = __any_sync(__activemask(), !(hasL && hasR));
             if (r0 >= r1) continue;
-#define BROW(Y, A, B) brow(sb + (size_t)(clampi((Y), 0, h - 1) - lo) * w, cg, w, A, B)
-            uint32_t a0, a1, a2, a3, a4, b0, b1, b2, b3, b4;
-            BROW(2 * r0 - 2, a0, b0);
-            BROW(2 * r0 - 1, a1, b1);
-            BROW(2 * r0, a2, b2);
-            BROW(2 * r0 + 1, a3, b3);
-            BROW(2 * r0 + 2, a4, b4);
-            for (int oy = r0;; ) {
-                const uint32_t va = (a0 + a4) + 4u * (a1 + a3) + 6u * a2 + 0x00800080u;
-                const uint32_t vb = (b0 + b4) + 4u * (b1 + b3) + 6u * b2 + 0x00800080u;
-                *reinterpret_cast<uint32_t*>(d + (size_t)oy * ow + 4 * cg) = __byte_perm(va, vb, 0x7531);
-                if (++oy >= r1) break;
-                a0 = a2;
-                b0 = b2;
-                a1 = a3;
-                b1 = b3;
-                a2 = a4;
-                b2 = b4;
-                BROW(2 * oy + 1, a3, b3);
-                BROW(2 * oy + 2, a4, b4);
-            }
-#undef BROW
+            uint32_t* op = reinterpret_cast<uint32_t*>(d + (size_t)r0 * ow + 4 * cg);
+            if (edge)
+                band_rows<true>(sb + 8 * cg, w, h, lo, olast, r0, r1, op, ow / 4, hasL, hasR);
+            else
+                band_rows<false>(sb + 8 * cg, w, h, lo, olast, r0, r1, op, ow / 4, hasL, hasR);
         }
         __syncthreads();  // buffer `buf` is refilled by the issue of iteration k + 1
     }
