@@ -313,6 +313,155 @@ __global__ void __launch_bounds__(BT, MINB) pyramid_bulk_kernel(const uint8_t* _
     }
 }
 
+// ---------------------------------------------------------------------------
+// Carry variant (one column group per thread, i.e. >= BT/2 groups): each CTA
+// takes a contiguous run of (frame, band) items, so consecutive items are
+// usually consecutive bands of one frame.  The thread's five filtered rows
+// then carry over from the previous band, and the next band's buffer holds
+// only its new rows (2 oy0 + 1 .. 2 oy1): no 3-row prologue and no halo
+// re-load per band.  A frame's first band (or a CTA's first item) starts with
+// the 5-row prologue as in pyramid_bulk_kernel.
+struct Rows5 {
+    uint32_t a0, a1, a2, a3, a4, b0, b1, b2, b3, b4;
+};
+
+template <bool EDGE>
+__device__ __forceinline__ void carry_band(Rows5& S, bool carry, const uint8_t* cb, int w, int h, int lo, int last,
+                                           int oy0, int oy1, uint32_t* op, int ostep, bool hasL, bool hasR) {
+    auto brow = [&](const uint8_t* rp, uint32_t& a, uint32_t& b) {
+        const uint2 xy = *reinterpret_cast<const uint2*>(rp);
+        uint32_t L, R;
+        if (EDGE) {
+            L = hasL ? *reinterpret_cast<const uint32_t*>(rp - 4) : (xy.x & 0xFFu) * 0x01010101u;
+            R = hasR ? *reinterpret_cast<const uint32_t*>(rp + 8) : (xy.y >> 24) * 0x01010101u;
+        } else {
+            L = *reinterpret_cast<const uint32_t*>(rp - 4);
+            R = *reinterpret_cast<const uint32_t*>(rp + 8);
+        }
+        hrow(L, xy.x, xy.y, R, a, b);
+    };
+    const uint8_t* lastp = cb + last;
+    const uint8_t* rp = cb + (2 * oy0 + 1 - lo) * w;  // row 2 oy0 + 1
+    if (carry) {  // the previous band left the rows of output oy0 - 1
+        S.a0 = S.a2;
+        S.b0 = S.b2;
+        S.a1 = S.a3;
+        S.b1 = S.b3;
+        S.a2 = S.a4;
+        S.b2 = S.b4;
+        brow(rp, S.a3, S.b3);
+        const uint8_t* rq = rp + w;
+        brow(rq < lastp ? rq : lastp, S.a4, S.b4);
+    } else {
+        auto rowp = [&](int y) { return cb + (clampi(y, 0, h - 1) - lo) * w; };
+        brow(rowp(2 * oy0 - 2), S.a0, S.b0);
+        brow(rowp(2 * oy0 - 1), S.a1, S.b1);
+        brow(rowp(2 * oy0), S.a2, S.b2);
+        brow(rowp(2 * oy0 + 1), S.a3, S.b3);
+        brow(rowp(2 * oy0 + 2), S.a4, S.b4);
+    }
+    rp += 2 * w;  // row 2 oy0 + 3
+    for (int oy = oy0;; rp += 2 * w, op += ostep) {
+        const uint32_t va = (S.a0 + S.a4) + 4u * (S.a1 + S.a3) + 6u * S.a2 + 0x00800080u;
+        const uint32_t vb = (S.b0 + S.b4) + 4u * (S.b1 + S.b3) + 6u * S.b2 + 0x00800080u;
+        *op = __byte_perm(va, vb, 0x7531);
+        if (++oy >= oy1) break;
+        S.a0 = S.a2;
+        S.b0 = S.b2;
+        S.a1 = S.a3;
+        S.b1 = S.b3;
+        S.a2 = S.a4;
+        S.b2 = S.b4;
+        brow(rp, S.a3, S.b3);
+        const uint8_t* rq = rp + w;
+        brow(rq < lastp ? rq : lastp, S.a4, S.b4);
+    }
+}
+
+template <int BT, int BBUF, int MINB>
+__global__ void __launch_bounds__(BT, MINB) pyramid_carry_kernel(const uint8_t* __restrict__ src, size_t src_stride,
+                                                                  int w, int h, uint8_t* __restrict__ dst,
+                                                                  size_t dst_stride, int frames, int band) {
+    extern __shared__ __align__(128) uint8_t pyr_smem[];
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const int ow = w / 2, oh = h / 2;
+    const int nb = (oh + band - 1) / band;
+    const long long total = (long long)nb * frames;
+    const long long i0 = total * blockIdx.x / gridDim.x, i1 = total * (blockIdx.x + 1) / gridDim.x;
+    const int tid = threadIdx.x;
+    auto carry_of = [&](long long item) { return item > i0 && (item % nb) != 0; };
+    auto region = [&](long long item, int& lo, int& hi) {
+        const int b = (int)(item % nb), oy0 = b * band, oy1 = min(oy0 + band, oh);
+        lo = carry_of(item) ? 2 * oy0 + 1 : max(0, 2 * oy0 - 2);
+        hi = min(h - 1, 2 * oy1);
+    };
+    auto issue = [&](long long item, int buf) {
+        const int f = (int)(item / nb);
+        int lo, hi;
+        region(item, lo, hi);
+        const uint32_t bytes = (uint32_t)(hi - lo + 1) * (uint32_t)w;
+        const uint32_t bar = su32(&mbar[buf]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                su32(pyr_smem + buf * BBUF)),
+            "l"(src + (size_t)f * src_stride + (size_t)lo * w), "r"(bytes), "r"(bar)
+            : "memory");
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (i0 < i1) issue(i0, 0);
+    }
+    __syncthreads();
+    const int ncg = ow / 4, cg = tid;
+    const bool act = cg < ncg, hasL = cg > 0, hasR = 8 * cg + 8 < w;
+    const bool edge = __any_sync(0xFFFFFFFFu, act && !(hasL && hasR));
+    Rows5 S{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int k = 0;
+    for (long long item = i0; item < i1; ++item, ++k) {
+        const int buf = k & 1;
+        if (tid == 0 && item + 1 < i1) issue(item + 1, buf ^ 1);
+        {
+            const uint32_t bar = su32(&mbar[buf]), phase = (uint32_t)((k >> 1) & 1);
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done)
+                    : "r"(bar), "r"(phase)
+                    : "memory");
+        }
+        if (act) {
+            const int f = (int)(item / nb), b = (int)(item % nb);
+            const int oy0 = b * band, oy1 = min(oy0 + band, oh);
+            int lo, hi;
+            region(item, lo, hi);
+            const uint8_t* cb = pyr_smem + buf * BBUF + 8 * cg;
+            uint32_t* op = reinterpret_cast<uint32_t*>(dst + (size_t)f * dst_stride + (size_t)oy0 * ow + 4 * cg);
+            const bool carry = carry_of(item);
+            if (edge)
+                carry_band<true>(S, carry, cb, w, h, lo, (hi - lo) * w, oy0, oy1, op, ow / 4, hasL, hasR);
+            else
+                carry_band<false>(S, carry, cb, w, h, lo, (hi - lo) * w, oy0, oy1, op, ow / 4, hasL, hasR);
+        }
+        __syncthreads();  // buffer `buf` is refilled by the issue of iteration k + 1
+    }
+}
+
+template <int BT, int BBUF, int MINB>
+void launch_carry(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst, size_t dst_stride, int frames,
+                  cudaStream_t st) {
+    const int oh = h / 2;
+    const int band = std::min(oh, BBUF / w / 2 - 1);  // 2 band + 4 rows (fresh) <= BBUF / w
+    ensure_smem(pyramid_carry_kernel<BT, BBUF, MINB>, 2 * BBUF);
+    const long long items = (long long)((oh + band - 1) / band) * frames;
+    const int grid = (int)std::min<long long>(items, (long long)sm_count() * MINB);
+    pyramid_carry_kernel<BT, BBUF, MINB><<<grid, BT, 2 * BBUF, st>>>(src, src_stride, w, h, dst, dst_stride, frames, band);
+}
+
 template <int BT, int BBUF, int MINB>
 void launch_bulk(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst, size_t dst_stride, int frames,
                  cudaStream_t st) {
@@ -343,7 +492,9 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
     if (bulk) {
         // two 48 KB buffers per CTA, two CTAs per SM (one CTA's loads overlap the
         // other's filtering); rows wider than ~3 KB take two 96 KB buffers
-        if ((48 * 1024 / w - 4) / 2 >= 6)
+        if (ow / 4 > 128 && ow / 4 <= 256 && 48 * 1024 / w / 2 - 1 >= 6)  // one column group per thread
+            launch_carry<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
+        else if ((48 * 1024 / w - 4) / 2 >= 6)
             launch_bulk<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
         else
             launch_bulk<512, 96 * 1024, 1>(src, src_stride, w, h, dst, dst_stride, frames, st);
