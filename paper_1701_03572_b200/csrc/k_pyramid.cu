@@ -492,8 +492,14 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
     if (bulk) {
         // two 48 KB buffers per CTA, two CTAs per SM (one CTA's loads overlap the
         // other's filtering); rows wider than ~3 KB take two 96 KB buffers
-        if (ow / 4 > 128 && ow / 4 <= 256 && 48 * 1024 / w / 2 - 1 >= 6)  // one column group per thread
+        // carry kernel when one CTA row of threads covers the row (one column group per thread)
+        const int ncg = ow / 4;
+        if (ncg > 256 && ncg <= 512 && 96 * 1024 / w / 2 - 1 >= 6)
+            launch_carry<512, 96 * 1024, 1>(src, src_stride, w, h, dst, dst_stride, frames, st);
+        else if (ncg > 128 && ncg <= 256 && 48 * 1024 / w / 2 - 1 >= 6)
             launch_carry<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
+        else if (ncg > 64 && ncg <= 128 && 24 * 1024 / w / 2 - 1 >= 6)
+            launch_carry<128, 24 * 1024, 4>(src, src_stride, w, h, dst, dst_stride, frames, st);
         else if ((48 * 1024 / w - 4) / 2 >= 6)
             launch_bulk<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
         else
