@@ -765,21 +765,26 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                         ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
                     }
                     const unsigned live = __ballot_sync(0xffffffffu, ok);
-                    unsigned conf = 0;  // earlier live lanes closer than min_distance
-                    for (unsigned rem = live; rem; rem &= rem - 1) {
-                        const int src = __ffs(rem) - 1;
+                    // earlier live lanes closer than min_distance: all 32 sources in an
+                    // unrolled loop, so the shuffles issue back to back instead of as a
+                    // dependent chain over the live set
+                    unsigned conf = 0;
+#pragma unroll
+                    for (int src = 0; src < 32; ++src) {
                         const int sx = __shfl_sync(0xffffffffu, x, src);
                         const int sy = __shfl_sync(0xffffffffu, y, src);
-                        if (src < lane) {
-                            const long long dx = x - sx, dy = y - sy;
-                            if ((double)(dx * dx + dy * dy) < md2) conf |= 1u << src;
-                        }
+                        const long long dx = x - sx, dy = y - sy;
+                        if (src < lane && ((live >> src) & 1u) && (double)(dx * dx + dy * dy) < md2)
+                            conf |= 1u << src;
                     }
-                    unsigned acc = 0;
-                    for (unsigned rem = live; rem; rem &= rem - 1) {
-                        const int k = __ffs(rem) - 1;
-                        const unsigned ck2 = __shfl_sync(0xffffffffu, conf, k);
-                        if (!(ck2 & acc)) acc |= 1u << k;
+                    unsigned acc = live;  // no conflict inside the batch: every live lane is accepted
+                    if (__ballot_sync(0xffffffffu, conf != 0)) {  // rank-order resolution
+                        acc = 0;
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            const unsigned ck2 = __shfl_sync(0xffffffffu, conf, k);
+                            if (((live >> k) & 1u) && !(ck2 & acc)) acc |= 1u << k;
+                        }
                     }
                     const int room = maxc - nacc;
                     while (__popc(acc) > room) acc &= ~(1u << (31 - __clz(acc)));
