@@ -15,13 +15,15 @@
 //   3. the output tile is written with 16-byte streaming stores.
 // So HBM sees one read and one write per plane byte.
 //
-// Exactness without fp64 per pixel.  Coordinates are carried in 16.48 fixed
-// point (int64 multiply-adds), the bilinear blend in fp32.  Each decision the
-// reference takes — integer part of a coordinate, in-bounds test, lround of
-// the blended value — is taken on the fast path only when the fast value is
-// provably on the same side of the decision boundary (coordinate error
-// < 2^-29 px against a 2.4e-7 px guard; value error <= 1.5e-4 against a
-// 2.5e-4 guard).  Per-row fixed-point starts (16.48) and the crop tables are
+// Exactness without fp64 per pixel.  Coordinates are carried in fixed point
+// (16.48 in the per-frame tables, 32.32 in the TMA kernel's row loops), the
+// bilinear blend in fp32.  Each decision the reference takes — integer part
+// of a coordinate, in-bounds test, lround of the blended value — is taken on
+// the fast path only when the fast value is provably on the same side of the
+// decision boundary (coordinate error < 5e-9 px against a 2.4e-7 px guard;
+// value error <= 6.4e-5 against a 1e-4 guard); away from the frame edges the
+// coordinate guard is not needed at all (see the 32.32 section below).
+// Per-row fixed-point starts (16.48) and the crop tables are
 // computed once per frame / geometry by compose_prep_kernel, so a tile's
 // setup is a handful of loads.  Otherwise the pixel is queued and recomputed
 // with the reference's own fp64 arithmetic — for luma including the
@@ -740,52 +742,13 @@ __device__ __forceinline__ uint32_t blend_bad(uint32_t a, uint32_t b, uint32_t c
     return (uint32_t)__float_as_int(m) & 0xFFu;
 }
 
-// Fast-path coordinate decode of a 16.48 point: fractions, integer parts,
-// in-bounds test; bad when a coordinate is within the guard of an integer.
+// Fast-path coordinate decode result (decode32 below): fractions, integer
+// parts, in-bounds test.
 struct Pt {
     float fx, fy;
     int ix, iy;
     bool inb;
 };
-
-__device__ __forceinline__ Pt decode(long long X, long long Y, unsigned limx, unsigned limy, bool valid,
-                                     bool& bad) {
-    Pt t;
-    const uint32_t fxs = (uint32_t)(X >> 16), fys = (uint32_t)(Y >> 16);
-    bad = valid && ((fxs + GUARD) < 2 * GUARD || (fys + GUARD) < 2 * GUARD);
-    t.ix = (int)(X >> 48);
-    t.iy = (int)(Y >> 48);
-    t.inb = valid && (unsigned)t.ix <= limx && (unsigned)t.iy <= limy;
-    t.fx = frac_f(fxs);
-    t.fy = frac_f(fys);
-    return t;
-}
-
-// One fast-path sample, branch-free: out-of-frame lanes read offset 0 and
-// take `outv`; bad when a decision is not certain.
-template <typename P>
-__device__ __forceinline__ uint32_t px1(P src, int pitch, int obase, long long X, long long Yc, unsigned limx,
-                                        unsigned limy, bool valid, uint32_t outv, bool& bad) {
-    const Pt t = decode(X, Yc, limx, limy, valid, bad);
-    const int o = t.inb ? t.iy * pitch + t.ix + obase : 0;
-    bool vb = false;
-    const uint32_t v = blend_bad(src[o], src[o + 1], src[o + pitch], src[o + pitch + 1], t.fx, t.fy, vb);
-    bad = bad || (t.inb && vb);
-    return t.inb ? v : outv;
-}
-
-// Two planes sharing a coordinate (chroma): b | r << 8
-template <typename P>
-__device__ __forceinline__ uint32_t px2(P s1, P s2, int pitch, int obase, long long X, long long Yc,
-                                        unsigned limx, unsigned limy, bool valid, bool& bad) {
-    const Pt t = decode(X, Yc, limx, limy, valid, bad);
-    const int o = t.inb ? t.iy * pitch + t.ix + obase : 0;
-    bool vb = false;
-    const uint32_t b = blend_bad(s1[o], s1[o + 1], s1[o + pitch], s1[o + pitch + 1], t.fx, t.fy, vb);
-    const uint32_t r = blend_bad(s2[o], s2[o + 1], s2[o + pitch], s2[o + pitch + 1], t.fx, t.fy, vb);
-    bad = bad || (t.inb && vb);
-    return t.inb ? (b | (r << 8)) : 0x8080u;
-}
 
 // Two fast blends at once on the packed fp32x2 pipe (FFMA2/FADD2): the
 // same arithmetic as blend_bad, lane-wise.  Returns rp | rq << 8.
