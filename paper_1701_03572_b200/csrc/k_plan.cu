@@ -28,6 +28,8 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
     // together), so lane 0 never waits on a dependent global load per frame.
     constexpr int RW = sizeof(stabgpu_motion_record) / 8;  // 15 eight-byte words
     __shared__ unsigned long long buf[32][RW];
+    __shared__ int finfo[32];
+    __shared__ double4 fcum[32];
     const int lane = threadIdx.x & 31;
     // one block per independent stream
     motion += blockIdx.x * stride;
@@ -47,58 +49,79 @@ __global__ void plan_scan_kernel(const stabgpu_motion_record* __restrict__ motio
             for (int k = 0; k < RW; ++k) buf[lane][k] = v[k];
         }
         __syncwarp();
+        // lane 0: the recurrences only (selector state, trajectory prefix) in
+        // reference order; the frame records are assembled by all lanes after
         if (lane == 0) {
             for (long long f = f0; f < f0 + nf; ++f) {
-        const stabgpu_motion_record m = *reinterpret_cast<const stabgpu_motion_record*>(buf[f - f0]);
-        stabgpu_frame_record r;
-        memset(&r, 0, sizeof r);
-        r.frame_kind = m.frame_kind;
-        r.n_tracks = m.n_tracks;
-        stabgpu_delta d{0.0, 0.0, 0.0, 0.0, s.current, 0};
-        if (m.frame_kind != STABGPU_FRAME_TRACKED) {
-            // note_skipped (motion.cpp:185-191)
-            if (s.since == 0) s.pending = 1;
-            s.since = (s.since + 1) % sel.dwell;
-            d.kind = s.current;
-            d.skipped = m.frame_kind == STABGPU_FRAME_SKIPPED;
-        } else {
-            if (s.since == 0) s.pending = 1;
-            const int st_r = m.status & 0xff, st_s = (m.status >> 8) & 0xff;
-            int use_rigid;
-            if (sel.mode == STABGPU_FORCE_RIGID || sel.mode == STABGPU_FORCE_SIMILARITY) {
-                use_rigid = sel.mode == STABGPU_FORCE_RIGID;
-                if (s.pending) {
-                    s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
-                    s.pending = 0;
-                    r.decision = 1;
+                const int j = (int)(f - f0);
+                const stabgpu_motion_record& m = *reinterpret_cast<const stabgpu_motion_record*>(buf[j]);
+                int info;  // bit 0: tracked, bit 1: rigid delta, bit 2: decision, bits 8+: kind of a zero delta
+                double dx = 0.0, dy = 0.0, da = 0.0, dls = 0.0;
+                if (m.frame_kind != STABGPU_FRAME_TRACKED) {
+                    // note_skipped (motion.cpp:185-191)
+                    if (s.since == 0) s.pending = 1;
+                    s.since = s.since + 1 == sel.dwell ? 0 : s.since + 1;
+                    info = s.current << 8;
+                } else {
+                    if (s.since == 0) s.pending = 1;
+                    const int st_r = m.status & 0xff, st_s = (m.status >> 8) & 0xff;
+                    int use_rigid, decision = 0;
+                    if (sel.mode == STABGPU_FORCE_RIGID || sel.mode == STABGPU_FORCE_SIMILARITY) {
+                        use_rigid = sel.mode == STABGPU_FORCE_RIGID;
+                        if (s.pending) {
+                            s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
+                            s.pending = 0;
+                            decision = 1;
+                        }
+                        const int e = use_rigid ? st_r : st_s;
+                        if (e && *err == 0) *err = e | (int)(f << 4);
+                    } else if (s.pending) {
+                        if ((st_r || st_s) && *err == 0) *err = (st_r ? st_r : st_s) | (int)(f << 4);
+                        use_rigid = m.e_rigid <= dmul(m.e_similarity, dadd(1.0, sel.margin));
+                        s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
+                        s.pending = 0;
+                        decision = 1;
+                    } else {
+                        use_rigid = s.current == STABGPU_RIGID;
+                        const int e = use_rigid ? st_r : st_s;
+                        if (e && *err == 0) *err = e | (int)(f << 4);
+                    }
+                    s.since = s.since + 1 == sel.dwell ? 0 : s.since + 1;
+                    const stabgpu_delta& d = use_rigid ? m.rigid : m.similarity;
+                    dx = d.dx;
+                    dy = d.dy;
+                    da = d.da;
+                    dls = d.dls;
+                    info = 1 | (use_rigid << 1) | (decision << 2);
                 }
-                const int e = use_rigid ? st_r : st_s;
-                if (e && *err == 0) *err = e | (int)(f << 4);
-            } else if (s.pending) {
-                if ((st_r || st_s) && *err == 0) *err = (st_r ? st_r : st_s) | (int)(f << 4);
-                use_rigid = m.e_rigid <= dmul(m.e_similarity, dadd(1.0, sel.margin));
-                s.current = use_rigid ? STABGPU_RIGID : STABGPU_SIMILARITY;
-                s.pending = 0;
-                r.decision = 1;
-            } else {
-                use_rigid = s.current == STABGPU_RIGID;
-                const int e = use_rigid ? st_r : st_s;
-                if (e && *err == 0) *err = e | (int)(f << 4);
+                // Trajectory::append (smoothing.cpp:16-24)
+                s.cum[0] = dadd(s.cum[0], dx);
+                s.cum[1] = dadd(s.cum[1], dy);
+                s.cum[2] = dadd(s.cum[2], da);
+                s.cum[3] = dadd(s.cum[3], dls);
+                finfo[j] = info;
+                fcum[j] = make_double4(s.cum[0], s.cum[1], s.cum[2], s.cum[3]);
             }
-            s.since = (s.since + 1) % sel.dwell;
-            d = use_rigid ? m.rigid : m.similarity;
-            d.skipped = 0;
-            r.n_inliers = use_rigid ? m.n_inliers_rigid : m.n_inliers_similarity;
         }
-        // Trajectory::append (smoothing.cpp:16-24)
-        s.cum[0] = dadd(s.cum[0], d.dx);
-        s.cum[1] = dadd(s.cum[1], d.dy);
-        s.cum[2] = dadd(s.cum[2], d.da);
-        s.cum[3] = dadd(s.cum[3], d.dls);
-        cum[f] = make_double4(s.cum[0], s.cum[1], s.cum[2], s.cum[3]);
-        r.delta = d;
-        rec[f] = r;
+        __syncwarp();
+        if (lane < nf) {  // frame record f0 + lane
+            const stabgpu_motion_record& m = *reinterpret_cast<const stabgpu_motion_record*>(buf[lane]);
+            const int info = finfo[lane];
+            stabgpu_frame_record r;
+            memset(&r, 0, sizeof r);
+            r.frame_kind = m.frame_kind;
+            r.n_tracks = m.n_tracks;
+            if (info & 1) {
+                const bool rigid = info & 2;
+                r.delta = rigid ? m.rigid : m.similarity;
+                r.delta.skipped = 0;
+                r.n_inliers = rigid ? m.n_inliers_rigid : m.n_inliers_similarity;
+                r.decision = (info >> 2) & 1;
+            } else {
+                r.delta = stabgpu_delta{0.0, 0.0, 0.0, 0.0, info >> 8, m.frame_kind == STABGPU_FRAME_SKIPPED};
             }
+            rec[f0 + lane] = r;
+            cum[f0 + lane] = fcum[lane];
         }
         __syncwarp();
     }
