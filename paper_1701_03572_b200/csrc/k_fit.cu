@@ -170,15 +170,25 @@ __device__ int2 ransac_score(const double2* P, const double2* Q, int n, bool rig
     const double thr2 = dmul(rc.threshold, rc.threshold);
     const uint64_t key = ransac_key(rc, frame);
     int best_c = 0, best_h = -1;
-    for (int h = first + wid; h < rc.iterations; h += stride) {
-        Model m;
-        if (!hypothesis(P, Q, n, rigid, key, h, m)) continue;
-        int cnt = 0;
-        for (int k = lane; k < n; k += 32) cnt += inlier(m, P[k], Q[k], thr2) ? 1 : 0;
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (cnt > best_c) {  // h ascends within a warp: strict > keeps the lowest h
-            best_c = cnt;
-            best_h = h;
+    // the warp's hypotheses h = first + wid + k * stride, 32 at a time: lane l
+    // builds the minimal model of k = kb + l (one model per lane instead of
+    // every lane building every model), then the warp scores them in k order
+    for (int h0 = first + wid; h0 < rc.iterations; h0 += 32 * stride) {
+        const int hl = h0 + lane * stride;
+        Model ml{0, 0, 0, 0};
+        const bool vl = hl < rc.iterations && hypothesis(P, Q, n, rigid, key, hl, ml);
+        const unsigned valid = __ballot_sync(0xffffffffu, vl);
+        for (unsigned rem = valid; rem; rem &= rem - 1) {
+            const int j = __ffs(rem) - 1;
+            const Model m{__shfl_sync(0xffffffffu, ml.a, j), __shfl_sync(0xffffffffu, ml.b, j),
+                          __shfl_sync(0xffffffffu, ml.tx, j), __shfl_sync(0xffffffffu, ml.ty, j)};
+            int cnt = 0;
+            for (int k = lane; k < n; k += 32) cnt += inlier(m, P[k], Q[k], thr2) ? 1 : 0;
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (cnt > best_c) {  // h ascends within a warp: strict > keeps the lowest h
+                best_c = cnt;
+                best_h = h0 + j * stride;
+            }
         }
     }
     if (lane == 0) {
