@@ -45,6 +45,7 @@ typedef enum stabgpu_status {
 #define STABGPU_MIN_FRAME_DIM 16 /* kMinFrameDim, frame.hpp:12 */
 #define STABGPU_MAX_LEVELS 16    /* pyramid levels a context can hold */
 #define STABGPU_MAX_RADIUS 31    /* flow.cpp:247-249 */
+#define STABGPU_MAX_RANSAC_ITERATIONS (1 << 24) /* RANSAC is new; bound keeps hypothesis indices in int */
 
 /* ---- configuration records (same field names and defaults) ---------- */
 
@@ -178,6 +179,13 @@ size_t stabgpu_pyramid_bytes(int w, int h, int max_levels);
 int stabgpu_build_pyramid(stabgpu_ctx* ctx, const uint8_t* host_src, int w, int h, int max_levels,
                           stabgpu_pyramid* out);
 
+/* build_pyramid over n frames of one size (host frames back to back) in the
+ * batched per-level launches Stage I uses.  host_out receives n packed
+ * pyramids of stabgpu_pyramid_bytes() each, levels in stabgpu_pyramid order;
+ * each equals build_pyramid of that frame alone. */
+int stabgpu_build_pyramid_batch(stabgpu_ctx* ctx, const uint8_t* host_frames, int n, int w, int h,
+                                int max_levels, uint8_t* host_out);
+
 /* gradients, image_ops.hpp:15 / image_ops.cpp:79-96 (host doubles out). */
 int stabgpu_gradients(stabgpu_ctx* ctx, const uint8_t* host_src, int w, int h, double* host_gx,
                       double* host_gy);
@@ -211,6 +219,14 @@ int stabgpu_min_eig_response(stabgpu_ctx* ctx, const uint8_t* host_src, int w, i
 int stabgpu_detect_corners(stabgpu_ctx* ctx, const uint8_t* host_src, int w, int h,
                            const stabgpu_detect_cfg* cfg, double* host_xy, double* host_score,
                            int* n_out);
+
+/* detect_corners over n frames of one size in one batch (host frames
+ * back to back, w*h bytes each): the batched K2-K4 launch Stage I uses.
+ * Frame f's corners: host_xy[2*max_corners*f ...], host_score[max_corners*f
+ * ...], n_out[f].  Each frame equals detect_corners of that frame alone. */
+int stabgpu_detect_corners_batch(stabgpu_ctx* ctx, const uint8_t* host_frames, int n, int w, int h,
+                                 const stabgpu_detect_cfg* cfg, double* host_xy, double* host_score,
+                                 int* n_out);
 
 /* track_lk, flow.hpp:35-36 / flow.cpp:243-256. */
 int stabgpu_track_lk(stabgpu_ctx* ctx, const stabgpu_pyramid* prev, const stabgpu_pyramid* cur,
@@ -376,6 +392,11 @@ typedef struct stabgpu_stats {
     long long lk_iterations;
 } stabgpu_stats;
 int stabgpu_get_stats(stabgpu_ctx* ctx, stabgpu_stats* out);
+
+/* Test/diagnostic hook: copies up to `bytes` of the context's named device
+ * scratch buffer (e.g. "trk_prev", "trk_n" of the last Stage I motion pass)
+ * to host; *have = the buffer's size.  No reference analogue. */
+int stabgpu_debug_read_scratch(stabgpu_ctx* ctx, const char* name, void* host, size_t bytes, size_t* have);
 int stabgpu_enable_timing(stabgpu_ctx* ctx, int on);
 
 #ifdef __cplusplus

@@ -100,6 +100,7 @@ PROTOTYPES = {
     "stabgpu_synchronize": (I, [V]),
     "stabgpu_pyramid_bytes": (C.c_size_t, [I, I, I]),
     "stabgpu_build_pyramid": (I, [V, V, I, I, I, P(Pyramid)]),
+    "stabgpu_build_pyramid_batch": (I, [V, V, I, I, I, I, V]),
     "stabgpu_gradients": (I, [V, V, I, I, V, V]),
     "stabgpu_warp_similarity": (I, [V, V, I, I, P(Transform), V]),
     "stabgpu_crop_resize": (I, [V, V, I, I, C.c_double, V]),
@@ -107,6 +108,7 @@ PROTOTYPES = {
     "stabgpu_detection_roi": (I, [I, I, C.c_double, P(Roi)]),
     "stabgpu_min_eig_response": (I, [V, V, I, I, I, V]),
     "stabgpu_detect_corners": (I, [V, V, I, I, P(DetectCfg), V, V, c_ip]),
+    "stabgpu_detect_corners_batch": (I, [V, V, I, I, I, P(DetectCfg), V, V, c_ip]),
     "stabgpu_track_lk": (I, [V, P(Pyramid), P(Pyramid), V, I, P(FlowCfg), V, V]),
     "stabgpu_weed_tracks": (I, [V, P(Pyramid), P(Pyramid), V, V, I, P(FlowCfg), V, V, c_ip]),
     "stabgpu_estimate": (I, [V, V, V, I, I, P(Transform)]),
@@ -132,6 +134,7 @@ PROTOTYPES = {
     "stabgpu_stabilize_sequence_rgb": (I, [V, V, I, I, I, P(Config), V, V]),
     "stabgpu_interframe_sse": (I, [V, V, I, I, I, C.c_double, V, P(C.c_int64)]),
     "stabgpu_get_stats": (I, [V, P(Stats)]),
+    "stabgpu_debug_read_scratch": (I, [V, C.c_char_p, V, C.c_size_t, C.POINTER(C.c_size_t)]),
     "stabgpu_enable_timing": (I, [V, I]),
 }
 

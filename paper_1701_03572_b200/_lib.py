@@ -107,6 +107,19 @@ class Context:
         check(load().stabgpu_get_stats(self.handle, C.byref(s)))
         return s
 
+    def read_scratch(self, name: str, dtype, count: int | None = None):
+        """Diagnostic: a copy of the named device scratch buffer as numpy."""
+        import numpy as np
+
+        have = C.c_size_t(0)
+        check(load().stabgpu_debug_read_scratch(self.handle, name.encode(), None, 0, C.byref(have)))
+        dt = np.dtype(dtype)
+        n = have.value // dt.itemsize if count is None else count
+        out = np.zeros(n, dt)
+        check(load().stabgpu_debug_read_scratch(self.handle, name.encode(), C.c_void_p(out.ctypes.data),
+                                                out.nbytes, None))
+        return out
+
     def enable_timing(self, on: bool = True) -> None:
         check(load().stabgpu_enable_timing(self.handle, 1 if on else 0))
 
@@ -119,3 +132,13 @@ def context(device: int = 0) -> Context:
         with _lock:
             _contexts[device] = ctx
     return ctx
+
+
+def reset_contexts() -> None:
+    """Destroys the cached contexts (the next call gets a fresh one with empty
+    scratch pools)."""
+    with _lock:
+        ctxs = list(_contexts.values())
+        _contexts.clear()
+    for c in ctxs:
+        c.close()

@@ -109,16 +109,19 @@ inline int sm_count() {
     return n;
 }
 
-// opt the kernel in to `bytes` of dynamic shared memory (only when it grows)
+// opt the kernel in to `bytes` of dynamic shared memory (only when it grows).
+// The size is cached only when the attribute was accepted; a refused size
+// leaves the error for the launch check (check_launch) to report.
 template <typename K>
-inline void ensure_smem(K* fn, size_t bytes) {
+inline cudaError_t ensure_smem(K* fn, size_t bytes) {
     LaunchCache& c = launch_cache();
     const auto key = std::make_pair(reinterpret_cast<const void*>(fn), cur_device());
     std::lock_guard<std::mutex> g(c.m);
     auto it = c.smem.find(key);
-    if (it != c.smem.end() && it->second >= bytes) return;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    c.smem[key] = bytes;
+    if (it != c.smem.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c.smem[key] = bytes;
+    return e;
 }
 
 template <typename K>

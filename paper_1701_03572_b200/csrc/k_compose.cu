@@ -1337,7 +1337,8 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
     const size_t bytes = sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) +
                          sizeof(TileParams) * ntiles + 512;
     char* buf = nullptr;
-    cudaMallocAsync((void**)&buf, bytes, st);
+    // a failed allocation stays in cudaGetLastError for the caller's check_launch
+    if (cudaMallocAsync((void**)&buf, bytes, st) != cudaSuccess) return;
     Tables T;
     long long* q = reinterpret_cast<long long*>(buf);
     T.rxf = q;

@@ -893,8 +893,13 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     int* g_anext = nullptr;
     if (cfg.max_corners > SMEM_CORNERS) {
         // large budgets keep the accepted list in global scratch (sort_idx tail is free)
-        cudaMallocAsync((void**)&g_axy, sizeof(short2) * (size_t)nD * cfg.max_corners, st);
-        cudaMallocAsync((void**)&g_anext, sizeof(int) * (size_t)nD * cfg.max_corners, st);
+        // a failed allocation stays in cudaGetLastError for the caller's check_launch
+        if (cudaMallocAsync((void**)&g_axy, sizeof(short2) * (size_t)nD * cfg.max_corners, st) != cudaSuccess)
+            return;
+        if (cudaMallocAsync((void**)&g_anext, sizeof(int) * (size_t)nD * cfg.max_corners, st) != cudaSuccess) {
+            cudaFreeAsync(g_axy, st);
+            return;
+        }
     }
     DetectScratch sf = s;
     if (!fast) sf.flags = nullptr;

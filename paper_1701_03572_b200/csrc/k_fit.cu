@@ -23,6 +23,8 @@ namespace {
 
 constexpr int FIT_THREADS = 512;
 constexpr int FIT_WARPS = FIT_THREADS / 32;
+// dynamic shared memory above this goes to the in-place (global memory) path
+constexpr size_t kFitSmemMax = 200 * 1024;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
                                                           long long frame_index0, stabgpu_config cfg,
                                                           stabgpu_motion_record* __restrict__ out,
                                                           long long stream_frames, const int2* __restrict__ pre,
-                                                          int pre_ctas) {
+                                                          int pre_ctas, uint8_t* __restrict__ gmask) {
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ double red[FIT_WARPS];
     __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
@@ -315,12 +317,23 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
         return;
     }
     rec.frame_kind = STABGPU_FRAME_TRACKED;
-    double2* P = reinterpret_cast<double2*>(fsm);
-    double2* Q = P + max_pts;
-    uint8_t* mask = reinterpret_cast<uint8_t*>(Q + max_pts);
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        P[k] = trk_prev[(size_t)f * max_pts + k];
-        Q[k] = trk_cur[(size_t)f * max_pts + k];
+    const double2* P;
+    const double2* Q;
+    uint8_t* mask;
+    if (gmask) {  // TrackSets too large for shared memory: work in place in global memory
+        P = trk_prev + (size_t)f * max_pts;
+        Q = trk_cur + (size_t)f * max_pts;
+        mask = gmask + (size_t)f * max_pts;
+    } else {
+        double2* sP = reinterpret_cast<double2*>(fsm);
+        double2* sQ = sP + max_pts;
+        mask = reinterpret_cast<uint8_t*>(sQ + max_pts);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            sP[k] = trk_prev[(size_t)f * max_pts + k];
+            sQ[k] = trk_cur[(size_t)f * max_pts + k];
+        }
+        P = sP;
+        Q = sQ;
     }
     __syncthreads();
     const int mode = cfg.selector.mode;
@@ -375,11 +388,19 @@ void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
                 stabgpu_motion_record* out, cudaStream_t st, long long stream_frames, int2* pre_scratch) {
     if (nframes <= 0) return;
-    const size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
+    size_t smem = (size_t)max_pts * (2 * sizeof(double2) + 1);
+    uint8_t* gmask = nullptr;
+    if (smem > kFitSmemMax) {
+        // more pairs than shared memory holds: the kernel reads the TrackSets in
+        // place and keeps the inlier masks in stream-ordered global scratch (a
+        // failed allocation stays in cudaGetLastError for check_launch)
+        if (cudaMallocAsync((void**)&gmask, (size_t)nframes * max_pts, st) != cudaSuccess) return;
+        smem = 0;
+    }
     ensure_smem(fit_kernel, smem);
     const int2* pre = nullptr;
     int G = 0;
-    if (nframes == 1 && pre_scratch && cfg.ransac.iterations > 0 && stream_frames == 0) {
+    if (!gmask && nframes == 1 && pre_scratch && cfg.ransac.iterations > 0 && stream_frames == 0) {
         // one frame: spread its hypotheses over G CTAs (one per warp), then fit
         G = std::min(kFitPreCtas, (cfg.ransac.iterations + FIT_WARPS - 1) / FIT_WARPS);
         const size_t ssm = (size_t)max_pts * 2 * sizeof(double2);
@@ -388,7 +409,8 @@ void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_
         pre = pre_scratch;
     }
     fit_kernel<<<nframes, FIT_THREADS, smem, st>>>(trk_prev, trk_cur, trk_n, max_pts, frame_index0,
-                                                   cfg, out, stream_frames, pre, G);
+                                                   cfg, out, stream_frames, pre, G, gmask);
+    if (gmask) cudaFreeAsync(gmask, st);
 }
 
 }  // namespace stabgpu
@@ -400,18 +422,25 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_single_kernel(const double2* 
                                                                  int n, int kind,
                                                                  stabgpu_ransac_cfg rc, int min_tracks,
                                                                  long long frame, FitResult* out,
-                                                                 uint8_t* __restrict__ gmask) {
+                                                                 uint8_t* __restrict__ gmask, bool in_place) {
     extern __shared__ __align__(16) unsigned char fsm[];
     __shared__ double red[FIT_WARPS];
     __shared__ int wbest_c[FIT_WARPS], wbest_h[FIT_WARPS];
-    double2* P = reinterpret_cast<double2*>(fsm);
-    double2* Q = P + n;
-    uint8_t* mask = reinterpret_cast<uint8_t*>(Q + n);
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        P[k] = gP[k];
-        Q[k] = gQ[k];
-        mask[k] = 1;
+    const double2* P = gP;
+    const double2* Q = gQ;
+    uint8_t* mask = gmask;  // in_place: too many pairs for shared memory, work in global memory
+    if (!in_place) {
+        double2* sP = reinterpret_cast<double2*>(fsm);
+        double2* sQ = sP + n;
+        mask = reinterpret_cast<uint8_t*>(sQ + n);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            sP[k] = gP[k];
+            sQ[k] = gQ[k];
+        }
+        P = sP;
+        Q = sQ;
     }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) mask[k] = 1;
     __syncthreads();
     const bool rigid = kind == STABGPU_RIGID;
     int used = n;
@@ -421,8 +450,9 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_single_kernel(const double2* 
         m = used == n ? nullptr : mask;
     }
     const FitOut r = estimate(P, Q, m, n, used, rigid, red);
-    for (int k = threadIdx.x; k < n; k += blockDim.x)
-        if (gmask) gmask[k] = mask[k];
+    if (!in_place)
+        for (int k = threadIdx.x; k < n; k += blockDim.x)
+            if (gmask) gmask[k] = mask[k];
     if (threadIdx.x == 0) *out = FitResult{r.tx, r.ty, r.theta, r.s, r.status, used};
 }
 
@@ -440,9 +470,11 @@ __global__ void __launch_bounds__(FIT_THREADS) rms_single_kernel(const double2* 
 void launch_fit_single(const double2* P, const double2* Q, int n, int kind,
                        const stabgpu_ransac_cfg& rc, int min_tracks, long long frame,
                        FitResult* out, uint8_t* mask, cudaStream_t st) {
-    const size_t smem = (size_t)n * (2 * sizeof(double2) + 1) + 16;
+    size_t smem = (size_t)n * (2 * sizeof(double2) + 1) + 16;
+    const bool in_place = smem > kFitSmemMax && mask;
+    if (in_place) smem = 0;
     ensure_smem(fit_single_kernel, smem);
-    fit_single_kernel<<<1, FIT_THREADS, smem, st>>>(P, Q, n, kind, rc, min_tracks, frame, out, mask);
+    fit_single_kernel<<<1, FIT_THREADS, smem, st>>>(P, Q, n, kind, rc, min_tracks, frame, out, mask, in_place);
 }
 
 void launch_rms_single(const double2* P, const double2* Q, int n, stabgpu_transform t, double* out,

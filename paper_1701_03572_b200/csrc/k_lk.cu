@@ -975,7 +975,7 @@ void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t
     ensure_smem(kern, smem);
     const int sms = sm_count(), per_sm = blocks_per_sm(kern, wpc * 32, smem);
     cudaMemsetAsync(c.work, 0, sizeof(unsigned), st);
-    cudaMemsetAsync(c.alive, 0, (size_t)c.R * c.nseg * c.max_pts, st);
+    cudaMemsetAsync(c.alive, 0, (size_t)c.steps * c.nseg * c.max_pts, st);
     const long long items = (long long)c.nseg * c.max_pts;
     const long long want = (items + wpc - 1) / wpc;
     const int grid = (int)std::min<long long>(want, (long long)sms * std::max(per_sm, 1));

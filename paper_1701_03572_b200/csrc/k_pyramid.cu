@@ -451,11 +451,16 @@ __global__ void __launch_bounds__(BT, MINB) pyramid_carry_kernel(const uint8_t* 
     }
 }
 
+// output rows per band of the carry kernel with `bbuf`-byte buffers
+inline int carry_band_rows(int bbuf, int w) { return (bbuf / w - 3) / 2; }
+
 template <int BT, int BBUF, int MINB>
 void launch_carry(const uint8_t* src, size_t src_stride, int w, int h, uint8_t* dst, size_t dst_stride, int frames,
                   cudaStream_t st) {
     const int oh = h / 2;
-    const int band = std::min(oh, BBUF / w / 2 - 1);  // 2 band + 4 rows (fresh) <= BBUF / w
+    // a CTA's first band (no carry) stages rows 2 oy0 - 2 .. 2 oy0 + 2 band:
+    // 2 band + 3 rows must fit the buffer
+    const int band = std::min(oh, carry_band_rows(BBUF, w));
     ensure_smem(pyramid_carry_kernel<BT, BBUF, MINB>, 2 * BBUF);
     const long long items = (long long)((oh + band - 1) / band) * frames;
     const int grid = (int)std::min<long long>(items, (long long)sm_count() * MINB);
@@ -494,11 +499,11 @@ void launch_pyramid_level(const uint8_t* src, size_t src_stride, int w, int h, u
         // other's filtering); rows wider than ~3 KB take two 96 KB buffers
         // carry kernel when one CTA row of threads covers the row (one column group per thread)
         const int ncg = ow / 4;
-        if (ncg > 256 && ncg <= 512 && 96 * 1024 / w / 2 - 1 >= 6)
+        if (ncg > 256 && ncg <= 512 && carry_band_rows(96 * 1024, w) >= 6)
             launch_carry<512, 96 * 1024, 1>(src, src_stride, w, h, dst, dst_stride, frames, st);
-        else if (ncg > 128 && ncg <= 256 && 48 * 1024 / w / 2 - 1 >= 6)
+        else if (ncg > 128 && ncg <= 256 && carry_band_rows(48 * 1024, w) >= 6)
             launch_carry<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);
-        else if (ncg > 64 && ncg <= 128 && 24 * 1024 / w / 2 - 1 >= 6)
+        else if (ncg > 64 && ncg <= 128 && carry_band_rows(24 * 1024, w) >= 6)
             launch_carry<128, 24 * 1024, 4>(src, src_stride, w, h, dst, dst_stride, frames, st);
         else if ((48 * 1024 / w - 4) / 2 >= 6)
             launch_bulk<256, 48 * 1024, 2>(src, src_stride, w, h, dst, dst_stride, frames, st);

@@ -123,6 +123,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st);
 struct LkChain {
     DevPyramid pyr;
     int R, nseg, max_pts, nframes;
+    int steps;           // planes of pos/alive: min(R, F - 1), the most steps any segment takes
     int F, nsps;         // segment map (seg_base / seg_end)
     const double2* pts;  // [nseg][max_pts] detected points (frame seg_base(seg))
     const int* npts;     // [nseg]

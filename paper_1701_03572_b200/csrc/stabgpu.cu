@@ -304,6 +304,7 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         LkChain c;
         c.pyr = P;
         c.R = R;
+        c.steps = steps;
         c.nseg = nseg;
         c.max_pts = maxc;
         c.nframes = nF;
@@ -443,6 +444,9 @@ int validate_all(const stabgpu_config& c) {
         return set_err(STABGPU_INVALID_CONFIG, "window_radius above 31 is not supported");
     if (c.ransac.iterations < 0 || (c.ransac.iterations > 0 && !(c.ransac.threshold > 0.0)))
         return set_err(STABGPU_INVALID_CONFIG, "ransac needs iterations >= 0 and threshold > 0");
+    // hypothesis indices stay in int with the scoring strides (h + 32 * stride)
+    if (c.ransac.iterations > STABGPU_MAX_RANSAC_ITERATIONS)
+        return set_err(STABGPU_INVALID_CONFIG, "ransac iterations above 2^24 are not supported");
     if (c.selector.mode < 0 || c.selector.mode > 2)
         return set_err(STABGPU_INVALID_CONFIG, "unknown selection mode");
     return STABGPU_OK;
@@ -544,6 +548,20 @@ int stabgpu_get_stats(stabgpu_ctx* c, stabgpu_stats* out) {
     return STABGPU_OK;
 }
 
+int stabgpu_debug_read_scratch(stabgpu_ctx* c, const char* name, void* host, size_t bytes, size_t* have) {
+    cudaSetDevice(c->device);
+    auto it = c->bufs.find(name);
+    if (it == c->bufs.end() || !it->second.p) {
+        if (have) *have = 0;
+        return set_err(STABGPU_INVALID_INPUT, "no scratch buffer named '%s'", name);
+    }
+    if (have) *have = it->second.n;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const size_t nb = std::min(bytes, it->second.n);
+    if (host && nb) CUDA_TRY(cudaMemcpy(host, it->second.p, nb, cudaMemcpyDeviceToHost));
+    return STABGPU_OK;
+}
+
 size_t stabgpu_pyramid_bytes(int w, int h, int max_levels) {
     int lw[STABGPU_MAX_LEVELS], lh[STABGPU_MAX_LEVELS];
     if (w < 1 || h < 1 || max_levels < 1) return 0;
@@ -554,6 +572,38 @@ size_t stabgpu_pyramid_bytes(int w, int h, int max_levels) {
 }
 
 // ---- per-stage ABI ----------------------------------------------------
+
+int stabgpu_build_pyramid_batch(stabgpu_ctx* ctx, const uint8_t* src, int nframes, int w, int h,
+                                int max_levels, uint8_t* out) {
+    TRY(validate_frame(w, h));
+    if (max_levels < 1) return set_err(STABGPU_INVALID_INPUT, "max_levels must be >= 1");
+    if (nframes < 1) return set_err(STABGPU_INVALID_INPUT, "build_pyramid_batch needs at least 1 frame");
+    cudaSetDevice(ctx->device);
+    int lw[STABGPU_MAX_LEVELS], lh[STABGPU_MAX_LEVELS];
+    const int L = level_dims(w, h, max_levels, lw, lh);
+    const size_t per = stabgpu_pyramid_bytes(w, h, max_levels);
+    cudaStream_t st = ctx->stream;
+    // the Stage I layout: one [frames][h_l][w_l] array per level, one launch per level
+    DBUF(uint8_t, d, "api_pyr_batch", per * nframes);
+    CUDA_TRY(cudaMemcpyAsync(d, src, (size_t)w * h * nframes, cudaMemcpyHostToDevice, st));
+    size_t lvl_off = 0, pk_off = 0;
+    for (int l = 0; l < L; ++l) {
+        const size_t stride = (size_t)lw[l] * lh[l];
+        if (l > 0) {
+            const size_t pstride = (size_t)lw[l - 1] * lh[l - 1];
+            launch_pyramid_level(d + lvl_off - pstride * nframes, pstride, lw[l - 1], lh[l - 1], d + lvl_off, stride,
+                                 nframes, st);
+            ++ctx->stats.launches;
+        }
+        // frame f's level l goes to out + f * per + pk_off (stabgpu_pyramid packing)
+        CUDA_TRY(cudaMemcpy2DAsync(out + pk_off, per, d + lvl_off, stride, stride, nframes, cudaMemcpyDeviceToHost, st));
+        lvl_off += stride * nframes;
+        pk_off += stride;
+    }
+    TRY(check_launch("pyramid"));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return STABGPU_OK;
+}
 
 int stabgpu_build_pyramid(stabgpu_ctx* ctx, const uint8_t* src, int w, int h, int max_levels,
                           stabgpu_pyramid* out) {
@@ -626,44 +676,53 @@ int stabgpu_detection_roi(int w, int h, double margin, stabgpu_roi* out) {
 
 int stabgpu_detect_corners(stabgpu_ctx* ctx, const uint8_t* src, int w, int h,
                            const stabgpu_detect_cfg* cfg, double* xy, double* score, int* n_out) {
-    *n_out = 0;
+    return stabgpu_detect_corners_batch(ctx, src, 1, w, h, cfg, xy, score, n_out);
+}
+
+int stabgpu_detect_corners_batch(stabgpu_ctx* ctx, const uint8_t* src, int nframes, int w, int h,
+                                 const stabgpu_detect_cfg* cfg, double* xy, double* score, int* n_out) {
+    for (int f = 0; f < nframes; ++f) n_out[f] = 0;
     TRY(validate_frame(w, h));
     TRY(validate_detect(*cfg));
+    if (nframes < 1) return set_err(STABGPU_INVALID_INPUT, "detect_corners_batch needs at least 1 frame");
     stabgpu_roi roi;
     TRY(roi_of(w, h, cfg->roi_margin, &roi));
     cudaSetDevice(ctx->device);
     const size_t n = (size_t)w * h, cap = (size_t)(roi.x1 - roi.x0) * (roi.y1 - roi.y0);
-    const int maxc = cfg->max_corners;
+    const int maxc = cfg->max_corners, nb = nframes;
     cudaStream_t st = ctx->stream;
-    DBUF(uint8_t, d, "api_img", n);
-    DBUF(unsigned long long, maxbits, "det_max", 1);
-    DBUF(unsigned int, dcount, "det_count", 1);
-    DBUF(unsigned long long, ckey, "det_ckey", cap);
-    DBUF(unsigned int, cidx, "det_cidx", cap);
-    DBUF(unsigned long long, skey, "det_skey", cap);
-    DBUF(unsigned int, sidx, "det_sidx", cap);
-    DBUF(double2, pts, "api_pts", maxc);
-    DBUF(double, sc, "api_score", maxc);
-    DBUF(int, nn, "api_n", 1);
-    CUDA_TRY(cudaMemcpyAsync(d, src, n, cudaMemcpyHostToDevice, st));
-    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins);
-    DBUF(double, dlo, "det_lo", 1);
-    DBUF(unsigned char, dflags, "det_flags", 1);
-    DBUF(unsigned, dmlo, "det_mlo", 1);
+    DBUF(uint8_t, d, "api_img", n * nb);
+    DBUF(unsigned long long, maxbits, "det_max", nb);
+    DBUF(unsigned int, dcount, "det_count", nb);
+    DBUF(unsigned long long, ckey, "det_ckey", cap * nb);
+    DBUF(unsigned int, cidx, "det_cidx", cap * nb);
+    DBUF(unsigned long long, skey, "det_skey", cap * nb);
+    DBUF(unsigned int, sidx, "det_sidx", cap * nb);
+    DBUF(double2, pts, "api_pts", (size_t)maxc * nb);
+    DBUF(double, sc, "api_score", (size_t)maxc * nb);
+    DBUF(int, nn, "api_n", nb);
+    CUDA_TRY(cudaMemcpyAsync(d, src, n * nb, cudaMemcpyHostToDevice, st));
+    DBUF(unsigned int, dhist, "det_hist", (size_t)kRespBins * nb);
+    DBUF(double, dlo, "det_lo", nb);
+    DBUF(unsigned char, dflags, "det_flags", nb);
+    DBUF(unsigned, dmlo, "det_mlo", nb);
     DetectScratch ds{maxbits, dcount, dhist, ckey, cidx, skey, sidx, cap, dlo, dflags, dmlo};
     PlaneBatch fb{d, n, w, h};
-    launch_detect(fb, 1, *cfg, roi, ds, pts, sc, nn, st);
+    launch_detect(fb, nb, *cfg, roi, ds, pts, sc, nn, st);
     ctx->stats.launches += 3;
     TRY(check_launch("detect"));
-    int nc = 0;
-    CUDA_TRY(cudaMemcpyAsync(&nc, nn, sizeof nc, cudaMemcpyDeviceToHost, st));
+    std::vector<int> nc(nb);
+    CUDA_TRY(cudaMemcpyAsync(nc.data(), nn, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (nc > 0) {
-        CUDA_TRY(cudaMemcpyAsync(xy, pts, sizeof(double2) * nc, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(score, sc, sizeof(double) * nc, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-    }
-    *n_out = nc;
+    for (int f = 0; f < nb; ++f)
+        if (nc[f] > 0) {
+            CUDA_TRY(cudaMemcpyAsync(xy + (size_t)2 * maxc * f, pts + (size_t)maxc * f, sizeof(double2) * nc[f],
+                                     cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(score + (size_t)maxc * f, sc + (size_t)maxc * f, sizeof(double) * nc[f],
+                                     cudaMemcpyDeviceToHost, st));
+        }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int f = 0; f < nb; ++f) n_out[f] = nc[f];
     return STABGPU_OK;
 }
 

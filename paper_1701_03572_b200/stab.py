@@ -211,6 +211,39 @@ def build_pyramid(frame, max_levels: int, device: int = 0) -> Pyramid:
     return p
 
 
+def build_pyramid_batch(frames, max_levels: int, device: int = 0) -> list[list[np.ndarray]]:
+    """build_pyramid of every frame of an (n, h, w) stack in the batched
+    per-level launches Stage I uses -> per frame, its list of levels."""
+    f = np.ascontiguousarray(frames, np.uint8)
+    if f.ndim != 3:
+        raise InvalidInputError("frames must be (n, h, w)")
+    n, h, w = f.shape
+    if w < K_MIN_FRAME_DIM or h < K_MIN_FRAME_DIM:
+        raise InvalidInputError("frame smaller than 16x16")
+    if max_levels < 1:
+        raise InvalidInputError("max_levels must be >= 1")
+    lib = load()
+    per = lib.stabgpu_pyramid_bytes(w, h, max_levels)
+    out = np.empty((n, per), np.uint8)
+    check(lib.stabgpu_build_pyramid_batch(context(device).handle, _ptr(f), n, w, h, max_levels, _ptr(out)))
+    dims = []
+    lw, lh = w, h
+    for lev in range(max_levels):  # image_ops.cpp:71
+        if lev > 0:
+            if lw // 2 < K_MIN_FRAME_DIM or lh // 2 < K_MIN_FRAME_DIM:
+                break
+            lw, lh = lw // 2, lh // 2
+        dims.append((lh, lw))
+    res = []
+    for i in range(n):
+        off, lv = 0, []
+        for (hh, ww) in dims:
+            lv.append(out[i, off:off + hh * ww].reshape(hh, ww))
+            off += hh * ww
+        res.append(lv)
+    return res
+
+
 def gradients(frame, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
     """gradients, image_ops.hpp:15 / image_ops.cpp:79-96."""
     f = _frame(frame)
@@ -291,6 +324,24 @@ def detect_corners(frame, cfg: DetectConfig, device: int = 0) -> tuple[np.ndarra
     check(load().stabgpu_detect_corners(context(device).handle, _ptr(f), f.shape[1], f.shape[0],
                                         C.byref(cc), _ptr(xy), _ptr(sc), C.byref(n)))
     return xy[:n.value].copy(), sc[:n.value].copy()
+
+
+def detect_corners_batch(frames, cfg: DetectConfig, device: int = 0) -> list[tuple[np.ndarray, np.ndarray]]:
+    """detect_corners on every frame of an (n, h, w) stack in one batched
+    launch (the K2-K4 batch Stage I runs); frame f's result equals
+    detect_corners(frames[f])."""
+    f = np.ascontiguousarray(frames, np.uint8)
+    if f.ndim != 3:
+        raise InvalidInputError("frames must be (n, h, w)")
+    nb, h, w = f.shape
+    m = max(cfg.max_corners, 1)
+    xy = np.empty((nb, m, 2), np.float64)
+    sc = np.empty((nb, m), np.float64)
+    nn = np.zeros(nb, np.int32)
+    cc = cfg.c()
+    check(load().stabgpu_detect_corners_batch(context(device).handle, _ptr(f), nb, w, h, C.byref(cc),
+                                              _ptr(xy), _ptr(sc), nn.ctypes.data_as(C.POINTER(C.c_int))))
+    return [(xy[i, :nn[i]].copy(), sc[i, :nn[i]].copy()) for i in range(nb)]
 
 
 # ------------------------------------------------------------------ flow -----

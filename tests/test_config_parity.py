@@ -1,0 +1,162 @@
+"""GPU Stage I against the reference CPU path at BASELINE.json config scale
+(SURVEY.md §8d "Parity runs"): C1 and C2 full length, C3 and C4 first 100
+frames, C5 8 full streams.  Inputs are the seeded BASELINE generator's
+videos (synth/videogen.c), the same bytes for both sides.
+
+Checker: the unmodified reference compiled from its sources
+(oracle/_ref/libstabref.so; its segment-parallel driver is bit-identical to
+run_offline, test_oracle_pin.py) or, where that was not built, the C
+restatement (oracle/liboracle.so).  Contract: run_offline,
+/root/reference/proj/src/pipeline.cpp:182-235.
+
+Bars (north_star): identical corner sets on every detection frame; tracked
+positions within 0.01 px with identical ok flags; equal frame kinds, track and
+inlier counts, decisions; transform parameters within 1e-3; pixels within +-1.
+Each case prints its summary (pytest -s) and appends it to $PARITY_LOG when
+set."""
+from __future__ import annotations
+
+import json
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from paper_1701_03572_b200 import pipeline, stab
+from paper_1701_03572_b200.synth import CONFIGS, Video
+
+from . import _oracle, _parity
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# frames per config (SURVEY §8d parity runs)
+FRAMES = {"c1": 300, "c2": 600, "c3": 100, "c4": 100}
+POS_TOL = 0.01  # px, north_star
+
+
+def _checker():
+    if _oracle.have_reference():
+        return _oracle.reference(), os.cpu_count() or 1
+    return _oracle.oracle(), 1
+
+
+def _log(name, summary):
+    print(f"\n[parity {name}] " + json.dumps(summary))
+    p = os.environ.get("PARITY_LOG")
+    if p:
+        with open(p, "a") as f:
+            f.write(json.dumps({"case": name, **summary}) + "\n")
+
+
+def _render(name, count):
+    cfg = CONFIGS[name]
+    planes = Video(cfg.video, threads=os.cpu_count() or 1).render(0, count)
+    return cfg, planes
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_config_sequence(name):
+    cfg, planes = _render(name, FRAMES[name])
+    y = planes[0]
+    cb, cr = (planes[1], planes[2]) if len(planes) == 3 else (None, None)
+    gy, gb, gr, grec = pipeline.stabilize_sequence(y, cfg.stab, cb, cr)
+    ref, threads = _checker()
+    kw = {"threads": threads} if ref.prefix == "ref_" else {}
+    oy, ob, orr, orec = ref.stabilize_sequence(y, cfg.stab, cb, cr, **kw)
+    s = _parity.summarize(grec, orec, [gy, gb, gr], [oy, ob, orr])
+    s["checker"] = ref.prefix.rstrip("_")
+    _log(f"{name} sequence ({len(y)} frames)", s)
+    assert s["frame_kind_equal"] and s["kind_equal"] and s["decision_equal"]
+    assert s["n_tracks_equal"] and s["n_inliers_equal"]
+    assert s["max_delta_err"] <= _parity.PARAM_TOL and s["max_correction_err"] <= _parity.PARAM_TOL
+    assert s["max_pixel_diff"] <= _parity.PIXEL_TOL
+    # off-by-one pixels are rare .5-tie flips, not a systematic drift
+    assert s["pixels_off_frac"] <= 1e-3
+    # in practice the only difference is LK/fit summation order (~1e-12)
+    assert s["max_delta_err"] <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_config_detection_frames(name):
+    """Corner sets (positions, scores, order) of every detection frame of the
+    parity run are identical (features.cpp:89-141)."""
+    cfg, planes = _render(name, FRAMES[name])
+    y = planes[0]
+    R = cfg.stab.flow.redetect_interval
+    frames = list(range(0, len(y) - 1, R))
+    ref, _ = _checker()
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:  # ctypes releases the GIL
+        cpu = list(ex.map(lambda f: ref.detect_corners(y[f], cfg.stab.detect), frames))
+    bad = []
+    counts = []
+    for f, (oxy, osc) in zip(frames, cpu):
+        gxy, gsc = stab.detect_corners(y[f], cfg.stab.detect)
+        counts.append(len(gxy))
+        if not (np.array_equal(gxy, oxy) and np.array_equal(gsc, osc)):
+            bad.append(f)
+    _log(f"{name} detection", {"detection_frames": len(frames), "mismatched": bad,
+                               "corners_min": min(counts), "corners_max": max(counts)})
+    assert not bad
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_config_tracking(name):
+    """track_lk + weed_tracks on the first segment's frame pairs at config
+    scale: identical ok flags and weeded sets, positions within 0.01 px
+    (flow.cpp:132-280)."""
+    cfg, planes = _render(name, 6)
+    y = planes[0]
+    fc = cfg.stab.flow
+    ref, _ = _checker()
+    pts, _ = ref.detect_corners(y[0], cfg.stab.detect)
+    gp = [stab.build_pyramid(y[i], fc.max_levels) for i in range(len(y))]
+    op = [ref.build_pyramid(y[i], fc.max_levels)[0] for i in range(len(y))]
+    worst, flips, kept = 0.0, 0, 0
+    g_pts = o_pts = pts
+    for t in range(1, len(y)):
+        pg, okg = stab.track_lk(gp[t - 1], gp[t], g_pts, fc)
+        po, oko = ref.track_lk(op[t - 1], op[t], o_pts, fc)
+        flips += int((okg != oko).sum())
+        assert np.array_equal(okg, oko), f"ok flags differ at step {t}"
+        worst = max(worst, float(np.abs(pg[okg] - po[oko]).max()) if okg.any() else 0.0)
+        ts = stab.weed_tracks(gp[t - 1], gp[t], g_pts[okg], pg[okg], fc)
+        kp, kc = ref.weed_tracks(op[t - 1], op[t], o_pts[oko], po[oko], fc)
+        assert ts.size() == len(kp), f"weeded sets differ at step {t}"
+        if len(kc):  # carried points: each side tracks its own (they differ by ~1e-13)
+            worst = max(worst, float(np.abs(ts.prev_points - kp).max()), float(np.abs(ts.cur_points - kc).max()))
+        kept += len(kp)
+        g_pts, o_pts = ts.cur_points, kc  # carried points (flow.cpp:326)
+    _log(f"{name} tracking", {"steps": len(y) - 1, "points": len(pts), "kept_pairs": kept,
+                              "max_pos_err_px": worst, "ok_flips": flips})
+    assert worst <= POS_TOL
+
+
+def test_config_c5_streams():
+    """C5: 8 full 240-frame streams through the many-stream entry point, each
+    against the reference run on that stream alone."""
+    cfg = CONFIGS["c5"]
+    S = 8
+    spec = cfg.video
+    y = np.empty((S, spec.frames, spec.height, spec.width), np.uint8)
+    for k in range(S):
+        Video(spec, stream=k, threads=os.cpu_count() or 1).render(0, spec.frames, out=[y[k]])
+    gy, _, _, grec = pipeline.stabilize_streams(y, cfg.stab)
+    ref, threads = _checker()
+    kw = {"threads": threads} if ref.prefix == "ref_" else {}
+    summaries = []
+    for k in range(S):
+        oy, _, _, orec = ref.stabilize_sequence(y[k], cfg.stab, **kw)
+        summaries.append(_parity.summarize(grec[k], orec, [gy[k]], [oy]))
+    agg = {"streams": S, "frames": sum(s["frames"] for s in summaries),
+           "all_ok": all(s["ok"] for s in summaries),
+           "max_delta_err": max(s["max_delta_err"] for s in summaries),
+           "max_correction_err": max(s["max_correction_err"] for s in summaries),
+           "max_pixel_diff": max(s["max_pixel_diff"] for s in summaries),
+           "pixels_off": sum(s["pixels_off"] for s in summaries),
+           "pixels": sum(s["pixels"] for s in summaries)}
+    _log("c5 streams", agg)
+    for s in summaries:
+        assert s["frame_kind_equal"] and s["n_tracks_equal"] and s["n_inliers_equal"] and s["decision_equal"]
+        assert s["max_delta_err"] <= _parity.PARAM_TOL and s["max_pixel_diff"] <= _parity.PIXEL_TOL
+    assert agg["pixels_off"] <= 1e-3 * agg["pixels"]

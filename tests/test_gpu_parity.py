@@ -72,6 +72,33 @@ def test_pyramid_level_batches(orc, w, h, n):
         assert np.array_equal(got[i], ref[1]), i
 
 
+@pytest.mark.parametrize("w,h,n,levels", [
+    (640, 480, 60, 3),     # C1: 128-thread carry kernel at level 1, bulk below
+    (1280, 720, 40, 4),    # C2/C5: 256-thread carry kernel
+    (1920, 1080, 40, 4),   # C3: 256-thread carry kernel, then 128-thread carry (960)
+    (3840, 2160, 12, 5),   # C4: 512-thread carry kernel
+    (1008, 600, 50, 4),    # carry band rounding (buffer / width not a whole number of rows)
+    (976, 100, 300, 3),    # many short frames: CTA runs cross frame boundaries
+])
+def test_pyramid_batch_every_frame(orc, w, h, n, levels):
+    """Batched K1 (the Stage I launch) equals the reference pyramid on every
+    frame, at the BASELINE geometries and with enough frames that a CTA's run
+    of (frame, band) items carries filtered rows from band to band.  (Round 1
+    sized the 128-thread carry kernel's band one row too large for 640-wide
+    frames; its first band overran the staging buffer.)"""
+    rng = np.random.default_rng(w + h + n)
+    base = _data.noise_frame(w, h, 11)
+    frames = np.stack([np.roll(base, (3 * i, 5 * i), axis=(0, 1)) ^ rng.integers(0, 4, size=(h, w), dtype=np.uint8)
+                       for i in range(n)])
+    frames[0, :h // 3] = 255
+    got = stab.build_pyramid_batch(frames, levels)
+    for i in range(n):
+        _, ref = orc.build_pyramid(frames[i], levels)
+        assert len(got[i]) == len(ref)
+        for lev, (a, b) in enumerate(zip(got[i], ref)):
+            assert np.array_equal(a, b), (i, lev)
+
+
 @pytest.mark.parametrize("f,name", FRAMES)
 def test_gradients_response_bitexact(orc, f, name):
     gx, gy = stab.gradients(f)
@@ -325,6 +352,23 @@ def test_sequence_many_detection_frames(orc):
     n = 5 * (torch.cuda.get_device_properties(0).multi_processor_count + 12) + 1
     y = _data.video(frames=n, objects=1, jit_t=3.0)[0]
     cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    gy, _, _, grec = pipeline.stabilize_sequence(y, cfg)
+    oy, _, _, orec = orc.stabilize_sequence(y, cfg)
+    _compare_records(grec, orec)
+    mx, cnt = _offby(gy, oy)
+    assert mx <= 1 and cnt <= 0.0005 * gy.size
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_short_clip_large_corner_budget(orc, n):
+    """Fewer frames than the re-detect interval with a 1000-corner budget: the
+    chain's per-step planes are sized min(R, n - 1), and nothing is written
+    past them (run this file under compute-sanitizer to see it)."""
+    from paper_1701_03572_b200 import _lib
+
+    y = _data.video(320, 240, frames=n, jit_t=2.0, tex=512, blobs=200)[0]
+    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=50, corners=1000, min_dist=3.0)
+    _lib.reset_contexts()  # fresh context: no scratch left over from larger runs
     gy, _, _, grec = pipeline.stabilize_sequence(y, cfg)
     oy, _, _, orec = orc.stabilize_sequence(y, cfg)
     _compare_records(grec, orec)
