@@ -192,10 +192,24 @@ def cpu_reference(cfg, frames_y, frames_cb, frames_cr, threads):
     cb = None if frames_cb is None else np.ascontiguousarray(frames_cb)
     cr = None if frames_cr is None else np.ascontiguousarray(frames_cr)
     t0 = time.perf_counter()
-    ref.stabilize_sequence(y, cfg.stab, cb, cr, compose=True, threads=threads)
+    out = ref.stabilize_sequence(y, cfg.stab, cb, cr, compose=True, threads=threads)
     dt = time.perf_counter() - t0
     del C
-    return len(y) / dt, dt
+    return len(y) / dt, dt, out
+
+
+def sample_parity(cfg, planes, ref_out):
+    """Our Stage I on the cpu_baseline sample against the reference's output
+    for it (tests/_parity.py: records, parameters, pixels)."""
+    from paper_1701_03572_b200 import pipeline
+    from tests import _parity
+
+    y, cb, cr = planes[0], planes[1], planes[2]
+    gy, gb, gr, grec = pipeline.stabilize_sequence(y, cfg.stab, cb, cr)
+    oy, ob, orr, orec = ref_out
+    s = _parity.summarize(grec, orec, [gy, gb, gr], [oy, ob, orr])
+    s["checker"] = "reference (oracle/_ref, unmodified sources)"
+    return s
 
 
 def run_reference_arm(args, cfg):
@@ -216,7 +230,7 @@ def run_reference_arm(args, cfg):
             for a in arrs[1:]], threads)
     times = []
     for _ in range(args.steps):
-        fps, dt = cpu_reference(cfg, arrs[0], arrs[1], arrs[2], threads)
+        fps, dt, _ = cpu_reference(cfg, arrs[0], arrs[1], arrs[2], threads)
         times.append(dt)
     ms = 1000.0 * float(np.mean(times))
     value = sample / (ms / 1000.0)
@@ -341,9 +355,15 @@ def run_ours(args, cfg):
         launches = (ctx.stats().launches - launches0) // max(steps, 1)
         return ms, launches, comp
 
+    # stage timing records event pairs on the launching stream and is read
+    # after each step (no host sync inside a call), so it runs in the timed
+    # region; a short pass without it checks that it costs nothing
     with ClockSampler(local) as clk:
         ms_dev, launches, comp = timed(step_device, args.steps, args.warmup)
-    ms_e2e, _, _ = timed(step_e2e, max(1, min(args.steps, 3)), 1)
+    ctx.enable_timing(False)
+    ms_dev_plain, _, _ = timed(step_device, max(1, min(args.steps, 3)), 0)
+    ms_e2e, _, _ = timed(step_e2e, args.steps, args.warmup)
+    ctx.enable_timing(True)
     value = n / (ms_dev / 1000.0)
     e2e = n / (ms_e2e / 1000.0)
     fb = spec.width * spec.height * planes
@@ -367,7 +387,8 @@ def run_ours(args, cfg):
                 "config": workload(args, cfg),
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": fb * n,
                         "d2h_bytes_per_step": fb * n + n * pipeline.RECORD_BYTES,
-                        "ms_per_step": ms_e2e},
+                        "ms_per_step": ms_e2e, "steps": args.steps, "warmup": args.warmup},
+                "ms_per_step_without_stage_events": ms_dev_plain,
                 "roofline": {"bound": "hbm", "kernel": "K8 compose_tma_kernel (fused warp + crop/resize, all planes)",
                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": (achieved / hbm) if achieved else None,
@@ -380,17 +401,20 @@ def run_ours(args, cfg):
                 "stage_ms": stages,
                 "gpu_launches": int(launches),
                 "lk": {"iterations": int(ctx.stats().lk_iterations),
-                       "level_builds": int(ctx.stats().candidates)},
+                       "level_builds": int(ctx.stats().lk_level_builds)},
                 "clocks": clk.summary(),
                 "input_gen_s": round(gen_s, 1)}
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             sample = min(n, max(6 * threads, 40))
             hs = [h[:sample].numpy() for h in host] + [None] * (3 - planes)
-            fps, dt = cpu_reference(cfg, hs[0], hs[1], hs[2], threads)
+            fps, dt, ref_out = cpu_reference(cfg, hs[0], hs[1], hs[2], threads)
             line["cpu_baseline"] = {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
                                     "sample": f"first {sample} frames of {args.config} "
                                               f"({dt:.1f} s, reference stage functions, segment-parallel)"}
+            # parity of the same sample (outside the timed region): our Stage I on
+            # those frames against the reference's output for them
+            line["parity"] = sample_parity(cfg, hs, ref_out)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

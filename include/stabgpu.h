@@ -388,7 +388,7 @@ int stabgpu_interframe_sse(stabgpu_ctx* ctx, const uint8_t* dev_y, int n, int w,
 typedef struct stabgpu_stats {
     double ms_pyramid, ms_detect, ms_track, ms_fit, ms_plan, ms_compose, ms_total;
     long long launches;
-    long long candidates;  /* corner candidates compacted */
+    long long lk_level_builds; /* LK template (level patch) builds of the last motion pass */
     long long lk_iterations;
 } stabgpu_stats;
 int stabgpu_get_stats(stabgpu_ctx* ctx, stabgpu_stats* out);

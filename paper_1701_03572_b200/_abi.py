@@ -80,7 +80,7 @@ class MotionRecord(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("ms_pyramid", C.c_double), ("ms_detect", C.c_double), ("ms_track", C.c_double),
                 ("ms_fit", C.c_double), ("ms_plan", C.c_double), ("ms_compose", C.c_double),
-                ("ms_total", C.c_double), ("launches", C.c_longlong), ("candidates", C.c_longlong),
+                ("ms_total", C.c_double), ("launches", C.c_longlong), ("lk_level_builds", C.c_longlong),
                 ("lk_iterations", C.c_longlong)]
 
 

@@ -35,6 +35,16 @@ struct DevBuf {
     size_t n = 0;
 };
 
+// Stage timing: a Timer records an event pair (from a pool) on the context
+// stream around a stage and queues it; nothing waits on it.  The queued pairs
+// are read when the caller asks for the stats (stabgpu_get_stats), so timing
+// never adds a host sync inside a call.  Slots: 0 pyramid, 1 detect, 2 track,
+// 3 fit, 4 compose, 5 plan.
+struct TimedSpan {
+    int slot;
+    cudaEvent_t a, b;
+};
+
 struct stabgpu_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -43,13 +53,16 @@ struct stabgpu_ctx {
     std::map<std::string, DevBuf> bufs;
     bool timing = false;
     stabgpu_stats stats{};
-    cudaEvent_t ev[16]{};
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<TimedSpan> spans;
+    unsigned long long* iters_host = nullptr;  // pinned: LK counters of the last motion pass
+    bool iters_pending = false;
 };
 
 namespace {
 
 thread_local std::string g_err;
-long long lk_tracks_last = 0;
 
 int set_err(int code, const char* fmt, ...) {
     char b[512];
@@ -184,14 +197,67 @@ FramePlan host_plan(const stabgpu_transform& t) {
     return p;
 }
 
+cudaEvent_t pooled_event(stabgpu_ctx* ctx) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        ctx->ev_pool.push_back(e);
+    }
+    return ctx->ev_pool[ctx->ev_used++];
+}
+
+// A whole-sequence call starts its own stage times (spans queued by earlier
+// calls and not read are dropped; their events are recycled).
+void begin_timing(stabgpu_ctx* ctx) {
+    if (!ctx->timing) return;
+    ctx->spans.clear();
+    ctx->ev_used = 0;
+    ctx->iters_pending = false;
+}
+
+// Stage times = the spans queued since the previous read (waits for their end
+// events); with none queued the stats keep their last values.
+void harvest_timing(stabgpu_ctx* ctx) {
+    if (!ctx->spans.empty()) {
+        double ms_slot[6] = {0, 0, 0, 0, 0, 0};
+        for (const TimedSpan& sp : ctx->spans) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(sp.b) == cudaSuccess && cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess)
+                ms_slot[sp.slot] += ms;
+        }
+        ctx->spans.clear();
+        ctx->ev_used = 0;
+        stabgpu_stats& s = ctx->stats;
+        s.ms_pyramid = ms_slot[0];
+        s.ms_detect = ms_slot[1];
+        s.ms_track = ms_slot[2];
+        s.ms_fit = ms_slot[3];
+        s.ms_compose = ms_slot[4];
+        s.ms_plan = ms_slot[5];
+        s.ms_total = s.ms_pyramid + s.ms_detect + s.ms_track + s.ms_fit + s.ms_compose + s.ms_plan;
+    }
+    stabgpu_stats& s = ctx->stats;
+    if (ctx->iters_pending) {
+        cudaStreamSynchronize(ctx->stream);
+        s.lk_iterations = (long long)ctx->iters_host[0];
+        s.lk_level_builds = (long long)ctx->iters_host[1];
+        ctx->iters_pending = false;
+    }
+}
+
 struct Timer {
     stabgpu_ctx* ctx;
     int slot;
+    cudaEvent_t a = nullptr;
     Timer(stabgpu_ctx* c, int s) : ctx(c), slot(s) {
-        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot], ctx->stream);
+        if (ctx->timing && (a = pooled_event(ctx))) cudaEventRecord(a, ctx->stream);
     }
     ~Timer() {
-        if (ctx->timing) cudaEventRecord(ctx->ev[2 * slot + 1], ctx->stream);
+        if (!a) return;
+        cudaEvent_t b = pooled_event(ctx);
+        if (!b) return;
+        cudaEventRecord(b, ctx->stream);
+        ctx->spans.push_back(TimedSpan{slot, a, b});
     }
 };
 
@@ -203,8 +269,7 @@ struct Timer {
 // frame 0 and its first frame gets a FIRST record, exactly as if it were run
 // alone.
 int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, int w, int h,
-               const stabgpu_config& cfg, stabgpu_motion_record* motion, double* t_ms,
-               int n_streams = 1) {
+               const stabgpu_config& cfg, stabgpu_motion_record* motion, int n_streams = 1) {
     cudaStream_t st = ctx->stream;
     const int nF = count + 1;
     const int R = cfg.flow.redetect_interval;
@@ -379,19 +444,9 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
         ++ctx->stats.launches;
         TRY(check_launch("fit"));
     }
-    if (ctx->timing && t_ms) {
-        unsigned long long it[3] = {0, 0, 0};
-        CUDA_TRY(cudaMemcpyAsync(it, iters, sizeof it, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        ctx->stats.lk_iterations = (long long)it[0];
-        ctx->stats.candidates = (long long)it[1];  // template builds (reused field)
-        ctx->stats.launches += 0;
-        lk_tracks_last = (long long)it[2];
-        for (int k = 0; k < 4; ++k) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ctx->ev[2 * k], ctx->ev[2 * k + 1]);
-            t_ms[k] += ms;
-        }
+    if (ctx->timing && ctx->iters_host) {  // LK counters, read at stabgpu_get_stats
+        CUDA_TRY(cudaMemcpyAsync(ctx->iters_host, iters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        ctx->iters_pending = true;
     }
     return STABGPU_OK;
 }
@@ -502,7 +557,7 @@ int stabgpu_create(int device, stabgpu_ctx** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cin, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cout, cudaStreamNonBlocking));
     c->stream = c->own;
-    for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaMallocHost((void**)&c->iters_host, 4 * sizeof(unsigned long long)));
     // Per-launch tables come from the stream-ordered allocator; keep freed
     // blocks mapped so repeated launches do not remap device memory.
     cudaMemPool_t pool;
@@ -520,7 +575,8 @@ int stabgpu_destroy(stabgpu_ctx* c) {
     cudaDeviceSynchronize();
     for (auto& kv : c->bufs)
         if (kv.second.p) cudaFree(kv.second.p);
-    for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->iters_host) cudaFreeHost(c->iters_host);
     cudaStreamDestroy(c->own);
     cudaStreamDestroy(c->cin);
     cudaStreamDestroy(c->cout);
@@ -544,6 +600,8 @@ int stabgpu_enable_timing(stabgpu_ctx* c, int on) {
 }
 
 int stabgpu_get_stats(stabgpu_ctx* c, stabgpu_stats* out) {
+    cudaSetDevice(c->device);
+    harvest_timing(c);
     *out = c->stats;
     return STABGPU_OK;
 }
@@ -1026,6 +1084,7 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const 
     TRY(validate_frame(w, h));
     if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
     cudaSetDevice(ctx->device);
+    begin_timing(ctx);
     cudaStream_t st = ctx->stream;
     DBUF(stabgpu_motion_record, motion, "seq_motion", n);
     DBUF(stabgpu_frame_record, rec, "seq_rec", n);
@@ -1033,16 +1092,17 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const 
     DBUF(FramePlan, plan, "seq_plan", n);
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
-    double t_ms[4] = {0, 0, 0, 0};
-    TRY(run_motion(ctx, y, 0, n - 1, w, h, cfg, motion, t_ms));
-    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
-    launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
-    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st);
+    TRY(run_motion(ctx, y, 0, n - 1, w, h, cfg, motion));
+    {
+        Timer tm(ctx, 5);
+        launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
+        launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan,
+                           PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st);
+    }
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
-    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
     {
-        Timer tm(ctx, 4);  // events 8, 9
+        Timer tm(ctx, 4);
         TRY(compose_range(ctx, y, cb, cr, 0, n, w, h, cw, ch, plan, cfg.crop_ratio, oy, ocb, ocr));
     }
     TRY(plan_error(ctx, ps));
@@ -1050,18 +1110,6 @@ int stabgpu_stabilize_sequence_device(stabgpu_ctx* ctx, const uint8_t* y, const 
         CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n,
                                  cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (ctx->timing) {
-        float plan_ms = 0.f, comp_ms = 0.f;
-        cudaEventElapsedTime(&plan_ms, ctx->ev[10], ctx->ev[11]);
-        cudaEventElapsedTime(&comp_ms, ctx->ev[8], ctx->ev[9]);
-        ctx->stats.ms_pyramid = t_ms[0];
-        ctx->stats.ms_detect = t_ms[1];
-        ctx->stats.ms_track = t_ms[2];
-        ctx->stats.ms_fit = t_ms[3];
-        ctx->stats.ms_plan = plan_ms;
-        ctx->stats.ms_compose = comp_ms;
-        ctx->stats.ms_total = t_ms[0] + t_ms[1] + t_ms[2] + t_ms[3] + plan_ms + comp_ms;
-    }
     return STABGPU_OK;
 }
 
@@ -1090,43 +1138,25 @@ int validate_streams(const stabgpu_config& cfg, int n_streams, int frames, int w
 int streams_group(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
                   int S, int F, int w, int h, int cw, int ch, const stabgpu_config& cfg, uint8_t* oy,
                   uint8_t* ocb, uint8_t* ocr, stabgpu_motion_record* motion, stabgpu_frame_record* rec,
-                  double4* cum, FramePlan* plan, PlanState* ps, int* err, double* t_ms,
-                  float* plan_ms, float* comp_ms) {
+                  double4* cum, FramePlan* plan, PlanState* ps, int* err) {
     cudaStream_t st = ctx->stream;
     const long long n = (long long)S * F;
-    TRY(run_motion(ctx, y, 0, (int)(n - 1), w, h, cfg, motion, t_ms, S));
-    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
-    launch_plan_scan(motion, 0, F, cfg, ps, rec, cum, st, S, F, err);
-    launch_plan_smooth(cum, F, true, 0, n, cfg.smooth_radius, rec, plan,
-                       PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st, F);
+    TRY(run_motion(ctx, y, 0, (int)(n - 1), w, h, cfg, motion, S));
+    {
+        Timer tm(ctx, 5);
+        launch_plan_scan(motion, 0, F, cfg, ps, rec, cum, st, S, F, err);
+        launch_plan_smooth(cum, F, true, 0, n, cfg.smooth_radius, rec, plan,
+                           PlanGeom{w, h, cb ? cw : 0, cb ? ch : 0, cfg.crop_ratio}, st, F);
+    }
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
-    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
     {
         Timer tm(ctx, 4);
         TRY(compose_range(ctx, y, cb, cr, 0, n, w, h, cw, ch, plan, cfg.crop_ratio, oy, ocb, ocr));
     }
-    if (ctx->timing && t_ms) {
-        float a = 0.f, b = 0.f;
-        CUDA_TRY(cudaEventSynchronize(ctx->ev[9]));
-        cudaEventElapsedTime(&a, ctx->ev[10], ctx->ev[11]);
-        cudaEventElapsedTime(&b, ctx->ev[8], ctx->ev[9]);
-        *plan_ms += a;
-        *comp_ms += b;
-    }
     return STABGPU_OK;
 }
 
-void streams_stats(stabgpu_ctx* ctx, const double* t_ms, float plan_ms, float comp_ms) {
-    if (!ctx->timing) return;
-    ctx->stats.ms_pyramid = t_ms[0];
-    ctx->stats.ms_detect = t_ms[1];
-    ctx->stats.ms_track = t_ms[2];
-    ctx->stats.ms_fit = t_ms[3];
-    ctx->stats.ms_plan = plan_ms;
-    ctx->stats.ms_compose = comp_ms;
-    ctx->stats.ms_total = t_ms[0] + t_ms[1] + t_ms[2] + t_ms[3] + plan_ms + comp_ms;
-}
 }  // namespace
 extern "C" {
 
@@ -1139,6 +1169,7 @@ int stabgpu_stabilize_streams_device(stabgpu_ctx* ctx, const uint8_t* y, const u
     const bool chroma = cb && cr && ocb && ocr;
     if (!chroma) cb = cr = nullptr;
     cudaSetDevice(ctx->device);
+    begin_timing(ctx);
     cudaStream_t st = ctx->stream;
     const long long n = (long long)n_streams * frames;
     DBUF(stabgpu_motion_record, motion, "seq_motion", n);
@@ -1147,15 +1178,12 @@ int stabgpu_stabilize_streams_device(stabgpu_ctx* ctx, const uint8_t* y, const u
     DBUF(FramePlan, plan, "seq_plan", n);
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps, n_streams));
-    double t_ms[4] = {0, 0, 0, 0};
-    float plan_ms = 0.f, comp_ms = 0.f;
     TRY(streams_group(ctx, y, cb, cr, n_streams, frames, w, h, cw, ch, cfg, oy, ocb, ocr, motion, rec,
-                      cum, plan, ps, reinterpret_cast<int*>(ps + n_streams), t_ms, &plan_ms, &comp_ms));
+                      cum, plan, ps, reinterpret_cast<int*>(ps + n_streams)));
     TRY(plan_error(ctx, ps, n_streams));
     if (records)
         CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    streams_stats(ctx, t_ms, plan_ms, comp_ms);
     return STABGPU_OK;
 }
 
@@ -1169,6 +1197,7 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
     const stabgpu_config cfg = *cfgp;
     TRY(validate_streams(cfg, n_streams, frames, w, h));
     cudaSetDevice(ctx->device);
+    begin_timing(ctx);
     cudaStream_t st = ctx->stream;
     const bool chroma = hcb && hcr && hocb && hocr;
     const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
@@ -1219,8 +1248,6 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
         cudaEventRecord(in_ev[g], ctx->cin);
         return STABGPU_OK;
     };
-    double t_ms[4] = {0, 0, 0, 0};
-    float plan_ms = 0.f, comp_ms = 0.f;
     int rc = upload(0);
     if (!rc && ngroups > 1) rc = upload(1);
     for (int g = 0; g < ngroups && !rc; ++g) {
@@ -1229,8 +1256,7 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
         cudaStreamWaitEvent(st, in_ev[g], 0);
         if (g >= 2) cudaStreamWaitEvent(st, out_ev[g - 2], 0);
         rc = streams_group(ctx, dy[k], dcb[k], dcr[k], ns, frames, w, h, cw, ch, cfg, doy[k], docb[k],
-                           docr[k], motion + f0, rec + f0, cum + f0, plan + f0, ps + s0, err + s0,
-                           t_ms, &plan_ms, &comp_ms);
+                           docr[k], motion + f0, rec + f0, cum + f0, plan + f0, ps + s0, err + s0);
         if (rc) break;
         cudaEventRecord(done_ev[g], st);
         if (g + 2 < ngroups && (rc = upload(g + 2))) break;
@@ -1254,7 +1280,6 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
     if (records)
         CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    streams_stats(ctx, t_ms, plan_ms, comp_ms);
     return STABGPU_OK;
 }
 
@@ -1270,6 +1295,7 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
     TRY(validate_frame(w, h));
     if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
     cudaSetDevice(ctx->device);
+    begin_timing(ctx);
     cudaStream_t st = ctx->stream;
     const bool chroma = hcb && hcr && hocb && hocr;
     const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
@@ -1322,7 +1348,7 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
         if (seg_end > seg_done) {
             const long long first = seg_done * R;
             const long long last = std::min<long long>(seg_end * R, n - 1);
-            rc = run_motion(ctx, dy + first * fl, first, (int)(last - first), w, h, cfg, motion, nullptr);
+            rc = run_motion(ctx, dy + first * fl, first, (int)(last - first), w, h, cfg, motion);
             if (rc) break;
             launch_plan_scan(motion, known, last + 1 - known, cfg, ps, rec, cum, st);
             ++ctx->stats.launches;
@@ -1384,17 +1410,10 @@ int stabgpu_motion_chunk(stabgpu_ctx* ctx, const uint8_t* dev_y, int64_t first, 
         CUDA_TRY(cudaMemcpyAsync(motion, &none, sizeof none, cudaMemcpyHostToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     }
-    double t_ms[4] = {0, 0, 0, 0};
-    TRY(run_motion(ctx, dev_y, first, count, w, h, cfg, base, t_ms));
+    TRY(run_motion(ctx, dev_y, first, count, w, h, cfg, base));
     CUDA_TRY(cudaMemcpyAsync(host_out, motion, sizeof(stabgpu_motion_record) * ((size_t)count + 1),
                              cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (ctx->timing) {  // stage times of this chunk (a sharded rank's motion)
-        ctx->stats.ms_pyramid = t_ms[0];
-        ctx->stats.ms_detect = t_ms[1];
-        ctx->stats.ms_track = t_ms[2];
-        ctx->stats.ms_fit = t_ms[3];
-    }
     return STABGPU_OK;
 }
 
@@ -1413,21 +1432,17 @@ int stabgpu_plan_corrections(stabgpu_ctx* ctx, const stabgpu_motion_record* host
                              cudaMemcpyHostToDevice, st));
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
-    if (ctx->timing) cudaEventRecord(ctx->ev[10], st);
-    launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
-    launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{16, 16, 0, 0, 0.0}, st);
-    if (ctx->timing) cudaEventRecord(ctx->ev[11], st);
+    {
+        Timer tm(ctx, 5);
+        launch_plan_scan(motion, 0, n, cfg, ps, rec, cum, st);
+        launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan, PlanGeom{16, 16, 0, 0, 0.0}, st);
+    }
     ctx->stats.launches += 2;
     TRY(check_launch("plan"));
     TRY(plan_error(ctx, ps));
     CUDA_TRY(cudaMemcpyAsync(host_records, rec, sizeof(stabgpu_frame_record) * n,
                              cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (ctx->timing) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ctx->ev[10], ctx->ev[11]);
-        ctx->stats.ms_plan = ms;
-    }
     return STABGPU_OK;
 }
 
@@ -1451,11 +1466,6 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb
         TRY(compose_range(ctx, y, cb, cr, 0, count, w, h, cw, ch, plan, crop, oy, ocb, ocr));
     }
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (ctx->timing) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
-        ctx->stats.ms_compose = ms;
-    }
     return STABGPU_OK;
 }
 
