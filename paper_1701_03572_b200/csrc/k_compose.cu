@@ -691,6 +691,10 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
         tp.lbx = (xmn - 1) & ~15;
         tp.lby = ymn - 1;
         tp.lfit = (xmx + 2) - tp.lbx < BW && (ymx + 2) - tp.lby < BH;
+        // interior tile: every W sample's integer parts lie in [1, w-3] x [1, h-3]
+        // (one pixel of slack for the 32.32 conversion), so the lean row loop
+        // needs no per-pixel bounds or near-integer decisions (see inner32)
+        if (tp.lfit && nu <= TW && xmn >= 2 && xmx <= w - 4 && ymn >= 2 && ymx <= h - 4) tp.pad0 |= 1;
     }
     if (chroma) {
         int xmn = INT_MAX, xmx = INT_MIN, ymn = INT_MAX, ymx = INT_MIN;
@@ -706,6 +710,7 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
         tp.cbx = (xmn - 1) & ~15;
         tp.cby = ymn - 1;
         tp.cfit = (xmx + 2) - tp.cbx < BW && (ymx + 2) - tp.cby < BH;
+        if (tp.cfit && xmn >= 2 && xmx <= cw - 4 && ymn >= 2 && ymx <= ch - 4) tp.pad0 |= 2;
     }
     int4* dst = T.tiles + 3 * id;
     const int4* src = reinterpret_cast<const int4*>(&tp);
@@ -983,6 +988,95 @@ __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, c
     return qn;
 }
 
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+__device__ __forceinline__ void stg_u16(uint8_t* p, uint32_t v) {
+    __stcs(reinterpret_cast<unsigned short*>(p), (unsigned short)v);
+}
+
+// ---- lean row loops of interior tiles -------------------------------------
+// An interior tile (tile_prep_kernel: pad0 bit 0 luma, bit 1 chroma) has every
+// sample's 2x2 taps inside the frame and inside the staged TMA box, with the
+// integer parts in [1, w-3] x [1, h-3]: by the continuity argument above
+// (inner32) no coordinate decision is needed, only the blended value's .5-tie
+// guard.  Lane l owns the adjacent columns 2l and 2l+1, so its two results
+// are adjacent bytes (one 16-bit store) and the packed-fp32 blend works on
+// the pair.  Columns past the tile's width re-sample its last column (in the
+// box) and are not stored.
+__device__ __forceinline__ int w_rows_lean(const uint8_t* box, int ob1, const long long* __restrict__ rxf,
+                                           const long long* __restrict__ ryf, uint32_t wsm, int nu, int nv, int u0,
+                                           long long cf, long long snf, long long RSX, long long RSY, unsigned* q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = 2 * lane, c1 = c0 + 1;
+    const bool v0 = c0 < nu, v1 = c1 < nu;
+    int qn = 0;
+    uint32_t row = wsm + warp * WTW + c0;
+    const int r0 = min(warp, nv - 1);
+    const long long ua = (long long)(u0 + min(c0, nu - 1)), ub = (long long)(u0 + min(c1, nu - 1));
+    long long XA = to32(__ldg(rxf + r0) + ua * cf), YA = to32(__ldg(ryf + r0) - ua * snf);
+    long long XB = to32(__ldg(rxf + r0) + ub * cf), YB = to32(__ldg(ryf + r0) - ub * snf);
+    const long long rsx = RSX >> 16, rsy = RSY >> 16;
+    for (int r = warp; r < nv; r += NW, row += NW * WTW, XA += rsx, YA += rsy, XB += rsx, YB += rsy) {
+        bool b0, b1;
+        const uint32_t pr = blend2_bad(fetch4i(box, BW, ob1, XA, YA, true), fetch4i(box, BW, ob1, XB, YB, true),
+                                       frac2(XA, XB), frac2(YA, YB), b0, b1);
+        b0 = b0 && v0;
+        b1 = b1 && v1;
+        if (v1) sts_u16(row, pr);
+        else if (v0) sts_u8(row, pr & 0xFF);
+        if (__any_sync(0xFFFFFFFFu, b0 || b1)) {
+            const unsigned it = ((unsigned)r << 8) | (unsigned)c0;
+            wq_push(q, qn, b0, it);
+            wq_push(q, qn, b1, it + 1);
+        }
+    }
+    return qn;
+}
+
+__device__ __forceinline__ int chroma_rows_lean(const uint8_t* s1, const uint8_t* s2, int ob1,
+                                                const long long* __restrict__ pxf, const long long* __restrict__ pyf,
+                                                uint8_t* ob, uint8_t* orr, int cw, int nx, int ny, int X0,
+                                                long long kxx, long long kyx, long long RSX, long long RSY,
+                                                unsigned* q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = 2 * lane, c1 = c0 + 1;
+    const bool v0 = c0 < nx, v1 = c1 < nx;
+    int qn = 0;
+    const size_t step = (size_t)NW * cw;
+    uint8_t* pb = ob + (size_t)warp * cw + c0;
+    uint8_t* pr = orr + (size_t)warp * cw + c0;
+    const int r0 = min(warp, ny - 1);
+    const long long xa = (long long)(X0 + min(c0, nx - 1)), xb = (long long)(X0 + min(c1, nx - 1));
+    long long XA = to32(__ldg(pxf + r0) + xa * kxx), YA = to32(__ldg(pyf + r0) + xa * kyx);
+    long long XB = to32(__ldg(pxf + r0) + xb * kxx), YB = to32(__ldg(pyf + r0) + xb * kyx);
+    const long long rsx = RSX >> 16, rsy = RSY >> 16;
+    for (int r = warp; r < ny; r += NW, pb += step, pr += step, XA += rsx, YA += rsy, XB += rsx, YB += rsy) {
+        const float2 fx = frac2(XA, XB), fy = frac2(YA, YB);
+        bool e0, e1, e2, e3;
+        // one packed blend per plane: (pixel 2l, pixel 2l+1) share the pipe
+        const uint32_t vb = blend2_bad(fetch4i(s1, BW, ob1, XA, YA, true), fetch4i(s1, BW, ob1, XB, YB, true), fx,
+                                       fy, e0, e1);
+        const uint32_t vr = blend2_bad(fetch4i(s2, BW, ob1, XA, YA, true), fetch4i(s2, BW, ob1, XB, YB, true), fx,
+                                       fy, e2, e3);
+        const bool b0 = v0 && (e0 || e2), b1 = v1 && (e1 || e3);
+        if (v1) {
+            stg_u16(pb, vb);
+            stg_u16(pr, vr);
+        } else if (v0) {
+            stg_u8(pb, vb & 0xFF);
+            stg_u8(pr, vr & 0xFF);
+        }
+        if (__any_sync(0xFFFFFFFFu, b0 || b1)) {
+            const unsigned it = ((unsigned)r << 8) | (unsigned)c0;
+            wq_push(q, qn, b0, it);
+            wq_push(q, qn, b1, it + 1);
+        }
+    }
+    return qn;
+}
+
 // Persistent TMA compose.  Per tile: every warp waits on the tile's mbarrier,
 // computes W rows (-> shared wt) and chroma rows (-> global), one CTA
 // barrier, then crop_resize rows of W (-> global).  Undecidable pixels take
@@ -1069,7 +1163,10 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             const uint8_t* bx = &S.box[b][0][0];
             const uint32_t wsm = smem_u32(wt);
             int qn;
-            if (tp.lfit)
+            if (tp.pad0 & 1)
+                qn = w_rows_lean(bx, BW + 1 - (tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, u0, cf, snf, NW * snf,
+                                 NW * cf, S.wq[warp]);
+            else if (tp.lfit)
                 qn = w_rows_q(bx, BW, -(tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf,
                               NW * snf, NW * cf, limx, limy, S.wq[warp]);
             else
@@ -1105,7 +1202,10 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             uint8_t* ob = oCB + (size_t)f * CB.stride + (size_t)Y0 * cw + X0;
             uint8_t* orr = oCR + (size_t)f * CR.stride + (size_t)Y0 * cw + X0;
             int qn;
-            if (tp.cfit)
+            if (tp.pad0 & 2)
+                qn = chroma_rows_lean(b1p, b2p, BW + 1 - (tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, X0,
+                                      kxx, kyx, NW * kxy, NW * kyy, S.wq[warp]);
+            else if (tp.cfit)
                 qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY,
                                    32 * kxx, 32 * kyx, NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
             else
@@ -1136,19 +1236,22 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
         __syncthreads();  // wt[b] complete; box[b] free for tile k+2 after this
         // ------------------------------------------- crop_resize of W -> global
         if (LUMA) {
-            uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + lane;
-            const bool c0 = lane < nx, c1 = lane + 32 < nx;
             if (identity) {
+                uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + lane;
+                const bool c0 = lane < nx, c1 = lane + 32 < nx;
                 for (int r = warp; r < ny; r += NT / 32) {
                     if (c0) stg_u8(oy + (size_t)r * w, wt[r * WTW + lane]);
                     if (c1) stg_u8(oy + (size_t)r * w + 32, wt[r * WTW + lane + 32]);
                 }
             } else {
+                // lane l owns output columns 2l and 2l+1 (one 16-bit store per row)
+                uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + 2 * lane;
+                const bool c0 = 2 * lane < nx, c1 = 2 * lane + 1 < nx;
                 int x0[2], x1[2];
                 float fxv[2];
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
-                    const int c = X0 + min(lane + 32 * j, nx - 1);
+                    const int c = X0 + min(2 * lane + j, nx - 1);
                     const int cx = __ldg(T.cx0 + c);
                     x0[j] = cx - u0;
                     x1[j] = min(cx + 1, w - 1) - u0;
@@ -1204,14 +1307,14 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
                     const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
                     const uint32_t a0 = __float_as_uint(m.x) & 0xFFu, a1 = __float_as_uint(m.y) & 0xFFu;
-                    if (c0) stg_u8(py, a0);
-                    if (c1) stg_u8(py + 32, a1);
+                    if (c1) stg_u16(py, a0 | (a1 << 8));
+                    else if (c0) stg_u8(py, a0);
                     const bool b0 = c0 & (fabsf(dv.x) > 0.5f - VGUARD);
                     const bool b1 = c1 & (fabsf(dv.y) > 0.5f - VGUARD);
                     if (__any_sync(FULL, b0 | b1)) {
-                        const unsigned it = ((unsigned)r << 8) | (unsigned)lane;
+                        const unsigned it = ((unsigned)r << 8) | (unsigned)(2 * lane);
                         wq_push(S.wq[warp], qn, b0, it);
-                        wq_push(S.wq[warp], qn, b1, it + 32);
+                        wq_push(S.wq[warp], qn, b1, it + 1);
                     }
                 }
                 if (__any_sync(FULL, qn > 0)) {
@@ -1227,7 +1330,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                             r = rb + i / nx;
                             c = i % nx;
                         }
-                        stg_u8(oy + (size_t)r * w + c - lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
+                        stg_u8(oy + (size_t)r * w + c - 2 * lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
                     }
                     __syncwarp();
                 }
