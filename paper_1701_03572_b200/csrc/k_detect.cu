@@ -15,17 +15,17 @@
 //     bit pattern (responses are >= 0, so bit order == value order).
 // K3 (cand_kernel): recomputes the response (cheaper than writing an 8 B/px
 //     map), keeps r >= quality*max && r > 0, warp-ballot compaction.
-// K4 (select_kernel): one 512-thread CTA per detection frame (two per SM).  Candidates
-//     are bucketed by a monotone 13-bit-truncated float key (histogram +
-//     scatter in shared memory), then consumed in score order in chunks of
-//     <= 4096: each chunk is first tested against the accepted-corner grid
-//     (cell >= min_distance, so only the 3x3 neighbourhood can conflict),
-//     the survivors are bitonic-sorted by (score desc, y*w+x asc) — the
+// K4 (select_kernel): one CTA per detection frame.  Candidates are bucketed
+//     by a monotone 13-bit-truncated float key (histogram + scatter), then
+//     consumed in score order in chunks of whole buckets: each chunk is
+//     prefiltered against the corners accepted so far (a grid of cells >=
+//     min_distance, or, when every candidate is listed, an exact exclusion
+//     bitmap), the survivors are sorted by (score desc, y*w+x asc) — the
 //     reference comparator, features.cpp:119-123 — and one warp runs the
 //     greedy scan 32 candidates at a time with ballots, which reproduces the
 //     sequential rank-order rule exactly, including the early stop at
-//     max_corners.  A bucket holding more than 4096 candidates (large ties)
-//     is merge-sorted in global memory first.
+//     max_corners.  A bucket larger than a chunk (large ties) is merge-sorted
+//     in global memory first.
 #include <algorithm>
 #include <cfloat>
 
@@ -37,6 +37,7 @@ namespace stabgpu {
 namespace {
 
 constexpr int RTW = 32, RTH = 16;  // response tile
+constexpr int kHwMax = 256;        // K4: disc half-widths tabulated for row offsets 0 .. kHwMax-1
 
 __device__ __forceinline__ double min_eig_q(int sxx4, int sxy4, int syy4) {
     // features.cpp:41-45 on the exact quarter-integer sums
@@ -338,25 +339,48 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
 // back to the full list when lo > quality * max and the prefix runs out before
 // max_corners.
 __global__ void resp_cut_kernel(double quality, DetectScratch s, unsigned keep) {
-    const int d = blockIdx.x;
-    if (threadIdx.x != 0) return;
+    // one warp per frame: lane l sums bins [2047 - 64 l - 63, 2047 - 64 l]
+    // (descending), a shuffle scan finds the segment where the running count
+    // from the top reaches `keep`, and that lane walks it: the same bin b as
+    // the serial scan from b = 2047 down to 1
+    static_assert(kRespBins == 2048, "64 bins per lane");
+    const int d = blockIdx.x, lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
     const double m = (double)__uint_as_float(s.mlo[d]);
     double lo = 0.0;
     if (m > 0.0) {
         lo = dmul(quality, m);
-        unsigned cum = 0;
         const unsigned* hs = s.hist + (size_t)d * kRespBins;
-        for (int b = kRespBins - 1; b > 0; --b) {
-            cum += hs[b];
-            if (cum >= keep) {
-                const double edge = (double)__uint_as_float((unsigned)b << 20);
-                lo = fmin(fmax(edge, lo), m);
-                break;
+        const int top = kRespBins - 1 - 64 * lane;  // bins top .. top - 63 (bin 0 is never counted)
+        unsigned seg = 0;
+        for (int b = top; b > top - 64; --b) seg += b > 0 ? hs[b] : 0u;
+        unsigned incl = seg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const unsigned reach = __ballot_sync(0xFFFFFFFFu, incl >= keep);
+        if (reach) {
+            const int l0 = __ffs(reach) - 1;
+            if (lane == l0) {
+                unsigned cum = incl - seg;
+                for (int b = top; b > top - 64 && b > 0; --b) {
+                    cum += hs[b];
+                    if (cum >= keep) {
+                        const double edge = (double)__uint_as_float((unsigned)b << 20);
+                        lo = fmin(fmax(edge, lo), m);
+                        break;
+                    }
+                }
             }
+            lo = __shfl_sync(0xFFFFFFFFu, lo, l0);
         }
     }
-    s.lo[d] = lo;
-    s.flags[d] = 0;
+    if (lane == 0) {
+        s.lo[d] = lo;
+        s.flags[d] = 0;
+    }
 }
 
 __global__ void resp_redo_reset_kernel(DetectScratch s) {
@@ -409,20 +433,9 @@ __global__ void resp_generic_kernel(PlaneBatch fr, stabgpu_roi roi, int half, in
 
 // ---------------------------------------------------------------- K4 ----
 
-// Two shapes of the select CTA: 1024 threads with 4096-candidate chunks
-// (fastest per frame), or 512 threads with 3072-candidate chunks in ~110 KB
+// Two shapes of the select CTA: 1024 threads, or 512 threads in <= 114 KB
 // of shared memory, two frames per SM, so a batch with more frames than SMs
 // runs its serial greedies (one warp per frame) two at a time on every SM.
-constexpr int CAP_MAX = 4096;
-#ifndef SEL_CHUNK
-#define SEL_CHUNK 1024
-#endif
-// whole buckets are grouped into chunks of about SEL_CHUNK candidates: small
-// chunks let the parallel grid prefilter see more accepted corners, so the
-// serial warp greedy examines fewer candidates
-constexpr int CHUNK = SEL_CHUNK;
-constexpr int MAX_CELLS = 8192; // accepted-corner grid cells
-constexpr int SMEM_CORNERS = 8192;
 
 __device__ __forceinline__ unsigned bucket_of(unsigned long long key, unsigned maxf_bits) {
     const float sf = __double2float_rn(__longlong_as_double((long long)key));
@@ -468,11 +481,8 @@ struct SelShared {
     unsigned bstart[kBuckets + 1];
     unsigned warp_tot[32];
     unsigned total;
-    int naccepted;
-    int done;
-    int gw, gh, cell;
-    int b0, b1, big;
-    int chunk;  // adaptive chunk size (candidates grouped per pass)
+    int nacc;
+    short hw[kHwMax];  // disc half-width per row offset (-1: row outside the disc)
 };
 
 // bitonic sort of n (power of two) keys in shared memory, (score desc, idx asc)
@@ -499,20 +509,43 @@ __device__ void bitonic_sort(unsigned long long* key, unsigned* idx, int n) {
     }
 }
 
-// Does (x, y) lie closer than min_dist to an accepted corner?
-__device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy,
-                                          const int* anext, int gw, int gh, int cell, int rx0,
-                                          int ry0, double md2) {
-    const int cx = (x - rx0) / cell, cy = (y - ry0) / cell;
-    for (int gy = max(cy - 1, 0); gy <= min(cy + 1, gh - 1); ++gy)
-        for (int gx = max(cx - 1, 0); gx <= min(cx + 1, gw - 1); ++gx)
-            for (int a = heads[gy * gw + gx]; a >= 0; a = anext[a]) {
-                const short2 p = axy[a];
-                const long long dx = x - p.x, dy = y - p.y;
-                if ((double)(dx * dx + dy * dy) < md2) return true;
-            }
-    return false;
+// Exclusion bitmap of the accepted corners over the ROI (one bit per ROI
+// pixel, rows of `wr` 32-bit words): a pixel's bit is set iff it lies closer
+// than min_distance to an accepted corner, i.e. dx*dx + dy*dy < min_dist2 in
+// the reference's double arithmetic (features.cpp:127-139; integer
+// coordinates, so the disc is an exact set of offsets).  A candidate test is
+// one shared (or L1-cached global) word; a new corner marks its disc.
+__device__ __forceinline__ bool excluded(const uint32_t* bm, int wr, int x, int y) {
+    return (bm[y * wr + (x >> 5)] >> (x & 31)) & 1u;
 }
+
+// largest R >= 0 with R*R < md2 (the disc's row reach), or -1 if none
+__device__ __forceinline__ int disc_reach(double md2, int dy) {
+    const double d2 = (double)((long long)dy * dy);
+    if (!(d2 < md2)) return -1;
+    int hw = (int)sqrt(fmax(md2 - d2, 0.0));
+    while ((double)((long long)(hw + 1) * (hw + 1)) + d2 < md2) ++hw;
+    while (hw > 0 && !((double)((long long)hw * hw) + d2 < md2)) --hw;
+    return hw;
+}
+
+// Marks row dy of the disc of corner (ax, ay) (ROI coordinates).
+__device__ __forceinline__ void mark_row(uint32_t* bm, int wr, int rw, int rh, int ax, int ay, int dy, double md2,
+                                         const short* hwt) {
+    const int yy = ay + dy;
+    if (yy < 0 || yy >= rh) return;
+    const int ady = abs(dy);
+    const int hw = ady < kHwMax ? hwt[ady] : disc_reach(md2, dy);
+    if (hw < 0) return;
+    const int x0 = max(ax - hw, 0), x1 = min(ax + hw, rw - 1);
+    uint32_t* row = bm + (size_t)yy * wr;
+    for (int wd = x0 >> 5; wd <= (x1 >> 5); ++wd) {
+        const int lo = max(x0 - 32 * wd, 0), hi = min(x1 - 32 * wd, 31);
+        const uint32_t m = (hi == 31 ? 0xFFFFFFFFu : ((1u << (hi + 1)) - 1u)) & (0xFFFFFFFFu << lo);
+        atomicOr(row + wd, m);
+    }
+}
+
 
 // In-place stable-free merge sort of [0, m) by (score desc, idx asc) in
 // global memory, ping-ponging with tmp (keys are unique, so rank-merging is
@@ -556,24 +589,87 @@ __device__ void global_merge_sort(unsigned long long* key, unsigned* idx, unsign
     __syncthreads();
 }
 
-template <int SEL_THREADS, int CAP>
+// Warp bitonic sort of up to 32 (key, idx) pairs held one per lane, into
+// the reference order (score desc, idx asc): lane 0 ends with the first.
+// Empty lanes hold (0, ~0u), which sorts last (kept keys are > 0).
+__device__ __forceinline__ void warp_sort32(unsigned long long& key, unsigned& idx) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, j);
+            const unsigned oi = __shfl_xor_sync(0xffffffffu, idx, j);
+            const bool lower = (lane & j) == 0, up = (lane & k) == 0;
+            const bool ob = before(ok, oi, key, idx);
+            if (lower == up ? ob : !ob) {
+                key = ok;
+                idx = oi;
+            }
+        }
+}
+
+// Does (x, y) lie closer than min_distance to an accepted corner?  Accepted
+// corners are kept in a grid of cells >= min_distance (linked lists), so only
+// the 3x3 neighbourhood can conflict (features.cpp:127-139).
+constexpr int MAX_CELLS = 8192;
+constexpr int SMEM_CORNERS = 8192;
+
+__device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy, const int* anext, int gw,
+                                          int gh, int cell, int rx0, int ry0, double md2) {
+    const int cx = (x - rx0) / cell, cy = (y - ry0) / cell;
+    for (int gy = max(cy - 1, 0); gy <= min(cy + 1, gh - 1); ++gy)
+        for (int gx = max(cx - 1, 0); gx <= min(cx + 1, gw - 1); ++gx)
+            for (int a = heads[gy * gw + gx]; a >= 0; a = anext[a]) {
+                const short2 p = axy[a];
+                const long long dx = x - p.x, dy = y - p.y;
+                if ((double)(dx * dx + dy * dy) < md2) return true;
+            }
+    return false;
+}
+
+// K4: one CTA per detection frame.
+//   A. the candidates >= quality * max are bucketed by a monotone 13-bit
+//      truncated float key (histogram, scan, scatter) into sort_key/sort_idx,
+//      so whole buckets come in score order;
+//   B. the accepted-corner grid (and exclusion bitmap) are cleared, and on a
+//      redo seeded with the first pass's corners;
+//   C. chunks of whole buckets (<= ch candidates) in score order: every thread
+//      prefilters its candidates against the corners accepted so far, the
+//      survivors are compacted and sorted exactly (in registers when <= 32,
+//      else a shared-memory bitonic sort), and one warp walks them 32 at a
+//      time against the grid, resolving live lanes against each other in rank
+//      order — the reference's sequential greedy (features.cpp:127-139),
+//      including the early stop at max_corners.  A bucket larger than a chunk
+//      (large ties) is merge-sorted in global memory first.
+// The prefilter tests the grid, or — when every candidate is listed (no cut,
+// e.g. C1: ~190k candidates for ~160 corners) and it fits in shared memory —
+// an exclusion bitmap with one bit per ROI pixel (set iff closer than
+// min_distance to an accepted corner: dx*dx + dy*dy < min_dist2 in the
+// reference's double arithmetic on integer offsets, an exact set), which the
+// whole CTA marks after each chunk's walk.
+//
+// Dynamic shared memory: chunk buffer (ch keys + ch indices, ch a power of
+// two) | grid heads | accepted corners (when max_corners <= SMEM_CORNERS) |
+// bitmap (use_bm); the bucket cursor of phase A aliases its start.
+template <int SEL_THREADS>
 __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     select_kernel(stabgpu_detect_cfg cfg, stabgpu_roi roi, int w, DetectScratch s,
                   double2* __restrict__ out_xy, double* __restrict__ out_score,
-                  int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext, int redo) {
-    static_assert(12 * CAP >= 4 * kBuckets, "the bucket cursor aliases the chunk arrays");
-    static_assert(kBuckets % SEL_THREADS == 0 && CAP % SEL_THREADS == 0, "per-thread strides");
+                  int* __restrict__ out_n, short2* __restrict__ g_axy, int* __restrict__ g_anext, int ch,
+                  int use_bm, int redo) {
+    static_assert(kBuckets % SEL_THREADS == 0, "per-thread strides");
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ SelShared S;
     if (redo && !(s.flags ? (s.flags[blockIdx.x] & 2) : 0)) return;
-    SelShared& S = *reinterpret_cast<SelShared*>(smem);
-    unsigned char* p = smem + ((sizeof(SelShared) + 15) & ~size_t(15));
+    unsigned char* p = smem;
     unsigned long long* ckey = reinterpret_cast<unsigned long long*>(p);
-    p += sizeof(unsigned long long) * CAP;
+    p += sizeof(unsigned long long) * ch;
     unsigned* cidx = reinterpret_cast<unsigned*>(p);
-    p += sizeof(unsigned) * CAP;
-    unsigned* cursor = reinterpret_cast<unsigned*>(ckey);  // aliases the chunk during scatter
+    p += sizeof(unsigned) * ch;
     int* heads = reinterpret_cast<int*>(p);
     p += sizeof(int) * MAX_CELLS;
+    unsigned* cursor = reinterpret_cast<unsigned*>(smem);  // aliases chunk buffer + grid during the scatter
     const int maxc = cfg.max_corners;
     const int d = blockIdx.x;
     short2* axy;
@@ -582,11 +678,14 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         axy = reinterpret_cast<short2*>(p);
         p += sizeof(short2) * maxc;
         anext = reinterpret_cast<int*>(p);
+        p += sizeof(int) * maxc;
     } else {
         axy = g_axy + (size_t)d * maxc;
         anext = g_anext + (size_t)d * maxc;
     }
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0, wr = (rw + 31) >> 5;
+    uint32_t* bm = reinterpret_cast<uint32_t*>(p);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned n = s.count[d];
     const unsigned long long mb = s.maxbits[d];
     // candidates below quality * max are not the reference's (the fast path's
@@ -607,7 +706,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     unsigned long long* sk = s.sort_key + (size_t)d * s.cap;
     unsigned* si = s.sort_idx + (size_t)d * s.cap;
 
-    // ---- histogram + exclusive scan + scatter into bucket order
+    // ---- A. histogram + exclusive scan + scatter into bucket order
     for (int b = tid; b < kBuckets; b += SEL_THREADS) cursor[b] = 0;
     __syncthreads();
     for (unsigned i = tid; i < n; i += SEL_THREADS)
@@ -638,123 +737,125 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         sk[pos] = k;
         si[pos] = ci[i];
     }
-    // ---- accepted-corner grid: cell >= min_distance and <= MAX_CELLS cells
-    if (tid == 0) {
-        const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
-        int cell = max(1, (int)ceil(cfg.min_distance));
-        while ((long long)((rw + cell - 1) / cell) * ((rh + cell - 1) / cell) > MAX_CELLS) ++cell;
-        S.cell = cell;
-        S.gw = (rw + cell - 1) / cell;
-        S.gh = (rh + cell - 1) / cell;
-        S.naccepted = 0;
-        S.done = 0;
-        S.b0 = 0;
-        S.chunk = CHUNK;
-    }
-    __syncthreads();
-    for (int c = tid; c < S.gw * S.gh; c += SEL_THREADS) heads[c] = -1;
     __threadfence_block();
     __syncthreads();
+    // ---- B. grid (cells >= min_distance, <= MAX_CELLS) and bitmap, cleared
+    int cell = max(1, (int)ceil(cfg.min_distance));
+    while ((long long)((rw + cell - 1) / cell) * ((rh + cell - 1) / cell) > MAX_CELLS) ++cell;
+    const int gw = (rw + cell - 1) / cell, gh = (rh + cell - 1) / cell;
+    for (int c = tid; c < gw * gh; c += SEL_THREADS) heads[c] = -1;
     const double md2 = dmul(cfg.min_distance, cfg.min_distance);
-    const int gw = S.gw, gh = S.gh, cell = S.cell;
+    int R = 0;  // largest row offset of a disc: R*R < md2
+    if (use_bm) {
+        for (size_t k = tid; k < (size_t)wr * rh; k += SEL_THREADS) bm[k] = 0u;
+        R = (int)sqrt(md2);
+        while ((double)((long long)(R + 1) * (R + 1)) < md2) ++R;
+        while (R > 0 && !((double)((long long)R * R) < md2)) --R;
+        for (int k = tid; k < kHwMax; k += SEL_THREADS) S.hw[k] = (short)min(disc_reach(md2, k), 32767);
+    }
+    __threadfence_block();
+    __syncthreads();
+    int nacc = 0;
     if (redo) {
         // continue after the first pass: its corners are the reference's first
         // out_n corners (the cut list was a prefix), so they seed the grid and
         // only the band below the first cut is scanned
-        const int n0 = out_n[d];
-        for (int k = tid; k < n0; k += SEL_THREADS) {
+        nacc = out_n[d];
+        for (int k = tid; k < nacc; k += SEL_THREADS) {
             const double2 q = out_xy[(size_t)d * maxc + k];
             const int x = (int)q.x, y = (int)q.y;
             axy[k] = make_short2((short)x, (short)y);
             anext[k] = atomicExch(&heads[((y - roi.y0) / cell) * gw + (x - roi.x0) / cell], k);
         }
-        if (tid == 0) S.naccepted = n0;
         __threadfence_block();
         __syncthreads();
     }
-
-    while (true) {
-        // ---- next chunk of whole buckets [b0, b1) with <= CAP candidates
-        if (tid == 0) {
-            int b0 = S.b0;
-            while (b0 < kBuckets && S.bstart[b0 + 1] == S.bstart[b0]) ++b0;
-            S.b0 = b0;
-            if (b0 >= kBuckets) {
-                S.done = 1;
-            } else {
-                const unsigned limit = S.bstart[b0] + S.chunk;
-                int lo = b0 + 1, hi = kBuckets;  // largest b1 with bstart[b1] <= limit
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (S.bstart[mid] <= limit) lo = mid;
-                    else hi = mid - 1;
-                }
-                S.big = S.bstart[b0 + 1] - S.bstart[b0] > (unsigned)CAP;
-                S.b1 = S.big ? b0 + 1 : lo;
+    int marked = 0;  // corners [0, marked) are in the bitmap
+    // ---- C. chunks of whole buckets in score order
+    int b0 = 0;
+    while (b0 < kBuckets && nacc < maxc) {
+        if (use_bm && marked < nacc) {  // the CTA marks the new corners' discs: (corner, row) items
+            const int rows = 2 * R + 1;
+            const long long items = (long long)(nacc - marked) * rows;
+            for (long long i = tid; i < items; i += SEL_THREADS) {
+                const int k = marked + (int)(i / rows), dy = (int)(i % rows) - R;
+                const short2 q = axy[k];
+                mark_row(bm, wr, rw, rh, q.x - roi.x0, q.y - roi.y0, dy, md2, S.hw);
             }
+            marked = nacc;
+            __threadfence_block();
+            __syncthreads();
         }
-        __syncthreads();
-        if (S.done) break;
-        const unsigned lo = S.bstart[S.b0], hi = S.bstart[S.b1];
-        const bool big = S.big;
-        if (big) {  // rare: tie-heavy bucket -> sort it in global memory
-            global_merge_sort(sk + lo, si + lo, const_cast<unsigned long long*>(ck) + lo,
-                              const_cast<unsigned*>(ci) + lo, hi - lo);
-        }
-        for (unsigned c0 = lo; c0 < hi; c0 += CAP) {
-            const unsigned m = min((unsigned)CAP, hi - c0);
-            // load + grid prefilter + compaction (survivors keep relative order
-            // only within a sorted big bucket; otherwise they are sorted below)
-            constexpr int PER = CAP / SEL_THREADS;
-            unsigned long long kk[PER];
-            unsigned ii[PER];
-            unsigned alive = 0;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const unsigned j = tid * PER + q;
-                kk[q] = 0;
-                ii[q] = 0;
-                if (j < m) {
-                    kk[q] = sk[c0 + j];
-                    ii[q] = si[c0 + j];
-                    const int x = (int)(ii[q] % (unsigned)w), y = (int)(ii[q] / (unsigned)w);
-                    if (!conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2))
-                        alive |= 1u << q;
-                }
+        int b1;  // largest run of whole buckets with <= ch candidates (at least one)
+        {
+            const unsigned limit = S.bstart[b0] + (unsigned)ch;
+            int lo = b0 + 1, hi = kBuckets;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (S.bstart[mid] <= limit) lo = mid;
+                else hi = mid - 1;
             }
-            const unsigned off = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
+            b1 = lo;
+        }
+        const unsigned c_lo = S.bstart[b0], c_hi = S.bstart[b1];
+        b0 = b1;
+        if (c_hi == c_lo) continue;
+        const bool big = c_hi - c_lo > (unsigned)ch;  // one tie-heavy bucket: exact order in global first
+        if (big)
+            global_merge_sort(sk + c_lo, si + c_lo, const_cast<unsigned long long*>(ck) + c_lo,
+                              const_cast<unsigned*>(ci) + c_lo, c_hi - c_lo);
+        for (unsigned c0 = c_lo; c0 < c_hi && nacc < maxc; c0 += ch) {
+            const unsigned m = min((unsigned)ch, c_hi - c0);
+            // prefilter: thread t tests the contiguous run [t*per, (t+1)*per)
+            const unsigned per = (m + SEL_THREADS - 1) / SEL_THREADS;
+            const unsigned j0 = min(tid * per, m), j1 = min(j0 + per, m);
+            unsigned alive = 0;  // bit q: candidate j0 + q survives (per <= 32: ch <= 32 * threads)
+            for (unsigned j = j0; j < j1; ++j) {
+                const unsigned id = si[c0 + j];
+                const int x = (int)(id % (unsigned)w), y = (int)(id / (unsigned)w);
+                const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
+                                       : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
+                if (!ex) alive |= 1u << (j - j0);
+            }
+            unsigned o = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
             const unsigned ns = S.total;
-            // adapt the chunk: few survivors -> larger chunks (fewer passes);
-            // many -> smaller ones (more prefiltering before the serial greedy)
-            if (tid == 0) {
-                if (ns < 64 && S.chunk < CAP) S.chunk = min(2 * S.chunk, CAP);  // whole chunks stay <= CAP
-                else if (ns > 512 && S.chunk > 256) S.chunk /= 2;
-            }
-            {
-                unsigned o = off;
-#pragma unroll
-                for (int q = 0; q < PER; ++q)
-                    if (alive & (1u << q)) {
-                        ckey[o] = kk[q];
-                        cidx[o] = ii[q];
-                        ++o;
-                    }
+            for (unsigned a = alive; a; a &= a - 1) {
+                const unsigned j = j0 + __ffs(a) - 1;
+                ckey[o] = sk[c0 + j];
+                cidx[o] = si[c0 + j];
+                ++o;
             }
             __syncthreads();
             if (ns == 0) continue;
+            // exact order of the survivors (a merge-sorted big bucket is in order already)
             if (!big) {
-                int np = 1;
-                while (np < (int)ns) np <<= 1;
-                for (int j = ns + tid; j < np; j += SEL_THREADS) {
-                    ckey[j] = 0;
-                    cidx[j] = 0xffffffffu;
+                if (ns <= 32) {
+                    if (warp == 0) {
+                        unsigned long long k = 0;
+                        unsigned id = 0xffffffffu;
+                        if ((unsigned)lane < ns) {
+                            k = ckey[lane];
+                            id = cidx[lane];
+                        }
+                        warp_sort32(k, id);
+                        if ((unsigned)lane < ns) {
+                            ckey[lane] = k;
+                            cidx[lane] = id;
+                        }
+                    }
+                } else {
+                    int np = 1;
+                    while (np < (int)ns) np <<= 1;
+                    for (int j = ns + tid; j < np; j += SEL_THREADS) {
+                        ckey[j] = 0;
+                        cidx[j] = 0xffffffffu;
+                    }
+                    __syncthreads();
+                    bitonic_sort(ckey, cidx, np);
                 }
-                __syncthreads();
-                bitonic_sort(ckey, cidx, np);
             }
-            // ---- exact greedy over the sorted survivors, 32 at a time
-            if (tid < 32) {
-                int nacc = S.naccepted;
+            // ---- the greedy walk over the sorted survivors, 32 at a time
+            if (warp == 0) {
                 for (unsigned w0 = 0; w0 < ns && nacc < maxc; w0 += 32) {
                     const unsigned j = w0 + lane;
                     int x = 0, y = 0;
@@ -765,17 +866,20 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                         ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
                     }
                     const unsigned live = __ballot_sync(0xffffffffu, ok);
+                    if (!live) continue;
                     // earlier live lanes closer than min_distance: all 32 sources in an
                     // unrolled loop, so the shuffles issue back to back instead of as a
-                    // dependent chain over the live set
+                    // dependent chain over the live set (one live lane needs none)
                     unsigned conf = 0;
+                    if (live & (live - 1)) {
 #pragma unroll
-                    for (int src = 0; src < 32; ++src) {
-                        const int sx = __shfl_sync(0xffffffffu, x, src);
-                        const int sy = __shfl_sync(0xffffffffu, y, src);
-                        const long long dx = x - sx, dy = y - sy;
-                        if (src < lane && ((live >> src) & 1u) && (double)(dx * dx + dy * dy) < md2)
-                            conf |= 1u << src;
+                        for (int src = 0; src < 32; ++src) {
+                            const int sx = __shfl_sync(0xffffffffu, x, src);
+                            const int sy = __shfl_sync(0xffffffffu, y, src);
+                            const long long dx = x - sx, dy = y - sy;
+                            if (src < lane && ((live >> src) & 1u) && (double)(dx * dx + dy * dy) < md2)
+                                conf |= 1u << src;
+                        }
                     }
                     unsigned acc = live;  // no conflict inside the batch: every live lane is accepted
                     if (__ballot_sync(0xffffffffu, conf != 0)) {  // rank-order resolution
@@ -794,28 +898,33 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                         const int cid = ((y - roi.y0) / cell) * gw + (x - roi.x0) / cell;
                         anext[slot] = atomicExch(&heads[cid], slot);
                         out_xy[(size_t)d * maxc + slot] = make_double2((double)x, (double)y);
-                        out_score[(size_t)d * maxc + slot] =
-                            __longlong_as_double((long long)ckey[j]);
+                        out_score[(size_t)d * maxc + slot] = __longlong_as_double((long long)ckey[j]);
                     }
                     nacc += __popc(acc);
                     __syncwarp();
                 }
-                if (lane == 0) {
-                    S.naccepted = nacc;
-                    if (nacc >= maxc) S.done = 1;
-                }
+                if (lane == 0) S.nacc = nacc;
             }
             __syncthreads();
-            if (S.done) break;
+            nacc = S.nacc;
+            if (use_bm && c0 + ch < c_hi) {  // more slices of a big bucket follow: mark now
+                const int rows = 2 * R + 1;
+                const long long items = (long long)(nacc - marked) * rows;
+                for (long long i = tid; i < items; i += SEL_THREADS) {
+                    const int k = marked + (int)(i / rows), dy = (int)(i % rows) - R;
+                    const short2 q = axy[k];
+                    mark_row(bm, wr, rw, rh, q.x - roi.x0, q.y - roi.y0, dy, md2, S.hw);
+                }
+                marked = nacc;
+                __threadfence_block();
+                __syncthreads();
+            }
         }
-        if (S.done) break;
-        if (tid == 0) S.b0 = S.b1;
-        __syncthreads();
     }
     if (tid == 0) {
-        out_n[d] = S.naccepted;
+        out_n[d] = nacc;
         // the cut prefix ran out before max_corners: redo from the full list
-        if (!redo && cut && S.naccepted < maxc) s.flags[d] |= 2;
+        if (!redo && cut && nacc < maxc) s.flags[d] |= 2;
     }
 }
 
@@ -831,14 +940,10 @@ __global__ void gradients_kernel(const uint8_t* __restrict__ f, int w, int h, do
 
 }  // namespace
 
-size_t select_smem_bytes(const stabgpu_detect_cfg& cfg, int cap) {
-    size_t b = ((sizeof(SelShared) + 15) & ~size_t(15)) + (sizeof(unsigned long long) + sizeof(unsigned)) * cap +
-               sizeof(int) * MAX_CELLS;
-    if (cfg.max_corners <= SMEM_CORNERS) b += (sizeof(short2) + sizeof(int)) * cfg.max_corners;
-    return b;
+size_t bitmap_words(stabgpu_roi roi) {
+    return (size_t)((roi.x1 - roi.x0 + 31) >> 5) * (roi.y1 - roi.y0);
 }
 
-size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int, int) { return select_smem_bytes(cfg, CAP_MAX); }
 
 void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
                    DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
@@ -882,18 +987,43 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
         resp_generic_kernel<<<grid, 128, 0, st>>>(fr, roi, half, 1, cfg.quality_level, s.maxbits,
                                                   s.count, s.cand_key, s.cand_idx, s.cap, nullptr);
     }
-    // two 512-thread CTAs per SM when the batch outnumbers the SMs and both fit
-    const size_t smem_small = select_smem_bytes(cfg, 3072);
-    const bool pair = nD > sm_count() && 2 * (smem_small + 1024) <= 228 * 1024;
-    const size_t smem = pair ? smem_small : select_smem_bytes(cfg, CAP_MAX);
-    auto sel = pair ? select_kernel<512, 3072> : select_kernel<1024, CAP_MAX>;
+    // shared memory per CTA: chunk buffer (12 B per candidate) + grid (32 KB) +
+    // accepted corners (8 B each, when <= SMEM_CORNERS) [+ exclusion bitmap
+    // when every candidate is listed (no cut) and it fits]; two 512-thread CTAs
+    // per SM when the batch outnumbers the SMs and a 2048-candidate chunk fits
+    // twice (static shared memory included)
+    const bool no_cut = !fast || cfg.max_corners * 3.141592653589793 * cfg.min_distance * cfg.min_distance > 2.0 * rw * rh;
+    const size_t bm_bytes = no_cut ? 4 * bitmap_words(roi) : 0;
+    const size_t fixed = sizeof(int) * MAX_CELLS +
+                         (cfg.max_corners <= SMEM_CORNERS ? (sizeof(short2) + sizeof(int)) * cfg.max_corners : 0);
+    const size_t stat = sizeof(SelShared) + 1024;  // static shared + per-CTA reserve
+    auto fit = [&](size_t budget, int cmin, int& ch, bool& bm) {  // largest chunk, bitmap if it fits
+        for (int pass = 0; pass < 2; ++pass) {
+            bm = pass == 0 && bm_bytes > 0;
+            if (pass == 0 && !bm) continue;
+            for (int c = 8192; c >= cmin; c >>= 1)
+                if (stat + 12 * (size_t)c + fixed + (bm ? bm_bytes : 0) <= budget) {
+                    ch = c;
+                    return true;
+                }
+        }
+        bm = false;
+        return false;
+    };
+    int ch = 1024;
+    bool use_bm = false;
+    const bool pair = nD > sm_count() && fit(114 * 1024, 2048, ch, use_bm);
+    if (!pair) fit(227 * 1024, 256, ch, use_bm);
+    ch = std::min(ch, 2048);  // measured: larger chunks sort more survivors per walk (C1 1.04 ms at 2048, 1.09 at 4096)
+    const size_t smem = std::max<size_t>(12 * (size_t)ch + fixed + (use_bm ? bm_bytes : 0), 4 * kBuckets);
+    auto sel = pair ? select_kernel<512> : select_kernel<1024>;
     const int sel_threads = pair ? 512 : 1024;
     ensure_smem(sel, smem);
     short2* g_axy = nullptr;
     int* g_anext = nullptr;
     if (cfg.max_corners > SMEM_CORNERS) {
-        // large budgets keep the accepted list in global scratch (sort_idx tail is free)
-        // a failed allocation stays in cudaGetLastError for the caller's check_launch
+        // large budgets keep the accepted list in global scratch
+        // (a failed allocation stays in cudaGetLastError for the caller's check_launch)
         if (cudaMallocAsync((void**)&g_axy, sizeof(short2) * (size_t)nD * cfg.max_corners, st) != cudaSuccess)
             return;
         if (cudaMallocAsync((void**)&g_anext, sizeof(int) * (size_t)nD * cfg.max_corners, st) != cudaSuccess) {
@@ -903,12 +1033,14 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     }
     DetectScratch sf = s;
     if (!fast) sf.flags = nullptr;
-    sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy, g_anext, 0);
+    sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy, g_anext, ch,
+                                       use_bm ? 1 : 0, 0);
     if (fast) {  // frames whose cut prefix ran out: full candidate list (usually none)
         resp_redo_reset_kernel<<<nD, 32, 0, st>>>(s);
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 1);
-        sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy, g_anext, 1);
+        sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy, g_anext, ch,
+                                           use_bm ? 1 : 0, 1);
     }
     if (g_axy) {
         cudaFreeAsync(g_axy, st);

@@ -76,7 +76,6 @@ struct DetectScratch {
 constexpr int kRespBins = 2048;
 constexpr int kBuckets = 8192;
 constexpr int kBucketShift = 13;
-size_t detect_smem_bytes(const stabgpu_detect_cfg& cfg, int roi_w, int roi_h);
 // Detects corners on nD frames at base + d*stride (d = 0..nD-1); writes up to
 // max_corners points per frame (out_xy[d*max + k], out_score) and out_n[d].
 void launch_detect(PlaneBatch frames, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
