@@ -289,21 +289,28 @@ def run_ours(args, cfg):
     host = render(cfg, lo, count, pinned=True)
     gen_s = time.time() - t0
     dev = [h.cuda() for h in host]
-    outs = [torch.empty_like(d) for d in dev]
-    host_out = [torch.empty_like(h, pin_memory=True) for h in host]
+    own = (sh.own_end - sh.own_begin) if world > 1 else n
+    outs = [torch.empty((own,) + tuple(d.shape[1:]), dtype=d.dtype, device=d.device) for d in dev]
+    host_out = [torch.empty((own,) + tuple(h.shape[1:]), dtype=h.dtype, pin_memory=True) for h in host]
     ctx = _lib.context(local)
     ctx.enable_timing(True)
     stream = torch.cuda.current_stream(local)
     ctx.set_stream(stream.cuda_stream)
+    nccl = world > 1 and args.dist_backend == "nccl"
+    if nccl:  # the context's own NCCL communicator: records all-gathered device to device
+        pipeline.init_comm(ctx)
+
+    chroma = (dev[1], dev[2]) if planes == 3 else (None, None)
+    ochroma = (outs[1], outs[2]) if planes == 3 else (None, None)
 
     def step_device():
         if world == 1:
-            pipeline.stabilize_sequence_device(dev[0], cfg.stab, *(dev[1:] if planes == 3 else (None, None)),
-                                               out_y=outs[0], out_cb=outs[1] if planes == 3 else None,
-                                               out_cr=outs[2] if planes == 3 else None, records=False)
-        else:
-            pipeline.stabilize_sharded(n, dev[0], lo, cfg.stab, rank, world,
-                                       *(dev[1:] if planes == 3 else (None, None)), device=local)
+            pipeline.stabilize_sequence_device(dev[0], cfg.stab, *chroma, out_y=outs[0], out_cb=ochroma[0],
+                                               out_cr=ochroma[1], records=False)
+        elif nccl:
+            pipeline.stabilize_sharded_device(ctx, n, dev[0], cfg.stab, *chroma, outs[0], *ochroma, records=False)
+        else:  # gloo functional check: host-side exchange of the records
+            pipeline.stabilize_sharded(n, dev[0], lo, cfg.stab, rank, world, *chroma, device=local)
 
     cfg_c = cfg.stab.c()
     rec = np.zeros(n, pipeline.RECORD_DT)
@@ -315,18 +322,19 @@ def run_ours(args, cfg):
                 n, spec.width, spec.height, spec.width if planes == 3 else 0,
                 spec.height if planes == 3 else 0, cfg_c, host_out[0],
                 host_out[1] if planes == 3 else None, host_out[2] if planes == 3 else None, rec)
-        else:
-            d = [h.cuda(non_blocking=True) for h in host]
-            oy, ob, orr, _ = pipeline.stabilize_sharded(n, d[0], lo, cfg.stab, rank, world,
-                                                        *(d[1:] if planes == 3 else (None, None)),
-                                                        device=local)
-            a, b = sh.own_begin - lo, sh.own_end - lo
-            if oy is not None:
-                host_out[0][a:b].copy_(oy, non_blocking=True)
-                if planes == 3:
-                    host_out[1][a:b].copy_(ob, non_blocking=True)
-                    host_out[2][a:b].copy_(orr, non_blocking=True)
-            torch.cuda.synchronize()
+        elif nccl:  # C-ABI host-buffer entry point: chunked upload/motion, NCCL all-gather, compose/download
+            pipeline.stabilize_sharded_host(ctx, n, host[0], cfg.stab, *(host[1:] if planes == 3 else (None, None)),
+                                            host_out[0], *(host_out[1:] if planes == 3 else (None, None)),
+                                            records=False)
+        else:  # gloo: the same entry point split at the exchange
+            hch = host[1:] if planes == 3 else (None, None)
+            mine = pipeline.shard_motion(ctx, n, world, rank, host[0], cfg.stab, *hch)
+            shards = pipeline.shard_ranges(n, cfg.stab.flow.redetect_interval, world)
+            gathered = pipeline.exchange_motion(mine, max(s.count for s in shards))
+            motion = pipeline.assemble_motion(n, list(zip(shards, gathered)))
+            pipeline.shard_compose(ctx, n, world, rank, motion, cfg.stab, spec.width, spec.height,
+                                   spec.width if planes == 3 else 0, spec.height if planes == 3 else 0,
+                                   host_out[0], *(host_out[1:] if planes == 3 else (None, None)))
 
     def barrier():
         if world > 1:
@@ -385,8 +393,9 @@ def run_ours(args, cfg):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded BASELINE generator, host C)",
                 "config": workload(args, cfg),
-                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": fb * n,
-                        "d2h_bytes_per_step": fb * n + n * pipeline.RECORD_BYTES,
+                "e2e": {"value": e2e, "unit": UNIT,
+                        "h2d_bytes_per_step": fb * (sum(s.count + 1 for s in shards if s.count) if world > 1 else n),
+                        "d2h_bytes_per_step": fb * n + (n * pipeline.RECORD_BYTES if world == 1 else 0),
                         "ms_per_step": ms_e2e, "steps": args.steps, "warmup": args.warmup},
                 "ms_per_step_without_stage_events": ms_dev_plain,
                 "roofline": {"bound": "hbm", "kernel": "K8 compose_tma_kernel (fused warp + crop/resize, all planes)",

@@ -335,6 +335,55 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* dev_y, const uint8_t
                            const stabgpu_transform* host_corrections, double crop_ratio,
                            uint8_t* dev_out_y, uint8_t* dev_out_cb, uint8_t* dev_out_cr);
 
+/* ---- sharded Stage I over the GPUs of a box ------------
+ * The sequence is cut into contiguous re-detect-aligned shards (tracking
+ * state resets at every re-detect frame, flow.cpp:326-330): rank g estimates
+ * the motion of frames first_g+1 .. first_g+count_g from its resident frames
+ * first_g .. first_g+count_g (frame first_g, the previous rank's last frame,
+ * is the one-frame halo), the ~120 B/frame motion records of all ranks are
+ * all-gathered, every rank runs the sequential selector/trajectory/smoothing
+ * scan on identical input (bit-identical corrections everywhere) and
+ * composes its own frames [own_begin_g, own_end_g).  The partition is
+ * stabgpu_shard_range (== pipeline.shard_ranges). */
+#define STABGPU_NCCL_ID_BYTES 128
+int stabgpu_shard_range(int64_t n, int redetect_interval, int world, int rank, int64_t* first, int* count,
+                        int64_t* own_begin, int64_t* own_end);
+/* NCCL communicator owned by the context (one rank per GPU): rank 0 calls
+ * stabgpu_nccl_unique_id and shares the 128 bytes (e.g. over
+ * torch.distributed), every rank calls stabgpu_comm_init.  NCCL is resolved
+ * from libnccl.so.2 at run time. */
+int stabgpu_nccl_unique_id(unsigned char* id_out);
+int stabgpu_comm_init(stabgpu_ctx* ctx, const unsigned char* id, int nranks, int rank);
+/* One call per rank (world/rank from stabgpu_comm_init; a context without a
+ * communicator is world 1): host planes of the rank's frames first..first+
+ * count in, host planes of its own frames out.  Chunked upload overlaps the
+ * motion passes; the records are all-gathered device to device (ncclAllGather
+ * on the context stream); the compose of each chunk of own frames overlaps
+ * the download of the previous one.  records (optional): all n frames. */
+int stabgpu_stabilize_sharded(stabgpu_ctx* ctx, const uint8_t* host_y, const uint8_t* host_cb,
+                              const uint8_t* host_cr, int64_t n, int w, int h, int cw, int ch,
+                              const stabgpu_config* cfg, uint8_t* host_out_y, uint8_t* host_out_cb,
+                              uint8_t* host_out_cr, stabgpu_frame_record* records);
+/* Device-resident variant: dev_* hold the rank's frames first..first+count,
+ * dev_out_* receive its own frames [own_begin, own_end). */
+int stabgpu_stabilize_sharded_device(stabgpu_ctx* ctx, const uint8_t* dev_y, const uint8_t* dev_cb,
+                                     const uint8_t* dev_cr, int64_t n, int w, int h, int cw, int ch,
+                                     const stabgpu_config* cfg, uint8_t* dev_out_y, uint8_t* dev_out_cb,
+                                     uint8_t* dev_out_cr, stabgpu_frame_record* records);
+/* The same call split at the exchange, for a host-side all-gather (e.g. a
+ * gloo process group, or ranks emulated in one process): shard_motion keeps
+ * the rank's frames resident in the context and returns its count+1 motion
+ * records (record 0: frame first — the FIRST record on rank 0); the caller
+ * assembles all n records (pipeline.assemble_motion) and shard_compose plans
+ * and composes the rank's own frames. */
+int stabgpu_shard_motion(stabgpu_ctx* ctx, const uint8_t* host_y, const uint8_t* host_cb,
+                         const uint8_t* host_cr, int64_t n, int world, int rank, int w, int h, int cw,
+                         int ch, const stabgpu_config* cfg, stabgpu_motion_record* host_motion);
+int stabgpu_shard_compose(stabgpu_ctx* ctx, const stabgpu_motion_record* host_all_motion, int64_t n,
+                          int world, int rank, int w, int h, int cw, int ch, const stabgpu_config* cfg,
+                          uint8_t* host_out_y, uint8_t* host_out_cb, uint8_t* host_out_cr,
+                          stabgpu_frame_record* records);
+
 /* ---- Stage II: streaming (one frame at a time) ------------------------
  * Replaces run_streaming (pipeline.hpp:72-76 / pipeline.cpp:237-365) and the
  * MotionStage -> CompensationPlanner -> compose loop of run_offline

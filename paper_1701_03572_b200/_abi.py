@@ -124,6 +124,13 @@ PROTOTYPES = {
     "stabgpu_motion_chunk": (I, [V, V, C.c_int64, I, I, I, P(Config), V]),
     "stabgpu_plan_corrections": (I, [V, V, I, P(Config), V]),
     "stabgpu_compose_frames": (I, [V, V, V, V, I, I, I, I, I, V, C.c_double, V, V, V]),
+    "stabgpu_shard_range": (I, [C.c_int64, I, I, I, P(C.c_int64), c_ip, P(C.c_int64), P(C.c_int64)]),
+    "stabgpu_nccl_unique_id": (I, [V]),
+    "stabgpu_comm_init": (I, [V, V, I, I]),
+    "stabgpu_stabilize_sharded": (I, [V, V, V, V, C.c_int64, I, I, I, I, P(Config), V, V, V, V]),
+    "stabgpu_stabilize_sharded_device": (I, [V, V, V, V, C.c_int64, I, I, I, I, P(Config), V, V, V, V]),
+    "stabgpu_shard_motion": (I, [V, V, V, V, C.c_int64, I, I, I, I, I, I, P(Config), V]),
+    "stabgpu_shard_compose": (I, [V, V, C.c_int64, I, I, I, I, I, I, P(Config), V, V, V, V]),
     "stabgpu_stream_create": (I, [V, P(Config), I, I, I, I, P(V)]),
     "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
     "stabgpu_stream_finish": (I, [V, c_ip]),

@@ -25,6 +25,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the functions are resolved from libnccl.so.2 at run time
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -58,7 +61,39 @@ struct stabgpu_ctx {
     std::vector<TimedSpan> spans;
     unsigned long long* iters_host = nullptr;  // pinned: LK counters of the last motion pass
     bool iters_pending = false;
+    ncclComm_t comm = nullptr;  // multi-GPU sharding (stabgpu_comm_init)
+    int nranks = 1, rank = 0;
 };
+
+namespace {
+// NCCL is resolved at run time (dlopen), so the library loads without it and
+// shares the process's libnccl.so.2 (e.g. the one torch.distributed loaded).
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi a = [] {
+        NcclApi r;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return r;
+        r.get_unique_id = reinterpret_cast<decltype(r.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        r.comm_init_rank = reinterpret_cast<decltype(r.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        r.all_gather = reinterpret_cast<decltype(r.all_gather)>(dlsym(h, "ncclAllGather"));
+        r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+        r.ok = r.get_unique_id && r.comm_init_rank && r.all_gather && r.comm_destroy && r.error_string;
+        return r;
+    }();
+    return a;
+}
+}  // namespace
 
 namespace {
 
@@ -577,6 +612,7 @@ int stabgpu_destroy(stabgpu_ctx* c) {
         if (kv.second.p) cudaFree(kv.second.p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->iters_host) cudaFreeHost(c->iters_host);
+    if (c->comm) nccl_api().comm_destroy(c->comm);
     cudaStreamDestroy(c->own);
     cudaStreamDestroy(c->cin);
     cudaStreamDestroy(c->cout);
@@ -1467,6 +1503,324 @@ int stabgpu_compose_frames(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb
     }
     CUDA_TRY(cudaStreamSynchronize(st));
     return STABGPU_OK;
+}
+
+// ---- sharded Stage I ------------------------------------------
+int stabgpu_nccl_unique_id(unsigned char* out) {
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return set_err(STABGPU_CUDA, "libnccl.so.2 not found (needed for multi-GPU sharding)");
+    ncclUniqueId id;
+    const ncclResult_t r = api.get_unique_id(&id);
+    if (r != ncclSuccess) return set_err(STABGPU_CUDA, "ncclGetUniqueId: %s", api.error_string(r));
+    std::memcpy(out, id.internal, STABGPU_NCCL_ID_BYTES);
+    return STABGPU_OK;
+}
+
+int stabgpu_comm_init(stabgpu_ctx* ctx, const unsigned char* id, int nranks, int rank) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(STABGPU_INVALID_INPUT, "bad rank %d of %d", rank, nranks);
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return set_err(STABGPU_CUDA, "libnccl.so.2 not found (needed for multi-GPU sharding)");
+    cudaSetDevice(ctx->device);
+    if (ctx->comm) {
+        api.comm_destroy(ctx->comm);
+        ctx->comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, STABGPU_NCCL_ID_BYTES);
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = api.comm_init_rank(&c, nranks, uid, rank);
+    if (r != ncclSuccess) return set_err(STABGPU_CUDA, "ncclCommInitRank: %s", api.error_string(r));
+    ctx->comm = c;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return STABGPU_OK;
+}
+
+}  // extern "C"
+namespace {
+// Shard geometry of every rank: the pipeline.shard_ranges partition.
+struct ShardGeo {
+    long long first;  // motion chunk frames first .. first+count (first: a re-detect frame)
+    int count;        // 0: the rank idles (more ranks than segments)
+    long long own_begin, own_end;
+};
+
+ShardGeo shard_geo(long long n, int R, int world, int g) {
+    const long long nseg = (n - 1 + R - 1) / R;
+    const long long s0 = nseg * g / world, s1 = nseg * (g + 1) / world;
+    ShardGeo o;
+    o.first = std::min(s0 * R, n - 1);
+    const long long last = std::min(s1 * R, n - 1);
+    o.own_begin = s0 == 0 ? 0 : o.first + 1;
+    o.own_end = last + 1;
+    o.count = (int)(last - o.first);
+    if (s0 == s1) o.first = o.count = 0, o.own_begin = o.own_end = 0;
+    return o;
+}
+
+// Uploads this rank's frames [first, first+count] into the context's resident
+// shard buffers in chunks and estimates the motion of each segment as soon as
+// its last frame has arrived (upload of chunk k+1 overlaps the motion of chunk
+// k).  local_motion[0 .. count]: frame `first` (FIRST record on rank 0, else
+// untouched), frames first+1 .. first+count.
+int shard_motion(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const uint8_t* hcr, const ShardGeo& g,
+                 int w, int h, int cw, int ch, const stabgpu_config& cfg, stabgpu_motion_record* local_motion) {
+    cudaStream_t st = ctx->stream;
+    const bool chroma = hcb && hcr;
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    const long long nres = (long long)g.count + 1;
+    DBUF(uint8_t, dy, "shard_y", fl * nres);
+    if (chroma) {
+        DBUF(uint8_t, a, "shard_cb", fc * nres);
+        DBUF(uint8_t, b, "shard_cr", fc * nres);
+        (void)a;
+        (void)b;
+    }
+    uint8_t* dcb = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cb"].p) : nullptr;
+    uint8_t* dcr = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cr"].p) : nullptr;
+    stabgpu_motion_record* base = local_motion - g.first;  // motion[global frame]
+    const int R = cfg.flow.redetect_interval;
+    const int C = R * std::max(1, 60 / R);  // frames per upload chunk
+    const int nchunks = (int)((nres + C - 1) / C);
+    std::vector<cudaEvent_t> in_ev(nchunks);
+    for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int rc = STABGPU_OK;
+    for (int k = 0; k < nchunks && !rc; ++k) {
+        const size_t f0 = (size_t)k * C, nf = std::min<size_t>(C, nres - f0);
+        if (cudaMemcpyAsync(dy + f0 * fl, hy + f0 * fl, nf * fl, cudaMemcpyHostToDevice, ctx->cin) ||
+            (chroma && (cudaMemcpyAsync(dcb + f0 * fc, hcb + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin) ||
+                        cudaMemcpyAsync(dcr + f0 * fc, hcr + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin))))
+            rc = set_err(STABGPU_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+        cudaEventRecord(in_ev[k], ctx->cin);
+    }
+    // segments [first + s R, min(first + (s+1) R, first + count)] of the chunk
+    const long long nseg = (g.count + R - 1) / R;
+    long long seg_done = 0;
+    for (int k = 0; k < nchunks && !rc; ++k) {
+        cudaStreamWaitEvent(st, in_ev[k], 0);
+        const long long arrived = std::min<long long>((long long)(k + 1) * C, nres);  // local frames [0, arrived)
+        long long seg_end = seg_done;
+        while (seg_end < nseg && std::min<long long>((seg_end + 1) * R, g.count) < arrived) ++seg_end;
+        if (seg_end > seg_done) {
+            const long long a = seg_done * R, b = std::min<long long>(seg_end * R, g.count);
+            rc = run_motion(ctx, dy + a * fl, g.first + a, (int)(b - a), w, h, cfg, base);
+            seg_done = seg_end;
+        }
+    }
+    cudaStreamSynchronize(ctx->cin);
+    for (auto& e : in_ev) cudaEventDestroy(e);
+    return rc;
+}
+
+// Plans all n frames from the device motion records (the sequential scan,
+// identical on every rank) and composes this rank's own frames.  vy/vcb/vcr
+// and voy/vocb/vocr are frame-indexed device views (frame i at view + i *
+// plane); with host outputs, each chunk of own frames is downloaded behind
+// the compose of the next.
+int shard_finish(stabgpu_ctx* ctx, const stabgpu_motion_record* motion_all, long long n, const ShardGeo& g, int w,
+                 int h, int cw, int ch, bool chroma, const stabgpu_config& cfg, const uint8_t* vy,
+                 const uint8_t* vcb, const uint8_t* vcr, uint8_t* voy, uint8_t* vocb, uint8_t* vocr, uint8_t* hoy,
+                 uint8_t* hocb, uint8_t* hocr, stabgpu_frame_record* records) {
+    cudaStream_t st = ctx->stream;
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    DBUF(stabgpu_frame_record, rec, "seq_rec", n);
+    DBUF(double4, cum, "seq_cum", n);
+    DBUF(FramePlan, plan, "seq_plan", n);
+    PlanState* ps;
+    TRY(init_plan_state(ctx, cfg, &ps));
+    {
+        Timer tm(ctx, 5);
+        launch_plan_scan(motion_all, 0, n, cfg, ps, rec, cum, st);
+        // every frame's correction (the records cover all n frames; n threads)
+        launch_plan_smooth(cum, n, true, 0, n, cfg.smooth_radius, rec, plan,
+                           PlanGeom{w, h, chroma ? cw : 0, chroma ? ch : 0, cfg.crop_ratio}, st);
+    }
+    ctx->stats.launches += 2;
+    TRY(check_launch("plan"));
+    const long long own = g.own_end - g.own_begin;
+    int rc = STABGPU_OK;
+    if (own > 0) {
+        const int C = hoy ? 60 : (int)own;  // host outputs: chunks downloaded behind the next compose
+        const int nchunks = (int)((own + C - 1) / C);
+        std::vector<cudaEvent_t> done(nchunks);
+        for (auto& e : done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (int k = 0; k < nchunks && !rc; ++k) {
+            const long long f0 = g.own_begin + (long long)k * C, nf = std::min<long long>(C, g.own_end - f0);
+            {
+                Timer tm(ctx, 4);
+                rc = compose_range(ctx, vy, vcb, vcr, f0, nf, w, h, cw, ch, plan, cfg.crop_ratio, voy, vocb, vocr);
+            }
+            if (rc) break;
+            if (!hoy) continue;
+            cudaEventRecord(done[k], st);
+            cudaStreamWaitEvent(ctx->cout, done[k], 0);
+            const size_t o = (size_t)(f0 - g.own_begin);
+            if (cudaMemcpyAsync(hoy + o * fl, voy + f0 * fl, nf * fl, cudaMemcpyDeviceToHost, ctx->cout) ||
+                (chroma && (cudaMemcpyAsync(hocb + o * fc, vocb + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout) ||
+                            cudaMemcpyAsync(hocr + o * fc, vocr + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout))))
+                rc = set_err(STABGPU_CUDA, "download failed: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+        cudaStreamSynchronize(ctx->cout);
+        for (auto& e : done) cudaEventDestroy(e);
+    }
+    if (rc) return rc;
+    TRY(plan_error(ctx, ps));
+    if (records)
+        CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return check_launch("stabilize_sharded");
+}
+
+// shard_finish on the context's resident shard buffers (host entry points)
+int shard_finish_host(stabgpu_ctx* ctx, const stabgpu_motion_record* motion_all, long long n, const ShardGeo& g,
+                      int w, int h, int cw, int ch, bool chroma, const stabgpu_config& cfg, uint8_t* hoy,
+                      uint8_t* hocb, uint8_t* hocr, stabgpu_frame_record* records) {
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    const long long own = std::max<long long>(g.own_end - g.own_begin, 1);
+    uint8_t* dy = static_cast<uint8_t*>(ctx->bufs["shard_y"].p);
+    uint8_t* dcb = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cb"].p) : nullptr;
+    uint8_t* dcr = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cr"].p) : nullptr;
+    DBUF(uint8_t, doy, "shard_oy", fl * own);
+    uint8_t *docb = nullptr, *docr = nullptr;
+    if (chroma) {
+        DBUF(uint8_t, a, "shard_ocb", fc * own);
+        DBUF(uint8_t, b, "shard_ocr", fc * own);
+        docb = a;
+        docr = b;
+    }
+    // frame-indexed views: frame i of the sequence at view + i * plane
+    return shard_finish(ctx, motion_all, n, g, w, h, cw, ch, chroma, cfg, dy ? dy - g.first * fl : nullptr,
+                        chroma ? dcb - g.first * fc : nullptr, chroma ? dcr - g.first * fc : nullptr,
+                        doy - g.own_begin * fl, chroma ? docb - g.own_begin * fc : nullptr,
+                        chroma ? docr - g.own_begin * fc : nullptr, hoy, hocb, hocr, records);
+}
+
+// The all-gather of every rank's count+1 records (send) and their scatter
+// into the frame-indexed motion array ma (record 0 of rank 0 is frame 0).
+int shard_exchange(stabgpu_ctx* ctx, long long n, int R, int world, const stabgpu_motion_record* send,
+                   stabgpu_motion_record* recv, size_t blk, stabgpu_motion_record* ma) {
+    cudaStream_t st = ctx->stream;
+    const size_t bytes = blk * sizeof(stabgpu_motion_record);
+    if (world > 1) {
+        const ncclResult_t r = nccl_api().all_gather(send, recv, bytes, ncclUint8, ctx->comm, st);
+        if (r != ncclSuccess) return set_err(STABGPU_CUDA, "ncclAllGather: %s", nccl_api().error_string(r));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    for (int k = 0; k < world; ++k) {
+        const ShardGeo o = shard_geo(n, R, world, k);
+        if (o.count == 0) continue;
+        const stabgpu_motion_record* src = recv + (size_t)k * blk;
+        if (o.first == 0) CUDA_TRY(cudaMemcpyAsync(ma, src, sizeof(stabgpu_motion_record), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ma + o.first + 1, src + 1, sizeof(stabgpu_motion_record) * o.count,
+                                 cudaMemcpyDeviceToDevice, st));
+    }
+    return STABGPU_OK;
+}
+
+int validate_shard(const stabgpu_config& cfg, long long n, int world, int rank, int w, int h) {
+    TRY(validate_all(cfg));
+    TRY(validate_frame(w, h));
+    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
+    if (world < 1 || rank < 0 || rank >= world) return set_err(STABGPU_INVALID_INPUT, "bad rank %d of %d", rank, world);
+    return STABGPU_OK;
+}
+}  // namespace
+extern "C" {
+
+int stabgpu_shard_range(int64_t n, int redetect_interval, int world, int rank, int64_t* first, int* count,
+                        int64_t* own_begin, int64_t* own_end) {
+    if (n < 2 || redetect_interval < 1 || world < 1 || rank < 0 || rank >= world)
+        return set_err(STABGPU_INVALID_INPUT, "bad shard request");
+    const ShardGeo g = shard_geo(n, redetect_interval, world, rank);
+    *first = g.first;
+    *count = g.count;
+    *own_begin = g.own_begin;
+    *own_end = g.own_end;
+    return STABGPU_OK;
+}
+
+int stabgpu_shard_motion(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const uint8_t* hcr, int64_t n,
+                         int world, int rank, int w, int h, int cw, int ch, const stabgpu_config* cfgp,
+                         stabgpu_motion_record* host_motion) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_shard(cfg, n, world, rank, w, h));
+    cudaSetDevice(ctx->device);
+    begin_timing(ctx);
+    const ShardGeo g = shard_geo(n, cfg.flow.redetect_interval, world, rank);
+    if (g.count == 0) return STABGPU_OK;
+    DBUF(stabgpu_motion_record, lm, "shard_motion", (size_t)g.count + 1);
+    TRY(shard_motion(ctx, hy, (hcb && hcr) ? hcb : nullptr, (hcb && hcr) ? hcr : nullptr, g, w, h, cw, ch, cfg, lm));
+    CUDA_TRY(cudaMemcpyAsync(host_motion, lm, sizeof(stabgpu_motion_record) * ((size_t)g.count + 1),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return check_launch("shard_motion");
+}
+
+int stabgpu_shard_compose(stabgpu_ctx* ctx, const stabgpu_motion_record* host_all_motion, int64_t n, int world,
+                          int rank, int w, int h, int cw, int ch, const stabgpu_config* cfgp, uint8_t* hoy,
+                          uint8_t* hocb, uint8_t* hocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    TRY(validate_shard(cfg, n, world, rank, w, h));
+    cudaSetDevice(ctx->device);
+    const ShardGeo g = shard_geo(n, cfg.flow.redetect_interval, world, rank);
+    const bool chroma = hocb && hocr && cw > 0 && ch > 0 && ctx->bufs.count("shard_cb");
+    DBUF(stabgpu_motion_record, ma, "shard_motion_all", n);
+    CUDA_TRY(cudaMemcpyAsync(ma, host_all_motion, sizeof(stabgpu_motion_record) * n, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    return shard_finish_host(ctx, ma, n, g, w, h, cw, ch, chroma, cfg, hoy, hocb, hocr, records);
+}
+
+int stabgpu_stabilize_sharded(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const uint8_t* hcr, int64_t n,
+                              int w, int h, int cw, int ch, const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
+                              uint8_t* hocr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    const int world = ctx->nranks, rank = ctx->rank;
+    TRY(validate_shard(cfg, n, world, rank, w, h));
+    if (world > 1 && !ctx->comm) return set_err(STABGPU_SEQUENCING, "stabilize_sharded needs stabgpu_comm_init first");
+    cudaSetDevice(ctx->device);
+    begin_timing(ctx);
+    cudaStream_t st = ctx->stream;
+    const int R = cfg.flow.redetect_interval;
+    const bool chroma = hcb && hcr && hocb && hocr;
+    const ShardGeo g = shard_geo(n, R, world, rank);
+    int maxcount = 0;
+    for (int k = 0; k < world; ++k) maxcount = std::max(maxcount, shard_geo(n, R, world, k).count);
+    const size_t blk = (size_t)maxcount + 1;  // records per rank in the all-gather
+    DBUF(stabgpu_motion_record, send, "shard_send", blk);
+    DBUF(stabgpu_motion_record, recv, "shard_recv", blk * world);
+    DBUF(stabgpu_motion_record, ma, "shard_motion_all", n);
+    if (g.count > 0) TRY(shard_motion(ctx, hy, chroma ? hcb : nullptr, chroma ? hcr : nullptr, g, w, h, cw, ch, cfg, send));
+    // ---- the one exchange: every rank's motion records, device to device
+    TRY(shard_exchange(ctx, n, R, world, send, recv, blk, ma));
+    return shard_finish_host(ctx, ma, n, g, w, h, cw, ch, chroma, cfg, hoy, hocb, hocr, records);
+}
+
+int stabgpu_stabilize_sharded_device(stabgpu_ctx* ctx, const uint8_t* dy, const uint8_t* dcb, const uint8_t* dcr,
+                                     int64_t n, int w, int h, int cw, int ch, const stabgpu_config* cfgp,
+                                     uint8_t* doy, uint8_t* docb, uint8_t* docr, stabgpu_frame_record* records) {
+    const stabgpu_config cfg = *cfgp;
+    const int world = ctx->nranks, rank = ctx->rank;
+    TRY(validate_shard(cfg, n, world, rank, w, h));
+    if (world > 1 && !ctx->comm) return set_err(STABGPU_SEQUENCING, "stabilize_sharded needs stabgpu_comm_init first");
+    cudaSetDevice(ctx->device);
+    begin_timing(ctx);
+    const int R = cfg.flow.redetect_interval;
+    const bool chroma = dcb && dcr && docb && docr;
+    const ShardGeo g = shard_geo(n, R, world, rank);
+    int maxcount = 0;
+    for (int k = 0; k < world; ++k) maxcount = std::max(maxcount, shard_geo(n, R, world, k).count);
+    const size_t blk = (size_t)maxcount + 1;
+    DBUF(stabgpu_motion_record, send, "shard_send", blk);
+    DBUF(stabgpu_motion_record, recv, "shard_recv", blk * world);
+    DBUF(stabgpu_motion_record, ma, "shard_motion_all", n);
+    if (g.count > 0) TRY(run_motion(ctx, dy, g.first, g.count, w, h, cfg, send - g.first));
+    TRY(shard_exchange(ctx, n, R, world, send, recv, blk, ma));
+    const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
+    return shard_finish(ctx, ma, n, g, w, h, cw, ch, chroma, cfg, dy - g.first * fl,
+                        chroma ? dcb - g.first * fc : nullptr, chroma ? dcr - g.first * fc : nullptr,
+                        doy - g.own_begin * fl, chroma ? docb - g.own_begin * fc : nullptr,
+                        chroma ? docr - g.own_begin * fc : nullptr, nullptr, nullptr, nullptr, records);
 }
 
 // ---- Stage II streaming ---------------------------------------------------

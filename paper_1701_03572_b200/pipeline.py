@@ -311,6 +311,94 @@ def stabilize_sharded(n: int, local_y, local_first: int, cfg: StabConfig, rank: 
     return oy, ob, orr, rec
 
 
+def shard_range_c(n: int, redetect_interval: int, world: int, rank: int) -> Shard:
+    """The library's partition (stabgpu_shard_range); equals shard_ranges()."""
+    first, own_b, own_e = C.c_int64(), C.c_int64(), C.c_int64()
+    count = C.c_int()
+    check(load().stabgpu_shard_range(n, redetect_interval, world, rank, C.byref(first), C.byref(count),
+                                     C.byref(own_b), C.byref(own_e)))
+    return Shard(rank, first.value, count.value, own_b.value, own_e.value)
+
+
+def init_comm(ctx, group=None) -> None:
+    """Gives the context an NCCL communicator over the ranks of a
+    torch.distributed group (rank 0 makes the unique id; the group broadcasts
+    the 128 bytes: plumbing only, the records themselves go device to device)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = np.zeros(128, np.uint8)
+    if rank == 0:
+        check(load().stabgpu_nccl_unique_id(_vp(uid)))
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(uid).to(dev)
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    uid = t.cpu().numpy()
+    check(load().stabgpu_comm_init(ctx.handle, _vp(uid), world, rank))
+
+
+def stabilize_sharded_host(ctx, n: int, y, cfg: StabConfig, cb=None, cr=None, out_y=None, out_cb=None,
+                           out_cr=None, records: bool = True):
+    """One rank of the sharded Stage I through the C ABI host-buffer entry
+    point (stabgpu_stabilize_sharded): y/cb/cr hold this rank's frames
+    first..first+count (host, ideally pinned), out_* receive its own frames.
+    The context's communicator (init_comm) sets world and rank; without one it
+    is world 1."""
+    _, h, w = y.shape
+    ch = cw = 0
+    if cb is not None:
+        _, ch, cw = cb.shape
+    rec = np.zeros(n, RECORD_DT) if records else None
+    c = cfg.c()
+    check(load().stabgpu_stabilize_sharded(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, w, h, cw, ch, C.byref(c),
+                                           _vp(out_y), _vp(out_cb), _vp(out_cr), _vp(rec)))
+    return rec
+
+
+def stabilize_sharded_device(ctx, n: int, y, cfg: StabConfig, cb=None, cr=None, out_y=None, out_cb=None,
+                             out_cr=None, records: bool = True):
+    """Device-resident variant (stabgpu_stabilize_sharded_device)."""
+    _, h, w = y.shape
+    ch = cw = 0
+    if cb is not None:
+        _, ch, cw = cb.shape
+    rec = np.zeros(n, RECORD_DT) if records else None
+    c = cfg.c()
+    check(load().stabgpu_stabilize_sharded_device(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, w, h, cw, ch,
+                                                  C.byref(c), _vp(out_y), _vp(out_cb), _vp(out_cr), _vp(rec)))
+    return rec
+
+
+def shard_motion(ctx, n: int, world: int, rank: int, y, cfg: StabConfig, cb=None, cr=None) -> np.ndarray:
+    """First half of stabgpu_stabilize_sharded (host-side exchange): uploads
+    the rank's frames (kept resident in ctx) and returns its count+1 motion
+    records."""
+    sh = shard_range_c(n, cfg.flow.redetect_interval, world, rank)
+    _, h, w = y.shape
+    ch = cw = 0
+    if cb is not None:
+        _, ch, cw = cb.shape
+    out = np.zeros(max(sh.count + 1, 1), MOTION_DT)
+    c = cfg.c()
+    check(load().stabgpu_shard_motion(ctx.handle, _vp(y), _vp(cb), _vp(cr), n, world, rank, w, h, cw, ch,
+                                      C.byref(c), _vp(out)))
+    return out
+
+
+def shard_compose(ctx, n: int, world: int, rank: int, motion_all: np.ndarray, cfg: StabConfig, w: int, h: int,
+                  cw: int = 0, ch: int = 0, out_y=None, out_cb=None, out_cr=None) -> np.ndarray:
+    """Second half: plan all n frames from the gathered records and compose
+    the rank's own frames from its resident ones."""
+    rec = np.zeros(n, RECORD_DT)
+    c = cfg.c()
+    m = np.ascontiguousarray(motion_all, MOTION_DT)
+    check(load().stabgpu_shard_compose(ctx.handle, _vp(m), n, world, rank, w, h, cw, ch, C.byref(c),
+                                       _vp(out_y), _vp(out_cb), _vp(out_cr), _vp(rec)))
+    return rec
+
+
 # ------------------------------------------------------------ Stage II -----
 class StreamStabilizer:
     """Stage II (one frame at a time): the reference's run_offline /

@@ -662,3 +662,74 @@ def test_streams_errors():
     bad.smooth_radius = 40
     with pytest.raises(stab.InvalidConfigError):
         pipeline.stabilize_streams(y, bad)
+
+
+@pytest.mark.parametrize("color", [False, True])
+def test_sharded_entry_points_equal_single(color):
+    """The C-ABI sharded Stage I: the host split (shard_motion -> host
+    all-gather -> shard_compose) for 2, 3, 4 and 11 ranks emulated in one
+    process (one context per rank, as one rank per GPU would have), the
+    one-call host entry point, and the device entry point over a 1-rank NCCL
+    communicator, all bitwise equal to the one-GPU run."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1701_03572_b200 import _lib
+
+    y, cb, cr = _data.video(frames=53, objects=1, color=True)
+    if not color:
+        cb = cr = None
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=100)
+    n, h, w = y.shape
+    ch, cw = (0, 0) if cb is None else cb.shape[1:]
+    ref_y, ref_b, ref_r, ref_rec = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    R = cfg.flow.redetect_interval
+    for world in (2, 3, 4, 11):
+        shards = [pipeline.shard_range_c(n, R, world, g) for g in range(world)]
+        assert shards == pipeline.shard_ranges(n, R, world)
+        ctxs = [_lib.Context(0) for _ in range(world)]
+        parts = []
+        for sh, ctx in zip(shards, ctxs):
+            sl = slice(sh.first, sh.first + sh.count + 1)
+            parts.append((sh, pipeline.shard_motion(ctx, n, world, sh.rank, y[sl], cfg,
+                                                    None if cb is None else cb[sl], None if cr is None else cr[sl])))
+        motion = pipeline.assemble_motion(n, parts)
+        out = [np.zeros_like(a) if a is not None else None for a in (y, cb, cr)]
+        for sh, ctx in zip(shards, ctxs):
+            a, b = sh.own_begin, sh.own_end
+            oy = np.zeros((max(b - a, 1), h, w), np.uint8)
+            ob = orr = None
+            if cb is not None:
+                ob, orr = (np.zeros((max(b - a, 1), ch, cw), np.uint8) for _ in range(2))
+            rec = pipeline.shard_compose(ctx, n, world, sh.rank, motion, cfg, w, h, cw, ch, oy, ob, orr)
+            assert rec.tobytes() == ref_rec.tobytes(), (world, sh.rank)
+            if b > a:
+                out[0][a:b] = oy[: b - a]
+                if cb is not None:
+                    out[1][a:b], out[2][a:b] = ob[: b - a], orr[: b - a]
+        for c in ctxs:
+            c.close()
+        assert np.array_equal(out[0], ref_y), world
+        if cb is not None:
+            assert np.array_equal(out[1], ref_b) and np.array_equal(out[2], ref_r)
+    # one-call entry points, world 1 (no communicator, then a 1-rank NCCL one)
+    ctx = _lib.Context(0)
+    oy, ob, orr = np.zeros_like(y), None if cb is None else np.zeros_like(cb), None if cr is None else np.zeros_like(cr)
+    rec = pipeline.stabilize_sharded_host(ctx, n, y, cfg, cb, cr, oy, ob, orr)
+    assert rec.tobytes() == ref_rec.tobytes() and np.array_equal(oy, ref_y)
+    uid = np.zeros(128, np.uint8)
+    _lib.check(_lib.load().stabgpu_nccl_unique_id(C.c_void_p(uid.ctypes.data)))
+    _lib.check(_lib.load().stabgpu_comm_init(ctx.handle, C.c_void_p(uid.ctypes.data), 1, 0))
+    oy2 = np.zeros_like(y)
+    rec2 = pipeline.stabilize_sharded_host(ctx, n, y, cfg, cb, cr, oy2, ob, orr)
+    assert rec2.tobytes() == ref_rec.tobytes() and np.array_equal(oy2, ref_y)
+    if cb is not None:
+        assert np.array_equal(ob, ref_b) and np.array_equal(orr, ref_r)
+    dev = [None if a is None else torch.from_numpy(a).cuda() for a in (y, cb, cr)]
+    outs = [None if a is None else torch.empty_like(a) for a in dev]
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    rec3 = pipeline.stabilize_sharded_device(ctx, n, dev[0], cfg, dev[1], dev[2], *outs)
+    torch.cuda.synchronize()
+    assert rec3.tobytes() == ref_rec.tobytes() and np.array_equal(outs[0].cpu().numpy(), ref_y)
+    ctx.close()

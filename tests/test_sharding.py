@@ -121,3 +121,11 @@ def test_gloo_world2_exchange():
     _, _, _, want = _oracle.reference().stabilize_sequence(y, cfg, threads=1)
     assert res[0] == res[1] == want.tobytes()
     assert (want["frame_kind"][1:] == _abi.FRAME_TRACKED).all()
+
+
+@pytest.mark.parametrize("R", [1, 5, 7])
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 11])
+@pytest.mark.parametrize("n", [2, 3, 11, 53, 1000])
+def test_library_partition_equals_python(n, R, world):
+    """stabgpu_shard_range (the C ABI's partition, host-only) == shard_ranges."""
+    assert [pipeline.shard_range_c(n, R, world, g) for g in range(world)] == pipeline.shard_ranges(n, R, world)
