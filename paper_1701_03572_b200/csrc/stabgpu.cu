@@ -1860,6 +1860,11 @@ struct stabgpu_stream {
     double4* cum = nullptr;
     FramePlan* plan = nullptr;
     PlanState* ps = nullptr;
+    // copy/compute overlap: input slot k is free once the compose of its
+    // frame ran (slot_free[k]); output slot k is downloadable once its frame
+    // is composed (out_done[k]); pinned error word of the selector scan
+    std::vector<cudaEvent_t> slot_free, out_done, in_done;
+    int* err_host = nullptr;
 };
 
 namespace {
@@ -1904,7 +1909,8 @@ int stream_grow(stabgpu_stream* s, long long need) {
     return STABGPU_OK;
 }
 
-// composes released frame i into output slot i % ocap and queues it
+// composes released frame i into output slot i % ocap and queues it; the
+// input slot is free and the output slot downloadable after it (events)
 int stream_release(stabgpu_stream* s, long long i) {
     cudaStream_t st = s->ctx->stream;
     const int r = s->cfg.smooth_radius;
@@ -1917,6 +1923,8 @@ int stream_release(stabgpu_stream* s, long long i) {
     PlaneBatch rb{s->chroma ? s->ring_cr + in * fc : nullptr, fc, s->cw, s->ch};
     launch_compose(yb, bb, rb, s->plan + i, 1, s->cfg.crop_ratio, s->out_y + o * fl,
                    s->chroma ? s->out_cb + o * fc : nullptr, s->chroma ? s->out_cr + o * fc : nullptr, st);
+    cudaEventRecord(s->slot_free[in], st);
+    cudaEventRecord(s->out_done[o], st);
     s->ctx->stats.launches += 2;
     s->ready.push_back(i);
     return check_launch("stream compose");
@@ -1995,6 +2003,16 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
         (rc = salloc(s, &s->fit_pre, 2 * kFitPreCtas)))
         return fail(rc);
     if ((rc = stream_grow(s, 256))) return fail(rc);
+    s->slot_free.resize(s->cap);
+    s->in_done.resize(s->cap);
+    s->out_done.resize(s->ocap);
+    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done})
+        for (auto& e : *v)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return fail(set_err(STABGPU_CUDA, "stream: event creation failed"));
+    if (cudaMallocHost((void**)&s->err_host, sizeof(int)) != cudaSuccess)
+        return fail(set_err(STABGPU_CUDA, "stream: pinned allocation failed"));
+    *s->err_host = 0;
     if ((rc = init_plan_state(ctx, cfg, &s->ps))) return fail(rc);
     // init_plan_state keeps its state in a context buffer: give the stream its own copy
     PlanState* own;
@@ -2024,11 +2042,18 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch;
     const size_t slot = (size_t)(f % s->cap);
     uint8_t* fy = s->ring_y + slot * fl;
-    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyHostToDevice, st));
+    // upload on the input copy stream once the slot's previous frame was
+    // composed; the compute stream waits for it.  The host buffers are read
+    // before push returns (the upload is waited for at the end), while the
+    // previous frames' compute and downloads keep running.
+    if (f >= s->cap) CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->slot_free[slot], 0));
+    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyHostToDevice, ctx->cin));
     if (s->chroma) {
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyHostToDevice, ctx->cin));
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyHostToDevice, ctx->cin));
     }
+    CUDA_TRY(cudaEventRecord(s->in_done[slot], ctx->cin));
+    CUDA_TRY(cudaStreamWaitEvent(st, s->in_done[slot], 0));
     // K1: the pyramid of the current frame, levels >= 1 into slot f & 1; no
     // copies: level 0 stays in the ring, and the tracker sees (previous,
     // current) through a pyramid view whose frame stride is the signed
@@ -2051,12 +2076,9 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         }
     }
     if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88) + detection (flow.cpp:303-308)
-        stabgpu_motion_record f0;
-        std::memset(&f0, 0, sizeof f0);
-        f0.frame_kind = STABGPU_FRAME_FIRST;
-        CUDA_TRY(cudaMemcpyAsync(s->motion, &f0, sizeof f0, cudaMemcpyHostToDevice, st));
+        static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
+        CUDA_TRY(cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st));
         launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
-        CUDA_TRY(cudaStreamSynchronize(st));  // f0 is a stack temporary
     } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
         LkStep k;
         std::memset(&k, 0, sizeof k);
@@ -2086,6 +2108,7 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     TRY(check_launch("stream push"));
     s->pushed = f + 1;
     TRY(stream_release_ready(s));
+    CUDA_TRY(cudaEventSynchronize(s->in_done[slot]));  // the caller's buffers are consumed
     if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
     return STABGPU_OK;
 }
@@ -2111,13 +2134,20 @@ int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* 
         s->ready.clear();
         s->ready_head = 0;
     }
+    // the download waits for this frame's compose only (frames pushed since
+    // keep computing on the compute stream)
     const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch, o = (size_t)(i % s->ocap);
-    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDeviceToHost, st));
-    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDeviceToHost, st));
-    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDeviceToHost, st));
-    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    TRY(plan_error(s->ctx, s->ps));
+    cudaStream_t co = s->ctx->cout;
+    (void)st;
+    CUDA_TRY(cudaStreamWaitEvent(co, s->out_done[o], 0));
+    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDeviceToHost, co));
+    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDeviceToHost, co));
+    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDeviceToHost, co));
+    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, co));
+    // the selector scan's error word (written before the frame was released)
+    CUDA_TRY(cudaMemcpyAsync(s->err_host, reinterpret_cast<int*>(s->ps + 1), sizeof(int), cudaMemcpyDeviceToHost, co));
+    CUDA_TRY(cudaStreamSynchronize(co));
+    if (*s->err_host) TRY(plan_error(s->ctx, s->ps));
     if (index) *index = i;
     return STABGPU_OK;
 }
@@ -2126,7 +2156,13 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
     if (!s) return STABGPU_OK;
     cudaSetDevice(s->ctx->device);
     cudaStreamSynchronize(s->ctx->stream);
+    cudaStreamSynchronize(s->ctx->cin);
+    cudaStreamSynchronize(s->ctx->cout);
     for (void* p : s->allocs) cudaFree(p);
+    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done})
+        for (auto e : *v)
+            if (e) cudaEventDestroy(e);
+    if (s->err_host) cudaFreeHost(s->err_host);
     delete s;
     return STABGPU_OK;
 }

@@ -469,6 +469,45 @@ def test_stream_equals_stage1(mode, ransac, smooth):
         assert grec.tobytes() == srec[i].tobytes(), i
 
 
+@pytest.mark.parametrize("name,frames", [("c1", 90), ("c3", 40)])
+def test_stream_equals_oracle_config(name, frames):
+    """Stage II against the CPU reference path directly (not through Stage
+    I): the first frames of a BASELINE config pushed one at a time, every
+    released frame and record compared with the reference's run_offline
+    semantics on the same frames (oracle/_ref when built, else the C
+    restatement); pixels bit-identical, parameters to 1e-9."""
+    from paper_1701_03572_b200.synth import CONFIGS, Video
+
+    from . import _parity
+
+    cfg = CONFIGS[name]
+    planes = Video(cfg.video).render(0, frames)
+    y = planes[0]
+    cb, cr = (planes[1], planes[2]) if len(planes) == 3 else (None, None)
+    ref = _oracle.reference() if _oracle.have_reference() else orc_checker()
+    kw = {"threads": 8} if ref.prefix == "ref_" else {}
+    oy, ob, orr, orec = ref.stabilize_sequence(y, cfg.stab, cb, cr, **kw)
+    h, w = y.shape[1:]
+    s = pipeline.StreamStabilizer(cfg.stab, w, h, 0 if cb is None else cb.shape[2], 0 if cb is None else cb.shape[1])
+    got = []
+    for k in range(frames):
+        got += s.push(y[k], None if cb is None else cb[k], None if cr is None else cr[k])
+    got += s.finish()
+    s.close()
+    assert [g[0] for g in got] == list(range(frames))
+    gy = np.stack([g[1] for g in got])
+    grec = np.stack([g[4] for g in got]).reshape(-1)
+    gp = [gy] + ([np.stack([g[2] for g in got]), np.stack([g[3] for g in got])] if cb is not None else [])
+    op = [oy] + ([ob, orr] if cb is not None else [])
+    summ = _parity.summarize(grec, orec, gp, op)
+    assert summ["ok"], summ
+    assert summ["max_delta_err"] <= 1e-9 and summ["max_pixel_diff"] == 0, summ
+
+
+def orc_checker():
+    return _oracle.oracle()
+
+
 def test_stream_gray_and_errors():
     y = _data.video(frames=14)[0]
     cfg = _data.small_cfg(smooth=3)

@@ -36,13 +36,21 @@ def pop_all(k):
 pop_all.n = 0
 lat = []
 nr = C.c_int()
+lag = "--lag" in sys.argv  # pop a push late: frame k+1 uploads while frame k computes and k-r downloads
 t0 = time.perf_counter()
+pending = 0
 for k in range(n):
     t1 = time.perf_counter()
     assert lib.stabgpu_stream_push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
                                    vp(pin[2], k) if col else None, C.byref(nr)) == 0
-    pop_all(nr.value)
+    if lag:
+        pop_all(pending)  # frames released by earlier pushes
+        pending = nr.value - pending
+    else:
+        pop_all(nr.value)
     lat.append(time.perf_counter() - t1)
+if lag:
+    pop_all(pending)
 assert lib.stabgpu_stream_finish(hs, C.byref(nr)) == 0
 pop_all(nr.value)
 dt = time.perf_counter() - t0
