@@ -384,6 +384,24 @@ int stabgpu_shard_compose(stabgpu_ctx* ctx, const stabgpu_motion_record* host_al
                           uint8_t* host_out_y, uint8_t* host_out_cb, uint8_t* host_out_cr,
                           stabgpu_frame_record* records);
 
+/* ---- device-resident Tracker (flow.hpp:56-82, flow.cpp:297-337) -------
+ * Tracker::advance with the previous pyramid, the carried points and the
+ * re-detect cadence kept on the device: advance uploads one frame, builds
+ * its pyramid, tracks forward + weeds backward, re-detects every
+ * redetect_interval frames and returns the TrackSet (n pairs of prev / cur
+ * points, each host array holding 2 * max_corners doubles) and the kind
+ * (STABGPU_FRAME_FIRST / SKIPPED when n < min_tracks / TRACKED); n_active
+ * (optional) = active_point_count() after the call.  Errors as the reference
+ * (SequencingError on a non-increasing index). */
+typedef struct stabgpu_tracker stabgpu_tracker;
+int stabgpu_tracker_create(stabgpu_ctx* ctx, const stabgpu_flow_cfg* flow, const stabgpu_detect_cfg* detect, int w,
+                           int h, stabgpu_tracker** out);
+int stabgpu_tracker_advance(stabgpu_tracker* t, const uint8_t* host_frame, int64_t index, int* kind,
+                            double* host_prev_xy, double* host_cur_xy, int* n_out, int* n_active);
+/* active_point_count() (flow.hpp:69) */
+int stabgpu_tracker_points(stabgpu_tracker* t, int* n_out);
+int stabgpu_tracker_destroy(stabgpu_tracker* t);
+
 /* ---- Stage II: streaming (one frame at a time) ------------------------
  * Replaces run_streaming (pipeline.hpp:72-76 / pipeline.cpp:237-365) and the
  * MotionStage -> CompensationPlanner -> compose loop of run_offline

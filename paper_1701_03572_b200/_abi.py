@@ -131,6 +131,10 @@ PROTOTYPES = {
     "stabgpu_stabilize_sharded_device": (I, [V, V, V, V, C.c_int64, I, I, I, I, P(Config), V, V, V, V]),
     "stabgpu_shard_motion": (I, [V, V, V, V, C.c_int64, I, I, I, I, I, I, P(Config), V]),
     "stabgpu_shard_compose": (I, [V, V, C.c_int64, I, I, I, I, I, I, P(Config), V, V, V, V]),
+    "stabgpu_tracker_create": (I, [V, P(FlowCfg), P(DetectCfg), I, I, P(V)]),
+    "stabgpu_tracker_advance": (I, [V, V, C.c_int64, c_ip, V, V, c_ip, c_ip]),
+    "stabgpu_tracker_points": (I, [V, c_ip]),
+    "stabgpu_tracker_destroy": (I, [V]),
     "stabgpu_stream_create": (I, [V, P(Config), I, I, I, I, P(V)]),
     "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
     "stabgpu_stream_finish": (I, [V, c_ip]),

@@ -2168,6 +2168,204 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
 }
 
 
+}  // extern "C"
+
+// ---- device-resident Tracker (flow.hpp:56-82) -------------------------------
+// Tracker::advance with its state on the device: the previous frame's
+// pyramid (two slots, level 0 included), the carried points and the cadence
+// counter.  One call uploads the new frame, builds its pyramid, tracks the
+// points forward and weeds them backward (the Stage II LK step), compacts the
+// TrackSet and re-detects every redetect_interval frames; only the TrackSet
+// comes back.  The reference's frame-by-frame callers (MotionStage, the
+// acceptance harness) keep their loop; the pyramids never cross PCIe.
+struct stabgpu_tracker {
+    stabgpu_ctx* ctx = nullptr;
+    stabgpu_flow_cfg flow{};
+    stabgpu_detect_cfg detect{};
+    int w = 0, h = 0;
+    long long last_index = -1, frames = 0;
+    int since_detect = 0;
+    long long detections = 0;
+    std::vector<void*> allocs;
+    uint8_t* frame[2] = {nullptr, nullptr};  // level 0 of slots 0 / 1
+    DevPyramid P{};                          // levels >= 1 of both slots (slot stride = level size)
+    stabgpu_roi roi{};
+    DetectScratch ds{};
+    double2 *pts = nullptr, *nxt = nullptr, *fwd = nullptr, *trk_prev = nullptr, *trk_cur = nullptr;
+    int *npts = nullptr, *nnxt = nullptr, *trk_n = nullptr;
+    double* score = nullptr;
+    uint8_t* keep = nullptr;
+    unsigned* work = nullptr;
+    int* host_n = nullptr;  // pinned: TrackSet size, active points
+};
+
+namespace {
+template <typename T>
+int talloc(stabgpu_tracker* t, T** p, size_t count) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, count * sizeof(T) + 256) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(STABGPU_CUDA, "tracker: device allocation of %zu bytes failed", count * sizeof(T));
+    }
+    t->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return STABGPU_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int stabgpu_tracker_create(stabgpu_ctx* ctx, const stabgpu_flow_cfg* flow, const stabgpu_detect_cfg* detect, int w,
+                           int h, stabgpu_tracker** out) {
+    *out = nullptr;
+    if (!ctx) return set_err(STABGPU_INVALID_INPUT, "tracker: null context");
+    TRY(validate_flow(*flow));
+    TRY(validate_detect(*detect));
+    TRY(validate_frame(w, h));
+    if (flow->window_radius > STABGPU_MAX_RADIUS)
+        return set_err(STABGPU_INVALID_CONFIG, "window_radius above 31 is not supported");
+    cudaSetDevice(ctx->device);
+    auto* t = new stabgpu_tracker();
+    t->ctx = ctx;
+    t->flow = *flow;
+    t->detect = *detect;
+    t->w = w;
+    t->h = h;
+    int rc = STABGPU_OK;
+    auto fail = [&](int code) {
+        stabgpu_tracker_destroy(t);
+        return code;
+    };
+    const int maxc = detect->max_corners;
+    const size_t fl = (size_t)w * h;
+    if ((rc = talloc(t, &t->frame[0], 2 * fl))) return fail(rc);
+    t->frame[1] = t->frame[0] + fl;
+    t->P.levels = level_dims(w, h, flow->max_levels, t->P.w, t->P.h);
+    t->P.stride[0] = fl;
+    for (int l = 1; l < t->P.levels; ++l) {
+        uint8_t* lv;
+        t->P.stride[l] = (size_t)t->P.w[l] * t->P.h[l];
+        if ((rc = talloc(t, &lv, 2 * t->P.stride[l]))) return fail(rc);
+        t->P.lvl[l] = lv;
+    }
+    if ((rc = roi_of(w, h, detect->roi_margin, &t->roi))) return fail(rc);
+    const size_t cap = (size_t)(t->roi.x1 - t->roi.x0) * (t->roi.y1 - t->roi.y0);
+    DetectScratch& d = t->ds;
+    d.cap = cap;
+    if ((rc = talloc(t, &d.maxbits, 1)) || (rc = talloc(t, &d.count, 1)) || (rc = talloc(t, &d.hist, kRespBins)) ||
+        (rc = talloc(t, &d.cand_key, cap)) || (rc = talloc(t, &d.cand_idx, cap)) ||
+        (rc = talloc(t, &d.sort_key, cap)) || (rc = talloc(t, &d.sort_idx, cap)) || (rc = talloc(t, &d.lo, 1)) ||
+        (rc = talloc(t, &d.flags, 1)) || (rc = talloc(t, &d.mlo, 1)))
+        return fail(rc);
+    if ((rc = talloc(t, &t->pts, maxc)) || (rc = talloc(t, &t->nxt, maxc)) || (rc = talloc(t, &t->fwd, maxc)) ||
+        (rc = talloc(t, &t->trk_prev, maxc)) || (rc = talloc(t, &t->trk_cur, maxc)) || (rc = talloc(t, &t->npts, 1)) ||
+        (rc = talloc(t, &t->nnxt, 1)) || (rc = talloc(t, &t->trk_n, 1)) || (rc = talloc(t, &t->score, maxc)) ||
+        (rc = talloc(t, &t->keep, maxc)) || (rc = talloc(t, &t->work, 1)))
+        return fail(rc);
+    if (cudaMallocHost((void**)&t->host_n, 2 * sizeof(int)) != cudaSuccess)
+        return fail(set_err(STABGPU_CUDA, "tracker: pinned allocation failed"));
+    *out = t;
+    return STABGPU_OK;
+}
+
+int stabgpu_tracker_advance(stabgpu_tracker* t, const uint8_t* host_frame, int64_t index, int* kind,
+                            double* prev_xy, double* cur_xy, int* n_out, int* n_active) {
+    if (!t) return set_err(STABGPU_INVALID_INPUT, "tracker: null handle");
+    *n_out = 0;
+    if (index <= t->last_index) return set_err(STABGPU_SEQUENCING, "frame index must be strictly increasing");
+    stabgpu_ctx* ctx = t->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->stream;
+    t->last_index = index;
+    const long long f = t->frames;
+    const int cs = (int)(f & 1), ps = cs ^ 1;
+    const size_t fl = (size_t)t->w * t->h;
+    uint8_t* fy = t->frame[cs];
+    CUDA_TRY(cudaMemcpyAsync(fy, host_frame, fl, cudaMemcpyHostToDevice, st));
+    DevPyramid& P = t->P;
+    for (int l = 1; l < P.levels; ++l)  // build_pyramid (image_ops.cpp:62-77) into slot cs
+        launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
+                             P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, st);
+    ctx->stats.launches += P.levels - 1;
+    PlaneBatch cur{fy, fl, t->w, t->h};
+    const int maxc = t->detect.max_corners;
+    int n = 0;
+    if (f == 0) {  // first frame: detect_fresh (flow.cpp:303-308)
+        launch_detect(cur, 1, t->detect, t->roi, t->ds, t->pts, t->score, t->npts, st);
+        t->since_detect = 0;
+        ++t->detections;
+        *kind = STABGPU_FRAME_FIRST;
+    } else {  // track_lk forward + weed_tracks (flow.cpp:316-323) as one LK step
+        DevPyramid V = P;  // frame 0 = previous slot, frame 1 = current slot
+        V.lvl[0] = t->frame[ps];
+        V.stride[0] = (size_t)(fy - t->frame[ps]);
+        for (int l = 1; l < P.levels; ++l) {
+            V.lvl[l] = P.lvl[l] + ps * P.stride[l];
+            V.stride[l] = (size_t)((ptrdiff_t)(cs - ps) * (ptrdiff_t)P.stride[l]);
+        }
+        LkStep k;
+        std::memset(&k, 0, sizeof k);
+        k.pyr = V;
+        k.frame0 = 0;
+        k.seg_len = t->flow.redetect_interval;
+        k.t = 1;
+        k.nseg = 1;
+        k.max_pts = maxc;
+        k.pts = t->pts;
+        k.npts = t->npts;
+        k.fwd = t->fwd;
+        k.keep = t->keep;
+        k.nframes = 2;
+        k.mode = 1;
+        k.work = t->work;
+        launch_lk(k, t->flow, st);
+        launch_compact(k, t->nxt, t->nnxt, t->trk_prev, t->trk_cur, t->trk_n, 1, st);
+        std::swap(t->pts, t->nxt);  // points_ = tracks.cur_points (flow.cpp:326)
+        std::swap(t->npts, t->nnxt);
+        ctx->stats.launches += 2;
+        if (++t->since_detect >= t->flow.redetect_interval) {  // flow.cpp:327-330
+            launch_detect(cur, 1, t->detect, t->roi, t->ds, t->pts, t->score, t->npts, st);
+            t->since_detect = 0;
+            ++t->detections;
+        }
+        // the whole point arrays come back with the counts (one round trip;
+        // max_corners pairs are a few KB)
+        CUDA_TRY(cudaMemcpyAsync(t->host_n, t->trk_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(t->host_n + 1, t->npts, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(prev_xy, t->trk_prev, sizeof(double2) * maxc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(cur_xy, t->trk_cur, sizeof(double2) * maxc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        n = t->host_n[0];
+        *kind = n < t->flow.min_tracks ? STABGPU_FRAME_SKIPPED : STABGPU_FRAME_TRACKED;
+    }
+    if (f == 0) CUDA_TRY(cudaMemcpyAsync(t->host_n + 1, t->npts, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TRY(check_launch("tracker"));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    t->frames = f + 1;
+    *n_out = n;
+    if (n_active) *n_active = t->host_n[1];
+    return STABGPU_OK;
+}
+
+int stabgpu_tracker_points(stabgpu_tracker* t, int* n_out) {
+    if (!t) return set_err(STABGPU_INVALID_INPUT, "tracker: null handle");
+    cudaSetDevice(t->ctx->device);
+    CUDA_TRY(cudaMemcpyAsync(t->host_n, t->npts, sizeof(int), cudaMemcpyDeviceToHost, t->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+    *n_out = t->frames ? *t->host_n : 0;
+    return STABGPU_OK;
+}
+
+int stabgpu_tracker_destroy(stabgpu_tracker* t) {
+    if (!t) return STABGPU_OK;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    for (void* p : t->allocs) cudaFree(p);
+    if (t->host_n) cudaFreeHost(t->host_n);
+    delete t;
+    return STABGPU_OK;
+}
+
 // ---- colour I/O + evaluation -----------------------------------------------
 int stabgpu_rgb_to_ycbcr(stabgpu_ctx* ctx, const uint8_t* rgb, int n, int w, int h, uint8_t* y, uint8_t* cb,
                          uint8_t* cr) {

@@ -17,7 +17,9 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../include/stabgpu.h"
@@ -294,10 +296,40 @@ TrackSet weed_tracks(const Pyramid& prev, const Pyramid& cur, std::span<const Po
     return set;
 }
 
-// Tracker: re-detect cadence and point carrying (flow.cpp:282-337 semantics).
+}  // namespace stab
+
+namespace {
+// Device state of each Tracker (flow.hpp:74-82 fixes its private members, so
+// it lives beside them, keyed by the object's address): the previous
+// pyramid and the carried points stay on the B200 between advance() calls
+// (stabgpu_tracker_*); the private members keep the host bookkeeping
+// (last_index_, since_detect_, detections_run_, the size of points_).
+struct DevTracker {
+    stabgpu_ctx* c = nullptr;  // its own context: outlives the creating thread's context
+    stabgpu_tracker* t = nullptr;
+    int w = 0, h = 0;
+    ~DevTracker() {
+        if (t) stabgpu_tracker_destroy(t);
+        if (c) stabgpu_destroy(c);
+    }
+};
+std::mutex g_trk_mu;
+std::unordered_map<const stab::Tracker*, std::unique_ptr<DevTracker>>& trackers() {
+    static auto* m = new std::unordered_map<const stab::Tracker*, std::unique_ptr<DevTracker>>();  // outlives statics
+    return *m;
+}
+}  // namespace
+
+namespace stab {
+
+// Tracker: re-detect cadence and point carrying (flow.cpp:282-337 semantics),
+// with the pyramids and points on the device.
 Tracker::Tracker(FlowConfig flow_cfg, DetectConfig detect_cfg) : flow_(flow_cfg), detect_(detect_cfg) {
     validate(flow_);
     validate(detect_);
+    if (flow_.window_radius > 31) throw InvalidConfigError("window_radius above 31 is not supported");
+    std::lock_guard<std::mutex> g(g_trk_mu);
+    trackers().erase(this);  // a new object at a recycled address starts fresh
 }
 
 void Tracker::detect_fresh(const GrayFrame& frame) {
@@ -310,29 +342,50 @@ void Tracker::detect_fresh(const GrayFrame& frame) {
 Tracker::Advance Tracker::advance(const GrayFrame& cur) {
     validate(cur);
     if (cur.index <= last_index_) throw SequencingError("frame index must be strictly increasing");
-    last_index_ = cur.index;
-    Pyramid pyr = build_pyramid(cur, flow_.max_levels);
-    if (!prev_) {
-        detect_fresh(cur);
-        prev_ = std::move(pyr);
-        return {Advance::Kind::FirstFrame, {}};
+    DevTracker* dt;
+    {
+        std::lock_guard<std::mutex> g(g_trk_mu);
+        auto& slot = trackers()[this];
+        if (!slot) {
+            if (prev_) throw Error("stabgpu: a copied or moved Tracker cannot continue a sequence (device state stays with the original)");
+            slot = std::make_unique<DevTracker>();
+        }
+        dt = slot.get();
     }
+    if (!dt->t) {
+        const stabgpu_flow_cfg fc = to_c(flow_);
+        const stabgpu_detect_cfg dc = to_c(detect_);
+        if (!dt->c) check(stabgpu_create(0, &dt->c));
+        check(stabgpu_tracker_create(dt->c, &fc, &dc, cur.width, cur.height, &dt->t));
+        dt->w = cur.width;
+        dt->h = cur.height;
+    } else if (cur.width != dt->w || cur.height != dt->h) {
+        throw InvalidInputError("pyramid levels differ in size");  // check_pyramids (flow.cpp:229-239)
+    }
+    last_index_ = cur.index;
+    std::vector<double> p(2 * static_cast<size_t>(detect_.max_corners)), q(p.size());
+    int kind = 0, n = 0, active = 0;
+    check(stabgpu_tracker_advance(dt->t, cur.pixels.data(), cur.index, &kind, p.data(), q.data(), &n, &active));
+    const bool first = !prev_;
+    if (first) {
+        ++detections_run_;
+        since_detect_ = 0;
+        prev_ = Pyramid{};  // marks "a previous frame exists"; its levels live on the device
+    } else if (++since_detect_ >= flow_.redetect_interval) {
+        since_detect_ = 0;
+        ++detections_run_;
+    }
+    points_.assign(static_cast<size_t>(active), Point2{});  // active_point_count(); positions on the device
+    if (first) return {Advance::Kind::FirstFrame, {}};
     TrackSet tracks;
     tracks.frame_index = cur.index;
-    if (!points_.empty()) {
-        const std::vector<TrackedPoint> fwd = track_lk(*prev_, pyr, points_, flow_);
-        std::vector<Point2> from, to;
-        for (size_t i = 0; i < fwd.size(); ++i)
-            if (fwd[i].ok) {
-                from.push_back(points_[i]);
-                to.push_back(fwd[i].position);
-            }
-        tracks = weed_tracks(*prev_, pyr, from, to, flow_);
+    tracks.prev_points.resize(n);
+    tracks.cur_points.resize(n);
+    for (int i = 0; i < n; ++i) {
+        tracks.prev_points[i] = Point2{p[2 * i], p[2 * i + 1]};
+        tracks.cur_points[i] = Point2{q[2 * i], q[2 * i + 1]};
     }
-    points_ = tracks.cur_points;
-    if (++since_detect_ >= flow_.redetect_interval) detect_fresh(cur);
-    prev_ = std::move(pyr);
-    if (tracks.size() < static_cast<size_t>(flow_.min_tracks)) return {Advance::Kind::Skipped, {}};
+    if (kind == STABGPU_FRAME_SKIPPED) return {Advance::Kind::Skipped, {}};
     return {Advance::Kind::Tracked, std::move(tracks)};
 }
 

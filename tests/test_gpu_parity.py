@@ -772,3 +772,53 @@ def test_sharded_entry_points_equal_single(color):
     torch.cuda.synchronize()
     assert rec3.tobytes() == ref_rec.tobytes() and np.array_equal(outs[0].cpu().numpy(), ref_y)
     ctx.close()
+
+
+def test_device_tracker_matches_reference_tracker(orc):
+    """stabgpu_tracker_* (Tracker::advance with device-resident state, the
+    drop-in's Tracker) against the reference Tracker's semantics restated
+    with the oracle's stage functions (flow.cpp:297-337): same kinds, same
+    TrackSets (positions to 1e-9 px), same active point counts."""
+    import ctypes as C
+
+    from paper_1701_03572_b200 import _lib
+
+    y = _data.video(320, 240, frames=23, jit_t=3.0, tex=512, blobs=200)[0]
+    fc, dc = FlowConfig(max_levels=3), DetectConfig(max_corners=80, min_distance=6.0)
+    lib = _lib.load()
+    ctx = _lib.Context(0)
+    h = C.c_void_p()
+    f_c, d_c = fc.c(), dc.c()
+    _lib.check(lib.stabgpu_tracker_create(ctx.handle, C.byref(f_c), C.byref(d_c), 320, 240, C.byref(h)))
+    pts, prev_pyr = None, None
+    since = 0
+    for i in range(len(y)):
+        p = np.zeros((dc.max_corners, 2))
+        q = np.zeros((dc.max_corners, 2))
+        kind, n, act = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(lib.stabgpu_tracker_advance(h, C.c_void_p(np.ascontiguousarray(y[i]).ctypes.data), i, C.byref(kind),
+                                               C.c_void_p(p.ctypes.data), C.c_void_p(q.ctypes.data), C.byref(n),
+                                               C.byref(act)))
+        pyr = orc.build_pyramid(y[i], fc.max_levels)[0]
+        if prev_pyr is None:
+            pts, _ = orc.detect_corners(y[i], dc)
+            assert kind.value == _abi.FRAME_FIRST and act.value == len(pts)
+        else:
+            fwd, ok = orc.track_lk(prev_pyr, pyr, pts, fc)
+            kp, kc = orc.weed_tracks(prev_pyr, pyr, pts[ok], fwd[ok], fc)
+            assert n.value == len(kp), i
+            assert np.abs(p[: n.value] - kp).max(initial=0) <= 1e-9 and np.abs(q[: n.value] - kc).max(initial=0) <= 1e-9
+            want = _abi.FRAME_SKIPPED if len(kp) < fc.min_tracks else _abi.FRAME_TRACKED
+            assert kind.value == want
+            pts = kc
+            since += 1
+            if since >= fc.redetect_interval:
+                pts, _ = orc.detect_corners(y[i], dc)
+                since = 0
+            assert act.value == len(pts), i
+        prev_pyr = pyr
+    with pytest.raises(stab.SequencingError):
+        _lib.check(lib.stabgpu_tracker_advance(h, C.c_void_p(np.ascontiguousarray(y[0]).ctypes.data), 3, C.byref(kind),
+                                               C.c_void_p(p.ctypes.data), C.c_void_p(q.ctypes.data), C.byref(n), None))
+    lib.stabgpu_tracker_destroy(h)
+    ctx.close()
