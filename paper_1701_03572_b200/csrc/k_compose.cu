@@ -996,85 +996,184 @@ __device__ __forceinline__ void stg_u16(uint8_t* p, uint32_t v) {
     __stcs(reinterpret_cast<unsigned short*>(p), (unsigned short)v);
 }
 
-// ---- lean row loops of interior tiles -------------------------------------
-// An interior tile (tile_prep_kernel: pad0 bit 0 luma, bit 1 chroma) has every
-// sample's 2x2 taps inside the frame and inside the staged TMA box, with the
-// integer parts in [1, w-3] x [1, h-3]: by the continuity argument above
-// (inner32) no coordinate decision is needed, only the blended value's .5-tie
-// guard.  Lane l owns the adjacent columns 2l and 2l+1, so its two results
-// are adjacent bytes (one 16-bit store) and the packed-fp32 blend works on
-// the pair.  Columns past the tile's width re-sample its last column (in the
-// box) and are not stored.
-__device__ __forceinline__ int w_rows_lean(const uint8_t* box, int ob1, const long long* __restrict__ rxf,
-                                           const long long* __restrict__ ryf, uint32_t wsm, int nu, int nv, int u0,
-                                           long long cf, long long snf, long long RSX, long long RSY, unsigned* q) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c0 = 2 * lane, c1 = c0 + 1;
-    const bool v0 = c0 < nu, v1 = c1 < nu;
-    int qn = 0;
-    uint32_t row = wsm + warp * WTW + c0;
-    const int r0 = min(warp, nv - 1);
-    const long long ua = (long long)(u0 + min(c0, nu - 1)), ub = (long long)(u0 + min(c1, nu - 1));
-    long long XA = to32(__ldg(rxf + r0) + ua * cf), YA = to32(__ldg(ryf + r0) - ua * snf);
-    long long XB = to32(__ldg(rxf + r0) + ub * cf), YB = to32(__ldg(ryf + r0) - ub * snf);
-    const long long rsx = RSX >> 16, rsy = RSY >> 16;
-    for (int r = warp; r < nv; r += NW, row += NW * WTW, XA += rsx, YA += rsy, XB += rsx, YB += rsy) {
-        bool b0, b1;
-        const uint32_t pr = blend2_bad(fetch4i(box, BW, ob1, XA, YA, true), fetch4i(box, BW, ob1, XB, YB, true),
-                                       frac2(XA, XB), frac2(YA, YB), b0, b1);
-        b0 = b0 && v0;
-        b1 = b1 && v1;
-        if (v1) sts_u16(row, pr);
-        else if (v0) sts_u8(row, pr & 0xFF);
-        if (__any_sync(0xFFFFFFFFu, b0 || b1)) {
-            const unsigned it = ((unsigned)r << 8) | (unsigned)c0;
-            wq_push(q, qn, b0, it);
-            wq_push(q, qn, b1, it + 1);
-        }
-    }
-    return qn;
+// ---- lean row loops, v2 (interior tiles) ----------------------------------
+// Same exactness argument as w_rows_lean / chroma_rows_lean; fewer issued
+// instructions per sample:
+//  * the 32.32 coordinates are taken relative to the staged box origin once
+//    per tile (hi word = tap column / row inside the box), so a tap address
+//    is one IMAD and the four taps are immediate offsets;
+//  * the lane's second column is its first plus one column step (one 64-bit
+//    add; lanes past the tile width repeat their first column);
+//  * both fractions of a coordinate pair come from one FADD2;
+//  * the two rounded bytes are packed with one PRMT and stored unconditionally
+//    (W-tile columns past nu are never read; output widths of the TMA path are
+//    multiples of 16, so a lane's two columns are valid together);
+//  * undecided pixels set one bit per row in a lane-local mask (<= 17 rows per
+//    warp and tile) instead of a warp vote per row; the lane recomputes its
+//    flagged rows with the exact reference path after the loop (divergent,
+//    about one warp row in sixty).
+// Coordinate error as before: <= 2^-32 per conversion / step, < 20 steps per
+// tile: < 5e-9 px.
+__device__ __forceinline__ float2 frac2p(uint32_t a, uint32_t b) {
+    return __fadd2_rn(make_float2(__uint_as_float(0x3F800000u | (a >> 9)), __uint_as_float(0x3F800000u | (b >> 9))),
+                      make_float2(-0.99999994f, -0.99999994f));
 }
 
-__device__ __forceinline__ int chroma_rows_lean(const uint8_t* s1, const uint8_t* s2, int ob1,
-                                                const long long* __restrict__ pxf, const long long* __restrict__ pyf,
-                                                uint8_t* ob, uint8_t* orr, int cw, int nx, int ny, int X0,
-                                                long long kxx, long long kyx, long long RSX, long long RSY,
-                                                unsigned* q) {
+// blend2_bad with the two bytes packed by one PRMT (low 16 bits = p | q << 8)
+__device__ __forceinline__ uint32_t blend2p(const Q4& p, const Q4& q, float2 fx, float2 fy, bool& bad) {
+    const float2 fa = make_float2(b256(p.a), b256(q.a)), fb = make_float2(b256(p.b), b256(q.b));
+    const float2 fc = make_float2(b256(p.c), b256(q.c)), fd = make_float2(b256(p.d), b256(q.d));
+    const float2 top = __ffma2_rn(fx, sub2(fb, fa), fa);
+    const float2 bot = __ffma2_rn(fx, sub2(fd, fc), fc);
+    const float2 v = __ffma2_rn(fy, sub2(bot, top), top);
+    const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
+    const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
+    bad = fmaxf(fabsf(dv.x), fabsf(dv.y)) > 0.5f - VGUARD;
+    return __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x0040);
+}
+
+__device__ __forceinline__ Q4 taps(const uint8_t* p) { return Q4{p[0], p[1], p[BW], p[BW + 1]}; }
+
+__device__ __forceinline__ const uint8_t* tap_ptr(const uint8_t* box, long long X, long long Y) {
+    return box + hi32(Y) * BW + hi32(X);
+}
+
+// W rows of an interior tile into wt (lane: columns 2l, 2l+1)
+__device__ __forceinline__ void w_rows_lean2(const uint8_t* box, int lbx, int lby, const long long* __restrict__ rxf,
+                                             const long long* __restrict__ ryf, uint8_t* wt, int nu, int nv, int u0,
+                                             int v0, long long cf, long long snf, const FramePlan* __restrict__ plan,
+                                             int f, int w, int h) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c0 = 2 * lane, c1 = c0 + 1;
-    const bool v0 = c0 < nx, v1 = c1 < nx;
-    int qn = 0;
+    const int c0 = 2 * lane;
+    const int r0 = min(warp, nv - 1);
+    const long long ua = (long long)(u0 + min(c0, nu - 1));
+    long long XA = ((__ldg(rxf + r0) + ua * cf) >> 16) - ((long long)lbx << 32);
+    long long YA = ((__ldg(ryf + r0) - ua * snf) >> 16) - ((long long)lby << 32);
+    const bool vA = c0 < nu, vB = c0 + 1 < nu;
+    const long long DX = vB ? (cf >> 16) : 0, DY = vB ? -(snf >> 16) : 0;
+    const long long RX = ((long long)NW * snf) >> 16, RY = ((long long)NW * cf) >> 16;
+    uint8_t* wr = wt + warp * WTW + c0;
+    uint32_t bad = 0, bit = 1;
+#pragma unroll 2
+    for (int r = warp; r < nv; r += NW, wr += NW * WTW, bit <<= 1, XA += RX, YA += RY) {
+        const long long XB = XA + DX, YB = YA + DY;
+        bool b;
+        const uint32_t v = blend2p(taps(tap_ptr(box, XA, YA)), taps(tap_ptr(box, XB, YB)),
+                                   frac2p((uint32_t)XA, (uint32_t)XB), frac2p((uint32_t)YA, (uint32_t)YB), b);
+        *reinterpret_cast<uint16_t*>(wr) = (uint16_t)v;
+        if (b) bad |= bit;
+    }
+    if (!vA) bad = 0;
+    for (; bad; bad &= bad - 1) {  // this lane's undecided rows (both columns recomputed)
+        const int r = warp + NW * (__ffs(bad) - 1);
+        wt[r * WTW + c0] = (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0, v0 + r);
+        if (vB) wt[r * WTW + c0 + 1] = (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0 + 1, v0 + r);
+    }
+}
+
+// 4:4:4 chroma rows of an interior tile straight to the output planes; the
+// Cr box follows the Cb box (one immediate offset)
+__device__ __forceinline__ void chroma_rows_lean2(const uint8_t* s1, int cbx, int cby, const long long* __restrict__ pxf,
+                                                  const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int cw,
+                                                  int ch, int nx, int ny, int X0, int Y0, long long kxx, long long kyx,
+                                                  long long kxy, long long kyy, const FramePlan* __restrict__ plan, int f,
+                                                  CropGeom g, int w, int h) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = 2 * lane;
+    const int r0 = min(warp, ny - 1);
+    const long long xa = (long long)(X0 + min(c0, nx - 1));
+    long long XA = ((__ldg(pxf + r0) + xa * kxx) >> 16) - ((long long)cbx << 32);
+    long long YA = ((__ldg(pyf + r0) + xa * kyx) >> 16) - ((long long)cby << 32);
+    const bool vA = c0 < nx, vB = c0 + 1 < nx;
+    const long long DX = vB ? (kxx >> 16) : 0, DY = vB ? (kyx >> 16) : 0;
+    const long long RX = ((long long)NW * kxy) >> 16, RY = ((long long)NW * kyy) >> 16;
     const size_t step = (size_t)NW * cw;
     uint8_t* pb = ob + (size_t)warp * cw + c0;
-    uint8_t* pr = orr + (size_t)warp * cw + c0;
-    const int r0 = min(warp, ny - 1);
-    const long long xa = (long long)(X0 + min(c0, nx - 1)), xb = (long long)(X0 + min(c1, nx - 1));
-    long long XA = to32(__ldg(pxf + r0) + xa * kxx), YA = to32(__ldg(pyf + r0) + xa * kyx);
-    long long XB = to32(__ldg(pxf + r0) + xb * kxx), YB = to32(__ldg(pyf + r0) + xb * kyx);
-    const long long rsx = RSX >> 16, rsy = RSY >> 16;
-    for (int r = warp; r < ny; r += NW, pb += step, pr += step, XA += rsx, YA += rsy, XB += rsx, YB += rsy) {
-        const float2 fx = frac2(XA, XB), fy = frac2(YA, YB);
-        bool e0, e1, e2, e3;
-        // one packed blend per plane: (pixel 2l, pixel 2l+1) share the pipe
-        const uint32_t vb = blend2_bad(fetch4i(s1, BW, ob1, XA, YA, true), fetch4i(s1, BW, ob1, XB, YB, true), fx,
-                                       fy, e0, e1);
-        const uint32_t vr = blend2_bad(fetch4i(s2, BW, ob1, XA, YA, true), fetch4i(s2, BW, ob1, XB, YB, true), fx,
-                                       fy, e2, e3);
-        const bool b0 = v0 && (e0 || e2), b1 = v1 && (e1 || e3);
-        if (v1) {
+    const ptrdiff_t dr = orr - ob;
+    uint32_t bad = 0, bit = 1;
+#pragma unroll 2
+    for (int r = warp; r < ny; r += NW, pb += step, bit <<= 1, XA += RX, YA += RY) {
+        const long long XB = XA + DX, YB = YA + DY;
+        const float2 fx = frac2p((uint32_t)XA, (uint32_t)XB), fy = frac2p((uint32_t)YA, (uint32_t)YB);
+        const uint8_t* pa = tap_ptr(s1, XA, YA);
+        const uint8_t* pq = tap_ptr(s1, XB, YB);
+        bool e1, e2;
+        const uint32_t vb = blend2p(taps(pa), taps(pq), fx, fy, e1);
+        const uint32_t vr = blend2p(taps(pa + BH * BW), taps(pq + BH * BW), fx, fy, e2);
+        if (vA) {
             stg_u16(pb, vb);
-            stg_u16(pr, vr);
-        } else if (v0) {
-            stg_u8(pb, vb & 0xFF);
-            stg_u8(pr, vr & 0xFF);
+            stg_u16(pb + dr, vr);
         }
-        if (__any_sync(0xFFFFFFFFu, b0 || b1)) {
-            const unsigned it = ((unsigned)r << 8) | (unsigned)c0;
-            wq_push(q, qn, b0, it);
-            wq_push(q, qn, b1, it + 1);
+        if (e1 | e2) bad |= bit;
+    }
+    if (!vA) bad = 0;
+    for (; bad; bad &= bad - 1) {
+        const int r = warp + NW * (__ffs(bad) - 1);
+        for (int j = 0; j < 2; ++j) {
+            const int c = c0 + j;
+            if (c >= nx) break;
+            const uint32_t v = chroma_exact_tile(plan, f, g, s1, s1 + BH * BW, cbx, cby, 1, nullptr, nullptr, w, h, cw,
+                                                 ch, X0 + c, Y0 + r);
+            const size_t o = (size_t)r * cw + c;
+            stg_u8(ob + o, v & 0xFF);
+            stg_u8(orr + o, v >> 8);
         }
     }
-    return qn;
+}
+
+// crop_resize rows of the W tile (image_ops.cpp:136-159) when every lane's two
+// taps are x0, x0 + 1 and the bottom row never clamps (crop margins >= 1 px):
+// each warp walks a contiguous run of output rows; cy0 advances by 0 or 1 per
+// row (step < 1), so the new top lerp is the previous bottom one when it
+// advances, and the bottom lerp is recomputed every row (the same value when
+// cy0 stays) — no per-row branch.  Lane: output columns 2l, 2l+1.
+__device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, uint8_t* oy, int w, int h, int nx,
+                                           int ny, int X0, int Y0, int u0, int v0) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (ny + NW - 1) / NW;
+    const int rb = warp * per, re = min(rb + per, ny);
+    if (rb >= re) return;
+    const int ca = X0 + min(2 * lane, nx - 1), cb = X0 + min(2 * lane + 1, nx - 1);
+    const int xa = __ldg(T.cx0 + ca) - u0, xb = __ldg(T.cx0 + cb) - u0;
+    const float2 fx2 = make_float2((float)__ldg(T.cfx + ca), (float)__ldg(T.cfx + cb));
+    const bool vA = 2 * lane < nx, vB = 2 * lane + 1 < nx;
+    const uint8_t* wl = wt - v0 * WTW;  // indexed by absolute W row
+    auto hl2 = [&](int row) {
+        const uint8_t* rp = wl + row * WTW;
+        const float2 fa = make_float2(b256(rp[xa]), b256(rp[xb])), fb = make_float2(b256(rp[xa + 1]), b256(rp[xb + 1]));
+        return __ffma2_rn(fx2, sub2(fb, fa), fa);
+    };
+    const int myr = min(rb + lane, ny - 1);
+    const int mycy = __ldg(T.cy0 + Y0 + myr);
+    const float myfy = (float)__ldg(T.cfy + Y0 + myr);
+    int trow = __shfl_sync(FULL, mycy, 0);
+    float2 top = hl2(trow), bot = top;
+    uint8_t* py = oy + (size_t)(Y0 + rb) * w + X0 + 2 * lane;
+    uint32_t bad = 0, bit = 1;
+    for (int r = rb; r < re; ++r, py += w, bit <<= 1) {
+        const int cy = __shfl_sync(FULL, mycy, r - rb);
+        const float fy = __shfl_sync(FULL, myfy, r - rb);
+        if (r > rb) {
+            const bool adv = cy != trow;
+            top.x = adv ? bot.x : top.x;
+            top.y = adv ? bot.y : top.y;
+        }
+        bot = hl2(cy + 1);
+        trow = cy;
+        const float2 v = __ffma2_rn(make_float2(fy, fy), sub2(bot, top), top);
+        const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
+        const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
+        if (vA) stg_u16(py, __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x0040));
+        if (fmaxf(fabsf(dv.x), fabsf(dv.y)) > 0.5f - VGUARD) bad |= bit;
+    }
+    if (!vA) bad = 0;
+    for (; bad; bad &= bad - 1) {
+        const int r = rb + __ffs(bad) - 1;
+        uint8_t* o = oy + (size_t)(Y0 + r) * w + X0 + 2 * lane;
+        o[0] = crop_exact_tile(wt, T, X0 + 2 * lane, Y0 + r, u0, v0, w, h);
+        if (vB) o[1] = crop_exact_tile(wt, T, X0 + 2 * lane + 1, Y0 + r, u0, v0, w, h);
+    }
 }
 
 // Persistent TMA compose.  Per tile: every warp waits on the tile's mbarrier,
@@ -1162,10 +1261,9 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             const long long* ryf = T.ryf + (size_t)f * h + v0;
             const uint8_t* bx = &S.box[b][0][0];
             const uint32_t wsm = smem_u32(wt);
-            int qn;
+            int qn = 0;
             if (tp.pad0 & 1)
-                qn = w_rows_lean(bx, BW + 1 - (tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, u0, cf, snf, NW * snf,
-                                 NW * cf, S.wq[warp]);
+                w_rows_lean2(bx, tp.lbx, tp.lby, rxf, ryf, &S.wt[b][0][0], nu, nv, u0, v0, cf, snf, plan, f, w, h);
             else if (tp.lfit)
                 qn = w_rows_q(bx, BW, -(tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf,
                               NW * snf, NW * cf, limx, limy, S.wq[warp]);
@@ -1201,10 +1299,10 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             const uint8_t* b2p = &S.box[b][2][0];
             uint8_t* ob = oCB + (size_t)f * CB.stride + (size_t)Y0 * cw + X0;
             uint8_t* orr = oCR + (size_t)f * CR.stride + (size_t)Y0 * cw + X0;
-            int qn;
+            int qn = 0;
             if (tp.pad0 & 2)
-                qn = chroma_rows_lean(b1p, b2p, BW + 1 - (tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, X0,
-                                      kxx, kyx, NW * kxy, NW * kyy, S.wq[warp]);
+                chroma_rows_lean2(b1p, tp.cbx, tp.cby, pxf, pyf, ob, orr, cw, ch, nx, ny, X0, Y0, kxx, kyx, kxy, kyy,
+                                  plan, f, g, w, h);
             else if (tp.cfit)
                 qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY,
                                    32 * kxx, 32 * kyx, NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
@@ -1243,6 +1341,9 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     if (c0) stg_u8(oy + (size_t)r * w, wt[r * WTW + lane]);
                     if (c1) stg_u8(oy + (size_t)r * w + 32, wt[r * WTW + lane + 32]);
                 }
+            } else if (g.my >= 1 && __all_sync(FULL, __ldg(T.cx0 + X0 + min(2 * lane, nx - 1)) + 1 <= w - 1 &&
+                                                         __ldg(T.cx0 + X0 + min(2 * lane + 1, nx - 1)) + 1 <= w - 1)) {
+                crop_rows2(wt, T, oY + (size_t)f * Y.stride, w, h, nx, ny, X0, Y0, u0, v0);
             } else {
                 // lane l owns output columns 2l and 2l+1 (one 16-bit store per row)
                 uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + 2 * lane;
