@@ -411,8 +411,12 @@ int stabgpu_tracker_destroy(stabgpu_tracker* t);
  * frame whose smoothing window is complete, pipeline.cpp:137-150), so the
  * latency is exactly r frames and the first emission happens at frame 2r.
  * The released frames are bit-identical to Stage I (stabilize_sequence).
- * Planes are host pointers (pitch = width).  After every push / finish the
- * caller pops the ready frames in arrival order. */
+ * Planes are host (pageable or pinned) or device pointers (unified
+ * addressing; pitch = width).  After every push / finish the caller pops the
+ * ready frames in arrival order.  Each push's launches (K1, the K5 step +
+ * compaction + K6 fit or the re-detection, the K7 scan, and the smoothing +
+ * K8 compose of the frame it releases) run as one CUDA graph, instantiated
+ * once per topology and updated in place per frame. */
 typedef struct stabgpu_stream stabgpu_stream;
 
 int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfg, int w, int h, int cw, int ch,
@@ -426,6 +430,10 @@ int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready);
 int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* out_y, uint8_t* out_cb,
                        uint8_t* out_cr, stabgpu_frame_record* record);
 int stabgpu_stream_destroy(stabgpu_stream* s);
+/* Per-frame CUDA graphs on (default) or off (one launch per kernel); off is
+ * forced when a launch sequence needs stream-ordered scratch (more than 8192
+ * corners).  Results are identical either way. */
+int stabgpu_stream_set_graphs(stabgpu_stream* s, int on);
 
 /* ---- colour I/O and evaluation ---------------------
  * Device-resident, n frames of w x h (pitch = width).  RGB is interleaved

@@ -140,6 +140,7 @@ PROTOTYPES = {
     "stabgpu_stream_finish": (I, [V, c_ip]),
     "stabgpu_stream_pop": (I, [V, P(C.c_int64), V, V, V, V]),
     "stabgpu_stream_destroy": (I, [V]),
+    "stabgpu_stream_set_graphs": (I, [V, I]),
     "stabgpu_rgb_to_ycbcr": (I, [V, V, I, I, I, V, V, V]),
     "stabgpu_ycbcr_to_rgb": (I, [V, V, V, V, I, I, I, V]),
     "stabgpu_stabilize_sequence_rgb": (I, [V, V, I, I, I, P(Config), V, V]),

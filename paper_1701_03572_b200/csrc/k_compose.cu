@@ -1525,24 +1525,32 @@ void launch_tiles(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* p
     }
 }
 
+// bytes of the per-launch tables (row starts, crop tables, tile parameters)
+size_t table_bytes(int w, int h, int cw, int ch, int frames) {
+    const bool sep = cw > 0 && !(cw == w && ch == h);
+    const size_t nrow = (size_t)frames * h, ncrow = (size_t)frames * ch;
+    const int tw_tiles = sep ? std::max((w + TW - 1) / TW, (cw + TW - 1) / TW) : (w + TW - 1) / TW;
+    const int th_tiles = sep ? std::max((h + TH - 1) / TH, (ch + TH - 1) / TH) : (h + TH - 1) / TH;
+    const size_t ntiles = (size_t)tw_tiles * th_tiles * frames;
+    return sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) +
+           sizeof(TileParams) * ntiles + 512;
+}
+
 void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
-                 double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr, cudaStream_t st) {
+                 double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr, cudaStream_t st,
+                 void* scratch = nullptr, size_t scratch_bytes = 0) {
     if (frames <= 0) return;
     const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
     const bool chroma = cb.base && cr.base && out_cb && out_cr;
     const int w = y.w, h = y.h, cw = chroma ? cb.w : 0, ch = chroma ? cb.h : 0;
-    // per-launch tables, stream-ordered allocation
+    // per-launch tables: the caller's scratch, else a stream-ordered allocation
     const size_t nrow = (size_t)frames * h, ncrow = (size_t)frames * ch;
-    const int tw_tiles = ((chroma && !(cb.w == y.w && cb.h == y.h)) ? std::max((w + TW - 1) / TW, (cw + TW - 1) / TW)
-                                                                       : (w + TW - 1) / TW);
-    const int th_tiles = ((chroma && !(cb.w == y.w && cb.h == y.h)) ? std::max((h + TH - 1) / TH, (ch + TH - 1) / TH)
-                                                                       : (h + TH - 1) / TH);
-    const size_t ntiles = (size_t)tw_tiles * th_tiles * frames;
-    const size_t bytes = sizeof(long long) * (2 * nrow + 2 * ncrow) + (sizeof(int) + sizeof(double)) * (w + h) +
-                         sizeof(TileParams) * ntiles + 512;
+    const size_t bytes = table_bytes(w, h, cw, ch, frames);
     char* buf = nullptr;
+    const bool own = !(scratch && scratch_bytes >= bytes);
+    if (!own) buf = static_cast<char*>(scratch);
     // a failed allocation stays in cudaGetLastError for the caller's check_launch
-    if (cudaMallocAsync((void**)&buf, bytes, st) != cudaSuccess) return;
+    else if (cudaMallocAsync((void**)&buf, bytes, st) != cudaSuccess) return;
     Tables T;
     long long* q = reinterpret_cast<long long*>(buf);
     T.rxf = q;
@@ -1582,16 +1590,18 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
             !(frames_ok && launch_tma<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st)))
             launch_tiles<false, true>(y, cb, cr, plan, frames, g, T, nullptr, out_cb, out_cr, st);
     }
-    cudaFreeAsync(buf, st);
+    if (own) cudaFreeAsync(buf, st);
 }
 
 }  // namespace
 
 void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
                     double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
-                    cudaStream_t st) {
-    run_compose(y, cb, cr, plan, frames, crop_ratio, out_y, out_cb, out_cr, st);
+                    cudaStream_t st, void* scratch, size_t scratch_bytes) {
+    run_compose(y, cb, cr, plan, frames, crop_ratio, out_y, out_cb, out_cr, st, scratch, scratch_bytes);
 }
+
+size_t compose_scratch_bytes(int w, int h, int cw, int ch, int frames) { return table_bytes(w, h, cw, ch, frames); }
 
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st) {

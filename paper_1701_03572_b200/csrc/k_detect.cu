@@ -1048,6 +1048,8 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     }
 }
 
+bool detect_allocates(const stabgpu_detect_cfg& cfg) { return cfg.max_corners > SMEM_CORNERS; }
+
 void launch_gradients(const uint8_t* src, int w, int h, double* gx, double* gy, cudaStream_t st) {
     dim3 grid((w + 127) / 128, h);
     gradients_kernel<<<grid, 128, 0, st>>>(src, w, h, gx, gy);

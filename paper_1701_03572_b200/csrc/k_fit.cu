@@ -384,6 +384,8 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const double2* __restr
 
 }  // namespace
 
+bool fit_allocates(int max_pts) { return (size_t)max_pts * (2 * sizeof(double2) + 1) > kFitSmemMax; }
+
 void launch_fit(const double2* trk_prev, const double2* trk_cur, const int* trk_n, int max_pts,
                 int nframes, long long frame_index0, const stabgpu_config& cfg,
                 stabgpu_motion_record* out, cudaStream_t st, long long stream_frames, int2* pre_scratch) {

@@ -168,10 +168,19 @@ void launch_plan_smooth(const double4* cum, long long n_known, bool complete, lo
                         long long count, int radius, stabgpu_frame_record* rec, FramePlan* plan,
                         PlanGeom geo, cudaStream_t st, long long stream_frames = 0);
 
+// launch sequences that allocate stream-ordered scratch (cannot be updated
+// in place inside a CUDA graph): K4 with more corners than shared memory
+// holds, K6 with more pairs than its shared budget
+bool detect_allocates(const stabgpu_detect_cfg& cfg);
+bool fit_allocates(int max_pts);
+
 // ---- K8 compose (k_compose.cu) ----
+// scratch: optional caller-owned table buffer of compose_scratch_bytes() bytes
+// (no stream-ordered allocation inside: CUDA-graph friendly)
 void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
                     double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
-                    cudaStream_t st);
+                    cudaStream_t st, void* scratch = nullptr, size_t scratch_bytes = 0);
+size_t compose_scratch_bytes(int w, int h, int cw, int ch, int frames);
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st);
 void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,

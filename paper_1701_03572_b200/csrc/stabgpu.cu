@@ -1865,6 +1865,16 @@ struct stabgpu_stream {
     // is composed (out_done[k]); pinned error word of the selector scan
     std::vector<cudaEvent_t> slot_free, out_done, in_done;
     int* err_host = nullptr;
+    // per-frame CUDA graphs: each push's launch sequence (K1 levels, K5 step +
+    // compaction + K6 fit or the detection, the K7 scan, and the smoothing +
+    // K8 compose of the frame it releases) is stream-captured and launched as
+    // one graph; the executable graph of each topology (first frame /
+    // re-detect / tracking, 0 or 1 release) is instantiated once and updated
+    // in place with the frame's parameters afterwards
+    bool graphs = false;
+    std::map<int, cudaGraphExec_t> execs;
+    void* cscratch = nullptr;  // K8 tables of one frame (no allocation inside a graph)
+    size_t cscratch_bytes = 0;
 };
 
 namespace {
@@ -1909,9 +1919,12 @@ int stream_grow(stabgpu_stream* s, long long need) {
     return STABGPU_OK;
 }
 
-// composes released frame i into output slot i % ocap and queues it; the
-// input slot is free and the output slot downloadable after it (events)
-int stream_release(stabgpu_stream* s, long long i) {
+bool graph_safe(const stabgpu_config& c) {
+    return !detect_allocates(c.detect) && !fit_allocates(c.detect.max_corners);
+}
+
+// smoothing + K8 compose of released frame i into output slot i % ocap
+void stream_release_kernels(stabgpu_stream* s, long long i) {
     cudaStream_t st = s->ctx->stream;
     const int r = s->cfg.smooth_radius;
     launch_plan_smooth(s->cum, s->pushed, s->complete, i, 1, r, s->rec, s->plan,
@@ -1922,24 +1935,65 @@ int stream_release(stabgpu_stream* s, long long i) {
     PlaneBatch bb{s->chroma ? s->ring_cb + in * fc : nullptr, fc, s->cw, s->ch};
     PlaneBatch rb{s->chroma ? s->ring_cr + in * fc : nullptr, fc, s->cw, s->ch};
     launch_compose(yb, bb, rb, s->plan + i, 1, s->cfg.crop_ratio, s->out_y + o * fl,
-                   s->chroma ? s->out_cb + o * fc : nullptr, s->chroma ? s->out_cr + o * fc : nullptr, st);
-    cudaEventRecord(s->slot_free[in], st);
-    cudaEventRecord(s->out_done[o], st);
+                   s->chroma ? s->out_cb + o * fc : nullptr, s->chroma ? s->out_cr + o * fc : nullptr, st,
+                   s->cscratch, s->cscratch_bytes);
     s->ctx->stats.launches += 2;
-    s->ready.push_back(i);
-    return check_launch("stream compose");
 }
 
-// CompensationPlanner::release (pipeline.cpp:137-150)
-int stream_release_ready(stabgpu_stream* s) {
+// after frame i's release kernels were issued: its input slot is free and
+// its output slot downloadable (events), and it is queued for pop
+void stream_release_done(stabgpu_stream* s, long long i) {
+    cudaStream_t st = s->ctx->stream;
+    cudaEventRecord(s->slot_free[(size_t)(i % s->cap)], st);
+    cudaEventRecord(s->out_done[(size_t)(i % s->ocap)], st);
+    s->ready.push_back(i);
+}
+
+// CompensationPlanner::release (pipeline.cpp:137-150): the frames
+// [s->next, s->next + count) are released now
+int stream_release_count(const stabgpu_stream* s, long long* count) {
+    *count = 0;
     const int r = s->cfg.smooth_radius;
     if (!s->complete && s->pushed < 2LL * r) return STABGPU_OK;
-    while (s->next < s->pushed && (s->complete || s->next + r < s->pushed)) {
-        if ((long long)(s->ready.size() - s->ready_head) >= s->ocap)
+    long long n = s->next;
+    while (n < s->pushed && (s->complete || n + r < s->pushed)) {
+        if ((long long)(s->ready.size() - s->ready_head) + (n - s->next) >= s->ocap)
             return set_err(STABGPU_SEQUENCING, "stream: %d released frames not popped", s->ocap);
-        TRY(stream_release(s, s->next));
-        ++s->next;
+        ++n;
     }
+    *count = n - s->next;
+    return STABGPU_OK;
+}
+
+int stream_release_ready(stabgpu_stream* s) {
+    long long n;
+    TRY(stream_release_count(s, &n));
+    for (long long k = 0; k < n; ++k) stream_release_kernels(s, s->next + k);
+    TRY(check_launch("stream compose"));
+    for (long long k = 0; k < n; ++k) stream_release_done(s, s->next + k);
+    s->next += n;
+    return STABGPU_OK;
+}
+
+// launches a captured push graph through the executable graph of its topology
+int stream_launch_graph(stabgpu_stream* s, int key, cudaGraph_t g) {
+    cudaStream_t st = s->ctx->stream;
+    auto it = s->execs.find(key);
+    if (it != s->execs.end()) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(it->second, g, &info) != cudaSuccess) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(it->second);
+            s->execs.erase(it);
+            it = s->execs.end();
+        }
+    }
+    if (it == s->execs.end()) {
+        cudaGraphExec_t ex = nullptr;
+        CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
+        it = s->execs.emplace(key, ex).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, st));
     return STABGPU_OK;
 }
 
@@ -2003,6 +2057,11 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
         (rc = salloc(s, &s->fit_pre, 2 * kFitPreCtas)))
         return fail(rc);
     if ((rc = stream_grow(s, 256))) return fail(rc);
+    s->cscratch_bytes = compose_scratch_bytes(w, h, s->cw, s->ch, 1);
+    if ((rc = salloc(s, reinterpret_cast<uint8_t**>(&s->cscratch), s->cscratch_bytes))) return fail(rc);
+    // graphs need launch sequences without stream-ordered allocations: K4's
+    // accepted list fits shared memory and K6's pairs fit its shared budget
+    s->graphs = graph_safe(cfg);
     s->slot_free.resize(s->cap);
     s->in_done.resize(s->cap);
     s->out_done.resize(s->ocap);
@@ -2047,13 +2106,23 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     // before push returns (the upload is waited for at the end), while the
     // previous frames' compute and downloads keep running.
     if (f >= s->cap) CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->slot_free[slot], 0));
-    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyHostToDevice, ctx->cin));
+    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyDefault, ctx->cin));
     if (s->chroma) {
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyHostToDevice, ctx->cin));
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyHostToDevice, ctx->cin));
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyDefault, ctx->cin));
+        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyDefault, ctx->cin));
     }
     CUDA_TRY(cudaEventRecord(s->in_done[slot], ctx->cin));
     CUDA_TRY(cudaStreamWaitEvent(st, s->in_done[slot], 0));
+    // the frames this push releases (CompensationPlanner::release)
+    s->pushed = f + 1;
+    long long nrel = 0;
+    if (int rc = stream_release_count(s, &nrel)) {
+        s->pushed = f;
+        return rc;
+    }
+    const bool detect = f == 0 || f % R == 0;
+    const bool graph = s->graphs && nrel <= 1;
+    if (graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     // K1: the pyramid of the current frame, levels >= 1 into slot f & 1; no
     // copies: level 0 stays in the ring, and the tracker sees (previous,
     // current) through a pyramid view whose frame stride is the signed
@@ -2077,7 +2146,7 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     }
     if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88) + detection (flow.cpp:303-308)
         static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
-        CUDA_TRY(cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st));
+        cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st);
         launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
     } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
         LkStep k;
@@ -2105,9 +2174,20 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     }
     // K7: selector + trajectory prefix for this frame
     launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
-    TRY(check_launch("stream push"));
-    s->pushed = f + 1;
-    TRY(stream_release_ready(s));
+    for (long long k = 0; k < nrel; ++k) stream_release_kernels(s, s->next + k);
+    int rc = check_launch("stream push");
+    if (graph) {
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (rc == STABGPU_OK && e != cudaSuccess)
+            rc = set_err(STABGPU_CUDA, "stream: graph capture failed: %s", cudaGetErrorString(e));
+        if (rc == STABGPU_OK) rc = stream_launch_graph(s, (f == 0 ? 1 : 0) | (detect ? 2 : 0) | (int)(nrel << 2), g);
+        if (g) cudaGraphDestroy(g);
+        ctx->stats.launches += 1;
+    }
+    TRY(rc);
+    for (long long k = 0; k < nrel; ++k) stream_release_done(s, s->next + k);
+    s->next += nrel;
     CUDA_TRY(cudaEventSynchronize(s->in_done[slot]));  // the caller's buffers are consumed
     if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
     return STABGPU_OK;
@@ -2140,15 +2220,21 @@ int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* 
     cudaStream_t co = s->ctx->cout;
     (void)st;
     CUDA_TRY(cudaStreamWaitEvent(co, s->out_done[o], 0));
-    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDeviceToHost, co));
-    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDeviceToHost, co));
-    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDeviceToHost, co));
-    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, co));
+    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDefault, co));
+    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDefault, co));
+    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDefault, co));
+    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDefault, co));
     // the selector scan's error word (written before the frame was released)
     CUDA_TRY(cudaMemcpyAsync(s->err_host, reinterpret_cast<int*>(s->ps + 1), sizeof(int), cudaMemcpyDeviceToHost, co));
     CUDA_TRY(cudaStreamSynchronize(co));
     if (*s->err_host) TRY(plan_error(s->ctx, s->ps));
     if (index) *index = i;
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_set_graphs(stabgpu_stream* s, int on) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    s->graphs = on != 0 && graph_safe(s->cfg);
     return STABGPU_OK;
 }
 
@@ -2162,6 +2248,7 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
     for (auto* v : {&s->slot_free, &s->in_done, &s->out_done})
         for (auto e : *v)
             if (e) cudaEventDestroy(e);
+    for (auto& kv : s->execs) cudaGraphExecDestroy(kv.second);
     if (s->err_host) cudaFreeHost(s->err_host);
     delete s;
     return STABGPU_OK;

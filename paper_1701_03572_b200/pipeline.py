@@ -410,7 +410,8 @@ class StreamStabilizer:
     releases the rest.  Each released frame is (index, y, cb, cr, record) and
     is bit-identical to Stage I's output for that frame."""
 
-    def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0):
+    def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0,
+                 graphs: bool = True):
         self.w, self.h, self.cw, self.ch = w, h, cw, ch
         self._c = cfg.c()
         self._lib = load()
@@ -418,6 +419,8 @@ class StreamStabilizer:
         self._h = C.c_void_p()
         check(self._lib.stabgpu_stream_create(self._ctx.handle, C.byref(self._c), w, h, cw, ch,
                                               C.byref(self._h)))
+        # per-frame CUDA graphs (default) or one launch per kernel; same results
+        check(self._lib.stabgpu_stream_set_graphs(self._h, int(graphs)))
 
     def _pop_all(self, n: int):
         out = []

@@ -443,16 +443,18 @@ def _release_schedule(n, r):
     return out, list(range(nxt, n))
 
 
-@pytest.mark.parametrize("mode,ransac,smooth", [("similarity", 0, 5), ("hybrid", 200, 4), ("rigid", 100, 9)])
-def test_stream_equals_stage1(mode, ransac, smooth):
+@pytest.mark.parametrize("mode,ransac,smooth,graphs", [("similarity", 0, 5, True), ("hybrid", 200, 4, True),
+                                                         ("rigid", 100, 9, True), ("hybrid", 200, 4, False)])
+def test_stream_equals_stage1(mode, ransac, smooth, graphs):
     """Stage II (push one frame at a time) releases frames on the reference's
     schedule (latency r, first emission at 2r) and each released frame and
-    record is bit-identical to Stage I."""
+    record is bit-identical to Stage I, with the per-frame CUDA graphs and
+    with one launch per kernel."""
     y, cb, cr = _data.video(frames=41, objects=2, jit_t=3.0, color=True)
     cfg = _data.small_cfg(_data.MODES[mode], ransac=ransac, smooth=smooth)
     sy, sb, sr, srec = pipeline.stabilize_sequence(y, cfg, cb, cr)
     n, (h, w) = len(y), y.shape[1:]
-    s = pipeline.StreamStabilizer(cfg, w, h, cb.shape[2], cb.shape[1])
+    s = pipeline.StreamStabilizer(cfg, w, h, cb.shape[2], cb.shape[1], graphs=graphs)
     sched, tail = _release_schedule(n, cfg.smooth_radius)
     got = []
     for k in range(n):
@@ -506,6 +508,41 @@ def test_stream_equals_oracle_config(name, frames):
 
 def orc_checker():
     return _oracle.oracle()
+
+
+def test_stream_device_pointers():
+    """push/pop take device pointers too (unified addressing): frames already
+    in HBM stream through the same path with the same results."""
+    import ctypes as C
+
+    import torch
+
+    y = _data.video(frames=16)[0]
+    cfg = _data.small_cfg(smooth=3)
+    sy, _, _, _ = pipeline.stabilize_sequence(y, cfg)
+    h, w = y.shape[1:]
+    s = pipeline.StreamStabilizer(cfg, w, h)
+    dy = torch.from_numpy(y).cuda()
+    out = torch.empty_like(dy)
+    lib, hs = s._lib, s._h
+    n = C.c_int()
+    popped = []
+
+    def pop(k):
+        for _ in range(k):
+            idx = C.c_int64()
+            j = len(popped)
+            assert lib.stabgpu_stream_pop(hs, C.byref(idx), C.c_void_p(out[j].data_ptr()), None, None, None) == 0
+            popped.append(idx.value)
+
+    for k in range(len(y)):
+        assert lib.stabgpu_stream_push(hs, C.c_void_p(dy[k].data_ptr()), None, None, C.byref(n)) == 0
+        pop(n.value)
+    assert lib.stabgpu_stream_finish(hs, C.byref(n)) == 0
+    pop(n.value)
+    s.close()
+    assert popped == list(range(len(y)))
+    assert np.array_equal(out.cpu().numpy(), sy)
 
 
 def test_stream_gray_and_errors():

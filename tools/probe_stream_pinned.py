@@ -1,5 +1,8 @@
 """Stage II at a benchmark config with pinned host buffers, straight through
-the C ABI (push frame k from a pinned array, pop into a pinned array)."""
+the C ABI (push frame k from a pinned array, pop into a pinned array).
+--device: frames already in HBM (push/pop device pointers); --nographs:
+one launch per kernel instead of the per-frame CUDA graph; --lag: pop one
+push late."""
 import ctypes as C
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,8 +14,9 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 cfg = synth.CONFIGS[name]
 planes = synth.Video(cfg.video).render(0, n)
-pin = [torch.from_numpy(p).pin_memory() for p in planes]
-outp = [torch.empty_like(p).pin_memory() for p in pin]
+dev = "--device" in sys.argv
+pin = [torch.from_numpy(p).cuda() if dev else torch.from_numpy(p).pin_memory() for p in planes]
+outp = [torch.empty_like(p) if dev else torch.empty_like(p).pin_memory() for p in pin]
 h, w = planes[0].shape[1:]
 col = len(planes) == 3
 cw, ch = (planes[1].shape[2], planes[1].shape[1]) if col else (0, 0)
@@ -21,6 +25,8 @@ ctx = context(0)
 c = cfg.stab.c()
 hs = C.c_void_p()
 assert lib.stabgpu_stream_create(ctx.handle, C.byref(c), w, h, cw, ch, C.byref(hs)) == 0
+graphs = "--nographs" not in sys.argv
+assert lib.stabgpu_stream_set_graphs(hs, int(graphs)) == 0
 rec = np.zeros(1, pipeline.RECORD_DT)
 vp = lambda t, k: C.c_void_p(t[k].data_ptr())
 def pop_all(k):
@@ -56,5 +62,5 @@ pop_all(nr.value)
 dt = time.perf_counter() - t0
 lib.stabgpu_stream_destroy(hs)
 lat = np.array(lat) * 1e3
-print(f"{name} pinned: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
+print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
       f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out")
