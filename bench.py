@@ -371,6 +371,24 @@ def run_ours(args, cfg):
     ctx.enable_timing(False)
     ms_dev_plain, _, _ = timed(step_device, max(1, min(args.steps, 3)), 0)
     ms_e2e, _, _ = timed(step_e2e, args.steps, args.warmup)
+    ms_rgb = None
+    if world == 1 and planes == 3:
+        # C3 is an RGB workload: the same step from interleaved RGB host frames
+        # to interleaved RGB host frames (media_io's conversions on the device:
+        # per-chunk RGB -> Y/Cb/Cr after upload, Y/Cb/Cr -> RGB fused into K8's
+        # store); the RGB source is the device conversion of the planes
+        from paper_1701_03572_b200 import evaluate
+        rgb_in = torch.empty((n, spec.height, spec.width, 3), dtype=torch.uint8, pin_memory=True)
+        for f0 in range(0, n, 100):
+            rgb_in[f0:f0 + 100].copy_(evaluate.ycbcr_to_rgb(dev[0][f0:f0 + 100], dev[1][f0:f0 + 100],
+                                                             dev[2][f0:f0 + 100]))
+        rgb_out = torch.empty_like(rgb_in).pin_memory()
+
+        def step_rgb():
+            pipeline.stabilize_sequence_rgb_host_buffers(ctx, rgb_in, n, spec.width, spec.height, cfg_c, rgb_out, rec)
+
+        ms_rgb, _, _ = timed(step_rgb, args.steps, args.warmup)
+        del rgb_in, rgb_out
     ctx.enable_timing(True)
     value = n / (ms_dev / 1000.0)
     e2e = n / (ms_e2e / 1000.0)
@@ -398,6 +416,10 @@ def run_ours(args, cfg):
                         "d2h_bytes_per_step": fb * n + (n * pipeline.RECORD_BYTES if world == 1 else 0),
                         "ms_per_step": ms_e2e, "steps": args.steps, "warmup": args.warmup},
                 "ms_per_step_without_stage_events": ms_dev_plain,
+                "e2e_rgb": None if ms_rgb is None else {
+                    "value": n / (ms_rgb / 1000.0), "unit": UNIT, "h2d_bytes_per_step": fb * n,
+                    "d2h_bytes_per_step": fb * n + n * pipeline.RECORD_BYTES, "ms_per_step": ms_rgb,
+                    "path": "stabgpu_stabilize_sequence_rgb: interleaved RGB pinned host frames in and out"},
                 "roofline": {"bound": "hbm", "kernel": "K8 compose_tma_kernel (fused warp + crop/resize, all planes)",
                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": (achieved / hbm) if achieved else None,

@@ -37,6 +37,7 @@
 #include <climits>
 #include <cstring>
 
+#include "colour.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "walk.h"
@@ -933,17 +934,18 @@ __device__ __forceinline__ int w_rows_q(P src, int pitch, int obase, const long 
 // warp's queue length.
 template <typename P>
 __device__ __forceinline__ int chroma_rows_q(P s1, P s2, int pitch, int obase, const long long* __restrict__ pxf,
-                                             const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int cw,
+                                             const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int op,
                                              int nx, int ny, long long xKX, long long xKY, long long KX32,
                                              long long KY32, long long RSX, long long RSY, unsigned limx,
                                              unsigned limy, unsigned* q) {
+    // op: output row pitch
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool v0 = lane < nx, v1 = lane + 32 < nx;
     const int ob1 = obase + pitch + 1;
     int qn = 0;
-    const size_t step = (size_t)NW * cw;
-    uint8_t* pb = ob + (size_t)warp * cw + lane;
-    uint8_t* pr = orr + (size_t)warp * cw + lane;
+    const size_t step = (size_t)NW * op;
+    uint8_t* pb = ob + (size_t)warp * op + lane;
+    uint8_t* pr = orr + (size_t)warp * op + lane;
     long long PX = to32(__ldg(pxf + min(warp, ny - 1)) + xKX), PY = to32(__ldg(pyf + min(warp, ny - 1)) + xKY);
     const long long kx = KX32 >> 16, ky = KY32 >> 16, rsx = RSX >> 16, rsy = RSY >> 16;
     for (int r = warp; r < ny; r += NW, pb += step, pr += step, PX += rsx, PY += rsy) {
@@ -1074,10 +1076,11 @@ __device__ __forceinline__ void w_rows_lean2(const uint8_t* box, int lbx, int lb
 // 4:4:4 chroma rows of an interior tile straight to the output planes; the
 // Cr box follows the Cb box (one immediate offset)
 __device__ __forceinline__ void chroma_rows_lean2(const uint8_t* s1, int cbx, int cby, const long long* __restrict__ pxf,
-                                                  const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int cw,
-                                                  int ch, int nx, int ny, int X0, int Y0, long long kxx, long long kyx,
-                                                  long long kxy, long long kyy, const FramePlan* __restrict__ plan, int f,
-                                                  CropGeom g, int w, int h) {
+                                                  const long long* __restrict__ pyf, uint8_t* ob, uint8_t* orr, int op,
+                                                  int cw, int ch, int nx, int ny, int X0, int Y0, long long kxx,
+                                                  long long kyx, long long kxy, long long kyy,
+                                                  const FramePlan* __restrict__ plan, int f, CropGeom g, int w, int h) {
+    // op: output row pitch
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c0 = 2 * lane;
     const int r0 = min(warp, ny - 1);
@@ -1087,8 +1090,8 @@ __device__ __forceinline__ void chroma_rows_lean2(const uint8_t* s1, int cbx, in
     const bool vA = c0 < nx, vB = c0 + 1 < nx;
     const long long DX = vB ? (kxx >> 16) : 0, DY = vB ? (kyx >> 16) : 0;
     const long long RX = ((long long)NW * kxy) >> 16, RY = ((long long)NW * kyy) >> 16;
-    const size_t step = (size_t)NW * cw;
-    uint8_t* pb = ob + (size_t)warp * cw + c0;
+    const size_t step = (size_t)NW * op;
+    uint8_t* pb = ob + (size_t)warp * op + c0;
     const ptrdiff_t dr = orr - ob;
     uint32_t bad = 0, bit = 1;
 #pragma unroll 2
@@ -1114,11 +1117,22 @@ __device__ __forceinline__ void chroma_rows_lean2(const uint8_t* s1, int cbx, in
             if (c >= nx) break;
             const uint32_t v = chroma_exact_tile(plan, f, g, s1, s1 + BH * BW, cbx, cby, 1, nullptr, nullptr, w, h, cw,
                                                  ch, X0 + c, Y0 + r);
-            const size_t o = (size_t)r * cw + c;
+            const size_t o = (size_t)r * op + c;
             stg_u8(ob + o, v & 0xFF);
             stg_u8(orr + o, v >> 8);
         }
     }
+}
+
+// two RGB pixels (6 bytes, 2-byte aligned) from two luma bytes yy (low 16
+// bits) and the Cb / Cr pairs at c (chroma output tile, Cr TTH * TW later)
+__device__ __forceinline__ void store_rgb2(uint8_t* p, uint32_t yy, const uint8_t* c) {
+    const uint32_t cb = *reinterpret_cast<const uint16_t*>(c), cr = *reinterpret_cast<const uint16_t*>(c + TTH * TW);
+    const uint32_t p0 = colour::ycc_to_rgb(yy & 0xFF, cb & 0xFF, cr & 0xFF);
+    const uint32_t p1 = colour::ycc_to_rgb((yy >> 8) & 0xFF, cb >> 8, cr >> 8);
+    stg_u16(p, p0);
+    stg_u16(p + 2, (p0 >> 16) | (p1 << 8));
+    stg_u16(p + 4, p1 >> 8);
 }
 
 // crop_resize rows of the W tile (image_ops.cpp:136-159) when every lane's two
@@ -1127,8 +1141,13 @@ __device__ __forceinline__ void chroma_rows_lean2(const uint8_t* s1, int cbx, in
 // row (step < 1), so the new top lerp is the previous bottom one when it
 // advances, and the bottom lerp is recomputed every row (the same value when
 // cy0 stays) — no per-row branch.  Lane: output columns 2l, 2l+1.
+// RGBO: the luma bytes are combined with the tile's Cb / Cr (csc: the chroma
+// pass's output tile, pitch TW, Cr TTH * TW after Cb) and stored as
+// interleaved RGB (yuv_to_rgb, colour.cuh) into the RGB frame oy (pitch 3w):
+// Y/Cb/Cr -> RGB fused into the compose store.
+template <bool RGBO>
 __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, uint8_t* oy, int w, int h, int nx,
-                                           int ny, int X0, int Y0, int u0, int v0) {
+                                           int ny, int X0, int Y0, int u0, int v0, const uint8_t* csc) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (ny + NW - 1) / NW;
@@ -1149,9 +1168,11 @@ __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, u
     const float myfy = (float)__ldg(T.cfy + Y0 + myr);
     int trow = __shfl_sync(FULL, mycy, 0);
     float2 top = hl2(trow), bot = top;
-    uint8_t* py = oy + (size_t)(Y0 + rb) * w + X0 + 2 * lane;
+    const int OP = RGBO ? 3 * w : w;  // output pitch
+    uint8_t* py = oy + ((size_t)(Y0 + rb) * w + X0 + 2 * lane) * (RGBO ? 3 : 1);
+    const uint8_t* pc = csc + rb * TW + 2 * lane;
     uint32_t bad = 0, bit = 1;
-    for (int r = rb; r < re; ++r, py += w, bit <<= 1) {
+    for (int r = rb; r < re; ++r, py += OP, pc += TW, bit <<= 1) {
         const int cy = __shfl_sync(FULL, mycy, r - rb);
         const float fy = __shfl_sync(FULL, myfy, r - rb);
         if (r > rb) {
@@ -1164,15 +1185,26 @@ __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, u
         const float2 v = __ffma2_rn(make_float2(fy, fy), sub2(bot, top), top);
         const float2 m = __fadd2_rn(v, make_float2(8388608.0f, 8388608.0f));
         const float2 dv = sub2(v, __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f)));
-        if (vA) stg_u16(py, __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x0040));
+        const uint32_t yy = __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x0040);
+        if (RGBO) {
+            if (vA) store_rgb2(py, yy, pc);
+        } else if (vA) {
+            stg_u16(py, yy);
+        }
         if (fmaxf(fabsf(dv.x), fabsf(dv.y)) > 0.5f - VGUARD) bad |= bit;
     }
     if (!vA) bad = 0;
     for (; bad; bad &= bad - 1) {
         const int r = rb + __ffs(bad) - 1;
-        uint8_t* o = oy + (size_t)(Y0 + r) * w + X0 + 2 * lane;
-        o[0] = crop_exact_tile(wt, T, X0 + 2 * lane, Y0 + r, u0, v0, w, h);
-        if (vB) o[1] = crop_exact_tile(wt, T, X0 + 2 * lane + 1, Y0 + r, u0, v0, w, h);
+        const uint32_t y0 = crop_exact_tile(wt, T, X0 + 2 * lane, Y0 + r, u0, v0, w, h);
+        const uint32_t y1 = vB ? crop_exact_tile(wt, T, X0 + 2 * lane + 1, Y0 + r, u0, v0, w, h) : 0u;
+        if (RGBO) {
+            store_rgb2(oy + ((size_t)(Y0 + r) * w + X0 + 2 * lane) * 3, y0 | y1 << 8, csc + r * TW + 2 * lane);
+        } else {
+            uint8_t* o = oy + (size_t)(Y0 + r) * w + X0 + 2 * lane;
+            o[0] = (uint8_t)y0;
+            if (vB) o[1] = (uint8_t)y1;
+        }
     }
 }
 
@@ -1182,12 +1214,18 @@ __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, u
 // the exact reference path inline (the warp diverges for them only).  wt is
 // double-buffered and the TMA box of tile k+2 is issued only after the
 // barrier of tile k+1, so a fast warp may run ahead into the next tile.
-template <bool LUMA, bool CHROMA>
+//
+// RGBO (4:4:4, crop margins >= 1 px): the chroma rows go to a per-CTA Cb / Cr
+// tile in global scratch (double-buffered like wt; 32 KB per CTA, L2-resident),
+// and the crop pass combines each luma byte with its Cb / Cr into interleaved
+// RGB at oY (3 bytes per pixel) — no plane ever reaches HBM.
+template <bool LUMA, bool CHROMA, bool RGBO>
 __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
     PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
     Tables T, int tiles_x, int tiles_y, int frames, const __grid_constant__ CUtensorMap mapY,
     const __grid_constant__ CUtensorMap mapCB, const __grid_constant__ CUtensorMap mapCR,
-    uint8_t* __restrict__ oY, uint8_t* __restrict__ oCB, uint8_t* __restrict__ oCR) {
+    uint8_t* __restrict__ oY, uint8_t* __restrict__ oCB, uint8_t* __restrict__ oCR, uint8_t* scr) {
+    static_assert(!RGBO || (LUMA && CHROMA), "RGB output needs luma and 4:4:4 chroma");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1252,6 +1290,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
         const uint8_t* gcb = CHROMA ? CB.base + (size_t)f * CB.stride : nullptr;
         const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
         const uint8_t* wt = &S.wt[b][0][0];
+        uint8_t* csc = RGBO ? scr + ((size_t)blockIdx.x * 2 + b) * (2 * TTH * TW) : nullptr;
         mbar_wait(smem_u32(&S.mbar[b]), (uint32_t)((k >> 1) & 1));
         // ------------------------------------------- W rows -> wt[b]
         if (LUMA) {
@@ -1297,17 +1336,18 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             const long long* pyf = T.pyf + (size_t)f * ch + Y0;
             const uint8_t* b1p = &S.box[b][1][0];
             const uint8_t* b2p = &S.box[b][2][0];
-            uint8_t* ob = oCB + (size_t)f * CB.stride + (size_t)Y0 * cw + X0;
-            uint8_t* orr = oCR + (size_t)f * CR.stride + (size_t)Y0 * cw + X0;
+            uint8_t* ob = RGBO ? csc : oCB + (size_t)f * CB.stride + (size_t)Y0 * cw + X0;
+            uint8_t* orr = RGBO ? csc + TTH * TW : oCR + (size_t)f * CR.stride + (size_t)Y0 * cw + X0;
+            const int op = RGBO ? TW : cw;  // output row pitch
             int qn = 0;
             if (tp.pad0 & 2)
-                chroma_rows_lean2(b1p, tp.cbx, tp.cby, pxf, pyf, ob, orr, cw, ch, nx, ny, X0, Y0, kxx, kyx, kxy, kyy,
-                                  plan, f, g, w, h);
+                chroma_rows_lean2(b1p, tp.cbx, tp.cby, pxf, pyf, ob, orr, op, cw, ch, nx, ny, X0, Y0, kxx, kyx, kxy,
+                                  kyy, plan, f, g, w, h);
             else if (tp.cfit)
-                qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY,
+                qn = chroma_rows_q(b1p, b2p, BW, -(tp.cby * BW + tp.cbx), pxf, pyf, ob, orr, op, nx, ny, xKX, xKY,
                                    32 * kxx, 32 * kyx, NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
             else
-                qn = chroma_rows_q(gcb, gcr, cw, 0, pxf, pyf, ob, orr, cw, nx, ny, xKX, xKY, 32 * kxx, 32 * kyx,
+                qn = chroma_rows_q(gcb, gcr, cw, 0, pxf, pyf, ob, orr, op, nx, ny, xKX, xKY, 32 * kxx, 32 * kyx,
                                    NW * kxy, NW * kyy, limx, limy, S.wq[warp]);
             if (__any_sync(FULL, qn > 0)) {
                 __syncwarp();
@@ -1324,7 +1364,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                     }
                     const uint32_t v = chroma_exact_tile(plan, f, g, b1p, b2p, tp.cbx, tp.cby, tp.cfit, gcb, gcr, w,
                                                          h, cw, ch, X0 + c, Y0 + r);
-                    const size_t o = (size_t)r * cw + c;
+                    const size_t o = (size_t)r * op + c;
                     stg_u8(ob + o, v & 0xFF);
                     stg_u8(orr + o, v >> 8);
                 }
@@ -1333,7 +1373,9 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
         }
         __syncthreads();  // wt[b] complete; box[b] free for tile k+2 after this
         // ------------------------------------------- crop_resize of W -> global
-        if (LUMA) {
+        if (RGBO) {  // the host checked the crop_rows2 preconditions (margins >= 1 px)
+            crop_rows2<true>(wt, T, oY + (size_t)f * Y.stride * 3, w, h, nx, ny, X0, Y0, u0, v0, csc);
+        } else if (LUMA) {
             if (identity) {
                 uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + lane;
                 const bool c0 = lane < nx, c1 = lane + 32 < nx;
@@ -1343,7 +1385,7 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 }
             } else if (g.my >= 1 && __all_sync(FULL, __ldg(T.cx0 + X0 + min(2 * lane, nx - 1)) + 1 <= w - 1 &&
                                                          __ldg(T.cx0 + X0 + min(2 * lane + 1, nx - 1)) + 1 <= w - 1)) {
-                crop_rows2(wt, T, oY + (size_t)f * Y.stride, w, h, nx, ny, X0, Y0, u0, v0);
+                crop_rows2<false>(wt, T, oY + (size_t)f * Y.stride, w, h, nx, ny, X0, Y0, u0, v0, nullptr);
             } else {
                 // lane l owns output columns 2l and 2l+1 (one 16-bit store per row)
                 uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + 2 * lane;
@@ -1440,6 +1482,17 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
     }
 }
 
+// persistent grid of the TMA kernel (every instantiation has the same
+// shared-memory and register footprint): SMs x resident CTAs
+long long tma_grid() {
+    static long long g = 0;
+    if (!g) {
+        ensure_smem(compose_tma_kernel<true, true, false>, sizeof(SmemT));
+        g = (long long)sm_count() * std::max(blocks_per_sm(compose_tma_kernel<true, true, false>, NT, sizeof(SmemT)), 1);
+    }
+    return g;
+}
+
 typedef PFN_cuTensorMapEncodeTiled_v12000 EncodeFn;
 
 EncodeFn get_encode() {
@@ -1472,9 +1525,10 @@ bool tma_ok(const PlaneBatch& p) {
            (p.stride % 16) == 0 && p.stride == (size_t)p.w * p.h;
 }
 
-template <bool L, bool C>
+template <bool L, bool C, bool RGBO = false>
 bool launch_tma(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
-                CropGeom g, Tables T, uint8_t* oy, uint8_t* ocb, uint8_t* ocr, cudaStream_t st) {
+                CropGeom g, Tables T, uint8_t* oy, uint8_t* ocb, uint8_t* ocr, cudaStream_t st,
+                uint8_t* scr = nullptr) {
     if ((L && !tma_ok(y)) || (C && (!tma_ok(cb) || !tma_ok(cr)))) return false;
     CUtensorMap my, mb, mr;
     memset(&my, 0, sizeof my);
@@ -1489,11 +1543,10 @@ bool launch_tma(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pla
     tile_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plan, frames, tx, ty, W, H, y.w, y.h,
                                                                     cb.w, cb.h, g, T, L ? 1 : 0, C ? 1 : 0);
     const size_t smem = sizeof(SmemT);
-    ensure_smem(compose_tma_kernel<L, C>, smem);
-    const int sms = sm_count(), per = blocks_per_sm(compose_tma_kernel<L, C>, NT, smem);
-    const long long grid = std::min<long long>(total, (long long)sms * std::max(per, 1));
-    compose_tma_kernel<L, C><<<(unsigned)grid, NT, smem, st>>>(y, cb, cr, plan, g, T, tx, ty, frames, my, mb, mr,
-                                                               oy, ocb, ocr);
+    ensure_smem(compose_tma_kernel<L, C, RGBO>, smem);
+    const long long grid = std::min<long long>(total, tma_grid());
+    compose_tma_kernel<L, C, RGBO><<<(unsigned)grid, NT, smem, st>>>(y, cb, cr, plan, g, T, tx, ty, frames, my, mb,
+                                                                     mr, oy, ocb, ocr, scr);
     return true;
 }
 
@@ -1536,16 +1589,26 @@ size_t table_bytes(int w, int h, int cw, int ch, int frames) {
            sizeof(TileParams) * ntiles + 512;
 }
 
+// RGB output (Y/Cb/Cr -> RGB fused into K8's store) is possible for 4:4:4
+// chroma on the TMA path with crop margins of at least one pixel
+bool rgb_ok(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, int frames, double crop_ratio) {
+    const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
+    return frames <= 65535 && cb.w == y.w && cb.h == y.h && g.mx >= 1 && g.my >= 1 && tma_ok(y) && tma_ok(cb) &&
+           tma_ok(cr);
+}
+
 void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
                  double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr, cudaStream_t st,
-                 void* scratch = nullptr, size_t scratch_bytes = 0) {
+                 void* scratch = nullptr, size_t scratch_bytes = 0, uint8_t* out_rgb = nullptr) {
     if (frames <= 0) return;
     const CropGeom g = crop_geom(y.w, y.h, crop_ratio);
-    const bool chroma = cb.base && cr.base && out_cb && out_cr;
+    const bool chroma = (cb.base && cr.base && out_cb && out_cr) || out_rgb;
     const int w = y.w, h = y.h, cw = chroma ? cb.w : 0, ch = chroma ? cb.h : 0;
     // per-launch tables: the caller's scratch, else a stream-ordered allocation
     const size_t nrow = (size_t)frames * h, ncrow = (size_t)frames * ch;
-    const size_t bytes = table_bytes(w, h, cw, ch, frames);
+    const size_t tbytes = table_bytes(w, h, cw, ch, frames);
+    // RGB output: + the per-CTA Cb / Cr tiles (2 buffers x 2 planes x TTH x TW)
+    const size_t bytes = tbytes + (out_rgb ? (size_t)tma_grid() * 4 * TTH * TW + 256 : 0);
     char* buf = nullptr;
     const bool own = !(scratch && scratch_bytes >= bytes);
     if (!own) buf = static_cast<char*>(scratch);
@@ -1580,7 +1643,10 @@ void run_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* pl
         compose_prep_kernel<<<grid, 128, 0, st>>>(plan + f0, w, h, cw, ch, g, t);
     }
     const bool frames_ok = frames <= 65535;
-    if (chroma && cb.w == y.w && cb.h == y.h) {
+    if (out_rgb) {  // the caller checked rgb_ok
+        uint8_t* scr = reinterpret_cast<uint8_t*>(((uintptr_t)(buf + tbytes) + 255) & ~uintptr_t(255));
+        launch_tma<true, true, true>(y, cb, cr, plan, frames, g, T, out_rgb, nullptr, nullptr, st, scr);
+    } else if (chroma && cb.w == y.w && cb.h == y.h) {
         if (!(frames_ok && launch_tma<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st)))
             launch_tiles<true, true>(y, cb, cr, plan, frames, g, T, out_y, out_cb, out_cr, st);
     } else {
@@ -1602,6 +1668,13 @@ void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan*
 }
 
 size_t compose_scratch_bytes(int w, int h, int cw, int ch, int frames) { return table_bytes(w, h, cw, ch, frames); }
+
+bool launch_compose_rgb(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                        double crop_ratio, uint8_t* out_rgb, cudaStream_t st) {
+    if (!rgb_ok(y, cb, cr, frames, crop_ratio)) return false;
+    run_compose(y, cb, cr, plan, frames, crop_ratio, nullptr, nullptr, nullptr, st, nullptr, 0, out_rgb);
+    return true;
+}
 
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st) {

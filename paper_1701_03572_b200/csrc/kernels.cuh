@@ -181,6 +181,11 @@ void launch_compose(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan*
                     double crop_ratio, uint8_t* out_y, uint8_t* out_cb, uint8_t* out_cr,
                     cudaStream_t st, void* scratch = nullptr, size_t scratch_bytes = 0);
 size_t compose_scratch_bytes(int w, int h, int cw, int ch, int frames);
+// K8 with interleaved RGB output (the Y/Cb/Cr -> RGB conversion fused into
+// the store; 4:4:4 chroma, crop margins >= 1 px, 16-byte aligned planes);
+// false (nothing launched) when not applicable
+bool launch_compose_rgb(PlaneBatch y, PlaneBatch cb, PlaneBatch cr, const FramePlan* plan, int frames,
+                        double crop_ratio, uint8_t* out_rgb, cudaStream_t st);
 void launch_warp_only(const uint8_t* src, int w, int h, const FramePlan* plan, uint8_t* out,
                       cudaStream_t st);
 void launch_crop_only(const uint8_t* src, int w, int h, double crop_ratio, uint8_t* out,
@@ -203,7 +208,8 @@ void launch_prefix(const stabgpu_delta* d, long long n, double4* cum, cudaStream
 void launch_plan_from_corrections(const stabgpu_transform* corr, long long n, FramePlan* plan,
                                   PlanGeom geo, cudaStream_t st);
 // ---- colour conversion + evaluation (k_eval.cu) ----
-void launch_rgb_to_ycbcr(const uint8_t* rgb, size_t npx, uint8_t* y, uint8_t* cb, uint8_t* cr, cudaStream_t st);
+void launch_rgb_to_ycbcr(const uint8_t* rgb, size_t npx, uint8_t* y, uint8_t* cb, uint8_t* cr, cudaStream_t st,
+                         bool zero_copy = false);
 void launch_ycbcr_to_rgb(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, size_t npx, uint8_t* rgb,
                          cudaStream_t st);
 void launch_interframe_sse(const uint8_t* frames, int n, int w, int h, int mx, int my, unsigned long long* sse,

@@ -1319,13 +1319,23 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
     return STABGPU_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
 // Host buffers: chunked upload -> motion -> incremental plan -> compose ->
 // download, with the copies on two copy streams so upload, compute and
 // download of different chunks overlap (PCIe is full duplex).
-int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb,
-                               const uint8_t* hcr, int n, int w, int h, int cw, int ch,
-                               const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
-                               uint8_t* hocr, stabgpu_frame_record* records) {
+// RGB mode (hrgb / hout_rgb, interleaved 8-bit, 4:4:4): media_io's load /
+// save conversions around run_offline.  Each uploaded chunk is converted
+// (RGB -> Y/Cb/Cr) on the input copy stream as it lands — or, opt-in
+// (STABGPU_RGB_ZEROCOPY), read and converted by the kernel itself straight
+// from pinned host memory over PCIe — and K8 writes interleaved RGB
+// (Y/Cb/Cr -> RGB fused into the compose store) when the geometry allows,
+// else composes planes and converts.
+int sequence_host(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const uint8_t* hcr, const uint8_t* hrgb,
+                  int n, int w, int h, int cw, int ch, const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
+                  uint8_t* hocr, uint8_t* hout_rgb, stabgpu_frame_record* records) {
     const stabgpu_config cfg = *cfgp;
     TRY(validate_all(cfg));
     TRY(validate_frame(w, h));
@@ -1333,10 +1343,36 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
     cudaSetDevice(ctx->device);
     begin_timing(ctx);
     cudaStream_t st = ctx->stream;
-    const bool chroma = hcb && hcr && hocb && hocr;
+    const bool rgb = hrgb != nullptr;
+    if (rgb) {
+        cw = w;
+        ch = h;
+    }
+    const bool chroma = rgb || (hcb && hcr && hocb && hocr);
     const size_t fl = (size_t)w * h, fc = chroma ? (size_t)cw * ch : 0;
     DBUF(uint8_t, dy, "io_y", fl * n);
     DBUF(uint8_t, doy, "io_oy", fl * n);
+    // RGB: zero-copy upload when the host buffer is pinned (device-accessible)
+    const uint8_t* zc_rgb = nullptr;
+    uint8_t *drgb_in = nullptr, *drgb_out = nullptr;
+    if (rgb) {
+        cudaPointerAttributes pa;
+        // Zero-copy is opt-in: alone it streams at 40-48 GB/s, but inside the
+        // overlapped pipeline (downloads and compute running) it measured 4.1k
+        // frames/s e2e at C3 against 6.7k for the copy-engine staging
+        // (profiles/r2_rgb_probe.log), so the staged upload is the default.
+        const bool zc_on = getenv("STABGPU_RGB_ZEROCOPY") != nullptr;
+        if (zc_on && cudaPointerGetAttributes(&pa, hrgb) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer)
+            zc_rgb = static_cast<const uint8_t*>(pa.devicePointer);
+        cudaGetLastError();
+        if (!zc_rgb) {
+            DBUF(uint8_t, a, "io_rgb_in", 3 * fl * n);
+            drgb_in = a;
+        }
+        DBUF(uint8_t, b, "io_rgb_out", 3 * fl * n);
+        drgb_out = b;
+    }
     uint8_t *dcb = nullptr, *dcr = nullptr, *docb = nullptr, *docr = nullptr;
     if (chroma) {
         DBUF(uint8_t, a, "io_cb", fc * n);
@@ -1364,10 +1400,19 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
     // uploads, all queued up front on the input copy stream
     for (int k = 0; k < nchunks && !rc; ++k) {
         const size_t f0 = (size_t)k * C, nf = std::min<size_t>(C, n - f0);
-        if (cudaMemcpyAsync(dy + f0 * fl, hy + f0 * fl, nf * fl, cudaMemcpyHostToDevice, ctx->cin) ||
-            (chroma && (cudaMemcpyAsync(dcb + f0 * fc, hcb + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin) ||
-                        cudaMemcpyAsync(dcr + f0 * fc, hcr + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin))))
+        if (rgb) {
+            const uint8_t* src = zc_rgb ? zc_rgb + 3 * f0 * fl : drgb_in + 3 * f0 * fl;
+            if (!zc_rgb && cudaMemcpyAsync(drgb_in + 3 * f0 * fl, hrgb + 3 * f0 * fl, 3 * nf * fl,
+                                           cudaMemcpyHostToDevice, ctx->cin))
+                rc = set_err(STABGPU_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+            launch_rgb_to_ycbcr(src, nf * fl, dy + f0 * fl, dcb + f0 * fl, dcr + f0 * fl, ctx->cin, zc_rgb != nullptr);
+            ++ctx->stats.launches;
+        } else if (cudaMemcpyAsync(dy + f0 * fl, hy + f0 * fl, nf * fl, cudaMemcpyHostToDevice, ctx->cin) ||
+                   (chroma &&
+                    (cudaMemcpyAsync(dcb + f0 * fc, hcb + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin) ||
+                     cudaMemcpyAsync(dcr + f0 * fc, hcr + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin)))) {
             rc = set_err(STABGPU_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+        }
         cudaEventRecord(in_ev[k], ctx->cin);
     }
     long long seg_done = 0;   // segments whose motion is computed
@@ -1397,16 +1442,38 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
             launch_plan_smooth(cum, known, complete, composed, ready - composed, r, rec, plan,
                                PlanGeom{w, h, chroma ? cw : 0, chroma ? ch : 0, cfg.crop_ratio}, st);
             ++ctx->stats.launches;
-            rc = compose_range(ctx, dy, dcb, dcr, composed, ready - composed, w, h, cw, ch, plan,
-                               cfg.crop_ratio, doy, docb, docr);
+            const size_t f0 = composed, nf = ready - composed;
+            if (rgb) {
+                Timer tm(ctx, 4);
+                PlaneBatch yb{dy + f0 * fl, fl, w, h}, bb{dcb + f0 * fl, fl, w, h}, cb2{dcr + f0 * fl, fl, w, h};
+                if (!launch_compose_rgb(yb, bb, cb2, plan + f0, (int)nf, cfg.crop_ratio, drgb_out + 3 * f0 * fl, st)) {
+                    // geometry without the fused store: planes, then the conversion
+                    launch_compose(yb, bb, cb2, plan + f0, (int)nf, cfg.crop_ratio, doy + f0 * fl, docb + f0 * fl,
+                                   docr + f0 * fl, st);
+                    launch_ycbcr_to_rgb(doy + f0 * fl, docb + f0 * fl, docr + f0 * fl, nf * fl,
+                                        drgb_out + 3 * f0 * fl, st);
+                    ++ctx->stats.launches;
+                }
+                ++ctx->stats.launches;
+                rc = check_launch("compose");
+            } else {
+                rc = compose_range(ctx, dy, dcb, dcr, composed, ready - composed, w, h, cw, ch, plan,
+                                   cfg.crop_ratio, doy, docb, docr);
+            }
             if (rc) break;
             cudaEventRecord(out_ev[k], st);
             cudaStreamWaitEvent(ctx->cout, out_ev[k], 0);
-            const size_t f0 = composed, nf = ready - composed;
-            if (cudaMemcpyAsync(hoy + f0 * fl, doy + f0 * fl, nf * fl, cudaMemcpyDeviceToHost, ctx->cout) ||
-                (chroma && (cudaMemcpyAsync(hocb + f0 * fc, docb + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout) ||
-                            cudaMemcpyAsync(hocr + f0 * fc, docr + f0 * fc, nf * fc, cudaMemcpyDeviceToHost, ctx->cout))))
+            if (rgb) {
+                if (cudaMemcpyAsync(hout_rgb + 3 * f0 * fl, drgb_out + 3 * f0 * fl, 3 * nf * fl,
+                                    cudaMemcpyDeviceToHost, ctx->cout))
+                    rc = set_err(STABGPU_CUDA, "download failed: %s", cudaGetErrorString(cudaGetLastError()));
+            } else if (cudaMemcpyAsync(hoy + f0 * fl, doy + f0 * fl, nf * fl, cudaMemcpyDeviceToHost, ctx->cout) ||
+                       (chroma && (cudaMemcpyAsync(hocb + f0 * fc, docb + f0 * fc, nf * fc, cudaMemcpyDeviceToHost,
+                                                   ctx->cout) ||
+                                   cudaMemcpyAsync(hocr + f0 * fc, docr + f0 * fc, nf * fc, cudaMemcpyDeviceToHost,
+                                                   ctx->cout)))) {
                 rc = set_err(STABGPU_CUDA, "download failed: %s", cudaGetErrorString(cudaGetLastError()));
+            }
             composed = ready;
         }
     }
@@ -1422,6 +1489,17 @@ int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_
         CUDA_TRY(cudaMemcpyAsync(records, rec, sizeof(stabgpu_frame_record) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     return check_launch("stabilize_sequence");
+}
+
+}  // namespace
+
+extern "C" {
+
+int stabgpu_stabilize_sequence(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb,
+                               const uint8_t* hcr, int n, int w, int h, int cw, int ch,
+                               const stabgpu_config* cfgp, uint8_t* hoy, uint8_t* hocb,
+                               uint8_t* hocr, stabgpu_frame_record* records) {
+    return sequence_host(ctx, hy, hcb, hcr, nullptr, n, w, h, cw, ch, cfgp, hoy, hocb, hocr, nullptr, records);
 }
 
 // ---- multi-GPU split ------------------------------------------------------
@@ -2481,40 +2559,9 @@ int stabgpu_ycbcr_to_rgb(stabgpu_ctx* ctx, const uint8_t* y, const uint8_t* cb, 
 int stabgpu_stabilize_sequence_rgb(stabgpu_ctx* ctx, const uint8_t* host_rgb, int n, int w, int h,
                                    const stabgpu_config* cfg, uint8_t* host_out_rgb,
                                    stabgpu_frame_record* records) {
-    TRY(validate_all(*cfg));
-    TRY(validate_frame(w, h));
-    if (n < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
-    cudaSetDevice(ctx->device);
-    cudaStream_t st = ctx->stream;
-    const size_t fl = (size_t)w * h;
-    DBUF(uint8_t, rgb, "rgb_io", 3 * fl * n);
-    DBUF(uint8_t, y, "rgb_y", fl * n);
-    DBUF(uint8_t, cb, "rgb_cb", fl * n);
-    DBUF(uint8_t, cr, "rgb_cr", fl * n);
-    DBUF(uint8_t, oy, "rgb_oy", fl * n);
-    DBUF(uint8_t, ocb, "rgb_ocb", fl * n);
-    DBUF(uint8_t, ocr, "rgb_ocr", fl * n);
-    // chunked upload + conversion (copy engine and SMs overlap across chunks)
-    const int C = 64;
-    std::vector<cudaEvent_t> ev((n + C - 1) / C);
-    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (int k = 0, f0 = 0; f0 < n; ++k, f0 += C) {
-        const size_t nf = std::min(C, n - f0);
-        CUDA_TRY(cudaMemcpyAsync(rgb + 3 * fl * f0, host_rgb + 3 * fl * f0, 3 * fl * nf, cudaMemcpyHostToDevice,
-                                 ctx->cin));
-        cudaEventRecord(ev[k], ctx->cin);
-        cudaStreamWaitEvent(st, ev[k], 0);
-        launch_rgb_to_ycbcr(rgb + 3 * fl * f0, fl * nf, y + fl * f0, cb + fl * f0, cr + fl * f0, st);
-    }
-    for (auto& e : ev) cudaEventDestroy(e);
-    TRY(check_launch("rgb_to_ycbcr"));
-    TRY(stabgpu_stabilize_sequence_device(ctx, y, cb, cr, n, w, h, w, h, cfg, oy, ocb, ocr, records));
-    launch_ycbcr_to_rgb(oy, ocb, ocr, fl * n, rgb, st);
-    TRY(check_launch("ycbcr_to_rgb"));
-    CUDA_TRY(cudaMemcpyAsync(host_out_rgb, rgb, 3 * fl * n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    ctx->stats.launches += 2;
-    return STABGPU_OK;
+    if (!host_rgb || !host_out_rgb) return set_err(STABGPU_INVALID_INPUT, "rgb: null buffer");
+    return sequence_host(ctx, nullptr, nullptr, nullptr, host_rgb, n, w, h, w, h, cfg, nullptr, nullptr, nullptr,
+                         host_out_rgb, records);
 }
 
 int stabgpu_interframe_sse(stabgpu_ctx* ctx, const uint8_t* y, int n, int w, int h, double crop,

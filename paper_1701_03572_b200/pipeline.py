@@ -79,6 +79,13 @@ def stabilize_sequence_host_buffers(ctx, y, cb, cr, n, w, h, cw, ch, cfg_c, oy, 
                                             C.byref(cfg_c), _vp(oy), _vp(ocb), _vp(ocr), _vp(rec)))
 
 
+def stabilize_sequence_rgb_host_buffers(ctx, rgb, n, w, h, cfg_c, out_rgb, rec):
+    """Raw C-ABI call: interleaved RGB host frames in and out (media_io load /
+    save conversions on the device around run_offline)."""
+    check(load().stabgpu_stabilize_sequence_rgb(ctx.handle, _vp(rgb), n, w, h, C.byref(cfg_c), _vp(out_rgb),
+                                                _vp(rec)))
+
+
 def stabilize_sequence_device(y, cfg: StabConfig, cb=None, cr=None, out_y=None, out_cb=None,
                               out_cr=None, device: int | None = None, records: bool = True):
     """Device-resident planes (torch CUDA tensors) in and out."""

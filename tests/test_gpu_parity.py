@@ -584,27 +584,76 @@ def test_colour_conversions_exhaustive_gpu():
     assert np.array_equal(g.cpu().numpy(), o2(trip[..., 0], trip[..., 1], trip[..., 2]))
 
 
-def test_stabilize_rgb_equals_planes():
+@pytest.mark.parametrize("pinned,crop,zero_copy", [(False, 0.04, False), (True, 0.04, False), (True, 0.04, True),
+                                                    (True, 0.0, True), (False, 0.001, False)])
+def test_stabilize_rgb_equals_planes(pinned, crop, zero_copy, monkeypatch):
     """RGB in / RGB out (media_io load -> run_offline -> save) equals the
-    plane path with the reference conversions around it."""
-    from paper_1701_03572_b200 import _abi as A
+    plane path with the reference conversions around it: the staged upload
+    (copy engine + conversion per chunk) and the zero-copy one (pinned input
+    read by the conversion kernel over PCIe), the RGB store fused into K8
+    (crop margins >= 1 px) and the planes + conversion fallback (crop 0, or a
+    margin rounding to 0 px on one axis)."""
+    import dataclasses
+
+    if zero_copy:
+        monkeypatch.setenv("STABGPU_RGB_ZEROCOPY", "1")
+    else:
+        monkeypatch.delenv("STABGPU_RGB_ZEROCOPY", raising=False)
+
+    import torch
+
     from paper_1701_03572_b200._lib import check, context, load
     import ctypes as C
     o1, o2, _ = _oracle.colour_and_psnr(_oracle.ORACLE, "orc_")
     y, cb, cr = _data.video(frames=23, objects=1, color=True)
     rgb = o2(y, cb, cr)  # a plausible RGB source
-    cfg = _data.small_cfg(_data.MODES["similarity"], ransac=100)
+    cfg = dataclasses.replace(_data.small_cfg(_data.MODES["similarity"], ransac=100), crop_ratio=crop)
     py, pb, pr = o1(rgb)
     sy, sb, sr, srec = pipeline.stabilize_sequence(py, cfg, pb, pr)
     want = o2(sy, sb, sr)
-    out = np.empty_like(rgb)
+    src = torch.from_numpy(rgb).pin_memory() if pinned else torch.from_numpy(rgb)
+    out = torch.empty_like(src).pin_memory() if pinned else torch.empty_like(src)
     rec = np.zeros(len(rgb), pipeline.RECORD_DT)
     c = cfg.c()
     n, h, w = y.shape
-    check(load().stabgpu_stabilize_sequence_rgb(context(0).handle, C.c_void_p(rgb.ctypes.data), n, w, h, C.byref(c),
-                                                C.c_void_p(out.ctypes.data), C.c_void_p(rec.ctypes.data)))
-    assert np.array_equal(out, want)
+    check(load().stabgpu_stabilize_sequence_rgb(context(0).handle, C.c_void_p(src.data_ptr()), n, w, h, C.byref(c),
+                                                C.c_void_p(out.data_ptr()), C.c_void_p(rec.ctypes.data)))
+    assert np.array_equal(out.numpy(), want)
     assert rec.tobytes() == srec.tobytes()
+
+
+def test_stabilize_rgb_config_c3():
+    """BASELINE C3 (1920x1080 RGB, first 30 frames) through the RGB entry
+    point with pinned buffers (fused upload + fused RGB store) against the
+    reference: its own BT.601 load conversion, run_offline semantics, and its
+    yuv_to_rgb at save (oracle/_ref when built, else the C restatement)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1701_03572_b200._lib import check, context, load
+    from paper_1701_03572_b200.synth import CONFIGS, Video
+
+    cfg = CONFIGS["c3"]
+    y, cb, cr = Video(cfg.video).render(0, 30)
+    ref = _oracle.reference() if _oracle.have_reference() else _oracle.oracle()
+    lib, pre = (_oracle.REF, "ref_") if _oracle.have_reference() else (_oracle.ORACLE, "orc_")
+    _, to_rgb, _ = _oracle.colour_and_psnr(lib, pre)
+    rgb = to_rgb(y, cb, cr)  # an RGB source whose conversion gives these planes back (checked below)
+    r2y, _, _ = _oracle.colour_and_psnr(lib, pre)
+    py, pb, pr = r2y(rgb)
+    kw = {"threads": 8} if ref.prefix == "ref_" else {}
+    oy, ob, orr, orec = ref.stabilize_sequence(py, cfg.stab, pb, pr, **kw)
+    want = to_rgb(oy, ob, orr)
+    src = torch.from_numpy(rgb).pin_memory()
+    out = torch.empty_like(src).pin_memory()
+    rec = np.zeros(len(rgb), pipeline.RECORD_DT)
+    c = cfg.stab.c()
+    n, h, w = py.shape
+    check(load().stabgpu_stabilize_sequence_rgb(context(0).handle, C.c_void_p(src.data_ptr()), n, w, h, C.byref(c),
+                                                C.c_void_p(out.data_ptr()), C.c_void_p(rec.ctypes.data)))
+    assert np.array_equal(rec["frame_kind"], orec["frame_kind"])
+    assert np.array_equal(out.numpy(), want)
 
 
 @pytest.mark.parametrize("crop", [0.0, 0.04])
