@@ -249,6 +249,14 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
 constexpr int SM_MARGIN = 3;
 constexpr int SM_PITCH = 48;  // bytes per staged row (>= 32 + 1 + 2 * margin + 3)
 constexpr int SM_ROWS = 40;   // >= 32 + 2 * margin
+// Per-warp shared layout (doubles): the system record first (2x2 system,
+// level origin, 1/det, S_uv, step count, level bounds, thresholds), then the
+// staged window, then the template gradients.  With one warp per CTA (the
+// chain kernel) every record address is a constant offset of the shared
+// window: no address arithmetic in the iteration loop.
+constexpr int SYS_D = 24;
+constexpr int STG_D = SM_ROWS * SM_PITCH / 8;
+__host__ __device__ constexpr int lk_per_warp(int side) { return SYS_D + STG_D + 2 * (side * side + 1); }
 
 // Copies image block [x0, x0+sw) x [y0, y0+sh) (clamped at the border) to a
 // per-warp shared tile (row pitch SM_PITCH) and returns the tile column of
@@ -501,7 +509,10 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             break;
         }
     const int min_count = max(25, side * side / 4);
-    const double r2 = (double)r * r, eps2 = dmul(cfg.epsilon, cfg.epsilon);
+    if (lane == 0) {  // per-call thresholds in the shared system record (sys[21..22])
+        sys[21] = (double)r * r;
+        sys[22] = dmul(cfg.epsilon, cfg.epsilon);
+    }
     const int nt = f1 >= 0 ? 2 : 1;
     // per-tracker guesses in scalars (no local-memory arrays)
     double gx0 = 0.0, gy0 = 0.0, gx1 = 0.0, gy1 = 0.0;
@@ -566,6 +577,8 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 sys[6] = plx;
                 sys[7] = ply;
                 sys[8] = ddiv(1.0, det);  // RN(1/det), for div_rn_recip
+                sys[19] = (double)pi.w - 1.0;  // inside() bounds of the level (every frame has its dims)
+                sys[20] = (double)pi.h - 1.0;
             }
             __syncwarp();
         }
@@ -587,7 +600,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             int ccx = INT_MIN / 2, ccy = INT_MIN / 2;  // window cell whose S_uv are in sys[10..17]
             for (int k = 0; k < cfg.max_iterations; ++k) {
                 const double qx = dadd(dadd(ldsv(sys + 6), gfx), vx), qy = dadd(dadd(ldsv(sys + 7), gfy), vy);
-                if (!inside(ci, qx, qy)) {
+                if (!(qx >= 0.0 && qy >= 0.0 && qx <= ldsv(sys + 19) && qy <= ldsv(sys + 20))) {  // inside()
                     diverged = true;
                     break;
                 }
@@ -623,11 +636,11 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                 const double dy = div_rn_recip(dsub(dmul(sxx, by), dmul(sxy, bx)), sdet, rdet);
                 vx = dadd(vx, dx);
                 vy = dadd(vy, dy);
-                if (dadd(dmul(vx, vx), dmul(vy, vy)) > r2) {
+                if (dadd(dmul(vx, vx), dmul(vy, vy)) > ldsv(sys + 21)) {
                     diverged = true;
                     break;
                 }
-                if (dadd(dmul(dx, dx), dmul(dy, dy)) < eps2) break;
+                if (dadd(dmul(dx, dx), dmul(dy, dy)) < ldsv(sys + 22)) break;
             }
             __syncwarp();
             if (j) it1 += nit;
@@ -674,13 +687,12 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
 }
 
 __device__ __forceinline__ bool track_warp_fast(const DevPyramid& P, int fprev, int fcur, double px, double py,
-                                                const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg,
+                                                const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, double* sys,
                                                 double& ox, double& oy, unsigned& iters, unsigned& builds) {
     bool ok0, ok1;
     double2 o0, o1;
     unsigned it0 = 0, it1 = 0;
-    track_dual(P, fprev, px, py, fcur, -1, cfg, tg, stg, reinterpret_cast<double*>(stg + SM_ROWS * SM_PITCH), ok0, ok1,
-               o0, o1, it0, it1, builds);
+    track_dual(P, fprev, px, py, fcur, -1, cfg, tg, stg, sys, ok0, ok1, o0, o1, it0, it1, builds);
     iters += it0;
     if (ok0) {
         ox = o0.x;
@@ -695,9 +707,9 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
                                                       unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* tg = lsm + (size_t)warp * smem_per_warp;
-    const int side = 2 * cfg.window_radius + 1;
-    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * (side * side + 1));
+    double* sys = lsm + (size_t)warp * smem_per_warp;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(sys + SYS_D);
+    double* tg = sys + SYS_D + STG_D;
     const unsigned total = (unsigned)s.nseg * (unsigned)s.max_pts;
     while (true) {
         unsigned item = 0;
@@ -718,7 +730,7 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
         double ax = p.x, ay = p.y, ox = 0.0, oy = 0.0;
         bool keep = true;
         for (int pass = 0; pass < passes && keep; ++pass) {
-            keep = track_warp_fast(s.pyr, fa, fb, ax, ay, cfg, tg, stg, ox, oy, iters, builds);
+            keep = track_warp_fast(s.pyr, fa, fb, ax, ay, cfg, tg, stg, sys, ox, oy, iters, builds);
             if (keep && pass == 0 && s.mode != 2) {
                 fx = ox;
                 fy = oy;
@@ -764,9 +776,10 @@ __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain 
                                                                        unsigned* __restrict__ work, int smem_per_warp) {
     extern __shared__ __align__(16) double lsm[];
     const int warp = CH_WPC == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* tg = lsm + (size_t)warp * smem_per_warp;
-    const int side = 2 * cfg.window_radius + 1;
-    uint8_t* stg = reinterpret_cast<uint8_t*>(tg + 2 * (side * side + 1));
+    double* sys = lsm + (size_t)warp * smem_per_warp;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(sys + SYS_D);
+    double* tg = sys + SYS_D + STG_D;
+    int* nst_sh = reinterpret_cast<int*>(sys + 18);  // the segment's step count (MS)
     const unsigned total = (unsigned)c.nseg * (unsigned)c.max_pts;
     const size_t plane = (size_t)c.nseg * c.max_pts;
     const double thr2 = dmul(cfg.fb_threshold, cfg.fb_threshold);
@@ -782,7 +795,7 @@ __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain 
             // steps this segment may take, parked in shared memory (registers are full)
             const int nst = min(c.R, seg_end(seg, c.F, c.nsps, c.nframes) - 1 - b0);
             if (nst <= 0 || k >= c.npts[seg]) continue;
-            if (lane == 0) *reinterpret_cast<int*>(stg + SM_ROWS * SM_PITCH + 18 * 8) = nst;
+            if (lane == 0) *nst_sh = nst;
             __syncwarp();
         } else {
             b0 = seg * c.R;
@@ -801,8 +814,7 @@ __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain 
         double2 q = p;
         while (true) {
             unsigned it0 = 0, it1 = 0;
-            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, reinterpret_cast<double*>(stg + SM_ROWS * SM_PITCH),
-                       ok0, ok1, o0, o1, it0, it1, blds);
+            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, sys, ok0, ok1, o0, o1, it0, it1, blds);
             its += it0;
             if (t == 0) {
                 if (!ok0) break;
@@ -830,7 +842,7 @@ __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain 
             q = f;
             f0 = ft - 1;
             if (MS)
-                f1 = t < *reinterpret_cast<volatile int*>(stg + SM_ROWS * SM_PITCH + 18 * 8) ? ft + 1 : -1;
+                f1 = t < *reinterpret_cast<volatile int*>(nst_sh) ? ft + 1 : -1;
             else
                 f1 = (t < c.R && ft + 1 < c.nframes) ? ft + 1 : -1;
         }
@@ -943,7 +955,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     const int r = cfg.window_radius, side = 2 * r + 1, es = 2 * r + 3;
     if (r <= 15) {
         // doubles: template gradients {gx, gy}[side][32] + the staged window (bytes)
-        const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;
+        const int per_warp = lk_per_warp(side);
         const int wpc = 4;
         const size_t smem = (size_t)wpc * per_warp * sizeof(double);
         ensure_smem(lk_fast_kernel, smem);
@@ -967,7 +979,7 @@ void launch_lk(const LkStep& s, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
 void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st) {
     if (c.nseg <= 0 || c.max_pts <= 0) return;
     const int side = 2 * cfg.window_radius + 1;
-    const int per_warp = 2 * (side * side + 1) + SM_ROWS * SM_PITCH / 8 + 20;  // doubles (+ system, S_uv, step count; even: 16 B aligned)
+    const int per_warp = lk_per_warp(side);  // doubles (even: 16 B aligned)
     const int wpc = CH_WPC;
     const size_t smem = (size_t)wpc * per_warp * sizeof(double);
     const bool multi = c.nsps != c.nseg;  // several streams in the chunk
