@@ -622,13 +622,16 @@ static_assert((TTH + NW - 1) / NW <= 32, "the crop loop shuffles one row table e
 constexpr int TWTH = 132;          // its W tile rows (<= 130 used)
 constexpr int QW = 64;  // per-warp exact-path queue
 
+constexpr int PROWS = 18, PWP = 64;  // private W rows per warp (<= 17 used) and their pitch
+
 struct SmemT {
     alignas(128) uint8_t box[2][3][BH * BW];  // TMA source footprints, double-buffered
-    uint8_t wt[2][TWTH][WTW];                 // warped luma of the tile, double-buffered
-    TileParams tp[3];  // tile k uses tp[k % 3]; tile k+2's are in flight (cp.async)
-    unsigned long long mbar[2];
-    unsigned wq[NT / 32][QW];  // per-warp queues of pixels for the exact path
+    uint8_t wt[2][TWTH][WTW];  // warped luma of the tile (shared mode) or the warps' private W rows
+    unsigned long long mbar[2];  // TMA transaction barrier of each buffer
+    unsigned done[2];            // warps finished with the buffer's tile
+    unsigned wq[NT / 32][QW];    // per-warp queues of pixels for the exact path
 };
+static_assert(NW * PROWS * PWP <= TWTH * WTW, "private W rows fit the tile buffer");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -696,6 +699,10 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
         // (one pixel of slack for the 32.32 conversion), so the lean row loop
         // needs no per-pixel bounds or near-integer decisions (see inner32)
         if (tp.lfit && nu <= TW && xmn >= 2 && xmx <= w - 4 && ymn >= 2 && ymx <= h - 4) tp.pad0 |= 1;
+        // private W rows (each warp computes the W rows its crop rows read, no
+        // CTA barrier): interior tile whose crop taps are x0, x0 + 1 and whose
+        // bottom row never clamps (crop_rows2)
+        if ((tp.pad0 & 1) && !identity && g.my >= 1 && T.cx0[X0 + nx - 1] + 1 <= w - 1) tp.pad0 |= 4;
     }
     if (chroma) {
         int xmn = INT_MAX, xmx = INT_MIN, ymn = INT_MAX, ymx = INT_MIN;
@@ -810,12 +817,13 @@ __device__ __noinline__ uint32_t chroma_exact_tile(const FramePlan* __restrict__
 }
 
 // crop_resize pixel (image_ops.cpp:151-157) of output (X, Y) from the W tile
-__device__ __noinline__ uint32_t crop_exact_tile(const uint8_t* wt, const Tables T, int X, int Y, int u0, int v0,
+// (wl: the W rows indexed by absolute row, row pitch wp)
+__device__ __noinline__ uint32_t crop_exact_tile(const uint8_t* wl, int wp, const Tables T, int X, int Y, int u0,
                                                  int w, int h) {
     const int x0 = T.cx0[X], y0 = T.cy0[Y];
     const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
-    const double a = wt[(y0 - v0) * WTW + x0 - u0], b = wt[(y0 - v0) * WTW + x1 - u0];
-    const double cc = wt[(y1 - v0) * WTW + x0 - u0], d = wt[(y1 - v0) * WTW + x1 - u0];
+    const double a = wl[y0 * wp + x0 - u0], b = wl[y0 * wp + x1 - u0];
+    const double cc = wl[y1 * wp + x0 - u0], d = wl[y1 * wp + x1 - u0];
     const double top = dadd(a, dmul(T.cfx[X], dsub(b, a)));
     const double bot = dadd(cc, dmul(T.cfx[X], dsub(d, cc)));
     return round_u8(dadd(top, dmul(T.cfy[Y], dsub(bot, top))));
@@ -1040,24 +1048,26 @@ __device__ __forceinline__ const uint8_t* tap_ptr(const uint8_t* box, long long 
     return box + hi32(Y) * BW + hi32(X);
 }
 
-// W rows of an interior tile into wt (lane: columns 2l, 2l+1)
+// W rows r = rs, rs + RS, ... < re (tile rows, relative to v0) of an interior
+// tile; the k-th row of the call goes to out + k * OP (lane: columns 2l, 2l+1)
+template <int RS, int OP>
 __device__ __forceinline__ void w_rows_lean2(const uint8_t* box, int lbx, int lby, const long long* __restrict__ rxf,
-                                             const long long* __restrict__ ryf, uint8_t* wt, int nu, int nv, int u0,
-                                             int v0, long long cf, long long snf, const FramePlan* __restrict__ plan,
-                                             int f, int w, int h) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                             const long long* __restrict__ ryf, uint8_t* out, int rs, int re, int nu,
+                                             int u0, int v0, long long cf, long long snf,
+                                             const FramePlan* __restrict__ plan, int f, int w, int h) {
+    if (rs >= re) return;
+    const int lane = threadIdx.x & 31;
     const int c0 = 2 * lane;
-    const int r0 = min(warp, nv - 1);
     const long long ua = (long long)(u0 + min(c0, nu - 1));
-    long long XA = ((__ldg(rxf + r0) + ua * cf) >> 16) - ((long long)lbx << 32);
-    long long YA = ((__ldg(ryf + r0) - ua * snf) >> 16) - ((long long)lby << 32);
+    long long XA = ((__ldg(rxf + rs) + ua * cf) >> 16) - ((long long)lbx << 32);
+    long long YA = ((__ldg(ryf + rs) - ua * snf) >> 16) - ((long long)lby << 32);
     const bool vA = c0 < nu, vB = c0 + 1 < nu;
     const long long DX = vB ? (cf >> 16) : 0, DY = vB ? -(snf >> 16) : 0;
-    const long long RX = ((long long)NW * snf) >> 16, RY = ((long long)NW * cf) >> 16;
-    uint8_t* wr = wt + warp * WTW + c0;
+    const long long RX = ((long long)RS * snf) >> 16, RY = ((long long)RS * cf) >> 16;
+    uint8_t* wr = out + c0;
     uint32_t bad = 0, bit = 1;
 #pragma unroll 2
-    for (int r = warp; r < nv; r += NW, wr += NW * WTW, bit <<= 1, XA += RX, YA += RY) {
+    for (int r = rs; r < re; r += RS, wr += OP, bit <<= 1, XA += RX, YA += RY) {
         const long long XB = XA + DX, YB = YA + DY;
         bool b;
         const uint32_t v = blend2p(taps(tap_ptr(box, XA, YA)), taps(tap_ptr(box, XB, YB)),
@@ -1067,9 +1077,11 @@ __device__ __forceinline__ void w_rows_lean2(const uint8_t* box, int lbx, int lb
     }
     if (!vA) bad = 0;
     for (; bad; bad &= bad - 1) {  // this lane's undecided rows (both columns recomputed)
-        const int r = warp + NW * (__ffs(bad) - 1);
-        wt[r * WTW + c0] = (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0, v0 + r);
-        if (vB) wt[r * WTW + c0 + 1] = (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0 + 1, v0 + r);
+        const int k = __ffs(bad) - 1, r = rs + RS * k;
+        out[k * OP + c0] = (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0, v0 + r);
+        if (vB)
+            out[k * OP + c0 + 1] =
+                (uint8_t)w_exact_tile(plan, f, box, lbx, lby, 1, nullptr, w, h, u0 + c0 + 1, v0 + r);
     }
 }
 
@@ -1145,21 +1157,21 @@ __device__ __forceinline__ void store_rgb2(uint8_t* p, uint32_t yy, const uint8_
 // pass's output tile, pitch TW, Cr TTH * TW after Cb) and stored as
 // interleaved RGB (yuv_to_rgb, colour.cuh) into the RGB frame oy (pitch 3w):
 // Y/Cb/Cr -> RGB fused into the compose store.
-template <bool RGBO>
-__device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, uint8_t* oy, int w, int h, int nx,
-                                           int ny, int X0, int Y0, int u0, int v0, const uint8_t* csc) {
+// wl: the W rows indexed by absolute W row, row pitch WP; rows [rb, re) of
+// the tile (crop_rows_of)
+template <bool RGBO, int WP>
+__device__ __forceinline__ void crop_rows2(const uint8_t* wl, const Tables& T, uint8_t* oy, int w, int h, int nx,
+                                           int rb, int re, int X0, int Y0, int u0, const uint8_t* csc) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int per = (ny + NW - 1) / NW;
-    const int rb = warp * per, re = min(rb + per, ny);
+    const int lane = threadIdx.x & 31;
+    const int ny = re;  // rows past re are never read (myr clamps to re - 1)
     if (rb >= re) return;
     const int ca = X0 + min(2 * lane, nx - 1), cb = X0 + min(2 * lane + 1, nx - 1);
     const int xa = __ldg(T.cx0 + ca) - u0, xb = __ldg(T.cx0 + cb) - u0;
     const float2 fx2 = make_float2((float)__ldg(T.cfx + ca), (float)__ldg(T.cfx + cb));
     const bool vA = 2 * lane < nx, vB = 2 * lane + 1 < nx;
-    const uint8_t* wl = wt - v0 * WTW;  // indexed by absolute W row
     auto hl2 = [&](int row) {
-        const uint8_t* rp = wl + row * WTW;
+        const uint8_t* rp = wl + row * WP;
         const float2 fa = make_float2(b256(rp[xa]), b256(rp[xb])), fb = make_float2(b256(rp[xa + 1]), b256(rp[xb + 1]));
         return __ffma2_rn(fx2, sub2(fb, fa), fa);
     };
@@ -1196,8 +1208,8 @@ __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, u
     if (!vA) bad = 0;
     for (; bad; bad &= bad - 1) {
         const int r = rb + __ffs(bad) - 1;
-        const uint32_t y0 = crop_exact_tile(wt, T, X0 + 2 * lane, Y0 + r, u0, v0, w, h);
-        const uint32_t y1 = vB ? crop_exact_tile(wt, T, X0 + 2 * lane + 1, Y0 + r, u0, v0, w, h) : 0u;
+        const uint32_t y0 = crop_exact_tile(wl, WP, T, X0 + 2 * lane, Y0 + r, u0, w, h);
+        const uint32_t y1 = vB ? crop_exact_tile(wl, WP, T, X0 + 2 * lane + 1, Y0 + r, u0, w, h) : 0u;
         if (RGBO) {
             store_rgb2(oy + ((size_t)(Y0 + r) * w + X0 + 2 * lane) * 3, y0 | y1 << 8, csc + r * TW + 2 * lane);
         } else {
@@ -1208,17 +1220,19 @@ __device__ __forceinline__ void crop_rows2(const uint8_t* wt, const Tables& T, u
     }
 }
 
-// Persistent TMA compose.  Per tile: every warp waits on the tile's mbarrier,
-// computes W rows (-> shared wt) and chroma rows (-> global), one CTA
-// barrier, then crop_resize rows of W (-> global).  Undecidable pixels take
-// the exact reference path inline (the warp diverges for them only).  wt is
-// double-buffered and the TMA box of tile k+2 is issued only after the
-// barrier of tile k+1, so a fast warp may run ahead into the next tile.
-//
-// RGBO (4:4:4, crop margins >= 1 px): the chroma rows go to a per-CTA Cb / Cr
-// tile in global scratch (double-buffered like wt; 32 KB per CTA, L2-resident),
-// and the crop pass combines each luma byte with its Cb / Cr into interleaved
-// RGB at oY (3 bytes per pixel) — no plane ever reaches HBM.
+// Persistent TMA compose.  Per tile: every warp waits on the buffer's TMA
+// mbarrier, computes the W rows (-> shared memory) and chroma rows (->
+// global), then the crop_resize rows of W (-> global).  Two modes per tile:
+//  * private (interior tiles, tile_prep pad0 bit 2): each warp computes the W
+//    rows its own (contiguous) crop rows read into its private rows of wt[b]
+//    (<= 17 rows; a row shared by two warps is computed by both), so the
+//    crop follows after a __syncwarp — no CTA barrier;
+//  * shared (edge tiles): W rows warp-strided into wt[b], one CTA barrier.
+// Buffer reuse: each warp counts itself done with buffer b at the end of its
+// tile; the last one issues the TMA of the tile two steps ahead into b (and
+// resets the count), so a fast warp runs ahead into the next tile while slow
+// ones finish.  Undecidable pixels take the exact reference path inline (the
+// lane diverges for them only).
 template <bool LUMA, bool CHROMA, bool RGBO>
 __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
     PlaneBatch Y, PlaneBatch CB, PlaneBatch CR, const FramePlan* __restrict__ plan, CropGeom g,
@@ -1232,57 +1246,56 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
     const int W = LUMA ? Y.w : CB.w, H = LUMA ? Y.h : CB.h;
     const int w = Y.w, h = Y.h, cw = CB.w, ch = CB.h;
     const bool identity = g.mx == 0 && g.my == 0;
-    const long long tpf = (long long)tiles_x * tiles_y;
-    const long long total = tpf * frames;
+    const int tpf = tiles_x * tiles_y;
+    const long long total = (long long)tpf * frames;
     const uint32_t bytes_l = LUMA ? BW * BH : 0, bytes_c = CHROMA ? 2 * BW * BH : 0;
     constexpr unsigned FULL = 0xFFFFFFFFu;
 
-    auto prefetch = [&](long long t, int slot) {  // thread 0: tile t's params -> tp[slot], async
-        const char* src = reinterpret_cast<const char*>(T.tiles + 3 * t);
-        const uint32_t dst = smem_u32(&S.tp[slot]);
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(src + 16 * i)
-                         : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto issue = [&](long long t, int b, int slot) {  // thread 0: TMA of tile t into buffer b
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        const TileParams& tp = S.tp[slot];
+    auto issue = [&](long long t, int b) {  // one thread: TMA of tile t into buffer b
+        const int4 p1 = __ldg(T.tiles + 3 * t + 1), p2 = __ldg(T.tiles + 3 * t + 2);  // lbx lby cbx cby | lfit cfit
         const int f = (int)(t / tpf);
         const uint32_t bar = smem_u32(&S.mbar[b]);
-        const uint32_t bytes = (LUMA && tp.lfit ? bytes_l : 0) + (CHROMA && tp.cfit ? bytes_c : 0);
+        const bool lfit = LUMA && p2.x, cfit = CHROMA && p2.y;
+        const uint32_t bytes = (lfit ? bytes_l : 0) + (cfit ? bytes_c : 0);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        if (LUMA && tp.lfit) tma_load3(smem_u32(&S.box[b][0][0]), &mapY, tp.lbx, tp.lby, f, bar);
-        if (CHROMA && tp.cfit) {
-            tma_load3(smem_u32(&S.box[b][1][0]), &mapCB, tp.cbx, tp.cby, f, bar);
-            tma_load3(smem_u32(&S.box[b][2][0]), &mapCR, tp.cbx, tp.cby, f, bar);
+        if (lfit) tma_load3(smem_u32(&S.box[b][0][0]), &mapY, p1.x, p1.y, f, bar);
+        if (cfit) {
+            tma_load3(smem_u32(&S.box[b][1][0]), &mapCB, p1.z, p1.w, f, bar);
+            tma_load3(smem_u32(&S.box[b][2][0]), &mapCR, p1.z, p1.w, f, bar);
         }
     };
     long long t = blockIdx.x;
+    const long long G = gridDim.x;
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[1])));
+        S.done[0] = S.done[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (t < total) {
-            prefetch(t, 0);
-            issue(t, 0, 0);
-            if (t + gridDim.x < total) prefetch(t + gridDim.x, 1);
-        }
+        if (t < total) issue(t, 0);
+        if (t + G < total) issue(t + G, 1);
     }
     __syncthreads();
-    for (int k = 0; t < total; ++k, t += gridDim.x) {
+    // frame / tile-in-frame of t, advanced incrementally
+    int f = (int)(t / tpf), ti = (int)(t - (long long)f * tpf);
+    const int df = (int)(G / tpf), dti = (int)(G - (long long)df * tpf);
+    for (int k = 0; t < total; ++k, t += G) {
         const int b = k & 1;
-        const long long tn = t + gridDim.x;
-        if (tid == 0 && tn < total) {
-            issue(tn, b ^ 1, (k + 1) % 3);
-            if (tn + gridDim.x < total) prefetch(tn + gridDim.x, (k + 2) % 3);
+        if (k) {
+            f += df;
+            ti += dti;
+            if (ti >= tpf) {
+                ti -= tpf;
+                ++f;
+            }
         }
-        const int f = (int)(t / tpf), ti = (int)(t - f * tpf);
         const int X0 = (ti % tiles_x) * TW, Y0 = (ti / tiles_x) * TTH;
         const int nx = min(TW, W - X0), ny = min(TTH, H - Y0);
-        const TileParams tp = S.tp[k % 3];
+        TileParams tp;
+        {
+            const int4 a0 = __ldg(T.tiles + 3 * t), a1 = __ldg(T.tiles + 3 * t + 1), a2 = __ldg(T.tiles + 3 * t + 2);
+            tp = TileParams{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        }
         const int u0 = tp.u0, v0 = tp.v0, nu = tp.nu, nv = tp.nv;
         const long long cf = plan[f].cf, snf = plan[f].snf, kxx = plan[f].kxx, kyx = plan[f].kyx;
         const long long kxy = plan[f].kxy, kyy = plan[f].kyy;
@@ -1291,6 +1304,10 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
         const uint8_t* gcr = CHROMA ? CR.base + (size_t)f * CR.stride : nullptr;
         const uint8_t* wt = &S.wt[b][0][0];
         uint8_t* csc = RGBO ? scr + ((size_t)blockIdx.x * 2 + b) * (2 * TTH * TW) : nullptr;
+        // private mode: this warp's crop rows [crb, cre) and the W rows they read
+        const bool priv = LUMA && (tp.pad0 & 4);
+        const int cper = (ny + NW - 1) / NW, crb = warp * cper, cre = min(crb + cper, ny);
+        int pw0 = 0;  // first private W row (absolute)
         mbar_wait(smem_u32(&S.mbar[b]), (uint32_t)((k >> 1) & 1));
         // ------------------------------------------- W rows -> wt[b]
         if (LUMA) {
@@ -1301,8 +1318,18 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
             const uint8_t* bx = &S.box[b][0][0];
             const uint32_t wsm = smem_u32(wt);
             int qn = 0;
-            if (tp.pad0 & 1)
-                w_rows_lean2(bx, tp.lbx, tp.lby, rxf, ryf, &S.wt[b][0][0], nu, nv, u0, v0, cf, snf, plan, f, w, h);
+            if (priv) {
+                uint8_t* pr = &S.wt[b][0][0] + warp * PROWS * PWP;
+                if (crb < cre) {
+                    pw0 = __ldg(T.cy0 + Y0 + crb);
+                    const int pw1 = __ldg(T.cy0 + Y0 + cre - 1) + 1;
+                    w_rows_lean2<1, PWP>(bx, tp.lbx, tp.lby, rxf, ryf, pr, pw0 - v0, pw1 - v0 + 1, nu, u0, v0, cf,
+                                         snf, plan, f, w, h);
+                }
+                __syncwarp();
+            } else if (tp.pad0 & 1)
+                w_rows_lean2<NW, NW * WTW>(bx, tp.lbx, tp.lby, rxf, ryf, &S.wt[b][0][0] + warp * WTW, warp, nv, nu,
+                                           u0, v0, cf, snf, plan, f, w, h);
             else if (tp.lfit)
                 qn = w_rows_q(bx, BW, -(tp.lby * BW + tp.lbx), rxf, ryf, wsm, nu, nv, uCF, uSN, 32 * cf, 32 * snf,
                               NW * snf, NW * cf, limx, limy, S.wq[warp]);
@@ -1371,10 +1398,20 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 __syncwarp();
             }
         }
-        __syncthreads();  // wt[b] complete; box[b] free for tile k+2 after this
+        if (!priv) __syncthreads();  // shared mode: wt[b] complete (RGBO: the Cb / Cr tile too)
         // ------------------------------------------- crop_resize of W -> global
-        if (RGBO) {  // the host checked the crop_rows2 preconditions (margins >= 1 px)
-            crop_rows2<true>(wt, T, oY + (size_t)f * Y.stride * 3, w, h, nx, ny, X0, Y0, u0, v0, csc);
+        if (priv) {
+            const uint8_t* wl = &S.wt[b][0][0] + warp * PROWS * PWP - pw0 * PWP;
+            if (RGBO) {
+                // the Cb / Cr rows of this warp's crop rows come from other warps
+                __syncthreads();
+                crop_rows2<true, PWP>(wl, T, oY + (size_t)f * Y.stride * 3, w, h, nx, crb, cre, X0, Y0, u0, csc);
+            } else {
+                crop_rows2<false, PWP>(wl, T, oY + (size_t)f * Y.stride, w, h, nx, crb, cre, X0, Y0, u0, nullptr);
+            }
+        } else if (RGBO) {  // the host checked the crop_rows2 preconditions (margins >= 1 px)
+            crop_rows2<true, WTW>(wt - v0 * WTW, T, oY + (size_t)f * Y.stride * 3, w, h, nx, crb, cre, X0, Y0, u0,
+                                  csc);
         } else if (LUMA) {
             if (identity) {
                 uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + lane;
@@ -1385,7 +1422,8 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 }
             } else if (g.my >= 1 && __all_sync(FULL, __ldg(T.cx0 + X0 + min(2 * lane, nx - 1)) + 1 <= w - 1 &&
                                                          __ldg(T.cx0 + X0 + min(2 * lane + 1, nx - 1)) + 1 <= w - 1)) {
-                crop_rows2<false>(wt, T, oY + (size_t)f * Y.stride, w, h, nx, ny, X0, Y0, u0, v0, nullptr);
+                crop_rows2<false, WTW>(wt - v0 * WTW, T, oY + (size_t)f * Y.stride, w, h, nx, crb, cre, X0, Y0, u0,
+                                       nullptr);
             } else {
                 // lane l owns output columns 2l and 2l+1 (one 16-bit store per row)
                 uint8_t* oy = oY + (size_t)f * Y.stride + (size_t)Y0 * w + X0 + 2 * lane;
@@ -1473,10 +1511,22 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                             r = rb + i / nx;
                             c = i % nx;
                         }
-                        stg_u8(oy + (size_t)r * w + c - 2 * lane, crop_exact_tile(wt, T, X0 + c, Y0 + r, u0, v0, w, h));
+                        stg_u8(oy + (size_t)r * w + c - 2 * lane,
+                               crop_exact_tile(wt - v0 * WTW, WTW, T, X0 + c, Y0 + r, u0, w, h));
                     }
                     __syncwarp();
                 }
+            }
+        }
+        // ------------------------------------------- release buffer b
+        // (the last warp done with it issues the tile two steps ahead)
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();  // this warp's reads of box[b] / wt[b] happen before the count
+            if (atomicAdd(&S.done[b], 1u) == NW - 1) {
+                __threadfence_block();
+                atomicExch(&S.done[b], 0u);
+                if (t + 2 * G < total) issue(t + 2 * G, b);
             }
         }
     }
