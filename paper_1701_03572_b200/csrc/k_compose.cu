@@ -630,6 +630,7 @@ struct SmemT {
     unsigned long long mbar[2];  // TMA transaction barrier of each buffer
     unsigned done[2];            // warps finished with the buffer's tile
     unsigned wq[NT / 32][QW];    // per-warp queues of pixels for the exact path
+    alignas(16) TileParams tpw[NW][2];  // per-warp copies: the next tile's parameters arrive by cp.async
 };
 static_assert(NW * PROWS * PWP <= TWTH * WTW, "private W rows fit the tile buffer");
 
@@ -649,7 +650,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     while (!done) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
@@ -720,6 +721,7 @@ __global__ void tile_prep_kernel(const FramePlan* __restrict__ plan, int frames,
         tp.cfit = (xmx + 2) - tp.cbx < BW && (ymx + 2) - tp.cby < BH;
         if (tp.cfit && xmn >= 2 && xmx <= cw - 4 && ymn >= 2 && ymx <= ch - 4) tp.pad0 |= 2;
     }
+    tp.pad1 = (X0 / TW) | (Y0 / TTH) << 16;  // tile coordinates (no division in the compose loop)
     int4* dst = T.tiles + 3 * id;
     const int4* src = reinterpret_cast<const int4*>(&tp);
     dst[0] = src[0];
@@ -1276,9 +1278,20 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
         if (t + G < total) issue(t + G, 1);
     }
     __syncthreads();
-    // frame / tile-in-frame of t, advanced incrementally
+    // frame of t, advanced incrementally
     int f = (int)(t / tpf), ti = (int)(t - (long long)f * tpf);
     const int df = (int)(G / tpf), dti = (int)(G - (long long)df * tpf);
+    // this warp's copy of tile t's parameters, then of tile t + G (lanes 0-2,
+    // 16 bytes each), one tile ahead
+    auto fetch_tp = [&](long long tt, int slot) {
+        if (lane < 3 && tt < total) {
+            const uint32_t dst = smem_u32(&S.tpw[warp][slot]) + 16 * lane;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(T.tiles + 3 * tt + lane)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch_tp(t, 0);
     for (int k = 0; t < total; ++k, t += G) {
         const int b = k & 1;
         if (k) {
@@ -1289,13 +1302,13 @@ __global__ void __launch_bounds__(NT, 2) compose_tma_kernel(
                 ++f;
             }
         }
-        const int X0 = (ti % tiles_x) * TW, Y0 = (ti / tiles_x) * TTH;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const TileParams tp = S.tpw[warp][k & 1];
+        __syncwarp();
+        fetch_tp(t + G, (k + 1) & 1);
+        const int X0 = (tp.pad1 & 0xFFFF) * TW, Y0 = (tp.pad1 >> 16) * TTH;
         const int nx = min(TW, W - X0), ny = min(TTH, H - Y0);
-        TileParams tp;
-        {
-            const int4 a0 = __ldg(T.tiles + 3 * t), a1 = __ldg(T.tiles + 3 * t + 1), a2 = __ldg(T.tiles + 3 * t + 2);
-            tp = TileParams{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
-        }
         const int u0 = tp.u0, v0 = tp.v0, nu = tp.nu, nv = tp.nv;
         const long long cf = plan[f].cf, snf = plan[f].snf, kxx = plan[f].kxx, kyx = plan[f].kyx;
         const long long kxy = plan[f].kxy, kyy = plan[f].kyy;
