@@ -21,7 +21,7 @@
 // of a coordinate, in-bounds test, lround of the blended value — is taken on
 // the fast path only when the fast value is provably on the same side of the
 // decision boundary (coordinate error < 5e-9 px against a 2.4e-7 px guard;
-// value error <= 6.4e-5 against a 1e-4 guard); away from the frame edges the
+// value error <= 6.4e-5 against a 7e-5 guard); away from the frame edges the
 // coordinate guard is not needed at all (see the 32.32 section below).
 // Per-row fixed-point starts (16.48) and the crop tables are
 // computed once per frame / geometry by compose_prep_kernel, so a tile's
@@ -53,7 +53,7 @@ constexpr int WTW = 72, WTH = 36;        // warped-luma tile (<= 66 x 34 used)
 constexpr int SRC_W = 128, SRC_H = 80;   // staged source capacity per plane
 constexpr int QCAP = 1024;               // exact-path queue
 constexpr uint32_t GUARD = 1024;         // coordinate guard, units of 2^-32 px
-constexpr float VGUARD = 1.0e-4f;        // blended-value guard (the fast error is <= 6.1e-5)
+constexpr float VGUARD = 7.0e-5f;        // blended-value guard (the fast error is <= 6.35e-5)
 constexpr double FIX48 = 281474976710656.0;  // 2^48
 
 struct CropGeom {
@@ -120,8 +120,12 @@ __device__ __forceinline__ float b256(uint32_t b) { return __uint_as_float(0x438
 // lround; -1 when the rounding decision is within the error guard of a .5
 // tie.  Error budget against the reference's fp64 value: in [256, 512)
 // differences are exact (Sterbenz) and the three fma roundings contribute
-// <= 2 * 2^-16 to v; the fractions are within 2^-24 (+1e-9 px coordinate
-// error), <= 255 * 2^-24 each.  Total <= 6.1e-5 < VGUARD.
+// <= 2 * 2^-16 = 3.05e-5 to v (top and bot each <= 2^-16, weighted by 1-fy
+// and fy, plus v's own); the fractions are within 2^-24 of the coordinate's
+// (the crop's double table fractions within 2^-25), which is itself within
+// 5e-9 px of the reference's, and |dv/dfx|, |dv/dfy| <= 255 — across an
+// integer too, where the blend is continuous — so <= 2 * 255 * 6.46e-8 =
+// 3.3e-5.  Total <= 6.35e-5 < VGUARD = 7e-5; |v - round(v)| is exact in fp32.
 __device__ __forceinline__ int blend_round(uint32_t a, uint32_t b, uint32_t c, uint32_t d, float fx,
                                            float fy) {
     const float fa = b256(a), fc = b256(c);
