@@ -1586,6 +1586,25 @@ bool make_map(CUtensorMap* m, const uint8_t* base, int w, int h, int frames) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+}  // namespace
+
+// 3D uint8 tensor map (x, y, frame) with a box_w x box_h x 1 box; false when
+// the driver entry point is missing or the layout is not TMA-eligible
+bool encode_u8_3d(CUtensorMap* m, const uint8_t* base, int w, int h, int frames, size_t frame_stride, int box_w,
+                  int box_h) {
+    EncodeFn enc = get_encode();
+    if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (w & 15) || (frame_stride & 15)) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {(cuuint64_t)w, (cuuint64_t)frame_stride};
+    const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+
 // TMA eligibility: 16-byte aligned planes with 16-byte pitches
 bool tma_ok(const PlaneBatch& p) {
     return p.base && (p.w % 16) == 0 && (reinterpret_cast<uintptr_t>(p.base) % 16) == 0 &&

@@ -18,6 +18,10 @@
 #include <algorithm>
 #include <climits>
 
+#include <cuda.h>
+
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -28,6 +32,15 @@ namespace {
 struct Level {
     const uint8_t* px;
     int w, h;
+    const CUtensorMap* map = nullptr;  // TMA map of the pyramid level (chain kernel), or none
+    int frame = 0;                     // frame index of px inside that map
+};
+
+// Per-level TMA maps of the pyramid (3D: x, y, frame; box 64 x SM_ROWS x 1),
+// passed to the chain kernel as one grid constant; bit l of mask: level l has one
+struct LkMaps {
+    CUtensorMap m[STABGPU_MAX_LEVELS];
+    unsigned mask;
 };
 
 __device__ __forceinline__ bool inside(const Level& L, double x, double y) {
@@ -247,15 +260,16 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
 // are independent, so the global latency is paid once per staging instead of
 // once per row.
 constexpr int SM_MARGIN = 3;
-constexpr int SM_PITCH = 48;  // bytes per staged row (>= 32 + 1 + 2 * margin + 3)
-constexpr int SM_ROWS = 40;   // >= 32 + 2 * margin
+constexpr int SM_PITCH = 64;  // bytes per staged row (>= 15 + 32 + 1 + 2 * margin + 3: the TMA box width)
+constexpr int SM_ROWS = 40;   // >= 32 + 2 * margin (the TMA box height)
 // Per-warp shared layout (doubles): the system record first (2x2 system,
 // level origin, 1/det, S_uv, step count, level bounds, thresholds), then the
 // staged window, then the template gradients.  With one warp per CTA (the
 // chain kernel) every record address is a constant offset of the shared
 // window: no address arithmetic in the iteration loop.
-constexpr int SYS_D = 24;
+constexpr int SYS_D = 32;  // 256 B: the staged window after it is 128-byte aligned (TMA destination)
 constexpr int STG_D = SM_ROWS * SM_PITCH / 8;
+constexpr int SYS_TMA_PHASE = 23, SYS_TMA_BAR = 24;  // sys slots: TMA mbarrier parity (int) and the mbarrier
 __host__ __device__ constexpr int lk_per_warp(int side) { return SYS_D + STG_D + 2 * (side * side + 1); }
 
 // Copies image block [x0, x0+sw) x [y0, y0+sh) (clamped at the border) to a
@@ -263,8 +277,40 @@ __host__ __device__ constexpr int lk_per_warp(int side) { return SYS_D + STG_D +
 // image column x0.  Interior blocks of 4-byte-aligned rows go as aligned
 // 32-bit words, several rows per warp instruction (lane -> (row, word)); the
 // border case goes byte by byte with the reference's clamped indices.
-__device__ __forceinline__ int stage_block(const Level& L, int x0, int y0, int sw, int sh, uint8_t* dst) {
+__device__ __forceinline__ int stage_block(const Level& L, int x0, int y0, int sw, int sh, uint8_t* dst,
+                                           double* sys = nullptr) {
     const int lane = threadIdx.x & 31;
+    // interior block of a level with a TMA map: one bulk-tensor copy of the
+    // 64 x SM_ROWS box at (x0 & ~15, y0) by lane 0, completion on the warp's
+    // mbarrier (bytes past the image are zero-filled and never read)
+    if (L.map && x0 >= 0 && y0 >= 0 && x0 + sw <= L.w && y0 + sh <= L.h && (x0 & 15) + sw <= SM_PITCH &&
+        sh <= SM_ROWS) {
+        const int xa = x0 & ~15;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sys + SYS_TMA_BAR);
+        int* php = reinterpret_cast<int*>(sys + SYS_TMA_PHASE);
+        const uint32_t ph = (uint32_t)*php;
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this warp's reads of the old block
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SM_PITCH * SM_ROWS)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                "l"(L.map), "r"(xa), "r"(y0), "r"(L.frame), "r"(bar)
+                : "memory");
+        }
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(done)
+                : "r"(bar), "r"(ph)
+                : "memory");
+        __syncwarp();
+        if (lane == 0) *php = (int)(ph ^ 1u);
+        return x0 - xa;
+    }
     const int xw = x0 & ~3;
     const int nw = ((x0 + sw - 1) >> 2) - (xw >> 2) + 1;  // words per row (<= SM_PITCH / 4)
     const bool words = ((L.w & 3) == 0) && ((reinterpret_cast<uintptr_t>(L.px) & 3) == 0) && x0 >= 0 &&
@@ -498,7 +544,8 @@ __device__ __forceinline__ double div_rn_recip(double a, double b, double y) {
 // fails both, exactly as it fails a lone track_one.
 __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, int f0, int f1,
                            const stabgpu_flow_cfg& cfg, double* tg, uint8_t* stg, double* sys, bool& ok0, bool& ok1,
-                           double2& o0, double2& o1, unsigned& it0, unsigned& it1, unsigned& builds) {
+                           double2& o0, double2& o1, unsigned& it0, unsigned& it1, unsigned& builds,
+                           const LkMaps* maps = nullptr) {
     const int lane = threadIdx.x & 31;
     const int r = cfg.window_radius, side = 2 * r + 1;
     const int e = r + 1, es = 2 * e + 1;  // extended template patch (flow.cpp:79-81)
@@ -519,7 +566,8 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
     bool al0 = true, al1 = f1 >= 0;
     ok0 = ok1 = false;
     for (int level = start_level; level >= 0; --level) {
-        const Level pi{P.lvl[level] + (size_t)ft * P.stride[level], P.w[level], P.h[level]};
+        const CUtensorMap* lmap = (maps && ((maps->mask >> level) & 1u)) ? &maps->m[level] : nullptr;
+        const Level pi{P.lvl[level] + (size_t)ft * P.stride[level], P.w[level], P.h[level], lmap, ft};
         const double scale = (double)(1u << level);
         const double plx = ddiv(px, scale), ply = ddiv(py, scale);
         if (!inside(pi, plx, ply)) return;
@@ -546,7 +594,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
         double gxx = 0.0, gxy = 0.0, gyy = 0.0, tx = 0.0, ty = 0.0;
         const uint32_t ga0 = (uint32_t)__cvta_generic_to_shared(tg);
         __syncwarp();
-        const int toff = stage_block(pi, xb, yb, es + 2, es + 1, stg);
+        const int toff = stage_block(pi, xb, yb, es + 2, es + 1, stg, sys);
         __syncwarp();
         const uint32_t grow = (uint32_t)vw * 16u;  // gradients: [vh][vw] {gx, gy}, then a zero slot
         if (es > 31) template_pass<true>(stg + toff, fx, fy, jv0, jv1, iv0, iv1, ga0, grow, gxx, gxy, gyy, tx, ty);
@@ -590,7 +638,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
         for (int j = 0; j < nt; ++j) {
             if (!(j ? al1 : al0)) continue;
             const int fc = j == 0 ? f0 : f1;
-            const Level ci{P.lvl[level] + (size_t)fc * P.stride[level], P.w[level], P.h[level]};
+            const Level ci{P.lvl[level] + (size_t)fc * P.stride[level], P.w[level], P.h[level], lmap, fc};
             double gfx = j ? gx1 : gx0, gfy = j ? gy1 : gy0;
             unsigned nit = 0;
             // ---- iterations (flow.cpp:184-209): lane L <-> valid column iv0 + L
@@ -613,7 +661,7 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
                         sx0 = cx - SM_MARGIN;
                         sy0 = cy - SM_MARGIN;
                         __syncwarp();
-                        soff = stage_block(ci, sx0, sy0, sw, sh, stg);
+                        soff = stage_block(ci, sx0, sy0, sw, sh, stg, sys);
                         __syncwarp();
                     }
                     double sv[8];
@@ -773,14 +821,21 @@ __global__ void __launch_bounds__(128, 4) lk_fast_kernel(LkStep s, stabgpu_flow_
 constexpr int CH_WPC = 1, CH_CTAS = 20;
 template <bool MS>
 __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain c, stabgpu_flow_cfg cfg,
-                                                                       unsigned* __restrict__ work, int smem_per_warp) {
-    extern __shared__ __align__(16) double lsm[];
+                                                                       unsigned* __restrict__ work, int smem_per_warp,
+                                                                       const __grid_constant__ LkMaps maps) {
+    extern __shared__ __align__(128) double lsm[];
     const int warp = CH_WPC == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sys = lsm + (size_t)warp * smem_per_warp;
     uint8_t* stg = reinterpret_cast<uint8_t*>(sys + SYS_D);
     double* tg = sys + SYS_D + STG_D;
     int* nst_sh = reinterpret_cast<int*>(sys + 18);  // the segment's step count (MS)
     const unsigned total = (unsigned)c.nseg * (unsigned)c.max_pts;
+    if (lane == 0) {  // the warp's TMA staging barrier
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(sys + SYS_TMA_BAR)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        *reinterpret_cast<int*>(sys + SYS_TMA_PHASE) = 0;
+    }
+    __syncwarp();
     const size_t plane = (size_t)c.nseg * c.max_pts;
     const double thr2 = dmul(cfg.fb_threshold, cfg.fb_threshold);
     while (true) {
@@ -814,7 +869,8 @@ __global__ void __launch_bounds__(32 * CH_WPC, CH_CTAS) lk_chain_kernel(LkChain 
         double2 q = p;
         while (true) {
             unsigned it0 = 0, it1 = 0;
-            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, sys, ok0, ok1, o0, o1, it0, it1, blds);
+            track_dual(c.pyr, ft, q.x, q.y, f0, f1, cfg, tg, stg, sys, ok0, ok1, o0, o1, it0, it1, blds,
+                       maps.mask ? &maps : nullptr);
             its += it0;
             if (t == 0) {
                 if (!ok0) break;
@@ -991,7 +1047,16 @@ void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t
     const long long items = (long long)c.nseg * c.max_pts;
     const long long want = (items + wpc - 1) / wpc;
     const int grid = (int)std::min<long long>(want, (long long)sms * std::max(per_sm, 1));
-    kern<<<grid, wpc * 32, smem, st>>>(c, cfg, c.work, per_warp);
+    // TMA maps of the levels whose frames are a regular 16-byte aligned 3D array
+    LkMaps maps;
+    memset(&maps, 0, sizeof maps);
+    for (int l = 0; l < c.pyr.levels; ++l) {
+        const size_t fs = (size_t)c.pyr.w[l] * c.pyr.h[l];
+        if (c.pyr.stride[l] == fs && (c.pyr.w[l] % 16) == 0 &&
+            encode_u8_3d(&maps.m[l], c.pyr.lvl[l], c.pyr.w[l], c.pyr.h[l], c.nframes, fs, SM_PITCH, SM_ROWS))
+            maps.mask |= 1u << l;
+    }
+    kern<<<grid, wpc * 32, smem, st>>>(c, cfg, c.work, per_warp, maps);
 }
 
 void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,

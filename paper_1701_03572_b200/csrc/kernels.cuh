@@ -1,6 +1,8 @@
 // kernels.cuh — host-side launchers of the sm_100a kernels (internal).
 #pragma once
 
+#include <cuda.h>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -132,6 +134,9 @@ struct LkChain {
     unsigned* work;
 };
 void launch_lk_chain(const LkChain& c, const stabgpu_flow_cfg& cfg, cudaStream_t st);
+// 3D uint8 tensor map (x, y, frame) with a box_w x box_h x 1 box (k_compose.cu)
+bool encode_u8_3d(CUtensorMap* m, const uint8_t* base, int w, int h, int frames, size_t frame_stride, int box_w,
+                  int box_h);
 // Ordered compaction of kept pairs: TrackSet of frame (frame0 + s*R + t) and
 // the next points of each segment.
 void launch_compact(const LkStep& s, double2* next_pts, int* next_n, double2* trk_prev,
