@@ -628,6 +628,103 @@ __device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const 
     return false;
 }
 
+// K4 phase A over many CTAs per frame (when the scratch has bucket arrays):
+// counts per bucket (shared histogram, then one global atomic per bin), an
+// exclusive scan per frame, and a scatter in which each CTA reserves its range
+// of every bucket once and fills it through shared-memory cursors.  The order inside a bucket is irrelevant (chunks are sorted
+// exactly before the greedy), so the result is the phase the select CTA ran
+// itself, with the candidate list read by ~16 CTAs per frame instead of one.
+__device__ __forceinline__ bool bucket_frame(const DetectScratch& s, int d, int redo, unsigned& n,
+                                             unsigned long long& thrb, unsigned& maxf, double quality) {
+    if (redo && !(s.flags[d] & 2)) return false;
+    n = s.count[d];
+    const unsigned long long mb = s.maxbits[d];
+    if (n == 0 || mb == 0) return false;
+    thrb = dbits(dmul(quality, __longlong_as_double((long long)mb)));
+    maxf = __float_as_uint(__double2float_rn(__longlong_as_double((long long)mb)));
+    return true;
+}
+
+__global__ void __launch_bounds__(512) bucket_count_kernel(DetectScratch s, double quality, int redo) {
+    const int d = blockIdx.y;
+    unsigned n, maxf;
+    unsigned long long thrb;
+    if (!bucket_frame(s, d, redo, n, thrb, maxf, quality)) return;
+    __shared__ unsigned hb[kBuckets];
+    for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) hb[b] = 0;
+    __syncthreads();
+    const unsigned long long* ck = s.cand_key + (size_t)d * s.cap;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long k = ck[i];
+        if (k >= thrb) atomicAdd(&hb[bucket_of(k, maxf)], 1u);
+    }
+    __syncthreads();
+    unsigned* cnt = s.bstart + (size_t)d * (kBuckets + 1);
+    for (int b = threadIdx.x; b < kBuckets; b += blockDim.x)
+        if (hb[b]) atomicAdd(&cnt[b], hb[b]);
+}
+
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(DetectScratch s, double quality, int redo) {
+    const int d = blockIdx.x;
+    unsigned n, maxf;
+    unsigned long long thrb;
+    if (!bucket_frame(s, d, redo, n, thrb, maxf, quality)) return;
+    __shared__ unsigned warp_tot[32], total;
+    constexpr int PER = kBuckets / 1024;
+    unsigned* st = s.bstart + (size_t)d * (kBuckets + 1);
+    unsigned* cur = s.bcur + (size_t)d * kBuckets;
+    unsigned v[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        v[k] = st[threadIdx.x * PER + k];
+        sum += v[k];
+    }
+    unsigned off = block_excl_scan(sum, warp_tot, &total);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        st[threadIdx.x * PER + k] = off;
+        cur[threadIdx.x * PER + k] = off;
+        off += v[k];
+    }
+    if (threadIdx.x == 0) st[kBuckets] = total;
+}
+
+__global__ void __launch_bounds__(512) bucket_scatter_kernel(DetectScratch s, double quality, int redo) {
+    // each CTA takes a contiguous slice: counts it per bucket in shared memory,
+    // reserves its range of every non-empty bucket with one global atomic, then
+    // scatters through shared cursors (no global atomic per candidate)
+    const int d = blockIdx.y;
+    unsigned n, maxf;
+    unsigned long long thrb;
+    if (!bucket_frame(s, d, redo, n, thrb, maxf, quality)) return;
+    __shared__ unsigned hb[kBuckets];
+    for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) hb[b] = 0;
+    __syncthreads();
+    const unsigned per = (n + gridDim.x - 1) / gridDim.x;
+    const unsigned lo = min(blockIdx.x * per, n), hi = min(lo + per, n);
+    const unsigned long long* ck = s.cand_key + (size_t)d * s.cap;
+    const unsigned* ci = s.cand_idx + (size_t)d * s.cap;
+    for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const unsigned long long k = ck[i];
+        if (k >= thrb) atomicAdd(&hb[bucket_of(k, maxf)], 1u);
+    }
+    __syncthreads();
+    unsigned* cur = s.bcur + (size_t)d * kBuckets;
+    for (int b = threadIdx.x; b < kBuckets; b += blockDim.x)
+        if (hb[b]) hb[b] = atomicAdd(&cur[b], hb[b]);
+    __syncthreads();
+    unsigned long long* sk = s.sort_key + (size_t)d * s.cap;
+    unsigned* si = s.sort_idx + (size_t)d * s.cap;
+    for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const unsigned long long k = ck[i];
+        if (k >= thrb) {
+            const unsigned pos = atomicAdd(&hb[bucket_of(k, maxf)], 1u);
+            sk[pos] = k;
+            si[pos] = ci[i];
+        }
+    }
+}
+
 // K4: one CTA per detection frame.
 //   A. the candidates >= quality * max are bucketed by a monotone 13-bit
 //      truncated float key (histogram, scan, scatter) into sort_key/sort_idx,
@@ -706,7 +803,13 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     unsigned long long* sk = s.sort_key + (size_t)d * s.cap;
     unsigned* si = s.sort_idx + (size_t)d * s.cap;
 
-    // ---- A. histogram + exclusive scan + scatter into bucket order
+    // ---- A. histogram + exclusive scan + scatter into bucket order (or the
+    // multi-CTA bucket kernels' result)
+    if (s.bstart) {
+        const unsigned* st = s.bstart + (size_t)d * (kBuckets + 1);
+        for (int b = tid; b <= kBuckets; b += SEL_THREADS) S.bstart[b] = st[b];
+        __syncthreads();
+    } else {
     for (int b = tid; b < kBuckets; b += SEL_THREADS) cursor[b] = 0;
     __syncthreads();
     for (unsigned i = tid; i < n; i += SEL_THREADS)
@@ -739,6 +842,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     }
     __threadfence_block();
     __syncthreads();
+    }
     // ---- B. grid (cells >= min_distance, <= MAX_CELLS) and bitmap, cleared
     int cell = max(1, (int)ceil(cfg.min_distance));
     while ((long long)((rw + cell - 1) / cell) * ((rh + cell - 1) / cell) > MAX_CELLS) ++cell;
@@ -945,6 +1049,17 @@ size_t bitmap_words(stabgpu_roi roi) {
 }
 
 
+namespace {
+void launch_buckets(const DetectScratch& s, int nD, double quality, int redo, cudaStream_t st) {
+    if (!s.bstart || !s.bcur) return;
+    cudaMemsetAsync(s.bstart, 0, sizeof(unsigned) * (kBuckets + 1) * (size_t)nD, st);
+    const dim3 grid(16, nD);
+    bucket_count_kernel<<<grid, 512, 0, st>>>(s, quality, redo);
+    bucket_scan_kernel<<<nD, 1024, 0, st>>>(s, quality, redo);
+    bucket_scatter_kernel<<<grid, 512, 0, st>>>(s, quality, redo);
+}
+}  // namespace
+
 void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu_roi roi,
                    DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
                    cudaStream_t st) {
@@ -1031,15 +1146,23 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
             return;
         }
     }
+    // phase A by the multi-CTA bucket kernels when the batch is too small to
+    // fill the GPU with select CTAs (Stage II, single frames: C1 stream 3.6k ->
+    // 4.3k frames/s); large batches keep it inside select (no gain measured)
     DetectScratch sf = s;
     if (!fast) sf.flags = nullptr;
+    if (nD > 32) sf.bstart = sf.bcur = nullptr;
+    launch_buckets(sf, nD, cfg.quality_level, 0, st);
     sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy, g_anext, ch,
                                        use_bm ? 1 : 0, 0);
     if (fast) {  // frames whose cut prefix ran out: full candidate list (usually none)
         resp_redo_reset_kernel<<<nD, 32, 0, st>>>(s);
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 1);
-        sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, s, out_xy, out_score, out_n, g_axy, g_anext, ch,
+        DetectScratch sr = s;
+        if (nD > 32) sr.bstart = sr.bcur = nullptr;
+        launch_buckets(sr, nD, cfg.quality_level, 1, st);
+        sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sr, out_xy, out_score, out_n, g_axy, g_anext, ch,
                                            use_bm ? 1 : 0, 1);
     }
     if (g_axy) {

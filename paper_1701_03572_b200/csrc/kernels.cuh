@@ -74,6 +74,9 @@ struct DetectScratch {
     double* lo;                   // [nD] candidate cut (fast path)
     unsigned char* flags;         // [nD] bit 1: redo with the full candidate list
     unsigned* mlo;                // [nD] fp32 bits of a lower bound of the max response
+    // optional multi-CTA bucketing of the candidates (K4 phase A), or null:
+    unsigned* bstart = nullptr;   // [nD][kBuckets + 1] bucket starts in sort order (counts first)
+    unsigned* bcur = nullptr;     // [nD][kBuckets] scatter cursors
 };
 constexpr int kRespBins = 2048;
 constexpr int kBuckets = 8192;

@@ -354,6 +354,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     DBUF(double, dlo, "det_lo", dbatch);
     DBUF(unsigned char, dflags, "det_flags", dbatch);
     DBUF(unsigned, dmlo, "det_mlo", dbatch);
+    DBUF(unsigned, dbst, "det_bstart", (size_t)(kBuckets + 1) * dbatch);
+    DBUF(unsigned, dbcur, "det_bcur", (size_t)kBuckets * dbatch);
     ds.maxbits = maxbits;
     ds.count = dcount;
     ds.hist = dhist;
@@ -365,6 +367,8 @@ int run_motion(stabgpu_ctx* ctx, const uint8_t* y, long long first, int count, i
     ds.lo = dlo;
     ds.flags = dflags;
     ds.mlo = dmlo;
+    ds.bstart = dbst;
+    ds.bcur = dbcur;
     DBUF(double2, ptsA, "seg_ptsA", (size_t)nseg * maxc);
     DBUF(double2, ptsB, "seg_ptsB", (size_t)nseg * maxc);
     DBUF(int, nA, "seg_nA", nseg);
@@ -2126,7 +2130,8 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     if ((rc = salloc(s, &d.maxbits, 1)) || (rc = salloc(s, &d.count, 1)) || (rc = salloc(s, &d.hist, kRespBins)) ||
         (rc = salloc(s, &d.cand_key, cap)) || (rc = salloc(s, &d.cand_idx, cap)) ||
         (rc = salloc(s, &d.sort_key, cap)) || (rc = salloc(s, &d.sort_idx, cap)) || (rc = salloc(s, &d.lo, 1)) ||
-        (rc = salloc(s, &d.flags, 1)) || (rc = salloc(s, &d.mlo, 1)))
+        (rc = salloc(s, &d.flags, 1)) || (rc = salloc(s, &d.mlo, 1)) || (rc = salloc(s, &d.bstart, kBuckets + 1)) ||
+        (rc = salloc(s, &d.bcur, kBuckets)))
         return fail(rc);
     if ((rc = salloc(s, &s->pts, maxc)) || (rc = salloc(s, &s->nxt, maxc)) || (rc = salloc(s, &s->fwd, maxc)) ||
         (rc = salloc(s, &s->trk_prev, maxc)) || (rc = salloc(s, &s->trk_cur, maxc)) ||
@@ -2420,7 +2425,8 @@ int stabgpu_tracker_create(stabgpu_ctx* ctx, const stabgpu_flow_cfg* flow, const
     if ((rc = talloc(t, &d.maxbits, 1)) || (rc = talloc(t, &d.count, 1)) || (rc = talloc(t, &d.hist, kRespBins)) ||
         (rc = talloc(t, &d.cand_key, cap)) || (rc = talloc(t, &d.cand_idx, cap)) ||
         (rc = talloc(t, &d.sort_key, cap)) || (rc = talloc(t, &d.sort_idx, cap)) || (rc = talloc(t, &d.lo, 1)) ||
-        (rc = talloc(t, &d.flags, 1)) || (rc = talloc(t, &d.mlo, 1)))
+        (rc = talloc(t, &d.flags, 1)) || (rc = talloc(t, &d.mlo, 1)) || (rc = talloc(t, &d.bstart, kBuckets + 1)) ||
+        (rc = talloc(t, &d.bcur, kBuckets)))
         return fail(rc);
     if ((rc = talloc(t, &t->pts, maxc)) || (rc = talloc(t, &t->nxt, maxc)) || (rc = talloc(t, &t->fwd, maxc)) ||
         (rc = talloc(t, &t->trk_prev, maxc)) || (rc = talloc(t, &t->trk_cur, maxc)) || (rc = talloc(t, &t->npts, 1)) ||
