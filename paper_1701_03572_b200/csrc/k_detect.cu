@@ -200,7 +200,10 @@ __device__ __forceinline__ int flush_cands(DetectScratch& s, int d, const unsign
     return 0;
 }
 
-// MODE 0: exact per-frame max (bits) + histogram of fp32 responses.
+// MODE 0: a proven lower bound of the per-frame max response + histogram of
+//         fp32 responses, both over the output rows y = 4k only (any lower
+//         bound of the max keeps the max pixel above the cut, and the
+//         histogram only steers the cut), so product rows 4k+2 are skipped.
 // MODE 1: candidates r >= lo[d] (or the threshold itself when redo) with r > 0.
 template <int MODE>
 __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu_roi roi, double quality,
@@ -261,6 +264,11 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
     const uint8_t* rp = bp + SB_W;  // row r
 #pragma unroll 2
     for (int r = Y0 - 1; r <= Y1; ++r, rp += SB_W) {
+        if (MODE == 0 && (r & 3) == 2) {  // product row 4k+2: no sampled output row (4k, 4k+4) reads it
+            Im = I0;
+            I0 = rp[SB_W];
+            continue;
+        }
         const int L = rp[-1], R = rp[1], Ip = rp[SB_W];
         const bool inr = in_x && r >= 0 && r < h;  // products outside the frame are zero
         const int gx = inr ? R - L : 0, gy = inr ? Ip - Im : 0;
@@ -271,20 +279,20 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         const int y = r - 1;  // output row whose window is rows r-2 .. r
         bool keep = false;
         unsigned long long key = 0;
-        if (y >= Y0 && out_col) {
+        if (y >= Y0 && out_col && (MODE == 1 || (y & 3) == 0)) {
             const int sxx = axx + bxx + pxx, sxy = axy + bxy + pxy, syy = ayy + byy + pyy;
             const float fxx = (float)sxx, fxy = (float)sxy, fyy = (float)syy;  // exact (< 2^24)
             // 4 * (half trace, half difference): the quarter scaling is folded in
             const float ht = 0.5f * (fxx + fyy), hd = 0.5f * (fxx - fyy);
             const float r32 = 0.25f * (ht - sqrt_approx(fmaf(hd, hd, fxy * fxy)));
             const float e = ht * SW_EPS + 1e-30f;
-            if (MODE == 0) {
-                if ((y & 3) == 0 && r32 > 0.0f) {  // histogram steers the cut only: every 4th row, x4
+            if (MODE == 0) {  // rows y = 4k only: the histogram (x4) and a lower bound of the max
+                if (r32 > 0.0f) {  // histogram steers the cut only
                     const unsigned bin = resp_bin(r32);
                     const unsigned peers = __match_any_sync(__activemask(), bin);
                     if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], 4u * __popc(peers));
                 }
-                best_low = fmaxf(best_low, r32 - e);  // max(r32 - e) <= exact max response
+                best_low = fmaxf(best_low, r32 - e);  // max(r32 - e) over the sampled rows <= exact max
             } else if (r32 + e >= lo32) {
                 const double rr = min_eig_q(sxx, sxy, syy);
                 keep = rr >= lo && rr > 0.0 && (!redo || rr < hi_excl);
