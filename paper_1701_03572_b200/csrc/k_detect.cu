@@ -201,9 +201,10 @@ __device__ __forceinline__ int flush_cands(DetectScratch& s, int d, const unsign
 }
 
 // MODE 0: a proven lower bound of the per-frame max response + histogram of
-//         fp32 responses, both over the output rows y = 4k only (any lower
+//         fp32 responses, both over the output rows y = 8k only (any lower
 //         bound of the max keeps the max pixel above the cut, and the
-//         histogram only steers the cut), so product rows 4k+2 are skipped.
+//         histogram only steers the cut), so only product rows 8k-1 .. 8k+1
+//         are formed.
 // MODE 1: candidates r >= lo[d] (or the threshold itself when redo) with r > 0.
 template <int MODE>
 __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu_roi roi, double quality,
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
     const uint8_t* rp = bp + SB_W;  // row r
 #pragma unroll 2
     for (int r = Y0 - 1; r <= Y1; ++r, rp += SB_W) {
-        if (MODE == 0 && (r & 3) == 2) {  // product row 4k+2: no sampled output row (4k, 4k+4) reads it
+        if (MODE == 0 && ((r + 1) & 7) > 2) {  // product rows 8k+2 .. 8k+6: no sampled output row (8k) reads them
             Im = I0;
             I0 = rp[SB_W];
             continue;
@@ -279,18 +280,18 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
         const int y = r - 1;  // output row whose window is rows r-2 .. r
         bool keep = false;
         unsigned long long key = 0;
-        if (y >= Y0 && out_col && (MODE == 1 || (y & 3) == 0)) {
+        if (y >= Y0 && out_col && (MODE == 1 || (y & 7) == 0)) {
             const int sxx = axx + bxx + pxx, sxy = axy + bxy + pxy, syy = ayy + byy + pyy;
             const float fxx = (float)sxx, fxy = (float)sxy, fyy = (float)syy;  // exact (< 2^24)
             // 4 * (half trace, half difference): the quarter scaling is folded in
             const float ht = 0.5f * (fxx + fyy), hd = 0.5f * (fxx - fyy);
             const float r32 = 0.25f * (ht - sqrt_approx(fmaf(hd, hd, fxy * fxy)));
             const float e = ht * SW_EPS + 1e-30f;
-            if (MODE == 0) {  // rows y = 4k only: the histogram (x4) and a lower bound of the max
+            if (MODE == 0) {  // rows y = 8k only: the histogram (x8) and a lower bound of the max
                 if (r32 > 0.0f) {  // histogram steers the cut only
                     const unsigned bin = resp_bin(r32);
                     const unsigned peers = __match_any_sync(__activemask(), bin);
-                    if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], 4u * __popc(peers));
+                    if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], 8u * __popc(peers));
                 }
                 best_low = fmaxf(best_low, r32 - e);  // max(r32 - e) over the sampled rows <= exact max
             } else if (r32 + e >= lo32) {
