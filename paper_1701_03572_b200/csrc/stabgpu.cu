@@ -1327,6 +1327,39 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
 
 namespace {
 
+// Upload chunk boundaries 0 = b_0 < b_1 < ... < b_k = n: 60-frame chunks in
+// the middle, ramped 10, 20, 40 frames at both ends, so the pipeline fills
+// (the first motion waits only for a 10-frame upload) and drains (the last
+// compute releases the last chunk plus the smoothing tail, whose download is
+// not overlapped) quickly.
+std::vector<long long> chunk_bounds(long long n) {
+    static const long long ramp[3] = {10, 20, 40};
+    static const bool flat = getenv("STABGPU_FLAT_CHUNKS") != nullptr;  // A/B switch (60-frame chunks only)
+    std::vector<long long> sizes, tail;
+    long long rem = n;
+    if (flat) rem = 0;
+    for (long long f = 0; flat && f < n; f += 60) sizes.push_back(std::min<long long>(60, n - f));
+    for (long long r : ramp)
+        if (rem > r) {
+            sizes.push_back(r);
+            rem -= r;
+        }
+    for (long long r : ramp)
+        if (rem > r + 60) {
+            tail.push_back(r);
+            rem -= r;
+        }
+    while (rem > 0) {
+        const long long c = std::min<long long>(60, rem);
+        sizes.push_back(c);
+        rem -= c;
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
+    std::vector<long long> b(1, 0);
+    for (long long c : sizes) b.push_back(b.back() + c);
+    return b;
+}
+
 // Host buffers: chunked upload -> motion -> incremental plan -> compose ->
 // download, with the copies on two copy streams so upload, compute and
 // download of different chunks overlap (PCIe is full duplex).
@@ -1395,15 +1428,15 @@ int sequence_host(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
     const int R = cfg.flow.redetect_interval;
-    const int C = R * std::max(1, 60 / R);  // frames per upload chunk
-    const int nchunks = (n + C - 1) / C;
+    const std::vector<long long> cb = chunk_bounds(n);  // upload chunks
+    const int nchunks = (int)cb.size() - 1;
     std::vector<cudaEvent_t> in_ev(nchunks), out_ev(nchunks + 1);
     for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : out_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int rc = STABGPU_OK;
     // uploads, all queued up front on the input copy stream
     for (int k = 0; k < nchunks && !rc; ++k) {
-        const size_t f0 = (size_t)k * C, nf = std::min<size_t>(C, n - f0);
+        const size_t f0 = (size_t)cb[k], nf = (size_t)(cb[k + 1] - cb[k]);
         if (rgb) {
             const uint8_t* src = zc_rgb ? zc_rgb + 3 * f0 * fl : drgb_in + 3 * f0 * fl;
             if (!zc_rgb && cudaMemcpyAsync(drgb_in + 3 * f0 * fl, hrgb + 3 * f0 * fl, 3 * nf * fl,
@@ -1426,7 +1459,7 @@ int sequence_host(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const
     const int r = cfg.smooth_radius;
     for (int k = 0; k < nchunks && !rc; ++k) {
         cudaStreamWaitEvent(st, in_ev[k], 0);
-        const long long arrived = std::min<long long>((long long)(k + 1) * C, n);  // frames [0, arrived)
+        const long long arrived = cb[k + 1];  // frames [0, arrived)
         // segments [s*R, min((s+1)R, n-1)] whose last frame has arrived
         long long seg_end = seg_done;
         while (seg_end < nseg_total && std::min<long long>((seg_end + 1) * R, n - 1) < arrived) ++seg_end;
@@ -1662,13 +1695,13 @@ int shard_motion(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const 
     uint8_t* dcr = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cr"].p) : nullptr;
     stabgpu_motion_record* base = local_motion - g.first;  // motion[global frame]
     const int R = cfg.flow.redetect_interval;
-    const int C = R * std::max(1, 60 / R);  // frames per upload chunk
-    const int nchunks = (int)((nres + C - 1) / C);
+    const std::vector<long long> cbd = chunk_bounds(nres);  // upload chunks
+    const int nchunks = (int)cbd.size() - 1;
     std::vector<cudaEvent_t> in_ev(nchunks);
     for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int rc = STABGPU_OK;
     for (int k = 0; k < nchunks && !rc; ++k) {
-        const size_t f0 = (size_t)k * C, nf = std::min<size_t>(C, nres - f0);
+        const size_t f0 = (size_t)cbd[k], nf = (size_t)(cbd[k + 1] - cbd[k]);
         if (cudaMemcpyAsync(dy + f0 * fl, hy + f0 * fl, nf * fl, cudaMemcpyHostToDevice, ctx->cin) ||
             (chroma && (cudaMemcpyAsync(dcb + f0 * fc, hcb + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin) ||
                         cudaMemcpyAsync(dcr + f0 * fc, hcr + f0 * fc, nf * fc, cudaMemcpyHostToDevice, ctx->cin))))
@@ -1680,7 +1713,7 @@ int shard_motion(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const 
     long long seg_done = 0;
     for (int k = 0; k < nchunks && !rc; ++k) {
         cudaStreamWaitEvent(st, in_ev[k], 0);
-        const long long arrived = std::min<long long>((long long)(k + 1) * C, nres);  // local frames [0, arrived)
+        const long long arrived = cbd[k + 1];  // local frames [0, arrived)
         long long seg_end = seg_done;
         while (seg_end < nseg && std::min<long long>((seg_end + 1) * R, g.count) < arrived) ++seg_end;
         if (seg_end > seg_done) {
