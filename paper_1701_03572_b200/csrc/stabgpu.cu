@@ -1328,13 +1328,15 @@ int stabgpu_stabilize_streams(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t
 namespace {
 
 // Upload chunk boundaries 0 = b_0 < b_1 < ... < b_k = n: 60-frame chunks in
-// the middle, ramped 10, 20, 40 frames at both ends, so the pipeline fills
-// (the first motion waits only for a 10-frame upload) and drains (the last
-// compute releases the last chunk plus the smoothing tail, whose download is
-// not overlapped) quickly.
-std::vector<long long> chunk_bounds(long long n) {
+// the middle, ramped 10, 20, 40 frames at both ends when a 60-frame chunk is
+// large (>= 256 MB: the copies bound the pipeline), so it fills (the first
+// motion waits only for a 10-frame upload) and drains (the last compute
+// releases the last chunk plus the smoothing tail, whose download is not
+// overlapped) quickly.  Small frames keep flat chunks: there the per-chunk
+// launches bound the pipeline (C1 e2e 42k flat vs 30k ramped).
+std::vector<long long> chunk_bounds(long long n, size_t frame_bytes) {
     static const long long ramp[3] = {10, 20, 40};
-    static const bool flat = getenv("STABGPU_FLAT_CHUNKS") != nullptr;  // A/B switch (60-frame chunks only)
+    const bool flat = getenv("STABGPU_FLAT_CHUNKS") != nullptr || frame_bytes * 60 < (256ull << 20);
     std::vector<long long> sizes, tail;
     long long rem = n;
     if (flat) rem = 0;
@@ -1428,7 +1430,7 @@ int sequence_host(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const
     PlanState* ps;
     TRY(init_plan_state(ctx, cfg, &ps));
     const int R = cfg.flow.redetect_interval;
-    const std::vector<long long> cb = chunk_bounds(n);  // upload chunks
+    const std::vector<long long> cb = chunk_bounds(n, rgb ? 3 * fl : fl + 2 * fc);  // upload chunks
     const int nchunks = (int)cb.size() - 1;
     std::vector<cudaEvent_t> in_ev(nchunks), out_ev(nchunks + 1);
     for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1695,7 +1697,7 @@ int shard_motion(stabgpu_ctx* ctx, const uint8_t* hy, const uint8_t* hcb, const 
     uint8_t* dcr = chroma ? static_cast<uint8_t*>(ctx->bufs["shard_cr"].p) : nullptr;
     stabgpu_motion_record* base = local_motion - g.first;  // motion[global frame]
     const int R = cfg.flow.redetect_interval;
-    const std::vector<long long> cbd = chunk_bounds(nres);  // upload chunks
+    const std::vector<long long> cbd = chunk_bounds(nres, fl + 2 * fc);  // upload chunks
     const int nchunks = (int)cbd.size() - 1;
     std::vector<cudaEvent_t> in_ev(nchunks);
     for (auto& e : in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
