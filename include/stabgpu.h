@@ -413,10 +413,13 @@ int stabgpu_tracker_destroy(stabgpu_tracker* t);
  * The released frames are bit-identical to Stage I (stabilize_sequence).
  * Planes are host (pageable or pinned) or device pointers (unified
  * addressing; pitch = width).  After every push / finish the caller pops the
- * ready frames in arrival order.  Each push's launches (K1, the K5 step +
- * compaction + K6 fit or the re-detection, the K7 scan, and the smoothing +
- * K8 compose of the frame it releases) run as one CUDA graph, instantiated
- * once per topology and updated in place per frame. */
+ * ready frames in arrival order.  A push's launches run on three streams:
+ * the motion chain (K1, the K5 step + compaction + K6 fit, the K7 scan), the
+ * release chain (smoothing + K8 compose of the frame it releases, behind the
+ * scan) and, every redetect_interval frames, the re-detection (beside the
+ * frame's own K5 step; the next frame's K5 waits for it) - so frame k+1's
+ * motion overlaps frame k's compose.  Each chain is one CUDA graph,
+ * instantiated once per topology and updated in place per frame. */
 typedef struct stabgpu_stream stabgpu_stream;
 
 int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfg, int w, int h, int cw, int ch,
@@ -429,6 +432,15 @@ int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready);
 /* Oldest ready frame (its index, planes and record); STABGPU_SEQUENCING if none. */
 int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* out_y, uint8_t* out_cb,
                        uint8_t* out_cr, stabgpu_frame_record* record);
+/* stabgpu_stream_pop that returns once the download is queued (the frame index
+ * is final; the planes and *record are valid after the next
+ * stabgpu_stream_wait_pops): pop_async, push the next frame, wait_pops lets the
+ * download of frame k-r overlap the upload of frame k+1 (the IC thread of
+ * run_streaming, pipeline.cpp:318-336, beside its reader thread). */
+int stabgpu_stream_pop_async(stabgpu_stream* s, int64_t* index, uint8_t* out_y, uint8_t* out_cb,
+                             uint8_t* out_cr, stabgpu_frame_record* record);
+/* Waits for every queued pop_async download; reports a selector error of the popped frames. */
+int stabgpu_stream_wait_pops(stabgpu_stream* s);
 int stabgpu_stream_destroy(stabgpu_stream* s);
 /* Per-frame CUDA graphs on (default) or off (one launch per kernel); off is
  * forced when a launch sequence needs stream-ordered scratch (more than 8192

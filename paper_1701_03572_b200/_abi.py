@@ -139,6 +139,8 @@ PROTOTYPES = {
     "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
     "stabgpu_stream_finish": (I, [V, c_ip]),
     "stabgpu_stream_pop": (I, [V, P(C.c_int64), V, V, V, V]),
+    "stabgpu_stream_pop_async": (I, [V, P(C.c_int64), V, V, V, V]),
+    "stabgpu_stream_wait_pops": (I, [V]),
     "stabgpu_stream_destroy": (I, [V]),
     "stabgpu_stream_set_graphs": (I, [V, I]),
     "stabgpu_rgb_to_ycbcr": (I, [V, V, I, I, I, V, V, V]),

@@ -491,6 +491,7 @@ struct SelShared {
     unsigned warp_tot[32];
     unsigned total;
     int nacc;
+    int sflag;  // run_rank_sort: a bucket run longer than kMaxRun (fall back to the bitonic sort)
     short hw[kHwMax];  // disc half-width per row offset (-1: row outside the disc)
 };
 
@@ -516,6 +517,59 @@ __device__ void bitonic_sort(unsigned long long* key, unsigned* idx, int n) {
             __syncthreads();
         }
     }
+}
+
+// Exact order of n survivors that arrive in bucket order (the prefilter's
+// compaction keeps the bucket-sorted order of the chunk): only the order
+// inside each run of equal buckets is open, so every survivor counts the
+// members of its run that precede it - (score desc, idx asc), a strict total
+// order - and moves to run start + count.  Two barriers instead of the
+// log^2(n) / 2 of a bitonic sort (78 at n = 4096).  Returns false (nothing
+// moved) when a run is longer than kMaxRun.  Called by the whole CTA;
+// S.sflag was cleared before the last barrier.
+constexpr int kMaxRun = 96, kSortPer = 8;
+__device__ bool run_rank_sort(unsigned long long* key, unsigned* idx, int n, unsigned maxf, int* sflag) {
+    unsigned long long k[kSortPer];
+    unsigned id[kSortPer];
+    int pos[kSortPer];
+    bool over = false;
+#pragma unroll
+    for (int q = 0; q < kSortPer; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        pos[q] = -1;
+        if (i >= n) continue;
+        k[q] = key[i];
+        id[q] = idx[i];
+        const unsigned b = bucket_of(k[q], maxf);
+        int first = i, cnt = 0;
+        for (int j = i - 1; j >= 0 && bucket_of(key[j], maxf) == b; --j) {
+            if (i - j > kMaxRun) {
+                over = true;
+                break;
+            }
+            cnt += before(key[j], idx[j], k[q], id[q]) ? 1 : 0;
+            first = j;
+        }
+        for (int j = i + 1; j < n && bucket_of(key[j], maxf) == b; ++j) {
+            if (j - i > kMaxRun) {
+                over = true;
+                break;
+            }
+            cnt += before(key[j], idx[j], k[q], id[q]) ? 1 : 0;
+        }
+        pos[q] = first + cnt;
+    }
+    if (over) atomicOr(sflag, 1);
+    __syncthreads();
+    if (*reinterpret_cast<volatile int*>(sflag)) return false;
+#pragma unroll
+    for (int q = 0; q < kSortPer; ++q)
+        if (pos[q] >= 0) {
+            key[pos[q]] = k[q];
+            idx[pos[q]] = id[q];
+        }
+    __syncthreads();
+    return true;
 }
 
 // Exclusion bitmap of the accepted corners over the ROI (one bit per ROI
@@ -938,6 +992,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                 cidx[o] = si[c0 + j];
                 ++o;
             }
+            if (tid == 0) S.sflag = 0;
             __syncthreads();
             if (ns == 0) continue;
             // exact order of the survivors (a merge-sorted big bucket is in order already)
@@ -956,7 +1011,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                             cidx[lane] = id;
                         }
                     }
-                } else {
+                } else if (ns > (unsigned)(kSortPer * SEL_THREADS) ||
+                           !run_rank_sort(ckey, cidx, (int)ns, maxf, &S.sflag)) {
                     int np = 1;
                     while (np < (int)ns) np <<= 1;
                     for (int j = ns + tid; j < np; j += SEL_THREADS) {

@@ -1966,6 +1966,10 @@ struct stabgpu_stream {
     DetectScratch ds{};
     double2 *pts = nullptr, *nxt = nullptr, *fwd = nullptr, *trk_prev = nullptr, *trk_cur = nullptr;
     int *npts = nullptr, *nnxt = nullptr, *trk_n = nullptr;
+    // third point buffer: a re-detection (detect stream) writes it while the
+    // frame's K5 step reads pts and its compaction writes nxt (motion stream)
+    double2* det = nullptr;
+    int* ndet = nullptr;
     int2* fit_pre = nullptr;  // per-CTA RANSAC results of the one-frame fit
     double* score = nullptr;
     uint8_t* keep = nullptr;
@@ -1982,6 +1986,20 @@ struct stabgpu_stream {
     // is composed (out_done[k]); pinned error word of the selector scan
     std::vector<cudaEvent_t> slot_free, out_done, in_done;
     int* err_host = nullptr;
+    // three compute streams: the motion chain (context stream: K1, K5 step,
+    // compaction, K6 fit, K7 scan), the release stream (smoothing + K8 compose
+    // of the released frame, behind that frame's scan) and the detect stream
+    // (the re-detection of frame kR beside its own K5 step; frame kR+1's K5
+    // waits for it).  motion_done[k]: the motion chain that read input slot k
+    // as its previous frame has run (the slot may be overwritten).
+    cudaStream_t rst = nullptr, dst = nullptr;
+    cudaEvent_t ev_scan = nullptr, ev_rel = nullptr, ev_det = nullptr, ev_motion = nullptr, ev_grow = nullptr;
+    std::vector<cudaEvent_t> motion_done;
+    bool det_wait = false, rel_any = false, grown = false, pops_pending = false;
+    // pop_async: records land in a pinned ring (a download into pageable memory
+    // would block the call) and reach the caller's pointers in wait_pops
+    stabgpu_frame_record* rec_host = nullptr;
+    std::vector<std::pair<stabgpu_frame_record*, int>> rec_owed;
     // per-frame CUDA graphs: each push's launch sequence (K1 levels, K5 step +
     // compaction + K6 fit or the detection, the K7 scan, and the smoothing +
     // K8 compose of the frame it releases) is stream-captured and launched as
@@ -2023,10 +2041,15 @@ int stream_grow(stabgpu_stream* s, long long need) {
     TRY(salloc(s, &c, nc));
     TRY(salloc(s, &pl, nc));
     if (s->fcap) {
+        // the release stream's smoothing wrote records and plans into the old blocks
+        if (s->rel_any) CUDA_TRY(cudaStreamWaitEvent(st, s->ev_rel, 0));
         CUDA_TRY(cudaMemcpyAsync(m, s->motion, sizeof(*m) * s->fcap, cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(r, s->rec, sizeof(*r) * s->fcap, cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(c, s->cum, sizeof(*c) * s->fcap, cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(pl, s->plan, sizeof(*pl) * s->fcap, cudaMemcpyDeviceToDevice, st));
+        // pops of frames released earlier read their records from the new block
+        CUDA_TRY(cudaEventRecord(s->ev_grow, st));
+        s->grown = true;
     }
     s->motion = m;
     s->rec = r;
@@ -2040,9 +2063,9 @@ bool graph_safe(const stabgpu_config& c) {
     return !detect_allocates(c.detect) && !fit_allocates(c.detect.max_corners);
 }
 
-// smoothing + K8 compose of released frame i into output slot i % ocap
+// smoothing + K8 compose of released frame i into output slot i % ocap (release stream)
 void stream_release_kernels(stabgpu_stream* s, long long i) {
-    cudaStream_t st = s->ctx->stream;
+    cudaStream_t st = s->rst;
     const int r = s->cfg.smooth_radius;
     launch_plan_smooth(s->cum, s->pushed, s->complete, i, 1, r, s->rec, s->plan,
                        PlanGeom{s->w, s->h, s->chroma ? s->cw : 0, s->chroma ? s->ch : 0, s->cfg.crop_ratio}, st);
@@ -2060,9 +2083,11 @@ void stream_release_kernels(stabgpu_stream* s, long long i) {
 // after frame i's release kernels were issued: its input slot is free and
 // its output slot downloadable (events), and it is queued for pop
 void stream_release_done(stabgpu_stream* s, long long i) {
-    cudaStream_t st = s->ctx->stream;
+    cudaStream_t st = s->rst;
     cudaEventRecord(s->slot_free[(size_t)(i % s->cap)], st);
     cudaEventRecord(s->out_done[(size_t)(i % s->ocap)], st);
+    cudaEventRecord(s->ev_rel, st);
+    s->rel_any = true;
     s->ready.push_back(i);
 }
 
@@ -2082,19 +2107,8 @@ int stream_release_count(const stabgpu_stream* s, long long* count) {
     return STABGPU_OK;
 }
 
-int stream_release_ready(stabgpu_stream* s) {
-    long long n;
-    TRY(stream_release_count(s, &n));
-    for (long long k = 0; k < n; ++k) stream_release_kernels(s, s->next + k);
-    TRY(check_launch("stream compose"));
-    for (long long k = 0; k < n; ++k) stream_release_done(s, s->next + k);
-    s->next += n;
-    return STABGPU_OK;
-}
-
-// launches a captured push graph through the executable graph of its topology
-int stream_launch_graph(stabgpu_stream* s, int key, cudaGraph_t g) {
-    cudaStream_t st = s->ctx->stream;
+// launches a captured graph through the executable graph of its topology
+int stream_launch_graph(stabgpu_stream* s, int key, cudaGraph_t g, cudaStream_t st) {
     auto it = s->execs.find(key);
     if (it != s->execs.end()) {
         cudaGraphExecUpdateResultInfo info;
@@ -2111,6 +2125,38 @@ int stream_launch_graph(stabgpu_stream* s, int key, cudaGraph_t g) {
         it = s->execs.emplace(key, ex).first;
     }
     CUDA_TRY(cudaGraphLaunch(it->second, st));
+    return STABGPU_OK;
+}
+
+// Runs `body` (kernel launches on st) as one CUDA graph keyed by its topology,
+// or directly when graphs are off.
+template <typename F>
+int stream_run(stabgpu_stream* s, bool graph, int key, cudaStream_t st, const char* what, F body) {
+    if (graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    body();
+    int rc = check_launch(what);
+    if (graph) {
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (rc == STABGPU_OK && e != cudaSuccess)
+            rc = set_err(STABGPU_CUDA, "stream: graph capture failed: %s", cudaGetErrorString(e));
+        if (rc == STABGPU_OK) rc = stream_launch_graph(s, key, g, st);
+        if (g) cudaGraphDestroy(g);
+        s->ctx->stats.launches += 1;
+    }
+    return rc;
+}
+
+// releases frames [s->next, s->next + n) on the release stream, behind the
+// scan of the newest frame (ev_scan)
+int stream_release(stabgpu_stream* s, long long n) {
+    if (n <= 0) return STABGPU_OK;
+    CUDA_TRY(cudaStreamWaitEvent(s->rst, s->ev_scan, 0));
+    TRY(stream_run(s, s->graphs && n == 1, 0x300, s->rst, "stream compose", [&] {
+        for (long long k = 0; k < n; ++k) stream_release_kernels(s, s->next + k);
+    }));
+    for (long long k = 0; k < n; ++k) stream_release_done(s, s->next + k);
+    s->next += n;
     return STABGPU_OK;
 }
 
@@ -2172,7 +2218,8 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
         (rc = salloc(s, &s->trk_prev, maxc)) || (rc = salloc(s, &s->trk_cur, maxc)) ||
         (rc = salloc(s, &s->npts, 1)) || (rc = salloc(s, &s->nnxt, 1)) || (rc = salloc(s, &s->trk_n, 1)) ||
         (rc = salloc(s, &s->score, maxc)) || (rc = salloc(s, &s->keep, maxc)) || (rc = salloc(s, &s->work, 1)) ||
-        (rc = salloc(s, &s->fit_pre, 2 * kFitPreCtas)))
+        (rc = salloc(s, &s->fit_pre, 2 * kFitPreCtas)) || (rc = salloc(s, &s->det, maxc)) ||
+        (rc = salloc(s, &s->ndet, 1)))
         return fail(rc);
     if ((rc = stream_grow(s, 256))) return fail(rc);
     s->cscratch_bytes = compose_scratch_bytes(w, h, s->cw, s->ch, 1);
@@ -2182,12 +2229,20 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     s->graphs = graph_safe(cfg);
     s->slot_free.resize(s->cap);
     s->in_done.resize(s->cap);
+    s->motion_done.resize(s->cap);
     s->out_done.resize(s->ocap);
-    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done})
+    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done, &s->motion_done})
         for (auto& e : *v)
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
                 return fail(set_err(STABGPU_CUDA, "stream: event creation failed"));
-    if (cudaMallocHost((void**)&s->err_host, sizeof(int)) != cudaSuccess)
+    for (cudaEvent_t* e : {&s->ev_scan, &s->ev_rel, &s->ev_det, &s->ev_motion, &s->ev_grow})
+        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
+            return fail(set_err(STABGPU_CUDA, "stream: event creation failed"));
+    if (cudaStreamCreateWithFlags(&s->rst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s->dst, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(set_err(STABGPU_CUDA, "stream: stream creation failed"));
+    if (cudaMallocHost((void**)&s->err_host, sizeof(int)) != cudaSuccess ||
+        cudaMallocHost((void**)&s->rec_host, sizeof(stabgpu_frame_record) * s->ocap) != cudaSuccess)
         return fail(set_err(STABGPU_CUDA, "stream: pinned allocation failed"));
     *s->err_host = 0;
     if ((rc = init_plan_state(ctx, cfg, &s->ps))) return fail(rc);
@@ -2220,10 +2275,14 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     const size_t slot = (size_t)(f % s->cap);
     uint8_t* fy = s->ring_y + slot * fl;
     // upload on the input copy stream once the slot's previous frame was
-    // composed; the compute stream waits for it.  The host buffers are read
-    // before push returns (the upload is waited for at the end), while the
-    // previous frames' compute and downloads keep running.
-    if (f >= s->cap) CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->slot_free[slot], 0));
+    // composed (and the motion chain that read it as its previous frame has
+    // run); the motion stream waits for it.  The host buffers are read before
+    // push returns (the upload is waited for at the end), while the previous
+    // frames' compute and downloads keep running.
+    if (f >= s->cap) {
+        CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->slot_free[slot], 0));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->motion_done[slot], 0));
+    }
     CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyDefault, ctx->cin));
     if (s->chroma) {
         CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyDefault, ctx->cin));
@@ -2239,19 +2298,30 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         return rc;
     }
     const bool detect = f == 0 || f % R == 0;
-    const bool graph = s->graphs && nrel <= 1;
-    if (graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    PlaneBatch cur{fy, fl, s->w, s->h};
+    // detection of this frame (flow.cpp:303-308, 327-330) on the detect stream,
+    // beside the frame's own K5 step: it reads the frame only.  It writes the
+    // third point buffer, last used by the motion chain R frames ago.
+    if (detect) {
+        CUDA_TRY(cudaStreamWaitEvent(s->dst, s->in_done[slot], 0));
+        if (f > 0) CUDA_TRY(cudaStreamWaitEvent(s->dst, s->ev_motion, 0));
+        TRY(stream_run(s, s->graphs, 0x200, s->dst, "stream detect", [&] {
+            launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->det, s->score, s->ndet, s->dst);
+        }));
+        CUDA_TRY(cudaEventRecord(s->ev_det, s->dst));
+        ctx->stats.launches += 3;
+    }
+    // the previous frame's re-detection feeds this frame's K5 step
+    if (s->det_wait) {
+        CUDA_TRY(cudaStreamWaitEvent(st, s->ev_det, 0));
+        s->det_wait = false;
+    }
     // K1: the pyramid of the current frame, levels >= 1 into slot f & 1; no
     // copies: level 0 stays in the ring, and the tracker sees (previous,
     // current) through a pyramid view whose frame stride is the signed
     // distance between the two slots
     DevPyramid& P = s->P;
     const int cs = (int)(f & 1), ps = cs ^ 1;
-    for (int l = 1; l < P.levels; ++l)
-        launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
-                             P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, st);
-    ctx->stats.launches += P.levels - 1;
-    PlaneBatch cur{fy, fl, s->w, s->h};
     DevPyramid V = P;  // frame 0 = previous, frame 1 = current
     if (f > 0) {
         const uint8_t* py = s->ring_y + (size_t)((f - 1) % s->cap) * fl;
@@ -2262,50 +2332,51 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
             V.stride[l] = (size_t)((ptrdiff_t)(cs - ps) * (ptrdiff_t)P.stride[l]);
         }
     }
-    if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88) + detection (flow.cpp:303-308)
-        static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
-        cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st);
-        launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
-    } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
-        LkStep k;
-        std::memset(&k, 0, sizeof k);
-        k.pyr = V;
-        k.frame0 = 0;
-        k.seg_len = R;
-        k.t = 1;
-        k.nseg = 1;
-        k.max_pts = maxc;
-        k.pts = s->pts;
-        k.npts = s->npts;
-        k.fwd = s->fwd;
-        k.keep = s->keep;
-        k.nframes = 2;
-        k.mode = 1;
-        k.work = s->work;
-        launch_lk(k, cfg.flow, st);
-        launch_compact(k, s->nxt, s->nnxt, s->trk_prev, s->trk_cur, s->trk_n, 1, st);
-        launch_fit(s->trk_prev, s->trk_cur, s->trk_n, maxc, 1, f, cfg, s->motion + f, st, 0, s->fit_pre);
+    TRY(stream_run(s, s->graphs, 0x100 | (f == 0 ? 1 : 0), st, "stream push", [&] {
+        for (int l = 1; l < P.levels; ++l)
+            launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
+                                 P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, st);
+        ctx->stats.launches += P.levels - 1;
+        if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88)
+            static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
+            cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st);
+        } else {  // Tracker::advance (flow.cpp:316-330): forward + weed, then fit
+            LkStep k;
+            std::memset(&k, 0, sizeof k);
+            k.pyr = V;
+            k.frame0 = 0;
+            k.seg_len = R;
+            k.t = 1;
+            k.nseg = 1;
+            k.max_pts = maxc;
+            k.pts = s->pts;
+            k.npts = s->npts;
+            k.fwd = s->fwd;
+            k.keep = s->keep;
+            k.nframes = 2;
+            k.mode = 1;
+            k.work = s->work;
+            launch_lk(k, cfg.flow, st);
+            launch_compact(k, s->nxt, s->nnxt, s->trk_prev, s->trk_cur, s->trk_n, 1, st);
+            launch_fit(s->trk_prev, s->trk_cur, s->trk_n, maxc, 1, f, cfg, s->motion + f, st, 0, s->fit_pre);
+            ctx->stats.launches += 3;
+        }
+        // K7: selector + trajectory prefix for this frame
+        launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
+    }));
+    CUDA_TRY(cudaEventRecord(s->ev_scan, st));
+    CUDA_TRY(cudaEventRecord(s->ev_motion, st));
+    if (f > 0) {  // this chain read the previous frame's slot
+        CUDA_TRY(cudaEventRecord(s->motion_done[(size_t)((f - 1) % s->cap)], st));
         std::swap(s->pts, s->nxt);
         std::swap(s->npts, s->nnxt);
-        if (f % R == 0) launch_detect(cur, 1, cfg.detect, s->roi, s->ds, s->pts, s->score, s->npts, st);
-        ctx->stats.launches += 3 + (f % R == 0 ? 3 : 0);
     }
-    // K7: selector + trajectory prefix for this frame
-    launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
-    for (long long k = 0; k < nrel; ++k) stream_release_kernels(s, s->next + k);
-    int rc = check_launch("stream push");
-    if (graph) {
-        cudaGraph_t g = nullptr;
-        const cudaError_t e = cudaStreamEndCapture(st, &g);
-        if (rc == STABGPU_OK && e != cudaSuccess)
-            rc = set_err(STABGPU_CUDA, "stream: graph capture failed: %s", cudaGetErrorString(e));
-        if (rc == STABGPU_OK) rc = stream_launch_graph(s, (f == 0 ? 1 : 0) | (detect ? 2 : 0) | (int)(nrel << 2), g);
-        if (g) cudaGraphDestroy(g);
-        ctx->stats.launches += 1;
+    if (detect) {  // the fresh corners replace the carried points (flow.cpp:327-330)
+        std::swap(s->pts, s->det);
+        std::swap(s->npts, s->ndet);
+        s->det_wait = true;
     }
-    TRY(rc);
-    for (long long k = 0; k < nrel; ++k) stream_release_done(s, s->next + k);
-    s->next += nrel;
+    TRY(stream_release(s, nrel));
     CUDA_TRY(cudaEventSynchronize(s->in_done[slot]));  // the caller's buffers are consumed
     if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
     return STABGPU_OK;
@@ -2316,38 +2387,61 @@ int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready) {
     if (s->pushed < 2) return set_err(STABGPU_INVALID_INPUT, "stabilization needs at least 2 frames");
     cudaSetDevice(s->ctx->device);
     s->complete = true;
-    TRY(stream_release_ready(s));
+    long long n;
+    TRY(stream_release_count(s, &n));
+    TRY(stream_release(s, n));
     if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
     return STABGPU_OK;
 }
 
-int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
-                       stabgpu_frame_record* record) {
+int stabgpu_stream_pop_async(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
+                             stabgpu_frame_record* record) {
     if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
     if (s->ready_head >= s->ready.size()) return set_err(STABGPU_SEQUENCING, "stream: no frame ready");
     cudaSetDevice(s->ctx->device);
-    cudaStream_t st = s->ctx->stream;
     const long long i = s->ready[s->ready_head++];
     if (s->ready_head == s->ready.size()) {
         s->ready.clear();
         s->ready_head = 0;
     }
     // the download waits for this frame's compose only (frames pushed since
-    // keep computing on the compute stream)
+    // keep computing on the other streams)
     const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch, o = (size_t)(i % s->ocap);
     cudaStream_t co = s->ctx->cout;
-    (void)st;
     CUDA_TRY(cudaStreamWaitEvent(co, s->out_done[o], 0));
+    if (s->grown) CUDA_TRY(cudaStreamWaitEvent(co, s->ev_grow, 0));  // the records may have moved
     if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDefault, co));
     if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDefault, co));
     if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDefault, co));
-    if (record) CUDA_TRY(cudaMemcpyAsync(record, s->rec + i, sizeof *record, cudaMemcpyDefault, co));
+    if (record) {
+        if ((int)s->rec_owed.size() >= s->ocap) TRY(stabgpu_stream_wait_pops(s));
+        const int j = (int)s->rec_owed.size();
+        CUDA_TRY(cudaMemcpyAsync(s->rec_host + j, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, co));
+        s->rec_owed.emplace_back(record, j);
+    }
     // the selector scan's error word (written before the frame was released)
     CUDA_TRY(cudaMemcpyAsync(s->err_host, reinterpret_cast<int*>(s->ps + 1), sizeof(int), cudaMemcpyDeviceToHost, co));
-    CUDA_TRY(cudaStreamSynchronize(co));
-    if (*s->err_host) TRY(plan_error(s->ctx, s->ps));
+    s->pops_pending = true;
     if (index) *index = i;
     return STABGPU_OK;
+}
+
+int stabgpu_stream_wait_pops(stabgpu_stream* s) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    if (!s->pops_pending) return STABGPU_OK;
+    cudaSetDevice(s->ctx->device);
+    s->pops_pending = false;
+    CUDA_TRY(cudaStreamSynchronize(s->ctx->cout));
+    for (const auto& o : s->rec_owed) *o.first = s->rec_host[o.second];
+    s->rec_owed.clear();
+    if (*s->err_host) TRY(plan_error(s->ctx, s->ps));
+    return STABGPU_OK;
+}
+
+int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* ocb, uint8_t* ocr,
+                       stabgpu_frame_record* record) {
+    TRY(stabgpu_stream_pop_async(s, index, oy, ocb, ocr, record));
+    return stabgpu_stream_wait_pops(s);
 }
 
 int stabgpu_stream_set_graphs(stabgpu_stream* s, int on) {
@@ -2362,12 +2456,19 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
     cudaStreamSynchronize(s->ctx->stream);
     cudaStreamSynchronize(s->ctx->cin);
     cudaStreamSynchronize(s->ctx->cout);
+    if (s->rst) cudaStreamSynchronize(s->rst);
+    if (s->dst) cudaStreamSynchronize(s->dst);
     for (void* p : s->allocs) cudaFree(p);
-    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done})
+    for (auto* v : {&s->slot_free, &s->in_done, &s->out_done, &s->motion_done})
         for (auto e : *v)
             if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {s->ev_scan, s->ev_rel, s->ev_det, s->ev_motion, s->ev_grow})
+        if (e) cudaEventDestroy(e);
+    if (s->rst) cudaStreamDestroy(s->rst);
+    if (s->dst) cudaStreamDestroy(s->dst);
     for (auto& kv : s->execs) cudaGraphExecDestroy(kv.second);
     if (s->err_host) cudaFreeHost(s->err_host);
+    if (s->rec_host) cudaFreeHost(s->rec_host);
     delete s;
     return STABGPU_OK;
 }

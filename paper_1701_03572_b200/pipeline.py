@@ -418,7 +418,13 @@ class StreamStabilizer:
     is bit-identical to Stage I's output for that frame."""
 
     def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0,
-                 graphs: bool = True):
+                 graphs: bool = True, overlap_pops: bool = False):
+        # overlap_pops: push() queues the downloads of the frames released by
+        # the PREVIOUS push (stabgpu_stream_pop_async), uploads and estimates
+        # the new frame, then waits for them - the D2H of frame k-r overlaps
+        # the H2D of frame k+1; frames come back one push late, same bytes
+        self.overlap_pops = overlap_pops
+        self._owed = 0
         self.w, self.h, self.cw, self.ch = w, h, cw, ch
         self._c = cfg.c()
         self._lib = load()
@@ -429,8 +435,9 @@ class StreamStabilizer:
         # per-frame CUDA graphs (default) or one launch per kernel; same results
         check(self._lib.stabgpu_stream_set_graphs(self._h, int(graphs)))
 
-    def _pop_all(self, n: int):
+    def _pop_all(self, n: int, wait: bool = True):
         out = []
+        pop = self._lib.stabgpu_stream_pop if wait else self._lib.stabgpu_stream_pop_async
         for _ in range(n):
             idx = C.c_int64()
             y = np.empty((self.h, self.w), np.uint8)
@@ -439,22 +446,33 @@ class StreamStabilizer:
                 cb = np.empty((self.ch, self.cw), np.uint8)
                 cr = np.empty((self.ch, self.cw), np.uint8)
             rec = np.zeros(1, RECORD_DT)
-            check(self._lib.stabgpu_stream_pop(self._h, C.byref(idx), _vp(y), _vp(cb), _vp(cr), _vp(rec)))
-            out.append((idx.value, y, cb, cr, rec[0]))
+            check(pop(self._h, C.byref(idx), _vp(y), _vp(cb), _vp(cr), _vp(rec)))
+            out.append([idx.value, y, cb, cr, rec])
         return out
+
+    @staticmethod
+    def _frames(popped):
+        return [(i, y, cb, cr, rec[0]) for i, y, cb, cr, rec in popped]
 
     def push(self, y: np.ndarray, cb: np.ndarray | None = None, cr: np.ndarray | None = None):
         y = np.ascontiguousarray(y, np.uint8)
         cb = None if cb is None else np.ascontiguousarray(cb, np.uint8)
         cr = None if cr is None else np.ascontiguousarray(cr, np.uint8)
         n = C.c_int()
+        if self.overlap_pops:
+            late = self._pop_all(self._owed, wait=False)
+            check(self._lib.stabgpu_stream_push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
+            check(self._lib.stabgpu_stream_wait_pops(self._h))
+            self._owed = n.value
+            return self._frames(late)
         check(self._lib.stabgpu_stream_push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
-        return self._pop_all(n.value)
+        return self._frames(self._pop_all(n.value))
 
     def finish(self):
         n = C.c_int()
         check(self._lib.stabgpu_stream_finish(self._h, C.byref(n)))
-        return self._pop_all(n.value)
+        self._owed = 0
+        return self._frames(self._pop_all(n.value))
 
     def close(self):
         if self._h:

@@ -444,7 +444,8 @@ def _release_schedule(n, r):
 
 
 @pytest.mark.parametrize("mode,ransac,smooth,graphs", [("similarity", 0, 5, True), ("hybrid", 200, 4, True),
-                                                         ("rigid", 100, 9, True), ("hybrid", 200, 4, False)])
+                                                         ("rigid", 100, 9, True), ("hybrid", 200, 4, False),
+                                                         ("similarity", 0, 1, True), ("similarity", 0, 1, False)])
 def test_stream_equals_stage1(mode, ransac, smooth, graphs):
     """Stage II (push one frame at a time) releases frames on the reference's
     schedule (latency r, first emission at 2r) and each released frame and
@@ -508,6 +509,33 @@ def test_stream_equals_oracle_config(name, frames):
 
 def orc_checker():
     return _oracle.oracle()
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_stream_overlapped_pops_long(graphs):
+    """pop_async / wait_pops (downloads of the frames released by the previous
+    push overlap the next upload) over a stream long enough to grow the
+    frame-indexed arrays (256 frames) and wrap the input ring many times, with
+    the motion, release and detect chains on their three streams: frames come
+    back one push late and are bitwise Stage I."""
+    y = _data.video(w=128, h=96, frames=300, jit_t=1.5)[0]
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=50, smooth=3, corners=40, levels=2, radius=7)
+    sy, _, _, srec = pipeline.stabilize_sequence(y, cfg)
+    s = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1], graphs=graphs, overlap_pops=True)
+    sched, tail = _release_schedule(len(y), cfg.smooth_radius)
+    got = []
+    for k in range(len(y)):
+        rel = s.push(y[k])
+        assert [r[0] for r in rel] == (sched[k - 1] if k else []), k
+        got += rel
+    rel = s.finish()
+    assert [r[0] for r in rel] == sched[-1] + tail
+    got += rel
+    s.close()
+    assert [g[0] for g in got] == list(range(len(y)))
+    for i, gy, _, _, grec in got:
+        assert np.array_equal(gy, sy[i]), i
+        assert grec.tobytes() == srec[i].tobytes(), i
 
 
 def test_stream_device_pointers():

@@ -2,7 +2,11 @@
 the C ABI (push frame k from a pinned array, pop into a pinned array).
 --device: frames already in HBM (push/pop device pointers); --nographs:
 one launch per kernel instead of the per-frame CUDA graph; --lag: pop one
-push late."""
+push late; --async: the frames released by the previous push are popped with
+stabgpu_stream_pop_async before the next push and waited for after it (their
+download overlaps the next upload); --depth N (default 2 with --async): the
+frames popped before push k are those released by push k-N, so their compose
+finished long before and the download runs beside the upload of frame k."""
 import ctypes as C
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,12 +33,16 @@ graphs = "--nographs" not in sys.argv
 assert lib.stabgpu_stream_set_graphs(hs, int(graphs)) == 0
 rec = np.zeros(1, pipeline.RECORD_DT)
 vp = lambda t, k: C.c_void_p(t[k].data_ptr())
+asyn = "--async" in sys.argv
+depth = int(sys.argv[sys.argv.index("--depth") + 1]) if "--depth" in sys.argv else 2
+owed = []  # --async: frames released by each push, not yet popped
 def pop_all(k):
+    pop = lib.stabgpu_stream_pop_async if asyn else lib.stabgpu_stream_pop
     for _ in range(k):
         idx = C.c_int64()
         j = 0
         # pop into the slot of the frame index (learned after the call: use a scratch slot first)
-        assert lib.stabgpu_stream_pop(hs, C.byref(idx), vp(outp[0], pop_all.n % n),
+        assert pop(hs, C.byref(idx), vp(outp[0], pop_all.n % n),
                                       vp(outp[1], pop_all.n % n) if col else None,
                                       vp(outp[2], pop_all.n % n) if col else None,
                                       C.c_void_p(rec.ctypes.data)) == 0
@@ -47,20 +55,27 @@ t0 = time.perf_counter()
 pending = 0
 for k in range(n):
     t1 = time.perf_counter()
+    if asyn and len(owed) >= depth:
+        pop_all(owed.pop(0))  # queue the downloads of the frames push k - depth released
     assert lib.stabgpu_stream_push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
                                    vp(pin[2], k) if col else None, C.byref(nr)) == 0
-    if lag:
+    if asyn:
+        assert lib.stabgpu_stream_wait_pops(hs) == 0
+        owed.append(nr.value - sum(owed))
+    elif lag:
         pop_all(pending)  # frames released by earlier pushes
         pending = nr.value - pending
     else:
         pop_all(nr.value)
     lat.append(time.perf_counter() - t1)
-if lag:
+if lag and not asyn:
     pop_all(pending)
 assert lib.stabgpu_stream_finish(hs, C.byref(nr)) == 0
 pop_all(nr.value)
+if asyn:
+    assert lib.stabgpu_stream_wait_pops(hs) == 0
 dt = time.perf_counter() - t0
 lib.stabgpu_stream_destroy(hs)
 lat = np.array(lat) * 1e3
-print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
+print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)} async={int(asyn) * depth}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
       f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out")
