@@ -938,8 +938,18 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         __syncthreads();
     }
     int marked = 0;  // corners [0, marked) are in the bitmap
-    // ---- C. chunks of whole buckets in score order
+    // ---- C. chunks of whole buckets in score order.  A chunk takes up to
+    // `che` candidates; the survivors of its prefilter must fit the chunk buffer
+    // (ch).  che adapts: once the accepted corners exclude nearly everything
+    // (few survivors per chunk) it doubles, up to 32 candidates per thread, so
+    // the tail of a long list costs a handful of passes instead of one
+    // barrier-bound pass per ch candidates; a chunk whose survivors overflow
+    // the buffer is retried with half the size (nothing was changed yet; at
+    // che == ch they always fit).  Any chunking is exact: the prefilter only
+    // drops candidates that conflict with corners accepted before the chunk.
     int b0 = 0;
+    unsigned che = (unsigned)ch;
+    const unsigned che_max = 32u * SEL_THREADS;
     while (b0 < kBuckets && nacc < maxc) {
         if (use_bm && marked < nacc) {  // the CTA marks the new corners' discs: (corner, row) items
             const int rows = 2 * R + 1;
@@ -953,9 +963,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             __threadfence_block();
             __syncthreads();
         }
-        int b1;  // largest run of whole buckets with <= ch candidates (at least one)
+        int b1;  // largest run of whole buckets with <= che candidates (at least one)
         {
-            const unsigned limit = S.bstart[b0] + (unsigned)ch;
+            const unsigned limit = S.bstart[b0] + che;
             int lo = b0 + 1, hi = kBuckets;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -965,27 +975,42 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             b1 = lo;
         }
         const unsigned c_lo = S.bstart[b0], c_hi = S.bstart[b1];
+        const int b0_run = b0;
         b0 = b1;
         if (c_hi == c_lo) continue;
-        const bool big = c_hi - c_lo > (unsigned)ch;  // one tie-heavy bucket: exact order in global first
+        const bool big = c_hi - c_lo > che;  // one tie-heavy bucket: exact order in global first
         if (big)
             global_merge_sort(sk + c_lo, si + c_lo, const_cast<unsigned long long*>(ck) + c_lo,
                               const_cast<unsigned*>(ci) + c_lo, c_hi - c_lo);
-        for (unsigned c0 = c_lo; c0 < c_hi && nacc < maxc; c0 += ch) {
-            const unsigned m = min((unsigned)ch, c_hi - c0);
+        bool rerun = false;
+        unsigned c0 = c_lo;
+        while (c0 < c_hi && nacc < maxc) {
+            const unsigned m = min(che, c_hi - c0);
             // prefilter: thread t tests the contiguous run [t*per, (t+1)*per)
             const unsigned per = (m + SEL_THREADS - 1) / SEL_THREADS;
             const unsigned j0 = min(tid * per, m), j1 = min(j0 + per, m);
-            unsigned alive = 0;  // bit q: candidate j0 + q survives (per <= 32: ch <= 32 * threads)
-            for (unsigned j = j0; j < j1; ++j) {
-                const unsigned id = si[c0 + j];
-                const int x = (int)(id % (unsigned)w), y = (int)(id / (unsigned)w);
-                const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
-                                       : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
-                if (!ex) alive |= 1u << (j - j0);
+            unsigned alive = 0;  // bit q: candidate j0 + q survives (per <= 32: che <= 32 * threads)
+            for (unsigned j = j0; j < j1; j += 8) {  // eight loads in flight per L2 latency
+                unsigned id[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) id[q] = j + q < j1 ? si[c0 + j + q] : 0xffffffffu;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (j + q >= j1) break;
+                    const int x = (int)(id[q] % (unsigned)w), y = (int)(id[q] / (unsigned)w);
+                    const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
+                                           : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
+                    if (!ex) alive |= 1u << (j + q - j0);
+                }
             }
             unsigned o = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
             const unsigned ns = S.total;
+            if (ns > (unsigned)ch) {  // the survivors overflow the chunk buffer: half the chunk
+                che = max((unsigned)ch, che >> 1);
+                if (big) continue;  // the same slice start, shorter
+                rerun = true;       // a shorter run of whole buckets
+                break;
+            }
             for (unsigned a = alive; a; a &= a - 1) {
                 const unsigned j = j0 + __ffs(a) - 1;
                 ckey[o] = sk[c0 + j];
@@ -994,6 +1019,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             }
             if (tid == 0) S.sflag = 0;
             __syncthreads();
+            c0 += m;
+            if (ns * 32 <= (unsigned)ch) che = min(che << 2, che_max);
+            else if (ns * 8 <= (unsigned)ch) che = min(che << 1, che_max);
+            else if (ns * 2 > (unsigned)ch) che = max((unsigned)ch, che >> 1);
             if (ns == 0) continue;
             // exact order of the survivors (a merge-sorted big bucket is in order already)
             if (!big) {
@@ -1076,7 +1105,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             }
             __syncthreads();
             nacc = S.nacc;
-            if (use_bm && c0 + ch < c_hi) {  // more slices of a big bucket follow: mark now
+            if (use_bm && c0 < c_hi) {  // more slices of a big bucket follow: mark now
                 const int rows = 2 * R + 1;
                 const long long items = (long long)(nacc - marked) * rows;
                 for (long long i = tid; i < items; i += SEL_THREADS) {
@@ -1089,6 +1118,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                 __syncthreads();
             }
         }
+        if (rerun) b0 = b0_run;
     }
     if (tid == 0) {
         out_n[d] = nacc;
