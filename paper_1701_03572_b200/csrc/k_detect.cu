@@ -945,11 +945,13 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     // the tail of a long list costs a handful of passes instead of one
     // barrier-bound pass per ch candidates; a chunk whose survivors overflow
     // the buffer is retried with half the size (nothing was changed yet; at
-    // che == ch they always fit).  Any chunking is exact: the prefilter only
+    // che <= ch they always fit); many survivors halve it (down to 256), so
+    // the early chunks mark their corners' discs before the neighbours of a
+    // strong corner are sorted and walked.  Any chunking is exact: the prefilter only
     // drops candidates that conflict with corners accepted before the chunk.
     int b0 = 0;
-    unsigned che = (unsigned)ch;
-    const unsigned che_max = 32u * SEL_THREADS;
+    const unsigned che_min = min(256u, (unsigned)ch), che_max = 32u * SEL_THREADS;
+    unsigned che = che_min;
     while (b0 < kBuckets && nacc < maxc) {
         if (use_bm && marked < nacc) {  // the CTA marks the new corners' discs: (corner, row) items
             const int rows = 2 * R + 1;
@@ -1006,7 +1008,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             unsigned o = block_excl_scan(__popc(alive), S.warp_tot, &S.total);
             const unsigned ns = S.total;
             if (ns > (unsigned)ch) {  // the survivors overflow the chunk buffer: half the chunk
-                che = max((unsigned)ch, che >> 1);
+                che = max(che_min, che >> 1);
                 if (big) continue;  // the same slice start, shorter
                 rerun = true;       // a shorter run of whole buckets
                 break;
@@ -1020,9 +1022,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             if (tid == 0) S.sflag = 0;
             __syncthreads();
             c0 += m;
-            if (ns * 32 <= (unsigned)ch) che = min(che << 2, che_max);
-            else if (ns * 8 <= (unsigned)ch) che = min(che << 1, che_max);
-            else if (ns * 2 > (unsigned)ch) che = max((unsigned)ch, che >> 1);
+            // the walk costs ~1.5 us per 32 survivors, a chunk ~6 us of barriers and
+            // latencies: aim at 2-8 walk batches per chunk
+            if (ns <= 16) che = min(che << 2, che_max);
+            else if (ns <= 64) che = min(che << 1, che_max);
+            else if (ns > 256) che = max(che_min, che >> 1);
             if (ns == 0) continue;
             // exact order of the survivors (a merge-sorted big bucket is in order already)
             if (!big) {
