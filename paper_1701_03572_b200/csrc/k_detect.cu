@@ -788,6 +788,23 @@ __global__ void __launch_bounds__(512) bucket_scatter_kernel(DetectScratch s, do
     }
 }
 
+// y = id / w for candidate indices id = y * w + x < 2^24 (frames up to 16.7M
+// pixels) by a 40-bit reciprocal: magic = ceil(2^40 / w) has error e = magic * w
+// - 2^40 < w < 2^16, and id * e < 2^40, so floor(id * magic / 2^40) is exact;
+// larger frames divide.
+constexpr unsigned kTopFirst = 4096;  // select: candidates bucketed before the first greedy chunks
+
+struct DivW {
+    unsigned long long magic;
+    unsigned w;
+    bool fast;
+    __device__ __forceinline__ void split(unsigned id, int& x, int& y) const {
+        const unsigned q = fast ? (unsigned)((id * magic) >> 40) : id / w;
+        y = (int)q;
+        x = (int)(id - q * w);
+    }
+};
+
 // K4: one CTA per detection frame.
 //   A. the candidates >= quality * max are bucketed by a monotone 13-bit
 //      truncated float key (histogram, scan, scatter) into sort_key/sort_idx,
@@ -866,6 +883,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     unsigned long long* sk = s.sort_key + (size_t)d * s.cap;
     unsigned* si = s.sort_idx + (size_t)d * s.cap;
 
+    int bc = kBuckets;  // round 0 takes the buckets [0, bc)
     // ---- A. histogram + exclusive scan + scatter into bucket order (or the
     // multi-CTA bucket kernels' result)
     if (s.bstart) {
@@ -875,8 +893,19 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     } else {
     for (int b = tid; b < kBuckets; b += SEL_THREADS) cursor[b] = 0;
     __syncthreads();
-    for (unsigned i = tid; i < n; i += SEL_THREADS)
-        if (ck[i] >= thrb) atomicAdd(&cursor[bucket_of(ck[i], maxf)], 1u);
+    // (eight independent loads per thread and pass: one CTA walks up to a ROI's
+    // worth of candidates, so the passes are bound by the load latency)
+    for (unsigned i0 = tid; i0 < n; i0 += 8 * SEL_THREADS) {
+        unsigned long long k[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned i = i0 + q * SEL_THREADS;
+            k[q] = i < n ? ck[i] : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (i0 + q * SEL_THREADS < n && k[q] >= thrb) atomicAdd(&cursor[bucket_of(k[q], maxf)], 1u);
+    }
     __syncthreads();
     {
         constexpr int PER = kBuckets / SEL_THREADS;
@@ -896,12 +925,40 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         if (tid == 0) S.bstart[kBuckets] = S.total;
     }
     __syncthreads();
-    for (unsigned i = tid; i < n; i += SEL_THREADS) {
-        const unsigned long long k = ck[i];
-        if (k < thrb) continue;
-        const unsigned pos = atomicAdd(&cursor[bucket_of(k, maxf)], 1u);
-        sk[pos] = k;
-        si[pos] = ci[i];
+    // Two rounds.  The scatter (two scattered global stores per candidate from
+    // one SM) is what a long list costs, and the greedy usually needs only its
+    // head: round 0 scatters the buckets [0, bc) holding the top ~kTopFirst
+    // candidates; if they run out before max_corners, round 1 re-buckets the
+    // rest, dropping every candidate that conflicts with a corner accepted so
+    // far (exact: the greedy would reject it) — in the dense regime (C1) that is
+    // nearly all of them.
+    if (S.total > 2u * kTopFirst) {
+        int lo = 1, hi = kBuckets;  // smallest b with bstart[b] >= kTopFirst
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (S.bstart[mid] >= kTopFirst) hi = mid;
+            else lo = mid + 1;
+        }
+        bc = lo;
+    }
+    for (unsigned i0 = tid; i0 < n; i0 += 8 * SEL_THREADS) {
+        unsigned long long k[8];
+        unsigned id[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned i = i0 + q * SEL_THREADS;
+            k[q] = i < n ? ck[i] : 0ull;
+            id[q] = i < n ? ci[i] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (i0 + q * SEL_THREADS >= n || k[q] < thrb) continue;
+            const unsigned b = bucket_of(k[q], maxf);
+            if ((int)b >= bc) continue;
+            const unsigned pos = atomicAdd(&cursor[b], 1u);
+            sk[pos] = k[q];
+            si[pos] = id[q];
+        }
     }
     __threadfence_block();
     __syncthreads();
@@ -937,6 +994,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         __threadfence_block();
         __syncthreads();
     }
+    DivW dw;
+    dw.w = (unsigned)w;
+    dw.magic = ((1ull << 40) + (unsigned)w - 1) / (unsigned)w;
+    dw.fast = s.cap <= (1u << 24) && (unsigned long long)w * (unsigned)(roi.y1 + 1) <= (1ull << 24) && w >= 16 && w < 65536;
     int marked = 0;  // corners [0, marked) are in the bitmap
     // ---- C. chunks of whole buckets in score order.  A chunk takes up to
     // `che` candidates; the survivors of its prefilter must fit the chunk buffer
@@ -952,7 +1013,108 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     int b0 = 0;
     const unsigned che_min = min(256u, (unsigned)ch), che_max = 32u * SEL_THREADS;
     unsigned che = che_min;
-    while (b0 < kBuckets && nacc < maxc) {
+    for (int round = 0; round < 2; ++round) {
+    int b_end = bc;
+    if (round == 1) {
+        if (bc >= kBuckets || nacc >= maxc) break;
+        // ---- round 1: the buckets [bc, kBuckets) minus the candidates excluded
+        // by the corners accepted so far, re-bucketed from position 0 (counts,
+        // then cursors, in S.bstart itself: the chunk buffer and the grid are live)
+        if (use_bm && marked < nacc) {
+            const int rows = 2 * R + 1;
+            const long long items = (long long)(nacc - marked) * rows;
+            for (long long i = tid; i < items; i += SEL_THREADS) {
+                const int k = marked + (int)(i / rows), dy = (int)(i % rows) - R;
+                const short2 q = axy[k];
+                mark_row(bm, wr, rw, rh, q.x - roi.x0, q.y - roi.y0, dy, md2, S.hw);
+            }
+            marked = nacc;
+        }
+        for (int b = tid; b <= kBuckets; b += SEL_THREADS) S.bstart[b] = 0;
+        __threadfence_block();
+        __syncthreads();
+        auto keeps = [&](unsigned long long k, unsigned id, unsigned& b) {
+            if (k < thrb) return false;
+            b = bucket_of(k, maxf);
+            if ((int)b < bc) return false;
+            int x, y;
+            dw.split(id, x, y);
+            return !(use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
+                            : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2));
+        };
+        for (unsigned i0 = tid; i0 < n; i0 += 4 * SEL_THREADS) {
+            unsigned long long k[4];
+            unsigned id[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned i = i0 + q * SEL_THREADS;
+                k[q] = i < n ? ck[i] : 0ull;
+                id[q] = i < n ? ci[i] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                unsigned b;
+                if (i0 + q * SEL_THREADS < n && keeps(k[q], id[q], b)) atomicAdd(&S.bstart[b], 1u);
+            }
+        }
+        __syncthreads();
+        {
+            constexpr int PER = kBuckets / SEL_THREADS;
+            unsigned v[PER], sum = 0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                v[k] = S.bstart[tid * PER + k];
+                sum += v[k];
+            }
+            unsigned off = block_excl_scan(sum, S.warp_tot, &S.total);
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                S.bstart[tid * PER + k] = off;  // the bucket's cursor during the scatter
+                off += v[k];
+            }
+        }
+        __syncthreads();
+        for (unsigned i0 = tid; i0 < n; i0 += 4 * SEL_THREADS) {
+            unsigned long long k[4];
+            unsigned id[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned i = i0 + q * SEL_THREADS;
+                k[q] = i < n ? ck[i] : 0ull;
+                id[q] = i < n ? ci[i] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                unsigned b;
+                if (i0 + q * SEL_THREADS >= n || !keeps(k[q], id[q], b)) continue;
+                const unsigned pos = atomicAdd(&S.bstart[b], 1u);
+                sk[pos] = k[q];
+                si[pos] = id[q];
+            }
+        }
+        __threadfence_block();
+        __syncthreads();
+        {
+            // the cursors ended at the next bucket's start: shift them back by one
+            constexpr int PER = kBuckets / SEL_THREADS;
+            unsigned v[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int b = tid * PER + k;
+                v[k] = b ? S.bstart[b - 1] : 0u;
+            }
+            const unsigned tot = S.bstart[kBuckets - 1];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < PER; ++k) S.bstart[tid * PER + k] = v[k];
+            if (tid == 0) S.bstart[kBuckets] = tot;
+            __syncthreads();
+        }
+        b0 = bc;
+        b_end = kBuckets;
+        che = min(che, (unsigned)ch / 2);
+    }
+    while (b0 < b_end && nacc < maxc) {
         if (use_bm && marked < nacc) {  // the CTA marks the new corners' discs: (corner, row) items
             const int rows = 2 * R + 1;
             const long long items = (long long)(nacc - marked) * rows;
@@ -968,7 +1130,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
         int b1;  // largest run of whole buckets with <= che candidates (at least one)
         {
             const unsigned limit = S.bstart[b0] + che;
-            int lo = b0 + 1, hi = kBuckets;
+            int lo = b0 + 1, hi = b_end;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 if (S.bstart[mid] <= limit) lo = mid;
@@ -999,7 +1161,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (j + q >= j1) break;
-                    const int x = (int)(id[q] % (unsigned)w), y = (int)(id[q] / (unsigned)w);
+                    int x, y;
+                    dw.split(id[q], x, y);
                     const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
                                            : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
                     if (!ex) alive |= 1u << (j + q - j0);
@@ -1063,8 +1226,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     int x = 0, y = 0;
                     bool ok = false;
                     if (j < ns) {
-                        x = (int)(cidx[j] % (unsigned)w);
-                        y = (int)(cidx[j] / (unsigned)w);
+                        dw.split(cidx[j], x, y);
                         ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
                     }
                     const unsigned live = __ballot_sync(0xffffffffu, ok);
@@ -1123,6 +1285,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             }
         }
         if (rerun) b0 = b0_run;
+    }
     }
     if (tid == 0) {
         out_n[d] = nacc;
