@@ -1340,7 +1340,36 @@ std::vector<long long> chunk_bounds(long long n, size_t frame_bytes) {
     std::vector<long long> sizes, tail;
     long long rem = n;
     if (flat) rem = 0;
-    for (long long f = 0; flat && f < n; f += 60) sizes.push_back(std::min<long long>(60, n - f));
+    // flat chunks: each chunk's motion costs ~1 ms of launch- and latency-bound
+    // work whatever its size (one select CTA per detection frame, one warp per
+    // LK chain), so small frames take chunks of ~128 MB (at least 60 frames, at
+    // most half the sequence so copies and compute still overlap): C1 runs as
+    // 2 x 150 frames, C2 as 140-frame chunks
+    long long cf = 60;
+    if (flat) {
+        if (const char* e = getenv("STABGPU_CHUNK_FRAMES")) cf = std::max(1, atoi(e));
+        else {
+            cf = (long long)((128ull << 20) / std::max<size_t>(frame_bytes, 1)) / 10 * 10;
+            cf = std::max<long long>(60, std::min<long long>(cf, (n + 1) / 2));
+        }
+    }
+    if (flat && n >= 3 * cf && cf >= 80 && !getenv("STABGPU_NO_FLAT_RAMP")) {
+        // quarter and half chunks at both ends: the first motion starts and the
+        // last download ends sooner
+        const long long q = cf / 4 / 5 * 5, h2 = cf / 2 / 5 * 5;
+        sizes.push_back(q);
+        sizes.push_back(h2);
+        long long mid = n - 2 * (q + h2);
+        while (mid > 0) {
+            const long long c = std::min(cf, mid);
+            sizes.push_back(c);
+            mid -= c;
+        }
+        sizes.push_back(h2);
+        sizes.push_back(q);
+    } else {
+        for (long long f = 0; flat && f < n; f += cf) sizes.push_back(std::min<long long>(cf, n - f));
+    }
     for (long long r : ramp)
         if (rem > r) {
             sizes.push_back(r);
