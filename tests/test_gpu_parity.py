@@ -149,6 +149,25 @@ def test_detect_cut_redo(orc):
         assert np.array_equal(xg, xo) and np.array_equal(sg.view(np.uint64), so.view(np.uint64))
 
 
+def test_detect_chunk_growth_and_retry(orc):
+    """K4's adaptive chunks: a few very strong clusters (their neighbours fill
+    the top of the list and are nearly all excluded, so the chunk size grows to
+    its maximum) followed by tens of thousands of weak, well separated
+    candidates (a maximum-size chunk whose survivors overflow the chunk buffer
+    and must be retried smaller).  With and without the candidate cut, one
+    round (max_corners reached in the list's head) and two (re-bucketed rest)."""
+    rng = np.random.default_rng(11)
+    f = rng.integers(120, 136, size=(480, 640)).astype(np.uint8)     # weak texture everywhere
+    for cy, cx in ((100, 120), (240, 330), (380, 520), (110, 500)):   # strong clusters
+        f[cy - 12:cy + 12, cx - 12:cx + 12] = rng.integers(0, 256, size=(24, 24))
+    for corners, dist, q in ((6000, 1.5, 0.0005), (3000, 2.0, 0.001), (400, 6.0, 0.001), (150, 45.0, 0.0005)):
+        cfg = DetectConfig(max_corners=corners, min_distance=dist, quality_level=q, roi_margin=0.05)
+        xg, sg = stab.detect_corners(f, cfg)
+        xo, so = orc.detect_corners(f, cfg)
+        assert len(xo) > 50
+        assert np.array_equal(xg, xo) and np.array_equal(sg.view(np.uint64), so.view(np.uint64))
+
+
 @pytest.mark.parametrize("w,h", [(1920, 1080), (640, 480)])
 def test_detect_full_size(orc, w, h):
     y = _data.video(w, h, frames=1, tex=2048, blobs=1600)[0][0]
