@@ -32,6 +32,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 # frames per config (SURVEY §8d parity runs)
 FRAMES = {"c1": 300, "c2": 600, "c3": 100, "c4": 100}
+if os.environ.get("STABGPU_PARITY_FULL"):  # every config at BASELINE's full length (profiles/r2_parity_full.log)
+    FRAMES.update({"c3": 1000, "c4": 500})
 POS_TOL = 0.01  # px, north_star
 
 
