@@ -679,14 +679,17 @@ constexpr int MAX_CELLS = 8192;
 constexpr int SMEM_CORNERS = 8192;
 
 __device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy, const int* anext, int gw,
-                                          int gh, int cell, int rx0, int ry0, double md2) {
+                                          int gh, int cell, int rx0, int ry0, unsigned imd2) {
+    // imd2 = ceil(min_distance^2): for the integer d2 = dx*dx + dy*dy (coordinates
+    // are 16-bit, so it fits 32 bits) d2 < md2 <=> d2 < imd2 — the reference's
+    // double comparison on exact integers, without the conversions
     const int cx = (x - rx0) / cell, cy = (y - ry0) / cell;
     for (int gy = max(cy - 1, 0); gy <= min(cy + 1, gh - 1); ++gy)
         for (int gx = max(cx - 1, 0); gx <= min(cx + 1, gw - 1); ++gx)
             for (int a = heads[gy * gw + gx]; a >= 0; a = anext[a]) {
                 const short2 p = axy[a];
-                const long long dx = x - p.x, dy = y - p.y;
-                if ((double)(dx * dx + dy * dy) < md2) return true;
+                const int dx = x - p.x, dy = y - p.y;
+                if ((unsigned)(dx * dx) + (unsigned)(dy * dy) < imd2) return true;
             }
     return false;
 }
@@ -969,6 +972,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     const int gw = (rw + cell - 1) / cell, gh = (rh + cell - 1) / cell;
     for (int c = tid; c < gw * gh; c += SEL_THREADS) heads[c] = -1;
     const double md2 = dmul(cfg.min_distance, cfg.min_distance);
+    const unsigned imd2 = (unsigned)fmin(ceil(md2), 4294967295.0);
     int R = 0;  // largest row offset of a disc: R*R < md2
     if (use_bm) {
         for (size_t k = tid; k < (size_t)wr * rh; k += SEL_THREADS) bm[k] = 0u;
@@ -1040,7 +1044,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             int x, y;
             dw.split(id, x, y);
             return !(use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
-                            : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2));
+                            : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2));
         };
         for (unsigned i0 = tid; i0 < n; i0 += 4 * SEL_THREADS) {
             unsigned long long k[4];
@@ -1164,7 +1168,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     int x, y;
                     dw.split(id[q], x, y);
                     const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
-                                           : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
+                                           : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2);
                     if (!ex) alive |= 1u << (j + q - j0);
                 }
             }
@@ -1227,7 +1231,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     bool ok = false;
                     if (j < ns) {
                         dw.split(cidx[j], x, y);
-                        ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, md2);
+                        ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2);
                     }
                     const unsigned live = __ballot_sync(0xffffffffu, ok);
                     if (!live) continue;
@@ -1240,8 +1244,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                         for (int src = 0; src < 32; ++src) {
                             const int sx = __shfl_sync(0xffffffffu, x, src);
                             const int sy = __shfl_sync(0xffffffffu, y, src);
-                            const long long dx = x - sx, dy = y - sy;
-                            if (src < lane && ((live >> src) & 1u) && (double)(dx * dx + dy * dy) < md2)
+                            const int dx = x - sx, dy = y - sy;
+                            if (src < lane && ((live >> src) & 1u) && (unsigned)(dx * dx) + (unsigned)(dy * dy) < imd2)
                                 conf |= 1u << src;
                         }
                     }
