@@ -2021,8 +2021,9 @@ struct stabgpu_stream {
     // (the re-detection of frame kR beside its own K5 step; frame kR+1's K5
     // waits for it).  motion_done[k]: the motion chain that read input slot k
     // as its previous frame has run (the slot may be overwritten).
-    cudaStream_t rst = nullptr, dst = nullptr;
+    cudaStream_t rst = nullptr, dst = nullptr, pst = nullptr;  // release chain, re-detection, pyramid
     cudaEvent_t ev_scan = nullptr, ev_rel = nullptr, ev_det = nullptr, ev_motion = nullptr, ev_grow = nullptr;
+    cudaEvent_t ev_pyr = nullptr, ev_chain[2] = {nullptr, nullptr};  // K1 of the frame; end of the chain of frame f (slot f & 1)
     std::vector<cudaEvent_t> motion_done;
     bool det_wait = false, rel_any = false, grown = false, pops_pending = false;
     // pop_async: records land in a pinned ring (a download into pageable memory
@@ -2222,14 +2223,15 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     if (s->chroma && ((rc = salloc(s, &s->ring_cb, fc * s->cap)) || (rc = salloc(s, &s->ring_cr, fc * s->cap)) ||
                       (rc = salloc(s, &s->out_cb, fc * s->ocap)) || (rc = salloc(s, &s->out_cr, fc * s->ocap))))
         return fail(rc);
-    // two-frame pyramid for levels >= 1 (frame f in slot f & 1); level 0 is
-    // the input ring itself
+    // three-frame pyramid for levels >= 1 (frame f in slot f % 3: frame f + 1's
+    // levels are built on the pyramid stream while the motion chain still
+    // tracks f - 1 -> f); level 0 is the input ring itself
     s->P.levels = level_dims(w, h, cfg.flow.max_levels, s->P.w, s->P.h);
     s->P.stride[0] = (size_t)w * h;
     for (int l = 1; l < s->P.levels; ++l) {
         uint8_t* lv;
         s->P.stride[l] = (size_t)s->P.w[l] * s->P.h[l];
-        if ((rc = salloc(s, &lv, 2 * s->P.stride[l]))) return fail(rc);
+        if ((rc = salloc(s, &lv, 3 * s->P.stride[l]))) return fail(rc);
         s->P.lvl[l] = lv;
     }
     // detection scratch (one frame)
@@ -2264,11 +2266,13 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
         for (auto& e : *v)
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
                 return fail(set_err(STABGPU_CUDA, "stream: event creation failed"));
-    for (cudaEvent_t* e : {&s->ev_scan, &s->ev_rel, &s->ev_det, &s->ev_motion, &s->ev_grow})
+    for (cudaEvent_t* e : {&s->ev_scan, &s->ev_rel, &s->ev_det, &s->ev_motion, &s->ev_grow, &s->ev_pyr, &s->ev_chain[0],
+                           &s->ev_chain[1]})
         if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
             return fail(set_err(STABGPU_CUDA, "stream: event creation failed"));
     if (cudaStreamCreateWithFlags(&s->rst, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&s->dst, cudaStreamNonBlocking) != cudaSuccess)
+        cudaStreamCreateWithFlags(&s->dst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s->pst, cudaStreamNonBlocking) != cudaSuccess)
         return fail(set_err(STABGPU_CUDA, "stream: stream creation failed"));
     if (cudaMallocHost((void**)&s->err_host, sizeof(int)) != cudaSuccess ||
         cudaMallocHost((void**)&s->rec_host, sizeof(stabgpu_frame_record) * s->ocap) != cudaSuccess)
@@ -2345,12 +2349,24 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         CUDA_TRY(cudaStreamWaitEvent(st, s->ev_det, 0));
         s->det_wait = false;
     }
-    // K1: the pyramid of the current frame, levels >= 1 into slot f & 1; no
-    // copies: level 0 stays in the ring, and the tracker sees (previous,
-    // current) through a pyramid view whose frame stride is the signed
-    // distance between the two slots
+    // K1: the pyramid of the current frame, levels >= 1 into slot f % 3, on the
+    // pyramid stream as soon as the frame has landed (off the motion chain: it
+    // overlaps the previous frame's K5 step; the slot was last read by the
+    // chain of frame f - 2).  No copies: level 0 stays in the ring, and the
+    // tracker sees (previous, current) through a pyramid view whose frame
+    // stride is the signed distance between the two slots
     DevPyramid& P = s->P;
-    const int cs = (int)(f & 1), ps = cs ^ 1;
+    const int cs = (int)(f % 3), ps = (int)((f + 2) % 3);
+    CUDA_TRY(cudaStreamWaitEvent(s->pst, s->in_done[slot], 0));
+    if (f >= 2) CUDA_TRY(cudaStreamWaitEvent(s->pst, s->ev_chain[f & 1], 0));
+    TRY(stream_run(s, false, 0x400, s->pst, "stream pyramid", [&] {  // three launches: cheaper direct than captured
+        for (int l = 1; l < P.levels; ++l)
+            launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
+                                 P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, s->pst);
+    }));
+    ctx->stats.launches += P.levels - 1;
+    CUDA_TRY(cudaEventRecord(s->ev_pyr, s->pst));
+    CUDA_TRY(cudaStreamWaitEvent(st, s->ev_pyr, 0));
     DevPyramid V = P;  // frame 0 = previous, frame 1 = current
     if (f > 0) {
         const uint8_t* py = s->ring_y + (size_t)((f - 1) % s->cap) * fl;
@@ -2362,10 +2378,6 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         }
     }
     TRY(stream_run(s, s->graphs, 0x100 | (f == 0 ? 1 : 0), st, "stream push", [&] {
-        for (int l = 1; l < P.levels; ++l)
-            launch_pyramid_level(l == 1 ? fy : P.lvl[l - 1] + cs * P.stride[l - 1], P.stride[l - 1], P.w[l - 1],
-                                 P.h[l - 1], const_cast<uint8_t*>(P.lvl[l]) + cs * P.stride[l], P.stride[l], 1, st);
-        ctx->stats.launches += P.levels - 1;
         if (f == 0) {  // MotionStage first frame (pipeline.cpp:84-88)
             static_assert(STABGPU_FRAME_FIRST == 0, "the FIRST record is all zero bytes");
             cudaMemsetAsync(s->motion, 0, sizeof(stabgpu_motion_record), st);
@@ -2395,6 +2407,7 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
     }));
     CUDA_TRY(cudaEventRecord(s->ev_scan, st));
     CUDA_TRY(cudaEventRecord(s->ev_motion, st));
+    CUDA_TRY(cudaEventRecord(s->ev_chain[f & 1], st));
     if (f > 0) {  // this chain read the previous frame's slot
         CUDA_TRY(cudaEventRecord(s->motion_done[(size_t)((f - 1) % s->cap)], st));
         std::swap(s->pts, s->nxt);
@@ -2487,14 +2500,16 @@ int stabgpu_stream_destroy(stabgpu_stream* s) {
     cudaStreamSynchronize(s->ctx->cout);
     if (s->rst) cudaStreamSynchronize(s->rst);
     if (s->dst) cudaStreamSynchronize(s->dst);
+    if (s->pst) cudaStreamSynchronize(s->pst);
     for (void* p : s->allocs) cudaFree(p);
     for (auto* v : {&s->slot_free, &s->in_done, &s->out_done, &s->motion_done})
         for (auto e : *v)
             if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {s->ev_scan, s->ev_rel, s->ev_det, s->ev_motion, s->ev_grow})
+    for (cudaEvent_t e : {s->ev_scan, s->ev_rel, s->ev_det, s->ev_motion, s->ev_grow, s->ev_pyr, s->ev_chain[0], s->ev_chain[1]})
         if (e) cudaEventDestroy(e);
     if (s->rst) cudaStreamDestroy(s->rst);
     if (s->dst) cudaStreamDestroy(s->dst);
+    if (s->pst) cudaStreamDestroy(s->pst);
     for (auto& kv : s->execs) cudaGraphExecDestroy(kv.second);
     if (s->err_host) cudaFreeHost(s->err_host);
     if (s->rec_host) cudaFreeHost(s->rec_host);
