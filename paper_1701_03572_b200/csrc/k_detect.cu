@@ -678,20 +678,38 @@ __device__ __forceinline__ void warp_sort32(unsigned long long& key, unsigned& i
 constexpr int MAX_CELLS = 8192;
 constexpr int SMEM_CORNERS = 8192;
 
-__device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy, const int* anext, int gw,
-                                          int gh, int cell, int rx0, int ry0, unsigned imd2) {
+// Grid geometry of the accepted corners: cell side (>= min_distance, so only
+// the 3x3 neighbourhood can conflict), grid size, ROI origin, and the cell
+// index of a ROI offset by a 32-bit reciprocal (offsets and cell < 2^16:
+// v * (rcp * cell - 2^32) < 2^32, so umulhi(v, rcp) == v / cell exactly).
+struct CellGrid {
+    int gw, gh, cell, rx0, ry0;
+    unsigned rcp;  // ceil(2^32 / cell); cell == 1 is handled apart (rcp would be 2^32)
+    __device__ __forceinline__ int cell_of(int v) const { return cell == 1 ? v : (int)__umulhi((unsigned)v, rcp); }
+};
+
+__device__ __forceinline__ bool conflicts(int x, int y, const int* heads, const short2* axy, const int* anext,
+                                          const CellGrid& g, unsigned imd2) {
     // imd2 = ceil(min_distance^2): for the integer d2 = dx*dx + dy*dy (coordinates
     // are 16-bit, so it fits 32 bits) d2 < md2 <=> d2 < imd2 — the reference's
     // double comparison on exact integers, without the conversions
-    const int cx = (x - rx0) / cell, cy = (y - ry0) / cell;
-    for (int gy = max(cy - 1, 0); gy <= min(cy + 1, gh - 1); ++gy)
-        for (int gx = max(cx - 1, 0); gx <= min(cx + 1, gw - 1); ++gx)
-            for (int a = heads[gy * gw + gx]; a >= 0; a = anext[a]) {
-                const short2 p = axy[a];
-                const int dx = x - p.x, dy = y - p.y;
-                if ((unsigned)(dx * dx) + (unsigned)(dy * dy) < imd2) return true;
-            }
-    return false;
+    const int cx = g.cell_of(x - g.rx0), cy = g.cell_of(y - g.ry0);
+    // the nine list heads first (independent loads; most cells are empty), then the lists
+    int hd[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int gx = cx + k % 3 - 1, gy = cy + k / 3 - 1;
+        hd[k] = (gx >= 0 && gx < g.gw && gy >= 0 && gy < g.gh) ? heads[gy * g.gw + gx] : -1;
+    }
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+        for (int a = hd[k]; a >= 0; a = anext[a]) {
+            const short2 p = axy[a];
+            const int dx = x - p.x, dy = y - p.y;
+            hit |= (unsigned)(dx * dx) + (unsigned)(dy * dy) < imd2;
+        }
+    return hit;
 }
 
 // K4 phase A over many CTAs per frame (when the scratch has bucket arrays):
@@ -970,6 +988,13 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     int cell = max(1, (int)ceil(cfg.min_distance));
     while ((long long)((rw + cell - 1) / cell) * ((rh + cell - 1) / cell) > MAX_CELLS) ++cell;
     const int gw = (rw + cell - 1) / cell, gh = (rh + cell - 1) / cell;
+    CellGrid cg;
+    cg.gw = gw;
+    cg.gh = gh;
+    cg.cell = cell;
+    cg.rx0 = roi.x0;
+    cg.ry0 = roi.y0;
+    cg.rcp = cell > 1 ? (unsigned)((0x100000000ull + (unsigned)cell - 1) / (unsigned)cell) : 0u;
     for (int c = tid; c < gw * gh; c += SEL_THREADS) heads[c] = -1;
     const double md2 = dmul(cfg.min_distance, cfg.min_distance);
     const unsigned imd2 = (unsigned)fmin(ceil(md2), 4294967295.0);
@@ -993,7 +1018,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             const double2 q = out_xy[(size_t)d * maxc + k];
             const int x = (int)q.x, y = (int)q.y;
             axy[k] = make_short2((short)x, (short)y);
-            anext[k] = atomicExch(&heads[((y - roi.y0) / cell) * gw + (x - roi.x0) / cell], k);
+            anext[k] = atomicExch(&heads[cg.cell_of(y - roi.y0) * gw + cg.cell_of(x - roi.x0)], k);
         }
         __threadfence_block();
         __syncthreads();
@@ -1044,7 +1069,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
             int x, y;
             dw.split(id, x, y);
             return !(use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
-                            : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2));
+                            : conflicts(x, y, heads, axy, anext, cg, imd2));
         };
         for (unsigned i0 = tid; i0 < n; i0 += 4 * SEL_THREADS) {
             unsigned long long k[4];
@@ -1168,7 +1193,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     int x, y;
                     dw.split(id[q], x, y);
                     const bool ex = use_bm ? excluded(bm, wr, x - roi.x0, y - roi.y0)
-                                           : conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2);
+                                           : conflicts(x, y, heads, axy, anext, cg, imd2);
                     if (!ex) alive |= 1u << (j + q - j0);
                 }
             }
@@ -1231,7 +1256,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     bool ok = false;
                     if (j < ns) {
                         dw.split(cidx[j], x, y);
-                        ok = !conflicts(x, y, heads, axy, anext, gw, gh, cell, roi.x0, roi.y0, imd2);
+                        ok = !conflicts(x, y, heads, axy, anext, cg, imd2);
                     }
                     const unsigned live = __ballot_sync(0xffffffffu, ok);
                     if (!live) continue;
@@ -1240,11 +1265,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     // dependent chain over the live set (one live lane needs none)
                     unsigned conf = 0;
                     if (live & (live - 1)) {
+                        const unsigned xy = (unsigned)x | ((unsigned)y << 16);  // 16-bit coordinates: one shuffle per source
 #pragma unroll
                         for (int src = 0; src < 32; ++src) {
-                            const int sx = __shfl_sync(0xffffffffu, x, src);
-                            const int sy = __shfl_sync(0xffffffffu, y, src);
-                            const int dx = x - sx, dy = y - sy;
+                            const unsigned sxy = __shfl_sync(0xffffffffu, xy, src);
+                            const int dx = x - (int)(sxy & 0xffffu), dy = y - (int)(sxy >> 16);
                             if (src < lane && ((live >> src) & 1u) && (unsigned)(dx * dx) + (unsigned)(dy * dy) < imd2)
                                 conf |= 1u << src;
                         }
@@ -1263,7 +1288,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
                     if (acc & (1u << lane)) {
                         const int slot = nacc + __popc(acc & ((1u << lane) - 1));
                         axy[slot] = make_short2((short)x, (short)y);
-                        const int cid = ((y - roi.y0) / cell) * gw + (x - roi.x0) / cell;
+                        const int cid = cg.cell_of(y - roi.y0) * gw + cg.cell_of(x - roi.x0);
                         anext[slot] = atomicExch(&heads[cid], slot);
                         out_xy[(size_t)d * maxc + slot] = make_double2((double)x, (double)y);
                         out_score[(size_t)d * maxc + slot] = __longlong_as_double((long long)ckey[j]);
