@@ -392,9 +392,19 @@ __global__ void resp_cut_kernel(double quality, DetectScratch s, unsigned keep) 
     }
 }
 
-__global__ void resp_redo_reset_kernel(DetectScratch s) {
+// One launch clears a batch's per-frame detection state (max, candidate count,
+// fp32 max bound, response histogram, bucket counts) instead of five memsets.
+__global__ void detect_reset_kernel(DetectScratch s, int fast, int buckets) {
     const int d = blockIdx.x;
-    if (threadIdx.x == 0 && (s.flags[d] & 2)) s.count[d] = 0;
+    if (threadIdx.x == 0) {
+        s.maxbits[d] = 0ull;
+        s.count[d] = 0u;
+        if (fast) s.mlo[d] = 0u;
+    }
+    if (fast)
+        for (int i = threadIdx.x; i < kRespBins; i += blockDim.x) s.hist[(size_t)d * kRespBins + i] = 0u;
+    if (buckets)
+        for (int i = threadIdx.x; i <= kBuckets; i += blockDim.x) s.bstart[(size_t)d * (kBuckets + 1) + i] = 0u;
 }
 
 // Generic block size (any odd >= 3): direct evaluation from global memory.
@@ -894,7 +904,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     if (n == 0 || mb == 0) {
         if (tid == 0 && !redo) {  // (redo: the first pass's corners stand)
             out_n[d] = 0;
-            if (cut && mb != 0) s.flags[d] |= 2;
+            if (cut && mb != 0) {
+                s.flags[d] |= 2;
+                s.count[d] = 0;
+            }
         }
         return;
     }
@@ -1319,7 +1332,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1024 / SEL_THREADS)
     if (tid == 0) {
         out_n[d] = nacc;
         // the cut prefix ran out before max_corners: redo from the full list
-        if (!redo && cut && nacc < maxc) s.flags[d] |= 2;
+        if (!redo && cut && nacc < maxc) {
+            s.flags[d] |= 2;
+            s.count[d] = 0;  // the redo pass lists the band below the cut from position 0
+        }
     }
 }
 
@@ -1342,8 +1358,7 @@ size_t bitmap_words(stabgpu_roi roi) {
 
 namespace {
 void launch_buckets(const DetectScratch& s, int nD, double quality, int redo, cudaStream_t st) {
-    if (!s.bstart || !s.bcur) return;
-    cudaMemsetAsync(s.bstart, 0, sizeof(unsigned) * (kBuckets + 1) * (size_t)nD, st);
+    if (!s.bstart || !s.bcur) return;  // (the bucket counts were cleared by detect_reset_kernel)
     const dim3 grid(16, nD);
     bucket_count_kernel<<<grid, 512, 0, st>>>(s, quality, redo);
     bucket_scan_kernel<<<nD, 1024, 0, st>>>(s, quality, redo);
@@ -1355,14 +1370,11 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
                    DetectScratch& s, double2* out_xy, double* out_score, int* out_n,
                    cudaStream_t st) {
     if (nD <= 0) return;
-    cudaMemsetAsync(s.maxbits, 0, sizeof(unsigned long long) * nD, st);
-    cudaMemsetAsync(s.count, 0, sizeof(unsigned) * nD, st);
     const int rw = roi.x1 - roi.x0, rh = roi.y1 - roi.y0;
     const int half = cfg.block_size / 2;
     const bool fast = half == 1 && s.hist && s.lo && s.flags && s.mlo;
+    detect_reset_kernel<<<nD, 256, 0, st>>>(s, fast ? 1 : 0, (nD <= 32 && s.bstart && s.bcur) ? 1 : 0);
     if (fast) {
-        cudaMemsetAsync(s.hist, 0, sizeof(unsigned) * kRespBins * (size_t)nD, st);
-        cudaMemsetAsync(s.mlo, 0, sizeof(unsigned) * (size_t)nD, st);
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<0><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 0);
         // the cut keeps ~16 candidates per corner.  When the corners' exclusion
@@ -1447,12 +1459,12 @@ void launch_detect(PlaneBatch fr, int nD, const stabgpu_detect_cfg& cfg, stabgpu
     sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sf, out_xy, out_score, out_n, g_axy, g_anext, ch,
                                        use_bm ? 1 : 0, 0);
     if (fast) {  // frames whose cut prefix ran out: full candidate list (usually none)
-        resp_redo_reset_kernel<<<nD, 32, 0, st>>>(s);
+        // (select cleared the candidate count of the frames it flagged; the redo
+        // buckets inside select: usually no frame takes it, so two launches, not six)
         dim3 grid((rw + 8 * SW_COLS - 1) / (8 * SW_COLS), (rh + SW_BAND - 1) / SW_BAND, nD);
         resp_stream_kernel<1><<<grid, 256, 0, st>>>(fr, roi, cfg.quality_level, s, 1);
         DetectScratch sr = s;
-        if (nD > 32) sr.bstart = sr.bcur = nullptr;
-        launch_buckets(sr, nD, cfg.quality_level, 1, st);
+        sr.bstart = sr.bcur = nullptr;
         sel<<<nD, sel_threads, smem, st>>>(cfg, roi, fr.w, sr, out_xy, out_score, out_n, g_axy, g_anext, ch,
                                            use_bm ? 1 : 0, 1);
     }
