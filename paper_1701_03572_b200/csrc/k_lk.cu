@@ -381,7 +381,10 @@ __device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const doub
     double a0x = 0.0, a0y = 0.0, b0x = 0.0, b0y = 0.0, a1x = 0.0, a1y = 0.0, b1x = 0.0, b1y = 0.0;
     // software-pipelined: row k+1's gradient and pixel bytes are loaded while
     // row k's products issue (the last prefetch reads one row past the
-    // window, inside the warp's shared area, and is discarded)
+    // window: pixel row vh + 1 of the staging buffer, and — the gradient rows
+    // being stored bottom-up, sa < 0 — the bytes in front of the gradient
+    // array, i.e. the staging buffer's tail; both inside the warp's shared
+    // area, both discarded)
     src += SM_PITCH;
     uint32_t pn = src[0], qn = src[1];
     double2 gn = ga[0];
@@ -463,7 +466,11 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
     const bool xtra = XTRA && lane == 31;
     const int ti = lane - 1;  // template column of this lane
     const bool tcol = ti >= iv0 && ti <= iv1;
-    ga += (uint32_t)((tcol ? ti - iv0 : 0) * 16);
+    // rows are stored bottom-up (row j at [jv1 - j][.]): the correlation pass
+    // walks them with a negative step, so its one-row-ahead prefetch past the
+    // last row lands in front of the array (the tail of the staging buffer),
+    // never past the end of the warp's shared memory
+    ga += (uint32_t)((tcol ? ti - iv0 : 0) * 16) + (uint32_t)(jv1 - jv0) * grow;
     src += lane + jv0 * SM_PITCH;
     // extended rows jv0 (eA) and jv0 + 1 (eB) from image rows jv0 .. jv0+2
     double hp = hlerp(src[0], src[1], fx), hpx = 0.0;
@@ -507,7 +514,7 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
         const double dy = ev - eA;
         if (tcol)
             asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ga), "d"(dx), "d"(dy));
-        ga += grow;
+        ga -= grow;
         gxx = fma(dx, dx, gxx);
         gxy = fma(dx, dy, gxy);
         gyy = fma(dy, dy, gyy);
@@ -631,8 +638,9 @@ __device__ void track_dual(const DevPyramid& P, int ft, double px, double py, in
             __syncwarp();
         }
         // lanes past the valid window read the zero slot (row step 0)
-        const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? lane : vh * vw);
-        const int gstep = lane < vw ? vw : 0;
+        // (gradient rows are stored bottom-up: row 0 is the last one, step -vw)
+        const double2* gcol = reinterpret_cast<const double2*>(tg) + (lane < vw ? (vh - 1) * vw + lane : vh * vw);
+        const int gstep = lane < vw ? -vw : 0;
         const int sw = vw + 1 + 2 * SM_MARGIN, sh = vh + 1 + 2 * SM_MARGIN;
 #pragma unroll 1
         for (int j = 0; j < nt; ++j) {
