@@ -388,7 +388,7 @@ __device__ __forceinline__ void corr_pass(const uint8_t* src, int vh, const doub
     src += SM_PITCH;
     uint32_t pn = src[0], qn = src[1];
     double2 gn = ga[0];
-#pragma unroll 2
+#pragma unroll 3
     for (int k = 0; k < vh; ++k) {
         const double2 g = gn;
         const double p1 = u2d(pn), q1 = u2d(qn);
