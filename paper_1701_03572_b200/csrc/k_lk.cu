@@ -493,7 +493,7 @@ __device__ __forceinline__ void template_pass(const uint8_t* src, double fx, dou
     // template values are formed (the last prefetch reads one row past the
     // staged block, inside the warp's shared area, and is discarded)
     uint32_t n0 = src[0], n1 = src[1], n2 = XTRA ? src[2] : 0u;
-#pragma unroll 2
+#pragma unroll 3
     for (int j = jv0; j <= jv1; ++j) {  // template row j: extended rows j .. j+2
         const uint32_t c0 = n0, c1 = n1, c2 = n2;
         src += SM_PITCH;
