@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) resp_stream_kernel(PlaneBatch fr, stabgpu
     float best_low = -1.0f;
     int qn = 0;                     // MODE 1: warp buffer fill (warp-uniform)
     const uint8_t* rp = bp + SB_W;  // row r
-#pragma unroll 2
+#pragma unroll 3
     for (int r = Y0 - 1; r <= Y1; ++r, rp += SB_W) {
         if (MODE == 0 && ((r + 1) & 7) > 2) {  // product rows 8k+2 .. 8k+6: no sampled output row (8k) reads them
             Im = I0;
