@@ -220,7 +220,9 @@ def run_reference_arm(args, cfg):
         return 0
     threads = os.cpu_count() or 1
     n_total = cfg.video.frames
-    sample = int(min(n_total, max(2 * threads * cfg.stab.flow.redetect_interval, 60)))
+    # five segments per thread (the segment-parallel driver needs a few per
+    # thread to keep every core busy), at most 400 frames per step
+    sample = int(min(n_total, max(5 * threads * cfg.stab.flow.redetect_interval, 60)))
     sample = min(sample, 400)
     planes = render(cfg, 0, sample, pinned=False)
     arrs = [p.numpy() for p in planes] + [None] * (3 - len(planes))
@@ -440,6 +442,14 @@ def run_ours(args, cfg):
             sample = min(n, max(6 * threads, 40))
             hs = [h[:sample].numpy() for h in host] + [None] * (3 - planes)
             fps, dt, ref_out = cpu_reference(cfg, hs[0], hs[1], hs[2], threads)
+            if dt < 5.0 and sample < n:  # a short sample: take one worth ~10 s of CPU work instead
+                R = cfg.stab.flow.redetect_interval
+                bigger = min(n, int(fps * 10.0) // R * R + 1)
+                if bigger > sample:
+                    sample = bigger
+                    del ref_out
+                    hs = [h[:sample].numpy() for h in host] + [None] * (3 - planes)
+                    fps, dt, ref_out = cpu_reference(cfg, hs[0], hs[1], hs[2], threads)
             line["cpu_baseline"] = {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference",
                                     "sample": f"first {sample} frames of {args.config} "
                                               f"({dt:.1f} s, reference stage functions, segment-parallel)"}
