@@ -413,8 +413,9 @@ int stabgpu_tracker_destroy(stabgpu_tracker* t);
  * The released frames are bit-identical to Stage I (stabilize_sequence).
  * Planes are host (pageable or pinned) or device pointers (unified
  * addressing; pitch = width).  After every push / finish the caller pops the
- * ready frames in arrival order.  A push's launches run on three streams:
- * the motion chain (K1, the K5 step + compaction + K6 fit, the K7 scan), the
+ * ready frames in arrival order.  A push's launches run on four streams:
+ * the pyramid stream (K1 of the frame as soon as it lands), the motion chain
+ * (the K5 step + compaction + K6 fit, the K7 scan), the
  * release chain (smoothing + K8 compose of the frame it releases, behind the
  * scan) and, every redetect_interval frames, the re-detection (beside the
  * frame's own K5 step; the next frame's K5 waits for it) - so frame k+1's
@@ -427,6 +428,14 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfg, int w, in
 /* Motion estimate of the next frame; *n_ready = frames ready to pop. */
 int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
                         int* n_ready);
+/* The same, returning before the frame's upload has landed (the launches are
+ * queued behind it): the caller keeps y/cb/cr unchanged until
+ * stabgpu_stream_wait_inputs or a later stabgpu_stream_push returns.  With two
+ * or more host frame buffers in rotation, frame k+1 uploads while frame k's
+ * motion runs (run_streaming's reader thread, pipeline.cpp:251-272). */
+int stabgpu_stream_push_async(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                              int* n_ready);
+int stabgpu_stream_wait_inputs(stabgpu_stream* s);
 /* End of stream: releases the remaining frames (at least 2 frames pushed). */
 int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready);
 /* Oldest ready frame (its index, planes and record); STABGPU_SEQUENCING if none. */

@@ -137,6 +137,8 @@ PROTOTYPES = {
     "stabgpu_tracker_destroy": (I, [V]),
     "stabgpu_stream_create": (I, [V, P(Config), I, I, I, I, P(V)]),
     "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
+    "stabgpu_stream_push_async": (I, [V, V, V, V, c_ip]),
+    "stabgpu_stream_wait_inputs": (I, [V]),
     "stabgpu_stream_finish": (I, [V, c_ip]),
     "stabgpu_stream_pop": (I, [V, P(C.c_int64), V, V, V, V]),
     "stabgpu_stream_pop_async": (I, [V, P(C.c_int64), V, V, V, V]),

@@ -2023,6 +2023,7 @@ struct stabgpu_stream {
     // as its previous frame has run (the slot may be overwritten).
     cudaStream_t rst = nullptr, dst = nullptr, pst = nullptr;  // release chain, re-detection, pyramid
     cudaEvent_t ev_scan = nullptr, ev_rel = nullptr, ev_det = nullptr, ev_motion = nullptr, ev_grow = nullptr;
+    cudaEvent_t last_in = nullptr;  // upload event of the last pushed frame (push_async / wait_inputs)
     cudaEvent_t ev_pyr = nullptr, ev_chain[2] = {nullptr, nullptr};  // K1 of the frame; end of the chain of frame f (slot f & 1)
     std::vector<cudaEvent_t> motion_done;
     bool det_wait = false, rel_any = false, grown = false, pops_pending = false;
@@ -2291,7 +2292,10 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
     return STABGPU_OK;
 }
 
-int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int* n_ready) {
+}  // extern "C"
+namespace {
+int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int* n_ready,
+                     bool wait_upload) {
     if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
     if (s->complete) return set_err(STABGPU_SEQUENCING, "stream: push after finish");
     if (!y || (s->chroma && (!cb || !cr))) return set_err(STABGPU_INVALID_INPUT, "stream: missing planes");
@@ -2419,8 +2423,29 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
         s->det_wait = true;
     }
     TRY(stream_release(s, nrel));
-    CUDA_TRY(cudaEventSynchronize(s->in_done[slot]));  // the caller's buffers are consumed
+    s->last_in = s->in_done[slot];
+    if (wait_upload) CUDA_TRY(cudaEventSynchronize(s->in_done[slot]));  // the caller's buffers are consumed
     if (n_ready) *n_ready = (int)(s->ready.size() - s->ready_head);
+    return STABGPU_OK;
+}
+}  // namespace
+extern "C" {
+
+int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr, int* n_ready) {
+    return stream_push_impl(s, y, cb, cr, n_ready, true);
+}
+
+int stabgpu_stream_push_async(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
+                              int* n_ready) {
+    return stream_push_impl(s, y, cb, cr, n_ready, false);
+}
+
+int stabgpu_stream_wait_inputs(stabgpu_stream* s) {
+    if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
+    if (s->last_in) {
+        cudaSetDevice(s->ctx->device);
+        CUDA_TRY(cudaEventSynchronize(s->last_in));  // uploads are in order on the input copy stream
+    }
     return STABGPU_OK;
 }
 

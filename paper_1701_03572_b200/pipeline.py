@@ -418,12 +418,18 @@ class StreamStabilizer:
     is bit-identical to Stage I's output for that frame."""
 
     def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0,
-                 graphs: bool = True, overlap_pops: bool = False):
+                 graphs: bool = True, overlap_pops: bool = False, async_push: bool = False):
         # overlap_pops: push() queues the downloads of the frames released by
         # the PREVIOUS push (stabgpu_stream_pop_async), uploads and estimates
         # the new frame, then waits for them - the D2H of frame k-r overlaps
         # the H2D of frame k+1; frames come back one push late, same bytes
         self.overlap_pops = overlap_pops
+        # async_push: push() returns before the frame's upload has landed
+        # (stabgpu_stream_push_async); the stabilizer keeps the frame's arrays
+        # alive and waits for the upload at the start of the next push, so with
+        # a new array per frame the upload of frame k+1 overlaps the motion of k
+        self.async_push = async_push
+        self._held = None
         self._owed = 0
         self.w, self.h, self.cw, self.ch = w, h, cw, ch
         self._c = cfg.c()
@@ -459,17 +465,25 @@ class StreamStabilizer:
         cb = None if cb is None else np.ascontiguousarray(cb, np.uint8)
         cr = None if cr is None else np.ascontiguousarray(cr, np.uint8)
         n = C.c_int()
+        push = self._lib.stabgpu_stream_push
+        if self.async_push:
+            check(self._lib.stabgpu_stream_wait_inputs(self._h))  # the previous frame's arrays may go now
+            self._held = (y, cb, cr)
+            push = self._lib.stabgpu_stream_push_async
         if self.overlap_pops:
             late = self._pop_all(self._owed, wait=False)
-            check(self._lib.stabgpu_stream_push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
+            check(push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
             check(self._lib.stabgpu_stream_wait_pops(self._h))
             self._owed = n.value
             return self._frames(late)
-        check(self._lib.stabgpu_stream_push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
+        check(push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
         return self._frames(self._pop_all(n.value))
 
     def finish(self):
         n = C.c_int()
+        if self.async_push:
+            check(self._lib.stabgpu_stream_wait_inputs(self._h))
+            self._held = None
         check(self._lib.stabgpu_stream_finish(self._h, C.byref(n)))
         self._owed = 0
         return self._frames(self._pop_all(n.value))

@@ -491,6 +491,27 @@ def test_stream_equals_stage1(mode, ransac, smooth, graphs):
         assert grec.tobytes() == srec[i].tobytes(), i
 
 
+@pytest.mark.parametrize("overlap", [False, True])
+def test_stream_async_push_equals_stage1(overlap):
+    """stabgpu_stream_push_async (push returns before the upload has landed;
+    a fresh host array per frame, kept alive until the next push) releases the
+    same frames, bit for bit, as the blocking push and as Stage I."""
+    y, cb, cr = _data.video(frames=37, objects=2, jit_t=3.0, color=True)
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=100, smooth=4)
+    sy, sb, sr, srec = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    n, (h, w) = len(y), y.shape[1:]
+    s = pipeline.StreamStabilizer(cfg, w, h, cb.shape[2], cb.shape[1], async_push=True, overlap_pops=overlap)
+    got = []
+    for k in range(n):
+        got += s.push(y[k].copy(), cb[k].copy(), cr[k].copy())
+    got += s.finish()
+    s.close()
+    assert [g[0] for g in got] == list(range(n))
+    for i, gy, gb, gr, grec in got:
+        assert np.array_equal(gy, sy[i]) and np.array_equal(gb, sb[i]) and np.array_equal(gr, sr[i]), i
+        assert grec.tobytes() == srec[i].tobytes(), i
+
+
 @pytest.mark.parametrize("name,frames", [("c1", 90), ("c3", 40)])
 def test_stream_equals_oracle_config(name, frames):
     """Stage II against the CPU reference path directly (not through Stage

@@ -50,6 +50,10 @@ def pop_all(k):
 pop_all.n = 0
 lat = []
 nr = C.c_int()
+# --push-async: stabgpu_stream_push_async (every frame has its own pinned array here,
+# so nothing is overwritten; wait_inputs once at the end)
+pasync = "--push-async" in sys.argv
+push = lib.stabgpu_stream_push_async if pasync else lib.stabgpu_stream_push
 lag = "--lag" in sys.argv  # pop a push late: frame k+1 uploads while frame k computes and k-r downloads
 t0 = time.perf_counter()
 pending = 0
@@ -57,8 +61,8 @@ for k in range(n):
     t1 = time.perf_counter()
     if asyn and len(owed) >= depth:
         pop_all(owed.pop(0))  # queue the downloads of the frames push k - depth released
-    assert lib.stabgpu_stream_push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
-                                   vp(pin[2], k) if col else None, C.byref(nr)) == 0
+    assert push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
+                vp(pin[2], k) if col else None, C.byref(nr)) == 0
     if asyn:
         assert lib.stabgpu_stream_wait_pops(hs) == 0
         owed.append(nr.value - sum(owed))
@@ -70,6 +74,7 @@ for k in range(n):
     lat.append(time.perf_counter() - t1)
 if lag and not asyn:
     pop_all(pending)
+assert lib.stabgpu_stream_wait_inputs(hs) == 0
 assert lib.stabgpu_stream_finish(hs, C.byref(nr)) == 0
 pop_all(nr.value)
 if asyn:
@@ -77,5 +82,5 @@ if asyn:
 dt = time.perf_counter() - t0
 lib.stabgpu_stream_destroy(hs)
 lat = np.array(lat) * 1e3
-print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)} async={int(asyn) * depth}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
+print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)} async={int(asyn) * depth} push_async={int(pasync)}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
       f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out")
