@@ -1985,8 +1985,13 @@ struct stabgpu_stream {
     long long pushed = 0, next = 0;  // frames pushed, next frame to release
     std::vector<void*> allocs;
     // frames
+    // input and output rings, frame-major: slot k holds Y | Cb | Cr at
+    // ring_y/cb/cr + k * fs (plane offsets padded to 256 B), so a caller whose
+    // frame is one contiguous planar buffer moves in one copy per direction
     uint8_t *ring_y = nullptr, *ring_cb = nullptr, *ring_cr = nullptr;
     uint8_t *out_y = nullptr, *out_cb = nullptr, *out_cr = nullptr;
+    size_t fs = 0;         // bytes between two ring slots
+    bool packed = false;   // no padding between the planes: Y, Cb, Cr of a slot are one contiguous run
     std::vector<long long> ready;    // released frame indices not yet popped (FIFO)
     size_t ready_head = 0;
     // motion state: two-frame pyramid (prev at 0, cur at 1)
@@ -2102,11 +2107,11 @@ void stream_release_kernels(stabgpu_stream* s, long long i) {
                        PlanGeom{s->w, s->h, s->chroma ? s->cw : 0, s->chroma ? s->ch : 0, s->cfg.crop_ratio}, st);
     const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch;
     const size_t in = (size_t)(i % s->cap), o = (size_t)(i % s->ocap);
-    PlaneBatch yb{s->ring_y + in * fl, fl, s->w, s->h};
-    PlaneBatch bb{s->chroma ? s->ring_cb + in * fc : nullptr, fc, s->cw, s->ch};
-    PlaneBatch rb{s->chroma ? s->ring_cr + in * fc : nullptr, fc, s->cw, s->ch};
-    launch_compose(yb, bb, rb, s->plan + i, 1, s->cfg.crop_ratio, s->out_y + o * fl,
-                   s->chroma ? s->out_cb + o * fc : nullptr, s->chroma ? s->out_cr + o * fc : nullptr, st,
+    PlaneBatch yb{s->ring_y + in * s->fs, fl, s->w, s->h};
+    PlaneBatch bb{s->chroma ? s->ring_cb + in * s->fs : nullptr, fc, s->cw, s->ch};
+    PlaneBatch rb{s->chroma ? s->ring_cr + in * s->fs : nullptr, fc, s->cw, s->ch};
+    launch_compose(yb, bb, rb, s->plan + i, 1, s->cfg.crop_ratio, s->out_y + o * s->fs,
+                   s->chroma ? s->out_cb + o * s->fs : nullptr, s->chroma ? s->out_cr + o * s->fs : nullptr, st,
                    s->cscratch, s->cscratch_bytes);
     s->ctx->stats.launches += 2;
 }
@@ -2220,10 +2225,19 @@ int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfgp, int w, i
         return code;
     };
     const size_t fl = (size_t)w * h, fc = (size_t)s->cw * s->ch;
-    if ((rc = salloc(s, &s->ring_y, fl * s->cap)) || (rc = salloc(s, &s->out_y, fl * s->ocap))) return fail(rc);
-    if (s->chroma && ((rc = salloc(s, &s->ring_cb, fc * s->cap)) || (rc = salloc(s, &s->ring_cr, fc * s->cap)) ||
-                      (rc = salloc(s, &s->out_cb, fc * s->ocap)) || (rc = salloc(s, &s->out_cr, fc * s->ocap))))
-        return fail(rc);
+    {
+        const size_t afl = (fl + 255) & ~(size_t)255, afc = s->chroma ? (fc + 255) & ~(size_t)255 : 0;
+        s->fs = afl + 2 * afc;
+        s->packed = afl == fl && afc == fc;
+        if ((rc = salloc(s, &s->ring_y, s->fs * s->cap)) || (rc = salloc(s, &s->out_y, s->fs * s->ocap)))
+            return fail(rc);
+        if (s->chroma) {
+            s->ring_cb = s->ring_y + afl;
+            s->ring_cr = s->ring_cb + afc;
+            s->out_cb = s->out_y + afl;
+            s->out_cr = s->out_cb + afc;
+        }
+    }
     // three-frame pyramid for levels >= 1 (frame f in slot f % 3: frame f + 1's
     // levels are built on the pyramid stream while the motion chain still
     // tracks f - 1 -> f); level 0 is the input ring itself
@@ -2310,7 +2324,7 @@ int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, con
     TRY(stream_grow(s, f + 1));
     const size_t fl = (size_t)s->w * s->h, fc = (size_t)s->cw * s->ch;
     const size_t slot = (size_t)(f % s->cap);
-    uint8_t* fy = s->ring_y + slot * fl;
+    uint8_t* fy = s->ring_y + slot * s->fs;
     // upload on the input copy stream once the slot's previous frame was
     // composed (and the motion chain that read it as its previous frame has
     // run); the motion stream waits for it.  The host buffers are read before
@@ -2320,10 +2334,16 @@ int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, con
         CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->slot_free[slot], 0));
         CUDA_TRY(cudaStreamWaitEvent(ctx->cin, s->motion_done[slot], 0));
     }
-    CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyDefault, ctx->cin));
-    if (s->chroma) {
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * fc, cb, fc, cudaMemcpyDefault, ctx->cin));
-        CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * fc, cr, fc, cudaMemcpyDefault, ctx->cin));
+    if (s->chroma && s->packed && cb == y + fl && cr == cb + fc) {
+        // the caller's frame is one planar buffer (Y | Cb | Cr): one copy
+        // (frame-sized copies keep PCIe at its duplex rate; 2 MB ones do not)
+        CUDA_TRY(cudaMemcpyAsync(fy, y, s->fs, cudaMemcpyDefault, ctx->cin));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(fy, y, fl, cudaMemcpyDefault, ctx->cin));
+        if (s->chroma) {
+            CUDA_TRY(cudaMemcpyAsync(s->ring_cb + slot * s->fs, cb, fc, cudaMemcpyDefault, ctx->cin));
+            CUDA_TRY(cudaMemcpyAsync(s->ring_cr + slot * s->fs, cr, fc, cudaMemcpyDefault, ctx->cin));
+        }
     }
     CUDA_TRY(cudaEventRecord(s->in_done[slot], ctx->cin));
     CUDA_TRY(cudaStreamWaitEvent(st, s->in_done[slot], 0));
@@ -2336,9 +2356,12 @@ int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, con
     }
     const bool detect = f == 0 || f % R == 0;
     PlaneBatch cur{fy, fl, s->w, s->h};
-    // detection of this frame (flow.cpp:303-308, 327-330) on the detect stream,
-    // beside the frame's own K5 step: it reads the frame only.  It writes the
-    // third point buffer, last used by the motion chain R frames ago.
+    // detection of this frame (flow.cpp:303-308, 327-330) on the detect stream
+    // as soon as the frame has landed: it reads the frame only, so with the
+    // caller a few frames ahead it runs beside the K5 steps of the frames
+    // before it instead of in front of the next one.  It writes the third
+    // point buffer, last touched by the motion chain of the previous detection
+    // frame (ev_motion: R frames ago).
     if (detect) {
         CUDA_TRY(cudaStreamWaitEvent(s->dst, s->in_done[slot], 0));
         if (f > 0) CUDA_TRY(cudaStreamWaitEvent(s->dst, s->ev_motion, 0));
@@ -2373,7 +2396,7 @@ int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, con
     CUDA_TRY(cudaStreamWaitEvent(st, s->ev_pyr, 0));
     DevPyramid V = P;  // frame 0 = previous, frame 1 = current
     if (f > 0) {
-        const uint8_t* py = s->ring_y + (size_t)((f - 1) % s->cap) * fl;
+        const uint8_t* py = s->ring_y + (size_t)((f - 1) % s->cap) * s->fs;
         V.lvl[0] = py;
         V.stride[0] = (size_t)(fy - py);  // two's complement: a wrapped ring gives a negative distance
         for (int l = 1; l < P.levels; ++l) {
@@ -2410,7 +2433,7 @@ int stream_push_impl(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, con
         launch_plan_scan(s->motion, f, 1, cfg, s->ps, s->rec, s->cum, st);
     }));
     CUDA_TRY(cudaEventRecord(s->ev_scan, st));
-    CUDA_TRY(cudaEventRecord(s->ev_motion, st));
+    if (detect) CUDA_TRY(cudaEventRecord(s->ev_motion, st));  // this chain's output buffer is the next detection's
     CUDA_TRY(cudaEventRecord(s->ev_chain[f & 1], st));
     if (f > 0) {  // this chain read the previous frame's slot
         CUDA_TRY(cudaEventRecord(s->motion_done[(size_t)((f - 1) % s->cap)], st));
@@ -2477,9 +2500,13 @@ int stabgpu_stream_pop_async(stabgpu_stream* s, int64_t* index, uint8_t* oy, uin
     cudaStream_t co = s->ctx->cout;
     CUDA_TRY(cudaStreamWaitEvent(co, s->out_done[o], 0));
     if (s->grown) CUDA_TRY(cudaStreamWaitEvent(co, s->ev_grow, 0));  // the records may have moved
-    if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * fl, fl, cudaMemcpyDefault, co));
-    if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * fc, fc, cudaMemcpyDefault, co));
-    if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * fc, fc, cudaMemcpyDefault, co));
+    if (s->chroma && s->packed && oy && ocb == oy + fl && ocr == ocb + fc) {
+        CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * s->fs, s->fs, cudaMemcpyDefault, co));  // one planar frame buffer
+    } else {
+        if (oy) CUDA_TRY(cudaMemcpyAsync(oy, s->out_y + o * s->fs, fl, cudaMemcpyDefault, co));
+        if (s->chroma && ocb) CUDA_TRY(cudaMemcpyAsync(ocb, s->out_cb + o * s->fs, fc, cudaMemcpyDefault, co));
+        if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * s->fs, fc, cudaMemcpyDefault, co));
+    }
     if (record) {
         if ((int)s->rec_owed.size() >= s->ocap) TRY(stabgpu_stream_wait_pops(s));
         const int j = (int)s->rec_owed.size();

@@ -613,6 +613,51 @@ def test_stream_device_pointers():
     assert np.array_equal(out.cpu().numpy(), sy)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h", [(256, 192), (200, 150)])
+def test_stream_packed_frames(w, h):
+    """A caller whose frame is one contiguous planar buffer (Y | Cb | Cr) on
+    both sides: push and pop move it in one copy when the planes tile the ring
+    slot exactly (plane sizes multiples of 256 B: 256x192), and plane by plane
+    otherwise (200x150); both equal Stage I bit for bit, and so does the same
+    stream fed from three separate arrays."""
+    import ctypes as C
+
+    y, cb, cr = _data.video(w=w, h=h, frames=18, color=True)
+    cfg = _data.small_cfg(smooth=3)
+    sy, sb, sr, _ = pipeline.stabilize_sequence(y, cfg, cb, cr)
+    n, fl = len(y), w * h
+    packed_in = np.concatenate([p.reshape(n, -1) for p in (y, cb, cr)], axis=1)
+    packed_in = np.ascontiguousarray(packed_in)
+    packed_out = np.zeros_like(packed_in)
+    s = pipeline.StreamStabilizer(cfg, w, h, w, h)
+    lib, hs = s._lib, s._h
+    nr = C.c_int()
+    popped = []
+
+    def ptr(a, k, plane):
+        return C.c_void_p(a.ctypes.data + k * a.strides[0] + plane * fl)
+
+    def pop(k):
+        for _ in range(k):
+            idx = C.c_int64()
+            j = len(popped)
+            assert lib.stabgpu_stream_pop(hs, C.byref(idx), ptr(packed_out, j, 0), ptr(packed_out, j, 1),
+                                          ptr(packed_out, j, 2), None) == 0
+            popped.append(idx.value)
+
+    for k in range(n):
+        assert lib.stabgpu_stream_push(hs, ptr(packed_in, k, 0), ptr(packed_in, k, 1), ptr(packed_in, k, 2),
+                                       C.byref(nr)) == 0
+        pop(nr.value)
+    assert lib.stabgpu_stream_finish(hs, C.byref(nr)) == 0
+    pop(nr.value)
+    s.close()
+    assert popped == list(range(n))
+    got = packed_out.reshape(n, 3, h, w)
+    assert np.array_equal(got[:, 0], sy) and np.array_equal(got[:, 1], sb) and np.array_equal(got[:, 2], sr)
+
+
 def test_stream_gray_and_errors():
     y = _data.video(frames=14)[0]
     cfg = _data.small_cfg(smooth=3)

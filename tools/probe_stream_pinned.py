@@ -6,7 +6,11 @@ push late; --async: the frames released by the previous push are popped with
 stabgpu_stream_pop_async before the next push and waited for after it (their
 download overlaps the next upload); --depth N (default 2 with --async): the
 frames popped before push k are those released by push k-N, so their compose
-finished long before and the download runs beside the upload of frame k."""
+finished long before and the download runs beside the upload of frame k;
+--packed: every frame is one contiguous planar buffer (Y | Cb | Cr) on both
+sides, so push and pop move it in one copy; --wait-every M (default 1): stabgpu_stream_wait_pops after every M-th push
+only (every popped frame has its own output array here), so the copy queues
+of both directions never drain between frames."""
 import ctypes as C
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -19,8 +23,26 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 cfg = synth.CONFIGS[name]
 planes = synth.Video(cfg.video).render(0, n)
 dev = "--device" in sys.argv
-pin = [torch.from_numpy(p).cuda() if dev else torch.from_numpy(p).pin_memory() for p in planes]
-outp = [torch.empty_like(p) if dev else torch.empty_like(p).pin_memory() for p in pin]
+dev_in = dev or "--device-in" in sys.argv    # input frames already in HBM
+dev_out = dev or "--device-out" in sys.argv  # output frames stay in HBM
+packed = "--packed" in sys.argv  # every frame one contiguous planar buffer (Y | Cb | Cr), in and out
+if packed and len(planes) == 3:
+    sizes = [int(np.prod(p.shape[1:])) for p in planes]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    def frames_buf(on_dev, fill):
+        t = torch.empty((n, int(offs[-1])), dtype=torch.uint8, device="cuda") if on_dev else \
+            torch.empty((n, int(offs[-1])), dtype=torch.uint8).pin_memory()
+        views = [t[:, int(offs[i]):int(offs[i + 1])] for i in range(3)]
+        if fill:
+            for v, p in zip(views, planes):
+                v.copy_(torch.from_numpy(p).reshape(n, -1))
+        return views
+    pin = frames_buf(dev_in, True)
+    outp = frames_buf(dev_out, False)
+else:
+    pin = [torch.from_numpy(p).cuda() if dev_in else torch.from_numpy(p).pin_memory() for p in planes]
+    outp = [torch.empty(p.shape, dtype=torch.uint8, device="cuda") if dev_out
+            else torch.empty(p.shape, dtype=torch.uint8).pin_memory() for p in pin]
 h, w = planes[0].shape[1:]
 col = len(planes) == 3
 cw, ch = (planes[1].shape[2], planes[1].shape[1]) if col else (0, 0)
@@ -35,6 +57,7 @@ rec = np.zeros(1, pipeline.RECORD_DT)
 vp = lambda t, k: C.c_void_p(t[k].data_ptr())
 asyn = "--async" in sys.argv
 depth = int(sys.argv[sys.argv.index("--depth") + 1]) if "--depth" in sys.argv else 2
+wait_every = int(sys.argv[sys.argv.index("--wait-every") + 1]) if "--wait-every" in sys.argv else 1
 owed = []  # --async: frames released by each push, not yet popped
 def pop_all(k):
     pop = lib.stabgpu_stream_pop_async if asyn else lib.stabgpu_stream_pop
@@ -64,7 +87,8 @@ for k in range(n):
     assert push(hs, vp(pin[0], k), vp(pin[1], k) if col else None,
                 vp(pin[2], k) if col else None, C.byref(nr)) == 0
     if asyn:
-        assert lib.stabgpu_stream_wait_pops(hs) == 0
+        if (k + 1) % wait_every == 0:
+            assert lib.stabgpu_stream_wait_pops(hs) == 0
         owed.append(nr.value - sum(owed))
     elif lag:
         pop_all(pending)  # frames released by earlier pushes
@@ -81,6 +105,8 @@ if asyn:
     assert lib.stabgpu_stream_wait_pops(hs) == 0
 dt = time.perf_counter() - t0
 lib.stabgpu_stream_destroy(hs)
+torch.cuda.synchronize()
+digest = int(sum(int(o.to(torch.int64).sum().item()) for o in outp))
 lat = np.array(lat) * 1e3
-print(f"{name} {'device' if dev else 'pinned'} graphs={int(graphs)} lag={int(lag)} async={int(asyn) * depth} push_async={int(pasync)}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
-      f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out")
+print(f"{name} {'device' if dev else 'pinned' if not (dev_in or dev_out) else ('device-in' if dev_in else 'device-out')} graphs={int(graphs)} lag={int(lag)} async={int(asyn) * depth} push_async={int(pasync)} wait_every={wait_every} packed={int(packed)}: {n} frames in {dt:.3f} s = {n / dt:.1f} frames/s; push+pop ms p50 {np.median(lat):.3f} "
+      f"p99 {np.percentile(lat, 99):.3f}; {pop_all.n} frames out, output sum {digest}")
