@@ -417,10 +417,16 @@ int stabgpu_tracker_destroy(stabgpu_tracker* t);
  * the pyramid stream (K1 of the frame as soon as it lands), the motion chain
  * (the K5 step + compaction + K6 fit, the K7 scan), the
  * release chain (smoothing + K8 compose of the frame it releases, behind the
- * scan) and, every redetect_interval frames, the re-detection (beside the
- * frame's own K5 step; the next frame's K5 waits for it) - so frame k+1's
- * motion overlaps frame k's compose.  Each chain is one CUDA graph,
- * instantiated once per topology and updated in place per frame. */
+ * scan) and, every redetect_interval frames, the re-detection (as soon as
+ * its frame has landed; the next frame's K5 waits for it, so a caller that
+ * keeps a few frames queued - push_async / pop_async - hides it behind the
+ * K5 steps of the frames before) - so frame k+1's motion overlaps frame k's
+ * compose.  Each chain is one CUDA graph, instantiated once per topology and
+ * updated in place per frame.
+ * Frames whose planes lie back to back in the caller's memory (cb == y + w*h,
+ * cr == cb + cw*ch: one planar buffer per frame, as a Y4M reader holds them,
+ * media_io.cpp:139-145) move in one copy per direction when the plane sizes
+ * are multiples of 256 bytes; anything else moves plane by plane. */
 typedef struct stabgpu_stream stabgpu_stream;
 
 int stabgpu_stream_create(stabgpu_ctx* ctx, const stabgpu_config* cfg, int w, int h, int cw, int ch,
