@@ -442,6 +442,13 @@ int stabgpu_stream_push(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, 
 int stabgpu_stream_push_async(stabgpu_stream* s, const uint8_t* y, const uint8_t* cb, const uint8_t* cr,
                               int* n_ready);
 int stabgpu_stream_wait_inputs(stabgpu_stream* s);
+/* Page-locked host memory (cudaHostAlloc / cudaFreeHost) for frames handed to
+ * the host-buffer and stream entry points: copies from and to it are
+ * asynchronous and run at the full PCIe rate, pageable memory is staged by
+ * the driver.  The drop-in run_offline / run_streaming (shim/pipeline_b200.cpp)
+ * stage the caller's std::vector frames (frame.hpp:14-33) through it. */
+int stabgpu_host_alloc(void** out, size_t bytes);
+int stabgpu_host_free(void* p);
 /* End of stream: releases the remaining frames (at least 2 frames pushed). */
 int stabgpu_stream_finish(stabgpu_stream* s, int* n_ready);
 /* Oldest ready frame (its index, planes and record); STABGPU_SEQUENCING if none. */

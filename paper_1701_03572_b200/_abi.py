@@ -139,6 +139,8 @@ PROTOTYPES = {
     "stabgpu_stream_push": (I, [V, V, V, V, c_ip]),
     "stabgpu_stream_push_async": (I, [V, V, V, V, c_ip]),
     "stabgpu_stream_wait_inputs": (I, [V]),
+    "stabgpu_host_alloc": (I, [C.POINTER(V), C.c_size_t]),
+    "stabgpu_host_free": (I, [V]),
     "stabgpu_stream_finish": (I, [V, c_ip]),
     "stabgpu_stream_pop": (I, [V, P(C.c_int64), V, V, V, V]),
     "stabgpu_stream_pop_async": (I, [V, P(C.c_int64), V, V, V, V]),

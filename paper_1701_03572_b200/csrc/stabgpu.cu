@@ -2538,6 +2538,24 @@ int stabgpu_stream_pop(stabgpu_stream* s, int64_t* index, uint8_t* oy, uint8_t* 
     return stabgpu_stream_wait_pops(s);
 }
 
+int stabgpu_host_alloc(void** out, size_t bytes) {
+    if (!out) return set_err(STABGPU_INVALID_INPUT, "host_alloc: null output pointer");
+    *out = nullptr;
+    if (cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(STABGPU_CUDA, "host_alloc: %zu page-locked bytes not available", bytes);
+    }
+    return STABGPU_OK;
+}
+
+int stabgpu_host_free(void* p) {
+    if (p && cudaFreeHost(p) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(STABGPU_CUDA, "host_free: not a stabgpu_host_alloc pointer");
+    }
+    return STABGPU_OK;
+}
+
 int stabgpu_stream_set_graphs(stabgpu_stream* s, int on) {
     if (!s) return set_err(STABGPU_INVALID_INPUT, "stream: null handle");
     s->graphs = on != 0 && graph_safe(s->cfg);

@@ -22,6 +22,7 @@
 // -Drun_offline=reference_run_offline -Drun_streaming=reference_run_streaming
 // (its other definitions — validate, summarize, to_json — stay) and link
 // libstabcore_b200.so; INTEGRATION.md §1.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -78,11 +79,16 @@ stabgpu_config to_c(const stab::StabConfig& cfg) {
 struct Stream {
     stabgpu_ctx* ctx = nullptr;
     stabgpu_stream* s = nullptr;
+    uint8_t* stage_in = nullptr;   // page-locked planar frames (Y | Cb | Cr): kIn upload slots
+    uint8_t* stage_out = nullptr;  // and kOut download slots
     ~Stream() {
         if (s) stabgpu_stream_destroy(s);
+        if (stage_in) stabgpu_host_free(stage_in);
+        if (stage_out) stabgpu_host_free(stage_out);
         if (ctx) stabgpu_destroy(ctx);
     }
 };
+constexpr int kIn = 3, kOut = 8;  // staging slots: uploads in flight, downloads queued per wait
 
 // One pass of the device pipeline; errors propagate (the caller decides on
 // sink.abort).  Phase 1 consumes the source; `finish` releases the tail.
@@ -100,11 +106,19 @@ class DeviceRun {
     bool enough() const { return frames_ >= 2; }
 
     void finish() {
+        deliver();
         int n = 0;
         const auto t0 = Clock::now();
+        ok(stabgpu_stream_wait_inputs(st_.s));
         ok(stabgpu_stream_finish(st_.s, &n));
         me_s_ += since(t0);
-        pop(n);
+        if (n > 0 && first_emit_ < 0) first_emit_ = frames_;
+        while (n > 0) {  // the tail, kOut frames per wait
+            const int m = std::min(n, kOut);
+            queue_pops(m);
+            deliver();
+            n -= m;
+        }
     }
 
     stab::RunSummary summary(Clock::time_point start) const {
@@ -145,6 +159,10 @@ class DeviceRun {
     std::int64_t rigid_ = 0, similarity_ = 0, skipped_ = 0;
     double me_s_ = 0.0, ic_s_ = 0.0;
     std::deque<std::int64_t> pending_;  // indices of frames not yet released
+    std::size_t fl_ = 0, fc_ = 0, fs_ = 0;  // luma / chroma plane bytes, bytes per staged frame
+    int queued_ = 0;                        // pops issued into stage_out slots 0..queued_-1, not yet delivered
+    stabgpu_frame_record recs_[kOut];
+    int64_t idx_[kOut];
     std::vector<stab::DeltaParams> deltas_;
 
     void push(const stab::VideoFrame& f) {
@@ -159,6 +177,14 @@ class DeviceRun {
             ch_ = col ? f.chroma_height : 0;
             ok(stabgpu_create(0, &st_.ctx));
             ok(stabgpu_stream_create(st_.ctx, &c_, w_, h_, cw_, ch_, &st_.s));
+            fl_ = static_cast<std::size_t>(w_) * h_;
+            fc_ = static_cast<std::size_t>(cw_) * ch_;
+            fs_ = fl_ + 2 * fc_;
+            void* p = nullptr;
+            ok(stabgpu_host_alloc(&p, fs_ * kIn));
+            st_.stage_in = static_cast<uint8_t*>(p);
+            ok(stabgpu_host_alloc(&p, fs_ * kOut));
+            st_.stage_out = static_cast<uint8_t*>(p);
             if (const char* g = std::getenv("STABGPU_STREAM_GRAPHS")) ok(stabgpu_stream_set_graphs(st_.s, std::atoi(g)));
         } else if (y.width != w_ || y.height != h_ || (col ? f.chroma_width : 0) != cw_ ||
                    (col ? f.chroma_height : 0) != ch_) {
@@ -168,32 +194,65 @@ class DeviceRun {
             throw stab::InvalidInputError("chroma planes do not match the chroma size");
         if (y.index <= last_index_) throw stab::SequencingError("frame index must be strictly increasing");
         last_index_ = y.index;
+        // The caller's frames are std::vectors (pageable).  Frame k is copied
+        // into a page-locked planar slot and pushed without waiting for its
+        // upload; released frames are downloaded into page-locked slots a few
+        // pushes after their release (their compose finished long before, so
+        // the copy only waits for PCIe) and handed to the sink one push later.
+        // The device therefore runs ahead of the host: the next frames' motion
+        // and the re-detections overlap the copies.  Order and bytes are those
+        // of popping at once; finish() drains.
+        deliver();  // the downloads queued by the previous push
         int n = 0;
         const auto t0 = Clock::now();
-        ok(stabgpu_stream_push(st_.s, y.pixels.data(), col ? f.cb.data() : nullptr, col ? f.cr.data() : nullptr,
-                               &n));
+        if (frames_ > kIn - 1 && (frames_ - 1) % (kIn - 1) == 0)
+            ok(stabgpu_stream_wait_inputs(st_.s));  // the slot written next was uploaded at least one wait ago
+        uint8_t* in = st_.stage_in + static_cast<std::size_t>((frames_ - 1) % kIn) * fs_;
+        std::memcpy(in, y.pixels.data(), fl_);
+        if (col) {
+            std::memcpy(in + fl_, f.cb.data(), fc_);
+            std::memcpy(in + fl_ + fc_, f.cr.data(), fc_);
+        }
+        ok(stabgpu_stream_push_async(st_.s, in, col ? in + fl_ : nullptr, col ? in + fl_ + fc_ : nullptr, &n));
         me_s_ += since(t0);
         pending_.push_back(y.index);
-        pop(n);
+        if (n > 0 && first_emit_ < 0) first_emit_ = frames_;  // the release schedule is the device's, not the pop's
+        const int lag = std::min(6, std::max(0, 2 * cfg_.smooth.radius - 2));
+        queue_pops(std::min(kOut, std::max(0, n - lag)));
     }
 
-    void pop(int n) {
-        if (n > 0 && first_emit_ < 0) first_emit_ = frames_;
-        for (int k = 0; k < n; ++k) {
-            const auto t0 = Clock::now();
+    // downloads of the next m released frames into the staging slots
+    void queue_pops(int m) {
+        const auto t0 = Clock::now();
+        for (int k = 0; k < m; ++k) {
+            uint8_t* o = st_.stage_out + static_cast<std::size_t>(k) * fs_;
+            ok(stabgpu_stream_pop_async(st_.s, &idx_[k], o, cw_ ? o + fl_ : nullptr, cw_ ? o + fl_ + fc_ : nullptr,
+                                        &recs_[k]));
+        }
+        queued_ = m;
+        ic_s_ += since(t0);
+    }
+
+    // hands the queued frames to the sink (after their downloads have landed)
+    void deliver() {
+        if (queued_ == 0) return;
+        const auto t0 = Clock::now();
+        ok(stabgpu_stream_wait_pops(st_.s));
+        for (int k = 0; k < queued_; ++k) {
+            const uint8_t* o = st_.stage_out + static_cast<std::size_t>(k) * fs_;
             stab::VideoFrame out;
-            out.luma = stab::GrayFrame(w_, h_, pending_.front());
+            out.luma.width = w_;
+            out.luma.height = h_;
+            out.luma.index = pending_.front();
+            out.luma.pixels.assign(o, o + fl_);
             pending_.pop_front();
             if (cw_ > 0) {
                 out.chroma_width = cw_;
                 out.chroma_height = ch_;
-                out.cb.resize(static_cast<std::size_t>(cw_) * ch_);
-                out.cr.resize(out.cb.size());
+                out.cb.assign(o + fl_, o + fl_ + fc_);
+                out.cr.assign(o + fl_ + fc_, o + fs_);
             }
-            stabgpu_frame_record rec;
-            int64_t idx = 0;
-            ok(stabgpu_stream_pop(st_.s, &idx, out.luma.pixels.data(), cw_ ? out.cb.data() : nullptr,
-                                  cw_ ? out.cr.data() : nullptr, &rec));
+            const stabgpu_frame_record& rec = recs_[k];
             stab::DeltaParams d;
             d.dx = rec.delta.dx;
             d.dy = rec.delta.dy;
@@ -204,9 +263,10 @@ class DeviceRun {
             deltas_.push_back(d);
             if (rec.decision) (rec.delta.kind == STABGPU_RIGID ? rigid_ : similarity_) += 1;
             if (rec.frame_kind == STABGPU_FRAME_SKIPPED) ++skipped_;
-            ic_s_ += since(t0);
             sink_.push(std::move(out));
         }
+        queued_ = 0;
+        ic_s_ += since(t0);
     }
 };
 
