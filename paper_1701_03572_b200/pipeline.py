@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from ._lib import check, context, load
+from ._lib import InvalidConfigError, check, context, load
 from .stab import StabConfig
 
 MOTION_BYTES = C.sizeof(_abi.MotionRecord)
@@ -418,19 +418,27 @@ class StreamStabilizer:
     is bit-identical to Stage I's output for that frame."""
 
     def __init__(self, cfg: StabConfig, w: int, h: int, cw: int = 0, ch: int = 0, device: int = 0,
-                 graphs: bool = True, overlap_pops: bool = False, async_push: bool = False):
+                 graphs: bool = True, overlap_pops: bool = False, async_push: bool = False, depth: int = 1):
         # overlap_pops: push() queues the downloads of the frames released by
         # the PREVIOUS push (stabgpu_stream_pop_async), uploads and estimates
         # the new frame, then waits for them - the D2H of frame k-r overlaps
         # the H2D of frame k+1; frames come back one push late, same bytes
         self.overlap_pops = overlap_pops
+        # depth (with overlap_pops): the frames popped at push k are those
+        # released by push k - depth.  With a few frames in flight the device
+        # runs ahead of the host: the re-detections (which start as soon as
+        # their frame has landed) overlap earlier frames' K5 steps.  depth must
+        # stay below the output ring (2 * smooth_radius + 2 released frames)
+        if depth < 1 or (overlap_pops and depth > max(1, 2 * cfg.smooth_radius)):
+            raise InvalidConfigError("StreamStabilizer: depth must lie in [1, 2 * smooth_radius]")
+        self.depth = depth
+        self._owed_q = []
         # async_push: push() returns before the frame's upload has landed
         # (stabgpu_stream_push_async); the stabilizer keeps the frame's arrays
         # alive and waits for the upload at the start of the next push, so with
         # a new array per frame the upload of frame k+1 overlaps the motion of k
         self.async_push = async_push
         self._held = None
-        self._owed = 0
         self.w, self.h, self.cw, self.ch = w, h, cw, ch
         self._c = cfg.c()
         self._lib = load()
@@ -471,10 +479,10 @@ class StreamStabilizer:
             self._held = (y, cb, cr)
             push = self._lib.stabgpu_stream_push_async
         if self.overlap_pops:
-            late = self._pop_all(self._owed, wait=False)
+            late = self._pop_all(self._owed_q.pop(0), wait=False) if len(self._owed_q) >= self.depth else []
             check(push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
             check(self._lib.stabgpu_stream_wait_pops(self._h))
-            self._owed = n.value
+            self._owed_q.append(n.value - sum(self._owed_q))  # released by this push
             return self._frames(late)
         check(push(self._h, _vp(y), _vp(cb), _vp(cr), C.byref(n)))
         return self._frames(self._pop_all(n.value))
@@ -485,7 +493,7 @@ class StreamStabilizer:
             check(self._lib.stabgpu_stream_wait_inputs(self._h))
             self._held = None
         check(self._lib.stabgpu_stream_finish(self._h, C.byref(n)))
-        self._owed = 0
+        self._owed_q = []
         return self._frames(self._pop_all(n.value))
 
     def close(self):

@@ -551,25 +551,26 @@ def orc_checker():
     return _oracle.oracle()
 
 
-@pytest.mark.parametrize("graphs", [True, False])
-def test_stream_overlapped_pops_long(graphs):
+@pytest.mark.parametrize("graphs,depth", [(True, 1), (False, 1), (True, 4)])
+def test_stream_overlapped_pops_long(graphs, depth):
     """pop_async / wait_pops (downloads of the frames released by the previous
     push overlap the next upload) over a stream long enough to grow the
     frame-indexed arrays (256 frames) and wrap the input ring many times, with
     the motion, release and detect chains on their three streams: frames come
-    back one push late and are bitwise Stage I."""
+    back `depth` pushes late (the device ahead of the host: re-detections start
+    as soon as their frame has landed) and are bitwise Stage I."""
     y = _data.video(w=128, h=96, frames=300, jit_t=1.5)[0]
     cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=50, smooth=3, corners=40, levels=2, radius=7)
     sy, _, _, srec = pipeline.stabilize_sequence(y, cfg)
-    s = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1], graphs=graphs, overlap_pops=True)
+    s = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1], graphs=graphs, overlap_pops=True, depth=depth)
     sched, tail = _release_schedule(len(y), cfg.smooth_radius)
     got = []
     for k in range(len(y)):
         rel = s.push(y[k])
-        assert [r[0] for r in rel] == (sched[k - 1] if k else []), k
+        assert [r[0] for r in rel] == (sched[k - depth] if k >= depth else []), k
         got += rel
     rel = s.finish()
-    assert [r[0] for r in rel] == sched[-1] + tail
+    assert [r[0] for r in rel] == sum(sched[len(y) - depth:], []) + tail
     got += rel
     s.close()
     assert [g[0] for g in got] == list(range(len(y)))
