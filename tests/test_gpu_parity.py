@@ -491,6 +491,41 @@ def test_stream_equals_stage1(mode, ransac, smooth, graphs):
         assert grec.tobytes() == srec[i].tobytes(), i
 
 
+@pytest.mark.parametrize("interval", [1, 2, 3, 7])
+def test_redetect_intervals(orc, interval):
+    """Other re-detection cadences than the default 5 (flow.cpp:326-330):
+    Stage I against the oracle (segment map, carried points), and Stage II with
+    the device several frames ahead of the host (re-detections start as soon as
+    their frame has landed; interval 1 re-detects every frame, so the point
+    buffers rotate every push) bitwise against Stage I."""
+    import dataclasses
+
+    y = _data.video(frames=33, objects=1, jit_t=2.5)[0]
+    cfg = _data.small_cfg(_data.MODES["hybrid"], ransac=60, smooth=4)
+    cfg = dataclasses.replace(cfg, flow=dataclasses.replace(cfg.flow, redetect_interval=interval))
+    sy, _, _, srec = pipeline.stabilize_sequence(y, cfg)
+    oy, _, _, orec = orc.stabilize_sequence(y, cfg)
+    assert np.array_equal(srec["frame_kind"], orec["frame_kind"])
+    tr = srec["frame_kind"] == 2
+    assert np.array_equal(srec["n_tracks"][tr], orec["n_tracks"][tr])
+    assert np.array_equal(srec["n_inliers"][tr], orec["n_inliers"][tr])
+    for k in ("dx", "dy", "da", "dls"):
+        assert np.abs(srec["delta"][k] - orec["delta"][k]).max() < 1e-6, k
+    d = np.abs(sy.astype(int) - oy.astype(int))
+    assert d.max() <= 1 and (d > 0).mean() < 1e-3
+    for depth in (1, 6):
+        s = pipeline.StreamStabilizer(cfg, y.shape[2], y.shape[1], overlap_pops=True, async_push=True, depth=depth)
+        got = []
+        for k in range(len(y)):
+            got += s.push(y[k].copy())
+        got += s.finish()
+        s.close()
+        assert [g[0] for g in got] == list(range(len(y)))
+        for i, gy, _, _, grec in got:
+            assert np.array_equal(gy, sy[i]), (depth, i)
+            assert grec.tobytes() == srec[i].tobytes(), (depth, i)
+
+
 @pytest.mark.parametrize("overlap", [False, True])
 def test_stream_async_push_equals_stage1(overlap):
     """stabgpu_stream_push_async (push returns before the upload has landed;
