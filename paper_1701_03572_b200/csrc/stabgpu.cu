@@ -2508,14 +2508,15 @@ int stabgpu_stream_pop_async(stabgpu_stream* s, int64_t* index, uint8_t* oy, uin
         if (s->chroma && ocr) CUDA_TRY(cudaMemcpyAsync(ocr, s->out_cr + o * s->fs, fc, cudaMemcpyDefault, co));
     }
     if (record) {
-        if ((int)s->rec_owed.size() >= s->ocap) TRY(stabgpu_stream_wait_pops(s));
-        const int j = (int)s->rec_owed.size();
-        CUDA_TRY(cudaMemcpyAsync(s->rec_host + j, s->rec + i, sizeof *record, cudaMemcpyDeviceToHost, co));
-        s->rec_owed.emplace_back(record, j);
+        // the records of the frames popped since the last wait are one
+        // contiguous run of s->rec (frames pop in order): wait_pops fetches
+        // them in one copy (a 96-byte copy per pop between the plane copies
+        // stalls the copy queue)
+        if (!s->rec_owed.empty() && i - s->rec_owed.front().second + 1 > s->ocap)  // the run must fit rec_host
+            TRY(stabgpu_stream_wait_pops(s));
+        s->rec_owed.emplace_back(record, (int)i);
     }
-    // the selector scan's error word (written before the frame was released)
-    CUDA_TRY(cudaMemcpyAsync(s->err_host, reinterpret_cast<int*>(s->ps + 1), sizeof(int), cudaMemcpyDeviceToHost, co));
-    s->pops_pending = true;
+    s->pops_pending = true;  // wait_pops reads the selector scan's error word behind these copies
     if (index) *index = i;
     return STABGPU_OK;
 }
@@ -2525,8 +2526,19 @@ int stabgpu_stream_wait_pops(stabgpu_stream* s) {
     if (!s->pops_pending) return STABGPU_OK;
     cudaSetDevice(s->ctx->device);
     s->pops_pending = false;
+    // the selector scan's error word, once per wait (written before the popped
+    // frames were released: the output copy stream has waited for their compose)
+    CUDA_TRY(cudaMemcpyAsync(s->err_host, reinterpret_cast<int*>(s->ps + 1), sizeof(int), cudaMemcpyDeviceToHost,
+                             s->ctx->cout));
+    const long long i0 = s->rec_owed.empty() ? 0 : s->rec_owed.front().second;
+    if (!s->rec_owed.empty()) {
+        if (s->grown) CUDA_TRY(cudaStreamWaitEvent(s->ctx->cout, s->ev_grow, 0));  // the records may have moved
+        const long long i1 = s->rec_owed.back().second;  // popped in order: [i0, i1] covers every owed record
+        CUDA_TRY(cudaMemcpyAsync(s->rec_host, s->rec + i0, sizeof(stabgpu_frame_record) * (size_t)(i1 - i0 + 1),
+                                 cudaMemcpyDeviceToHost, s->ctx->cout));
+    }
     CUDA_TRY(cudaStreamSynchronize(s->ctx->cout));
-    for (const auto& o : s->rec_owed) *o.first = s->rec_host[o.second];
+    for (const auto& o : s->rec_owed) *o.first = s->rec_host[o.second - i0];
     s->rec_owed.clear();
     if (*s->err_host) TRY(plan_error(s->ctx, s->ps));
     return STABGPU_OK;
